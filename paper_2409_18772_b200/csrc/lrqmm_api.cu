@@ -1,0 +1,586 @@
+// liblrqmm C ABI (include/lrqmm.h): handle lifetime, argument validation,
+// workspace layout and the stream-ordered orchestration of Algorithm 2
+// over the K1..K6 kernels.  No host synchronisation on the
+// hot path; NCCL collectives (world_size > 1) are enqueued on the same stream.
+#include <cuda.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "../../include/lrqmm.h"
+#include "kernels.h"
+
+using namespace lrqmm;
+
+namespace {
+
+constexpr int kMaxWidth = 64;
+
+struct Side {
+  int64_t rows = 0;
+  const float* X = nullptr;  // caller's fp32 operand (retained, not copied)
+  int64_t ldx = 0;
+  int8_t* codes = nullptr;   // rows x Kp
+  float* lam = nullptr;      // rows
+  float* row_amax = nullptr; // rows (per-tensor mode)
+  float* lam_scalar = nullptr;
+  float* Om = nullptr;       // K x W (zero-padded sketch)
+  float* Y = nullptr;        // rows x W : sketch / W = R Q1
+  float* Q0 = nullptr;       // rows x W
+  float* Z = nullptr;        // K x W
+  float* Q1 = nullptr;       // K x W
+  float* Gp = nullptr;       // rows x W : X~ Q1_other
+  double* G = nullptr;       // W x W
+  float* T = nullptr;        // W x W  (orth transforms, scratch)
+  float* VW = nullptr;       // W x W  (first r columns: truncation)
+};
+
+}  // namespace
+
+struct lrqmm_handle_s {
+  lrqmm_config_t cfg{};
+  int qmax = 0, Kp = 0, kk = 0, W = 0, r = 0, R2 = 0;
+  cudaStream_t st = nullptr;
+  lrqmm_status_t sticky = LRQMM_OK;
+  int state = 0;  // bit0: A quantized, bit1: B quantized, bit2: rsvd done
+  Side s[2];
+  float* LA = nullptr;  // m x R2
+  float* LB = nullptr;  // n x R2
+  float* partial = nullptr;
+  int64_t partial_elems = 0;
+  double* gpartial = nullptr;
+  int64_t gpartial_elems = 0;
+  double* Gcross = nullptr;  // W x W
+  float* VWbM = nullptr;     // W x W
+  EigJob* d_jobs = nullptr;  // device job tables
+  int* err_flag = nullptr;
+  alignas(64) CUtensorMap mapA;
+  alignas(64) CUtensorMap mapB;
+  cudaEvent_t ev[8] = {};
+  ncclComm_t comm = nullptr;
+  // run_host buffers
+  float *hA = nullptr, *hB = nullptr, *hOmA = nullptr, *hOmB = nullptr, *hD = nullptr;
+};
+
+// job-table slots (pairs A,B)
+enum { kJobOrth0 = 0, kJobOrth1 = 2, kJobOrth2 = 4, kJobTrunc = 6, kNumJobs = 8 };
+
+#define LQ_CUDA(call)                                                                          \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess) {                                                                   \
+      if (getenv("LRQMM_DEBUG")) fprintf(stderr, "lrqmm: %s -> %s\n", #call, cudaGetErrorString(e_)); \
+      return fail(h, LRQMM_ERR_CUDA);                                                          \
+    }                                                                                          \
+  } while (0)
+#define LQ_NCCL(call)                                     \
+  do {                                                    \
+    ncclResult_t r_ = (call);                             \
+    if (r_ != ncclSuccess) return fail(h, LRQMM_ERR_NCCL); \
+  } while (0)
+
+static lrqmm_status_t fail(lrqmm_handle_t h, lrqmm_status_t s) {
+  if (h && h->sticky == LRQMM_OK) h->sticky = s;
+  return s;
+}
+
+static int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+static lrqmm_status_t check_launch(lrqmm_handle_t h) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    if (getenv("LRQMM_DEBUG")) fprintf(stderr, "lrqmm: launch error %s\n", cudaGetErrorString(e));
+    return fail(h, LRQMM_ERR_CUDA);
+  }
+  return LRQMM_OK;
+}
+
+template <typename T>
+static bool dalloc(T** p, int64_t elems) {
+  if (elems <= 0) elems = 1;
+  if (cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * (size_t)elems) != cudaSuccess) return false;
+  return cudaMemset(*p, 0, sizeof(T) * (size_t)elems) == cudaSuccess;
+}
+
+extern "C" {
+
+const char* lrqmm_status_string(lrqmm_status_t s) {
+  switch (s) {
+    case LRQMM_OK: return "ok";
+    case LRQMM_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case LRQMM_ERR_SHAPE: return "shape error";
+    case LRQMM_ERR_RANK: return "rank + oversample exceeds min(rows, k) or 64";
+    case LRQMM_ERR_OVERFLOW: return "k * qmax^2 exceeds int32 accumulator range";
+    case LRQMM_ERR_NONFINITE: return "non-finite input";
+    case LRQMM_ERR_STATE: return "call out of order";
+    case LRQMM_ERR_CUDA: return "CUDA error";
+    case LRQMM_ERR_NCCL: return "NCCL error";
+    case LRQMM_ERR_ALLOC: return "allocation failure";
+    case LRQMM_ERR_UNSUPPORTED: return "unsupported configuration";
+  }
+  return "unknown status";
+}
+
+lrqmm_status_t lrqmm_get_unique_id(unsigned char out[128]) {
+  if (!out) return LRQMM_ERR_INVALID_ARGUMENT;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return LRQMM_ERR_NCCL;
+  static_assert(sizeof(id.internal) == 128, "ncclUniqueId size");
+  memcpy(out, id.internal, 128);
+  return LRQMM_OK;
+}
+
+static lrqmm_status_t validate(const lrqmm_config_t* c) {
+  if (!c) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (c->m < 0 || c->n < 0 || c->k < 0) return LRQMM_ERR_SHAPE;
+  if (c->k > INT32_MAX - 256 || c->n > INT32_MAX || c->m > ((int64_t)1 << 40)) return LRQMM_ERR_SHAPE;
+  if (c->bits != 4 && c->bits != 8) return LRQMM_ERR_UNSUPPORTED;
+  if (c->rounding < 0 || c->rounding > 2) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (c->granularity < 0 || c->granularity > 1) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (c->rank < 0 || c->oversample < 0) return LRQMM_ERR_RANK;
+  if (c->world_size < 1 || c->world_rank < 0 || c->world_rank >= c->world_size) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (c->world_size > 1 && !c->nccl_unique_id) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (c->world_size > 1 && c->granularity == LRQMM_SCALE_PER_TENSOR) return LRQMM_ERR_UNSUPPORTED;
+  const int64_t qmax = (1 << (c->bits - 1)) - 1;
+  if (c->k * qmax * qmax > (int64_t)INT32_MAX) return LRQMM_ERR_OVERFLOW;  // reading #24
+  if (c->rank > 0) {
+    if (c->power_iters < 1) return LRQMM_ERR_UNSUPPORTED;  // reading #10
+    const int64_t kk = (int64_t)c->rank + c->oversample;
+    if (kk > kMaxWidth || c->rank > 32) return LRQMM_ERR_RANK;
+    // r + p <= min(rows, K) of each side (A: global rows checked per shard)
+    if (kk > c->k || kk > c->n || (c->world_size == 1 && kk > c->m)) return LRQMM_ERR_RANK;
+  }
+  return LRQMM_OK;
+}
+
+lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
+  if (!h) return LRQMM_OK;
+  cudaSetDevice(h->cfg.device);
+  if (h->st) cudaStreamSynchronize(h->st);
+  for (auto& s : h->s) {
+    cudaFree(s.codes); cudaFree(s.lam); cudaFree(s.row_amax); cudaFree(s.lam_scalar); cudaFree(s.Om);
+    cudaFree(s.Y); cudaFree(s.Q0); cudaFree(s.Z); cudaFree(s.Q1); cudaFree(s.Gp); cudaFree(s.G);
+    cudaFree(s.T); cudaFree(s.VW);
+  }
+  cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->partial); cudaFree(h->gpartial); cudaFree(h->Gcross);
+  cudaFree(h->VWbM); cudaFree(h->d_jobs); cudaFree(h->err_flag);
+  cudaFree(h->hA); cudaFree(h->hB); cudaFree(h->hOmA); cudaFree(h->hOmB); cudaFree(h->hD);
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->comm) ncclCommDestroy(h->comm);
+  delete h;
+  return LRQMM_OK;
+}
+
+lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
+  if (!out) return LRQMM_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  lrqmm_status_t v = validate(cfg);
+  if (v != LRQMM_OK) return v;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) return LRQMM_ERR_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess) return LRQMM_ERR_CUDA;
+  if (prop.major != 10 || prop.minor != 0) return LRQMM_ERR_UNSUPPORTED;  // built for sm_100a only
+  if (cudaSetDevice(cfg->device) != cudaSuccess) return LRQMM_ERR_CUDA;
+
+  lrqmm_handle_t h = new (std::nothrow) lrqmm_handle_s();
+  if (!h) return LRQMM_ERR_ALLOC;
+  h->cfg = *cfg;
+  h->cfg.nccl_unique_id = nullptr;
+  h->st = reinterpret_cast<cudaStream_t>(cfg->stream);
+  h->qmax = (1 << (cfg->bits - 1)) - 1;
+  h->Kp = (int)roundup(std::max<int64_t>(cfg->k, 1), 128);
+  h->r = cfg->rank;
+  h->kk = cfg->rank > 0 ? cfg->rank + cfg->oversample : 0;
+  h->W = h->kk > 0 ? (int)roundup(h->kk, 8) : 0;
+  h->R2 = h->r > 0 ? (int)roundup(2 * h->r, 8) : 0;
+  h->s[0].rows = cfg->m;
+  h->s[1].rows = cfg->n;
+  const int64_t K = cfg->k;
+  bool ok = true;
+  for (auto& s : h->s) {
+    ok = ok && dalloc(&s.codes, s.rows * h->Kp) && dalloc(&s.lam, s.rows) && dalloc(&s.row_amax, s.rows) &&
+         dalloc(&s.lam_scalar, 1);
+    if (h->W > 0) {
+      ok = ok && dalloc(&s.Om, K * h->W) && dalloc(&s.Y, s.rows * h->W) && dalloc(&s.Q0, s.rows * h->W) &&
+           dalloc(&s.Z, K * h->W) && dalloc(&s.Q1, K * h->W) && dalloc(&s.Gp, s.rows * h->W) &&
+           dalloc(&s.G, (int64_t)h->W * h->W) && dalloc(&s.T, (int64_t)h->W * h->W) &&
+           dalloc(&s.VW, (int64_t)h->W * h->W);
+    }
+  }
+  if (h->W > 0) {
+    const int64_t maxrows = std::max<int64_t>({cfg->m, cfg->n, K});
+    // split-K / split-row partials: <= 2 outputs x ~4 waves of splits, bounded at 64 MiB
+    h->partial_elems = std::min<int64_t>((int64_t)16 << 20, 2 * 32 * maxrows * h->W);
+    h->gpartial_elems = 296LL * h->W * h->W;
+    ok = ok && dalloc(&h->LA, cfg->m * h->R2) && dalloc(&h->LB, cfg->n * h->R2) &&
+         dalloc(&h->partial, h->partial_elems) && dalloc(&h->gpartial, h->gpartial_elems) &&
+         dalloc(&h->Gcross, (int64_t)h->W * h->W) && dalloc(&h->VWbM, (int64_t)h->W * h->W) &&
+         dalloc(&h->d_jobs, kNumJobs);
+  }
+  ok = ok && dalloc(&h->err_flag, 4);
+  if (!ok) {
+    lrqmm_destroy(h);
+    return LRQMM_ERR_ALLOC;
+  }
+  if (h->W > 0) {
+    EigJob jobs[kNumJobs];
+    for (int sd = 0; sd < 2; ++sd) {
+      jobs[kJobOrth0 + sd] = EigJob{h->s[sd].G, h->s[sd].T, kEigOrth, 0};
+      jobs[kJobOrth1 + sd] = EigJob{h->s[sd].G, h->s[sd].T, kEigOrth, 0};
+      jobs[kJobOrth2 + sd] = EigJob{h->s[sd].G, h->s[sd].T, kEigOrth, 0};
+      jobs[kJobTrunc + sd] = EigJob{h->s[sd].G, h->s[sd].VW, kEigTrunc, h->r};
+    }
+    if (cudaMemcpy(h->d_jobs, jobs, sizeof(jobs), cudaMemcpyHostToDevice) != cudaSuccess) {
+      lrqmm_destroy(h);
+      return LRQMM_ERR_CUDA;
+    }
+  }
+  GemmArgs g{};
+  g.A = h->s[0].codes;
+  g.B = h->s[1].codes;
+  g.M = std::max<int64_t>(cfg->m, 1);
+  g.N = std::max<int64_t>(cfg->n, 1);
+  g.Kp = h->Kp;
+  if (gemm_prepare_maps(g, &h->mapA, &h->mapB) != 0) {
+    lrqmm_destroy(h);
+    return LRQMM_ERR_CUDA;
+  }
+  if (cfg->enable_timing) {
+    for (auto& e : h->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) {
+        lrqmm_destroy(h);
+        return LRQMM_ERR_CUDA;
+      }
+  }
+  if (cfg->world_size > 1) {
+    ncclUniqueId id;
+    memcpy(id.internal, cfg->nccl_unique_id, 128);
+    if (ncclCommInitRank(&h->comm, cfg->world_size, id, cfg->world_rank) != ncclSuccess) {
+      h->comm = nullptr;
+      lrqmm_destroy(h);
+      return LRQMM_ERR_NCCL;
+    }
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    lrqmm_destroy(h);
+    return LRQMM_ERR_CUDA;
+  }
+  *out = h;
+  return LRQMM_OK;
+}
+
+static void record(lrqmm_handle_t h, int i) {
+  if (h->cfg.enable_timing) cudaEventRecord(h->ev[i], h->st);
+}
+
+lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* X, int64_t ldx) {
+  if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (h->sticky != LRQMM_OK) return h->sticky;
+  if (side != LRQMM_SIDE_A && side != LRQMM_SIDE_B) return LRQMM_ERR_INVALID_ARGUMENT;
+  Side& s = h->s[side];
+  if ((!X && s.rows > 0 && h->cfg.k > 0) || ldx < h->cfg.k) return LRQMM_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(h->cfg.device);
+  s.X = X;
+  s.ldx = ldx;
+  record(h, side == LRQMM_SIDE_A ? 0 : 2);
+  if (h->cfg.granularity == LRQMM_SCALE_PER_TENSOR) {
+    launch_tensor_scale(X, ldx, s.rows, (int)h->cfg.k, h->qmax, s.row_amax, s.lam, s.lam_scalar, h->err_flag, h->st);
+  }
+  QuantArgs a;
+  a.X = X;
+  a.ldx = ldx;
+  a.rows = s.rows;
+  a.K = (int)h->cfg.k;
+  a.Kp = h->Kp;
+  a.qmax = h->qmax;
+  a.mode = h->cfg.rounding;
+  a.codes = s.codes;
+  a.lam = s.lam;
+  a.lam_fixed = h->cfg.granularity == LRQMM_SCALE_PER_TENSOR ? s.lam_scalar : nullptr;
+  a.err_flag = h->err_flag;
+  if (s.rows > 0) launch_quantize(a, h->st);
+  record(h, side == LRQMM_SIDE_A ? 1 : 3);
+  lrqmm_status_t e = check_launch(h);
+  if (e != LRQMM_OK) return e;
+  h->state |= (side == LRQMM_SIDE_A ? 1 : 2);
+  h->state &= ~4;
+  return LRQMM_OK;
+}
+
+static SideView view(lrqmm_handle_t h, int sd) {
+  SideView v;
+  v.X = h->s[sd].X;
+  v.ldx = h->s[sd].ldx;
+  v.rows = h->s[sd].rows;
+  v.K = (int)h->cfg.k;
+  v.lam = h->s[sd].lam;
+  v.qmax = h->qmax;
+  v.mode = h->cfg.rounding;
+  return v;
+}
+
+// allreduce (sum) of an A-side quantity across the row shards
+static lrqmm_status_t allreduce_f64(lrqmm_handle_t h, double* buf, size_t n) {
+  if (h->cfg.world_size == 1) return LRQMM_OK;
+  LQ_NCCL(ncclAllReduce(buf, buf, n, ncclFloat64, ncclSum, h->comm, h->st));
+  return LRQMM_OK;
+}
+static lrqmm_status_t allreduce_f32(lrqmm_handle_t h, float* buf, size_t n) {
+  if (h->cfg.world_size == 1) return LRQMM_OK;
+  LQ_NCCL(ncclAllReduce(buf, buf, n, ncclFloat32, ncclSum, h->comm, h->st));
+  return LRQMM_OK;
+}
+
+// Q <- orthonormal basis of span(Y) for both sides:  G = Y^T Y (fp64) -> eig -> Q = Y T
+static lrqmm_status_t orth_pair(lrqmm_handle_t h, float* const Y[2], const int64_t n[2], float* const Q[2], int job) {
+  const int W = h->W;
+  for (int sd = 0; sd < 2; ++sd) {
+    launch_gram(Y[sd], Y[sd], n[sd], W, h->s[sd].G, h->gpartial, h->gpartial_elems, h->st);
+    // A-side row-sharded quantities are summed over ranks (Y rows live on different ranks)
+    if (sd == 0 && n[0] == h->s[0].rows) {
+      lrqmm_status_t e = allreduce_f64(h, h->s[0].G, (size_t)W * W);
+      if (e != LRQMM_OK) return e;
+    }
+  }
+  launch_eig(h->d_jobs + job, 2, W, h->st);
+  for (int sd = 0; sd < 2; ++sd) launch_apply_small(Y[sd], h->s[sd].T, nullptr, nullptr, n[sd], W, W, W, Q[sd], W, 0, h->st);
+  return check_launch(h);
+}
+
+lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const float* omegaB, int64_t ldo) {
+  if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (h->sticky != LRQMM_OK) return h->sticky;
+  if (h->r == 0) return LRQMM_ERR_STATE;
+  if ((h->state & 3) != 3) return LRQMM_ERR_STATE;
+  if (!omegaA || !omegaB || ldo < h->kk) return LRQMM_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(h->cfg.device);
+  const int W = h->W;
+  const int64_t K = h->cfg.k;
+  record(h, 4);
+  // sketch Omega (K x kk, caller layout) -> zero-padded K x W
+  const float* om[2] = {omegaA, omegaB};
+  for (int sd = 0; sd < 2; ++sd)
+    LQ_CUDA(cudaMemcpy2DAsync(h->s[sd].Om, sizeof(float) * W, om[sd], sizeof(float) * ldo, sizeof(float) * h->kk, K,
+                              cudaMemcpyDeviceToDevice, h->st));
+  // S1: Y = R Omega   (Algorithm 1 sampling)
+  for (int sd = 0; sd < 2; ++sd)
+    launch_proj_rows(view(h, sd), h->s[sd].Om, kFRes, h->s[sd].Y, nullptr, 0, nullptr, W, h->partial,
+                     h->partial_elems, h->st);
+  const int64_t rows[2] = {h->s[0].rows, h->s[1].rows};
+  const int64_t kdim[2] = {K, K};
+  float* Ys[2] = {h->s[0].Y, h->s[1].Y};
+  float* Q0s[2] = {h->s[0].Q0, h->s[1].Q0};
+  float* Zs[2] = {h->s[0].Z, h->s[1].Z};
+  float* Q1s[2] = {h->s[0].Q1, h->s[1].Q1};
+  lrqmm_status_t e;
+  for (int it = 0; it < h->cfg.power_iters; ++it) {
+    // O1: Q0 = orth(Y)
+    if ((e = orth_pair(h, Ys, rows, Q0s, kJobOrth0)) != LRQMM_OK) return e;
+    // S2: Z = R^T Q0  (reduction over rows; A side summed over ranks)
+    for (int sd = 0; sd < 2; ++sd)
+      launch_proj_cols(view(h, sd), h->s[sd].Q0, kFRes, h->s[sd].Z, W, h->partial, h->partial_elems, h->st);
+    if ((e = allreduce_f32(h, h->s[0].Z, (size_t)K * W)) != LRQMM_OK) return e;
+    // O2: Q1 = orth(Z), then one re-orthonormalisation pass (CholQR2-style)
+    {
+      // K rows are replicated on every rank: no allreduce for these Grams
+      const int64_t n2[2] = {K, K};
+      for (int sd = 0; sd < 2; ++sd) launch_gram(Zs[sd], Zs[sd], K, W, h->s[sd].G, h->gpartial, h->gpartial_elems, h->st);
+      launch_eig(h->d_jobs + kJobOrth1, 2, W, h->st);
+      for (int sd = 0; sd < 2; ++sd) launch_apply_small(Zs[sd], h->s[sd].T, nullptr, nullptr, K, W, W, W, Q1s[sd], W, 0, h->st);
+      for (int sd = 0; sd < 2; ++sd) launch_gram(Q1s[sd], Q1s[sd], K, W, h->s[sd].G, h->gpartial, h->gpartial_elems, h->st);
+      launch_eig(h->d_jobs + kJobOrth2, 2, W, h->st);
+      // Z is free now: Q1' = Q1 T2 into Z, then swap roles by copying back
+      for (int sd = 0; sd < 2; ++sd) launch_apply_small(Q1s[sd], h->s[sd].T, nullptr, nullptr, n2[sd], W, W, W, Zs[sd], W, 0, h->st);
+      for (int sd = 0; sd < 2; ++sd)
+        LQ_CUDA(cudaMemcpyAsync(Q1s[sd], Zs[sd], sizeof(float) * K * W, cudaMemcpyDeviceToDevice, h->st));
+    }
+    if (it + 1 < h->cfg.power_iters) {
+      for (int sd = 0; sd < 2; ++sd)
+        launch_proj_rows(view(h, sd), Q1s[sd], kFRes, Ys[sd], nullptr, 0, nullptr, W, h->partial, h->partial_elems, h->st);
+    }
+  }
+  (void)kdim;
+  // S3 + cross: W_X = R_X Q1_X and G'_X = X~ Q1_other in one pass over X
+  //   (Algorithm 1 on R^T: B = Q1^T R^T = W^T; RC1/RC2 skinny products)
+  for (int sd = 0; sd < 2; ++sd)
+    launch_proj_rows(view(h, sd), Q1s[sd], kFRes, Ys[sd], Q1s[1 - sd], kFDeq, h->s[sd].Gp, W, h->partial,
+                     h->partial_elems, h->st);
+  // T: truncation to rank r via eig(W^T W) (Algorithm 1)
+  for (int sd = 0; sd < 2; ++sd) {
+    launch_gram(Ys[sd], Ys[sd], rows[sd], W, h->s[sd].G, h->gpartial, h->gpartial_elems, h->st);
+    if (sd == 0 && (e = allreduce_f64(h, h->s[0].G, (size_t)W * W)) != LRQMM_OK) return e;
+  }
+  launch_eig(h->d_jobs + kJobTrunc, 2, W, h->st);
+  // V_B^T V_A core: Q1_B^T Q1_A (fp64, W x W) -> Mab, VWb Mab
+  launch_gram(Q1s[1], Q1s[0], K, W, h->Gcross, h->gpartial, h->gpartial_elems, h->st);
+  launch_cross_small(h->Gcross, h->s[0].VW, h->s[1].VW, W, h->r, h->VWbM, h->st);
+  // F: factor assembly (Algorithm 2 lines 361-366 folded into two rank-2r factors)
+  const int r = h->r;
+  launch_apply_small(Ys[0], h->s[0].VW, nullptr, nullptr, rows[0], W, W, r, h->LA, h->R2, 0, h->st);        // U_A S_A
+  launch_apply_small(h->s[0].Gp, h->s[1].VW, nullptr, nullptr, rows[0], W, W, r, h->LA, h->R2, r, h->st);   // A~ V_B
+  launch_apply_small(h->s[1].Gp, h->s[0].VW, Ys[1], h->VWbM, rows[1], W, W, r, h->LB, h->R2, 0, h->st);     // B~^T V_A + U_B S_B M
+  launch_apply_small(Ys[1], h->s[1].VW, nullptr, nullptr, rows[1], W, W, r, h->LB, h->R2, r, h->st);        // U_B S_B
+  record(h, 5);
+  if ((e = check_launch(h)) != LRQMM_OK) return e;
+  h->state |= 4;
+  return LRQMM_OK;
+}
+
+static lrqmm_status_t run_gemm(lrqmm_handle_t h, int epi, float alpha, float beta, float* D, int32_t* Cint,
+                               int64_t ldd) {
+  GemmArgs g{};
+  g.A = h->s[0].codes;
+  g.B = h->s[1].codes;
+  g.M = h->cfg.m;
+  g.N = h->cfg.n;
+  g.Kp = h->Kp;
+  g.epi = epi;
+  g.lam_a = h->s[0].lam;
+  g.lam_b = h->s[1].lam;
+  g.LA = h->LA;
+  g.LB = h->LB;
+  g.R2 = h->r > 0 ? h->R2 : 0;
+  g.alpha = alpha;
+  g.beta = beta;
+  g.D = D;
+  g.Cint = Cint;
+  g.ldd = ldd;
+  launch_gemm(g, &h->mapA, &h->mapB, h->st);
+  return check_launch(h);
+}
+
+lrqmm_status_t lrqmm_gemm(lrqmm_handle_t h, float alpha, float beta, float* D, int64_t ldd) {
+  if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (h->sticky != LRQMM_OK) return h->sticky;
+  if ((h->state & 3) != 3) return LRQMM_ERR_STATE;
+  if (h->r > 0 && !(h->state & 4)) return LRQMM_ERR_STATE;
+  if ((!D && h->cfg.m > 0 && h->cfg.n > 0) || ldd < h->cfg.n) return LRQMM_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(h->cfg.device);
+  record(h, 6);
+  lrqmm_status_t e = run_gemm(h, 1, alpha, beta, D, nullptr, ldd);
+  record(h, 7);
+  return e;
+}
+
+lrqmm_status_t lrqmm_gemm_int32(lrqmm_handle_t h, int32_t* Cint, int64_t ldc) {
+  if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (h->sticky != LRQMM_OK) return h->sticky;
+  if ((h->state & 3) != 3) return LRQMM_ERR_STATE;
+  if ((!Cint && h->cfg.m > 0 && h->cfg.n > 0) || ldc < h->cfg.n) return LRQMM_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(h->cfg.device);
+  return run_gemm(h, 0, 1.f, 0.f, nullptr, Cint, ldc);
+}
+
+lrqmm_status_t lrqmm_sync(lrqmm_handle_t h) {
+  if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(h->cfg.device);
+  if (cudaStreamSynchronize(h->st) != cudaSuccess) return fail(h, LRQMM_ERR_CUDA);
+  if (h->sticky != LRQMM_OK) return h->sticky;
+  int flag = 0;
+  if (cudaMemcpy(&flag, h->err_flag, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return fail(h, LRQMM_ERR_CUDA);
+  if (flag & 1) return fail(h, LRQMM_ERR_NONFINITE);
+  if (h->comm) {
+    ncclResult_t ar;
+    if (ncclCommGetAsyncError(h->comm, &ar) != ncclSuccess || ar != ncclSuccess) return fail(h, LRQMM_ERR_NCCL);
+  }
+  return LRQMM_OK;
+}
+
+lrqmm_status_t lrqmm_run_host(lrqmm_handle_t h, const float* A_host, const float* Bt_host, const float* omegaA_host,
+                              const float* omegaB_host, float alpha, float* D_host) {
+  if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (h->sticky != LRQMM_OK) return h->sticky;
+  const int64_t m = h->cfg.m, n = h->cfg.n, k = h->cfg.k, kk = h->kk;
+  if ((!A_host && m * k > 0) || (!Bt_host && n * k > 0) || (!D_host && m * n > 0)) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (h->r > 0 && (!omegaA_host || !omegaB_host)) return LRQMM_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(h->cfg.device);
+  if (!h->hA) {
+    bool ok = dalloc(&h->hA, m * k) && dalloc(&h->hB, n * k) && dalloc(&h->hD, m * n);
+    if (ok && kk > 0) ok = dalloc(&h->hOmA, k * kk) && dalloc(&h->hOmB, k * kk);
+    if (!ok) return fail(h, LRQMM_ERR_ALLOC);
+  }
+  LQ_CUDA(cudaMemcpyAsync(h->hA, A_host, sizeof(float) * m * k, cudaMemcpyHostToDevice, h->st));
+  LQ_CUDA(cudaMemcpyAsync(h->hB, Bt_host, sizeof(float) * n * k, cudaMemcpyHostToDevice, h->st));
+  if (kk > 0) {
+    LQ_CUDA(cudaMemcpyAsync(h->hOmA, omegaA_host, sizeof(float) * k * kk, cudaMemcpyHostToDevice, h->st));
+    LQ_CUDA(cudaMemcpyAsync(h->hOmB, omegaB_host, sizeof(float) * k * kk, cudaMemcpyHostToDevice, h->st));
+  }
+  lrqmm_status_t e;
+  if ((e = lrqmm_quantize(h, LRQMM_SIDE_A, h->hA, k)) != LRQMM_OK) return e;
+  if ((e = lrqmm_quantize(h, LRQMM_SIDE_B, h->hB, k)) != LRQMM_OK) return e;
+  if (h->r > 0 && (e = lrqmm_rsvd_residual(h, h->hOmA, h->hOmB, kk)) != LRQMM_OK) return e;
+  if ((e = lrqmm_gemm(h, alpha, 0.f, h->hD, n)) != LRQMM_OK) return e;
+  LQ_CUDA(cudaMemcpyAsync(D_host, h->hD, sizeof(float) * m * n, cudaMemcpyDeviceToHost, h->st));
+  return lrqmm_sync(h);
+}
+
+lrqmm_status_t lrqmm_get_codes(lrqmm_handle_t h, lrqmm_side_t side, signed char* dst, int64_t ld) {
+  if (!h || (side != 0 && side != 1) || ld < h->cfg.k) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (!(h->state & (side == 0 ? 1 : 2))) return LRQMM_ERR_STATE;
+  const Side& s = h->s[side];
+  if (s.rows == 0 || h->cfg.k == 0) return LRQMM_OK;
+  LQ_CUDA(cudaMemcpy2DAsync(dst, ld, s.codes, h->Kp, h->cfg.k, s.rows, cudaMemcpyDeviceToDevice, h->st));
+  return LRQMM_OK;
+}
+
+lrqmm_status_t lrqmm_get_scales(lrqmm_handle_t h, lrqmm_side_t side, float* lambda) {
+  if (!h || (side != 0 && side != 1) || !lambda) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (!(h->state & (side == 0 ? 1 : 2))) return LRQMM_ERR_STATE;
+  const Side& s = h->s[side];
+  if (s.rows == 0) return LRQMM_OK;
+  LQ_CUDA(cudaMemcpyAsync(lambda, s.lam, sizeof(float) * s.rows, cudaMemcpyDeviceToDevice, h->st));
+  return LRQMM_OK;
+}
+
+int lrqmm_correction_width(lrqmm_handle_t h) { return h ? h->R2 : 0; }
+
+lrqmm_status_t lrqmm_get_correction(lrqmm_handle_t h, lrqmm_side_t side, float* L) {
+  if (!h || (side != 0 && side != 1) || !L) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (!(h->state & 4)) return LRQMM_ERR_STATE;
+  const int64_t rows = h->s[side].rows;
+  LQ_CUDA(cudaMemcpyAsync(L, side == 0 ? h->LA : h->LB, sizeof(float) * rows * h->R2, cudaMemcpyDeviceToDevice, h->st));
+  return LRQMM_OK;
+}
+
+lrqmm_status_t lrqmm_get_factors(lrqmm_handle_t h, lrqmm_side_t side, float* USigma, float* V) {
+  if (!h || (side != 0 && side != 1) || !USigma || !V) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (!(h->state & 4)) return LRQMM_ERR_STATE;
+  const int64_t rows = h->s[side].rows;
+  const int r = h->r;
+  // U Sigma lives in L_A[:, 0:r] (side A) or L_B[:, r:2r] (side B)
+  const float* src = side == 0 ? h->LA : h->LB + r;
+  LQ_CUDA(cudaMemcpy2DAsync(USigma, sizeof(float) * r, src, sizeof(float) * h->R2, sizeof(float) * r, rows,
+                            cudaMemcpyDeviceToDevice, h->st));
+  // V = Q1 V_W (K x r)
+  launch_apply_small(h->s[side].Q1, h->s[side].VW, nullptr, nullptr, h->cfg.k, h->W, h->W, r, V, r, 0, h->st);
+  return check_launch(h);
+}
+
+lrqmm_status_t lrqmm_get_timings(lrqmm_handle_t h, double us[8]) {
+  if (!h || !us) return LRQMM_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < 8; ++i) us[i] = 0.0;
+  if (!h->cfg.enable_timing) return LRQMM_ERR_STATE;
+  lrqmm_status_t e = lrqmm_sync(h);
+  if (e != LRQMM_OK) return e;
+  const int pairs[4][2] = {{0, 1}, {2, 3}, {4, 5}, {6, 7}};
+  for (int i = 0; i < 4; ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, h->ev[pairs[i][0]], h->ev[pairs[i][1]]) == cudaSuccess) us[i] = 1000.0 * ms;
+  }
+  return LRQMM_OK;
+}
+
+int64_t lrqmm_launch_count(lrqmm_handle_t h, int reset) {
+  (void)h;
+  const int64_t c = launch_counter();
+  if (reset) launch_counter() = 0;
+  return c;
+}
+
+}  // extern "C"

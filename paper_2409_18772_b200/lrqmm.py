@@ -1,0 +1,249 @@
+"""Thin ctypes binding of liblrqmm (include/lrqmm.h) — argument marshalling only.
+
+Every step of LRQMM runs in the library's CUDA kernels; torch is used only for
+device memory (tensors passed by data pointer) and the current CUDA stream.
+There is no CPU fallback: if liblrqmm.so is missing or no sm_100 GPU is present
+the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblrqmm.so")
+
+SIDE_A, SIDE_B = 0, 1
+ROUND = {"floor": 0, "trunc": 1, "nearest": 2}
+GRAN = {"row": 0, "tensor": 1}
+
+STATUS = {
+    0: "LRQMM_OK", 1: "LRQMM_ERR_INVALID_ARGUMENT", 2: "LRQMM_ERR_SHAPE", 3: "LRQMM_ERR_RANK",
+    4: "LRQMM_ERR_OVERFLOW", 5: "LRQMM_ERR_NONFINITE", 6: "LRQMM_ERR_STATE", 7: "LRQMM_ERR_CUDA",
+    8: "LRQMM_ERR_NCCL", 9: "LRQMM_ERR_ALLOC", 10: "LRQMM_ERR_UNSUPPORTED",
+}
+
+# every symbol include/lrqmm.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "lrqmm_get_unique_id", "lrqmm_create", "lrqmm_quantize", "lrqmm_rsvd_residual", "lrqmm_gemm",
+    "lrqmm_destroy", "lrqmm_sync", "lrqmm_run_host", "lrqmm_get_codes", "lrqmm_get_scales",
+    "lrqmm_gemm_int32", "lrqmm_get_factors", "lrqmm_get_correction", "lrqmm_correction_width",
+    "lrqmm_get_timings", "lrqmm_launch_count", "lrqmm_status_string",
+)
+
+
+class LrqmmError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        super().__init__(f"{where}: {STATUS.get(code, code)}")
+
+
+class Config(ctypes.Structure):
+    _fields_ = [
+        ("m", ctypes.c_int64), ("n", ctypes.c_int64), ("k", ctypes.c_int64),
+        ("bits", ctypes.c_int), ("rank", ctypes.c_int), ("oversample", ctypes.c_int),
+        ("power_iters", ctypes.c_int), ("rounding", ctypes.c_int), ("granularity", ctypes.c_int),
+        ("world_size", ctypes.c_int), ("world_rank", ctypes.c_int),
+        ("nccl_unique_id", ctypes.c_void_p), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
+        ("enable_timing", ctypes.c_int),
+    ]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load liblrqmm.so (raises OSError if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise OSError(f"{path} not found: build it with `python -m paper_2409_18772_b200.build`")
+    lib = ctypes.CDLL(path)
+    P, I64, I, F = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float
+    sig = {
+        "lrqmm_get_unique_id": (I, [P]),
+        "lrqmm_create": (I, [ctypes.POINTER(Config), ctypes.POINTER(P)]),
+        "lrqmm_quantize": (I, [P, I, P, I64]),
+        "lrqmm_rsvd_residual": (I, [P, P, P, I64]),
+        "lrqmm_gemm": (I, [P, F, F, P, I64]),
+        "lrqmm_destroy": (I, [P]),
+        "lrqmm_sync": (I, [P]),
+        "lrqmm_run_host": (I, [P, P, P, P, P, F, P]),
+        "lrqmm_get_codes": (I, [P, I, P, I64]),
+        "lrqmm_get_scales": (I, [P, I, P]),
+        "lrqmm_gemm_int32": (I, [P, P, I64]),
+        "lrqmm_get_factors": (I, [P, I, P, P]),
+        "lrqmm_get_correction": (I, [P, I, P]),
+        "lrqmm_correction_width": (I, [P]),
+        "lrqmm_get_timings": (I, [P, ctypes.POINTER(ctypes.c_double)]),
+        "lrqmm_launch_count": (I64, [P, I]),
+        "lrqmm_status_string": (ctypes.c_char_p, [I]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(code: int, where: str):
+    if code != 0:
+        raise LrqmmError(code, where)
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def _ld(t) -> int:
+    assert t.dim() == 2 and t.stride(1) == 1, "row-major with unit column stride expected"
+    return int(t.stride(0))
+
+
+def get_unique_id() -> bytes:
+    lib = load_library()
+    buf = (ctypes.c_ubyte * 128)()
+    _check(lib.lrqmm_get_unique_id(buf), "lrqmm_get_unique_id")
+    return bytes(buf)
+
+
+class Lrqmm:
+    """Handle around one LRQMM problem shape (lrqmm_create ... lrqmm_destroy)."""
+
+    def __init__(self, m: int, n: int, k: int, bits: int = 4, rank: int = 16, oversample: int = 5,
+                 power_iters: int = 1, rounding: str = "floor", granularity: str = "row",
+                 world_size: int = 1, world_rank: int = 0, unique_id: bytes | None = None,
+                 device: int = 0, stream=None, enable_timing: bool = False):
+        import torch
+
+        lib = load_library()
+        self.lib = lib
+        self.m, self.n, self.k = m, n, k
+        self.bits, self.rank, self.oversample = bits, rank, oversample
+        self.device = device
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        self._uid = (ctypes.c_ubyte * 128).from_buffer_copy(unique_id) if unique_id else None
+        cfg = Config(m, n, k, bits, rank, oversample, power_iters, ROUND[rounding], GRAN[granularity],
+                     world_size, world_rank, ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None,
+                     device, ctypes.c_void_p(stream.cuda_stream), 1 if enable_timing else 0)
+        h = ctypes.c_void_p()
+        _check(lib.lrqmm_create(ctypes.byref(cfg), ctypes.byref(h)), "lrqmm_create")
+        self.h = h
+        self._keep = {}
+
+    # ---- the five calls of the boundary ----
+    def quantize(self, side: int, X):
+        """X: float32 cuda tensor (rows x k); retained until rsvd_residual completes."""
+        self._keep[side] = X
+        _check(self.lib.lrqmm_quantize(self.h, side, _ptr(X), _ld(X)), "lrqmm_quantize")
+
+    def rsvd_residual(self, omega_a, omega_b):
+        assert omega_a.stride(0) == omega_b.stride(0)
+        _check(self.lib.lrqmm_rsvd_residual(self.h, _ptr(omega_a), _ptr(omega_b), _ld(omega_a)), "lrqmm_rsvd_residual")
+
+    def gemm(self, D, alpha: float = 1.0, beta: float = 0.0):
+        _check(self.lib.lrqmm_gemm(self.h, alpha, beta, _ptr(D), _ld(D)), "lrqmm_gemm")
+        return D
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.lrqmm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---- inspection ----
+    def sync(self):
+        _check(self.lib.lrqmm_sync(self.h), "lrqmm_sync")
+
+    def gemm_int32(self, C):
+        _check(self.lib.lrqmm_gemm_int32(self.h, _ptr(C), _ld(C)), "lrqmm_gemm_int32")
+        return C
+
+    def codes(self, side: int):
+        import torch
+
+        rows = self.m if side == SIDE_A else self.n
+        out = torch.empty((rows, self.k), dtype=torch.int8, device=f"cuda:{self.device}")
+        _check(self.lib.lrqmm_get_codes(self.h, side, _ptr(out), self.k), "lrqmm_get_codes")
+        return out
+
+    def scales(self, side: int):
+        import torch
+
+        rows = self.m if side == SIDE_A else self.n
+        out = torch.empty((rows,), dtype=torch.float32, device=f"cuda:{self.device}")
+        _check(self.lib.lrqmm_get_scales(self.h, side, _ptr(out)), "lrqmm_get_scales")
+        return out
+
+    def factors(self, side: int):
+        import torch
+
+        rows = self.m if side == SIDE_A else self.n
+        us = torch.empty((rows, self.rank), dtype=torch.float32, device=f"cuda:{self.device}")
+        v = torch.empty((self.k, self.rank), dtype=torch.float32, device=f"cuda:{self.device}")
+        _check(self.lib.lrqmm_get_factors(self.h, side, _ptr(us), _ptr(v)), "lrqmm_get_factors")
+        return us, v
+
+    def correction(self, side: int):
+        import torch
+
+        rows = self.m if side == SIDE_A else self.n
+        w = self.lib.lrqmm_correction_width(self.h)
+        out = torch.empty((rows, w), dtype=torch.float32, device=f"cuda:{self.device}")
+        _check(self.lib.lrqmm_get_correction(self.h, side, _ptr(out)), "lrqmm_get_correction")
+        return out
+
+    def timings_us(self):
+        arr = (ctypes.c_double * 8)()
+        _check(self.lib.lrqmm_get_timings(self.h, arr), "lrqmm_get_timings")
+        return dict(quantize_a=arr[0], quantize_b=arr[1], rsvd=arr[2], gemm=arr[3])
+
+    def launch_count(self, reset: bool = False) -> int:
+        return int(self.lib.lrqmm_launch_count(self.h, 1 if reset else 0))
+
+    # ---- end to end from host buffers ----
+    def run_host(self, A: np.ndarray, Bt: np.ndarray, omega_a: np.ndarray | None, omega_b: np.ndarray | None,
+                 D: np.ndarray, alpha: float = 1.0):
+        """All arrays C-contiguous float32 host arrays (pinned memory recommended)."""
+        def hp(a):
+            return None if a is None else ctypes.c_void_p(a.ctypes.data)
+        _check(self.lib.lrqmm_run_host(self.h, hp(A), hp(Bt), hp(omega_a), hp(omega_b), alpha, hp(D)),
+               "lrqmm_run_host")
+        return D
+
+
+def lrqmm_matmul(A, Bt, omega_a=None, omega_b=None, bits: int = 4, rank: int = 16, oversample: int = 5,
+                 power_iters: int = 1, rounding: str = "floor", granularity: str = "row",
+                 alpha: float = 1.0, beta: float = 0.0, D=None):
+    """One-shot D = alpha * LRQMM(A, B) + beta * D on the GPU (A: m x k, Bt: n x k, cuda fp32)."""
+    import torch
+
+    m, k = A.shape
+    n = Bt.shape[0]
+    with Lrqmm(m, n, k, bits, rank, oversample, power_iters, rounding, granularity, device=A.device.index or 0) as h:
+        h.quantize(SIDE_A, A)
+        h.quantize(SIDE_B, Bt)
+        if rank > 0:
+            h.rsvd_residual(omega_a, omega_b)
+        if D is None:
+            D = torch.empty((m, n), dtype=torch.float32, device=A.device)
+        h.gemm(D, alpha, beta)
+        h.sync()
+    return D

@@ -1,0 +1,203 @@
+"""CUDA path (through the C ABI) vs the fp64 oracle, element by element.
+
+Bars (north_star / DESIGN.md "Parity"):
+  * codes, lambda (as bits) and int32 accumulators: bit-exact;
+  * D: ||D_gpu - D_oracle||_F / ||D_oracle||_F <= 1e-4 and
+       err(D_gpu) <= 1.05 * err(D_oracle) against the exact fp64 product.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth as S
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2409_18772_b200 import SIDE_A, SIDE_B, Lrqmm, LrqmmError  # noqa: E402
+
+DEV = "cuda:0"
+TOL_D = 1e-4
+ERR_RATIO = 1.05
+
+
+def cu(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
+
+
+def run_gpu(A, Bt, bits, r, p, OmA=None, OmB=None, q=1, rounding="floor", gran="row", alpha=1.0, beta=0.0, D0=None):
+    M, K = A.shape
+    N = Bt.shape[0]
+    with Lrqmm(M, N, K, bits, r, p, q, rounding, gran) as h:
+        a, b = cu(A), cu(Bt)
+        h.quantize(SIDE_A, a)
+        h.quantize(SIDE_B, b)
+        if r > 0:
+            h.rsvd_residual(cu(OmA[:, : r + p]), cu(OmB[:, : r + p]))
+        D = cu(D0.astype(np.float32)) if D0 is not None else torch.empty((M, N), device=DEV)
+        h.gemm(D, alpha, beta)
+        h.sync()
+        out = dict(D=D.cpu().numpy().astype(np.float64), codes_a=h.codes(SIDE_A).cpu().numpy(),
+                   codes_b=h.codes(SIDE_B).cpu().numpy(), lam_a=h.scales(SIDE_A).cpu().numpy(),
+                   lam_b=h.scales(SIDE_B).cpu().numpy())
+        C = torch.empty((M, N), dtype=torch.int32, device=DEV)
+        h.gemm_int32(C)
+        h.sync()
+        out["c_int"] = C.cpu().numpy()
+    return out
+
+
+# ------------------------------------------------------------- K1 quantize
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("rounding", ["floor", "trunc", "nearest"])
+@pytest.mark.parametrize("gran", ["row", "tensor"])
+@pytest.mark.parametrize("shape", [(300, 1000), (130, 130), (5, 40000), (1000, 77)])
+def test_quantize_bit_exact(bits, rounding, gran, shape):
+    rows, K = shape
+    X = S.gen_matrix("normal", rows, K, 7 + bits)
+    X[0, :5] = [0.0, -0.0, 1e-42, -1e-42, 3.0]
+    X[1] = 0.0  # zero row -> lambda = 1
+    if rows > 3:
+        # exact lattice points and neighbours
+        lam = O.compute_scale(np.max(np.abs(X[2])), bits)
+        c = np.arange(-O.qmax_of(bits), O.qmax_of(bits) + 1)
+        n = min(len(c), K // 3)
+        lat = (c[:n] / lam).astype(np.float32)
+        X[2, :n] = lat
+        X[2, n:2 * n] = np.nextafter(lat, np.float32(1e30))
+        X[2, 2 * n:3 * n] = np.nextafter(lat, np.float32(-1e30))
+    codes, lamr = O.quantize(X, bits, rounding, gran)
+    with Lrqmm(rows, rows, K, bits, 0, 0, 1, rounding, gran) as h:
+        h.quantize(SIDE_A, cu(X))
+        h.quantize(SIDE_B, cu(X))
+        h.sync()
+        gc = h.codes(SIDE_A).cpu().numpy()
+        gl = h.scales(SIDE_A).cpu().numpy()
+    assert np.array_equal(gl.view(np.uint32), lamr.view(np.uint32))
+    assert np.array_equal(gc.astype(np.int64), codes)
+
+
+def test_quantize_strided_input():
+    X = S.gen_matrix("u01", 64, 300, 3)
+    big = np.zeros((64, 333), np.float32)
+    big[:, :300] = X
+    codes, lam = O.quantize(X, 4)
+    t = cu(big)[:, :300]
+    with Lrqmm(64, 64, 300, 4, 0, 0) as h:
+        h.quantize(SIDE_A, t)
+        h.quantize(SIDE_B, t)
+        h.sync()
+        assert np.array_equal(h.codes(SIDE_A).cpu().numpy().astype(np.int64), codes)
+
+
+def test_nonfinite_is_reported():
+    X = S.gen_matrix("normal", 32, 64, 1)
+    X[3, 5] = np.nan
+    with Lrqmm(32, 32, 64, 4, 0, 0) as h:
+        h.quantize(SIDE_A, cu(X))
+        with pytest.raises(LrqmmError) as ei:
+            h.sync()
+        assert ei.value.code == 5
+
+
+# ------------------------------------------------------------ K6 int GEMM
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("shape", [(128, 256, 128), (300, 520, 1000), (1024, 768, 4096), (37, 1000, 147)])
+def test_int32_accumulators_bit_exact(bits, shape):
+    M, N, K = shape
+    A, Bt, _, _ = S.problem(M, N, K, 1, s=2)
+    out = run_gpu(A, Bt, bits, 0, 0)
+    ca, la = O.quantize(A, bits)
+    cb, lb = O.quantize(Bt, bits)
+    assert np.array_equal(out["codes_a"].astype(np.int64), ca)
+    assert np.array_equal(out["codes_b"].astype(np.int64), cb)
+    assert np.array_equal(out["c_int"].astype(np.int64), O.int_gemm(ca, cb))
+
+
+def test_int32_extreme_values_int8():
+    # all codes at +-qmax: the largest |acc| for this K
+    M, N, K = 256, 256, 8192
+    A = np.ones((M, K), np.float32)
+    A[:, ::2] = -1.0
+    Bt = np.ones((N, K), np.float32)
+    out = run_gpu(A, Bt, 8, 0, 0)
+    assert np.array_equal(out["c_int"].astype(np.int64), O.int_gemm(*[O.quantize(x, 8)[0] for x in (A, Bt)]))
+
+
+# ---------------------------------------------------------- full LRQMM path
+def check_d(A, Bt, out, ref):
+    C = O.matmul_exact(A, Bt)
+    diff = O.relative_error(ref, out["D"])
+    e_gpu, e_or = O.relative_error(C, out["D"]), O.relative_error(C, ref)
+    assert diff <= TOL_D, (diff, e_gpu, e_or)
+    assert e_gpu <= ERR_RATIO * e_or + 1e-12, (e_gpu, e_or)
+    return diff, e_gpu, e_or
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("dist", ["normal", "u01", "exp4", "pois10"])
+@pytest.mark.parametrize("shape,r,p", [((256, 256, 256), 8, 5), ((384, 272, 520), 10, 5), ((200, 333, 1100), 4, 0),
+                                       ((1000, 130, 700), 16, 5)])
+def test_lrqmm_matches_oracle(bits, dist, shape, r, p):
+    M, N, K = shape
+    A, Bt, OmA, OmB = S.problem(M, N, K, r + p, s=1, dist=dist)
+    ref, parts = O.lrqmm(A, Bt, bits, r, OmA, OmB, q=1, return_parts=True)
+    out = run_gpu(A, Bt, bits, r, p, OmA, OmB)
+    assert np.array_equal(out["codes_a"].astype(np.int64), parts["codes_a"])
+    assert np.array_equal(out["lam_b"].view(np.uint32), parts["lam_b"].view(np.uint32))
+    assert np.array_equal(out["c_int"].astype(np.int64), parts["c_int"])
+    check_d(A, Bt, out, ref)
+
+
+@pytest.mark.parametrize("q", [1, 2])
+@pytest.mark.parametrize("r,p", [(1, 0), (32, 5), (20, 20)])
+def test_lrqmm_rank_and_power_iters(q, r, p):
+    A, Bt, OmA, OmB = S.problem(320, 300, 640, r + p, s=5, dist="u01")
+    ref = O.lrqmm(A, Bt, 4, r, OmA, OmB, q=q)
+    check_d(A, Bt, run_gpu(A, Bt, 4, r, p, OmA, OmB, q=q), ref)
+
+
+def test_direct_quant_modes_match_oracle():
+    A, Bt, _, _ = S.problem(300, 260, 900, 1, s=3, dist="u01")
+    for rounding, gran in [("trunc", "tensor"), ("nearest", "row"), ("floor", "row")]:
+        ref = O.lrqmm(A, Bt, 4, 0, rounding=rounding, granularity=gran)
+        out = run_gpu(A, Bt, 4, 0, 0, rounding=rounding, gran=gran)
+        assert O.relative_error(ref, out["D"]) <= 1e-6
+
+
+def test_alpha_beta():
+    A, Bt, OmA, OmB = S.problem(256, 256, 384, 13, s=2)
+    D0 = np.random.default_rng(0).standard_normal((256, 256)).astype(np.float32)
+    ref = O.lrqmm(A, Bt, 4, 8, OmA, OmB, alpha=1.5, beta=-0.5, D=D0)
+    out = run_gpu(A, Bt, 4, 8, 5, OmA, OmB, alpha=1.5, beta=-0.5, D0=D0)
+    assert O.relative_error(ref, out["D"]) <= TOL_D
+
+
+def test_zero_residual_and_rank1_fixture():
+    rng = np.random.default_rng(8)
+    q = 7
+    ca = rng.integers(-q, q + 1, (200, 256))
+    cb = rng.integers(-q, q + 1, (136, 256))
+    ca[:, 0] = q
+    cb[:, 0] = -q
+    A = (ca / 4.0).astype(np.float32)
+    Bt = (cb / 0.5).astype(np.float32)
+    Om = S.gen_omega(256, 9, 3)
+    out = run_gpu(A, Bt, 4, 4, 5, Om, Om)
+    assert np.max(np.abs(out["D"] - O.matmul_exact(A, Bt))) <= 1e-5 * np.max(np.abs(O.matmul_exact(A, Bt)))
+
+
+def test_deterministic_reruns():
+    A, Bt, OmA, OmB = S.problem(512, 384, 1024, 21, s=4)
+    o1 = run_gpu(A, Bt, 4, 16, 5, OmA, OmB)
+    o2 = run_gpu(A, Bt, 4, 16, 5, OmA, OmB)
+    assert np.array_equal(o1["D"], o2["D"])
+
+
+def test_run_host_e2e_matches_device_path():
+    A, Bt, OmA, OmB = S.problem(256, 192, 320, 13, s=6)
+    ref = O.lrqmm(A, Bt, 4, 8, OmA, OmB)
+    D = np.empty((256, 192), np.float32)
+    with Lrqmm(256, 192, 320, 4, 8, 5) as h:
+        h.run_host(A, Bt, np.ascontiguousarray(OmA[:, :13]), np.ascontiguousarray(OmB[:, :13]), D)
+    assert O.relative_error(ref, D) <= TOL_D
