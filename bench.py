@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""LRQMM hot-path benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lrqmm|reference] [--config c3|c2|c1]
+
+A step = one pass of the whole hot path over one batch of synthetic input:
+quantize(A), quantize(B), rsvd_residual, gemm (Algorithm 2).
+Default workload (N=1): BASELINE.json configs[2], 16384^3 int4, rank 16, p=5, q=1,
+Gaussian A and B.  Under torchrun (N>1) every rank holds its own 16384-row block
+of A (global M = 16384*N, weak scaling) and the same B; the A-side RSVD is
+coupled across ranks by NCCL allreduces inside liblrqmm.
+
+One JSON line on rank 0.  `value` = effective TOPS (2*M*N*K / step time, all
+ranks), inputs resident in HBM (2 GiB of fp32 inputs per GPU > 126 MB L2, so no
+L2 flush is needed).  `e2e` = the same metric through lrqmm_run_host with pinned
+HOST buffers (H2D of A, B^T, Omega and D2H of D inside the timed region).
+`--impl reference` times the fp64 CPU oracle (test infrastructure) on a
+bounded row sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (M per rank, N, K, bits, rank, oversample, dist, workload label)
+    "c3": (16384, 16384, 16384, 4, 16, 5, "normal", "square 16384^3 int4 rank 16 (p=5, q=1) Gaussian, configs[2]"),
+    "c2": (4096, 4096, 4096, 4, 16, 5, "normal", "square 4096^3 int4 rank 16 (p=5, q=1) Gaussian, configs[1]"),
+    "c2i8": (4096, 4096, 4096, 8, 16, 5, "normal", "square 4096^3 int8 rank 16 (p=5, q=1) Gaussian, configs[1]"),
+    "c1": (256, 256, 256, 4, 8, 5, "normal", "square 256^3 int4 rank 8 (p=5, q=1) Gaussian, configs[0]"),
+    "c5": (4096, 32768, 32768, 4, 32, 5, "normal", "32768^3 int4 rank 32 row-sharded (4096 rows/rank), configs[4]"),
+}
+METRIC = "effective TOPS (2MNK/t) of the LRQMM hot path; overhead vs bare int8 GEMM; rel. Frobenius error vs direct quant"
+REF_ROWS = 256  # oracle row sample per reference / cpu_baseline step
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="lrqmm", choices=["lrqmm", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm_sorted = sorted(sm)
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        busy.sort()
+        return {"sm_mhz": busy[len(busy) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(pw), "sm_mhz_min": sm_sorted[0]}
+
+
+# -------------------------------------------------------------- dist utils
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, ws: int, local: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------ oracle legs
+def oracle_sample(cfg, seed_base=0, rows=REF_ROWS):
+    """Time the fp64 oracle (as it stands) on a bounded row sample of the workload:
+    the first `rows` rows of A against the full B.  Returns (seconds, ops_sampled)."""
+    import numpy as np
+
+    import oracle as O
+    import synth as S
+
+    M, N, K, bits, r, p, dist_name, _ = cfg
+    A = S.gen_matrix(dist_name, rows, K, 2 * seed_base)
+    Bt = S.gen_matrix(dist_name, N, K, 2 * seed_base + 1)
+    OmA = S.gen_omega(K, r + p, 1000 + 2 * seed_base)
+    OmB = S.gen_omega(K, r + p, 1001 + 2 * seed_base)
+    t0 = time.perf_counter()
+    O.lrqmm(A, Bt, bits, r, OmA, OmB, q=1)
+    dt = time.perf_counter() - t0
+    del A, Bt
+    return dt, 2.0 * rows * N * K
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args, ws, rank):
+    cfg = CONFIGS[args.config]
+    if rank != 0:
+        return
+    M, N, K = cfg[0] * ws, cfg[1], cfg[2]
+    times = []
+    ops = 0.0
+    for i in range(args.warmup + args.steps):
+        dt, ops = oracle_sample(cfg)
+        if i >= args.warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    val = ops / t / 1e12
+    sample = f"oracle (NumPy fp64) on the first {REF_ROWS} rows of A x full B^T ({cfg[1]}x{cfg[2]}), full quantize+RSVD of B"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "TOPS", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg[7], "M": M, "N": N, "K": K, "bits": cfg[3], "rank": cfg[4], "oversample": cfg[5],
+                   "power_iters": 1, "sample_rows": REF_ROWS},
+        "cpu_baseline": {"value": val, "unit": "TOPS", "cores": cpu_cores(), "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return
+
+    import numpy as np
+    import torch
+
+    import synth as S
+    from paper_2409_18772_b200 import SIDE_A, SIDE_B, Lrqmm, get_unique_id
+
+    cfg = CONFIGS[args.config]
+    Mloc, N, K, bits, r, p, dist_name, label = cfg
+    kk = r + p
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    # synthetic inputs (seeded, per-rank A block), resident in HBM
+    A = S.gen_matrix_torch(dist_name, Mloc, K, 2 * 0 + 7919 * rank, device=dev)
+    Bt = S.gen_matrix_torch(dist_name, N, K, 1, device=dev)
+    OmA = torch.from_numpy(S.gen_omega(K, kk, 1000)).to(dev)
+    OmB = torch.from_numpy(S.gen_omega(K, kk, 1001)).to(dev)
+    D = torch.empty((Mloc, N), device=dev)
+    Cint = torch.empty((Mloc, N), dtype=torch.int32, device=dev)
+
+    uid = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        t = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(get_unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        uid = bytes(t.cpu().numpy().tobytes())
+    h = Lrqmm(Mloc, N, K, bits, r, p, 1, "floor", "row", world_size=ws, world_rank=rank, unique_id=uid,
+              device=local, stream=stream, enable_timing=False)
+
+    def step():
+        h.quantize(SIDE_A, A)
+        h.quantize(SIDE_B, Bt)
+        h.rsvd_residual(OmA, OmB)
+        h.gemm(D)
+
+    for _ in range(args.warmup):
+        step()
+    h.sync()
+    torch.cuda.synchronize(dev)
+    barrier(ws)
+
+    # timed region: K steps, per-phase events on the launching stream
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    h.launch_count(reset=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        barrier(ws)
+        e0.record(stream)
+        for i in range(args.steps):
+            ev = evs[i]
+            ev[0].record(stream)
+            h.quantize(SIDE_A, A)
+            h.quantize(SIDE_B, Bt)
+            ev[1].record(stream)
+            h.rsvd_residual(OmA, OmB)
+            ev[2].record(stream)
+            h.gemm(D)
+            ev[3].record(stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier(ws)
+    launches = h.launch_count()
+    h.sync()
+    t_step = e0.elapsed_time(e1) / 1e3 / args.steps
+    ph = np.array([[ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])] for ev in evs]) / 1e3
+    t_quant, t_rsvd, t_gemm = [float(x) for x in ph.mean(axis=0)]
+    t_step = max_over_ranks(t_step, ws, local)
+
+    # bare int8 GEMM (same tcgen05 kernel, int32 epilogue): the overhead denominator
+    for _ in range(2):
+        h.gemm_int32(Cint)
+    torch.cuda.synchronize(dev)
+    b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    b0.record(stream)
+    for _ in range(args.steps):
+        h.gemm_int32(Cint)
+    b1.record(stream)
+    torch.cuda.synchronize(dev)
+    t_bare = b0.elapsed_time(b1) / 1e3 / args.steps
+
+    # direct-quant pipeline (quantize x2 + dequant GEMM, rank 0)
+    hd = Lrqmm(Mloc, N, K, bits, 0, 0, 1, "floor", "row", device=local, stream=stream)
+    for _ in range(2):
+        hd.quantize(SIDE_A, A); hd.quantize(SIDE_B, Bt); hd.gemm(D)
+    torch.cuda.synchronize(dev)
+    b0.record(stream)
+    for _ in range(args.steps):
+        hd.quantize(SIDE_A, A); hd.quantize(SIDE_B, Bt); hd.gemm(D)
+    b1.record(stream)
+    torch.cuda.synchronize(dev)
+    t_dq = b0.elapsed_time(b1) / 1e3 / args.steps
+    hd.close()
+
+    # accuracy on a row sample (exact product in fp64 for 256 rows)
+    errs = {}
+    if rank == 0:
+        rows = torch.arange(0, Mloc, max(1, Mloc // 256), device=dev)[:256]
+        Cex = A[rows].double() @ Bt.double().T
+        step()
+        h.sync()
+        nrm = torch.linalg.norm(Cex)
+        errs["lrqmm"] = float(torch.linalg.norm(D[rows].double() - Cex) / nrm)
+        for name, rnd, gran in (("dq_paper_trunc_tensor", "trunc", "tensor"), ("dq_nearest_row", "nearest", "row"),
+                                ("dq_floor_row", "floor", "row")):
+            with Lrqmm(Mloc, N, K, bits, 0, 0, 1, rnd, gran, device=local, stream=stream) as hq:
+                hq.quantize(SIDE_A, A); hq.quantize(SIDE_B, Bt); hq.gemm(D); hq.sync()
+            errs[name] = float(torch.linalg.norm(D[rows].double() - Cex) / nrm)
+        del Cex
+
+    # end to end through the C ABI with pinned HOST buffers (rank 0 measures; all ranks run)
+    e2e = None
+    if not args.no_e2e and ws == 1:
+        hA = torch.empty((Mloc, K), dtype=torch.float32, pin_memory=True)
+        hB = torch.empty((N, K), dtype=torch.float32, pin_memory=True)
+        hOa = torch.empty((K, kk), dtype=torch.float32, pin_memory=True)
+        hOb = torch.empty((K, kk), dtype=torch.float32, pin_memory=True)
+        hD = torch.empty((Mloc, N), dtype=torch.float32, pin_memory=True)
+        hA.copy_(A); hB.copy_(Bt); hOa.copy_(OmA); hOb.copy_(OmB)
+        he = Lrqmm(Mloc, N, K, bits, r, p, 1, "floor", "row", device=local, stream=stream)
+        npA, npB, npOa, npOb, npD = hA.numpy(), hB.numpy(), hOa.numpy(), hOb.numpy(), hD.numpy()
+        he.run_host(npA, npB, npOa, npOb, npD)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            he.run_host(npA, npB, npOa, npOb, npD)
+        t_e2e = (time.perf_counter() - t0) / args.e2e_steps
+        he.close()
+        h2d = 4 * (Mloc * K + N * K + 2 * K * kk)
+        d2h = 4 * Mloc * N
+        e2e = {"value": 2.0 * Mloc * N * K / t_e2e / 1e12, "unit": "TOPS", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
+               "note": "lrqmm_run_host: pinned host A, B^T, Omega -> device, full hot path, D -> host; host wall clock"}
+        del hA, hB, hD
+
+    h.close()
+    if rank != 0:
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return
+
+    Mtot = Mloc * ws
+    ops = 2.0 * Mtot * N * K
+    peaks, peak_src = load_peaks()
+    int8_peak = 2.0 * float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+    gemm_tops = 2.0 * Mloc * N * K / t_gemm / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "gemm_ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            if pj.get("config") == args.config:
+                traffic = pj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        dt, sops = oracle_sample(cfg)
+        cpu = {"value": sops / dt / 1e12, "unit": "TOPS", "cores": cpu_cores(), "kind": "oracle",
+               "sample": f"NumPy fp64 oracle on the first {REF_ROWS} rows of A x full B^T ({N}x{K}), "
+                         f"incl. full quantize + RSVD of B; {dt:.1f} s"}
+
+    line = {
+        "metric": METRIC,
+        "value": ops / t_step / 1e12,
+        "unit": "TOPS",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int8",
+        "data": "synthetic",
+        "config": {"workload": label, "M": Mtot, "M_per_gpu": Mloc, "N": N, "K": K, "bits": bits, "rank": r,
+                   "oversample": p, "power_iters": 1, "rounding": "floor", "scales": "per-row A / per-col B",
+                   "l2": "inputs 2 GiB fp32/GPU > 126 MB L2 (no flush)",
+                   "parallelism": f"row-shard A x{ws}, B replicated" if ws > 1 else "single GPU"},
+        "overhead_vs_bare_int8": t_step / t_bare,
+        "overhead_vs_direct_quant": t_step / t_dq,
+        "ms": {"bare_int8_gemm": t_bare * 1e3, "direct_quant_pipeline": t_dq * 1e3, "quantize_AB": t_quant * 1e3,
+               "rsvd_residual": t_rsvd * 1e3, "gemm_fused_epilogue": t_gemm * 1e3},
+        "bare_int8_tops": 2.0 * Mloc * N * K / t_bare / 1e12,
+        "rel_fro_error": errs,
+        "roofline": {"bound": "tensor", "kernel": "k6_gemm_i8 (tcgen05 kind::i8 + fused LRQMM epilogue)",
+                     "achieved": gemm_tops, "peak": int8_peak, "unit": "TFLOP/s", "frac": gemm_tops / int8_peak,
+                     "traffic": traffic,
+                     "peak_note": f"int8 dense = 2 x {peak_src} bf16 sustained ({peaks.get('bf16_tflops_sustained')}) "
+                                  "(guide nominal ratio 4.5/2.25)"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    if e2e:
+        line["e2e"] = e2e
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
