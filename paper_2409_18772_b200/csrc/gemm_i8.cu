@@ -28,14 +28,18 @@ constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int BK = 128;  // bytes = int8 elements per stage (one 128B swizzle atom row)
 constexpr int UK = 32;   // K per tcgen05.mma kind::i8
-constexpr int STAGES = 4;
 constexpr int kThreads = 192;
+constexpr int kEpiThreads = 128;
 constexpr int kABytes = BM * BK;
 constexpr int kBBytes = BN * BK;
 constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
 constexpr int kGroupM = 16;     // tile rasterisation: 16 M-blocks per group (L2 reuse)
-constexpr int kSmemBytes = STAGES * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
+// 4 smem stages while the L_B tile fits beside them, 3 for the widest corrections
+__host__ __device__ constexpr int stages_for(int r2) { return r2 > 32 ? 3 : 4; }
+__host__ __device__ constexpr int smem_bytes(int r2) {
+  return stages_for(r2) * kStageBytes + BN * r2 * 4 + BN * 4 + 256 /*barriers*/ + 1024 /*align*/;
+}
 }  // namespace g6
 
 struct G6Params {
@@ -47,7 +51,6 @@ struct G6Params {
   const float* lam_b;
   const float* LA;
   const float* LB;
-  int R2;
   float alpha, beta;
   float* D;
   int32_t* Cint;
@@ -65,59 +68,59 @@ LRQMM_DEV void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
   nb = in / gsize;
 }
 
+LRQMM_DEV void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(g6::kEpiThreads) : "memory"); }
+
+// one 8-column group of one output row: acc (int32 from TMEM) -> D or Cint.
+// Kept small and rolled (the 256-column tile is walked in 32 groups) so the
+// epilogue code stays resident in the instruction cache.
 template <int kR2>
-LRQMM_DEV void epilogue_chunk(const G6Params& p, const uint32_t (&acc)[32], int64_t row, int col0, float sa,
-                              const float (&la)[kR2 > 0 ? kR2 : 1]) {
-  if (row >= p.M) return;
+LRQMM_DEV void epilogue_group(const G6Params& p, const uint32_t (&acc)[8], int64_t row, int col0, int cl0,
+                              float sa, const float (&la)[kR2 > 0 ? kR2 : 1], const float* __restrict__ sLB,
+                              const float* __restrict__ sSB) {
+  if (row >= p.M || col0 >= p.N) return;
+  const bool full = p.vec_ok && col0 + 8 <= p.N;
   if (p.epi == 0) {
     int32_t* out = p.Cint + row * p.ldd + col0;
-    if (p.vec_ok && col0 + 32 <= p.N) {
-#pragma unroll
-      for (int c = 0; c < 32; c += 4)
-        *reinterpret_cast<int4*>(out + c) = make_int4((int)acc[c], (int)acc[c + 1], (int)acc[c + 2], (int)acc[c + 3]);
+    if (full) {
+      __stcs(reinterpret_cast<int4*>(out), make_int4((int)acc[0], (int)acc[1], (int)acc[2], (int)acc[3]));
+      __stcs(reinterpret_cast<int4*>(out + 4), make_int4((int)acc[4], (int)acc[5], (int)acc[6], (int)acc[7]));
     } else {
-      for (int c = 0; c < 32; ++c)
+      for (int c = 0; c < 8; ++c)
         if (col0 + c < p.N) out[c] = (int)acc[c];
     }
     return;
   }
-  float v[32];
+  // v = alpha * (acc / (lambda_a lambda_b) + L_A[row] . L_B[col]);  sa, la carry alpha
+  float v[8];
 #pragma unroll
-  for (int c = 0; c < 32; ++c) {
-    const int col = min(col0 + c, (int)p.N - 1);
-    const float sb = __frcp_rn(__ldg(p.lam_b + col));
-    float t = __fmul_rn(static_cast<float>(static_cast<int32_t>(acc[c])), __fmul_rn(sa, sb));
-    if constexpr (kR2 > 0) {
-      const float4* lb = reinterpret_cast<const float4*>(p.LB + (int64_t)col * kR2);
-      float corr = 0.f;
+  for (int c = 0; c < 8; ++c) v[c] = __fmul_rn(static_cast<float>(static_cast<int32_t>(acc[c])), __fmul_rn(sa, sSB[cl0 + c]));
+  if constexpr (kR2 > 0) {
 #pragma unroll
-      for (int l = 0; l < kR2; l += 4) {
-        const float4 b = __ldg(lb + (l >> 2));
-        corr = fmaf(la[l + 0], b.x, corr);
-        corr = fmaf(la[l + 1], b.y, corr);
-        corr = fmaf(la[l + 2], b.z, corr);
-        corr = fmaf(la[l + 3], b.w, corr);
+    for (int l = 0; l < kR2; l += 4) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 b = *reinterpret_cast<const float4*>(sLB + (cl0 + c) * kR2 + l);
+        v[c] = fmaf(la[l + 0], b.x, v[c]);
+        v[c] = fmaf(la[l + 1], b.y, v[c]);
+        v[c] = fmaf(la[l + 2], b.z, v[c]);
+        v[c] = fmaf(la[l + 3], b.w, v[c]);
       }
-      t = t + corr;
     }
-    v[c] = p.alpha * t;
   }
   float* out = p.D + row * p.ldd + col0;
-  if (p.vec_ok && col0 + 32 <= p.N) {
+  if (full) {
     if (p.beta != 0.f) {
-#pragma unroll
-      for (int c = 0; c < 32; c += 4) {
-        const float4 o = *reinterpret_cast<const float4*>(out + c);
-        v[c] = fmaf(p.beta, o.x, v[c]);
-        v[c + 1] = fmaf(p.beta, o.y, v[c + 1]);
-        v[c + 2] = fmaf(p.beta, o.z, v[c + 2]);
-        v[c + 3] = fmaf(p.beta, o.w, v[c + 3]);
-      }
+      const float4 o0 = *reinterpret_cast<const float4*>(out);
+      const float4 o1 = *reinterpret_cast<const float4*>(out + 4);
+      v[0] = fmaf(p.beta, o0.x, v[0]); v[1] = fmaf(p.beta, o0.y, v[1]);
+      v[2] = fmaf(p.beta, o0.z, v[2]); v[3] = fmaf(p.beta, o0.w, v[3]);
+      v[4] = fmaf(p.beta, o1.x, v[4]); v[5] = fmaf(p.beta, o1.y, v[5]);
+      v[6] = fmaf(p.beta, o1.z, v[6]); v[7] = fmaf(p.beta, o1.w, v[7]);
     }
-#pragma unroll
-    for (int c = 0; c < 32; c += 4) __stcs(reinterpret_cast<float4*>(out + c), make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]));
+    __stcs(reinterpret_cast<float4*>(out), make_float4(v[0], v[1], v[2], v[3]));
+    __stcs(reinterpret_cast<float4*>(out + 4), make_float4(v[4], v[5], v[6], v[7]));
   } else {
-    for (int c = 0; c < 32; ++c) {
+    for (int c = 0; c < 8; ++c) {
       if (col0 + c < p.N) {
         float o = v[c];
         if (p.beta != 0.f) o = fmaf(p.beta, out[c], o);
@@ -131,11 +134,14 @@ template <int kR2>
 __global__ void __launch_bounds__(g6::kThreads, 1)
     k6_gemm_i8(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, G6Params p) {
   using namespace g6;
+  constexpr int STAGES = stages_for(kR2);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * kABytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  float* sLB = reinterpret_cast<float*>(smem + STAGES * kStageBytes);  // BN x kR2
+  float* sSB = sLB + BN * kR2;                                           // BN : 1/lambda_b
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sSB + BN);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
@@ -155,7 +161,7 @@ __global__ void __launch_bounds__(g6::kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], kEpiThreads);
     }
     fence_mbar_init();
   }
@@ -216,7 +222,8 @@ __global__ void __launch_bounds__(g6::kThreads, 1)
     __syncwarp();
   } else {
     // ---------------------------------------------------------------- epilogue
-    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    const int et = threadIdx.x - 64;  // 0..127
+    const int quad = warp & 3;        // TMEM lane quadrant this warp may access
     int lt = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
       int mb, nb;
@@ -224,32 +231,52 @@ __global__ void __launch_bounds__(g6::kThreads, 1)
       const int acc = lt & 1;
       const uint32_t acc_phase = (lt >> 1) & 1;
       const int64_t row = (int64_t)mb * BM + quad * 32 + lane;
+      const int n0 = nb * BN;
       float sa = 0.f;
       float la[kR2 > 0 ? kR2 : 1];
-      if (p.epi == 1 && row < p.M) {
-        sa = __frcp_rn(p.lam_a[row]);
-        if constexpr (kR2 > 0) {
-          const float4* lr = reinterpret_cast<const float4*>(p.LA + row * kR2);
 #pragma unroll
-          for (int l = 0; l < kR2; l += 4) {
-            const float4 v = __ldg(lr + (l >> 2));
-            la[l] = v.x; la[l + 1] = v.y; la[l + 2] = v.z; la[l + 3] = v.w;
+      for (int l = 0; l < (kR2 > 0 ? kR2 : 1); ++l) la[l] = 0.f;
+      if (p.epi == 1) {
+        // stage this tile's column data (L_B rows, 1/lambda_b) while the mainloop runs
+        epi_bar();  // previous tile's readers are done
+        for (int j = et; j < BN; j += kEpiThreads) {
+          const int col = n0 + j;
+          sSB[j] = col < p.N ? __frcp_rn(__ldg(p.lam_b + col)) : 0.f;
+        }
+        if constexpr (kR2 > 0) {
+          const float4* src = reinterpret_cast<const float4*>(p.LB + (int64_t)n0 * kR2);
+          float4* dst = reinterpret_cast<float4*>(sLB);
+          const int total4 = BN * kR2 / 4;
+          const int valid4 = (int)((p.N - n0 < BN ? p.N - n0 : (int64_t)BN) * kR2 / 4);
+          for (int e = et; e < total4; e += kEpiThreads) dst[e] = e < valid4 ? __ldg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (row < p.M) {
+          sa = p.alpha * __frcp_rn(p.lam_a[row]);
+          if constexpr (kR2 > 0) {
+            const float4* lr = reinterpret_cast<const float4*>(p.LA + row * kR2);
+#pragma unroll
+            for (int l = 0; l < kR2; l += 4) {
+              const float4 v = __ldg(lr + (l >> 2));
+              la[l] = p.alpha * v.x; la[l + 1] = p.alpha * v.y; la[l + 2] = p.alpha * v.z; la[l + 3] = p.alpha * v.w;
+            }
           }
         }
-      } else {
-#pragma unroll
-        for (int l = 0; l < (kR2 > 0 ? kR2 : 1); ++l) la[l] = 0.f;
+        epi_bar();  // staged data visible to all epilogue warps
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      // ping-pong 8-column TMEM loads: load group g+1 while computing group g
+      uint32_t ra[8], rb[8];
+      tmem_ld_32x32b_x8(t_row, ra);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_row + c * 32, r);
+      for (int g = 0; g < BN / 8; g += 2) {
         tmem_ld_wait();
-        const int col0 = nb * BN + c * 32;
-        if (col0 < p.N) epilogue_chunk<kR2>(p, r, row, col0, sa, la);
+        tmem_ld_32x32b_x8(t_row + (g + 1) * 8, rb);
+        epilogue_group<kR2>(p, ra, row, n0 + g * 8, g * 8, sa, la, sLB, sSB);
+        tmem_ld_wait();
+        if (g + 2 < BN / 8) tmem_ld_32x32b_x8(t_row + (g + 2) * 8, ra);
+        epilogue_group<kR2>(p, rb, row, n0 + (g + 1) * 8, (g + 1) * 8, sa, la, sLB, sSB);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -300,12 +327,14 @@ int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB) {
 
 template <int kR2>
 static void launch_t(const G6Params& p, const CUtensorMap* mA, const CUtensorMap* mB, int grid, cudaStream_t st) {
+  constexpr int kSmem = g6::smem_bytes(kR2);
+  static_assert(kSmem <= 232448, "shared memory budget");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k6_gemm_i8<kR2>, cudaFuncAttributeMaxDynamicSharedMemorySize, g6::kSmemBytes);
+    cudaFuncSetAttribute(k6_gemm_i8<kR2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     attr = true;
   }
-  k6_gemm_i8<kR2><<<grid, g6::kThreads, g6::kSmemBytes, st>>>(*mA, *mB, p); ++launch_counter();
+  k6_gemm_i8<kR2><<<grid, g6::kThreads, kSmem, st>>>(*mA, *mB, p); ++launch_counter();
 }
 
 void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStream_t st) {
@@ -321,7 +350,6 @@ void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStre
   p.lam_b = g.lam_b;
   p.LA = g.LA;
   p.LB = g.LB;
-  p.R2 = g.R2;
   p.alpha = g.alpha;
   p.beta = g.beta;
   p.D = g.D;
