@@ -31,8 +31,7 @@ void launch_tensor_scale(const float* X, int64_t ldx, int64_t rows, int K, int q
 // ------------------------------------------------- K2/K3 skinny residual products
 // F(x_ij) is recomputed from X and lambda_i (never stored):
 //   residual  r = (lambda*x - code)/lambda            (Alg. 2)
-//   dequant   x~ = code / lambda                      (Alg. 2)
-enum { kFRes = 0, kFDeq = 1 };
+//   codes     c (exact in tf32), scaled by 1/lambda   (Alg. 2)
 struct SideView {
   const float* X;
   int64_t ldx;
@@ -41,33 +40,45 @@ struct SideView {
   const float* lam;
   int qmax, mode;
 };
-// OUT1[i,c] = sum_j F1(x_ij) P1[j,c]  (and optionally OUT2 with F2/P2), c < W.
-// P is K x W (ld W), OUT is rows x W (ld W).  Deterministic split-K with partial buffer.
-void launch_proj_rows(const SideView& s, const float* P1, int f1, float* OUT1, const float* P2, int f2, float* OUT2,
-                      int W, float* partial, int64_t partial_elems, cudaStream_t st);
-// OUT[j,c] = sum_i F(x_ij) P[i,c]: P is rows x W, OUT is K x W.
-void launch_proj_cols(const SideView& s, const float* P, int f, float* OUT, int W, float* partial,
-                      int64_t partial_elems, cudaStream_t st);
+// tcgen05 kind::tf32 (3-term split) passes, deterministic split-K partials:
+// ROW: OUT1 = R P1 (rows x W); dual (P2 != null): OUT2 = X~ P2.  P is K x W (ld W).
+void launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
+                         float* partial, int64_t partial_elems, cudaStream_t st);
+// COL: OUT = R^T P; P is rows x W, OUT is K x W.
+void launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t partial_elems,
+                         cudaStream_t st);
 
-// G = Y1^T Y2 (W x W, fp64) over n rows; Y ld W.  Deterministic 2-stage.
-void launch_gram(const float* Y1, const float* Y2, int64_t n, int W, double* G, double* partial, int64_t partial_elems,
-                 cudaStream_t st);
 // OUT[i, col0 + o] = sum_c IN1[i,c] S1[c,o] (+ sum_c IN2[i,c] S2[c,o]), o < nout; IN ld W, S ld ldS, OUT ld ldo
 void launch_apply_small(const float* IN1, const float* S1, const float* IN2, const float* S2, int64_t n, int W,
                         int ldS, int nout, float* OUT, int64_t ldo, int col0, cudaStream_t st);
 
 // ----------------------------------------------------------- K4 small solvers
-// For each of nsides problems: G (n x n fp64, symmetric) -> Jacobi eigendecomposition.
-//   mode ORTH : T[n x n] = V diag(keep ? lambda^-1/2 : 0), keep: lambda >= rtol2 * lambda_max
-//   mode TRUNC: T[n x n] = first r columns = top-r eigenvectors (descending), rest 0
-enum { kEigOrth = 0, kEigTrunc = 1 };
+struct GramJob {  // G = Y1^T Y2 (W x W, fp64) over n rows (Y ld W)
+  const float* Y1;
+  const float* Y2;
+  int64_t n;
+  double* G;
+  double* partial;  // >= 148 * W * W
+  int* counter;     // zero-initialised ticket
+};
+struct GramJobs {
+  GramJob j[2];
+  int n;
+};
+void launch_gram_jobs(const GramJobs& jobs, int W, cudaStream_t st);
 struct EigJob {
   const double* G;
   float* T;
-  int mode;
   int r;
 };
-void launch_eig(const EigJob* jobs, int njobs, int n, cudaStream_t st);
+struct EigJobs {
+  EigJob j[2];
+  int n;
+};
+// orth transform (pivoted Cholesky QR, reading #12 threshold): Q = Y T has orthonormal columns
+void launch_chol_orth(const EigJobs& jobs, int n, cudaStream_t st);
+// truncation: T[:, 0:r] = top-r eigenvectors of G (descending), rest 0
+void launch_eig_warp(const EigJobs& jobs, int n, cudaStream_t st);
 // Mab[r x r] = VWb^T C VWa  and  VWbM[n x r] = VWb Mab   (C = Q1_B^T Q1_A, n x n fp64)
 void launch_cross_small(const double* C, const float* VWa, const float* VWb, int n, int r, float* VWbM,
                         cudaStream_t st);

@@ -35,6 +35,8 @@ struct Side {
   float* Q1 = nullptr;       // K x W
   float* Gp = nullptr;       // rows x W : X~ Q1_other
   double* G = nullptr;       // W x W
+  double* gpart = nullptr;   // 148 x W x W Gram partials
+  int* counter = nullptr;    // Gram last-block ticket
   float* T = nullptr;        // W x W  (orth transforms, scratch)
   float* VW = nullptr;       // W x W  (first r columns: truncation)
 };
@@ -52,11 +54,10 @@ struct lrqmm_handle_s {
   float* LB = nullptr;  // n x R2
   float* partial = nullptr;
   int64_t partial_elems = 0;
-  double* gpartial = nullptr;
-  int64_t gpartial_elems = 0;
   double* Gcross = nullptr;  // W x W
+  double* gpart_cross = nullptr;
+  int* counter_cross = nullptr;
   float* VWbM = nullptr;     // W x W
-  EigJob* d_jobs = nullptr;  // device job tables
   int* err_flag = nullptr;
   alignas(64) CUtensorMap mapA;
   alignas(64) CUtensorMap mapB;
@@ -65,9 +66,6 @@ struct lrqmm_handle_s {
   // run_host buffers
   float *hA = nullptr, *hB = nullptr, *hOmA = nullptr, *hOmB = nullptr, *hD = nullptr;
 };
-
-// job-table slots (pairs A,B)
-enum { kJobOrth0 = 0, kJobOrth1 = 2, kJobOrth2 = 4, kJobTrunc = 6, kNumJobs = 8 };
 
 #define LQ_CUDA(call)                                                                          \
   do {                                                                                         \
@@ -164,10 +162,10 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   for (auto& s : h->s) {
     cudaFree(s.codes); cudaFree(s.lam); cudaFree(s.row_amax); cudaFree(s.lam_scalar); cudaFree(s.Om);
     cudaFree(s.Y); cudaFree(s.Q0); cudaFree(s.Z); cudaFree(s.Q1); cudaFree(s.Gp); cudaFree(s.G);
-    cudaFree(s.T); cudaFree(s.VW);
+    cudaFree(s.gpart); cudaFree(s.counter); cudaFree(s.T); cudaFree(s.VW);
   }
-  cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->partial); cudaFree(h->gpartial); cudaFree(h->Gcross);
-  cudaFree(h->VWbM); cudaFree(h->d_jobs); cudaFree(h->err_flag);
+  cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->partial); cudaFree(h->Gcross); cudaFree(h->gpart_cross);
+  cudaFree(h->counter_cross); cudaFree(h->VWbM); cudaFree(h->err_flag);
   cudaFree(h->hA); cudaFree(h->hB); cudaFree(h->hOmA); cudaFree(h->hOmB); cudaFree(h->hD);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
@@ -209,37 +207,23 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
     if (h->W > 0) {
       ok = ok && dalloc(&s.Om, K * h->W) && dalloc(&s.Y, s.rows * h->W) && dalloc(&s.Q0, s.rows * h->W) &&
            dalloc(&s.Z, K * h->W) && dalloc(&s.Q1, K * h->W) && dalloc(&s.Gp, s.rows * h->W) &&
-           dalloc(&s.G, (int64_t)h->W * h->W) && dalloc(&s.T, (int64_t)h->W * h->W) &&
-           dalloc(&s.VW, (int64_t)h->W * h->W);
+           dalloc(&s.G, (int64_t)h->W * h->W) && dalloc(&s.gpart, 148LL * h->W * h->W) &&
+           dalloc(&s.counter, 1) && dalloc(&s.T, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W);
     }
   }
   if (h->W > 0) {
     const int64_t maxrows = std::max<int64_t>({cfg->m, cfg->n, K});
     // split-K / split-row partials: <= 2 outputs x ~4 waves of splits, bounded at 64 MiB
     h->partial_elems = std::min<int64_t>((int64_t)16 << 20, 2 * 32 * maxrows * h->W);
-    h->gpartial_elems = 296LL * h->W * h->W;
     ok = ok && dalloc(&h->LA, cfg->m * h->R2) && dalloc(&h->LB, cfg->n * h->R2) &&
-         dalloc(&h->partial, h->partial_elems) && dalloc(&h->gpartial, h->gpartial_elems) &&
-         dalloc(&h->Gcross, (int64_t)h->W * h->W) && dalloc(&h->VWbM, (int64_t)h->W * h->W) &&
-         dalloc(&h->d_jobs, kNumJobs);
+         dalloc(&h->partial, h->partial_elems) && dalloc(&h->Gcross, (int64_t)h->W * h->W) &&
+         dalloc(&h->gpart_cross, 148LL * h->W * h->W) && dalloc(&h->counter_cross, 1) &&
+         dalloc(&h->VWbM, (int64_t)h->W * h->W);
   }
   ok = ok && dalloc(&h->err_flag, 4);
   if (!ok) {
     lrqmm_destroy(h);
     return LRQMM_ERR_ALLOC;
-  }
-  if (h->W > 0) {
-    EigJob jobs[kNumJobs];
-    for (int sd = 0; sd < 2; ++sd) {
-      jobs[kJobOrth0 + sd] = EigJob{h->s[sd].G, h->s[sd].T, kEigOrth, 0};
-      jobs[kJobOrth1 + sd] = EigJob{h->s[sd].G, h->s[sd].T, kEigOrth, 0};
-      jobs[kJobOrth2 + sd] = EigJob{h->s[sd].G, h->s[sd].T, kEigOrth, 0};
-      jobs[kJobTrunc + sd] = EigJob{h->s[sd].G, h->s[sd].VW, kEigTrunc, h->r};
-    }
-    if (cudaMemcpy(h->d_jobs, jobs, sizeof(jobs), cudaMemcpyHostToDevice) != cudaSuccess) {
-      lrqmm_destroy(h);
-      return LRQMM_ERR_CUDA;
-    }
   }
   GemmArgs g{};
   g.A = h->s[0].codes;
@@ -337,18 +321,29 @@ static lrqmm_status_t allreduce_f32(lrqmm_handle_t h, float* buf, size_t n) {
   return LRQMM_OK;
 }
 
-// Q <- orthonormal basis of span(Y) for both sides:  G = Y^T Y (fp64) -> eig -> Q = Y T
-static lrqmm_status_t orth_pair(lrqmm_handle_t h, float* const Y[2], const int64_t n[2], float* const Q[2], int job) {
+// G_s = Y1_s^T Y2_s for both sides (one launch)
+static void gram2(lrqmm_handle_t h, float* const Y1[2], float* const Y2[2], const int64_t n[2]) {
+  GramJobs j{};
+  j.n = 2;
+  for (int sd = 0; sd < 2; ++sd)
+    j.j[sd] = GramJob{Y1[sd], Y2[sd], n[sd], h->s[sd].G, h->s[sd].gpart, h->s[sd].counter};
+  launch_gram_jobs(j, h->W, h->st);
+}
+
+// Q_s <- orthonormal basis of span(Y_s) for both sides: G = Y^T Y (fp64), pivoted
+// Cholesky -> T, Q = Y T.  a_rows_sharded: Y_A's rows live on different ranks (sum G_A).
+static lrqmm_status_t orth_pair(lrqmm_handle_t h, float* const Y[2], const int64_t n[2], float* const Q[2],
+                                bool a_rows_sharded) {
   const int W = h->W;
-  for (int sd = 0; sd < 2; ++sd) {
-    launch_gram(Y[sd], Y[sd], n[sd], W, h->s[sd].G, h->gpartial, h->gpartial_elems, h->st);
-    // A-side row-sharded quantities are summed over ranks (Y rows live on different ranks)
-    if (sd == 0 && n[0] == h->s[0].rows) {
-      lrqmm_status_t e = allreduce_f64(h, h->s[0].G, (size_t)W * W);
-      if (e != LRQMM_OK) return e;
-    }
+  gram2(h, Y, Y, n);
+  if (a_rows_sharded) {
+    lrqmm_status_t e = allreduce_f64(h, h->s[0].G, (size_t)W * W);
+    if (e != LRQMM_OK) return e;
   }
-  launch_eig(h->d_jobs + job, 2, W, h->st);
+  EigJobs ej{};
+  ej.n = 2;
+  for (int sd = 0; sd < 2; ++sd) ej.j[sd] = EigJob{h->s[sd].G, h->s[sd].T, 0};
+  launch_chol_orth(ej, W, h->st);
   for (int sd = 0; sd < 2; ++sd) launch_apply_small(Y[sd], h->s[sd].T, nullptr, nullptr, n[sd], W, W, W, Q[sd], W, 0, h->st);
   return check_launch(h);
 }
@@ -370,62 +365,64 @@ lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const 
                               cudaMemcpyDeviceToDevice, h->st));
   // S1: Y = R Omega   (Algorithm 1 sampling)
   for (int sd = 0; sd < 2; ++sd)
-    launch_proj_rows(view(h, sd), h->s[sd].Om, kFRes, h->s[sd].Y, nullptr, 0, nullptr, W, h->partial,
-                     h->partial_elems, h->st);
+    launch_tc_proj_rows(view(h, sd), h->s[sd].Om, h->s[sd].Y, nullptr, nullptr, W, h->partial, h->partial_elems, h->st);
   const int64_t rows[2] = {h->s[0].rows, h->s[1].rows};
   const int64_t kdim[2] = {K, K};
-  float* Ys[2] = {h->s[0].Y, h->s[1].Y};
-  float* Q0s[2] = {h->s[0].Q0, h->s[1].Q0};
-  float* Zs[2] = {h->s[0].Z, h->s[1].Z};
-  float* Q1s[2] = {h->s[0].Q1, h->s[1].Q1};
   lrqmm_status_t e;
   for (int it = 0; it < h->cfg.power_iters; ++it) {
+    float* Ys[2] = {h->s[0].Y, h->s[1].Y};
+    float* Q0s[2] = {h->s[0].Q0, h->s[1].Q0};
     // O1: Q0 = orth(Y)
-    if ((e = orth_pair(h, Ys, rows, Q0s, kJobOrth0)) != LRQMM_OK) return e;
+    if ((e = orth_pair(h, Ys, rows, Q0s, true)) != LRQMM_OK) return e;
     // S2: Z = R^T Q0  (reduction over rows; A side summed over ranks)
     for (int sd = 0; sd < 2; ++sd)
-      launch_proj_cols(view(h, sd), h->s[sd].Q0, kFRes, h->s[sd].Z, W, h->partial, h->partial_elems, h->st);
+      launch_tc_proj_cols(view(h, sd), h->s[sd].Q0, h->s[sd].Z, W, h->partial, h->partial_elems, h->st);
     if ((e = allreduce_f32(h, h->s[0].Z, (size_t)K * W)) != LRQMM_OK) return e;
-    // O2: Q1 = orth(Z), then one re-orthonormalisation pass (CholQR2-style)
+    // O2: Q1 = orth(Z) and one re-orthonormalisation pass (CholQR2); K rows are replicated on every rank
     {
-      // K rows are replicated on every rank: no allreduce for these Grams
-      const int64_t n2[2] = {K, K};
-      for (int sd = 0; sd < 2; ++sd) launch_gram(Zs[sd], Zs[sd], K, W, h->s[sd].G, h->gpartial, h->gpartial_elems, h->st);
-      launch_eig(h->d_jobs + kJobOrth1, 2, W, h->st);
-      for (int sd = 0; sd < 2; ++sd) launch_apply_small(Zs[sd], h->s[sd].T, nullptr, nullptr, K, W, W, W, Q1s[sd], W, 0, h->st);
-      for (int sd = 0; sd < 2; ++sd) launch_gram(Q1s[sd], Q1s[sd], K, W, h->s[sd].G, h->gpartial, h->gpartial_elems, h->st);
-      launch_eig(h->d_jobs + kJobOrth2, 2, W, h->st);
-      // Z is free now: Q1' = Q1 T2 into Z, then swap roles by copying back
-      for (int sd = 0; sd < 2; ++sd) launch_apply_small(Q1s[sd], h->s[sd].T, nullptr, nullptr, n2[sd], W, W, W, Zs[sd], W, 0, h->st);
-      for (int sd = 0; sd < 2; ++sd)
-        LQ_CUDA(cudaMemcpyAsync(Q1s[sd], Zs[sd], sizeof(float) * K * W, cudaMemcpyDeviceToDevice, h->st));
+      float* Zs[2] = {h->s[0].Z, h->s[1].Z};
+      float* Q1s[2] = {h->s[0].Q1, h->s[1].Q1};
+      if ((e = orth_pair(h, Zs, kdim, Q1s, false)) != LRQMM_OK) return e;
+      if ((e = orth_pair(h, Q1s, kdim, Zs, false)) != LRQMM_OK) return e;
+      for (int sd = 0; sd < 2; ++sd) std::swap(h->s[sd].Z, h->s[sd].Q1);  // refined basis now in Q1
     }
     if (it + 1 < h->cfg.power_iters) {
       for (int sd = 0; sd < 2; ++sd)
-        launch_proj_rows(view(h, sd), Q1s[sd], kFRes, Ys[sd], nullptr, 0, nullptr, W, h->partial, h->partial_elems, h->st);
+        launch_tc_proj_rows(view(h, sd), h->s[sd].Q1, h->s[sd].Y, nullptr, nullptr, W, h->partial, h->partial_elems,
+                            h->st);
     }
   }
-  (void)kdim;
   // S3 + cross: W_X = R_X Q1_X and G'_X = X~ Q1_other in one pass over X
   //   (Algorithm 1 on R^T: B = Q1^T R^T = W^T; RC1/RC2 skinny products)
   for (int sd = 0; sd < 2; ++sd)
-    launch_proj_rows(view(h, sd), Q1s[sd], kFRes, Ys[sd], Q1s[1 - sd], kFDeq, h->s[sd].Gp, W, h->partial,
-                     h->partial_elems, h->st);
+    launch_tc_proj_rows(view(h, sd), h->s[sd].Q1, h->s[sd].Y, h->s[1 - sd].Q1, h->s[sd].Gp, W, h->partial,
+                        h->partial_elems, h->st);
   // T: truncation to rank r via eig(W^T W) (Algorithm 1)
-  for (int sd = 0; sd < 2; ++sd) {
-    launch_gram(Ys[sd], Ys[sd], rows[sd], W, h->s[sd].G, h->gpartial, h->gpartial_elems, h->st);
-    if (sd == 0 && (e = allreduce_f64(h, h->s[0].G, (size_t)W * W)) != LRQMM_OK) return e;
+  {
+    float* Ys[2] = {h->s[0].Y, h->s[1].Y};
+    gram2(h, Ys, Ys, rows);
+    if ((e = allreduce_f64(h, h->s[0].G, (size_t)W * W)) != LRQMM_OK) return e;
+    EigJobs ej{};
+    ej.n = 2;
+    for (int sd = 0; sd < 2; ++sd) ej.j[sd] = EigJob{h->s[sd].G, h->s[sd].VW, h->r};
+    launch_eig_warp(ej, W, h->st);
   }
-  launch_eig(h->d_jobs + kJobTrunc, 2, W, h->st);
   // V_B^T V_A core: Q1_B^T Q1_A (fp64, W x W) -> Mab, VWb Mab
-  launch_gram(Q1s[1], Q1s[0], K, W, h->Gcross, h->gpartial, h->gpartial_elems, h->st);
+  {
+    GramJobs j{};
+    j.n = 1;
+    j.j[0] = GramJob{h->s[1].Q1, h->s[0].Q1, K, h->Gcross, h->gpart_cross, h->counter_cross};
+    launch_gram_jobs(j, W, h->st);
+  }
   launch_cross_small(h->Gcross, h->s[0].VW, h->s[1].VW, W, h->r, h->VWbM, h->st);
   // F: factor assembly (Algorithm 2 lines 361-366 folded into two rank-2r factors)
   const int r = h->r;
-  launch_apply_small(Ys[0], h->s[0].VW, nullptr, nullptr, rows[0], W, W, r, h->LA, h->R2, 0, h->st);        // U_A S_A
+  float* YA = h->s[0].Y;
+  float* YB = h->s[1].Y;
+  launch_apply_small(YA, h->s[0].VW, nullptr, nullptr, rows[0], W, W, r, h->LA, h->R2, 0, h->st);          // U_A S_A
   launch_apply_small(h->s[0].Gp, h->s[1].VW, nullptr, nullptr, rows[0], W, W, r, h->LA, h->R2, r, h->st);   // A~ V_B
-  launch_apply_small(h->s[1].Gp, h->s[0].VW, Ys[1], h->VWbM, rows[1], W, W, r, h->LB, h->R2, 0, h->st);     // B~^T V_A + U_B S_B M
-  launch_apply_small(Ys[1], h->s[1].VW, nullptr, nullptr, rows[1], W, W, r, h->LB, h->R2, r, h->st);        // U_B S_B
+  launch_apply_small(h->s[1].Gp, h->s[0].VW, YB, h->VWbM, rows[1], W, W, r, h->LB, h->R2, 0, h->st);        // B~^T V_A + U_B S_B M
+  launch_apply_small(YB, h->s[1].VW, nullptr, nullptr, rows[1], W, W, r, h->LB, h->R2, r, h->st);           // U_B S_B
   record(h, 5);
   if ((e = check_launch(h)) != LRQMM_OK) return e;
   h->state |= 4;

@@ -1,0 +1,323 @@
+// K4 (fast path) — small dense kernels of the RSVD on W x W (W <= 64) problems.
+//
+//  k_gram      : G = Y1^T Y2 in fp64 over n rows, one launch: per-block partials,
+//                the last block (ticket counter) sums them in a fixed order
+//                (deterministic, no float atomics).  blockIdx.y = job.
+//  k_chol_orth : orthonormalising transform of a sketch (Algorithm 1 needs Q with
+//                "orthogonal columns") by pivoted Cholesky QR:
+//                G[p,p] = L L^T, T[p(a), b] = (L^-T)[a, b]  so  Q = Y T.  Directions whose
+//                pivot falls below 1e-10 x the largest diagonal entry (sigma < 1e-5 sigma_max,
+//                reading #12) are dropped (zero columns of T).  One warp per job.
+//  k_eig_warp  : symmetric Jacobi eigendecomposition for the rank-r truncation
+//                (Algorithm 1, Eq. k-svd), one warp per job,
+//                T = top-r eigenvectors in descending eigenvalue order.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lrqmm {
+
+constexpr int kN = 64;
+
+// ------------------------------------------------------------------- Gram
+__global__ void __launch_bounds__(256) k_gram(GramJobs jobs, int W) {
+  const GramJob jb = jobs.j[blockIdx.y];
+  const int npairs = W * W;
+  __shared__ float s1[32][kN + 1];
+  __shared__ float s2[32][kN + 1];
+  __shared__ int ticket;
+  const int64_t rpb = (jb.n + gridDim.x - 1) / gridDim.x;
+  const int64_t r_begin = (int64_t)blockIdx.x * rpb;
+  const int64_t r_end = (jb.n < r_begin + rpb) ? jb.n : r_begin + rpb;
+  double acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += 32) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * W; e += 256) {
+      const int i = e / W, c = e % W;
+      const bool in = r0 + i < r_end;
+      s1[i][c] = in ? jb.Y1[(r0 + i) * W + c] : 0.f;
+      s2[i][c] = in ? jb.Y2[(r0 + i) * W + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int pr = threadIdx.x + 256 * q;
+      if (pr < npairs) {
+        const int a = pr / W, c = pr % W;
+        double t0 = 0.0, t1 = 0.0;
+#pragma unroll 8
+        for (int i = 0; i < 32; i += 2) {
+          t0 = fma((double)s1[i][a], (double)s2[i][c], t0);
+          t1 = fma((double)s1[i + 1][a], (double)s2[i + 1][c], t1);
+        }
+        acc[q] += t0 + t1;
+      }
+    }
+  }
+  double* part = jb.partial + (int64_t)blockIdx.x * npairs;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int pr = threadIdx.x + 256 * q;
+    if (pr < npairs) part[pr] = acc[q];
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(jb.counter, 1);
+  __syncthreads();
+  if (ticket != (int)gridDim.x - 1) return;
+  __threadfence();
+  for (int pr = threadIdx.x; pr < npairs; pr += 256) {
+    double a = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) a += __ldcg(jb.partial + (int64_t)b * npairs + pr);
+    jb.G[pr] = a;
+  }
+  if (threadIdx.x == 0) *jb.counter = 0;  // re-arm for the next launch (stream ordered)
+}
+
+void launch_gram_jobs(const GramJobs& jobs, int W, cudaStream_t st) {
+  int64_t nmax = 0;
+  for (int i = 0; i < jobs.n; ++i) nmax = jobs.j[i].n > nmax ? jobs.j[i].n : nmax;
+  int64_t nb = (nmax + 127) / 128;
+  if (nb > 148) nb = 148;
+  if (nb < 1) nb = 1;
+  k_gram<<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs, W);
+  ++launch_counter();
+}
+
+// ------------------------------------------------- pivoted Cholesky orth
+__global__ void __launch_bounds__(32) k_chol_orth(EigJobs jobs, int n) {
+  extern __shared__ double dyn[];
+  double (*A)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn);
+  double (*Li)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn + kN * (kN + 1));  // L^-1 (lower)
+  __shared__ int piv[kN];
+  __shared__ int rank_s;
+  const EigJob job = jobs.j[blockIdx.x];
+  const int lane = threadIdx.x;
+  for (int e = lane; e < n * n; e += 32) {
+    const int i = e / n, j = e % n;
+    A[i][j] = 0.5 * (job.G[i * n + j] + job.G[j * n + i]);
+    Li[i][j] = 0.0;
+  }
+  if (lane < n) piv[lane] = lane;
+  if (n > 32 && lane + 32 < n) piv[lane + 32] = lane + 32;
+  __syncwarp();
+  // reference scale: largest diagonal entry
+  double dmax = 0.0;
+  for (int i = lane; i < n; i += 32) dmax = fmax(dmax, A[i][i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  const double thr = 1e-10 * dmax;
+  int k = 0;
+  for (; k < n; ++k) {
+    // pivot: largest remaining diagonal (ties -> lowest index)
+    double best = -1.0;
+    int bi = k;
+    for (int i = k + lane; i < n; i += 32) {
+      const double d = A[i][i];
+      if (d > best) { best = d; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (!(dmax > 0.0) || best < thr || best <= 0.0) break;
+    // symmetric swap of row/col k and bi
+    if (bi != k) {
+      for (int j = lane; j < n; j += 32) {
+        const double t = A[k][j]; A[k][j] = A[bi][j]; A[bi][j] = t;
+      }
+      __syncwarp();
+      for (int i = lane; i < n; i += 32) {
+        const double t = A[i][k]; A[i][k] = A[i][bi]; A[i][bi] = t;
+      }
+      if (lane == 0) { const int t = piv[k]; piv[k] = piv[bi]; piv[bi] = t; }
+      __syncwarp();
+    }
+    const double lkk = sqrt(A[k][k]);
+    const double inv = 1.0 / lkk;
+    __syncwarp();
+    // column k of L below the diagonal
+    for (int i = k + 1 + lane; i < n; i += 32) A[i][k] *= inv;
+    if (lane == 0) A[k][k] = lkk;
+    __syncwarp();
+    // trailing update A[i][j] -= L[i][k] L[j][k]  (full symmetric block: later swaps read both triangles)
+    const int m = n - k - 1;
+    for (int e = lane; e < m * m; e += 32) {
+      const int i = k + 1 + e / m, j = k + 1 + e % m;
+      A[i][j] -= A[i][k] * A[j][k];
+    }
+    __syncwarp();
+  }
+  if (lane == 0) rank_s = k;
+  __syncwarp();
+  const int rk = rank_s;
+  // Li = L^-1 (rk x rk lower triangular), column by column (lane = column)
+  for (int c = lane; c < rk; c += 32) {
+    for (int i = c; i < rk; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int t = c; t < i; ++t) s -= A[i][t] * Li[t][c];
+      Li[i][c] = s / A[i][i];
+    }
+  }
+  __syncwarp();
+  // T[piv[a]][b] = (L^-T)[a][b] = Li[b][a] for a, b < rk; zero elsewhere
+  for (int e = lane; e < n * n; e += 32) {
+    const int rr = e / n, b = e % n;  // T row rr (original index), column b
+    job.T[rr * n + b] = 0.f;
+  }
+  __syncwarp();
+  for (int e = lane; e < rk * rk; e += 32) {
+    const int a = e / rk, b = e % rk;
+    if (b >= a) job.T[piv[a] * n + b] = (float)Li[b][a];
+  }
+}
+
+static const int kDynSmem = 2 * kN * (kN + 1) * (int)sizeof(double);
+
+void launch_chol_orth(const EigJobs& jobs, int n, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_chol_orth, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+    attr = true;
+  }
+  k_chol_orth<<<jobs.n, 32, kDynSmem, st>>>(jobs, n);
+  ++launch_counter();
+}
+
+// ------------------------------------------------ one-warp Jacobi (truncation)
+__global__ void __launch_bounds__(32) k_eig_warp(EigJobs jobs, int n) {
+  extern __shared__ double dyn[];
+  double (*A)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn);
+  double (*V)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn + kN * (kN + 1));
+  __shared__ double cs[kN / 2], sn[kN / 2];
+  __shared__ int pp[kN / 2], qq[kN / 2];
+  __shared__ int order[kN];
+  const EigJob job = jobs.j[blockIdx.x];
+  const int lane = threadIdx.x;
+  for (int e = lane; e < n * n; e += 32) {
+    const int i = e / n, j = e % n;
+    A[i][j] = 0.5 * (job.G[i * n + j] + job.G[j * n + i]);
+    V[i][j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncwarp();
+  const int half = n / 2;
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    double off = 0.0, dg = 0.0;
+    for (int e = lane; e < n * n; e += 32) {
+      const int i = e / n, j = e % n;
+      const double v = A[i][j] * A[i][j];
+      if (i == j) dg += v; else off += v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      off += __shfl_xor_sync(0xffffffffu, off, o);
+      dg += __shfl_xor_sync(0xffffffffu, dg, o);
+    }
+    if (off <= 1e-30 * dg || off == 0.0) break;
+    for (int step = 0; step < n - 1; ++step) {
+      for (int k = lane; k < half; k += 32) {
+        int p, q;
+        if (k == 0) { p = 0; q = (step % (n - 1)) + 1; }
+        else { p = ((k + step) % (n - 1)) + 1; q = ((n - 1 - k + step) % (n - 1)) + 1; }
+        if (p > q) { const int t = p; p = q; q = t; }
+        const double apq = A[p][q];
+        double c = 1.0, s = 0.0;
+        if (apq != 0.0) {
+          const double theta = (A[q][q] - A[p][p]) / (2.0 * apq);
+          double t;
+          if (fabs(theta) > 1e150) t = 0.5 / theta;
+          else t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+          c = rsqrt(t * t + 1.0);
+          s = t * c;
+        }
+        pp[k] = p; qq[k] = q; cs[k] = c; sn[k] = s;
+      }
+      __syncwarp();
+      for (int e = lane; e < half * n; e += 32) {
+        const int k = e / n, j = e % n;
+        const int p = pp[k], q = qq[k];
+        const double c = cs[k], s = sn[k];
+        const double ap = A[p][j], aq = A[q][j];
+        A[p][j] = c * ap - s * aq;
+        A[q][j] = s * ap + c * aq;
+      }
+      __syncwarp();
+      for (int e = lane; e < half * n; e += 32) {
+        const int k = e / n, i = e % n;
+        const int p = pp[k], q = qq[k];
+        const double c = cs[k], s = sn[k];
+        const double ap = A[i][p], aq = A[i][q];
+        A[i][p] = c * ap - s * aq;
+        A[i][q] = s * ap + c * aq;
+        const double vp = V[i][p], vq = V[i][q];
+        V[i][p] = c * vp - s * vq;
+        V[i][q] = s * vp + c * vq;
+      }
+      __syncwarp();
+    }
+  }
+  for (int t = lane; t < n; t += 32) {
+    int rank = 0;
+    const double li = A[t][t];
+    for (int j = 0; j < n; ++j) {
+      const double lj = A[j][j];
+      rank += (lj > li) || (lj == li && j < t);
+    }
+    order[rank] = t;
+  }
+  __syncwarp();
+  for (int e = lane; e < n * n; e += 32) {
+    const int a = e / n, o = e % n;
+    job.T[a * n + o] = (o < job.r) ? (float)V[a][order[o]] : 0.f;
+  }
+}
+
+void launch_eig_warp(const EigJobs& jobs, int n, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_eig_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+    attr = true;
+  }
+  k_eig_warp<<<jobs.n, 32, kDynSmem, st>>>(jobs, n);
+  ++launch_counter();
+}
+
+// Mab = VWb^T C VWa (r x r), C = Q1_B^T Q1_A (n x n, fp64); VWbM = VWb Mab (n x r).
+// V_B^T V_A = VWb^T Q1_B^T Q1_A VWa: the r x r core of RC3 (Alg. 2).
+__global__ void __launch_bounds__(256) k_cross_small(const double* __restrict__ C, const float* __restrict__ VWa,
+                                                     const float* __restrict__ VWb, int n, int r,
+                                                     float* __restrict__ VWbM) {
+  __shared__ double T1[kN][kN / 2];      // C VWa  (n x r), r <= 32
+  __shared__ double M[kN / 2][kN / 2];   // r x r
+  const int tid = threadIdx.x;
+  for (int e = tid; e < n * r; e += 256) {
+    const int i = e / r, o = e % r;
+    double a = 0.0;
+    for (int c = 0; c < n; ++c) a += C[i * n + c] * (double)VWa[c * n + o];
+    T1[i][o] = a;
+  }
+  __syncthreads();
+  for (int e = tid; e < r * r; e += 256) {
+    const int u = e / r, o = e % r;
+    double a = 0.0;
+    for (int i = 0; i < n; ++i) a += (double)VWb[i * n + u] * T1[i][o];
+    M[u][o] = a;
+  }
+  __syncthreads();
+  for (int e = tid; e < n * r; e += 256) {
+    const int i = e / r, o = e % r;
+    double a = 0.0;
+    for (int u = 0; u < r; ++u) a += (double)VWb[i * n + u] * M[u][o];
+    VWbM[i * n + o] = (float)a;
+  }
+}
+
+void launch_cross_small(const double* C, const float* VWa, const float* VWb, int n, int r, float* VWbM,
+                        cudaStream_t st) {
+  k_cross_small<<<1, 256, 0, st>>>(C, VWa, VWb, n, r, VWbM); ++launch_counter();
+}
+
+}  // namespace lrqmm
