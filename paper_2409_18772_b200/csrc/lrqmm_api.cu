@@ -581,3 +581,45 @@ int64_t lrqmm_launch_count(lrqmm_handle_t h, int reset) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------- test hooks
+#include "../../include/lrqmm_debug.h"
+
+extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx, int64_t rows, int K,
+                                           const float* lam, int bits, int rounding, const float* P, const float* P2,
+                                           int W, float* OUT, float* OUT2, void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  SideView v{X, ldx, rows, K, lam, (1 << (bits - 1)) - 1, rounding};
+  const int64_t pe = (int64_t)16 << 20;
+  float* partial = nullptr;
+  if (cudaMalloc(&partial, sizeof(float) * pe) != cudaSuccess) return LRQMM_ERR_ALLOC;
+  if (mode == 0) launch_tc_proj_rows(v, P, OUT, nullptr, nullptr, W, partial, pe, st);
+  else if (mode == 1) launch_tc_proj_cols(v, P, OUT, W, partial, pe, st);
+  else launch_tc_proj_rows(v, P, OUT, P2, OUT2, W, partial, pe, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(partial);
+  return e == cudaSuccess ? LRQMM_OK : LRQMM_ERR_CUDA;
+}
+
+extern "C" lrqmm_status_t lrqmm_debug_small(int op, const float* Y, int64_t n, int W, int r, double* G, float* T,
+                                            void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  double* part = nullptr;
+  int* counter = nullptr;
+  if (cudaMalloc(&part, sizeof(double) * 148 * W * W) != cudaSuccess) return LRQMM_ERR_ALLOC;
+  if (cudaMalloc(&counter, sizeof(int)) != cudaSuccess) return LRQMM_ERR_ALLOC;
+  cudaMemsetAsync(counter, 0, sizeof(int), st);
+  GramJobs gj{};
+  gj.n = 1;
+  gj.j[0] = GramJob{Y, Y, n, G, part, counter};
+  launch_gram_jobs(gj, W, st);
+  EigJobs ej{};
+  ej.n = 1;
+  ej.j[0] = EigJob{G, T, r};
+  if (op == 1) launch_chol_orth(ej, W, st);
+  if (op == 2) launch_eig_warp(ej, W, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(part);
+  cudaFree(counter);
+  return e == cudaSuccess ? LRQMM_OK : LRQMM_ERR_CUDA;
+}

@@ -70,13 +70,16 @@ LRQMM_DEV float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0
 
 // UMMA smem descriptors (SW128).  K-major: SBO = 1024 B between 8-row groups.
 // MN-major: LBO = byte distance between 32-element MN atoms, SBO = between 8-deep K groups.
-LRQMM_DEV uint64_t desc_sw128(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+// tf32 operands: K-major uses SWIZZLE_128B (type 2); MN-major must use
+// SWIZZLE_128B_BASE32B (type 1: 32 MN x 4 K atoms of 512 B, 32-byte chunks XOR row),
+// the only MN-major layout the tensor core accepts for 32-bit operands (probed on B200).
+LRQMM_DEV uint64_t desc_sw128(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t type) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1u << 46;
-  d |= (uint64_t)2u << 61;
+  d |= (uint64_t)type << 61;
   return d;
 }
 // kind::tf32, D f32, M = 128, N = n; a_mn / b_mn: operand is MN-major
@@ -93,11 +96,12 @@ LRQMM_DEV void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32
 }
 LRQMM_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// byte offset of element (mn, k) in an MN-major SW128 tile with nA 32-wide MN atoms
+// byte offset of element (mn, k) in an MN-major SW128_BASE32B tile with nA 32-wide MN atoms
+// (LBO = 512 B between MN atoms, SBO = nA * 512 B between 4-deep K groups)
 LRQMM_DEV uint32_t off_mn(int mn, int k, int nA) {
-  const int row = k & 7;
-  const int chunk = (mn & 31) >> 2;
-  return (uint32_t)((k >> 3) * (nA * 1024) + (mn >> 5) * 1024 + row * 128 + ((chunk ^ row) << 4) + ((mn & 3) << 2));
+  const int row = k & 3;
+  return (uint32_t)((k >> 2) * (nA * 512) + (mn >> 5) * 512 + row * 128 + ((((mn & 31) >> 3) ^ row) << 5) +
+                    ((mn & 7) << 2));
 }
 // byte offset of element (mn, k) in a K-major SW128 tile (rows of 32 fp32)
 LRQMM_DEV uint32_t off_k(int mn, int k) {
@@ -302,8 +306,9 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(TcArgs a) {
       }
       tc_fence_before();
     }
-  } else if (lane == 0) {
+  } else {
     // ------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
     constexpr uint32_t idesc1 = idesc_tf32(WN, kMode == 1 ? 1u : 0u, 1u);
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % STAGES;
@@ -315,22 +320,22 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(TcArgs a) {
       const uint32_t bLo = bHi + kBTile, b2Hi = bLo + kBTile, b2Lo = b2Hi + kBTile;
 #pragma unroll
       for (int k = 0; k < BK / 8; ++k) {
-        uint32_t aoff, lboA, sboA;
-        if (kMode == 0) { aoff = k * 32; lboA = 16; sboA = 1024; }      // K-major: +32 B per 8 k
-        else { aoff = k * 4096; lboA = 1024; sboA = 4096; }             // MN-major: next 8-deep k group
+        uint32_t aoff, lboA, sboA, tA;
+        if (kMode == 0) { aoff = k * 32; lboA = 16; sboA = 1024; tA = 2; }        // K-major: +32 B per 8 k
+        else { aoff = k * 4096; lboA = 512; sboA = 2048; tA = 1; }                // MN-major: next two 4-deep groups
         const uint32_t boff = k * (NA * 1024);
-        const uint64_t dAhi = desc_sw128(aHi + aoff, lboA, sboA);
-        const uint64_t dAlo = desc_sw128(aLo + aoff, lboA, sboA);
-        const uint64_t dBhi = desc_sw128(bHi + boff, 1024, NA * 1024);
-        const uint64_t dBlo = desc_sw128(bLo + boff, 1024, NA * 1024);
+        const uint64_t dAhi = desc_sw128(aHi + aoff, lboA, sboA, tA);
+        const uint64_t dAlo = desc_sw128(aLo + aoff, lboA, sboA, tA);
+        const uint64_t dBhi = desc_sw128(bHi + boff, 512, NA * 512, 1);
+        const uint64_t dBlo = desc_sw128(bLo + boff, 512, NA * 512, 1);
         const uint32_t acc0 = (kb | k) != 0 ? 1u : 0u;
         umma_tf32(tmem, dAhi, dBhi, idesc1, acc0);
         umma_tf32(tmem, dAhi, dBlo, idesc1, 1u);
         umma_tf32(tmem, dAlo, dBhi, idesc1, 1u);
         if (kDual) {
-          const uint64_t dAc = desc_sw128(aC + aoff, lboA, sboA);
-          const uint64_t dB2hi = desc_sw128(b2Hi + boff, 1024, NA * 1024);
-          const uint64_t dB2lo = desc_sw128(b2Lo + boff, 1024, NA * 1024);
+          const uint64_t dAc = desc_sw128(aC + aoff, lboA, sboA, tA);
+          const uint64_t dB2hi = desc_sw128(b2Hi + boff, 512, NA * 512, 1);
+          const uint64_t dB2lo = desc_sw128(b2Lo + boff, 512, NA * 512, 1);
           umma_tf32(tmem + WN, dAc, dB2hi, idesc1, acc0);
           umma_tf32(tmem + WN, dAc, dB2lo, idesc1, 1u);
         }
@@ -338,6 +343,8 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(TcArgs a) {
       umma_commit(&empty[s]);
     }
     umma_commit(done);
+    }
+    __syncwarp();  // reconverge before the CTA barrier (bar.sync is .aligned)
   }
   __syncthreads();
   if (warp == 8) {

@@ -32,6 +32,7 @@ EXPORTS = (
     "lrqmm_gemm_int32", "lrqmm_get_factors", "lrqmm_get_correction", "lrqmm_correction_width",
     "lrqmm_get_timings", "lrqmm_launch_count", "lrqmm_status_string",
 )
+DEBUG_EXPORTS = ("lrqmm_debug_proj", "lrqmm_debug_small")
 
 
 class LrqmmError(RuntimeError):
@@ -81,6 +82,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lrqmm_get_timings": (I, [P, ctypes.POINTER(ctypes.c_double)]),
         "lrqmm_launch_count": (I64, [P, I]),
         "lrqmm_status_string": (ctypes.c_char_p, [I]),
+        # test hooks (include/lrqmm_debug.h)
+        "lrqmm_debug_proj": (I, [I, P, I64, I64, I, P, I, I, P, P, I, P, P, P]),
+        "lrqmm_debug_small": (I, [I, P, I64, I, I, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -11,8 +11,8 @@ from paper_2409_18772_b200 import lrqmm as L
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def header_symbols():
-    txt = open(os.path.join(ROOT, "include", "lrqmm.h")).read()
+def header_symbols(name="lrqmm.h"):
+    txt = open(os.path.join(ROOT, "include", name)).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
     return sorted(set(re.findall(r"\b(lrqmm_[a-z0-9_]+)\s*\(", txt)))
 
@@ -31,6 +31,10 @@ def test_library_exports_every_header_symbol(lib):
     for s in syms:
         assert hasattr(lib, s), s
     assert sorted(L.EXPORTS) == syms
+    dbg = header_symbols("lrqmm_debug.h")
+    assert sorted(L.DEBUG_EXPORTS) == dbg
+    for s in dbg:
+        assert hasattr(lib, s), s
 
 
 def test_status_strings(lib):
