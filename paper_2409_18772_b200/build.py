@@ -49,7 +49,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     nccl = _nccl_dir()
     inc = ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include")]
-    flags = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
+    extra = os.environ.get("LRQMM_EXTRA_NVCC", "").split()
+    flags = extra + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
              "--expt-relaxed-constexpr"] + ARCH + inc
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", f) for f in ("lrqmm.h", "lrqmm_debug.h")]
     objs = []

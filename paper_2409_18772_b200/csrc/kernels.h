@@ -102,6 +102,9 @@ struct GemmArgs {
   int64_t ldd;
 };
 int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB);  // returns 0 on success
+// 2D TMA map (no swizzle), dims {inner, outer} elements of fp32 (dtype_f32=1) or u8; returns 0 on success
+int encode_map_2d(void* map, int dtype_f32, const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
+                  uint32_t box_inner, uint32_t box_outer);
 void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStream_t st);
 
 }  // namespace lrqmm

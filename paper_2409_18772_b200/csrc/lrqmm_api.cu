@@ -22,8 +22,9 @@ constexpr int kMaxWidth = 64;
 
 struct Side {
   int64_t rows = 0;
-  const float* X = nullptr;  // caller's fp32 operand (retained, not copied)
+  const float* X = nullptr;  // caller's fp32 operand (retained, not copied) or the aligned stage
   int64_t ldx = 0;
+  float* stage = nullptr;    // aligned copy, only for layouts TMA cannot address
   int8_t* codes = nullptr;   // rows x Kp
   float* lam = nullptr;      // rows
   float* row_amax = nullptr; // rows (per-tensor mode)
@@ -162,7 +163,7 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   for (auto& s : h->s) {
     cudaFree(s.codes); cudaFree(s.lam); cudaFree(s.row_amax); cudaFree(s.lam_scalar); cudaFree(s.Om);
     cudaFree(s.Y); cudaFree(s.Q0); cudaFree(s.Z); cudaFree(s.Q1); cudaFree(s.Gp); cudaFree(s.G);
-    cudaFree(s.gpart); cudaFree(s.counter); cudaFree(s.T); cudaFree(s.VW);
+    cudaFree(s.gpart); cudaFree(s.counter); cudaFree(s.T); cudaFree(s.VW); cudaFree(s.stage);
   }
   cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->partial); cudaFree(h->Gcross); cudaFree(h->gpart_cross);
   cudaFree(h->counter_cross); cudaFree(h->VWbM); cudaFree(h->err_flag);
@@ -273,12 +274,21 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
   s.X = X;
   s.ldx = ldx;
   record(h, side == LRQMM_SIDE_A ? 0 : 2);
+  // the RSVD passes stream X with TMA: 16-byte aligned base and row stride required
+  if (h->W > 0 && s.rows > 0 && h->cfg.k > 0 && ((reinterpret_cast<uintptr_t>(X) & 15) != 0 || (ldx % 4) != 0)) {
+    const int64_t lds = (h->cfg.k + 3) / 4 * 4;
+    if (!s.stage && !dalloc(&s.stage, s.rows * lds)) return fail(h, LRQMM_ERR_ALLOC);
+    LQ_CUDA(cudaMemcpy2DAsync(s.stage, sizeof(float) * lds, X, sizeof(float) * ldx, sizeof(float) * h->cfg.k, s.rows,
+                              cudaMemcpyDeviceToDevice, h->st));
+    s.X = s.stage;
+    s.ldx = lds;
+  }
   if (h->cfg.granularity == LRQMM_SCALE_PER_TENSOR) {
     launch_tensor_scale(X, ldx, s.rows, (int)h->cfg.k, h->qmax, s.row_amax, s.lam, s.lam_scalar, h->err_flag, h->st);
   }
   QuantArgs a;
-  a.X = X;
-  a.ldx = ldx;
+  a.X = s.X;
+  a.ldx = s.ldx;
   a.rows = s.rows;
   a.K = (int)h->cfg.k;
   a.Kp = h->Kp;
@@ -589,6 +599,15 @@ extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx
                                            const float* lam, int bits, int rounding, const float* P, const float* P2,
                                            int W, float* OUT, float* OUT2, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  float* stage = nullptr;
+  if ((reinterpret_cast<uintptr_t>(X) & 15) != 0 || (ldx % 4) != 0) {
+    const int64_t lds = ((int64_t)K + 3) / 4 * 4;
+    if (cudaMalloc(&stage, sizeof(float) * rows * lds) != cudaSuccess) return LRQMM_ERR_ALLOC;
+    cudaMemcpy2DAsync(stage, sizeof(float) * lds, X, sizeof(float) * ldx, sizeof(float) * K, rows,
+                      cudaMemcpyDeviceToDevice, st);
+    X = stage;
+    ldx = lds;
+  }
   SideView v{X, ldx, rows, K, lam, (1 << (bits - 1)) - 1, rounding};
   const int64_t pe = (int64_t)16 << 20;
   float* partial = nullptr;
@@ -597,7 +616,9 @@ extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx
   else if (mode == 1) launch_tc_proj_cols(v, P, OUT, W, partial, pe, st);
   else launch_tc_proj_rows(v, P, OUT, P2, OUT2, W, partial, pe, st);
   cudaError_t e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = cudaGetLastError();
   cudaFree(partial);
+  if (stage) cudaFree(stage);
   return e == cudaSuccess ? LRQMM_OK : LRQMM_ERR_CUDA;
 }
 

@@ -2,31 +2,55 @@
 // residual (Algorithm 1 sampling / power iteration / projection, PAPER.md:124-140,
 // reading #11) and the cross products of Algorithm 2, computed as
 // tcgen05.mma kind::tf32 with a 3-term split (x = hi + lo, hi = tf32(x)):
-//     F(X) P ~= F_hi P_hi + F_hi P_lo + F_lo P_hi          (fp32-grade, E5 in SURVEY)
-// The operand F(X) (residual R or quantization codes) is recomputed from the fp32
-// side X and lambda by the producer warps, written to shared memory in the
-// canonical UMMA layouts, and consumed by one MMA thread; X is read from HBM once
-// per pass (the roofline of these passes), the FP32 pipes only do the O(1) per
-// element split.
+//     F(X) P ~= F_hi P_hi + F_hi P_lo + F_lo P_hi          (fp32-grade)
+// The operand F(X) (residual R, or the quantization codes) is recomputed from the
+// fp32 side X and lambda: X is read from HBM exactly once per pass, which is this
+// kernel's roofline (bytes per element = 4).
 //
 //   ROW mode  OUT1[i,:] = sum_j R[i,j] P1[j,:]          (S1: Y = R Omega, S3: W = R Q1)
 //             OUT2[i,:] = (1/lambda_i) sum_j C[i,j] P2[j,:]   (dual: A~ Q1_other, codes exact in tf32)
-//             A operand = F(X) tile, K-major (X's natural layout), B = P tile, MN-major.
+//             A operand = F(X) tile, K-major SW128; B = P tile, MN-major SW128_BASE32B.
 //   COL mode  OUT[j,:]  = sum_i R[i,j] P[i,:]            (S2: Z = R^T Q0)
-//             A operand = R tile, MN-major (X's natural layout again), B = P tile, MN-major.
-// Split-K partials are reduced in a fixed order by k_reduce_splits (deterministic).
+//             A operand = R tile, MN-major SW128_BASE32B (X's natural layout); B as above.
+//
+// Persistent, warp-specialised (448 threads, one CTA per SM):
+//   warp 13    : TMA issuer, streams raw X tiles (16 KB) through a 3-4 deep smem ring
+//   warps 0-7  : producers: raw X -> F(X) -> hi/lo split -> UMMA operand tiles (2 stages)
+//   warp 12    : TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 8-11 : epilogue: TMEM (double-buffered accumulators) -> split-K partials
+// Work unit = (128-row/col block, reduction split); partials are summed in a fixed
+// order by k_reduce_splits_tc (deterministic, no float atomics).
+#include <cuda.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace lrqmm {
 
 namespace tcp {
-constexpr int kProdThreads = 256;
-constexpr int kThreads = kProdThreads + 32;  // + one MMA warp
-constexpr int BM = 128;                      // output rows (ROW) / output cols (COL) per CTA
-constexpr int BK = 32;                       // reduction elements per stage (128 B of fp32)
-constexpr int STAGES = 2;
-constexpr int kATile = BM * BK * 4;          // 16 KB
+constexpr int kProd = 256;
+constexpr int kThreads = 448;
+constexpr int kMmaWarp = 12;
+constexpr int kTmaWarp = 13;
+constexpr int BM = 128;  // output rows (ROW) / output cols (COL) per unit
+constexpr int BK = 32;   // reduction elements per k-block
+#ifndef LRQMM_OPST
+#define LRQMM_OPST 2
+#endif
+constexpr int OPST = LRQMM_OPST;  // operand stages
+constexpr int kATile = BM * BK * 4;    // 16 KB
+constexpr int kRawTile = BM * BK * 4;  // 16 KB
+template <int NA, bool kDual>
+struct Cfg {
+  static constexpr int WN = 32 * NA;
+  static constexpr int kBTile = BK * WN * 4;
+  static constexpr int kStage = (kDual ? 3 : 2) * kATile + (kDual ? 4 : 2) * kBTile;
+  static constexpr int kRawSt = (4 * kRawTile + OPST * kStage <= 200 * 1024) ? 4 : 3;
+  static constexpr int kSmem = kRawSt * kRawTile + OPST * kStage + 256 + 1024;
+  static constexpr int kAccCols = (kDual ? 2 : 1) * WN;  // per accumulator buffer
+  static constexpr uint32_t kTmemCols =
+      2 * kAccCols <= 32 ? 32 : (2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : 256));
+};
 }  // namespace tcp
 
 struct TcArgs {
@@ -43,6 +67,7 @@ struct TcArgs {
   float* out2;
   int64_t nout;   // rows (ROW) or K (COL)
   int64_t chunk;  // reduction elements per split (multiple of BK)
+  int nblk, nsplit;
 };
 
 LRQMM_DEV float codef(float lam, float x, int mode, int qmax) {
@@ -68,8 +93,6 @@ LRQMM_DEV float codef(float lam, float x, int mode, int qmax) {
 }
 LRQMM_DEV float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
-// UMMA smem descriptors (SW128).  K-major: SBO = 1024 B between 8-row groups.
-// MN-major: LBO = byte distance between 32-element MN atoms, SBO = between 8-deep K groups.
 // tf32 operands: K-major uses SWIZZLE_128B (type 2); MN-major must use
 // SWIZZLE_128B_BASE32B (type 1: 32 MN x 4 K atoms of 512 B, 32-byte chunks XOR row),
 // the only MN-major layout the tensor core accepts for 32-bit operands (probed on B200).
@@ -111,180 +134,271 @@ LRQMM_DEV uint32_t off_k(int mn, int k) {
 }
 
 template <int kMode, int NA, bool kDual>
-__global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(TcArgs a) {
+__global__ void __launch_bounds__(tcp::kThreads, 1)
+    k_tc_proj(const __grid_constant__ CUtensorMap xmap, TcArgs a) {
   using namespace tcp;
-  constexpr int WN = 32 * NA;                 // MMA N
-  constexpr int kBTile = BK * WN * 4;         // 4 or 8 KB
-  constexpr int kStage = (kDual ? 3 : 2) * kATile + (kDual ? 4 : 2) * kBTile;
-  constexpr uint32_t kTmemCols = (kDual ? 2 : 1) * WN <= 32 ? 32 : ((kDual ? 2 : 1) * WN <= 64 ? 64 : 128);
+  using C = Cfg<NA, kDual>;
+  constexpr int WN = C::WN;
+  constexpr int kBTile = C::kBTile;
+  constexpr int kStage = C::kStage;
+  constexpr int RST = C::kRawSt;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * kStage);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + STAGES;
-  uint64_t* done = bars + 2 * STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+  uint8_t* sRaw = smem;                 // RST x 16 KB raw X tiles
+  uint8_t* sOp = smem + RST * kRawTile;  // OPST x kStage operand tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOp + OPST * kStage);
+  uint64_t* rfull = bars;            // RST
+  uint64_t* rempty = bars + RST;     // RST
+  uint64_t* ofull = bars + 2 * RST;  // OPST
+  uint64_t* oempty = ofull + OPST;   // OPST
+  uint64_t* tfull = oempty + OPST;   // 2
+  uint64_t* tempty = tfull + 2;      // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t o0 = (int64_t)blockIdx.x * BM;  // first output row (ROW) / col (COL)
-  const int64_t r_begin = (int64_t)blockIdx.y * a.chunk;
   const int64_t r_len = kMode == 0 ? (int64_t)a.K : a.rows;
-  const int64_t r_end = r_begin + a.chunk < r_len ? r_begin + a.chunk : r_len;
-  const int nkb = (int)((r_end - r_begin + BK - 1) / BK);
-  const bool vec = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
+  const int nunits = a.nblk * a.nsplit;
 
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], kProdThreads);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < RST; ++s) {
+      mbar_init(&rfull[s], 1);
+      mbar_init(&rempty[s], kProd);
     }
-    mbar_init(done, 1);
+    for (int s = 0; s < OPST; ++s) {
+      mbar_init(&ofull[s], kProd);
+      mbar_init(&oempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 128);
+    }
     fence_mbar_init();
   }
-  if (warp == 8) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 8) {
-    // ------------------------------------------------------------- producers
-    // per thread: 4 float4 of X per stage
-    float lam_r[4], inv_r[4];
-    if (kMode == 0) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t row = o0 + ((tid + 256 * u) >> 3);
-        lam_r[u] = row < a.rows ? a.lam[row] : 1.f;
-        inv_r[u] = __frcp_rn(lam_r[u]);
+  auto unit_range = [&](int u, int& blk, int& split, int64_t& r0, int& nkb) {
+    blk = u % a.nblk;
+    split = u / a.nblk;
+    r0 = (int64_t)split * a.chunk;
+    const int64_t r1 = r0 + a.chunk < r_len ? r0 + a.chunk : r_len;
+    nkb = (int)((r1 - r0 + BK - 1) / BK);
+  };
+
+  if (warp == kTmaWarp) {
+    // --------------------------------------------------------- TMA: raw X tiles
+    if (lane == 0) {
+      tma_prefetch_desc(&xmap);
+      int it = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        int blk, split, nkb;
+        int64_t r0;
+        unit_range(u, blk, split, r0, nkb);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % RST;
+          mbar_wait(&rempty[s], ((it / RST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&rfull[s], kRawTile);
+          const int k0 = (int)(r0 + (int64_t)kb * BK);
+          if (kMode == 0) tma_load_2d(sRaw + s * kRawTile, &xmap, &rfull[s], k0, blk * BM);
+          else tma_load_2d(sRaw + s * kRawTile, &xmap, &rfull[s], blk * BM, k0);
+        }
       }
     }
-    auto load = [&](int kb, float4 (&v)[4]) {
-      const int64_t k0 = r_begin + (int64_t)kb * BK;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int f = tid + 256 * u;
-        int64_t row, col;
-        if (kMode == 0) {
-          row = o0 + (f >> 3);
-          col = k0 + (f & 7) * 4;
-        } else {
-          row = k0 + (f >> 5);
-          col = o0 + (f & 31) * 4;
-        }
-        const int64_t rmax = kMode == 0 ? a.rows : r_end;
-        const int64_t cmax = kMode == 0 ? r_end : (int64_t)a.K;
-        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (row < rmax) {
-          const float* xr = a.X + row * a.ldx;
-          if (vec && col + 3 < cmax) {
-            t = __ldcs(reinterpret_cast<const float4*>(xr + col));
-          } else {
-            if (col + 0 < cmax) t.x = xr[col + 0];
-            if (col + 1 < cmax) t.y = xr[col + 1];
-            if (col + 2 < cmax) t.z = xr[col + 2];
-            if (col + 3 < cmax) t.w = xr[col + 3];
-          }
-        }
-        v[u] = t;
-      }
-    };
-    float4 cur[4];
-    if (nkb > 0) load(0, cur);
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (uint32_t)((kb / STAGES) & 1);
-      float4 nxt[4];
-      if (kb + 1 < nkb) load(kb + 1, nxt);
-      const int64_t k0 = r_begin + (int64_t)kb * BK;
-      float lam_c[4], inv_c[4];
-      if (kMode == 1) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int64_t row = k0 + ((tid + 256 * u) >> 5);
-          lam_c[u] = row < r_end ? a.lam[row] : 1.f;
-          inv_c[u] = __frcp_rn(lam_c[u]);
-        }
-      }
-      // B tile(s): P rows [k0, k0+BK) x WN (zero beyond W / range), MN-major
-      float4 pb1 = make_float4(0.f, 0.f, 0.f, 0.f), pb2 = pb1;
-      int pj = 0, pc = 0;
-      constexpr int kPB4 = BK * WN / 4;  // float4 per B tile
-      mbar_wait(&empty[s], ph ^ 1);
-      uint8_t* st = smem + s * kStage;
-      uint8_t* sAhi = st;
-      uint8_t* sAlo = st + kATile;
-      uint8_t* sAc = st + 2 * kATile;
-      uint8_t* sBhi = st + (kDual ? 3 : 2) * kATile;
-      uint8_t* sBlo = sBhi + kBTile;
-      uint8_t* sB2hi = sBlo + kBTile;
-      uint8_t* sB2lo = sB2hi + kBTile;
-      for (int e = tid; e < kPB4; e += kProdThreads) {
-        pj = e / (WN / 4);
-        pc = (e % (WN / 4)) * 4;
-        const int64_t k = k0 + pj;
-        pb1 = make_float4(0.f, 0.f, 0.f, 0.f);
-        pb2 = pb1;
-        if (k < r_end) {
-          const float* p1 = a.P1 + k * a.W;
-          if (pc + 0 < a.W) pb1.x = p1[pc + 0];
-          if (pc + 1 < a.W) pb1.y = p1[pc + 1];
-          if (pc + 2 < a.W) pb1.z = p1[pc + 2];
-          if (pc + 3 < a.W) pb1.w = p1[pc + 3];
-          if (kDual) {
-            const float* p2 = a.P2 + k * a.W;
-            if (pc + 0 < a.W) pb2.x = p2[pc + 0];
-            if (pc + 1 < a.W) pb2.y = p2[pc + 1];
-            if (pc + 2 < a.W) pb2.z = p2[pc + 2];
-            if (pc + 3 < a.W) pb2.w = p2[pc + 3];
-          }
-        }
-        const uint32_t off = off_mn(pc, pj, NA);
-        const float4 h1 = make_float4(tf32_hi(pb1.x), tf32_hi(pb1.y), tf32_hi(pb1.z), tf32_hi(pb1.w));
-        *reinterpret_cast<float4*>(sBhi + off) = h1;
-        *reinterpret_cast<float4*>(sBlo + off) = make_float4(pb1.x - h1.x, pb1.y - h1.y, pb1.z - h1.z, pb1.w - h1.w);
-        if (kDual) {
-          const float4 h2 = make_float4(tf32_hi(pb2.x), tf32_hi(pb2.y), tf32_hi(pb2.z), tf32_hi(pb2.w));
-          *reinterpret_cast<float4*>(sB2hi + off) = h2;
-          *reinterpret_cast<float4*>(sB2lo + off) = make_float4(pb2.x - h2.x, pb2.y - h2.y, pb2.z - h2.z, pb2.w - h2.w);
-        }
-      }
-      // A tile(s): F(X) hi / lo (+ codes)
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int f = tid + 256 * u;
-        const float l = kMode == 0 ? lam_r[u] : lam_c[u];
-        const float il = kMode == 0 ? inv_r[u] : inv_c[u];
-        const float xs[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
-        float r[4], c[4];
+    __syncwarp();
+  } else if (warp < 8) {
+    // --------------------------------------------------------------- producers
+    int it = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      int blk, split, nkb;
+      int64_t r0;
+      unit_range(u, blk, split, r0, nkb);
+      const int64_t o0 = (int64_t)blk * BM;
+      const int64_t r1 = r0 + a.chunk < r_len ? r0 + a.chunk : r_len;
+      float lam_r[4], inv_r[4];
+      if (kMode == 0) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          c[q] = codef(l, xs[q], a.mode, a.qmax);
-          r[q] = __fmul_rn(__fmaf_rn(l, xs[q], -c[q]), il);
+          const int64_t row = o0 + ((tid + 256 * q) >> 3);
+          lam_r[q] = row < a.rows ? __ldg(a.lam + row) : 1.f;
+          inv_r[q] = __frcp_rn(lam_r[q]);
         }
-        uint32_t off;
-        if (kMode == 0) off = off_k(f >> 3, (f & 7) * 4);
-        else off = off_mn((f & 31) * 4, f >> 5, 4);
-        const float4 h = make_float4(tf32_hi(r[0]), tf32_hi(r[1]), tf32_hi(r[2]), tf32_hi(r[3]));
-        *reinterpret_cast<float4*>(sAhi + off) = h;
-        *reinterpret_cast<float4*>(sAlo + off) = make_float4(r[0] - h.x, r[1] - h.y, r[2] - h.z, r[3] - h.w);
-        if (kDual) *reinterpret_cast<float4*>(sAc + off) = make_float4(c[0], c[1], c[2], c[3]);
       }
-      fence_proxy_async_smem();
-      mbar_arrive(&full[s]);
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int rs = it % RST;
+        const int os = it % OPST;
+        const int64_t k0 = r0 + (int64_t)kb * BK;
+        // B tile values (P rows [k0, k0+BK) x WN) from L2, before any waits
+        constexpr int kPB4 = BK * WN / 4;
+        constexpr int kPBper = (kPB4 + kProd - 1) / kProd;
+        float4 pb1[kPBper], pb2[kPBper];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+        for (int q = 0; q < kPBper; ++q) {
+          const int e = tid + kProd * q;
+          pb1[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+          pb2[q] = pb1[q];
+          if (e < kPB4) {
+            const int pj = e / (WN / 4), pc = (e % (WN / 4)) * 4;
+            const int64_t k = k0 + pj;
+            if (k < r1) {
+              const float* p1 = a.P1 + k * a.W;
+              if (pc + 0 < a.W) pb1[q].x = __ldg(p1 + pc + 0);
+              if (pc + 1 < a.W) pb1[q].y = __ldg(p1 + pc + 1);
+              if (pc + 2 < a.W) pb1[q].z = __ldg(p1 + pc + 2);
+              if (pc + 3 < a.W) pb1[q].w = __ldg(p1 + pc + 3);
+              if (kDual) {
+                const float* p2 = a.P2 + k * a.W;
+                if (pc + 0 < a.W) pb2[q].x = __ldg(p2 + pc + 0);
+                if (pc + 1 < a.W) pb2[q].y = __ldg(p2 + pc + 1);
+                if (pc + 2 < a.W) pb2[q].z = __ldg(p2 + pc + 2);
+                if (pc + 3 < a.W) pb2[q].w = __ldg(p2 + pc + 3);
+              }
+            }
+          }
+        }
+        float lam_c[4], inv_c[4];
+        if (kMode == 1) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int64_t row = k0 + ((tid + 256 * q) >> 5);
+            lam_c[q] = row < r1 ? __ldg(a.lam + row) : 1.f;
+            inv_c[q] = __frcp_rn(lam_c[q]);
+          }
+        }
+        // raw X tile -> registers, release the raw slot
+        mbar_wait(&rfull[rs], (it / RST) & 1);
+        float4 xv[4];
+        const uint8_t* raw = sRaw + rs * kRawTile;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int f = tid + 256 * q;
+          const uint32_t ro =
+              kMode == 0 ? (uint32_t)((f >> 3) * 128 + (f & 7) * 16) : (uint32_t)((f >> 5) * 512 + (f & 31) * 16);
+          xv[q] = *reinterpret_cast<const float4*>(raw + ro);
+        }
+        // The slot is refilled by TMA (async proxy) after this release: order our
+        // generic-proxy reads before it (without this fence rows were observed to be
+        // overwritten before they were read, ~40% of launches on B200).
+        fence_proxy_async_smem();
+        mbar_arrive(&rempty[rs]);
+        // operand stage
+        mbar_wait(&oempty[os], ((it / OPST) & 1) ^ 1);
+        uint8_t* st = sOp + os * kStage;
+        uint8_t* sAhi = st;
+        uint8_t* sAlo = st + kATile;
+        uint8_t* sAc = st + 2 * kATile;
+        uint8_t* sBhi = st + (kDual ? 3 : 2) * kATile;
+        uint8_t* sBlo = sBhi + kBTile;
+        uint8_t* sB2hi = sBlo + kBTile;
+        uint8_t* sB2lo = sB2hi + kBTile;
+#pragma unroll
+        for (int q = 0; q < kPBper; ++q) {
+          const int e = tid + kProd * q;
+          if (e < kPB4) {
+            const int pj = e / (WN / 4), pc = (e % (WN / 4)) * 4;
+            const uint32_t off = off_mn(pc, pj, NA);
+            const float4 h1 = make_float4(tf32_hi(pb1[q].x), tf32_hi(pb1[q].y), tf32_hi(pb1[q].z), tf32_hi(pb1[q].w));
+            *reinterpret_cast<float4*>(sBhi + off) = h1;
+            *reinterpret_cast<float4*>(sBlo + off) =
+                make_float4(pb1[q].x - h1.x, pb1[q].y - h1.y, pb1[q].z - h1.z, pb1[q].w - h1.w);
+            if (kDual) {
+              const float4 h2 = make_float4(tf32_hi(pb2[q].x), tf32_hi(pb2[q].y), tf32_hi(pb2[q].z), tf32_hi(pb2[q].w));
+              *reinterpret_cast<float4*>(sB2hi + off) = h2;
+              *reinterpret_cast<float4*>(sB2lo + off) =
+                  make_float4(pb2[q].x - h2.x, pb2[q].y - h2.y, pb2[q].z - h2.z, pb2[q].w - h2.w);
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int f = tid + 256 * q;
+          const float l = kMode == 0 ? lam_r[q] : lam_c[q];
+          const float il = kMode == 0 ? inv_r[q] : inv_c[q];
+          const float xs[4] = {xv[q].x, xv[q].y, xv[q].z, xv[q].w};
+          float r[4], c[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            c[e] = codef(l, xs[e], a.mode, a.qmax);
+            r[e] = __fmul_rn(__fmaf_rn(l, xs[e], -c[e]), il);
+          }
+          const uint32_t off = kMode == 0 ? off_k(f >> 3, (f & 7) * 4) : off_mn((f & 31) * 4, f >> 5, 4);
+          const float4 h = make_float4(tf32_hi(r[0]), tf32_hi(r[1]), tf32_hi(r[2]), tf32_hi(r[3]));
+          *reinterpret_cast<float4*>(sAhi + off) = h;
+          *reinterpret_cast<float4*>(sAlo + off) = make_float4(r[0] - h.x, r[1] - h.y, r[2] - h.z, r[3] - h.w);
+          if (kDual) *reinterpret_cast<float4*>(sAc + off) = make_float4(c[0], c[1], c[2], c[3]);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&ofull[os]);
+      }
     }
-    // ------------------------------------------------------------- epilogue
-    if (warp < 4) {
-      mbar_wait(done, 0);
+  } else if (warp == kMmaWarp) {
+    // --------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(WN, kMode == 1 ? 1u : 0u, 1u);
+      int it = 0, lu = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+        int blk, split, nkb;
+        int64_t r0;
+        unit_range(u, blk, split, r0, nkb);
+        const int acc = lu & 1;
+        mbar_wait(&tempty[acc], ((lu >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d1 = tmem + acc * C::kAccCols;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int os = it % OPST;
+          mbar_wait(&ofull[os], (it / OPST) & 1);
+          tc_fence_after();
+          const uint32_t st = smem_u32(sOp + os * kStage);
+          const uint32_t aHi = st, aLo = st + kATile, aC = st + 2 * kATile;
+          const uint32_t bHi = st + (kDual ? 3 : 2) * kATile;
+          const uint32_t bLo = bHi + kBTile, b2Hi = bLo + kBTile, b2Lo = b2Hi + kBTile;
+#pragma unroll
+          for (int k = 0; k < BK / 8; ++k) {
+            uint32_t aoff, lboA, sboA, tA;
+            if (kMode == 0) { aoff = k * 32; lboA = 16; sboA = 1024; tA = 2; }   // K-major: +32 B per 8 k
+            else { aoff = k * 4096; lboA = 512; sboA = 2048; tA = 1; }           // MN-major: two 4-deep groups
+            const uint32_t boff = k * (NA * 1024);
+            const uint32_t acc0 = (kb | k) != 0 ? 1u : 0u;
+            const uint64_t dAhi = desc_sw128(aHi + aoff, lboA, sboA, tA);
+            const uint64_t dAlo = desc_sw128(aLo + aoff, lboA, sboA, tA);
+            const uint64_t dBhi = desc_sw128(bHi + boff, 512, NA * 512, 1);
+            const uint64_t dBlo = desc_sw128(bLo + boff, 512, NA * 512, 1);
+            umma_tf32(d1, dAhi, dBhi, idesc, acc0);
+            umma_tf32(d1, dAhi, dBlo, idesc, 1u);
+            umma_tf32(d1, dAlo, dBhi, idesc, 1u);
+            if (kDual) {
+              const uint64_t dAc = desc_sw128(aC + aoff, lboA, sboA, tA);
+              const uint64_t dB2hi = desc_sw128(b2Hi + boff, 512, NA * 512, 1);
+              const uint64_t dB2lo = desc_sw128(b2Lo + boff, 512, NA * 512, 1);
+              umma_tf32(d1 + WN, dAc, dB2hi, idesc, acc0);
+              umma_tf32(d1 + WN, dAc, dB2lo, idesc, 1u);
+            }
+          }
+          umma_commit(&oempty[os]);
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    const int quad = warp & 3;
+    int lu = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+      int blk, split, nkb;
+      int64_t r0;
+      unit_range(u, blk, split, r0, nkb);
+      const int acc = lu & 1;
+      mbar_wait(&tfull[acc], (lu >> 1) & 1);
       tc_fence_after();
-      const int64_t orow = o0 + warp * 32 + lane;
-      const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+      const int64_t orow = (int64_t)blk * BM + quad * 32 + lane;
+      const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + acc * C::kAccCols;
       float inv_row = 1.f;
-      if (kDual) inv_row = orow < a.rows ? __frcp_rn(a.lam[orow]) : 1.f;
-      float* out1 = a.out1 + (int64_t)blockIdx.y * a.nout * a.W;
-      float* out2 = kDual ? a.out2 + (int64_t)blockIdx.y * a.nout * a.W : nullptr;
+      if (kDual) inv_row = orow < a.rows ? __frcp_rn(__ldg(a.lam + orow)) : 1.f;
+      float* out1 = a.out1 + (int64_t)split * a.nout * a.W;
+      float* out2 = kDual ? a.out2 + (int64_t)split * a.nout * a.W : nullptr;
 #pragma unroll
       for (int h = 0; h < NA * (kDual ? 2 : 1); ++h) {
         uint32_t v[32];
@@ -305,51 +419,13 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(TcArgs a) {
         }
       }
       tc_fence_before();
+      mbar_arrive(&tempty[acc]);
     }
-  } else {
-    // ------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-    constexpr uint32_t idesc1 = idesc_tf32(WN, kMode == 1 ? 1u : 0u, 1u);
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % STAGES;
-      mbar_wait(&full[s], (uint32_t)((kb / STAGES) & 1));
-      tc_fence_after();
-      const uint32_t st = smem_u32(smem + s * kStage);
-      const uint32_t aHi = st, aLo = st + kATile, aC = st + 2 * kATile;
-      const uint32_t bHi = st + (kDual ? 3 : 2) * kATile;
-      const uint32_t bLo = bHi + kBTile, b2Hi = bLo + kBTile, b2Lo = b2Hi + kBTile;
-#pragma unroll
-      for (int k = 0; k < BK / 8; ++k) {
-        uint32_t aoff, lboA, sboA, tA;
-        if (kMode == 0) { aoff = k * 32; lboA = 16; sboA = 1024; tA = 2; }        // K-major: +32 B per 8 k
-        else { aoff = k * 4096; lboA = 512; sboA = 2048; tA = 1; }                // MN-major: next two 4-deep groups
-        const uint32_t boff = k * (NA * 1024);
-        const uint64_t dAhi = desc_sw128(aHi + aoff, lboA, sboA, tA);
-        const uint64_t dAlo = desc_sw128(aLo + aoff, lboA, sboA, tA);
-        const uint64_t dBhi = desc_sw128(bHi + boff, 512, NA * 512, 1);
-        const uint64_t dBlo = desc_sw128(bLo + boff, 512, NA * 512, 1);
-        const uint32_t acc0 = (kb | k) != 0 ? 1u : 0u;
-        umma_tf32(tmem, dAhi, dBhi, idesc1, acc0);
-        umma_tf32(tmem, dAhi, dBlo, idesc1, 1u);
-        umma_tf32(tmem, dAlo, dBhi, idesc1, 1u);
-        if (kDual) {
-          const uint64_t dAc = desc_sw128(aC + aoff, lboA, sboA, tA);
-          const uint64_t dB2hi = desc_sw128(b2Hi + boff, 512, NA * 512, 1);
-          const uint64_t dB2lo = desc_sw128(b2Lo + boff, 512, NA * 512, 1);
-          umma_tf32(tmem + WN, dAc, dB2hi, idesc1, acc0);
-          umma_tf32(tmem + WN, dAc, dB2lo, idesc1, 1u);
-        }
-      }
-      umma_commit(&empty[s]);
-    }
-    umma_commit(done);
-    }
-    __syncwarp();  // reconverge before the CTA barrier (bar.sync is .aligned)
   }
   __syncthreads();
-  if (warp == 8) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
-    tmem_free<kTmemCols>(tmem);
+    tmem_free<C::kTmemCols>(tmem);
   }
 }
 
@@ -364,23 +440,21 @@ __global__ void k_reduce_splits_tc(const float* __restrict__ part, int nsplit, i
 template <int kMode, int NA, bool kDual>
 static void run_tc(const TcArgs& a0, float* OUT1, float* OUT2, float* partial, int64_t pe, cudaStream_t st) {
   using namespace tcp;
-  constexpr int WN = 32 * NA;
-  constexpr int kBTile = BK * WN * 4;
-  constexpr int kStage = (kDual ? 3 : 2) * kATile + (kDual ? 4 : 2) * kBTile;
-  constexpr int kSmem = STAGES * kStage + 1024 + 128;
+  using C = Cfg<NA, kDual>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_tc_proj<kMode, NA, kDual>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(k_tc_proj<kMode, NA, kDual>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr = true;
   }
   TcArgs a = a0;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t nblk = (a.nout + BM - 1) / BM;
   const int64_t rlen = kMode == 0 ? (int64_t)a.K : a.rows;
-  const int per_sm = kSmem <= 113 * 1024 ? 2 : 1;
-  const int64_t slots = 148LL * per_sm;
-  // splits so that the grid is ~3 waves of resident CTAs, each split >= 4 stages of work
-  int64_t ns = (3 * slots + nblk - 1) / nblk;
-  const int64_t maxs = (rlen + 4 * BK - 1) / (4 * BK);
+  // enough units for ~6 per SM (the persistent grid balances them), each >= 8 k-blocks
+  int64_t ns = (6LL * nsm + nblk - 1) / nblk;
+  const int64_t maxs = (rlen + 8 * BK - 1) / (8 * BK);
   if (ns > maxs) ns = maxs;
   const int64_t per = a.nout * a.W * (kDual ? 2 : 1);
   if (ns > 1 && ns * per > pe) ns = pe / per;
@@ -388,10 +462,16 @@ static void run_tc(const TcArgs& a0, float* OUT1, float* OUT2, float* partial, i
   a.chunk = ((rlen + ns - 1) / ns + BK - 1) / BK * BK;
   ns = (rlen + a.chunk - 1) / a.chunk;
   if (ns < 1) ns = 1;
+  a.nblk = (int)nblk;
+  a.nsplit = (int)ns;
   a.out1 = ns == 1 ? OUT1 : partial;
   a.out2 = ns == 1 ? OUT2 : partial + ns * a.nout * a.W;
-  dim3 grid((unsigned)nblk, (unsigned)ns);
-  k_tc_proj<kMode, NA, kDual><<<grid, kThreads, kSmem, st>>>(a);
+  alignas(64) CUtensorMap xmap;
+  if (kMode == 0) encode_map_2d(&xmap, 1, a.X, (uint64_t)a.K, (uint64_t)a.rows, (uint64_t)a.ldx * 4, BK, BM);
+  else encode_map_2d(&xmap, 1, a.X, (uint64_t)a.K, (uint64_t)a.rows, (uint64_t)a.ldx * 4, BM, BK);
+  const int64_t units = nblk * ns;
+  const int grid = (int)(units < nsm ? units : nsm);
+  k_tc_proj<kMode, NA, kDual><<<grid, kThreads, C::kSmem, st>>>(xmap, a);
   ++launch_counter();
   if (ns > 1) {
     const int64_t n = a.nout * a.W;
@@ -421,10 +501,11 @@ static TcArgs make_args(const SideView& s, const float* P1, const float* P2, int
   return a;
 }
 
-// ROW mode: OUT1 = R P1 (f1 must be residual); dual: OUT2 = X~ P2
+// X must be TMA-addressable: 16-byte aligned base and ldx % 4 == 0 (lrqmm_quantize
+// stages other layouts into an aligned handle-owned copy).
 void launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
                          float* partial, int64_t pe, cudaStream_t st) {
-  if (s.rows == 0) return;
+  if (s.rows == 0 || s.K == 0) return;
   TcArgs a = make_args(s, P1, P2, W, s.rows);
   if (W <= 32) {
     if (P2) run_tc<0, 1, true>(a, OUT1, OUT2, partial, pe, st);
@@ -435,10 +516,9 @@ void launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const 
   }
 }
 
-// COL mode: OUT = R^T P (P rows x W, OUT K x W)
 void launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t pe,
                          cudaStream_t st) {
-  if (s.K == 0) return;
+  if (s.K == 0 || s.rows == 0) return;
   TcArgs a = make_args(s, P, nullptr, W, s.K);
   if (W <= 32) run_tc<1, 1, false>(a, OUT, nullptr, partial, pe, st);
   else run_tc<1, 2, false>(a, OUT, nullptr, partial, pe, st);

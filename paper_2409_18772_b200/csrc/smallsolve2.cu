@@ -67,10 +67,19 @@ __global__ void __launch_bounds__(256) k_gram(GramJobs jobs, int W) {
   __syncthreads();
   if (ticket != (int)gridDim.x - 1) return;
   __threadfence();
+  // fixed-order 4-way split sum over the block partials (independent loads in flight)
+  const int nb = (int)gridDim.x;
   for (int pr = threadIdx.x; pr < npairs; pr += 256) {
-    double a = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) a += __ldcg(jb.partial + (int64_t)b * npairs + pr);
-    jb.G[pr] = a;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int b = 0;
+    for (; b + 3 < nb; b += 4) {
+      a0 += __ldcg(jb.partial + (int64_t)(b + 0) * npairs + pr);
+      a1 += __ldcg(jb.partial + (int64_t)(b + 1) * npairs + pr);
+      a2 += __ldcg(jb.partial + (int64_t)(b + 2) * npairs + pr);
+      a3 += __ldcg(jb.partial + (int64_t)(b + 3) * npairs + pr);
+    }
+    for (; b < nb; ++b) a0 += __ldcg(jb.partial + (int64_t)b * npairs + pr);
+    jb.G[pr] = (a0 + a1) + (a2 + a3);
   }
   if (threadIdx.x == 0) *jb.counter = 0;  // re-arm for the next launch (stream ordered)
 }
@@ -78,100 +87,108 @@ __global__ void __launch_bounds__(256) k_gram(GramJobs jobs, int W) {
 void launch_gram_jobs(const GramJobs& jobs, int W, cudaStream_t st) {
   int64_t nmax = 0;
   for (int i = 0; i < jobs.n; ++i) nmax = jobs.j[i].n > nmax ? jobs.j[i].n : nmax;
-  int64_t nb = (nmax + 127) / 128;
-  if (nb > 148) nb = 148;
+  int64_t nb = (nmax + 511) / 512;
+  if (nb > 64) nb = 64;
   if (nb < 1) nb = 1;
   k_gram<<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs, W);
   ++launch_counter();
 }
 
 // ------------------------------------------------- pivoted Cholesky orth
-__global__ void __launch_bounds__(32) k_chol_orth(EigJobs jobs, int n) {
+// 256 threads: pivot search by warp 0, column scaling and the trailing rank-1
+// update by the whole CTA; L^-1 by row-sequential forward substitution.
+__global__ void __launch_bounds__(256) k_chol_orth(EigJobs jobs, int n) {
   extern __shared__ double dyn[];
   double (*A)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn);
   double (*Li)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn + kN * (kN + 1));  // L^-1 (lower)
   __shared__ int piv[kN];
-  __shared__ int rank_s;
+  __shared__ int bi_s, stop_s;
+  __shared__ double dmax_s;
   const EigJob job = jobs.j[blockIdx.x];
-  const int lane = threadIdx.x;
-  for (int e = lane; e < n * n; e += 32) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int e = tid; e < n * n; e += 256) {
     const int i = e / n, j = e % n;
     A[i][j] = 0.5 * (job.G[i * n + j] + job.G[j * n + i]);
     Li[i][j] = 0.0;
   }
-  if (lane < n) piv[lane] = lane;
-  if (n > 32 && lane + 32 < n) piv[lane + 32] = lane + 32;
-  __syncwarp();
-  // reference scale: largest diagonal entry
-  double dmax = 0.0;
-  for (int i = lane; i < n; i += 32) dmax = fmax(dmax, A[i][i]);
+  if (tid < n) piv[tid] = tid;
+  __syncthreads();
+  if (tid < 32) {
+    double dm = 0.0;
+    for (int i = lane; i < n; i += 32) dm = fmax(dm, A[i][i]);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+    if (lane == 0) dmax_s = dm;
+  }
+  __syncthreads();
+  const double dmax = dmax_s;
   const double thr = 1e-10 * dmax;
   int k = 0;
   for (; k < n; ++k) {
-    // pivot: largest remaining diagonal (ties -> lowest index)
-    double best = -1.0;
-    int bi = k;
-    for (int i = k + lane; i < n; i += 32) {
-      const double d = A[i][i];
-      if (d > best) { best = d; bi = i; }
-    }
+    if (tid < 32) {
+      double best = -1.0;
+      int bi = k;
+      for (int i = k + lane; i < n; i += 32) {
+        const double d = A[i][i];
+        if (d > best) { best = d; bi = i; }
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) {
+        bi_s = bi;
+        stop_s = !(dmax > 0.0) || best < thr || best <= 0.0;
+      }
     }
-    if (!(dmax > 0.0) || best < thr || best <= 0.0) break;
-    // symmetric swap of row/col k and bi
-    if (bi != k) {
-      for (int j = lane; j < n; j += 32) {
+    __syncthreads();
+    if (stop_s) break;
+    const int bi = bi_s;
+    if (bi != k) {  // symmetric swap of row/col k and bi
+      for (int j = tid; j < n; j += 256) {
         const double t = A[k][j]; A[k][j] = A[bi][j]; A[bi][j] = t;
       }
-      __syncwarp();
-      for (int i = lane; i < n; i += 32) {
+      __syncthreads();
+      for (int i = tid; i < n; i += 256) {
         const double t = A[i][k]; A[i][k] = A[i][bi]; A[i][bi] = t;
       }
-      if (lane == 0) { const int t = piv[k]; piv[k] = piv[bi]; piv[bi] = t; }
-      __syncwarp();
+      if (tid == 0) { const int t = piv[k]; piv[k] = piv[bi]; piv[bi] = t; }
+      __syncthreads();
     }
     const double lkk = sqrt(A[k][k]);
     const double inv = 1.0 / lkk;
-    __syncwarp();
-    // column k of L below the diagonal
-    for (int i = k + 1 + lane; i < n; i += 32) A[i][k] *= inv;
-    if (lane == 0) A[k][k] = lkk;
-    __syncwarp();
-    // trailing update A[i][j] -= L[i][k] L[j][k]  (full symmetric block: later swaps read both triangles)
+    __syncthreads();
+    for (int i = k + 1 + tid; i < n; i += 256) A[i][k] *= inv;
+    if (tid == 0) A[k][k] = lkk;
+    __syncthreads();
     const int m = n - k - 1;
-    for (int e = lane; e < m * m; e += 32) {
+    for (int e = tid; e < m * m; e += 256) {
       const int i = k + 1 + e / m, j = k + 1 + e % m;
       A[i][j] -= A[i][k] * A[j][k];
     }
-    __syncwarp();
+    __syncthreads();
   }
-  if (lane == 0) rank_s = k;
-  __syncwarp();
-  const int rk = rank_s;
-  // Li = L^-1 (rk x rk lower triangular), column by column (lane = column)
-  for (int c = lane; c < rk; c += 32) {
-    for (int i = c; i < rk; ++i) {
-      double s = (i == c) ? 1.0 : 0.0;
-      for (int t = c; t < i; ++t) s -= A[i][t] * Li[t][c];
-      Li[i][c] = s / A[i][i];
+  const int rk = k;
+  // Li = L^-1: row i from rows < i (thread c computes Li[i][c], c <= i)
+  for (int i = 0; i < rk; ++i) {
+    if (tid <= i) {
+      const int c = tid;
+      double sacc = (i == c) ? 1.0 : 0.0;
+      for (int t = c; t < i; ++t) sacc -= A[i][t] * Li[t][c];
+      Li[i][c] = sacc / A[i][i];
     }
+    __syncthreads();
   }
-  __syncwarp();
-  // T[piv[a]][b] = (L^-T)[a][b] = Li[b][a] for a, b < rk; zero elsewhere
-  for (int e = lane; e < n * n; e += 32) {
-    const int rr = e / n, b = e % n;  // T row rr (original index), column b
-    job.T[rr * n + b] = 0.f;
-  }
-  __syncwarp();
-  for (int e = lane; e < rk * rk; e += 32) {
-    const int a = e / rk, b = e % rk;
-    if (b >= a) job.T[piv[a] * n + b] = (float)Li[b][a];
+  // T[piv[a]][b] = (L^-T)[a][b] = Li[b][a] for a <= b < rk; zero elsewhere
+  for (int e = tid; e < n * n; e += 256) {
+    const int rr = e / n, b = e % n;
+    float v = 0.f;
+    // find a with piv[a] == rr (a < rk)
+    for (int a2 = 0; a2 < rk; ++a2)
+      if (piv[a2] == rr && b >= a2 && b < rk) v = (float)Li[b][a2];
+    job.T[rr * n + b] = v;
   }
 }
 
@@ -183,30 +200,34 @@ void launch_chol_orth(const EigJobs& jobs, int n, cudaStream_t st) {
     cudaFuncSetAttribute(k_chol_orth, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
     attr = true;
   }
-  k_chol_orth<<<jobs.n, 32, kDynSmem, st>>>(jobs, n);
+  k_chol_orth<<<jobs.n, 256, kDynSmem, st>>>(jobs, n);
   ++launch_counter();
 }
 
-// ------------------------------------------------ one-warp Jacobi (truncation)
-__global__ void __launch_bounds__(32) k_eig_warp(EigJobs jobs, int n) {
+// --------------------------------------------- parallel Jacobi (truncation)
+// Round-robin pairing: n/2 disjoint rotations per step.  A' = J^T A J is applied
+// in ONE pass over 2x2 blocks (pair k1 rows x pair k2 cols), V' = V J in another.
+__global__ void __launch_bounds__(256) k_eig(EigJobs jobs, int n) {
   extern __shared__ double dyn[];
   double (*A)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn);
   double (*V)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn + kN * (kN + 1));
   __shared__ double cs[kN / 2], sn[kN / 2];
   __shared__ int pp[kN / 2], qq[kN / 2];
   __shared__ int order[kN];
+  __shared__ double red[8][2];
+  __shared__ int stop;
   const EigJob job = jobs.j[blockIdx.x];
-  const int lane = threadIdx.x;
-  for (int e = lane; e < n * n; e += 32) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < n * n; e += 256) {
     const int i = e / n, j = e % n;
     A[i][j] = 0.5 * (job.G[i * n + j] + job.G[j * n + i]);
     V[i][j] = (i == j) ? 1.0 : 0.0;
   }
-  __syncwarp();
+  __syncthreads();
   const int half = n / 2;
   for (int sweep = 0; sweep < 30; ++sweep) {
     double off = 0.0, dg = 0.0;
-    for (int e = lane; e < n * n; e += 32) {
+    for (int e = tid; e < n * n; e += 256) {
       const int i = e / n, j = e % n;
       const double v = A[i][j] * A[i][j];
       if (i == j) dg += v; else off += v;
@@ -216,9 +237,18 @@ __global__ void __launch_bounds__(32) k_eig_warp(EigJobs jobs, int n) {
       off += __shfl_xor_sync(0xffffffffu, off, o);
       dg += __shfl_xor_sync(0xffffffffu, dg, o);
     }
-    if (off <= 1e-30 * dg || off == 0.0) break;
+    if (lane == 0) { red[warp][0] = off; red[warp][1] = dg; }
+    __syncthreads();
+    if (tid == 0) {
+      double o2 = 0.0, d2 = 0.0;
+      for (int w = 0; w < 8; ++w) { o2 += red[w][0]; d2 += red[w][1]; }
+      stop = (o2 <= 1e-30 * d2) || (o2 == 0.0);
+    }
+    __syncthreads();
+    if (stop) break;
     for (int step = 0; step < n - 1; ++step) {
-      for (int k = lane; k < half; k += 32) {
+      if (tid < half) {
+        const int k = tid;
         int p, q;
         if (k == 0) { p = 0; q = (step % (n - 1)) + 1; }
         else { p = ((k + step) % (n - 1)) + 1; q = ((n - 1 - k + step) % (n - 1)) + 1; }
@@ -235,31 +265,48 @@ __global__ void __launch_bounds__(32) k_eig_warp(EigJobs jobs, int n) {
         }
         pp[k] = p; qq[k] = q; cs[k] = c; sn[k] = s;
       }
-      __syncwarp();
-      for (int e = lane; e < half * n; e += 32) {
-        const int k = e / n, j = e % n;
-        const int p = pp[k], q = qq[k];
-        const double c = cs[k], s = sn[k];
-        const double ap = A[p][j], aq = A[q][j];
-        A[p][j] = c * ap - s * aq;
-        A[q][j] = s * ap + c * aq;
+      __syncthreads();
+      // 2x2 blocks: rows (p1,q1) of pair k1 x cols (p2,q2) of pair k2; all reads, barrier, all writes
+      // (half^2 <= 1024 blocks -> at most 4 per thread)
+      double nb[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = tid + 256 * u;
+        if (e < half * half) {
+          const int k1 = e / half, k2 = e % half;
+          const int p1 = pp[k1], q1 = qq[k1], p2 = pp[k2], q2 = qq[k2];
+          const double c1 = cs[k1], s1 = sn[k1], c2 = cs[k2], s2 = sn[k2];
+          const double a = A[p1][p2], b = A[p1][q2], c = A[q1][p2], d = A[q1][q2];
+          const double ra = c1 * a - s1 * c, rb = c1 * b - s1 * d;
+          const double rc = s1 * a + c1 * c, rd = s1 * b + c1 * d;
+          nb[u][0] = c2 * ra - s2 * rb;
+          nb[u][1] = s2 * ra + c2 * rb;
+          nb[u][2] = c2 * rc - s2 * rd;
+          nb[u][3] = s2 * rc + c2 * rd;
+        }
       }
-      __syncwarp();
-      for (int e = lane; e < half * n; e += 32) {
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = tid + 256 * u;
+        if (e < half * half) {
+          const int k1 = e / half, k2 = e % half;
+          const int p1 = pp[k1], q1 = qq[k1], p2 = pp[k2], q2 = qq[k2];
+          A[p1][p2] = nb[u][0]; A[p1][q2] = nb[u][1]; A[q1][p2] = nb[u][2]; A[q1][q2] = nb[u][3];
+        }
+      }
+      for (int e = tid; e < half * n; e += 256) {
         const int k = e / n, i = e % n;
         const int p = pp[k], q = qq[k];
         const double c = cs[k], s = sn[k];
-        const double ap = A[i][p], aq = A[i][q];
-        A[i][p] = c * ap - s * aq;
-        A[i][q] = s * ap + c * aq;
         const double vp = V[i][p], vq = V[i][q];
         V[i][p] = c * vp - s * vq;
         V[i][q] = s * vp + c * vq;
       }
-      __syncwarp();
+      __syncthreads();
     }
   }
-  for (int t = lane; t < n; t += 32) {
+  for (int t = tid; t < n; t += 256) {
     int rank = 0;
     const double li = A[t][t];
     for (int j = 0; j < n; ++j) {
@@ -268,8 +315,8 @@ __global__ void __launch_bounds__(32) k_eig_warp(EigJobs jobs, int n) {
     }
     order[rank] = t;
   }
-  __syncwarp();
-  for (int e = lane; e < n * n; e += 32) {
+  __syncthreads();
+  for (int e = tid; e < n * n; e += 256) {
     const int a = e / n, o = e % n;
     job.T[a * n + o] = (o < job.r) ? (float)V[a][order[o]] : 0.f;
   }
@@ -278,10 +325,10 @@ __global__ void __launch_bounds__(32) k_eig_warp(EigJobs jobs, int n) {
 void launch_eig_warp(const EigJobs& jobs, int n, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_eig_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+    cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
     attr = true;
   }
-  k_eig_warp<<<jobs.n, 32, kDynSmem, st>>>(jobs, n);
+  k_eig<<<jobs.n, 256, kDynSmem, st>>>(jobs, n);
   ++launch_counter();
 }
 

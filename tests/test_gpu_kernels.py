@@ -38,7 +38,7 @@ def test_proj_rows(rows, K, W):
     st = torch.cuda.current_stream().cuda_stream
     assert lib.lrqmm_debug_proj(0, cu(X).data_ptr(), K, rows, K, cu(lam).data_ptr(), 4, 0, cu(P).data_ptr(), None,
                                 W, out.data_ptr(), None, st) == 0
-    assert rel(out.cpu().numpy(), R @ P.astype(np.float64)) < 2e-6
+    assert rel(out.cpu().numpy(), R @ P.astype(np.float64)) < 1e-5
 
 
 @pytest.mark.parametrize("rows,K,W", [(128, 128, 32), (300, 1000, 24), (1000, 333, 8), (4096, 257, 40)])
@@ -50,7 +50,7 @@ def test_proj_cols(rows, K, W):
     st = torch.cuda.current_stream().cuda_stream
     assert lib.lrqmm_debug_proj(1, cu(X).data_ptr(), K, rows, K, cu(lam).data_ptr(), 4, 0, cu(P).data_ptr(), None,
                                 W, out.data_ptr(), None, st) == 0
-    assert rel(out.cpu().numpy(), R.T @ P.astype(np.float64)) < 2e-6
+    assert rel(out.cpu().numpy(), R.T @ P.astype(np.float64)) < 1e-5
 
 
 @pytest.mark.parametrize("rows,K,W", [(128, 32, 32), (300, 1000, 24), (257, 2048, 48)])
@@ -65,8 +65,8 @@ def test_proj_rows_dual(rows, K, W):
     st = torch.cuda.current_stream().cuda_stream
     assert lib.lrqmm_debug_proj(2, cu(X).data_ptr(), K, rows, K, cu(lam).data_ptr(), 8, 0, cu(P).data_ptr(),
                                 cu(P2).data_ptr(), W, out.data_ptr(), out2.data_ptr(), st) == 0
-    assert rel(out.cpu().numpy(), R @ P.astype(np.float64)) < 2e-6
-    assert rel(out2.cpu().numpy(), O.dequantize(codes, lam) @ P2.astype(np.float64)) < 2e-6
+    assert rel(out.cpu().numpy(), R @ P.astype(np.float64)) < 1e-5
+    assert rel(out2.cpu().numpy(), O.dequantize(codes, lam) @ P2.astype(np.float64)) < 1e-5
 
 
 @pytest.mark.parametrize("n,W", [(1000, 24), (16384, 32), (77, 8), (5000, 64)])
