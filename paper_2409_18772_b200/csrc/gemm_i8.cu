@@ -334,6 +334,19 @@ int encode_map_2d(void* map, int dtype_f32, const void* base, uint64_t inner, ui
   return r == CUDA_SUCCESS ? 0 : 2;
 }
 
+int encode_map_1d_f32(void* map, const void* base, uint64_t n, uint32_t box) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return 1;
+  cuuint64_t dims[1] = {(cuuint64_t)n};
+  cuuint64_t strides[1] = {0};
+  cuuint32_t bx[1] = {box};
+  cuuint32_t estr[1] = {1};
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<void*>(base), dims,
+                   strides, bx, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : 2;
+}
+
 int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB) {
   if (encode_codes_map(reinterpret_cast<CUtensorMap*>(mapA), g.A, g.M, g.Kp, g6::BM)) return 1;
   if (encode_codes_map(reinterpret_cast<CUtensorMap*>(mapB), g.B, g.N, g.Kp, g6::BN)) return 1;

@@ -21,12 +21,13 @@ struct QuantArgs {
   int K, Kp, qmax, mode;
   int8_t* codes;          // rows x Kp
   float* lam;             // rows (written unless lam_fixed)
+  float* inv_lam;         // rows: RN(1/lambda) (written unless lam_fixed)
   const float* lam_fixed; // device scalar (per-tensor mode) or nullptr
   int* err_flag;          // bit 0: non-finite input
 };
 void launch_quantize(const QuantArgs& a, cudaStream_t st);
 void launch_tensor_scale(const float* X, int64_t ldx, int64_t rows, int K, int qmax, float* row_amax,
-                         float* lam_rows, float* lam_scalar, int* err_flag, cudaStream_t st);
+                         float* lam_rows, float* inv_rows, float* lam_scalar, int* err_flag, cudaStream_t st);
 
 // ------------------------------------------------- K2/K3 skinny residual products
 // F(x_ij) is recomputed from X and lambda_i (never stored):
@@ -38,6 +39,7 @@ struct SideView {
   int64_t rows;
   int K;
   const float* lam;
+  const float* inv_lam;  // RN(1/lambda)
   int qmax, mode;
 };
 // tcgen05 kind::tf32 (3-term split) passes, deterministic split-K partials:
@@ -105,6 +107,9 @@ int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB);  // returns 0 
 // 2D TMA map (no swizzle), dims {inner, outer} elements of fp32 (dtype_f32=1) or u8; returns 0 on success
 int encode_map_2d(void* map, int dtype_f32, const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
                   uint32_t box_inner, uint32_t box_outer);
+int encode_map_1d_f32(void* map, const void* base, uint64_t n, uint32_t box);
+// out[i] = RN(1 / in[i])
+void launch_recip(const float* in, float* out, int64_t n, cudaStream_t st);
 void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStream_t st);
 
 }  // namespace lrqmm

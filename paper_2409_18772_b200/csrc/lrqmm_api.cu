@@ -27,6 +27,7 @@ struct Side {
   float* stage = nullptr;    // aligned copy, only for layouts TMA cannot address
   int8_t* codes = nullptr;   // rows x Kp
   float* lam = nullptr;      // rows
+  float* inv_lam = nullptr;  // rows, RN(1/lambda)
   float* row_amax = nullptr; // rows (per-tensor mode)
   float* lam_scalar = nullptr;
   float* Om = nullptr;       // K x W (zero-padded sketch)
@@ -161,7 +162,7 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   cudaSetDevice(h->cfg.device);
   if (h->st) cudaStreamSynchronize(h->st);
   for (auto& s : h->s) {
-    cudaFree(s.codes); cudaFree(s.lam); cudaFree(s.row_amax); cudaFree(s.lam_scalar); cudaFree(s.Om);
+    cudaFree(s.codes); cudaFree(s.lam); cudaFree(s.inv_lam); cudaFree(s.row_amax); cudaFree(s.lam_scalar); cudaFree(s.Om);
     cudaFree(s.Y); cudaFree(s.Q0); cudaFree(s.Z); cudaFree(s.Q1); cudaFree(s.Gp); cudaFree(s.G);
     cudaFree(s.gpart); cudaFree(s.counter); cudaFree(s.T); cudaFree(s.VW); cudaFree(s.stage);
   }
@@ -203,7 +204,7 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
   const int64_t K = cfg->k;
   bool ok = true;
   for (auto& s : h->s) {
-    ok = ok && dalloc(&s.codes, s.rows * h->Kp) && dalloc(&s.lam, s.rows) && dalloc(&s.row_amax, s.rows) &&
+    ok = ok && dalloc(&s.codes, s.rows * h->Kp) && dalloc(&s.lam, s.rows) && dalloc(&s.inv_lam, s.rows) && dalloc(&s.row_amax, s.rows) &&
          dalloc(&s.lam_scalar, 1);
     if (h->W > 0) {
       ok = ok && dalloc(&s.Om, K * h->W) && dalloc(&s.Y, s.rows * h->W) && dalloc(&s.Q0, s.rows * h->W) &&
@@ -284,7 +285,8 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
     s.ldx = lds;
   }
   if (h->cfg.granularity == LRQMM_SCALE_PER_TENSOR) {
-    launch_tensor_scale(X, ldx, s.rows, (int)h->cfg.k, h->qmax, s.row_amax, s.lam, s.lam_scalar, h->err_flag, h->st);
+    launch_tensor_scale(s.X, s.ldx, s.rows, (int)h->cfg.k, h->qmax, s.row_amax, s.lam, s.inv_lam, s.lam_scalar, h->err_flag,
+                        h->st);
   }
   QuantArgs a;
   a.X = s.X;
@@ -296,6 +298,7 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
   a.mode = h->cfg.rounding;
   a.codes = s.codes;
   a.lam = s.lam;
+  a.inv_lam = s.inv_lam;
   a.lam_fixed = h->cfg.granularity == LRQMM_SCALE_PER_TENSOR ? s.lam_scalar : nullptr;
   a.err_flag = h->err_flag;
   if (s.rows > 0) launch_quantize(a, h->st);
@@ -314,6 +317,7 @@ static SideView view(lrqmm_handle_t h, int sd) {
   v.rows = h->s[sd].rows;
   v.K = (int)h->cfg.k;
   v.lam = h->s[sd].lam;
+  v.inv_lam = h->s[sd].inv_lam;
   v.qmax = h->qmax;
   v.mode = h->cfg.rounding;
   return v;
@@ -608,7 +612,10 @@ extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx
     X = stage;
     ldx = lds;
   }
-  SideView v{X, ldx, rows, K, lam, (1 << (bits - 1)) - 1, rounding};
+  float* inv = nullptr;
+  if (cudaMalloc(&inv, sizeof(float) * (rows > 0 ? rows : 1)) != cudaSuccess) return LRQMM_ERR_ALLOC;
+  launch_recip(lam, inv, rows, st);
+  SideView v{X, ldx, rows, K, lam, inv, (1 << (bits - 1)) - 1, rounding};
   const int64_t pe = (int64_t)16 << 20;
   float* partial = nullptr;
   if (cudaMalloc(&partial, sizeof(float) * pe) != cudaSuccess) return LRQMM_ERR_ALLOC;
@@ -618,6 +625,7 @@ extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx
   cudaError_t e = cudaStreamSynchronize(st);
   if (e == cudaSuccess) e = cudaGetLastError();
   cudaFree(partial);
+  cudaFree(inv);
   if (stage) cudaFree(stage);
   return e == cudaSuccess ? LRQMM_OK : LRQMM_ERR_CUDA;
 }

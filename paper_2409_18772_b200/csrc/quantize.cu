@@ -54,8 +54,8 @@ LRQMM_DEV uint32_t pack4(int8_t a, int8_t b, int8_t c, int8_t d) {
 template <int TPR, int VPT, bool kVec, bool kFixedLam>
 __global__ void __launch_bounds__(256) k1_quantize(const float* __restrict__ X, int64_t ldx, int rows, int K, int Kp,
                                                    int qmax, int mode, int8_t* __restrict__ codes,
-                                                   float* __restrict__ lam_out, const float* __restrict__ lam_in,
-                                                   int* __restrict__ err_flag) {
+                                                   float* __restrict__ lam_out, float* __restrict__ inv_out,
+                                                   const float* __restrict__ lam_in, int* __restrict__ err_flag) {
   constexpr int kRowsPerCta = 256 / TPR;
   constexpr int kWarpsPerRow = TPR / 32;
   __shared__ float red[8];
@@ -106,7 +106,10 @@ __global__ void __launch_bounds__(256) k1_quantize(const float* __restrict__ X, 
       lam = (amax == 0.f) ? 1.f : __fdiv_rn(static_cast<float>(qmax), amax);
     }
     if (active) {
-      if (!kFixedLam && sub == 0) lam_out[row] = lam;
+      if (!kFixedLam && sub == 0) {
+        lam_out[row] = lam;
+        inv_out[row] = __frcp_rn(lam);
+      }
       uint32_t* crow = reinterpret_cast<uint32_t*>(codes + row * (int64_t)Kp);
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
@@ -149,7 +152,8 @@ __global__ void __launch_bounds__(256) k1_row_amax(const float* __restrict__ X, 
 
 // Per-tensor mode step 2: global amax -> one lambda, broadcast to all rows.
 __global__ void __launch_bounds__(1024) k1_tensor_scale(const float* __restrict__ row_amax, int rows, int qmax,
-                                                        float* __restrict__ lam_rows, float* __restrict__ lam_scalar) {
+                                                        float* __restrict__ lam_rows, float* __restrict__ inv_rows,
+                                                        float* __restrict__ lam_scalar) {
   __shared__ float red[32];
   __shared__ float lam_s;
   float m = 0.f;
@@ -164,15 +168,19 @@ __global__ void __launch_bounds__(1024) k1_tensor_scale(const float* __restrict_
     lam_scalar[0] = lam_s;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < rows; i += blockDim.x) lam_rows[i] = lam_s;
+  const float inv_s = __frcp_rn(lam_s);
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+    lam_rows[i] = lam_s;
+    inv_rows[i] = inv_s;
+  }
 }
 
 // Generic path for very long rows (K > 32768): two passes over the row (the
 // second one mostly from L2).  Same rounding arithmetic.
 __global__ void __launch_bounds__(256) k1_quantize_long(const float* __restrict__ X, int64_t ldx, int rows, int K,
                                                         int Kp, int qmax, int mode, int8_t* __restrict__ codes,
-                                                        float* __restrict__ lam_out, const float* __restrict__ lam_in,
-                                                        int* __restrict__ err_flag) {
+                                                        float* __restrict__ lam_out, float* __restrict__ inv_out,
+                                                        const float* __restrict__ lam_in, int* __restrict__ err_flag) {
   __shared__ float red[8];
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
     const float* xr = X + row * ldx;
@@ -195,7 +203,10 @@ __global__ void __launch_bounds__(256) k1_quantize_long(const float* __restrict_
       for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
       __syncthreads();
       lam = (m == 0.f) ? 1.f : __fdiv_rn(static_cast<float>(qmax), m);
-      if (threadIdx.x == 0) lam_out[row] = lam;
+      if (threadIdx.x == 0) {
+        lam_out[row] = lam;
+        inv_out[row] = __frcp_rn(lam);
+      }
     }
     int8_t* crow = codes + row * (int64_t)Kp;
     for (int c = threadIdx.x; c < Kp; c += 256) crow[c] = (c < K) ? code_of(lam, xr[c], mode, qmax) : (int8_t)0;
@@ -210,7 +221,7 @@ static void launch_k1_t(const QuantArgs& a, bool vec, bool fixed, cudaStream_t s
   if (grid < 1) grid = 1;
 #define K1_LAUNCH(V, F)                                                                                  \
   k1_quantize<TPR, VPT, V, F><<<grid, 256, 0, st>>>(a.X, a.ldx, a.rows, a.K, a.Kp, a.qmax, a.mode, a.codes, \
-                                                    a.lam, a.lam_fixed, a.err_flag)
+                                                    a.lam, a.inv_lam, a.lam_fixed, a.err_flag)
   if (vec) {
     if (fixed) K1_LAUNCH(true, true); else K1_LAUNCH(true, false);
   } else {
@@ -237,17 +248,17 @@ void launch_quantize(const QuantArgs& a, cudaStream_t st) {
   else {
     int grid = a.rows < 148 * 16 ? (int)a.rows : 148 * 16;
     k1_quantize_long<<<grid, 256, 0, st>>>(a.X, a.ldx, a.rows, a.K, a.Kp, a.qmax, a.mode, a.codes, a.lam,
-                                           a.lam_fixed, a.err_flag); ++launch_counter();
+                                           a.inv_lam, a.lam_fixed, a.err_flag); ++launch_counter();
   }
 }
 
 void launch_tensor_scale(const float* X, int64_t ldx, int64_t rows, int K, int qmax, float* row_amax, float* lam_rows,
-                         float* lam_scalar, int* err_flag, cudaStream_t st) {
+                         float* inv_rows, float* lam_scalar, int* err_flag, cudaStream_t st) {
   if (rows > 0) {
     int grid = rows < 148 * 16 ? (int)rows : 148 * 16;
     k1_row_amax<<<grid, 256, 0, st>>>(X, ldx, (int)rows, K, row_amax, err_flag); ++launch_counter();
   }
-  k1_tensor_scale<<<1, 1024, 0, st>>>(row_amax, (int)rows, qmax, lam_rows, lam_scalar); ++launch_counter();
+  k1_tensor_scale<<<1, 1024, 0, st>>>(row_amax, (int)rows, qmax, lam_rows, inv_rows, lam_scalar); ++launch_counter();
 }
 
 }  // namespace lrqmm

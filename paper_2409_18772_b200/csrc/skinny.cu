@@ -46,4 +46,15 @@ void launch_apply_small(const float* IN1, const float* S1, const float* IN2, con
                                                                         col0); ++launch_counter();
 }
 
+__global__ void k_recip(const float* __restrict__ in, float* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __frcp_rn(in[i]);
+}
+
+void launch_recip(const float* in, float* out, int64_t n, cudaStream_t st) {
+  if (n == 0) return;
+  k_recip<<<clamp_grid((n + 255) / 256), 256, 0, st>>>(in, out, n);
+  ++launch_counter();
+}
+
 }  // namespace lrqmm

@@ -22,6 +22,8 @@
 // order by k_reduce_splits_tc (deterministic, no float atomics).
 #include <cuda.h>
 
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -40,13 +42,18 @@ constexpr int BK = 32;   // reduction elements per k-block
 constexpr int OPST = LRQMM_OPST;  // operand stages
 constexpr int kATile = BM * BK * 4;    // 16 KB
 constexpr int kRawTile = BM * BK * 4;  // 16 KB
-template <int NA, bool kDual>
+template <int kMode, int NA, bool kDual>
 struct Cfg {
   static constexpr int WN = 32 * NA;
-  static constexpr int kBTile = BK * WN * 4;
+  static constexpr int kBTile = BK * WN * 4;  // operand B tile (hi or lo)
   static constexpr int kStage = (kDual ? 3 : 2) * kATile + (kDual ? 4 : 2) * kBTile;
-  static constexpr int kRawSt = (4 * kRawTile + OPST * kStage <= 200 * 1024) ? 4 : 3;
-  static constexpr int kSmem = kRawSt * kRawTile + OPST * kStage + 256 + 1024;
+  // raw slot: X tile | P1 tile [BK][WN] | P2 tile | (COL) lambda[BK], 1/lambda[BK]
+  static constexpr int kRawP = BK * WN * 4;
+  static constexpr int kRawBytes = kRawTile + (kDual ? 2 : 1) * kRawP + (kMode == 1 ? 2 * BK * 4 : 0);
+  static constexpr int kRawSlot = (kRawBytes + 1023) / 1024 * 1024;
+  static constexpr int kRawSt = (4 * kRawSlot + OPST * kStage <= 216 * 1024) ? 4
+                                : ((3 * kRawSlot + OPST * kStage <= 216 * 1024) ? 3 : 2);
+  static constexpr int kSmem = kRawSt * kRawSlot + OPST * kStage + 256 + 1024;
   static constexpr int kAccCols = (kDual ? 2 : 1) * WN;  // per accumulator buffer
   static constexpr uint32_t kTmemCols =
       2 * kAccCols <= 32 ? 32 : (2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : 256));
@@ -59,6 +66,7 @@ struct TcArgs {
   int64_t rows;
   int K;
   const float* lam;
+  const float* inv_lam;
   int qmax, mode;
   const float* P1;  // ROW: K x W ; COL: rows x W
   const float* P2;  // ROW dual: K x W
@@ -133,19 +141,23 @@ LRQMM_DEV uint32_t off_k(int mn, int k) {
   return (uint32_t)((mn >> 3) * 1024 + row * 128 + ((chunk ^ row) << 4) + ((k & 3) << 2));
 }
 
+struct TcMaps {
+  CUtensorMap x, p1, p2, lam, inv;
+};
+
 template <int kMode, int NA, bool kDual>
-__global__ void __launch_bounds__(tcp::kThreads, 1)
-    k_tc_proj(const __grid_constant__ CUtensorMap xmap, TcArgs a) {
+__global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_constant__ TcMaps maps, TcArgs a) {
   using namespace tcp;
-  using C = Cfg<NA, kDual>;
+  using C = Cfg<kMode, NA, kDual>;
   constexpr int WN = C::WN;
   constexpr int kBTile = C::kBTile;
   constexpr int kStage = C::kStage;
   constexpr int RST = C::kRawSt;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sRaw = smem;                 // RST x 16 KB raw X tiles
-  uint8_t* sOp = smem + RST * kRawTile;  // OPST x kStage operand tiles
+  constexpr int kRawSlot = C::kRawSlot;
+  uint8_t* sRaw = smem;                  // RST raw slots (X, P, lambda tiles by TMA)
+  uint8_t* sOp = smem + RST * kRawSlot;  // OPST x kStage operand tiles
   uint64_t* bars = reinterpret_cast<uint64_t*>(sOp + OPST * kStage);
   uint64_t* rfull = bars;            // RST
   uint64_t* rempty = bars + RST;     // RST
@@ -191,7 +203,9 @@ __global__ void __launch_bounds__(tcp::kThreads, 1)
   if (warp == kTmaWarp) {
     // --------------------------------------------------------- TMA: raw X tiles
     if (lane == 0) {
-      tma_prefetch_desc(&xmap);
+      tma_prefetch_desc(&maps.x);
+      tma_prefetch_desc(&maps.p1);
+      if (kDual) tma_prefetch_desc(&maps.p2);
       int it = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         int blk, split, nkb;
@@ -200,10 +214,17 @@ __global__ void __launch_bounds__(tcp::kThreads, 1)
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % RST;
           mbar_wait(&rempty[s], ((it / RST) & 1) ^ 1);
-          mbar_arrive_expect_tx(&rfull[s], kRawTile);
+          uint8_t* slot = sRaw + s * kRawSlot;
+          mbar_arrive_expect_tx(&rfull[s], C::kRawBytes);
           const int k0 = (int)(r0 + (int64_t)kb * BK);
-          if (kMode == 0) tma_load_2d(sRaw + s * kRawTile, &xmap, &rfull[s], k0, blk * BM);
-          else tma_load_2d(sRaw + s * kRawTile, &xmap, &rfull[s], blk * BM, k0);
+          if (kMode == 0) tma_load_2d(slot, &maps.x, &rfull[s], k0, blk * BM);
+          else tma_load_2d(slot, &maps.x, &rfull[s], blk * BM, k0);
+          tma_load_2d(slot + kRawTile, &maps.p1, &rfull[s], 0, k0);
+          if (kDual) tma_load_2d(slot + kRawTile + C::kRawP, &maps.p2, &rfull[s], 0, k0);
+          if (kMode == 1) {
+            tma_load_1d(slot + kRawTile + C::kRawP, &maps.lam, &rfull[s], k0);
+            tma_load_1d(slot + kRawTile + C::kRawP + BK * 4, &maps.inv, &rfull[s], k0);
+          }
         }
       }
     }
@@ -223,54 +244,19 @@ __global__ void __launch_bounds__(tcp::kThreads, 1)
         for (int q = 0; q < 4; ++q) {
           const int64_t row = o0 + ((tid + 256 * q) >> 3);
           lam_r[q] = row < a.rows ? __ldg(a.lam + row) : 1.f;
-          inv_r[q] = __frcp_rn(lam_r[q]);
+          inv_r[q] = row < a.rows ? __ldg(a.inv_lam + row) : 1.f;
         }
       }
+      (void)r1;
       for (int kb = 0; kb < nkb; ++kb, ++it) {
         const int rs = it % RST;
         const int os = it % OPST;
-        const int64_t k0 = r0 + (int64_t)kb * BK;
-        // B tile values (P rows [k0, k0+BK) x WN) from L2, before any waits
         constexpr int kPB4 = BK * WN / 4;
         constexpr int kPBper = (kPB4 + kProd - 1) / kProd;
-        float4 pb1[kPBper], pb2[kPBper];
-#pragma unroll
-        for (int q = 0; q < kPBper; ++q) {
-          const int e = tid + kProd * q;
-          pb1[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-          pb2[q] = pb1[q];
-          if (e < kPB4) {
-            const int pj = e / (WN / 4), pc = (e % (WN / 4)) * 4;
-            const int64_t k = k0 + pj;
-            if (k < r1) {
-              const float* p1 = a.P1 + k * a.W;
-              if (pc + 0 < a.W) pb1[q].x = __ldg(p1 + pc + 0);
-              if (pc + 1 < a.W) pb1[q].y = __ldg(p1 + pc + 1);
-              if (pc + 2 < a.W) pb1[q].z = __ldg(p1 + pc + 2);
-              if (pc + 3 < a.W) pb1[q].w = __ldg(p1 + pc + 3);
-              if (kDual) {
-                const float* p2 = a.P2 + k * a.W;
-                if (pc + 0 < a.W) pb2[q].x = __ldg(p2 + pc + 0);
-                if (pc + 1 < a.W) pb2[q].y = __ldg(p2 + pc + 1);
-                if (pc + 2 < a.W) pb2[q].z = __ldg(p2 + pc + 2);
-                if (pc + 3 < a.W) pb2[q].w = __ldg(p2 + pc + 3);
-              }
-            }
-          }
-        }
-        float lam_c[4], inv_c[4];
-        if (kMode == 1) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int64_t row = k0 + ((tid + 256 * q) >> 5);
-            lam_c[q] = row < r1 ? __ldg(a.lam + row) : 1.f;
-            inv_c[q] = __frcp_rn(lam_c[q]);
-          }
-        }
-        // raw X tile -> registers, release the raw slot
+        // raw slot (X, P, lambda) -> registers, then release the slot
         mbar_wait(&rfull[rs], (it / RST) & 1);
+        const uint8_t* raw = sRaw + rs * kRawSlot;
         float4 xv[4];
-        const uint8_t* raw = sRaw + rs * kRawTile;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int f = tid + 256 * q;
@@ -278,9 +264,27 @@ __global__ void __launch_bounds__(tcp::kThreads, 1)
               kMode == 0 ? (uint32_t)((f >> 3) * 128 + (f & 7) * 16) : (uint32_t)((f >> 5) * 512 + (f & 31) * 16);
           xv[q] = *reinterpret_cast<const float4*>(raw + ro);
         }
+        float4 pb1[kPBper], pb2[kPBper];
+#pragma unroll
+        for (int q = 0; q < kPBper; ++q) {
+          const int e = tid + kProd * q;
+          if (e < kPB4) {
+            pb1[q] = *reinterpret_cast<const float4*>(raw + kRawTile + e * 16);
+            if (kDual) pb2[q] = *reinterpret_cast<const float4*>(raw + kRawTile + C::kRawP + e * 16);
+          }
+        }
+        float lam_c[4], inv_c[4];
+        if (kMode == 1) {
+          const float* sl = reinterpret_cast<const float*>(raw + kRawTile + C::kRawP);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            lam_c[q] = sl[(tid + 256 * q) >> 5];
+            inv_c[q] = sl[BK + ((tid + 256 * q) >> 5)];
+          }
+        }
         // The slot is refilled by TMA (async proxy) after this release: order our
         // generic-proxy reads before it (without this fence rows were observed to be
-        // overwritten before they were read, ~40% of launches on B200).
+        // overwritten before they were read on B200).
         fence_proxy_async_smem();
         mbar_arrive(&rempty[rs]);
         // operand stage
@@ -311,6 +315,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1)
             }
           }
         }
+        const bool floor_mode = a.mode == kRoundFloor;  // uniform: LRQMM's rounding gets the short path
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int f = tid + 256 * q;
@@ -318,10 +323,25 @@ __global__ void __launch_bounds__(tcp::kThreads, 1)
           const float il = kMode == 0 ? inv_r[q] : inv_c[q];
           const float xs[4] = {xv[q].x, xv[q].y, xv[q].z, xv[q].w};
           float r[4], c[4];
+          if (floor_mode) {
+            const float qf = static_cast<float>(a.qmax);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            c[e] = codef(l, xs[e], a.mode, a.qmax);
-            r[e] = __fmul_rn(__fmaf_rn(l, xs[e], -c[e]), il);
+            for (int e = 0; e < 4; ++e) {
+              // floor of the exact product: t = RN(l*x - floor(RN(l*x))) < 0 iff the product
+              // rounded up onto an integer; the x < 0 underflow case decides p == 0
+              float cc = floorf(__fmul_rn(l, xs[e]));
+              float t = __fmaf_rn(l, xs[e], -cc);
+              cc = (t < 0.f || (t == 0.f && cc == 0.f && xs[e] < 0.f)) ? cc - 1.f : cc;
+              cc = fminf(fmaxf(cc, -qf), qf);
+              c[e] = cc;
+              r[e] = __fmul_rn(__fmaf_rn(l, xs[e], -cc), il);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              c[e] = codef(l, xs[e], a.mode, a.qmax);
+              r[e] = __fmul_rn(__fmaf_rn(l, xs[e], -c[e]), il);
+            }
           }
           const uint32_t off = kMode == 0 ? off_k(f >> 3, (f & 7) * 4) : off_mn((f & 31) * 4, f >> 5, 4);
           const float4 h = make_float4(tf32_hi(r[0]), tf32_hi(r[1]), tf32_hi(r[2]), tf32_hi(r[3]));
@@ -396,7 +416,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1)
       const int64_t orow = (int64_t)blk * BM + quad * 32 + lane;
       const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + acc * C::kAccCols;
       float inv_row = 1.f;
-      if (kDual) inv_row = orow < a.rows ? __frcp_rn(__ldg(a.lam + orow)) : 1.f;
+      if (kDual) inv_row = orow < a.rows ? __ldg(a.inv_lam + orow) : 1.f;
       float* out1 = a.out1 + (int64_t)split * a.nout * a.W;
       float* out2 = kDual ? a.out2 + (int64_t)split * a.nout * a.W : nullptr;
 #pragma unroll
@@ -440,7 +460,7 @@ __global__ void k_reduce_splits_tc(const float* __restrict__ part, int nsplit, i
 template <int kMode, int NA, bool kDual>
 static void run_tc(const TcArgs& a0, float* OUT1, float* OUT2, float* partial, int64_t pe, cudaStream_t st) {
   using namespace tcp;
-  using C = Cfg<NA, kDual>;
+  using C = Cfg<kMode, NA, kDual>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_tc_proj<kMode, NA, kDual>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
@@ -466,12 +486,20 @@ static void run_tc(const TcArgs& a0, float* OUT1, float* OUT2, float* partial, i
   a.nsplit = (int)ns;
   a.out1 = ns == 1 ? OUT1 : partial;
   a.out2 = ns == 1 ? OUT2 : partial + ns * a.nout * a.W;
-  alignas(64) CUtensorMap xmap;
-  if (kMode == 0) encode_map_2d(&xmap, 1, a.X, (uint64_t)a.K, (uint64_t)a.rows, (uint64_t)a.ldx * 4, BK, BM);
-  else encode_map_2d(&xmap, 1, a.X, (uint64_t)a.K, (uint64_t)a.rows, (uint64_t)a.ldx * 4, BM, BK);
+  alignas(64) TcMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  if (kMode == 0) encode_map_2d(&maps.x, 1, a.X, (uint64_t)a.K, (uint64_t)a.rows, (uint64_t)a.ldx * 4, BK, BM);
+  else encode_map_2d(&maps.x, 1, a.X, (uint64_t)a.K, (uint64_t)a.rows, (uint64_t)a.ldx * 4, BM, BK);
+  // P tiles [BK rows][WN cols]; columns >= W and rows past the end are zero-filled by TMA
+  encode_map_2d(&maps.p1, 1, a.P1, (uint64_t)a.W, (uint64_t)rlen, (uint64_t)a.W * 4, C::WN, BK);
+  if (kDual) encode_map_2d(&maps.p2, 1, a.P2, (uint64_t)a.W, (uint64_t)rlen, (uint64_t)a.W * 4, C::WN, BK);
+  if (kMode == 1) {
+    encode_map_1d_f32(&maps.lam, a.lam, (uint64_t)a.rows, BK);
+    encode_map_1d_f32(&maps.inv, a.inv_lam, (uint64_t)a.rows, BK);
+  }
   const int64_t units = nblk * ns;
   const int grid = (int)(units < nsm ? units : nsm);
-  k_tc_proj<kMode, NA, kDual><<<grid, kThreads, C::kSmem, st>>>(xmap, a);
+  k_tc_proj<kMode, NA, kDual><<<grid, kThreads, C::kSmem, st>>>(maps, a);
   ++launch_counter();
   if (ns > 1) {
     const int64_t n = a.nout * a.W;
@@ -492,6 +520,7 @@ static TcArgs make_args(const SideView& s, const float* P1, const float* P2, int
   a.rows = s.rows;
   a.K = s.K;
   a.lam = s.lam;
+  a.inv_lam = s.inv_lam;
   a.qmax = s.qmax;
   a.mode = s.mode;
   a.P1 = P1;
