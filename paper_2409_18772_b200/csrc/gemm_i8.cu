@@ -47,8 +47,8 @@ struct G6Params {
   int num_kb;
   int num_m, num_n;
   int epi;
-  const float* lam_a;
-  const float* lam_b;
+  const float* inv_a;  // RN(1/lambda_A)
+  const float* inv_b;  // RN(1/lambda_B)
   const float* LA;
   const float* LB;
   float alpha, beta;
@@ -75,8 +75,7 @@ LRQMM_DEV void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(g6::kEpiThreads)
 // epilogue code stays resident in the instruction cache.
 template <int kR2>
 LRQMM_DEV void epilogue_group(const G6Params& p, const uint32_t (&acc)[8], int64_t row, int col0, int cl0,
-                              float sa, const float (&la)[kR2 > 0 ? kR2 : 1], const float* __restrict__ sLB,
-                              const float* __restrict__ sSB) {
+                              float sa, const float (&la)[kR2 > 0 ? kR2 : 1], uint32_t sLB, uint32_t sSB) {
   if (row >= p.M || col0 >= p.N) return;
   const bool full = p.vec_ok && col0 + 8 <= p.N;
   if (p.epi == 0) {
@@ -93,13 +92,14 @@ LRQMM_DEV void epilogue_group(const G6Params& p, const uint32_t (&acc)[8], int64
   // v = alpha * (acc / (lambda_a lambda_b) + L_A[row] . L_B[col]);  sa, la carry alpha
   float v[8];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) v[c] = __fmul_rn(static_cast<float>(static_cast<int32_t>(acc[c])), __fmul_rn(sa, sSB[cl0 + c]));
+  for (int c = 0; c < 8; ++c)
+    v[c] = __fmul_rn(static_cast<float>(static_cast<int32_t>(acc[c])), __fmul_rn(sa, lds32(sSB + 4 * (cl0 + c))));
   if constexpr (kR2 > 0) {
 #pragma unroll
     for (int l = 0; l < kR2; l += 4) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        const float4 b = *reinterpret_cast<const float4*>(sLB + (cl0 + c) * kR2 + l);
+        const float4 b = lds128(sLB + 4 * ((cl0 + c) * kR2 + l));
         v[c] = fmaf(la[l + 0], b.x, v[c]);
         v[c] = fmaf(la[l + 1], b.y, v[c]);
         v[c] = fmaf(la[l + 2], b.z, v[c]);
@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(g6::kThreads, 1)
   uint8_t* sB = smem + STAGES * kABytes;
   float* sLB = reinterpret_cast<float*>(smem + STAGES * kStageBytes);  // BN x kR2
   float* sSB = sLB + BN * kR2;                                           // BN : 1/lambda_b
+  const uint32_t sLBa = smem_u32(sLB), sSBa = smem_u32(sSB);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sSB + BN);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
@@ -241,17 +242,18 @@ __global__ void __launch_bounds__(g6::kThreads, 1)
         epi_bar();  // previous tile's readers are done
         for (int j = et; j < BN; j += kEpiThreads) {
           const int col = n0 + j;
-          sSB[j] = col < p.N ? __frcp_rn(__ldg(p.lam_b + col)) : 0.f;
+          const float v = col < p.N ? __ldg(p.inv_b + col) : 0.f;
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(sSBa + 4 * j), "f"(v) : "memory");
         }
         if constexpr (kR2 > 0) {
           const float4* src = reinterpret_cast<const float4*>(p.LB + (int64_t)n0 * kR2);
-          float4* dst = reinterpret_cast<float4*>(sLB);
           const int total4 = BN * kR2 / 4;
           const int valid4 = (int)((p.N - n0 < BN ? p.N - n0 : (int64_t)BN) * kR2 / 4);
-          for (int e = et; e < total4; e += kEpiThreads) dst[e] = e < valid4 ? __ldg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int e = et; e < total4; e += kEpiThreads)
+            sts128(sLBa + 16 * e, e < valid4 ? __ldg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f));
         }
         if (row < p.M) {
-          sa = p.alpha * __frcp_rn(p.lam_a[row]);
+          sa = p.alpha * __ldg(p.inv_a + row);
           if constexpr (kR2 > 0) {
             const float4* lr = reinterpret_cast<const float4*>(p.LA + row * kR2);
 #pragma unroll
@@ -273,10 +275,10 @@ __global__ void __launch_bounds__(g6::kThreads, 1)
       for (int g = 0; g < BN / 8; g += 2) {
         tmem_ld_wait();
         tmem_ld_32x32b_x8(t_row + (g + 1) * 8, rb);
-        epilogue_group<kR2>(p, ra, row, n0 + g * 8, g * 8, sa, la, sLB, sSB);
+        epilogue_group<kR2>(p, ra, row, n0 + g * 8, g * 8, sa, la, sLBa, sSBa);
         tmem_ld_wait();
         if (g + 2 < BN / 8) tmem_ld_32x32b_x8(t_row + (g + 2) * 8, ra);
-        epilogue_group<kR2>(p, rb, row, n0 + (g + 1) * 8, (g + 1) * 8, sa, la, sLB, sSB);
+        epilogue_group<kR2>(p, rb, row, n0 + (g + 1) * 8, (g + 1) * 8, sa, la, sLBa, sSBa);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -374,8 +376,8 @@ void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStre
   p.num_m = (int)((g.M + g6::BM - 1) / g6::BM);
   p.num_n = (int)((g.N + g6::BN - 1) / g6::BN);
   p.epi = g.epi;
-  p.lam_a = g.lam_a;
-  p.lam_b = g.lam_b;
+  p.inv_a = g.inv_a;
+  p.inv_b = g.inv_b;
   p.LA = g.LA;
   p.LB = g.LB;
   p.alpha = g.alpha;

@@ -93,8 +93,8 @@ struct GemmArgs {
   int Kp;
   // epilogue
   int epi;               // 0: int32 out; 1: fp32 LRQMM/DQ out
-  const float* lam_a;    // M
-  const float* lam_b;    // N
+  const float* inv_a;    // M: RN(1/lambda_A)
+  const float* inv_b;    // N: RN(1/lambda_B)
   const float* LA;       // M x R2 (may be null if R2 == 0)
   const float* LB;       // N x R2
   int R2;                // padded correction width roundup(2r, 8) <= 64

@@ -452,8 +452,8 @@ static lrqmm_status_t run_gemm(lrqmm_handle_t h, int epi, float alpha, float bet
   g.N = h->cfg.n;
   g.Kp = h->Kp;
   g.epi = epi;
-  g.lam_a = h->s[0].lam;
-  g.lam_b = h->s[1].lam;
+  g.inv_a = h->s[0].inv_lam;
+  g.inv_b = h->s[1].inv_lam;
   g.LA = h->LA;
   g.LB = h->LB;
   g.R2 = h->r > 0 ? h->R2 : 0;

@@ -255,31 +255,31 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
         constexpr int kPBper = (kPB4 + kProd - 1) / kProd;
         // raw slot (X, P, lambda) -> registers, then release the slot
         mbar_wait(&rfull[rs], (it / RST) & 1);
-        const uint8_t* raw = sRaw + rs * kRawSlot;
+        const uint32_t raw = smem_u32(sRaw) + rs * kRawSlot;
         float4 xv[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int f = tid + 256 * q;
           const uint32_t ro =
               kMode == 0 ? (uint32_t)((f >> 3) * 128 + (f & 7) * 16) : (uint32_t)((f >> 5) * 512 + (f & 31) * 16);
-          xv[q] = *reinterpret_cast<const float4*>(raw + ro);
+          xv[q] = lds128(raw + ro);
         }
         float4 pb1[kPBper], pb2[kPBper];
 #pragma unroll
         for (int q = 0; q < kPBper; ++q) {
           const int e = tid + kProd * q;
           if (e < kPB4) {
-            pb1[q] = *reinterpret_cast<const float4*>(raw + kRawTile + e * 16);
-            if (kDual) pb2[q] = *reinterpret_cast<const float4*>(raw + kRawTile + C::kRawP + e * 16);
+            pb1[q] = lds128(raw + kRawTile + e * 16);
+            if (kDual) pb2[q] = lds128(raw + kRawTile + C::kRawP + e * 16);
           }
         }
         float lam_c[4], inv_c[4];
         if (kMode == 1) {
-          const float* sl = reinterpret_cast<const float*>(raw + kRawTile + C::kRawP);
+          const uint32_t sl = raw + kRawTile + C::kRawP;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            lam_c[q] = sl[(tid + 256 * q) >> 5];
-            inv_c[q] = sl[BK + ((tid + 256 * q) >> 5)];
+            lam_c[q] = lds32(sl + 4 * ((tid + 256 * q) >> 5));
+            inv_c[q] = lds32(sl + 4 * (BK + ((tid + 256 * q) >> 5)));
           }
         }
         // The slot is refilled by TMA (async proxy) after this release: order our
@@ -289,14 +289,14 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
         mbar_arrive(&rempty[rs]);
         // operand stage
         mbar_wait(&oempty[os], ((it / OPST) & 1) ^ 1);
-        uint8_t* st = sOp + os * kStage;
-        uint8_t* sAhi = st;
-        uint8_t* sAlo = st + kATile;
-        uint8_t* sAc = st + 2 * kATile;
-        uint8_t* sBhi = st + (kDual ? 3 : 2) * kATile;
-        uint8_t* sBlo = sBhi + kBTile;
-        uint8_t* sB2hi = sBlo + kBTile;
-        uint8_t* sB2lo = sB2hi + kBTile;
+        const uint32_t st = smem_u32(sOp) + os * kStage;
+        const uint32_t sAhi = st;
+        const uint32_t sAlo = st + kATile;
+        const uint32_t sAc = st + 2 * kATile;
+        const uint32_t sBhi = st + (kDual ? 3 : 2) * kATile;
+        const uint32_t sBlo = sBhi + kBTile;
+        const uint32_t sB2hi = sBlo + kBTile;
+        const uint32_t sB2lo = sB2hi + kBTile;
 #pragma unroll
         for (int q = 0; q < kPBper; ++q) {
           const int e = tid + kProd * q;
@@ -304,14 +304,12 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
             const int pj = e / (WN / 4), pc = (e % (WN / 4)) * 4;
             const uint32_t off = off_mn(pc, pj, NA);
             const float4 h1 = make_float4(tf32_hi(pb1[q].x), tf32_hi(pb1[q].y), tf32_hi(pb1[q].z), tf32_hi(pb1[q].w));
-            *reinterpret_cast<float4*>(sBhi + off) = h1;
-            *reinterpret_cast<float4*>(sBlo + off) =
-                make_float4(pb1[q].x - h1.x, pb1[q].y - h1.y, pb1[q].z - h1.z, pb1[q].w - h1.w);
+            sts128(sBhi + off, h1);
+            sts128(sBlo + off, make_float4(pb1[q].x - h1.x, pb1[q].y - h1.y, pb1[q].z - h1.z, pb1[q].w - h1.w));
             if (kDual) {
               const float4 h2 = make_float4(tf32_hi(pb2[q].x), tf32_hi(pb2[q].y), tf32_hi(pb2[q].z), tf32_hi(pb2[q].w));
-              *reinterpret_cast<float4*>(sB2hi + off) = h2;
-              *reinterpret_cast<float4*>(sB2lo + off) =
-                  make_float4(pb2[q].x - h2.x, pb2[q].y - h2.y, pb2[q].z - h2.z, pb2[q].w - h2.w);
+              sts128(sB2hi + off, h2);
+              sts128(sB2lo + off, make_float4(pb2[q].x - h2.x, pb2[q].y - h2.y, pb2[q].z - h2.z, pb2[q].w - h2.w));
             }
           }
         }
@@ -345,9 +343,9 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
           }
           const uint32_t off = kMode == 0 ? off_k(f >> 3, (f & 7) * 4) : off_mn((f & 31) * 4, f >> 5, 4);
           const float4 h = make_float4(tf32_hi(r[0]), tf32_hi(r[1]), tf32_hi(r[2]), tf32_hi(r[3]));
-          *reinterpret_cast<float4*>(sAhi + off) = h;
-          *reinterpret_cast<float4*>(sAlo + off) = make_float4(r[0] - h.x, r[1] - h.y, r[2] - h.z, r[3] - h.w);
-          if (kDual) *reinterpret_cast<float4*>(sAc + off) = make_float4(c[0], c[1], c[2], c[3]);
+          sts128(sAhi + off, h);
+          sts128(sAlo + off, make_float4(r[0] - h.x, r[1] - h.y, r[2] - h.z, r[3] - h.w));
+          if (kDual) sts128(sAc + off, make_float4(c[0], c[1], c[2], c[3]));
         }
         fence_proxy_async_smem();
         mbar_arrive(&ofull[os]);
