@@ -30,10 +30,14 @@
 namespace lrqmm {
 
 namespace tcp {
-constexpr int kProd = 256;
-constexpr int kThreads = 448;
-constexpr int kMmaWarp = 12;
-constexpr int kTmaWarp = 13;
+constexpr int BM_ = 128;
+constexpr int kProd = 512;              // 16 producer warps
+constexpr int kProdWarps = kProd / 32;
+constexpr int kEpiWarp0 = kProdWarps;    // 4 epilogue warps
+constexpr int kMmaWarp = kProdWarps + 4;
+constexpr int kTmaWarp = kProdWarps + 5;
+constexpr int kThreads = (kProdWarps + 6) * 32;  // 704
+constexpr int kPer = BM_ * 32 / 4 / kProd;       // float4 of X per producer thread per k-block
 constexpr int BM = 128;  // output rows (ROW) / output cols (COL) per unit
 constexpr int BK = 32;   // reduction elements per k-block
 #ifndef LRQMM_OPST
@@ -174,10 +178,10 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   if (tid == 0) {
     for (int s = 0; s < RST; ++s) {
       mbar_init(&rfull[s], 1);
-      mbar_init(&rempty[s], kProd);
+      mbar_init(&rempty[s], kProdWarps);  // one elected arrival per producer warp
     }
     for (int s = 0; s < OPST; ++s) {
-      mbar_init(&ofull[s], kProd);
+      mbar_init(&ofull[s], kProdWarps);
       mbar_init(&oempty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       }
     }
     __syncwarp();
-  } else if (warp < 8) {
+  } else if (warp < kProdWarps) {
     // --------------------------------------------------------------- producers
     int it = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -238,13 +242,12 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       unit_range(u, blk, split, r0, nkb);
       const int64_t o0 = (int64_t)blk * BM;
       const int64_t r1 = r0 + a.chunk < r_len ? r0 + a.chunk : r_len;
-      float lam_r[4], inv_r[4];
+      float lam_r[kPer];
       if (kMode == 0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int64_t row = o0 + ((tid + 256 * q) >> 3);
+        for (int q = 0; q < kPer; ++q) {
+          const int64_t row = o0 + ((tid + kProd * q) >> 3);
           lam_r[q] = row < a.rows ? __ldg(a.lam + row) : 1.f;
-          inv_r[q] = row < a.rows ? __ldg(a.inv_lam + row) : 1.f;
         }
       }
       (void)r1;
@@ -256,10 +259,10 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
         // raw slot (X, P, lambda) -> registers, then release the slot
         mbar_wait(&rfull[rs], (it / RST) & 1);
         const uint32_t raw = smem_u32(sRaw) + rs * kRawSlot;
-        float4 xv[4];
+        float4 xv[kPer];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int f = tid + 256 * q;
+        for (int q = 0; q < kPer; ++q) {
+          const int f = tid + kProd * q;
           const uint32_t ro =
               kMode == 0 ? (uint32_t)((f >> 3) * 128 + (f & 7) * 16) : (uint32_t)((f >> 5) * 512 + (f & 31) * 16);
           xv[q] = lds128(raw + ro);
@@ -271,22 +274,23 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
           if (e < kPB4) {
             pb1[q] = lds128(raw + kRawTile + e * 16);
             if (kDual) pb2[q] = lds128(raw + kRawTile + C::kRawP + e * 16);
+            if (kMode == 1) {  // COL: R^T Q0 = U^T diag(1/lambda) Q0 -> scale B rows by 1/lambda_i
+              const float il = lds32(raw + kRawTile + C::kRawP + 4 * (BK + e / (WN / 4)));
+              pb1[q] = make_float4(pb1[q].x * il, pb1[q].y * il, pb1[q].z * il, pb1[q].w * il);
+            }
           }
         }
-        float lam_c[4], inv_c[4];
+        float lam_c[kPer];
         if (kMode == 1) {
-          const uint32_t sl = raw + kRawTile + C::kRawP;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            lam_c[q] = lds32(sl + 4 * ((tid + 256 * q) >> 5));
-            inv_c[q] = lds32(sl + 4 * (BK + ((tid + 256 * q) >> 5)));
-          }
+          for (int q = 0; q < kPer; ++q) lam_c[q] = lds32(raw + kRawTile + C::kRawP + 4 * ((tid + kProd * q) >> 5));
         }
         // The slot is refilled by TMA (async proxy) after this release: order our
         // generic-proxy reads before it (without this fence rows were observed to be
         // overwritten before they were read on B200).
         fence_proxy_async_smem();
-        mbar_arrive(&rempty[rs]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rempty[rs]);
         // operand stage
         mbar_wait(&oempty[os], ((it / OPST) & 1) ^ 1);
         const uint32_t st = smem_u32(sOp) + os * kStage;
@@ -313,42 +317,45 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
             }
           }
         }
-        const bool floor_mode = a.mode == kRoundFloor;  // uniform: LRQMM's rounding gets the short path
+        // A operand: the residual fraction u = lambda x - code (R = u / lambda; 1/lambda is applied
+        // to the accumulator rows (ROW) or folded into the B rows (COL))
+        const bool floor_mode = a.mode == kRoundFloor;  // uniform: LRQMM's rounding takes the short path
+        const float qf = static_cast<float>(a.qmax);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int f = tid + 256 * q;
+        for (int q = 0; q < kPer; ++q) {
+          const int f = tid + kProd * q;
           const float l = kMode == 0 ? lam_r[q] : lam_c[q];
-          const float il = kMode == 0 ? inv_r[q] : inv_c[q];
           const float xs[4] = {xv[q].x, xv[q].y, xv[q].z, xv[q].w};
-          float r[4], c[4];
+          float u[4], c[4];
           if (floor_mode) {
-            const float qf = static_cast<float>(a.qmax);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              // floor of the exact product: t = RN(l*x - floor(RN(l*x))) < 0 iff the product
-              // rounded up onto an integer; the x < 0 underflow case decides p == 0
+              // floor of the exact product: t = RN(l*x - floor(RN(l*x))) < 0 iff the product rounded up
+              // onto an integer; the x < 0 underflow-to-zero case is decided by the sign of x.  With
+              // lambda <= qmax/amax(1+2^-24) only the lower clamp can bind.
               float cc = floorf(__fmul_rn(l, xs[e]));
-              float t = __fmaf_rn(l, xs[e], -cc);
+              const float t = __fmaf_rn(l, xs[e], -cc);
               cc = (t < 0.f || (t == 0.f && cc == 0.f && xs[e] < 0.f)) ? cc - 1.f : cc;
-              cc = fminf(fmaxf(cc, -qf), qf);
+              cc = fmaxf(cc, -qf);
               c[e] = cc;
-              r[e] = __fmul_rn(__fmaf_rn(l, xs[e], -cc), il);
+              u[e] = __fmaf_rn(l, xs[e], -cc);
             }
           } else {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               c[e] = codef(l, xs[e], a.mode, a.qmax);
-              r[e] = __fmul_rn(__fmaf_rn(l, xs[e], -c[e]), il);
+              u[e] = __fmaf_rn(l, xs[e], -c[e]);
             }
           }
           const uint32_t off = kMode == 0 ? off_k(f >> 3, (f & 7) * 4) : off_mn((f & 31) * 4, f >> 5, 4);
-          const float4 h = make_float4(tf32_hi(r[0]), tf32_hi(r[1]), tf32_hi(r[2]), tf32_hi(r[3]));
+          const float4 h = make_float4(tf32_hi(u[0]), tf32_hi(u[1]), tf32_hi(u[2]), tf32_hi(u[3]));
           sts128(sAhi + off, h);
-          sts128(sAlo + off, make_float4(r[0] - h.x, r[1] - h.y, r[2] - h.z, r[3] - h.w));
+          sts128(sAlo + off, make_float4(u[0] - h.x, u[1] - h.y, u[2] - h.z, u[3] - h.w));
           if (kDual) sts128(sAc + off, make_float4(c[0], c[1], c[2], c[3]));
         }
         fence_proxy_async_smem();
-        mbar_arrive(&ofull[os]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ofull[os]);
       }
     }
   } else if (warp == kMmaWarp) {
@@ -413,8 +420,9 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       tc_fence_after();
       const int64_t orow = (int64_t)blk * BM + quad * 32 + lane;
       const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + acc * C::kAccCols;
+      // ROW: rows of R (and of X~) carry 1/lambda_i; COL already folded it into B
       float inv_row = 1.f;
-      if (kDual) inv_row = orow < a.rows ? __ldg(a.inv_lam + orow) : 1.f;
+      if (kMode == 0) inv_row = orow < a.rows ? __ldg(a.inv_lam + orow) : 1.f;
       float* out1 = a.out1 + (int64_t)split * a.nout * a.W;
       float* out2 = kDual ? a.out2 + (int64_t)split * a.nout * a.W : nullptr;
 #pragma unroll
@@ -429,9 +437,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
             if (cbase + c < a.W) {
-              float val = __uint_as_float(v[c]);
-              if (second) val = __fmul_rn(val, inv_row);
-              o[cbase + c] = val;
+              o[cbase + c] = __fmul_rn(__uint_as_float(v[c]), inv_row);
             }
           }
         }
