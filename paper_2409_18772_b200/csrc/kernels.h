@@ -42,25 +42,29 @@ struct SideView {
   const float* inv_lam;  // RN(1/lambda)
   int qmax, mode;
 };
-// tcgen05 kind::tf32 (3-term split) passes, deterministic split-K partials:
-// ROW: OUT1 = R P1 (rows x W); dual (P2 != null): OUT2 = X~ P2.  P is K x W (ld W).
-void launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
-                         float* partial, int64_t partial_elems, cudaStream_t st);
+// tcgen05 kind::tf32 (3-term split) passes, deterministic split-K partials; return the split count.
+// With reduce1 == false and > 1 splits, OUT1 stays as partials at `partial` (consumed by the fused
+// Gram kernel).  ROW: OUT1 = R P1 (rows x W); dual (P2 != null): OUT2 = X~ P2.  P is K x W (ld W).
+int launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
+                        float* partial, int64_t partial_elems, bool reduce1, cudaStream_t st);
 // COL: OUT = R^T P; P is rows x W, OUT is K x W.
-void launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t partial_elems,
-                         cudaStream_t st);
+int launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t partial_elems,
+                        bool reduce1, cudaStream_t st);
 
+// OUT[i, :] = IN[i, :] S (fp64 S, fp64 accumulation, fp32 out); IN and OUT ld W, S W x W
+void launch_apply64(const float* IN, const double* S, int64_t n, int W, float* OUT, cudaStream_t st);
 // OUT[i, col0 + o] = sum_c IN1[i,c] S1[c,o] (+ sum_c IN2[i,c] S2[c,o]), o < nout; IN ld W, S ld ldS, OUT ld ldo
 void launch_apply_small(const float* IN1, const float* S1, const float* IN2, const float* S2, int64_t n, int W,
                         int ldS, int nout, float* OUT, int64_t ldo, int col0, cudaStream_t st);
 
 // ----------------------------------------------------------- K4 small solvers
+constexpr int kGramMaxBlocks = 1024;  // Gram partial buffers hold kGramMaxBlocks x W x W doubles
 struct GramJob {  // G = Y1^T Y2 (W x W, fp64) over n rows (Y ld W)
   const float* Y1;
   const float* Y2;
   int64_t n;
   double* G;
-  double* partial;  // >= 148 * W * W
+  double* partial;  // >= kGramMaxBlocks * W * W
   int* counter;     // zero-initialised ticket
 };
 struct GramJobs {
@@ -70,17 +74,37 @@ struct GramJobs {
 void launch_gram_jobs(const GramJobs& jobs, int W, cudaStream_t st);
 struct EigJob {
   const double* G;
-  float* T;
+  float* T;     // truncation output (fp32)
+  double* T64;  // orthonormalising transform output (fp64, applied with fp64 accumulation)
   int r;
 };
 struct EigJobs {
   EigJob j[2];
   int n;
 };
-// orth transform (pivoted Cholesky QR, reading #12 threshold): Q = Y T has orthonormal columns
+// orth transform (pivoted Cholesky QR, reading #12 threshold): Q = Y T64 has orthonormal columns
 void launch_chol_orth(const EigJobs& jobs, int n, cudaStream_t st);
 // truncation: T[:, 0:r] = top-r eigenvectors of G (descending), rest 0
 void launch_eig_warp(const EigJobs& jobs, int n, cudaStream_t st);
+// Fused: Y = sum of nsplit partials (if nsplit > 1), G = Y^T Y (fp64), then mode 0: T64 = CholQR transform,
+// mode 1: T = top-r eigenvectors of G, mode 2: G only.  Both sides in one launch.
+struct SmallJob {
+  float* Y;            // n x W (output when nsplit > 1, input otherwise)
+  const float* part;   // nsplit x n x W split partials
+  int nsplit;
+  int64_t n;
+  double* G;
+  double* gpart;       // >= kGramMaxBlocks * W * W
+  int* counter;
+  double* T64;
+  float* T;
+  int r;
+};
+struct SmallJobs {
+  SmallJob j[2];
+  int n;
+};
+void launch_fused_small(const SmallJobs& jobs, int W, int mode, cudaStream_t st);
 // Mab[r x r] = VWb^T C VWa  and  VWbM[n x r] = VWb Mab   (C = Q1_B^T Q1_A, n x n fp64)
 void launch_cross_small(const double* C, const float* VWa, const float* VWb, int n, int r, float* VWbM,
                         cudaStream_t st);
@@ -110,6 +134,7 @@ int encode_map_2d(void* map, int dtype_f32, const void* base, uint64_t inner, ui
 int encode_map_1d_f32(void* map, const void* base, uint64_t n, uint32_t box);
 // out[i] = RN(1 / in[i])
 void launch_recip(const float* in, float* out, int64_t n, cudaStream_t st);
+void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t st);
 void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStream_t st);
 
 }  // namespace lrqmm

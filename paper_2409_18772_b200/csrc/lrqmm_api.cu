@@ -37,9 +37,9 @@ struct Side {
   float* Q1 = nullptr;       // K x W
   float* Gp = nullptr;       // rows x W : X~ Q1_other
   double* G = nullptr;       // W x W
-  double* gpart = nullptr;   // 148 x W x W Gram partials
+  double* gpart = nullptr;   // kGramMaxBlocks x W x W Gram partials
   int* counter = nullptr;    // Gram last-block ticket
-  float* T = nullptr;        // W x W  (orth transforms, scratch)
+  double* T64 = nullptr;     // W x W  (orth transform, fp64)
   float* VW = nullptr;       // W x W  (first r columns: truncation)
 };
 
@@ -164,7 +164,7 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   for (auto& s : h->s) {
     cudaFree(s.codes); cudaFree(s.lam); cudaFree(s.inv_lam); cudaFree(s.row_amax); cudaFree(s.lam_scalar); cudaFree(s.Om);
     cudaFree(s.Y); cudaFree(s.Q0); cudaFree(s.Z); cudaFree(s.Q1); cudaFree(s.Gp); cudaFree(s.G);
-    cudaFree(s.gpart); cudaFree(s.counter); cudaFree(s.T); cudaFree(s.VW); cudaFree(s.stage);
+    cudaFree(s.gpart); cudaFree(s.counter); cudaFree(s.T64); cudaFree(s.VW); cudaFree(s.stage);
   }
   cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->partial); cudaFree(h->Gcross); cudaFree(h->gpart_cross);
   cudaFree(h->counter_cross); cudaFree(h->VWbM); cudaFree(h->err_flag);
@@ -209,8 +209,8 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
     if (h->W > 0) {
       ok = ok && dalloc(&s.Om, K * h->W) && dalloc(&s.Y, s.rows * h->W) && dalloc(&s.Q0, s.rows * h->W) &&
            dalloc(&s.Z, K * h->W) && dalloc(&s.Q1, K * h->W) && dalloc(&s.Gp, s.rows * h->W) &&
-           dalloc(&s.G, (int64_t)h->W * h->W) && dalloc(&s.gpart, 148LL * h->W * h->W) &&
-           dalloc(&s.counter, 1) && dalloc(&s.T, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W);
+           dalloc(&s.G, (int64_t)h->W * h->W) && dalloc(&s.gpart, (int64_t)kGramMaxBlocks * h->W * h->W) &&
+           dalloc(&s.counter, 1) && dalloc(&s.T64, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W);
     }
   }
   if (h->W > 0) {
@@ -219,7 +219,7 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
     h->partial_elems = std::min<int64_t>((int64_t)16 << 20, 2 * 32 * maxrows * h->W);
     ok = ok && dalloc(&h->LA, cfg->m * h->R2) && dalloc(&h->LB, cfg->n * h->R2) &&
          dalloc(&h->partial, h->partial_elems) && dalloc(&h->Gcross, (int64_t)h->W * h->W) &&
-         dalloc(&h->gpart_cross, 148LL * h->W * h->W) && dalloc(&h->counter_cross, 1) &&
+         dalloc(&h->gpart_cross, (int64_t)kGramMaxBlocks * h->W * h->W) && dalloc(&h->counter_cross, 1) &&
          dalloc(&h->VWbM, (int64_t)h->W * h->W);
   }
   ok = ok && dalloc(&h->err_flag, 4);
@@ -335,30 +335,35 @@ static lrqmm_status_t allreduce_f32(lrqmm_handle_t h, float* buf, size_t n) {
   return LRQMM_OK;
 }
 
-// G_s = Y1_s^T Y2_s for both sides (one launch)
-static void gram2(lrqmm_handle_t h, float* const Y1[2], float* const Y2[2], const int64_t n[2]) {
-  GramJobs j{};
+// Split-K partial regions: one half of the partial buffer per side, so side A's partials can
+// wait for the fused Gram kernel while side B's pass runs.
+static float* part_of(lrqmm_handle_t h, int sd) { return h->partial + sd * (h->partial_elems / 2); }
+static int64_t part_elems(lrqmm_handle_t h) { return h->partial_elems / 2; }
+
+// After a skinny pass left Y_s as nsp[s] split partials: Y = sum(partials), G = Y^T Y, then
+// mode 0: CholQR transform T64 -> Q = Y T64 (fp64 accumulation); mode 1: truncation VW.
+// On a row-sharded A (world > 1, a_sharded) G_A is summed across ranks before the solve.
+static lrqmm_status_t gram_step(lrqmm_handle_t h, float* const Y[2], const int64_t n[2], const int nsp[2], int mode,
+                                float* const Q[2], bool a_sharded) {
+  const int W = h->W;
+  const bool ranks = a_sharded && h->cfg.world_size > 1;
+  SmallJobs j{};
   j.n = 2;
   for (int sd = 0; sd < 2; ++sd)
-    j.j[sd] = GramJob{Y1[sd], Y2[sd], n[sd], h->s[sd].G, h->s[sd].gpart, h->s[sd].counter};
-  launch_gram_jobs(j, h->W, h->st);
-}
-
-// Q_s <- orthonormal basis of span(Y_s) for both sides: G = Y^T Y (fp64), pivoted
-// Cholesky -> T, Q = Y T.  a_rows_sharded: Y_A's rows live on different ranks (sum G_A).
-static lrqmm_status_t orth_pair(lrqmm_handle_t h, float* const Y[2], const int64_t n[2], float* const Q[2],
-                                bool a_rows_sharded) {
-  const int W = h->W;
-  gram2(h, Y, Y, n);
-  if (a_rows_sharded) {
+    j.j[sd] = SmallJob{Y[sd], part_of(h, sd), nsp[sd], n[sd], h->s[sd].G, h->s[sd].gpart, h->s[sd].counter,
+                       h->s[sd].T64, h->s[sd].VW, h->r};
+  launch_fused_small(j, W, ranks ? 2 : mode, h->st);
+  if (ranks) {
     lrqmm_status_t e = allreduce_f64(h, h->s[0].G, (size_t)W * W);
     if (e != LRQMM_OK) return e;
+    EigJobs ej{};
+    ej.n = 2;
+    for (int sd = 0; sd < 2; ++sd) ej.j[sd] = EigJob{h->s[sd].G, h->s[sd].VW, h->s[sd].T64, h->r};
+    if (mode == 0) launch_chol_orth(ej, W, h->st);
+    else launch_eig_warp(ej, W, h->st);
   }
-  EigJobs ej{};
-  ej.n = 2;
-  for (int sd = 0; sd < 2; ++sd) ej.j[sd] = EigJob{h->s[sd].G, h->s[sd].T, 0};
-  launch_chol_orth(ej, W, h->st);
-  for (int sd = 0; sd < 2; ++sd) launch_apply_small(Y[sd], h->s[sd].T, nullptr, nullptr, n[sd], W, W, W, Q[sd], W, 0, h->st);
+  if (mode == 0)
+    for (int sd = 0; sd < 2; ++sd) launch_apply64(Y[sd], h->s[sd].T64, n[sd], W, Q[sd], h->st);
   return check_launch(h);
 }
 
@@ -371,56 +376,52 @@ lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const 
   cudaSetDevice(h->cfg.device);
   const int W = h->W;
   const int64_t K = h->cfg.k;
+  const bool multi = h->cfg.world_size > 1;
   record(h, 4);
   // sketch Omega (K x kk, caller layout) -> zero-padded K x W
   const float* om[2] = {omegaA, omegaB};
   for (int sd = 0; sd < 2; ++sd)
     LQ_CUDA(cudaMemcpy2DAsync(h->s[sd].Om, sizeof(float) * W, om[sd], sizeof(float) * ldo, sizeof(float) * h->kk, K,
                               cudaMemcpyDeviceToDevice, h->st));
-  // S1: Y = R Omega   (Algorithm 1 sampling, PAPER.md:124,128)
-  for (int sd = 0; sd < 2; ++sd)
-    launch_tc_proj_rows(view(h, sd), h->s[sd].Om, h->s[sd].Y, nullptr, nullptr, W, h->partial, h->partial_elems, h->st);
   const int64_t rows[2] = {h->s[0].rows, h->s[1].rows};
   const int64_t kdim[2] = {K, K};
+  float* Ys[2] = {h->s[0].Y, h->s[1].Y};
+  float* Q0s[2] = {h->s[0].Q0, h->s[1].Q0};
+  float* Zs[2] = {h->s[0].Z, h->s[1].Z};
+  float* Q1s[2] = {h->s[0].Q1, h->s[1].Q1};
+  int nsp[2];
   lrqmm_status_t e;
+  // S1: Y = R Omega   (Algorithm 1 sampling, PAPER.md:124,128)
+  for (int sd = 0; sd < 2; ++sd)
+    nsp[sd] = launch_tc_proj_rows(view(h, sd), h->s[sd].Om, Ys[sd], nullptr, nullptr, W, part_of(h, sd),
+                                  part_elems(h), false, h->st);
   for (int it = 0; it < h->cfg.power_iters; ++it) {
-    float* Ys[2] = {h->s[0].Y, h->s[1].Y};
-    float* Q0s[2] = {h->s[0].Q0, h->s[1].Q0};
-    // O1: Q0 = orth(Y)
-    if ((e = orth_pair(h, Ys, rows, Q0s, true)) != LRQMM_OK) return e;
-    // S2: Z = R^T Q0  (reduction over rows; A side summed over ranks)
+    // O1: Q0 = orth(Y)   (Y rows of A are sharded across ranks)
+    if ((e = gram_step(h, Ys, rows, nsp, 0, Q0s, true)) != LRQMM_OK) return e;
+    // S2: Z = R^T Q0  (reduction over rows; the A side is summed over ranks before its Gram)
     for (int sd = 0; sd < 2; ++sd)
-      launch_tc_proj_cols(view(h, sd), h->s[sd].Q0, h->s[sd].Z, W, h->partial, h->partial_elems, h->st);
-    if ((e = allreduce_f32(h, h->s[0].Z, (size_t)K * W)) != LRQMM_OK) return e;
-    // O2: Q1 = orth(Z) and one re-orthonormalisation pass (CholQR2); K rows are replicated on every rank
-    {
-      float* Zs[2] = {h->s[0].Z, h->s[1].Z};
-      float* Q1s[2] = {h->s[0].Q1, h->s[1].Q1};
-      if ((e = orth_pair(h, Zs, kdim, Q1s, false)) != LRQMM_OK) return e;
-      if ((e = orth_pair(h, Q1s, kdim, Zs, false)) != LRQMM_OK) return e;
-      for (int sd = 0; sd < 2; ++sd) std::swap(h->s[sd].Z, h->s[sd].Q1);  // refined basis now in Q1
+      nsp[sd] = launch_tc_proj_cols(view(h, sd), Q0s[sd], Zs[sd], W, part_of(h, sd), part_elems(h), multi, h->st);
+    if (multi) {
+      if ((e = allreduce_f32(h, Zs[0], (size_t)K * W)) != LRQMM_OK) return e;
+      nsp[0] = nsp[1] = 1;
+      // side B was reduced too (multi -> reduce1), both Z are final
     }
+    // O2: Q1 = orth(Z) (fp64 Gram + Cholesky, transform applied with fp64 accumulation, so Q1 is
+    // orthonormal to fp32 rounding); K rows are replicated on every rank
+    if ((e = gram_step(h, Zs, kdim, nsp, 0, Q1s, false)) != LRQMM_OK) return e;
     if (it + 1 < h->cfg.power_iters) {
       for (int sd = 0; sd < 2; ++sd)
-        launch_tc_proj_rows(view(h, sd), h->s[sd].Q1, h->s[sd].Y, nullptr, nullptr, W, h->partial, h->partial_elems,
-                            h->st);
+        nsp[sd] = launch_tc_proj_rows(view(h, sd), Q1s[sd], Ys[sd], nullptr, nullptr, W, part_of(h, sd),
+                                      part_elems(h), false, h->st);
     }
   }
   // S3 + cross: W_X = R_X Q1_X and G'_X = X~ Q1_other in one pass over X
   //   (Algorithm 1 on R^T: B = Q1^T R^T = W^T; RC1/RC2 skinny products)
   for (int sd = 0; sd < 2; ++sd)
-    launch_tc_proj_rows(view(h, sd), h->s[sd].Q1, h->s[sd].Y, h->s[1 - sd].Q1, h->s[sd].Gp, W, h->partial,
-                        h->partial_elems, h->st);
-  // T: truncation to rank r via eig(W^T W) (Algorithm 1)
-  {
-    float* Ys[2] = {h->s[0].Y, h->s[1].Y};
-    gram2(h, Ys, Ys, rows);
-    if ((e = allreduce_f64(h, h->s[0].G, (size_t)W * W)) != LRQMM_OK) return e;
-    EigJobs ej{};
-    ej.n = 2;
-    for (int sd = 0; sd < 2; ++sd) ej.j[sd] = EigJob{h->s[sd].G, h->s[sd].VW, h->r};
-    launch_eig_warp(ej, W, h->st);
-  }
+    nsp[sd] = launch_tc_proj_rows(view(h, sd), Q1s[sd], Ys[sd], Q1s[1 - sd], h->s[sd].Gp, W, part_of(h, sd),
+                                  part_elems(h), false, h->st);
+  // T: W = sum(partials), truncation to rank r via eig(W^T W) (Algorithm 1)
+  if ((e = gram_step(h, Ys, rows, nsp, 1, nullptr, true)) != LRQMM_OK) return e;
   // V_B^T V_A core: Q1_B^T Q1_A (fp64, W x W) -> Mab, VWb Mab
   {
     GramJobs j{};
@@ -619,9 +620,9 @@ extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx
   const int64_t pe = (int64_t)16 << 20;
   float* partial = nullptr;
   if (cudaMalloc(&partial, sizeof(float) * pe) != cudaSuccess) return LRQMM_ERR_ALLOC;
-  if (mode == 0) launch_tc_proj_rows(v, P, OUT, nullptr, nullptr, W, partial, pe, st);
-  else if (mode == 1) launch_tc_proj_cols(v, P, OUT, W, partial, pe, st);
-  else launch_tc_proj_rows(v, P, OUT, P2, OUT2, W, partial, pe, st);
+  if (mode == 0) launch_tc_proj_rows(v, P, OUT, nullptr, nullptr, W, partial, pe, true, st);
+  else if (mode == 1) launch_tc_proj_cols(v, P, OUT, W, partial, pe, true, st);
+  else launch_tc_proj_rows(v, P, OUT, P2, OUT2, W, partial, pe, true, st);
   cudaError_t e = cudaStreamSynchronize(st);
   if (e == cudaSuccess) e = cudaGetLastError();
   cudaFree(partial);
@@ -635,7 +636,7 @@ extern "C" lrqmm_status_t lrqmm_debug_small(int op, const float* Y, int64_t n, i
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   double* part = nullptr;
   int* counter = nullptr;
-  if (cudaMalloc(&part, sizeof(double) * 148 * W * W) != cudaSuccess) return LRQMM_ERR_ALLOC;
+  if (cudaMalloc(&part, sizeof(double) * kGramMaxBlocks * W * W) != cudaSuccess) return LRQMM_ERR_ALLOC;
   if (cudaMalloc(&counter, sizeof(int)) != cudaSuccess) return LRQMM_ERR_ALLOC;
   cudaMemsetAsync(counter, 0, sizeof(int), st);
   GramJobs gj{};
@@ -644,11 +645,17 @@ extern "C" lrqmm_status_t lrqmm_debug_small(int op, const float* Y, int64_t n, i
   launch_gram_jobs(gj, W, st);
   EigJobs ej{};
   ej.n = 1;
-  ej.j[0] = EigJob{G, T, r};
-  if (op == 1) launch_chol_orth(ej, W, st);
+  double* T64 = nullptr;
+  if (cudaMalloc(&T64, sizeof(double) * W * W) != cudaSuccess) return LRQMM_ERR_ALLOC;
+  ej.j[0] = EigJob{G, T, T64, r};
+  if (op == 1) {
+    launch_chol_orth(ej, W, st);
+    launch_f64_to_f32(T64, T, (int64_t)W * W, st);
+  }
   if (op == 2) launch_eig_warp(ej, W, st);
   cudaError_t e = cudaStreamSynchronize(st);
   cudaFree(part);
   cudaFree(counter);
+  cudaFree(T64);
   return e == cudaSuccess ? LRQMM_OK : LRQMM_ERR_CUDA;
 }

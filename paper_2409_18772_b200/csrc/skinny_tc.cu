@@ -43,7 +43,7 @@ constexpr int BK = 32;   // reduction elements per k-block
 #ifndef LRQMM_OPST
 #define LRQMM_OPST 2
 #endif
-constexpr int OPST = LRQMM_OPST;  // operand stages
+constexpr int OPST_MAX = LRQMM_OPST;  // operand stages (reduced per config to fit smem)
 constexpr int kATile = BM * BK * 4;    // 16 KB
 constexpr int kRawTile = BM * BK * 4;  // 16 KB
 template <int kMode, int NA, bool kDual>
@@ -55,9 +55,12 @@ struct Cfg {
   static constexpr int kRawP = BK * WN * 4;
   static constexpr int kRawBytes = kRawTile + (kDual ? 2 : 1) * kRawP + (kMode == 1 ? 2 * BK * 4 : 0);
   static constexpr int kRawSlot = (kRawBytes + 1023) / 1024 * 1024;
-  static constexpr int kRawSt = (4 * kRawSlot + OPST * kStage <= 216 * 1024) ? 4
-                                : ((3 * kRawSlot + OPST * kStage <= 216 * 1024) ? 3 : 2);
+  static constexpr int kBudget = 220 * 1024;
+  static constexpr int fits(int op, int raw) { return op * kStage + raw * kRawSlot <= kBudget; }
+  static constexpr int OPST = fits(OPST_MAX, 3) ? OPST_MAX : 2;
+  static constexpr int kRawSt = fits(OPST, 4) ? 4 : (fits(OPST, 3) ? 3 : 2);
   static constexpr int kSmem = kRawSt * kRawSlot + OPST * kStage + 256 + 1024;
+  static_assert(kSmem <= 227 * 1024, "shared memory budget");
   static constexpr int kAccCols = (kDual ? 2 : 1) * WN;  // per accumulator buffer
   static constexpr uint32_t kTmemCols =
       2 * kAccCols <= 32 ? 32 : (2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : 256));
@@ -157,6 +160,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   constexpr int kBTile = C::kBTile;
   constexpr int kStage = C::kStage;
   constexpr int RST = C::kRawSt;
+  constexpr int OPST = C::OPST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int kRawSlot = C::kRawSlot;
@@ -462,7 +466,7 @@ __global__ void k_reduce_splits_tc(const float* __restrict__ part, int nsplit, i
 }
 
 template <int kMode, int NA, bool kDual>
-static void run_tc(const TcArgs& a0, float* OUT1, float* OUT2, float* partial, int64_t pe, cudaStream_t st) {
+static int run_tc(const TcArgs& a0, float* OUT1, float* OUT2, float* partial, int64_t pe, bool reduce1, cudaStream_t st) {
   using namespace tcp;
   using C = Cfg<kMode, NA, kDual>;
   static bool attr = false;
@@ -508,13 +512,16 @@ static void run_tc(const TcArgs& a0, float* OUT1, float* OUT2, float* partial, i
   if (ns > 1) {
     const int64_t n = a.nout * a.W;
     const int g = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
-    k_reduce_splits_tc<<<g, 256, 0, st>>>(partial, (int)ns, n, OUT1);
-    ++launch_counter();
+    if (reduce1) {
+      k_reduce_splits_tc<<<g, 256, 0, st>>>(partial, (int)ns, n, OUT1);
+      ++launch_counter();
+    }
     if (kDual) {
       k_reduce_splits_tc<<<g, 256, 0, st>>>(partial + ns * a.nout * a.W, (int)ns, n, OUT2);
       ++launch_counter();
     }
   }
+  return (int)ns;
 }
 
 static TcArgs make_args(const SideView& s, const float* P1, const float* P2, int W, int64_t nout) {
@@ -535,26 +542,26 @@ static TcArgs make_args(const SideView& s, const float* P1, const float* P2, int
 }
 
 // X must be TMA-addressable: 16-byte aligned base and ldx % 4 == 0 (lrqmm_quantize
-// stages other layouts into an aligned handle-owned copy).
-void launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
-                         float* partial, int64_t pe, cudaStream_t st) {
-  if (s.rows == 0 || s.K == 0) return;
+// stages other layouts into an aligned handle-owned copy).  Returns the number of split-K
+// partials; with reduce1 == false and a result > 1, OUT1 is left as partials at `partial`.
+int launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
+                        float* partial, int64_t pe, bool reduce1, cudaStream_t st) {
+  if (s.rows == 0 || s.K == 0) return 0;
   TcArgs a = make_args(s, P1, P2, W, s.rows);
   if (W <= 32) {
-    if (P2) run_tc<0, 1, true>(a, OUT1, OUT2, partial, pe, st);
-    else run_tc<0, 1, false>(a, OUT1, OUT2, partial, pe, st);
-  } else {
-    if (P2) run_tc<0, 2, true>(a, OUT1, OUT2, partial, pe, st);
-    else run_tc<0, 2, false>(a, OUT1, OUT2, partial, pe, st);
+    if (P2) return run_tc<0, 1, true>(a, OUT1, OUT2, partial, pe, reduce1, st);
+    return run_tc<0, 1, false>(a, OUT1, OUT2, partial, pe, reduce1, st);
   }
+  if (P2) return run_tc<0, 2, true>(a, OUT1, OUT2, partial, pe, reduce1, st);
+  return run_tc<0, 2, false>(a, OUT1, OUT2, partial, pe, reduce1, st);
 }
 
-void launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t pe,
-                         cudaStream_t st) {
-  if (s.K == 0 || s.rows == 0) return;
+int launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t pe, bool reduce1,
+                        cudaStream_t st) {
+  if (s.K == 0 || s.rows == 0) return 0;
   TcArgs a = make_args(s, P, nullptr, W, s.K);
-  if (W <= 32) run_tc<1, 1, false>(a, OUT, nullptr, partial, pe, st);
-  else run_tc<1, 2, false>(a, OUT, nullptr, partial, pe, st);
+  if (W <= 32) return run_tc<1, 1, false>(a, OUT, nullptr, partial, pe, reduce1, st);
+  return run_tc<1, 2, false>(a, OUT, nullptr, partial, pe, reduce1, st);
 }
 
 }  // namespace lrqmm

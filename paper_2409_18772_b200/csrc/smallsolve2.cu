@@ -19,11 +19,15 @@ namespace lrqmm {
 constexpr int kN = 64;
 
 // ------------------------------------------------------------------- Gram
+// One launch: each block loads its row range in chunks of kGramRows (one chunk unless n > 64K), then
+// accumulates its W x W partial in fp64; the last block (ticket) sums the partials in a
+// fixed order.  blockIdx.y = job.
+constexpr int kGramRows = 64;
 __global__ void __launch_bounds__(256) k_gram(GramJobs jobs, int W) {
   const GramJob jb = jobs.j[blockIdx.y];
   const int npairs = W * W;
-  __shared__ float s1[32][kN + 1];
-  __shared__ float s2[32][kN + 1];
+  __shared__ float s1[kGramRows][kN + 1];
+  __shared__ float s2[kGramRows][kN + 1];
   __shared__ int ticket;
   const int64_t rpb = (jb.n + gridDim.x - 1) / gridDim.x;
   const int64_t r_begin = (int64_t)blockIdx.x * rpb;
@@ -31,13 +35,13 @@ __global__ void __launch_bounds__(256) k_gram(GramJobs jobs, int W) {
   double acc[16];
 #pragma unroll
   for (int q = 0; q < 16; ++q) acc[q] = 0.0;
-  for (int64_t r0 = r_begin; r0 < r_end; r0 += 32) {
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += kGramRows) {
+    const int nr = (int)(r_end - r0 < kGramRows ? r_end - r0 : kGramRows);
     __syncthreads();
-    for (int e = threadIdx.x; e < 32 * W; e += 256) {
+    for (int e = threadIdx.x; e < nr * W; e += 256) {
       const int i = e / W, c = e % W;
-      const bool in = r0 + i < r_end;
-      s1[i][c] = in ? jb.Y1[(r0 + i) * W + c] : 0.f;
-      s2[i][c] = in ? jb.Y2[(r0 + i) * W + c] : 0.f;
+      s1[i][c] = __ldg(jb.Y1 + (r0 + i) * W + c);
+      s2[i][c] = __ldg(jb.Y2 + (r0 + i) * W + c);
     }
     __syncthreads();
 #pragma unroll
@@ -45,13 +49,16 @@ __global__ void __launch_bounds__(256) k_gram(GramJobs jobs, int W) {
       const int pr = threadIdx.x + 256 * q;
       if (pr < npairs) {
         const int a = pr / W, c = pr % W;
-        double t0 = 0.0, t1 = 0.0;
-#pragma unroll 8
-        for (int i = 0; i < 32; i += 2) {
+        double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+        int i = 0;
+        for (; i + 3 < nr; i += 4) {
           t0 = fma((double)s1[i][a], (double)s2[i][c], t0);
           t1 = fma((double)s1[i + 1][a], (double)s2[i + 1][c], t1);
+          t2 = fma((double)s1[i + 2][a], (double)s2[i + 2][c], t2);
+          t3 = fma((double)s1[i + 3][a], (double)s2[i + 3][c], t3);
         }
-        acc[q] += t0 + t1;
+        for (; i < nr; ++i) t0 = fma((double)s1[i][a], (double)s2[i][c], t0);
+        acc[q] += (t0 + t1) + (t2 + t3);
       }
     }
   }
@@ -87,9 +94,11 @@ __global__ void __launch_bounds__(256) k_gram(GramJobs jobs, int W) {
 void launch_gram_jobs(const GramJobs& jobs, int W, cudaStream_t st) {
   int64_t nmax = 0;
   for (int i = 0; i < jobs.n; ++i) nmax = jobs.j[i].n > nmax ? jobs.j[i].n : nmax;
-  int64_t nb = (nmax + 511) / 512;
-  if (nb > 64) nb = 64;
+  // blocks <= kGramMaxBlocks (partial buffer), each <= kGramRows rows
+  int64_t nb = (nmax + kGramRows - 1) / kGramRows;
+  if (nb > kGramMaxBlocks) nb = kGramMaxBlocks;
   if (nb < 1) nb = 1;
+
   k_gram<<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs, W);
   ++launch_counter();
 }
@@ -97,18 +106,16 @@ void launch_gram_jobs(const GramJobs& jobs, int W, cudaStream_t st) {
 // ------------------------------------------------- pivoted Cholesky orth
 // 256 threads: pivot search by warp 0, column scaling and the trailing rank-1
 // update by the whole CTA; L^-1 by row-sequential forward substitution.
-__global__ void __launch_bounds__(256) k_chol_orth(EigJobs jobs, int n) {
-  extern __shared__ double dyn[];
+__device__ void dev_chol_orth(const double* G, double* T64, int n, double* dyn) {
   double (*A)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn);
   double (*Li)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn + kN * (kN + 1));  // L^-1 (lower)
   __shared__ int piv[kN];
   __shared__ int bi_s, stop_s;
   __shared__ double dmax_s;
-  const EigJob job = jobs.j[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31;
   for (int e = tid; e < n * n; e += 256) {
     const int i = e / n, j = e % n;
-    A[i][j] = 0.5 * (job.G[i * n + j] + job.G[j * n + i]);
+    A[i][j] = 0.5 * (G[i * n + j] + G[j * n + i]);
     Li[i][j] = 0.0;
   }
   if (tid < n) piv[tid] = tid;
@@ -184,12 +191,17 @@ __global__ void __launch_bounds__(256) k_chol_orth(EigJobs jobs, int n) {
   // T[piv[a]][b] = (L^-T)[a][b] = Li[b][a] for a <= b < rk; zero elsewhere
   for (int e = tid; e < n * n; e += 256) {
     const int rr = e / n, b = e % n;
-    float v = 0.f;
+    double v = 0.0;
     // find a with piv[a] == rr (a < rk)
     for (int a2 = 0; a2 < rk; ++a2)
-      if (piv[a2] == rr && b >= a2 && b < rk) v = (float)Li[b][a2];
-    job.T[rr * n + b] = v;
+      if (piv[a2] == rr && b >= a2 && b < rk) v = Li[b][a2];
+    T64[rr * n + b] = v;
   }
+}
+
+__global__ void __launch_bounds__(256) k_chol_orth(EigJobs jobs, int n) {
+  extern __shared__ double dyn[];
+  dev_chol_orth(jobs.j[blockIdx.x].G, jobs.j[blockIdx.x].T64, n, dyn);
 }
 
 static const int kDynSmem = 2 * kN * (kN + 1) * (int)sizeof(double);
@@ -207,8 +219,7 @@ void launch_chol_orth(const EigJobs& jobs, int n, cudaStream_t st) {
 // --------------------------------------------- parallel Jacobi (truncation)
 // Round-robin pairing: n/2 disjoint rotations per step.  A' = J^T A J is applied
 // in ONE pass over 2x2 blocks (pair k1 rows x pair k2 cols), V' = V J in another.
-__global__ void __launch_bounds__(256) k_eig(EigJobs jobs, int n) {
-  extern __shared__ double dyn[];
+__device__ void dev_eig_trunc(const double* G, float* T, int r, int n, double* dyn) {
   double (*A)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn);
   double (*V)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn + kN * (kN + 1));
   __shared__ double cs[kN / 2], sn[kN / 2];
@@ -216,11 +227,10 @@ __global__ void __launch_bounds__(256) k_eig(EigJobs jobs, int n) {
   __shared__ int order[kN];
   __shared__ double red[8][2];
   __shared__ int stop;
-  const EigJob job = jobs.j[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int e = tid; e < n * n; e += 256) {
     const int i = e / n, j = e % n;
-    A[i][j] = 0.5 * (job.G[i * n + j] + job.G[j * n + i]);
+    A[i][j] = 0.5 * (G[i * n + j] + G[j * n + i]);
     V[i][j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
@@ -256,12 +266,15 @@ __global__ void __launch_bounds__(256) k_eig(EigJobs jobs, int n) {
         const double apq = A[p][q];
         double c = 1.0, s = 0.0;
         if (apq != 0.0) {
-          const double theta = (A[q][q] - A[p][p]) / (2.0 * apq);
-          double t;
-          if (fabs(theta) > 1e150) t = 0.5 / theta;
-          else t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-          c = rsqrt(t * t + 1.0);
-          s = t * c;
+          // angle in fp32 (any rotation is an exact similarity; c, s below are orthonormal to
+          // fp64 rounding), which keeps the latency of the 2x2 solve short
+          const float theta = (float)((A[q][q] - A[p][p]) / (2.0 * apq));
+          float t;
+          if (fabsf(theta) > 1e18f) t = 0.5f / theta;
+          else t = copysignf(1.f, theta) / (fabsf(theta) + sqrtf(fmaf(theta, theta, 1.f)));
+          const double td = (double)t;
+          c = rsqrt(fma(td, td, 1.0));
+          s = td * c;
         }
         pp[k] = p; qq[k] = q; cs[k] = c; sn[k] = s;
       }
@@ -318,8 +331,13 @@ __global__ void __launch_bounds__(256) k_eig(EigJobs jobs, int n) {
   __syncthreads();
   for (int e = tid; e < n * n; e += 256) {
     const int a = e / n, o = e % n;
-    job.T[a * n + o] = (o < job.r) ? (float)V[a][order[o]] : 0.f;
+    T[a * n + o] = (o < r) ? (float)V[a][order[o]] : 0.f;
   }
+}
+
+__global__ void __launch_bounds__(256) k_eig(EigJobs jobs, int n) {
+  extern __shared__ double dyn[];
+  dev_eig_trunc(jobs.j[blockIdx.x].G, jobs.j[blockIdx.x].T, jobs.j[blockIdx.x].r, n, dyn);
 }
 
 void launch_eig_warp(const EigJobs& jobs, int n, cudaStream_t st) {
@@ -329,6 +347,109 @@ void launch_eig_warp(const EigJobs& jobs, int n, cudaStream_t st) {
     attr = true;
   }
   k_eig<<<jobs.n, 256, kDynSmem, st>>>(jobs, n);
+  ++launch_counter();
+}
+
+// ------------------------------------------------- fused orth / truncation
+// One launch per RSVD orthonormalisation (or truncation) step, both sides (blockIdx.y):
+//   phase 1 (all blocks): Y = sum of the split-K partials (fixed order) -> written once;
+//                         the block's rows are kept in smem and their fp64 Gram partial formed;
+//   phase 2 (last block by ticket): fixed-order sum of the Gram partials -> G, then the
+//                         pivoted CholQR transform (mode 0) or the truncation eigenvectors
+//                         (mode 1), or nothing (mode 2: G must first be summed across ranks).
+constexpr int kFRows = 64;
+__global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int W, int mode) {
+  extern __shared__ double dyn[];
+  const SmallJob jb = jobs.j[blockIdx.y];
+  float (*sY)[kN + 1] = reinterpret_cast<float (*)[kN + 1]>(dyn);  // kFRows x (kN+1) floats
+  __shared__ int ticket;
+  const int npairs = W * W;
+  const int64_t rpb = (jb.n + gridDim.x - 1) / gridDim.x;
+  const int64_t r_begin = (int64_t)blockIdx.x * rpb;
+  const int64_t r_end = (jb.n < r_begin + rpb) ? jb.n : r_begin + rpb;
+  const int64_t plane = jb.n * W;
+  double acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += kFRows) {
+    const int nr = (int)(r_end - r0 < kFRows ? r_end - r0 : kFRows);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * W; e += 256) {
+      const int i = e / W, c = e % W;
+      const int64_t g = (r0 + i) * W + c;
+      float v;
+      if (jb.nsplit > 1) {
+        float a0 = 0.f;
+        for (int sp = 0; sp < jb.nsplit; ++sp) a0 += __ldcg(jb.part + sp * plane + g);
+        jb.Y[g] = a0;
+        v = a0;
+      } else {
+        v = __ldcg(jb.Y + g);
+      }
+      sY[i][c] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int pr = threadIdx.x + 256 * q;
+      if (pr < npairs) {
+        const int a = pr / W, c = pr % W;
+        double t0 = 0.0, t1 = 0.0;
+        int i = 0;
+        for (; i + 1 < nr; i += 2) {
+          t0 = fma((double)sY[i][a], (double)sY[i][c], t0);
+          t1 = fma((double)sY[i + 1][a], (double)sY[i + 1][c], t1);
+        }
+        if (i < nr) t0 = fma((double)sY[i][a], (double)sY[i][c], t0);
+        acc[q] += t0 + t1;
+      }
+    }
+  }
+  double* part = jb.gpart + (int64_t)blockIdx.x * npairs;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int pr = threadIdx.x + 256 * q;
+    if (pr < npairs) part[pr] = acc[q];
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(jb.counter, 1);
+  __syncthreads();
+  if (ticket != (int)gridDim.x - 1) return;
+  __threadfence();
+  const int nb = (int)gridDim.x;
+  for (int pr = threadIdx.x; pr < npairs; pr += 256) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int b = 0;
+    for (; b + 3 < nb; b += 4) {
+      a0 += __ldcg(jb.gpart + (int64_t)(b + 0) * npairs + pr);
+      a1 += __ldcg(jb.gpart + (int64_t)(b + 1) * npairs + pr);
+      a2 += __ldcg(jb.gpart + (int64_t)(b + 2) * npairs + pr);
+      a3 += __ldcg(jb.gpart + (int64_t)(b + 3) * npairs + pr);
+    }
+    for (; b < nb; ++b) a0 += __ldcg(jb.gpart + (int64_t)b * npairs + pr);
+    jb.G[pr] = (a0 + a1) + (a2 + a3);
+  }
+  if (threadIdx.x == 0) *jb.counter = 0;  // re-arm for the next launch (stream ordered)
+  __threadfence_block();
+  __syncthreads();
+  if (mode == 0) dev_chol_orth(jb.G, jb.T64, W, dyn);
+  else if (mode == 1) dev_eig_trunc(jb.G, jb.T, jb.r, W, dyn);
+}
+
+void launch_fused_small(const SmallJobs& jobs, int W, int mode, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fused_small, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+    attr = true;
+  }
+  int64_t nmax = 0;
+  for (int i = 0; i < jobs.n; ++i) nmax = jobs.j[i].n > nmax ? jobs.j[i].n : nmax;
+  // ~4 row chunks per block keeps the last-block reduction short (<= 64 partials at 16K rows)
+  int64_t nb = (nmax + 4 * kFRows - 1) / (4 * kFRows);
+  if (nb > kGramMaxBlocks) nb = kGramMaxBlocks;
+  if (nb < 1) nb = 1;
+  k_fused_small<<<dim3((unsigned)nb, (unsigned)jobs.n), 256, kDynSmem, st>>>(jobs, W, mode);
   ++launch_counter();
 }
 
