@@ -17,17 +17,20 @@
 namespace lrqmm {
 
 constexpr int kN = 64;
+template <int n>
+__global__ void __launch_bounds__(32) k_warp_chol(EigJobs jobs);
 
 // ------------------------------------------------------------------- Gram
 // One launch: each block loads its row range in chunks of kGramRows (one chunk unless n > 64K), then
 // accumulates its W x W partial in fp64; the last block (ticket) sums the partials in a
 // fixed order.  blockIdx.y = job.
-constexpr int kGramRows = 64;
-__global__ void __launch_bounds__(256) k_gram(GramJobs jobs, int W) {
+constexpr int kGramRows = 32;
+template <int W>
+__global__ void __launch_bounds__(256) k_gram(GramJobs jobs) {
   const GramJob jb = jobs.j[blockIdx.y];
   const int npairs = W * W;
-  __shared__ float s1[kGramRows][kN + 1];
-  __shared__ float s2[kGramRows][kN + 1];
+  __shared__ double s1[kGramRows][kN + 1];
+  __shared__ double s2[kGramRows][kN + 1];
   __shared__ int ticket;
   const int64_t rpb = (jb.n + gridDim.x - 1) / gridDim.x;
   const int64_t r_begin = (int64_t)blockIdx.x * rpb;
@@ -38,10 +41,23 @@ __global__ void __launch_bounds__(256) k_gram(GramJobs jobs, int W) {
   for (int64_t r0 = r_begin; r0 < r_end; r0 += kGramRows) {
     const int nr = (int)(r_end - r0 < kGramRows ? r_end - r0 : kGramRows);
     __syncthreads();
-    for (int e = threadIdx.x; e < nr * W; e += 256) {
-      const int i = e / W, c = e % W;
-      s1[i][c] = __ldg(jb.Y1 + (r0 + i) * W + c);
-      s2[i][c] = __ldg(jb.Y2 + (r0 + i) * W + c);
+    const int ne = nr * W;
+    for (int e0 = threadIdx.x; e0 < ne; e0 += 256 * 4) {
+      float v1[4], v2[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + 256 * u;
+        v1[u] = e < ne ? __ldg(jb.Y1 + r0 * W + e) : 0.f;
+        v2[u] = e < ne ? __ldg(jb.Y2 + r0 * W + e) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + 256 * u;
+        if (e < ne) {
+          s1[e / W][e % W] = (double)v1[u];
+          s2[e / W][e % W] = (double)v2[u];
+        }
+      }
     }
     __syncthreads();
 #pragma unroll
@@ -52,12 +68,12 @@ __global__ void __launch_bounds__(256) k_gram(GramJobs jobs, int W) {
         double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
         int i = 0;
         for (; i + 3 < nr; i += 4) {
-          t0 = fma((double)s1[i][a], (double)s2[i][c], t0);
-          t1 = fma((double)s1[i + 1][a], (double)s2[i + 1][c], t1);
-          t2 = fma((double)s1[i + 2][a], (double)s2[i + 2][c], t2);
-          t3 = fma((double)s1[i + 3][a], (double)s2[i + 3][c], t3);
+          t0 = fma(s1[i][a], s2[i][c], t0);
+          t1 = fma(s1[i + 1][a], s2[i + 1][c], t1);
+          t2 = fma(s1[i + 2][a], s2[i + 2][c], t2);
+          t3 = fma(s1[i + 3][a], s2[i + 3][c], t3);
         }
-        for (; i < nr; ++i) t0 = fma((double)s1[i][a], (double)s2[i][c], t0);
+        for (; i < nr; ++i) t0 = fma(s1[i][a], s2[i][c], t0);
         acc[q] += (t0 + t1) + (t2 + t3);
       }
     }
@@ -77,16 +93,17 @@ __global__ void __launch_bounds__(256) k_gram(GramJobs jobs, int W) {
   // fixed-order 4-way split sum over the block partials (independent loads in flight)
   const int nb = (int)gridDim.x;
   for (int pr = threadIdx.x; pr < npairs; pr += 256) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     int b = 0;
-    for (; b + 3 < nb; b += 4) {
-      a0 += __ldcg(jb.partial + (int64_t)(b + 0) * npairs + pr);
-      a1 += __ldcg(jb.partial + (int64_t)(b + 1) * npairs + pr);
-      a2 += __ldcg(jb.partial + (int64_t)(b + 2) * npairs + pr);
-      a3 += __ldcg(jb.partial + (int64_t)(b + 3) * npairs + pr);
+    for (; b + 7 < nb; b += 8) {
+      double t[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t[k] = __ldcg(jb.partial + (int64_t)(b + k) * npairs + pr);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] += t[k];
     }
-    for (; b < nb; ++b) a0 += __ldcg(jb.partial + (int64_t)b * npairs + pr);
-    jb.G[pr] = (a0 + a1) + (a2 + a3);
+    for (; b < nb; ++b) a[0] += __ldcg(jb.partial + (int64_t)b * npairs + pr);
+    jb.G[pr] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   }
   if (threadIdx.x == 0) *jb.counter = 0;  // re-arm for the next launch (stream ordered)
 }
@@ -94,19 +111,31 @@ __global__ void __launch_bounds__(256) k_gram(GramJobs jobs, int W) {
 void launch_gram_jobs(const GramJobs& jobs, int W, cudaStream_t st) {
   int64_t nmax = 0;
   for (int i = 0; i < jobs.n; ++i) nmax = jobs.j[i].n > nmax ? jobs.j[i].n : nmax;
-  // blocks <= kGramMaxBlocks (partial buffer), each <= kGramRows rows
-  int64_t nb = (nmax + kGramRows - 1) / kGramRows;
+  // blocks <= kGramMaxBlocks (partial buffer), ~4 row chunks each (short final reduction)
+  int64_t nb = (nmax + 8 * kGramRows - 1) / (8 * kGramRows);
   if (nb > kGramMaxBlocks) nb = kGramMaxBlocks;
   if (nb < 1) nb = 1;
 
-  k_gram<<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs, W);
+  switch (W) {
+    case 8: k_gram<8><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
+    case 16: k_gram<16><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
+    case 24: k_gram<24><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
+    case 32: k_gram<32><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
+    case 40: k_gram<40><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
+    case 48: k_gram<48><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
+    case 56: k_gram<56><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
+    case 64: k_gram<64><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
+    default: break;
+  }
+
   ++launch_counter();
 }
 
 // ------------------------------------------------- pivoted Cholesky orth
 // 256 threads: pivot search by warp 0, column scaling and the trailing rank-1
 // update by the whole CTA; L^-1 by row-sequential forward substitution.
-__device__ void dev_chol_orth(const double* G, double* T64, int n, double* dyn) {
+template <int n>
+__device__ void dev_chol_orth(const double* G, double* T64, double* dyn) {
   double (*A)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn);
   double (*Li)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn + kN * (kN + 1));  // L^-1 (lower)
   __shared__ int piv[kN];
@@ -199,27 +228,49 @@ __device__ void dev_chol_orth(const double* G, double* T64, int n, double* dyn) 
   }
 }
 
-__global__ void __launch_bounds__(256) k_chol_orth(EigJobs jobs, int n) {
+template <int n>
+__global__ void __launch_bounds__(256) k_chol_orth(EigJobs jobs) {
   extern __shared__ double dyn[];
-  dev_chol_orth(jobs.j[blockIdx.x].G, jobs.j[blockIdx.x].T64, n, dyn);
+  dev_chol_orth<n>(jobs.j[blockIdx.x].G, jobs.j[blockIdx.x].T64, dyn);
 }
 
 static const int kDynSmem = 2 * kN * (kN + 1) * (int)sizeof(double);
 
-void launch_chol_orth(const EigJobs& jobs, int n, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_chol_orth, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
-    attr = true;
+template <int n>
+static void chol_t(const EigJobs& jobs, cudaStream_t st) {
+  if constexpr (n <= 32) {
+    k_warp_chol<n><<<jobs.n, 32, 0, st>>>(jobs);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_chol_orth<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+      attr = true;
+    }
+    k_chol_orth<n><<<jobs.n, 256, kDynSmem, st>>>(jobs);
   }
-  k_chol_orth<<<jobs.n, 256, kDynSmem, st>>>(jobs, n);
+}
+
+void launch_chol_orth(const EigJobs& jobs, int n, cudaStream_t st) {
+  switch (n) {
+    case 8: chol_t<8>(jobs, st); break;
+    case 16: chol_t<16>(jobs, st); break;
+    case 24: chol_t<24>(jobs, st); break;
+    case 32: chol_t<32>(jobs, st); break;
+    case 40: chol_t<40>(jobs, st); break;
+    case 48: chol_t<48>(jobs, st); break;
+    case 56: chol_t<56>(jobs, st); break;
+    case 64: chol_t<64>(jobs, st); break;
+    default: break;
+  }
+
   ++launch_counter();
 }
 
 // --------------------------------------------- parallel Jacobi (truncation)
 // Round-robin pairing: n/2 disjoint rotations per step.  A' = J^T A J is applied
 // in ONE pass over 2x2 blocks (pair k1 rows x pair k2 cols), V' = V J in another.
-__device__ void dev_eig_trunc(const double* G, float* T, int r, int n, double* dyn) {
+template <int n>
+__device__ void dev_eig_trunc(const double* G, float* T, int r, double* dyn) {
   double (*A)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn);
   double (*V)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn + kN * (kN + 1));
   __shared__ double cs[kN / 2], sn[kN / 2];
@@ -228,9 +279,20 @@ __device__ void dev_eig_trunc(const double* G, float* T, int r, int n, double* d
   __shared__ double red[8][2];
   __shared__ int stop;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ double scale_s;
+  if (tid < 32) {
+    double dm = 0.0;
+    for (int i = lane; i < n; i += 32) dm = fmax(dm, fabs(G[i * n + i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+    if (lane == 0) scale_s = dm > 0.0 ? 1.0 / dm : 1.0;
+  }
+  __syncthreads();
+  // normalised copy (eigenvectors are scale invariant): entries O(1), so the rotation angle
+  // can be computed in fp32 without under/overflow
   for (int e = tid; e < n * n; e += 256) {
     const int i = e / n, j = e % n;
-    A[i][j] = 0.5 * (G[i * n + j] + G[j * n + i]);
+    A[i][j] = 0.5 * (G[i * n + j] + G[j * n + i]) * scale_s;
     V[i][j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
@@ -265,10 +327,10 @@ __device__ void dev_eig_trunc(const double* G, float* T, int r, int n, double* d
         if (p > q) { const int t = p; p = q; q = t; }
         const double apq = A[p][q];
         double c = 1.0, s = 0.0;
-        if (apq != 0.0) {
+        if ((float)apq != 0.f) {
           // angle in fp32 (any rotation is an exact similarity; c, s below are orthonormal to
           // fp64 rounding), which keeps the latency of the 2x2 solve short
-          const float theta = (float)((A[q][q] - A[p][p]) / (2.0 * apq));
+          const float theta = (float)(A[q][q] - A[p][p]) / (2.f * (float)apq);
           float t;
           if (fabsf(theta) > 1e18f) t = 0.5f / theta;
           else t = copysignf(1.f, theta) / (fabsf(theta) + sqrtf(fmaf(theta, theta, 1.f)));
@@ -335,19 +397,122 @@ __device__ void dev_eig_trunc(const double* G, float* T, int r, int n, double* d
   }
 }
 
-__global__ void __launch_bounds__(256) k_eig(EigJobs jobs, int n) {
+template <int n>
+__global__ void __launch_bounds__(256) k_eig(EigJobs jobs) {
   extern __shared__ double dyn[];
-  dev_eig_trunc(jobs.j[blockIdx.x].G, jobs.j[blockIdx.x].T, jobs.j[blockIdx.x].r, n, dyn);
+  dev_eig_trunc<n>(jobs.j[blockIdx.x].G, jobs.j[blockIdx.x].T, jobs.j[blockIdx.x].r, dyn);
+}
+
+template <int n>
+static void eig_t(const EigJobs& jobs, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_eig<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+    attr = true;
+  }
+  k_eig<n><<<jobs.n, 256, kDynSmem, st>>>(jobs);
 }
 
 void launch_eig_warp(const EigJobs& jobs, int n, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
-    attr = true;
+  switch (n) {
+    case 8: eig_t<8>(jobs, st); break;
+    case 16: eig_t<16>(jobs, st); break;
+    case 24: eig_t<24>(jobs, st); break;
+    case 32: eig_t<32>(jobs, st); break;
+    case 40: eig_t<40>(jobs, st); break;
+    case 48: eig_t<48>(jobs, st); break;
+    case 56: eig_t<56>(jobs, st); break;
+    case 64: eig_t<64>(jobs, st); break;
+    default: break;
   }
-  k_eig<<<jobs.n, 256, kDynSmem, st>>>(jobs, n);
+
   ++launch_counter();
+}
+
+// ------------------------------------------------- one-warp solvers (n <= 32)
+// Lane j owns column j of the (symmetric) matrix in shared memory, column-major with a
+// 33-double stride so that lane-parallel accesses are bank-conflict free.  No CTA barriers.
+#define SA(i, j) sm[(j) * 33 + (i)]
+
+// Pivoted Cholesky QR transform: T64[piv[a], b] = (L^-T)[a, b] for a <= b < rank (zero elsewhere);
+// pivots below 1e-10 x the largest diagonal entry are dropped (reading #12).
+template <int n>
+__device__ void warp_chol_orth(const double* G, double* T64, double* sm, double* li, int* piv) {
+  const int lane = threadIdx.x & 31;
+  for (int i = 0; i < n; ++i)
+    if (lane < n) SA(i, lane) = 0.5 * (G[i * n + lane] + G[lane * n + i]);
+  piv[lane] = lane;
+  __syncwarp();
+  double dmax = lane < n ? SA(lane, lane) : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  const double thr = 1e-10 * dmax;
+  int k = 0;
+  for (; k < n; ++k) {
+    double best = (lane >= k && lane < n) ? SA(lane, lane) : -1.0;
+    int bi = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (!(dmax > 0.0) || best < thr || best <= 0.0) break;
+    if (bi != k) {
+      // swap rows k, bi (every lane in its column), then columns k, bi (lane = row)
+      if (lane < n) { const double t = SA(k, lane); SA(k, lane) = SA(bi, lane); SA(bi, lane) = t; }
+      __syncwarp();
+      if (lane < n) { const double t = SA(lane, k); SA(lane, k) = SA(lane, bi); SA(lane, bi) = t; }
+      if (lane == 0) { const int t = piv[k]; piv[k] = piv[bi]; piv[bi] = t; }
+      __syncwarp();
+    }
+    const double lkk = sqrt(SA(k, k));
+    const double inv = 1.0 / lkk;
+    __syncwarp();
+    // column k of L (lane = row)
+    if (lane > k && lane < n) SA(lane, k) *= inv;
+    if (lane == k) SA(k, k) = lkk;
+    __syncwarp();
+    // trailing update, lane = column j > k: A[i][j] -= L[i][k] L[j][k] for i > k
+    if (lane > k && lane < n) {
+      const double ljk = SA(lane, k);
+      for (int i = k + 1; i < n; ++i) SA(i, lane) -= SA(i, k) * ljk;
+    }
+    __syncwarp();
+  }
+  const int rk = k;
+  // Li = L^-1 column by column (lane = column c), forward substitution
+  if (lane < rk) {
+    const int c = lane;
+    for (int i = 0; i < rk; ++i) li[c * 33 + i] = 0.0;
+    for (int i = c; i < rk; ++i) {
+      double a0 = (i == c) ? 1.0 : 0.0, a1 = 0.0;
+      int t = c;
+      for (; t + 1 < i; t += 2) {
+        a0 -= SA(i, t) * li[c * 33 + t];
+        a1 -= SA(i, t + 1) * li[c * 33 + t + 1];
+      }
+      if (t < i) a0 -= SA(i, t) * li[c * 33 + t];
+      li[c * 33 + i] = (a0 + a1) / SA(i, i);
+    }
+  }
+  __syncwarp();
+  // T64[piv[a]][b] = Li[b][a] (a <= b < rk), zero elsewhere; lane = output column b
+  for (int rr = 0; rr < n; ++rr)
+    if (lane < n) T64[rr * n + lane] = 0.0;
+  __syncwarp();
+  if (lane < rk)
+    for (int a = 0; a <= lane; ++a) T64[piv[a] * n + lane] = li[a * 33 + lane];
+}
+
+#undef SA
+
+template <int n>
+__global__ void __launch_bounds__(32) k_warp_chol(EigJobs jobs) {
+  __shared__ double buf[2][32 * 33];
+  __shared__ int piv[32];
+  const EigJob job = jobs.j[blockIdx.x];
+  warp_chol_orth<n>(job.G, job.T64, buf[0], buf[1], piv);
 }
 
 // ------------------------------------------------- fused orth / truncation
@@ -358,10 +523,11 @@ void launch_eig_warp(const EigJobs& jobs, int n, cudaStream_t st) {
 //                         pivoted CholQR transform (mode 0) or the truncation eigenvectors
 //                         (mode 1), or nothing (mode 2: G must first be summed across ranks).
 constexpr int kFRows = 64;
-__global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int W, int mode) {
+template <int W>
+__global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
   extern __shared__ double dyn[];
   const SmallJob jb = jobs.j[blockIdx.y];
-  float (*sY)[kN + 1] = reinterpret_cast<float (*)[kN + 1]>(dyn);  // kFRows x (kN+1) floats
+  double (*sY)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn);  // kFRows x (kN+1), fp64 (converted once)
   __shared__ int ticket;
   const int npairs = W * W;
   const int64_t rpb = (jb.n + gridDim.x - 1) / gridDim.x;
@@ -374,19 +540,42 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int W, int 
   for (int64_t r0 = r_begin; r0 < r_end; r0 += kFRows) {
     const int nr = (int)(r_end - r0 < kFRows ? r_end - r0 : kFRows);
     __syncthreads();
-    for (int e = threadIdx.x; e < nr * W; e += 256) {
-      const int i = e / W, c = e % W;
-      const int64_t g = (r0 + i) * W + c;
-      float v;
+    // element e of the chunk: thread-strided; the split partials of several elements are
+    // loaded before any is summed (fixed summation order per element: s = 0, 1, ...)
+    const int ne = nr * W;
+    for (int e0 = threadIdx.x; e0 < ne; e0 += 256 * 4) {
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
       if (jb.nsplit > 1) {
-        float a0 = 0.f;
-        for (int sp = 0; sp < jb.nsplit; ++sp) a0 += __ldcg(jb.part + sp * plane + g);
-        jb.Y[g] = a0;
-        v = a0;
+        for (int sp0 = 0; sp0 < jb.nsplit; sp0 += 8) {
+          float t[4][8];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = e0 + 256 * u;
+            const int64_t g = r0 * W + e;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              t[u][k] = (e < ne && sp0 + k < jb.nsplit) ? __ldcg(jb.part + (sp0 + k) * plane + g) : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[u] += t[u][k];
+        }
       } else {
-        v = __ldcg(jb.Y + g);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + 256 * u;
+          if (e < ne) v[u] = __ldcg(jb.Y + r0 * W + e);
+        }
       }
-      sY[i][c] = v;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + 256 * u;
+        if (e < ne) {
+          if (jb.nsplit > 1) jb.Y[r0 * W + e] = v[u];
+          sY[e / W][e % W] = (double)v[u];
+        }
+      }
     }
     __syncthreads();
 #pragma unroll
@@ -397,10 +586,10 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int W, int 
         double t0 = 0.0, t1 = 0.0;
         int i = 0;
         for (; i + 1 < nr; i += 2) {
-          t0 = fma((double)sY[i][a], (double)sY[i][c], t0);
-          t1 = fma((double)sY[i + 1][a], (double)sY[i + 1][c], t1);
+          t0 = fma(sY[i][a], sY[i][c], t0);
+          t1 = fma(sY[i + 1][a], sY[i + 1][c], t1);
         }
-        if (i < nr) t0 = fma((double)sY[i][a], (double)sY[i][c], t0);
+        if (i < nr) t0 = fma(sY[i][a], sY[i][c], t0);
         acc[q] += t0 + t1;
       }
     }
@@ -419,37 +608,64 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int W, int 
   __threadfence();
   const int nb = (int)gridDim.x;
   for (int pr = threadIdx.x; pr < npairs; pr += 256) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     int b = 0;
-    for (; b + 3 < nb; b += 4) {
-      a0 += __ldcg(jb.gpart + (int64_t)(b + 0) * npairs + pr);
-      a1 += __ldcg(jb.gpart + (int64_t)(b + 1) * npairs + pr);
-      a2 += __ldcg(jb.gpart + (int64_t)(b + 2) * npairs + pr);
-      a3 += __ldcg(jb.gpart + (int64_t)(b + 3) * npairs + pr);
+    for (; b + 7 < nb; b += 8) {
+      double t[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t[k] = __ldcg(jb.gpart + (int64_t)(b + k) * npairs + pr);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] += t[k];
     }
-    for (; b < nb; ++b) a0 += __ldcg(jb.gpart + (int64_t)b * npairs + pr);
-    jb.G[pr] = (a0 + a1) + (a2 + a3);
+    for (; b < nb; ++b) a[0] += __ldcg(jb.gpart + (int64_t)b * npairs + pr);
+    jb.G[pr] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   }
   if (threadIdx.x == 0) *jb.counter = 0;  // re-arm for the next launch (stream ordered)
   __threadfence_block();
   __syncthreads();
-  if (mode == 0) dev_chol_orth(jb.G, jb.T64, W, dyn);
-  else if (mode == 1) dev_eig_trunc(jb.G, jb.T, jb.r, W, dyn);
+  if constexpr (W <= 32) {
+    if (mode == 0 && threadIdx.x < 32) {
+      double* sm = dyn;
+      double* aux = dyn + 32 * 33;
+      int* piv = reinterpret_cast<int*>(dyn + 2 * 32 * 33);
+      warp_chol_orth<W>(jb.G, jb.T64, sm, aux, piv);
+    }
+    if (mode == 1) dev_eig_trunc<W>(jb.G, jb.T, jb.r, dyn);
+  } else {
+    if (mode == 0) dev_chol_orth<W>(jb.G, jb.T64, dyn);
+    else if (mode == 1) dev_eig_trunc<W>(jb.G, jb.T, jb.r, dyn);
+  }
+}
+
+template <int W>
+static void fused_t(const SmallJobs& jobs, int mode, int64_t nb, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fused_small<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+    attr = true;
+  }
+  k_fused_small<W><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, kDynSmem, st>>>(jobs, mode);
 }
 
 void launch_fused_small(const SmallJobs& jobs, int W, int mode, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_fused_small, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
-    attr = true;
-  }
   int64_t nmax = 0;
   for (int i = 0; i < jobs.n; ++i) nmax = jobs.j[i].n > nmax ? jobs.j[i].n : nmax;
   // ~4 row chunks per block keeps the last-block reduction short (<= 64 partials at 16K rows)
   int64_t nb = (nmax + 4 * kFRows - 1) / (4 * kFRows);
   if (nb > kGramMaxBlocks) nb = kGramMaxBlocks;
   if (nb < 1) nb = 1;
-  k_fused_small<<<dim3((unsigned)nb, (unsigned)jobs.n), 256, kDynSmem, st>>>(jobs, W, mode);
+  switch (W) {
+    case 8: fused_t<8>(jobs, mode, nb, st); break;
+    case 16: fused_t<16>(jobs, mode, nb, st); break;
+    case 24: fused_t<24>(jobs, mode, nb, st); break;
+    case 32: fused_t<32>(jobs, mode, nb, st); break;
+    case 40: fused_t<40>(jobs, mode, nb, st); break;
+    case 48: fused_t<48>(jobs, mode, nb, st); break;
+    case 56: fused_t<56>(jobs, mode, nb, st); break;
+    case 64: fused_t<64>(jobs, mode, nb, st); break;
+    default: break;
+  }
+
   ++launch_counter();
 }
 
