@@ -94,12 +94,12 @@ lrqmm_status_t lrqmm_get_unique_id(unsigned char out[128]);
  * SHAPE, RANK, OVERFLOW, UNSUPPORTED, ALLOC, CUDA, NCCL. */
 lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out);
 
-/* Quantize one operand: X is A (m x k, ld ldx) or B^T (n x k, ld ldx), fp32.
+/* Quantize one operand: X is A (m x k, ld ldx) or B^T (n x k, ld ldx), fp32, any alignment.
  * Eq. quantA with lambda_i = RN32(qmax / max_j |x_ij|) (lambda = 1 for a zero row),
  * codes = clamp(round_mode(lambda_i * x_ij), -qmax, qmax) decided on the exact product
- * (Alg. 2).  X is RETAINED (not copied): it must stay unmodified
- * until the lrqmm_rsvd_residual work for this side has completed in stream order, because
- * the residual R = X - X_int/lambda (Alg. 2) is recomputed from it. */
+ * (Alg. 2).  When rank > 0 the same pass also stores the residual
+ * fraction u = lambda x - code (R = u / lambda, Alg. 2) in a handle-owned
+ * buffer, so X is not referenced after this call's work completes in stream order. */
 lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* X, int64_t ldx);
 
 /* RSVD of both residuals (Alg. 2) and assembly of the

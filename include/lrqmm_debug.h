@@ -13,14 +13,14 @@
 extern "C" {
 #endif
 
-/* Skinny residual products of the RSVD (K2/K3), X: rows x K (ld ldx), lam: rows scales.
+/* Skinny residual products of the RSVD (K2/K3) of a side X: rows x K (ld ldx), quantized
+ * per row by K1 (bits, rounding) inside the call:
  *   mode 0: OUT  = R P            (P: K x W, OUT: rows x W)
  *   mode 1: OUT  = R^T P          (P: rows x W, OUT: K x W)
  *   mode 2: OUT  = R P, OUT2 = X~ P2  (dual pass; X~ = code / lambda)
  * with R = X - code/lambda, code = clamp(round_mode(lambda x)) (Alg. 2). */
-lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx, int64_t rows, int K, const float* lam,
-                                int bits, int rounding, const float* P, const float* P2, int W, float* OUT,
-                                float* OUT2, void* stream);
+lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx, int64_t rows, int K, int bits, int rounding,
+                                const float* P, const float* P2, int W, float* OUT, float* OUT2, void* stream);
 
 /* Small solvers (K4) on Y (n x W):
  *   op 0: G = Y^T Y (fp64, W x W)

@@ -24,23 +24,25 @@ struct QuantArgs {
   float* inv_lam;         // rows: RN(1/lambda) (written unless lam_fixed)
   const float* lam_fixed; // device scalar (per-tensor mode) or nullptr
   int* err_flag;          // bit 0: non-finite input
+  float* U;               // rows x ldu residual fraction u = lambda x - code (or nullptr)
+  int64_t ldu;            // multiple of 4, >= K
 };
 void launch_quantize(const QuantArgs& a, cudaStream_t st);
 void launch_tensor_scale(const float* X, int64_t ldx, int64_t rows, int K, int qmax, float* row_amax,
                          float* lam_rows, float* inv_rows, float* lam_scalar, int* err_flag, cudaStream_t st);
 
 // ------------------------------------------------- K2/K3 skinny residual products
-// F(x_ij) is recomputed from X and lambda_i (never stored):
-//   residual  r = (lambda*x - code)/lambda            (Alg. 2)
-//   codes     c (exact in tf32), scaled by 1/lambda   (Alg. 2)
+// The passes stream the residual fraction u = lambda x - code written by K1 (R = u / lambda,
+// Alg. 2) and, for the cross products, the codes (X~ = code / lambda, line 352).
 struct SideView {
-  const float* X;
-  int64_t ldx;
+  const float* U;        // rows x ldu fp32
+  int64_t ldu;
   int64_t rows;
   int K;
+  const int8_t* codes;   // rows x Kp
+  int Kp;
   const float* lam;
   const float* inv_lam;  // RN(1/lambda)
-  int qmax, mode;
 };
 // tcgen05 kind::tf32 (3-term split) passes, deterministic split-K partials; return the split count.
 // With reduce1 == false and > 1 splits, OUT1 stays as partials at `partial` (consumed by the fused

@@ -22,9 +22,8 @@ constexpr int kMaxWidth = 64;
 
 struct Side {
   int64_t rows = 0;
-  const float* X = nullptr;  // caller's fp32 operand (retained, not copied) or the aligned stage
-  int64_t ldx = 0;
-  float* stage = nullptr;    // aligned copy, only for layouts TMA cannot address
+  int64_t ldu = 0;
+  float* U = nullptr;        // rows x ldu residual fraction u = lambda x - code (written by K1)
   int8_t* codes = nullptr;   // rows x Kp
   float* lam = nullptr;      // rows
   float* inv_lam = nullptr;  // rows, RN(1/lambda)
@@ -164,7 +163,7 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   for (auto& s : h->s) {
     cudaFree(s.codes); cudaFree(s.lam); cudaFree(s.inv_lam); cudaFree(s.row_amax); cudaFree(s.lam_scalar); cudaFree(s.Om);
     cudaFree(s.Y); cudaFree(s.Q0); cudaFree(s.Z); cudaFree(s.Q1); cudaFree(s.Gp); cudaFree(s.G);
-    cudaFree(s.gpart); cudaFree(s.counter); cudaFree(s.T64); cudaFree(s.VW); cudaFree(s.stage);
+    cudaFree(s.gpart); cudaFree(s.counter); cudaFree(s.T64); cudaFree(s.VW); cudaFree(s.U);
   }
   cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->partial); cudaFree(h->Gcross); cudaFree(h->gpart_cross);
   cudaFree(h->counter_cross); cudaFree(h->VWbM); cudaFree(h->err_flag);
@@ -207,7 +206,8 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
     ok = ok && dalloc(&s.codes, s.rows * h->Kp) && dalloc(&s.lam, s.rows) && dalloc(&s.inv_lam, s.rows) && dalloc(&s.row_amax, s.rows) &&
          dalloc(&s.lam_scalar, 1);
     if (h->W > 0) {
-      ok = ok && dalloc(&s.Om, K * h->W) && dalloc(&s.Y, s.rows * h->W) && dalloc(&s.Q0, s.rows * h->W) &&
+      s.ldu = (K + 3) / 4 * 4;
+      ok = ok && dalloc(&s.U, s.rows * s.ldu) && dalloc(&s.Om, K * h->W) && dalloc(&s.Y, s.rows * h->W) && dalloc(&s.Q0, s.rows * h->W) &&
            dalloc(&s.Z, K * h->W) && dalloc(&s.Q1, K * h->W) && dalloc(&s.Gp, s.rows * h->W) &&
            dalloc(&s.G, (int64_t)h->W * h->W) && dalloc(&s.gpart, (int64_t)kGramMaxBlocks * h->W * h->W) &&
            dalloc(&s.counter, 1) && dalloc(&s.T64, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W);
@@ -272,25 +272,14 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
   Side& s = h->s[side];
   if ((!X && s.rows > 0 && h->cfg.k > 0) || ldx < h->cfg.k) return LRQMM_ERR_INVALID_ARGUMENT;
   cudaSetDevice(h->cfg.device);
-  s.X = X;
-  s.ldx = ldx;
   record(h, side == LRQMM_SIDE_A ? 0 : 2);
-  // the RSVD passes stream X with TMA: 16-byte aligned base and row stride required
-  if (h->W > 0 && s.rows > 0 && h->cfg.k > 0 && ((reinterpret_cast<uintptr_t>(X) & 15) != 0 || (ldx % 4) != 0)) {
-    const int64_t lds = (h->cfg.k + 3) / 4 * 4;
-    if (!s.stage && !dalloc(&s.stage, s.rows * lds)) return fail(h, LRQMM_ERR_ALLOC);
-    LQ_CUDA(cudaMemcpy2DAsync(s.stage, sizeof(float) * lds, X, sizeof(float) * ldx, sizeof(float) * h->cfg.k, s.rows,
-                              cudaMemcpyDeviceToDevice, h->st));
-    s.X = s.stage;
-    s.ldx = lds;
-  }
   if (h->cfg.granularity == LRQMM_SCALE_PER_TENSOR) {
-    launch_tensor_scale(s.X, s.ldx, s.rows, (int)h->cfg.k, h->qmax, s.row_amax, s.lam, s.inv_lam, s.lam_scalar, h->err_flag,
+    launch_tensor_scale(X, ldx, s.rows, (int)h->cfg.k, h->qmax, s.row_amax, s.lam, s.inv_lam, s.lam_scalar, h->err_flag,
                         h->st);
   }
   QuantArgs a;
-  a.X = s.X;
-  a.ldx = s.ldx;
+  a.X = X;
+  a.ldx = ldx;
   a.rows = s.rows;
   a.K = (int)h->cfg.k;
   a.Kp = h->Kp;
@@ -301,6 +290,8 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
   a.inv_lam = s.inv_lam;
   a.lam_fixed = h->cfg.granularity == LRQMM_SCALE_PER_TENSOR ? s.lam_scalar : nullptr;
   a.err_flag = h->err_flag;
+  a.U = s.U;  // residual fractions for the RSVD passes (rank > 0 only)
+  a.ldu = s.ldu;
   if (s.rows > 0) launch_quantize(a, h->st);
   record(h, side == LRQMM_SIDE_A ? 1 : 3);
   lrqmm_status_t e = check_launch(h);
@@ -312,14 +303,14 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
 
 static SideView view(lrqmm_handle_t h, int sd) {
   SideView v;
-  v.X = h->s[sd].X;
-  v.ldx = h->s[sd].ldx;
+  v.U = h->s[sd].U;
+  v.ldu = h->s[sd].ldu;
   v.rows = h->s[sd].rows;
   v.K = (int)h->cfg.k;
+  v.codes = h->s[sd].codes;
+  v.Kp = h->Kp;
   v.lam = h->s[sd].lam;
   v.inv_lam = h->s[sd].inv_lam;
-  v.qmax = h->qmax;
-  v.mode = h->cfg.rounding;
   return v;
 }
 
@@ -600,35 +591,36 @@ int64_t lrqmm_launch_count(lrqmm_handle_t h, int reset) {
 // ------------------------------------------------------------- test hooks
 #include "../../include/lrqmm_debug.h"
 
-extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx, int64_t rows, int K,
-                                           const float* lam, int bits, int rounding, const float* P, const float* P2,
-                                           int W, float* OUT, float* OUT2, void* stream) {
+extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx, int64_t rows, int K, int bits,
+                                           int rounding, const float* P, const float* P2, int W, float* OUT,
+                                           float* OUT2, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  float* stage = nullptr;
-  if ((reinterpret_cast<uintptr_t>(X) & 15) != 0 || (ldx % 4) != 0) {
-    const int64_t lds = ((int64_t)K + 3) / 4 * 4;
-    if (cudaMalloc(&stage, sizeof(float) * rows * lds) != cudaSuccess) return LRQMM_ERR_ALLOC;
-    cudaMemcpy2DAsync(stage, sizeof(float) * lds, X, sizeof(float) * ldx, sizeof(float) * K, rows,
-                      cudaMemcpyDeviceToDevice, st);
-    X = stage;
-    ldx = lds;
-  }
-  float* inv = nullptr;
-  if (cudaMalloc(&inv, sizeof(float) * (rows > 0 ? rows : 1)) != cudaSuccess) return LRQMM_ERR_ALLOC;
-  launch_recip(lam, inv, rows, st);
-  SideView v{X, ldx, rows, K, lam, inv, (1 << (bits - 1)) - 1, rounding};
+  const int Kp = (int)roundup(K > 0 ? K : 1, 128);
+  const int64_t ldu = ((int64_t)K + 3) / 4 * 4;
   const int64_t pe = (int64_t)16 << 20;
-  float* partial = nullptr;
-  if (cudaMalloc(&partial, sizeof(float) * pe) != cudaSuccess) return LRQMM_ERR_ALLOC;
-  if (mode == 0) launch_tc_proj_rows(v, P, OUT, nullptr, nullptr, W, partial, pe, true, st);
-  else if (mode == 1) launch_tc_proj_cols(v, P, OUT, W, partial, pe, true, st);
-  else launch_tc_proj_rows(v, P, OUT, P2, OUT2, W, partial, pe, true, st);
-  cudaError_t e = cudaStreamSynchronize(st);
-  if (e == cudaSuccess) e = cudaGetLastError();
-  cudaFree(partial);
-  cudaFree(inv);
-  if (stage) cudaFree(stage);
-  return e == cudaSuccess ? LRQMM_OK : LRQMM_ERR_CUDA;
+  float *U = nullptr, *lam = nullptr, *inv = nullptr, *partial = nullptr;
+  int8_t* codes = nullptr;
+  int* flag = nullptr;
+  bool ok = cudaMalloc(&U, sizeof(float) * rows * ldu) == cudaSuccess &&
+            cudaMalloc(&lam, sizeof(float) * rows) == cudaSuccess && cudaMalloc(&inv, sizeof(float) * rows) == cudaSuccess &&
+            cudaMalloc(&codes, (size_t)rows * Kp) == cudaSuccess && cudaMalloc(&flag, sizeof(int)) == cudaSuccess &&
+            cudaMalloc(&partial, sizeof(float) * pe) == cudaSuccess;
+  cudaError_t e = cudaErrorMemoryAllocation;
+  if (ok) {
+    cudaMemsetAsync(flag, 0, sizeof(int), st);
+    QuantArgs q{};
+    q.X = X; q.ldx = ldx; q.rows = rows; q.K = K; q.Kp = Kp; q.qmax = (1 << (bits - 1)) - 1; q.mode = rounding;
+    q.codes = codes; q.lam = lam; q.inv_lam = inv; q.lam_fixed = nullptr; q.err_flag = flag; q.U = U; q.ldu = ldu;
+    launch_quantize(q, st);
+    SideView v{U, ldu, rows, K, codes, Kp, lam, inv};
+    if (mode == 0) launch_tc_proj_rows(v, P, OUT, nullptr, nullptr, W, partial, pe, true, st);
+    else if (mode == 1) launch_tc_proj_cols(v, P, OUT, W, partial, pe, true, st);
+    else launch_tc_proj_rows(v, P, OUT, P2, OUT2, W, partial, pe, true, st);
+    e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+  }
+  cudaFree(U); cudaFree(lam); cudaFree(inv); cudaFree(codes); cudaFree(flag); cudaFree(partial);
+  return e == cudaSuccess ? LRQMM_OK : (ok ? LRQMM_ERR_CUDA : LRQMM_ERR_ALLOC);
 }
 
 extern "C" lrqmm_status_t lrqmm_debug_small(int op, const float* Y, int64_t n, int W, int r, double* G, float* T,

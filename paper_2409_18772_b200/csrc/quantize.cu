@@ -55,7 +55,8 @@ template <int TPR, int VPT, bool kVec, bool kFixedLam>
 __global__ void __launch_bounds__(256) k1_quantize(const float* __restrict__ X, int64_t ldx, int rows, int K, int Kp,
                                                    int qmax, int mode, int8_t* __restrict__ codes,
                                                    float* __restrict__ lam_out, float* __restrict__ inv_out,
-                                                   const float* __restrict__ lam_in, int* __restrict__ err_flag) {
+                                                   const float* __restrict__ lam_in, int* __restrict__ err_flag,
+                                                   float* __restrict__ U, int64_t ldu) {
   constexpr int kRowsPerCta = 256 / TPR;
   constexpr int kWarpsPerRow = TPR / 32;
   __shared__ float red[8];
@@ -111,13 +112,21 @@ __global__ void __launch_bounds__(256) k1_quantize(const float* __restrict__ X, 
         inv_out[row] = __frcp_rn(lam);
       }
       uint32_t* crow = reinterpret_cast<uint32_t*>(codes + row * (int64_t)Kp);
+      float* urow = U ? U + row * ldu : nullptr;
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
         const int col = (sub + i * TPR) * 4;
         if (col < Kp) {
           // padded columns (K <= col < Kp) hold x = 0 -> code 0
-          crow[col >> 2] = pack4(code_of(lam, v[i].x, mode, qmax), code_of(lam, v[i].y, mode, qmax),
-                                 code_of(lam, v[i].z, mode, qmax), code_of(lam, v[i].w, mode, qmax));
+          const int8_t c0 = code_of(lam, v[i].x, mode, qmax), c1 = code_of(lam, v[i].y, mode, qmax);
+          const int8_t c2 = code_of(lam, v[i].z, mode, qmax), c3 = code_of(lam, v[i].w, mode, qmax);
+          crow[col >> 2] = pack4(c0, c1, c2, c3);
+          // residual fraction u = lambda x - code (R = u / lambda, Alg. 2), exactly rounded
+          if (urow && col < ldu) {
+            const float4 u = make_float4(__fmaf_rn(lam, v[i].x, -(float)c0), __fmaf_rn(lam, v[i].y, -(float)c1),
+                                         __fmaf_rn(lam, v[i].z, -(float)c2), __fmaf_rn(lam, v[i].w, -(float)c3));
+            __stcg(reinterpret_cast<float4*>(urow + col), u);
+          }
         }
       }
     }
@@ -180,7 +189,8 @@ __global__ void __launch_bounds__(1024) k1_tensor_scale(const float* __restrict_
 __global__ void __launch_bounds__(256) k1_quantize_long(const float* __restrict__ X, int64_t ldx, int rows, int K,
                                                         int Kp, int qmax, int mode, int8_t* __restrict__ codes,
                                                         float* __restrict__ lam_out, float* __restrict__ inv_out,
-                                                        const float* __restrict__ lam_in, int* __restrict__ err_flag) {
+                                                        const float* __restrict__ lam_in, int* __restrict__ err_flag,
+                                                        float* __restrict__ U, int64_t ldu) {
   __shared__ float red[8];
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
     const float* xr = X + row * ldx;
@@ -209,7 +219,12 @@ __global__ void __launch_bounds__(256) k1_quantize_long(const float* __restrict_
       }
     }
     int8_t* crow = codes + row * (int64_t)Kp;
-    for (int c = threadIdx.x; c < Kp; c += 256) crow[c] = (c < K) ? code_of(lam, xr[c], mode, qmax) : (int8_t)0;
+    for (int c = threadIdx.x; c < Kp; c += 256) {
+      const float x = c < K ? xr[c] : 0.f;
+      const int8_t q = code_of(lam, x, mode, qmax);
+      crow[c] = q;
+      if (U && c < ldu) U[row * ldu + c] = __fmaf_rn(lam, x, -(float)q);
+    }
   }
 }
 
@@ -221,7 +236,7 @@ static void launch_k1_t(const QuantArgs& a, bool vec, bool fixed, cudaStream_t s
   if (grid < 1) grid = 1;
 #define K1_LAUNCH(V, F)                                                                                  \
   k1_quantize<TPR, VPT, V, F><<<grid, 256, 0, st>>>(a.X, a.ldx, a.rows, a.K, a.Kp, a.qmax, a.mode, a.codes, \
-                                                    a.lam, a.inv_lam, a.lam_fixed, a.err_flag)
+                                                    a.lam, a.inv_lam, a.lam_fixed, a.err_flag, a.U, a.ldu)
   if (vec) {
     if (fixed) K1_LAUNCH(true, true); else K1_LAUNCH(true, false);
   } else {
@@ -248,7 +263,7 @@ void launch_quantize(const QuantArgs& a, cudaStream_t st) {
   else {
     int grid = a.rows < 148 * 16 ? (int)a.rows : 148 * 16;
     k1_quantize_long<<<grid, 256, 0, st>>>(a.X, a.ldx, a.rows, a.K, a.Kp, a.qmax, a.mode, a.codes, a.lam,
-                                           a.inv_lam, a.lam_fixed, a.err_flag); ++launch_counter();
+                                           a.inv_lam, a.lam_fixed, a.err_flag, a.U, a.ldu); ++launch_counter();
   }
 }
 

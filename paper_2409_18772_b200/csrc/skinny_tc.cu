@@ -2,24 +2,24 @@
 // residual (Algorithm 1 sampling / power iteration / projection, PAPER.md:124-140,
 // reading #11) and the cross products of Algorithm 2, computed as
 // tcgen05.mma kind::tf32 with a 3-term split (x = hi + lo, hi = tf32(x)):
-//     F(X) P ~= F_hi P_hi + F_hi P_lo + F_lo P_hi          (fp32-grade)
-// The operand F(X) (residual R, or the quantization codes) is recomputed from the
-// fp32 side X and lambda: X is read from HBM exactly once per pass, which is this
-// kernel's roofline (bytes per element = 4).
+//     U P ~= U_hi P_hi + U_hi P_lo + U_lo P_hi                 (fp32-grade)
+// U is the residual fraction u = lambda x - code written by K1 (R = diag(1/lambda) U),
+// so every pass streams 4 B per element from HBM — this kernel's roofline — and the
+// producer warps only split u into tf32 hi/lo operand tiles.
 //
-//   ROW mode  OUT1[i,:] = sum_j R[i,j] P1[j,:]          (S1: Y = R Omega, S3: W = R Q1)
-//             OUT2[i,:] = (1/lambda_i) sum_j C[i,j] P2[j,:]   (dual: A~ Q1_other, codes exact in tf32)
-//             A operand = F(X) tile, K-major SW128; B = P tile, MN-major SW128_BASE32B.
-//   COL mode  OUT[j,:]  = sum_i R[i,j] P[i,:]            (S2: Z = R^T Q0)
-//             A operand = R tile, MN-major SW128_BASE32B (X's natural layout); B as above.
+//   ROW mode  OUT1[i,:] = (1/lambda_i) sum_j U[i,j] P1[j,:]      (S1: Y = R Omega, S3: W = R Q1)
+//             OUT2[i,:] = (1/lambda_i) sum_j C[i,j] P2[j,:]      (dual: A~ Q1_other, codes exact in tf32)
+//             A operand = U tile, K-major SW128; B = P tile, MN-major SW128_BASE32B.
+//   COL mode  OUT[j,:]  = sum_i U[i,j] (P[i,:] / lambda_i)       (S2: Z = R^T Q0)
+//             A operand = U tile, MN-major SW128_BASE32B (U's natural layout); B as above.
 //
-// Persistent, warp-specialised (448 threads, one CTA per SM):
-//   warp 13    : TMA issuer, streams raw X tiles (16 KB) through a 3-4 deep smem ring
-//   warps 0-7  : producers: raw X -> F(X) -> hi/lo split -> UMMA operand tiles (2 stages)
-//   warp 12    : TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 8-11 : epilogue: TMEM (double-buffered accumulators) -> split-K partials
-// Work unit = (128-row/col block, reduction split); partials are summed in a fixed
-// order by k_reduce_splits_tc (deterministic, no float atomics).
+// Persistent, warp-specialised (704 threads, one CTA per SM):
+//   warp 21    : TMA issuer, streams raw tiles (U 16 KB, P, codes, 1/lambda) through a smem ring
+//   warps 0-15 : producers: raw U -> tf32 hi/lo operand tiles (+ codes -> fp32) (2-3 stages)
+//   warp 20    : TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 16-19: epilogue: TMEM (double-buffered accumulators) -> split-K partials
+// Work unit = (128-row/col block, reduction split); partials are summed in a fixed order
+// by the consumer (deterministic, no float atomics).
 #include <cuda.h>
 
 #include <cstring>
@@ -30,34 +30,36 @@
 namespace lrqmm {
 
 namespace tcp {
-constexpr int BM_ = 128;
-constexpr int kProd = 512;              // 16 producer warps
+constexpr int BM = 128;  // output rows (ROW) / output cols (COL) per unit
+constexpr int BK = 32;   // reduction elements per k-block
+constexpr int kProd = 512;  // 16 producer warps
 constexpr int kProdWarps = kProd / 32;
-constexpr int kEpiWarp0 = kProdWarps;    // 4 epilogue warps
 constexpr int kMmaWarp = kProdWarps + 4;
 constexpr int kTmaWarp = kProdWarps + 5;
 constexpr int kThreads = (kProdWarps + 6) * 32;  // 704
-constexpr int kPer = BM_ * 32 / 4 / kProd;       // float4 of X per producer thread per k-block
-constexpr int BM = 128;  // output rows (ROW) / output cols (COL) per unit
-constexpr int BK = 32;   // reduction elements per k-block
+constexpr int kPer = BM * BK / 4 / kProd;        // float4 of U per producer thread per k-block (2)
 #ifndef LRQMM_OPST
 #define LRQMM_OPST 2
 #endif
-constexpr int OPST_MAX = LRQMM_OPST;  // operand stages (reduced per config to fit smem)
-constexpr int kATile = BM * BK * 4;    // 16 KB
-constexpr int kRawTile = BM * BK * 4;  // 16 KB
+constexpr int OPST_MAX = LRQMM_OPST;
+constexpr int kATile = BM * BK * 4;    // 16 KB operand tile (hi or lo)
+constexpr int kRawTile = BM * BK * 4;  // 16 KB raw U tile
+constexpr int kRawCodes = BM * BK;     // 4 KB raw code tile (dual)
 template <int kMode, int NA, bool kDual>
 struct Cfg {
   static constexpr int WN = 32 * NA;
   static constexpr int kBTile = BK * WN * 4;  // operand B tile (hi or lo)
   static constexpr int kStage = (kDual ? 3 : 2) * kATile + (kDual ? 4 : 2) * kBTile;
-  // raw slot: X tile | P1 tile [BK][WN] | P2 tile | (COL) lambda[BK], 1/lambda[BK]
+  // raw slot: U tile | P1 tile [BK][WN] | P2 tile | codes tile (dual) | 1/lambda[BK] (COL)
   static constexpr int kRawP = BK * WN * 4;
-  static constexpr int kRawBytes = kRawTile + (kDual ? 2 : 1) * kRawP + (kMode == 1 ? 2 * BK * 4 : 0);
+  static constexpr int kOffP2 = kRawTile + kRawP;
+  static constexpr int kOffCodes = kRawTile + (kDual ? 2 : 1) * kRawP;
+  static constexpr int kOffInv = kOffCodes + (kDual ? kRawCodes : 0);
+  static constexpr int kRawBytes = kOffInv + (kMode == 1 ? BK * 4 : 0);
   static constexpr int kRawSlot = (kRawBytes + 1023) / 1024 * 1024;
   static constexpr int kBudget = 220 * 1024;
-  static constexpr int fits(int op, int raw) { return op * kStage + raw * kRawSlot <= kBudget; }
-  static constexpr int OPST = fits(OPST_MAX, 3) ? OPST_MAX : 2;
+  static constexpr bool fits(int op, int raw) { return op * kStage + raw * kRawSlot <= kBudget; }
+  static constexpr int OPST = fits(OPST_MAX, 3) ? OPST_MAX : (fits(2, 2) ? 2 : 1);
   static constexpr int kRawSt = fits(OPST, 4) ? 4 : (fits(OPST, 3) ? 3 : 2);
   static constexpr int kSmem = kRawSt * kRawSlot + OPST * kStage + 256 + 1024;
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
@@ -68,15 +70,9 @@ struct Cfg {
 }  // namespace tcp
 
 struct TcArgs {
-  const float* X;
-  int64_t ldx;
   int64_t rows;
   int K;
-  const float* lam;
   const float* inv_lam;
-  int qmax, mode;
-  const float* P1;  // ROW: K x W ; COL: rows x W
-  const float* P2;  // ROW dual: K x W
   int W;
   float* out1;  // partial base: split s at out + s * (nout * W)
   float* out2;
@@ -85,27 +81,10 @@ struct TcArgs {
   int nblk, nsplit;
 };
 
-LRQMM_DEV float codef(float lam, float x, int mode, int qmax) {
-  const float p = __fmul_rn(lam, x);
-  const float e = __fmaf_rn(lam, x, -p);
-  float c;
-  if (mode == kRoundFloor) {
-    c = floorf(p);
-    if (p == c && (e < 0.f || (p == 0.f && x < 0.f))) c -= 1.f;
-  } else if (mode == kRoundTrunc) {
-    c = truncf(p);
-    if (p == c && p != 0.f) {
-      if (p > 0.f && e < 0.f) c -= 1.f;
-      if (p < 0.f && e > 0.f) c += 1.f;
-    }
-  } else {
-    c = rintf(p);
-    const float fl = floorf(p);
-    if (p - fl == 0.5f && e != 0.f) c = (e > 0.f) ? fl + 1.f : fl;
-  }
-  const float q = static_cast<float>(qmax);
-  return fminf(fmaxf(c, -q), q);
-}
+struct TcMaps {
+  CUtensorMap u, p1, p2, codes, inv;
+};
+
 LRQMM_DEV float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
 // tf32 operands: K-major uses SWIZZLE_128B (type 2); MN-major must use
@@ -133,6 +112,11 @@ LRQMM_DEV void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32
       : "memory");
 }
 LRQMM_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+LRQMM_DEV uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
 
 // byte offset of element (mn, k) in an MN-major SW128_BASE32B tile with nA 32-wide MN atoms
 // (LBO = 512 B between MN atoms, SBO = nA * 512 B between 4-deep K groups)
@@ -148,10 +132,6 @@ LRQMM_DEV uint32_t off_k(int mn, int k) {
   return (uint32_t)((mn >> 3) * 1024 + row * 128 + ((chunk ^ row) << 4) + ((k & 3) << 2));
 }
 
-struct TcMaps {
-  CUtensorMap x, p1, p2, lam, inv;
-};
-
 template <int kMode, int NA, bool kDual>
 __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_constant__ TcMaps maps, TcArgs a) {
   using namespace tcp;
@@ -161,10 +141,10 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   constexpr int kStage = C::kStage;
   constexpr int RST = C::kRawSt;
   constexpr int OPST = C::OPST;
+  constexpr int kRawSlot = C::kRawSlot;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int kRawSlot = C::kRawSlot;
-  uint8_t* sRaw = smem;                  // RST raw slots (X, P, lambda tiles by TMA)
+  uint8_t* sRaw = smem;                  // RST raw slots (TMA)
   uint8_t* sOp = smem + RST * kRawSlot;  // OPST x kStage operand tiles
   uint64_t* bars = reinterpret_cast<uint64_t*>(sOp + OPST * kStage);
   uint64_t* rfull = bars;            // RST
@@ -209,11 +189,14 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   };
 
   if (warp == kTmaWarp) {
-    // --------------------------------------------------------- TMA: raw X tiles
+    // ------------------------------------------------------ TMA: raw tiles
     if (lane == 0) {
-      tma_prefetch_desc(&maps.x);
+      tma_prefetch_desc(&maps.u);
       tma_prefetch_desc(&maps.p1);
-      if (kDual) tma_prefetch_desc(&maps.p2);
+      if (kDual) {
+        tma_prefetch_desc(&maps.p2);
+        tma_prefetch_desc(&maps.codes);
+      }
       int it = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         int blk, split, nkb;
@@ -225,51 +208,42 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
           uint8_t* slot = sRaw + s * kRawSlot;
           mbar_arrive_expect_tx(&rfull[s], C::kRawBytes);
           const int k0 = (int)(r0 + (int64_t)kb * BK);
-          if (kMode == 0) tma_load_2d(slot, &maps.x, &rfull[s], k0, blk * BM);
-          else tma_load_2d(slot, &maps.x, &rfull[s], blk * BM, k0);
+          if (kMode == 0) tma_load_2d(slot, &maps.u, &rfull[s], k0, blk * BM);
+          else tma_load_2d(slot, &maps.u, &rfull[s], blk * BM, k0);
           tma_load_2d(slot + kRawTile, &maps.p1, &rfull[s], 0, k0);
-          if (kDual) tma_load_2d(slot + kRawTile + C::kRawP, &maps.p2, &rfull[s], 0, k0);
-          if (kMode == 1) {
-            tma_load_1d(slot + kRawTile + C::kRawP, &maps.lam, &rfull[s], k0);
-            tma_load_1d(slot + kRawTile + C::kRawP + BK * 4, &maps.inv, &rfull[s], k0);
+          if (kDual) {
+            tma_load_2d(slot + C::kOffP2, &maps.p2, &rfull[s], 0, k0);
+            tma_load_2d(slot + C::kOffCodes, &maps.codes, &rfull[s], k0, blk * BM);
           }
+          if (kMode == 1) tma_load_1d(slot + C::kOffInv, &maps.inv, &rfull[s], k0);
         }
       }
     }
     __syncwarp();
   } else if (warp < kProdWarps) {
-    // --------------------------------------------------------------- producers
+    // ------------------------------------------------------------ producers
+    constexpr int kPB4 = BK * WN / 4;
+    constexpr int kPBper = (kPB4 + kProd - 1) / kProd;
     int it = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       int blk, split, nkb;
       int64_t r0;
       unit_range(u, blk, split, r0, nkb);
-      const int64_t o0 = (int64_t)blk * BM;
-      const int64_t r1 = r0 + a.chunk < r_len ? r0 + a.chunk : r_len;
-      float lam_r[kPer];
-      if (kMode == 0) {
-#pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-          const int64_t row = o0 + ((tid + kProd * q) >> 3);
-          lam_r[q] = row < a.rows ? __ldg(a.lam + row) : 1.f;
-        }
-      }
-      (void)r1;
       for (int kb = 0; kb < nkb; ++kb, ++it) {
         const int rs = it % RST;
         const int os = it % OPST;
-        constexpr int kPB4 = BK * WN / 4;
-        constexpr int kPBper = (kPB4 + kProd - 1) / kProd;
-        // raw slot (X, P, lambda) -> registers, then release the slot
+        // raw slot -> registers, then release the slot
         mbar_wait(&rfull[rs], (it / RST) & 1);
         const uint32_t raw = smem_u32(sRaw) + rs * kRawSlot;
         float4 xv[kPer];
+        uint32_t cw[kPer];
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
           const int f = tid + kProd * q;
           const uint32_t ro =
               kMode == 0 ? (uint32_t)((f >> 3) * 128 + (f & 7) * 16) : (uint32_t)((f >> 5) * 512 + (f & 31) * 16);
           xv[q] = lds128(raw + ro);
+          if (kDual) cw[q] = lds_u32(raw + C::kOffCodes + (f >> 3) * 32 + (f & 7) * 4);
         }
         float4 pb1[kPBper], pb2[kPBper];
 #pragma unroll
@@ -277,17 +251,12 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
           const int e = tid + kProd * q;
           if (e < kPB4) {
             pb1[q] = lds128(raw + kRawTile + e * 16);
-            if (kDual) pb2[q] = lds128(raw + kRawTile + C::kRawP + e * 16);
-            if (kMode == 1) {  // COL: R^T Q0 = U^T diag(1/lambda) Q0 -> scale B rows by 1/lambda_i
-              const float il = lds32(raw + kRawTile + C::kRawP + 4 * (BK + e / (WN / 4)));
+            if (kDual) pb2[q] = lds128(raw + C::kOffP2 + e * 16);
+            if (kMode == 1) {  // COL: R^T Q0 = U^T diag(1/lambda) Q0 -> scale the B rows by 1/lambda_i
+              const float il = lds32(raw + C::kOffInv + 4 * (e / (WN / 4)));
               pb1[q] = make_float4(pb1[q].x * il, pb1[q].y * il, pb1[q].z * il, pb1[q].w * il);
             }
           }
-        }
-        float lam_c[kPer];
-        if (kMode == 1) {
-#pragma unroll
-          for (int q = 0; q < kPer; ++q) lam_c[q] = lds32(raw + kRawTile + C::kRawP + 4 * ((tid + kProd * q) >> 5));
         }
         // The slot is refilled by TMA (async proxy) after this release: order our
         // generic-proxy reads before it (without this fence rows were observed to be
@@ -321,41 +290,19 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
             }
           }
         }
-        // A operand: the residual fraction u = lambda x - code (R = u / lambda; 1/lambda is applied
-        // to the accumulator rows (ROW) or folded into the B rows (COL))
-        const bool floor_mode = a.mode == kRoundFloor;  // uniform: LRQMM's rounding takes the short path
-        const float qf = static_cast<float>(a.qmax);
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
           const int f = tid + kProd * q;
-          const float l = kMode == 0 ? lam_r[q] : lam_c[q];
-          const float xs[4] = {xv[q].x, xv[q].y, xv[q].z, xv[q].w};
-          float u[4], c[4];
-          if (floor_mode) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              // floor of the exact product: t = RN(l*x - floor(RN(l*x))) < 0 iff the product rounded up
-              // onto an integer; the x < 0 underflow-to-zero case is decided by the sign of x.  With
-              // lambda <= qmax/amax(1+2^-24) only the lower clamp can bind.
-              float cc = floorf(__fmul_rn(l, xs[e]));
-              const float t = __fmaf_rn(l, xs[e], -cc);
-              cc = (t < 0.f || (t == 0.f && cc == 0.f && xs[e] < 0.f)) ? cc - 1.f : cc;
-              cc = fmaxf(cc, -qf);
-              c[e] = cc;
-              u[e] = __fmaf_rn(l, xs[e], -cc);
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              c[e] = codef(l, xs[e], a.mode, a.qmax);
-              u[e] = __fmaf_rn(l, xs[e], -c[e]);
-            }
-          }
           const uint32_t off = kMode == 0 ? off_k(f >> 3, (f & 7) * 4) : off_mn((f & 31) * 4, f >> 5, 4);
-          const float4 h = make_float4(tf32_hi(u[0]), tf32_hi(u[1]), tf32_hi(u[2]), tf32_hi(u[3]));
+          const float4 uv = xv[q];
+          const float4 h = make_float4(tf32_hi(uv.x), tf32_hi(uv.y), tf32_hi(uv.z), tf32_hi(uv.w));
           sts128(sAhi + off, h);
-          sts128(sAlo + off, make_float4(u[0] - h.x, u[1] - h.y, u[2] - h.z, u[3] - h.w));
-          if (kDual) sts128(sAc + off, make_float4(c[0], c[1], c[2], c[3]));
+          sts128(sAlo + off, make_float4(uv.x - h.x, uv.y - h.y, uv.z - h.z, uv.w - h.w));
+          if (kDual) {
+            const uint32_t w = cw[q];
+            sts128(sAc + off, make_float4((float)(int8_t)(w & 0xff), (float)(int8_t)((w >> 8) & 0xff),
+                                          (float)(int8_t)((w >> 16) & 0xff), (float)(int8_t)(w >> 24)));
+          }
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -363,7 +310,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       }
     }
   } else if (warp == kMmaWarp) {
-    // --------------------------------------------------------------- MMA issuer
+    // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(WN, kMode == 1 ? 1u : 0u, 1u);
       int it = 0, lu = 0;
@@ -412,7 +359,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
     }
     __syncwarp();
   } else {
-    // ---------------------------------------------------------------- epilogue
+    // -------------------------------------------------------------- epilogue
     const int quad = warp & 3;
     int lu = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
@@ -439,11 +386,8 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
         if (orow < a.nout) {
           float* o = (second ? out2 : out1) + orow * a.W;
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            if (cbase + c < a.W) {
-              o[cbase + c] = __fmul_rn(__uint_as_float(v[c]), inv_row);
-            }
-          }
+          for (int c = 0; c < 32; ++c)
+            if (cbase + c < a.W) o[cbase + c] = __fmul_rn(__uint_as_float(v[c]), inv_row);
         }
       }
       tc_fence_before();
@@ -466,7 +410,8 @@ __global__ void k_reduce_splits_tc(const float* __restrict__ part, int nsplit, i
 }
 
 template <int kMode, int NA, bool kDual>
-static int run_tc(const TcArgs& a0, float* OUT1, float* OUT2, float* partial, int64_t pe, bool reduce1, cudaStream_t st) {
+static int run_tc(const SideView& s, const float* P1, const float* P2, int W, float* OUT1, float* OUT2, float* partial,
+                  int64_t pe, bool reduce1, cudaStream_t st) {
   using namespace tcp;
   using C = Cfg<kMode, NA, kDual>;
   static bool attr = false;
@@ -474,17 +419,22 @@ static int run_tc(const TcArgs& a0, float* OUT1, float* OUT2, float* partial, in
     cudaFuncSetAttribute(k_tc_proj<kMode, NA, kDual>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr = true;
   }
-  TcArgs a = a0;
+  TcArgs a{};
+  a.rows = s.rows;
+  a.K = s.K;
+  a.inv_lam = s.inv_lam;
+  a.W = W;
+  a.nout = kMode == 0 ? s.rows : (int64_t)s.K;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t nblk = (a.nout + BM - 1) / BM;
-  const int64_t rlen = kMode == 0 ? (int64_t)a.K : a.rows;
+  const int64_t rlen = kMode == 0 ? (int64_t)s.K : s.rows;
   // enough units for ~6 per SM (the persistent grid balances them), each >= 8 k-blocks
   int64_t ns = (6LL * nsm + nblk - 1) / nblk;
   const int64_t maxs = (rlen + 8 * BK - 1) / (8 * BK);
   if (ns > maxs) ns = maxs;
-  const int64_t per = a.nout * a.W * (kDual ? 2 : 1);
+  const int64_t per = a.nout * W * (kDual ? 2 : 1);
   if (ns > 1 && ns * per > pe) ns = pe / per;
   if (ns < 1) ns = 1;
   a.chunk = ((rlen + ns - 1) / ns + BK - 1) / BK * BK;
@@ -493,75 +443,56 @@ static int run_tc(const TcArgs& a0, float* OUT1, float* OUT2, float* partial, in
   a.nblk = (int)nblk;
   a.nsplit = (int)ns;
   a.out1 = ns == 1 ? OUT1 : partial;
-  a.out2 = ns == 1 ? OUT2 : partial + ns * a.nout * a.W;
+  a.out2 = ns == 1 ? OUT2 : partial + ns * a.nout * W;
   alignas(64) TcMaps maps;
   memset(&maps, 0, sizeof(maps));
-  if (kMode == 0) encode_map_2d(&maps.x, 1, a.X, (uint64_t)a.K, (uint64_t)a.rows, (uint64_t)a.ldx * 4, BK, BM);
-  else encode_map_2d(&maps.x, 1, a.X, (uint64_t)a.K, (uint64_t)a.rows, (uint64_t)a.ldx * 4, BM, BK);
+  if (kMode == 0) encode_map_2d(&maps.u, 1, s.U, (uint64_t)s.K, (uint64_t)s.rows, (uint64_t)s.ldu * 4, BK, BM);
+  else encode_map_2d(&maps.u, 1, s.U, (uint64_t)s.K, (uint64_t)s.rows, (uint64_t)s.ldu * 4, BM, BK);
   // P tiles [BK rows][WN cols]; columns >= W and rows past the end are zero-filled by TMA
-  encode_map_2d(&maps.p1, 1, a.P1, (uint64_t)a.W, (uint64_t)rlen, (uint64_t)a.W * 4, C::WN, BK);
-  if (kDual) encode_map_2d(&maps.p2, 1, a.P2, (uint64_t)a.W, (uint64_t)rlen, (uint64_t)a.W * 4, C::WN, BK);
-  if (kMode == 1) {
-    encode_map_1d_f32(&maps.lam, a.lam, (uint64_t)a.rows, BK);
-    encode_map_1d_f32(&maps.inv, a.inv_lam, (uint64_t)a.rows, BK);
+  encode_map_2d(&maps.p1, 1, P1, (uint64_t)W, (uint64_t)rlen, (uint64_t)W * 4, C::WN, BK);
+  if (kDual) {
+    encode_map_2d(&maps.p2, 1, P2, (uint64_t)W, (uint64_t)rlen, (uint64_t)W * 4, C::WN, BK);
+    encode_map_2d(&maps.codes, 0, s.codes, (uint64_t)s.Kp, (uint64_t)s.rows, (uint64_t)s.Kp, BK, BM);
   }
+  if (kMode == 1) encode_map_1d_f32(&maps.inv, s.inv_lam, (uint64_t)s.rows, BK);
   const int64_t units = nblk * ns;
   const int grid = (int)(units < nsm ? units : nsm);
   k_tc_proj<kMode, NA, kDual><<<grid, kThreads, C::kSmem, st>>>(maps, a);
   ++launch_counter();
   if (ns > 1) {
-    const int64_t n = a.nout * a.W;
+    const int64_t n = a.nout * W;
     const int g = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
     if (reduce1) {
       k_reduce_splits_tc<<<g, 256, 0, st>>>(partial, (int)ns, n, OUT1);
       ++launch_counter();
     }
     if (kDual) {
-      k_reduce_splits_tc<<<g, 256, 0, st>>>(partial + ns * a.nout * a.W, (int)ns, n, OUT2);
+      k_reduce_splits_tc<<<g, 256, 0, st>>>(partial + ns * a.nout * W, (int)ns, n, OUT2);
       ++launch_counter();
     }
   }
   return (int)ns;
 }
 
-static TcArgs make_args(const SideView& s, const float* P1, const float* P2, int W, int64_t nout) {
-  TcArgs a{};
-  a.X = s.X;
-  a.ldx = s.ldx;
-  a.rows = s.rows;
-  a.K = s.K;
-  a.lam = s.lam;
-  a.inv_lam = s.inv_lam;
-  a.qmax = s.qmax;
-  a.mode = s.mode;
-  a.P1 = P1;
-  a.P2 = P2;
-  a.W = W;
-  a.nout = nout;
-  return a;
-}
-
-// X must be TMA-addressable: 16-byte aligned base and ldx % 4 == 0 (lrqmm_quantize
-// stages other layouts into an aligned handle-owned copy).  Returns the number of split-K
-// partials; with reduce1 == false and a result > 1, OUT1 is left as partials at `partial`.
+// U (K1's residual fractions) is TMA-addressable by construction (ldu % 4 == 0).  Returns the
+// number of split-K partials; with reduce1 == false and a result > 1, OUT1 is left as
+// partials at `partial` (summed by the fused Gram kernel).
 int launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
                         float* partial, int64_t pe, bool reduce1, cudaStream_t st) {
   if (s.rows == 0 || s.K == 0) return 0;
-  TcArgs a = make_args(s, P1, P2, W, s.rows);
   if (W <= 32) {
-    if (P2) return run_tc<0, 1, true>(a, OUT1, OUT2, partial, pe, reduce1, st);
-    return run_tc<0, 1, false>(a, OUT1, OUT2, partial, pe, reduce1, st);
+    if (P2) return run_tc<0, 1, true>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, st);
+    return run_tc<0, 1, false>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, st);
   }
-  if (P2) return run_tc<0, 2, true>(a, OUT1, OUT2, partial, pe, reduce1, st);
-  return run_tc<0, 2, false>(a, OUT1, OUT2, partial, pe, reduce1, st);
+  if (P2) return run_tc<0, 2, true>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, st);
+  return run_tc<0, 2, false>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, st);
 }
 
 int launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t pe, bool reduce1,
                         cudaStream_t st) {
   if (s.K == 0 || s.rows == 0) return 0;
-  TcArgs a = make_args(s, P, nullptr, W, s.K);
-  if (W <= 32) return run_tc<1, 1, false>(a, OUT, nullptr, partial, pe, reduce1, st);
-  return run_tc<1, 2, false>(a, OUT, nullptr, partial, pe, reduce1, st);
+  if (W <= 32) return run_tc<1, 1, false>(s, P, nullptr, W, OUT, nullptr, partial, pe, reduce1, st);
+  return run_tc<1, 2, false>(s, P, nullptr, W, OUT, nullptr, partial, pe, reduce1, st);
 }
 
 }  // namespace lrqmm

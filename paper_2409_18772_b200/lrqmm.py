@@ -83,7 +83,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lrqmm_launch_count": (I64, [P, I]),
         "lrqmm_status_string": (ctypes.c_char_p, [I]),
         # test hooks (include/lrqmm_debug.h)
-        "lrqmm_debug_proj": (I, [I, P, I64, I64, I, P, I, I, P, P, I, P, P, P]),
+        "lrqmm_debug_proj": (I, [I, P, I64, I64, I, I, I, P, P, I, P, P, P]),
         "lrqmm_debug_small": (I, [I, P, I64, I, I, P, P, P]),
     }
     for name, (res, args) in sig.items():
@@ -143,8 +143,7 @@ class Lrqmm:
 
     # ---- the five calls of the boundary ----
     def quantize(self, side: int, X):
-        """X: float32 cuda tensor (rows x k); retained until rsvd_residual completes."""
-        self._keep[side] = X
+        """X: float32 cuda tensor (rows x k), any row stride."""
         _check(self.lib.lrqmm_quantize(self.h, side, _ptr(X), _ld(X)), "lrqmm_quantize")
 
     def rsvd_residual(self, omega_a, omega_b):

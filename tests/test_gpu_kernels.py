@@ -36,7 +36,7 @@ def test_proj_rows(rows, K, W):
     out = torch.zeros((rows, W), device=DEV)
     lib = L.load_library()
     st = torch.cuda.current_stream().cuda_stream
-    assert lib.lrqmm_debug_proj(0, cu(X).data_ptr(), K, rows, K, cu(lam).data_ptr(), 4, 0, cu(P).data_ptr(), None,
+    assert lib.lrqmm_debug_proj(0, cu(X).data_ptr(), K, rows, K, 4, 0, cu(P).data_ptr(), None,
                                 W, out.data_ptr(), None, st) == 0
     assert rel(out.cpu().numpy(), R @ P.astype(np.float64)) < 1e-5
 
@@ -48,7 +48,7 @@ def test_proj_cols(rows, K, W):
     out = torch.zeros((K, W), device=DEV)
     lib = L.load_library()
     st = torch.cuda.current_stream().cuda_stream
-    assert lib.lrqmm_debug_proj(1, cu(X).data_ptr(), K, rows, K, cu(lam).data_ptr(), 4, 0, cu(P).data_ptr(), None,
+    assert lib.lrqmm_debug_proj(1, cu(X).data_ptr(), K, rows, K, 4, 0, cu(P).data_ptr(), None,
                                 W, out.data_ptr(), None, st) == 0
     assert rel(out.cpu().numpy(), R.T @ P.astype(np.float64)) < 1e-5
 
@@ -63,7 +63,7 @@ def test_proj_rows_dual(rows, K, W):
     out2 = torch.zeros((rows, W), device=DEV)
     lib = L.load_library()
     st = torch.cuda.current_stream().cuda_stream
-    assert lib.lrqmm_debug_proj(2, cu(X).data_ptr(), K, rows, K, cu(lam).data_ptr(), 8, 0, cu(P).data_ptr(),
+    assert lib.lrqmm_debug_proj(2, cu(X).data_ptr(), K, rows, K, 8, 0, cu(P).data_ptr(),
                                 cu(P2).data_ptr(), W, out.data_ptr(), out2.data_ptr(), st) == 0
     assert rel(out.cpu().numpy(), R @ P.astype(np.float64)) < 1e-5
     assert rel(out2.cpu().numpy(), O.dequantize(codes, lam) @ P2.astype(np.float64)) < 1e-5

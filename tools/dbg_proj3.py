@@ -17,7 +17,7 @@ for rep in range(3):
         out = torch.zeros(ref.shape, device=dev)
         x, l, p = cu(X), cu(lam), cu(P)
         st = torch.cuda.current_stream().cuda_stream
-        lib.lrqmm_debug_proj(mode, x.data_ptr(), K, rows, K, l.data_ptr(), 4, 0, p.data_ptr(), None, W, out.data_ptr(), None, st)
+        lib.lrqmm_debug_proj(mode, x.data_ptr(), K, rows, K, 4, 0, p.data_ptr(), None, W, out.data_ptr(), None, st)
         o = out.cpu().numpy()
         e = np.linalg.norm(o-ref)/np.linalg.norm(ref)
         tot += 1; bad += e > 1e-5
