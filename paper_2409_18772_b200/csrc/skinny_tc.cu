@@ -32,12 +32,15 @@ namespace lrqmm {
 namespace tcp {
 constexpr int BM = 128;  // output rows (ROW) / output cols (COL) per unit
 constexpr int BK = 32;   // reduction elements per k-block
-constexpr int kProd = 512;  // 16 producer warps
+#ifndef LRQMM_PROD
+#define LRQMM_PROD 256
+#endif
+constexpr int kProd = LRQMM_PROD;  // producer threads
 constexpr int kProdWarps = kProd / 32;
 constexpr int kMmaWarp = kProdWarps + 4;
 constexpr int kTmaWarp = kProdWarps + 5;
-constexpr int kThreads = (kProdWarps + 6) * 32;  // 704
-constexpr int kPer = BM * BK / 4 / kProd;        // float4 of U per producer thread per k-block (2)
+constexpr int kThreads = (kProdWarps + 6) * 32;
+constexpr int kPer = BM * BK / 4 / kProd;        // float4 of U per producer thread per k-block
 #ifndef LRQMM_OPST
 #define LRQMM_OPST 2
 #endif
@@ -258,12 +261,6 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
             }
           }
         }
-        // The slot is refilled by TMA (async proxy) after this release: order our
-        // generic-proxy reads before it (without this fence rows were observed to be
-        // overwritten before they were read on B200).
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&rempty[rs]);
         // operand stage
         mbar_wait(&oempty[os], ((it / OPST) & 1) ^ 1);
         const uint32_t st = smem_u32(sOp) + os * kStage;
@@ -304,15 +301,28 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
                                           (float)(int8_t)((w >> 16) & 0xff), (float)(int8_t)(w >> 24)));
           }
         }
+        // one proxy fence orders this thread's operand-tile writes before the MMA (async proxy)
+        // reads them AND its raw-slot reads before the TMA (async proxy) refills the slot; a
+        // release without the fence let TMA overwrite rows before they were read on B200.
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&ofull[os]);
+        if (lane == 0) {
+          mbar_arrive(&ofull[os]);
+          mbar_arrive(&rempty[rs]);
+        }
       }
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(WN, kMode == 1 ? 1u : 0u, 1u);
+      // descriptors of stage 0 at k-step 0; other stages / k-steps differ only in the start
+      // address field (addr >> 4 in the low 14 bits, no carry below 256 KB of smem)
+      constexpr uint32_t lboA = kMode == 0 ? 16 : 512, sboA = kMode == 0 ? 1024 : 2048, tA = kMode == 0 ? 2 : 1;
+      constexpr uint32_t kAStep = kMode == 0 ? 32 : 4096;  // bytes per 8-deep k-step (K-major / MN-major)
+      const uint32_t st0 = smem_u32(sOp);
+      const uint64_t dA0 = desc_sw128(st0, lboA, sboA, tA);
+      const uint64_t dB0 = desc_sw128(st0 + (kDual ? 3 : 2) * kATile, 512, NA * 512, 1);
       int it = 0, lu = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
         int blk, split, nkb;
@@ -326,28 +336,23 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
           const int os = it % OPST;
           mbar_wait(&ofull[os], (it / OPST) & 1);
           tc_fence_after();
-          const uint32_t st = smem_u32(sOp + os * kStage);
-          const uint32_t aHi = st, aLo = st + kATile, aC = st + 2 * kATile;
-          const uint32_t bHi = st + (kDual ? 3 : 2) * kATile;
-          const uint32_t bLo = bHi + kBTile, b2Hi = bLo + kBTile, b2Lo = b2Hi + kBTile;
+          const uint64_t so = (uint64_t)((os * kStage) >> 4);
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
-            uint32_t aoff, lboA, sboA, tA;
-            if (kMode == 0) { aoff = k * 32; lboA = 16; sboA = 1024; tA = 2; }   // K-major: +32 B per 8 k
-            else { aoff = k * 4096; lboA = 512; sboA = 2048; tA = 1; }           // MN-major: two 4-deep groups
-            const uint32_t boff = k * (NA * 1024);
+            const uint64_t aoff = so + ((k * kAStep) >> 4);
+            const uint64_t boff = so + ((k * (NA * 1024)) >> 4);
+            const uint64_t dAhi = dA0 + aoff;
+            const uint64_t dAlo = dA0 + aoff + (kATile >> 4);
+            const uint64_t dBhi = dB0 + boff;
+            const uint64_t dBlo = dB0 + boff + (kBTile >> 4);
             const uint32_t acc0 = (kb | k) != 0 ? 1u : 0u;
-            const uint64_t dAhi = desc_sw128(aHi + aoff, lboA, sboA, tA);
-            const uint64_t dAlo = desc_sw128(aLo + aoff, lboA, sboA, tA);
-            const uint64_t dBhi = desc_sw128(bHi + boff, 512, NA * 512, 1);
-            const uint64_t dBlo = desc_sw128(bLo + boff, 512, NA * 512, 1);
             umma_tf32(d1, dAhi, dBhi, idesc, acc0);
             umma_tf32(d1, dAhi, dBlo, idesc, 1u);
             umma_tf32(d1, dAlo, dBhi, idesc, 1u);
             if (kDual) {
-              const uint64_t dAc = desc_sw128(aC + aoff, lboA, sboA, tA);
-              const uint64_t dB2hi = desc_sw128(b2Hi + boff, 512, NA * 512, 1);
-              const uint64_t dB2lo = desc_sw128(b2Lo + boff, 512, NA * 512, 1);
+              const uint64_t dAc = dA0 + aoff + ((2 * kATile) >> 4);
+              const uint64_t dB2hi = dB0 + boff + ((2 * kBTile) >> 4);
+              const uint64_t dB2lo = dB0 + boff + ((3 * kBTile) >> 4);
               umma_tf32(d1 + WN, dAc, dB2hi, idesc, acc0);
               umma_tf32(d1 + WN, dAc, dB2lo, idesc, 1u);
             }
