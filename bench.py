@@ -45,7 +45,7 @@ REF_ROWS = 256  # oracle row sample per reference / cpu_baseline step
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="lrqmm", choices=["lrqmm", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
@@ -65,61 +65,60 @@ def load_peaks():
 
 # --------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """Polls SM clock, max clock, power and throttle reasons through NVML every 10 ms while the
+    timed region runs (the profiling recipe's clocks line, sampled in-process)."""
 
-    def __init__(self, index: int):
+    REASONS = {  # nvmlClocksEventReason* bits
+        "sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, index: int, period_s: float = 0.01):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.period = period_s
+        self.samples = []
+        self.stop = threading.Event()
+        self.ok = False
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.ok = False
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+                self.samples.append((sm, rs, pw))
+            except Exception:
+                pass
+            self.stop.wait(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.ok:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, pw, reasons = [], [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-                pw.append(float(parts[2]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm_sorted = sorted(sm)
-        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
-        busy.sort()
-        return {"sm_mhz": busy[len(busy) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm), "power_w_max": max(pw), "sm_mhz_min": sm_sorted[0]}
+        sm = sorted(s[0] for s in self.samples)
+        reasons = sorted({nm for _, rs, _ in self.samples for nm, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_sm, "reasons": reasons,
+                "samples": len(sm), "sm_mhz_min": sm[0], "power_w_max": max(s[2] for s in self.samples)}
 
 
 # -------------------------------------------------------------- dist utils
@@ -335,28 +334,30 @@ def main():
             errs[name] = float(torch.linalg.norm(D[rows].double() - Cex) / nrm)
         del Cex
 
-    # end to end through the C ABI with pinned HOST buffers (rank 0 measures; all ranks run)
+    # end to end through the C ABI with pinned HOST buffers: every rank runs lrqmm_run_host on its
+    # own A block (H2D of A, B^T, Omega; full hot path; D2H of D); max over ranks of host wall time
     e2e = None
-    if not args.no_e2e and ws == 1:
+    if not args.no_e2e:
         hA = torch.empty((Mloc, K), dtype=torch.float32, pin_memory=True)
         hB = torch.empty((N, K), dtype=torch.float32, pin_memory=True)
         hOa = torch.empty((K, kk), dtype=torch.float32, pin_memory=True)
         hOb = torch.empty((K, kk), dtype=torch.float32, pin_memory=True)
         hD = torch.empty((Mloc, N), dtype=torch.float32, pin_memory=True)
         hA.copy_(A); hB.copy_(Bt); hOa.copy_(OmA); hOb.copy_(OmB)
-        he = Lrqmm(Mloc, N, K, bits, r, p, 1, "floor", "row", device=local, stream=stream)
         npA, npB, npOa, npOb, npD = hA.numpy(), hB.numpy(), hOa.numpy(), hOb.numpy(), hD.numpy()
-        he.run_host(npA, npB, npOa, npOb, npD)
+        h.run_host(npA, npB, npOa, npOb, npD)
+        barrier(ws)
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            he.run_host(npA, npB, npOa, npOb, npD)
+            h.run_host(npA, npB, npOa, npOb, npD)
         t_e2e = (time.perf_counter() - t0) / args.e2e_steps
-        he.close()
+        t_e2e = max_over_ranks(t_e2e, ws, local)
         h2d = 4 * (Mloc * K + N * K + 2 * K * kk)
         d2h = 4 * Mloc * N
-        e2e = {"value": 2.0 * Mloc * N * K / t_e2e / 1e12, "unit": "TOPS", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
-               "note": "lrqmm_run_host: pinned host A, B^T, Omega -> device, full hot path, D -> host; host wall clock"}
+        e2e = {"value": 2.0 * Mloc * ws * N * K / t_e2e / 1e12, "unit": "TOPS", "h2d_bytes_per_step": h2d * ws,
+               "d2h_bytes_per_step": d2h * ws, "ms_per_step": t_e2e * 1e3,
+               "note": "lrqmm_run_host: pinned host A, B^T, Omega -> device, full hot path, D -> host; "
+                       "host wall clock, max over ranks"}
         del hA, hB, hD
 
     h.close()
@@ -370,7 +371,11 @@ def main():
     Mtot = Mloc * ws
     ops = 2.0 * Mtot * N * K
     peaks, peak_src = load_peaks()
-    int8_peak = 2.0 * float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+    # int8 dense = 2 x the measured bf16 BURST figure (guide nominal ratio 4.5 / 2.25).  The GEMM runs
+    # inside a long step, but the bf16 "sustained" figure is a power-capped clock (~1.24 GHz) that
+    # the int8 kernel does not hit (it holds ~1.77 GHz), so it is not a ceiling for it; the burst
+    # figure is the larger, conservative denominator.
+    int8_peak = 2.0 * float(peaks["bf16_tflops"])
     gemm_tops = 2.0 * Mloc * N * K / t_gemm / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "gemm_ncu_summary.json")
@@ -415,8 +420,9 @@ def main():
         "roofline": {"bound": "tensor", "kernel": "k6_gemm_i8 (tcgen05 kind::i8 + fused LRQMM epilogue)",
                      "achieved": gemm_tops, "peak": int8_peak, "unit": "TFLOP/s", "frac": gemm_tops / int8_peak,
                      "traffic": traffic,
-                     "peak_note": f"int8 dense = 2 x {peak_src} bf16 sustained ({peaks.get('bf16_tflops_sustained')}) "
-                                  "(guide nominal ratio 4.5/2.25)"},
+                     "peak_note": f"int8 dense = 2 x {peak_src} bf16 burst ({peaks['bf16_tflops']} TFLOP/s; guide nominal "
+                                  "ratio 4.5/2.25); the bf16 sustained figure is power-capped below this "
+                                  "kernel's clock"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

@@ -34,7 +34,13 @@ constexpr int kABytes = BM * BK;
 constexpr int kBBytes = BN * BK;
 constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
-constexpr int kGroupM = 16;     // tile rasterisation: 16 M-blocks per group (L2 reuse)
+#ifndef LRQMM_L2HINT
+#define LRQMM_L2HINT 2  // 1: A evict_last + B evict_first, 2: A evict_last only
+#endif
+#ifndef LRQMM_GROUPM
+#define LRQMM_GROUPM 16
+#endif
+constexpr int kGroupM = LRQMM_GROUPM;  // tile rasterisation: M-blocks per group (L2 reuse)
 // 4 smem stages while the L_B tile fits beside them, 3 for the widest corrections
 __host__ __device__ constexpr int stages_for(int r2) { return r2 > 32 ? 3 : 4; }
 __host__ __device__ constexpr int smem_bytes(int r2) {
@@ -177,14 +183,29 @@ __global__ void __launch_bounds__(g6::kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+#if LRQMM_L2HINT
+      const uint64_t polA = l2_policy_evict_last();
+#if LRQMM_L2HINT == 1
+      const uint64_t polB = l2_policy_evict_first();
+#endif
+#endif
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int mb, nb;
         tile_coords(t, p.num_m, p.num_n, mb, nb);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], kStageBytes);
+#if LRQMM_L2HINT
+          tma_load_2d_hint(sA + stage * kABytes, &mapA, &full[stage], kb * BK, mb * BM, polA);
+#if LRQMM_L2HINT == 1
+          tma_load_2d_hint(sB + stage * kBBytes, &mapB, &full[stage], kb * BK, nb * BN, polB);
+#else
+          tma_load_2d(sB + stage * kBBytes, &mapB, &full[stage], kb * BK, nb * BN);
+#endif
+#else
           tma_load_2d(sA + stage * kABytes, &mapA, &full[stage], kb * BK, mb * BM);
           tma_load_2d(sB + stage * kBBytes, &mapB, &full[stage], kb * BK, nb * BN);
+#endif
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
