@@ -142,15 +142,38 @@ def barrier(ws):
         dist.barrier()
 
 
-def max_over_ranks(x: float, ws: int, local: int) -> float:
+def max_over_ranks(x: float, ws: int, device) -> float:
+    """Device time of the slowest rank (the contract's max over ranks)."""
     if ws == 1:
         return x
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def broadcast_unique_id(uid: bytes | None, ws: int, rank: int, device) -> bytes:
+    """Rank 0's 128-byte NCCL unique id (lrqmm_get_unique_id) to every rank, over the process group."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.zeros(128, dtype=torch.uint8, device=device)
+    if rank == 0:
+        assert uid is not None and len(uid) == 128
+        t.copy_(torch.frombuffer(bytearray(uid), dtype=torch.uint8))
+    if ws > 1:
+        dist.broadcast(t, 0)
+    return bytes(t.cpu().numpy().tobytes())
+
+
+def row_shard(M_total: int, ws: int, rank: int) -> tuple[int, int]:
+    """[start, stop) rows of A owned by `rank` when M_total rows are split over ws ranks
+    (contiguous blocks, the first M_total % ws ranks one row longer)."""
+    base, extra = divmod(M_total, ws)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
 
 
 # ------------------------------------------------------------ oracle legs
@@ -244,11 +267,7 @@ def main():
     if ws > 1:
         import torch.distributed as dist
 
-        t = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            t.copy_(torch.frombuffer(bytearray(get_unique_id()), dtype=torch.uint8))
-        dist.broadcast(t, 0)
-        uid = bytes(t.cpu().numpy().tobytes())
+        uid = broadcast_unique_id(get_unique_id() if rank == 0 else None, ws, rank, dev)
     h = Lrqmm(Mloc, N, K, bits, r, p, 1, "floor", "row", world_size=ws, world_rank=rank, unique_id=uid,
               device=local, stream=stream, enable_timing=False)
 
@@ -291,7 +310,7 @@ def main():
     t_step = e0.elapsed_time(e1) / 1e3 / args.steps
     ph = np.array([[ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])] for ev in evs]) / 1e3
     t_quant, t_rsvd, t_gemm = [float(x) for x in ph.mean(axis=0)]
-    t_step = max_over_ranks(t_step, ws, local)
+    t_step = max_over_ranks(t_step, ws, dev)
 
     # bare int8 GEMM (same tcgen05 kernel, int32 epilogue): the overhead denominator
     for _ in range(2):
@@ -351,7 +370,7 @@ def main():
         for _ in range(args.e2e_steps):
             h.run_host(npA, npB, npOa, npOb, npD)
         t_e2e = (time.perf_counter() - t0) / args.e2e_steps
-        t_e2e = max_over_ranks(t_e2e, ws, local)
+        t_e2e = max_over_ranks(t_e2e, ws, dev)
         h2d = 4 * (Mloc * K + N * K + 2 * K * kk)
         d2h = 4 * Mloc * N
         e2e = {"value": 2.0 * Mloc * ws * N * K / t_e2e / 1e12, "unit": "TOPS", "h2d_bytes_per_step": h2d * ws,
