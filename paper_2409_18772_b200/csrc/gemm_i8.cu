@@ -351,7 +351,8 @@ int encode_map_2d(void* map, int dtype_f32, const void* base, uint64_t inner, ui
   cuuint64_t strides[1] = {(cuuint64_t)stride_bytes};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(reinterpret_cast<CUtensorMap*>(map), dtype_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT8,
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(map), dtype_f32 == 1 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                   : (dtype_f32 == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8),
                    2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : 2;

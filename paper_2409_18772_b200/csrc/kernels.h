@@ -24,8 +24,8 @@ struct QuantArgs {
   float* inv_lam;         // rows: RN(1/lambda) (written unless lam_fixed)
   const float* lam_fixed; // device scalar (per-tensor mode) or nullptr
   int* err_flag;          // bit 0: non-finite input
-  float* U;               // rows x ldu residual fraction u = lambda x - code (or nullptr)
-  int64_t ldu;            // multiple of 4, >= K
+  int16_t* U;             // rows x ldu residual fraction u = lambda x - code, Q15 fixed point (or nullptr)
+  int64_t ldu;            // multiple of 8, >= K
 };
 void launch_quantize(const QuantArgs& a, cudaStream_t st);
 void launch_tensor_scale(const float* X, int64_t ldx, int64_t rows, int K, int qmax, float* row_amax,
@@ -34,8 +34,12 @@ void launch_tensor_scale(const float* X, int64_t ldx, int64_t rows, int K, int q
 // ------------------------------------------------- K2/K3 skinny residual products
 // The passes stream the residual fraction u = lambda x - code written by K1 (R = u / lambda,
 // Alg. 2) and, for the cross products, the codes (X~ = code / lambda, line 352).
+// u is stored as int16 Q15: u16 = clamp(RN(u * 2^15), +-32767) (|u| < 1 for every rounding mode;
+// |u16 / 2^15 - u| <= 2^-16, 2^-15 where u rounds past the clamp).  Half the bytes of fp32 on the three RSVD passes that stream it
+// (reading #28); u16 / 2^15 is exact in fp32 and splits exactly into tf32 hi + lo.
+constexpr float kUScale = 32768.f;
 struct SideView {
-  const float* U;        // rows x ldu fp32
+  const int16_t* U;      // rows x ldu, u in Q15 fixed point (kUScale)
   int64_t ldu;
   int64_t rows;
   int K;
@@ -131,7 +135,7 @@ struct GemmArgs {
 };
 int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB);  // returns 0 on success
 // 2D TMA map (no swizzle), dims {inner, outer} elements of fp32 (dtype_f32=1) or u8; returns 0 on success
-int encode_map_2d(void* map, int dtype_f32, const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
+int encode_map_2d(void* map, int dtype_f32 /* 1 f32, 2 16-bit, 0 8-bit */, const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
                   uint32_t box_inner, uint32_t box_outer);
 int encode_map_1d_f32(void* map, const void* base, uint64_t n, uint32_t box);
 // out[i] = RN(1 / in[i])

@@ -23,7 +23,7 @@ constexpr int kMaxWidth = 64;
 struct Side {
   int64_t rows = 0;
   int64_t ldu = 0;
-  float* U = nullptr;        // rows x ldu residual fraction u = lambda x - code (written by K1)
+  int16_t* U = nullptr;      // rows x ldu residual fraction u = lambda x - code, Q15 (written by K1)
   int8_t* codes = nullptr;   // rows x Kp
   float* lam = nullptr;      // rows
   float* inv_lam = nullptr;  // rows, RN(1/lambda)
@@ -206,7 +206,7 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
     ok = ok && dalloc(&s.codes, s.rows * h->Kp) && dalloc(&s.lam, s.rows) && dalloc(&s.inv_lam, s.rows) && dalloc(&s.row_amax, s.rows) &&
          dalloc(&s.lam_scalar, 1);
     if (h->W > 0) {
-      s.ldu = (K + 3) / 4 * 4;
+      s.ldu = (K + 7) / 8 * 8;
       ok = ok && dalloc(&s.U, s.rows * s.ldu) && dalloc(&s.Om, K * h->W) && dalloc(&s.Y, s.rows * h->W) && dalloc(&s.Q0, s.rows * h->W) &&
            dalloc(&s.Z, K * h->W) && dalloc(&s.Q1, K * h->W) && dalloc(&s.Gp, s.rows * h->W) &&
            dalloc(&s.G, (int64_t)h->W * h->W) && dalloc(&s.gpart, (int64_t)kGramMaxBlocks * h->W * h->W) &&
@@ -596,12 +596,13 @@ extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx
                                            float* OUT2, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int Kp = (int)roundup(K > 0 ? K : 1, 128);
-  const int64_t ldu = ((int64_t)K + 3) / 4 * 4;
+  const int64_t ldu = ((int64_t)K + 7) / 8 * 8;
   const int64_t pe = (int64_t)16 << 20;
-  float *U = nullptr, *lam = nullptr, *inv = nullptr, *partial = nullptr;
+  int16_t* U = nullptr;
+  float *lam = nullptr, *inv = nullptr, *partial = nullptr;
   int8_t* codes = nullptr;
   int* flag = nullptr;
-  bool ok = cudaMalloc(&U, sizeof(float) * rows * ldu) == cudaSuccess &&
+  bool ok = cudaMalloc(&U, sizeof(int16_t) * rows * ldu) == cudaSuccess &&
             cudaMalloc(&lam, sizeof(float) * rows) == cudaSuccess && cudaMalloc(&inv, sizeof(float) * rows) == cudaSuccess &&
             cudaMalloc(&codes, (size_t)rows * Kp) == cudaSuccess && cudaMalloc(&flag, sizeof(int)) == cudaSuccess &&
             cudaMalloc(&partial, sizeof(float) * pe) == cudaSuccess;

@@ -49,6 +49,13 @@ LRQMM_DEV uint32_t pack4(int8_t a, int8_t b, int8_t c, int8_t d) {
          ((uint32_t)(uint8_t)d << 24);
 }
 
+// residual fraction u (exact fp32, |u| < 1) -> Q15: clamp(RN(u * 2^15), +-32767); the scaling is exact
+LRQMM_DEV int u_fix(float u) {
+  const int q = __float2int_rn(u * kUScale);
+  return q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
+}
+LRQMM_DEV uint32_t pack_u16(int a, int b) { return ((uint32_t)a & 0xffffu) | ((uint32_t)b << 16); }
+
 // TPR threads cooperate on one row; each holds VPT float4 of it.  Row length
 // covered: TPR*VPT*4 >= Kp.  kFixedLam: lambda given (per-tensor mode), no amax.
 template <int TPR, int VPT, bool kVec, bool kFixedLam>
@@ -56,7 +63,7 @@ __global__ void __launch_bounds__(256) k1_quantize(const float* __restrict__ X, 
                                                    int qmax, int mode, int8_t* __restrict__ codes,
                                                    float* __restrict__ lam_out, float* __restrict__ inv_out,
                                                    const float* __restrict__ lam_in, int* __restrict__ err_flag,
-                                                   float* __restrict__ U, int64_t ldu) {
+                                                   int16_t* __restrict__ U, int64_t ldu) {
   constexpr int kRowsPerCta = 256 / TPR;
   constexpr int kWarpsPerRow = TPR / 32;
   __shared__ float red[8];
@@ -112,7 +119,7 @@ __global__ void __launch_bounds__(256) k1_quantize(const float* __restrict__ X, 
         inv_out[row] = __frcp_rn(lam);
       }
       uint32_t* crow = reinterpret_cast<uint32_t*>(codes + row * (int64_t)Kp);
-      float* urow = U ? U + row * ldu : nullptr;
+      int16_t* urow = U ? U + row * ldu : nullptr;
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
         const int col = (sub + i * TPR) * 4;
@@ -123,9 +130,9 @@ __global__ void __launch_bounds__(256) k1_quantize(const float* __restrict__ X, 
           crow[col >> 2] = pack4(c0, c1, c2, c3);
           // residual fraction u = lambda x - code (R = u / lambda, Alg. 2), exactly rounded
           if (urow && col < ldu) {
-            const float4 u = make_float4(__fmaf_rn(lam, v[i].x, -(float)c0), __fmaf_rn(lam, v[i].y, -(float)c1),
-                                         __fmaf_rn(lam, v[i].z, -(float)c2), __fmaf_rn(lam, v[i].w, -(float)c3));
-            __stcg(reinterpret_cast<float4*>(urow + col), u);
+            const uint32_t u01 = pack_u16(u_fix(__fmaf_rn(lam, v[i].x, -(float)c0)), u_fix(__fmaf_rn(lam, v[i].y, -(float)c1)));
+            const uint32_t u23 = pack_u16(u_fix(__fmaf_rn(lam, v[i].z, -(float)c2)), u_fix(__fmaf_rn(lam, v[i].w, -(float)c3)));
+            __stcg(reinterpret_cast<uint2*>(urow + col), make_uint2(u01, u23));
           }
         }
       }
@@ -190,7 +197,7 @@ __global__ void __launch_bounds__(256) k1_quantize_long(const float* __restrict_
                                                         int Kp, int qmax, int mode, int8_t* __restrict__ codes,
                                                         float* __restrict__ lam_out, float* __restrict__ inv_out,
                                                         const float* __restrict__ lam_in, int* __restrict__ err_flag,
-                                                        float* __restrict__ U, int64_t ldu) {
+                                                        int16_t* __restrict__ U, int64_t ldu) {
   __shared__ float red[8];
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
     const float* xr = X + row * ldx;
@@ -223,7 +230,7 @@ __global__ void __launch_bounds__(256) k1_quantize_long(const float* __restrict_
       const float x = c < K ? xr[c] : 0.f;
       const int8_t q = code_of(lam, x, mode, qmax);
       crow[c] = q;
-      if (U && c < ldu) U[row * ldu + c] = __fmaf_rn(lam, x, -(float)q);
+      if (U && c < ldu) U[row * ldu + c] = (int16_t)u_fix(__fmaf_rn(lam, x, -(float)q));
     }
   }
 }

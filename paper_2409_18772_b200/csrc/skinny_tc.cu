@@ -3,9 +3,10 @@
 // reading #11) and the cross products of Algorithm 2, computed as
 // tcgen05.mma kind::tf32 with a 3-term split (x = hi + lo, hi = tf32(x)):
 //     U P ~= U_hi P_hi + U_hi P_lo + U_lo P_hi                 (fp32-grade)
-// U is the residual fraction u = lambda x - code written by K1 (R = diag(1/lambda) U),
-// so every pass streams 4 B per element from HBM — this kernel's roofline — and the
-// producer warps only split u into tf32 hi/lo operand tiles.
+// U is the residual fraction u = lambda x - code written by K1 (R = diag(1/lambda) U) in Q15
+// fixed point, so every pass streams 2 B per element from HBM — this kernel's roofline — and
+// the producer warps only widen u to fp32 and split it into tf32 hi/lo operand tiles (exact:
+// u16 / 2^15 has <= 16 significant bits, hi keeps 11, lo the rest).
 //
 //   ROW mode  OUT1[i,:] = (1/lambda_i) sum_j U[i,j] P1[j,:]      (S1: Y = R Omega, S3: W = R Q1)
 //             OUT2[i,:] = (1/lambda_i) sum_j C[i,j] P2[j,:]      (dual: A~ Q1_other, codes exact in tf32)
@@ -13,11 +14,11 @@
 //   COL mode  OUT[j,:]  = sum_i U[i,j] (P[i,:] / lambda_i)       (S2: Z = R^T Q0)
 //             A operand = U tile, MN-major SW128_BASE32B (U's natural layout); B as above.
 //
-// Persistent, warp-specialised (704 threads, one CTA per SM):
-//   warp 21    : TMA issuer, streams raw tiles (U 16 KB, P, codes, 1/lambda) through a smem ring
-//   warps 0-15 : producers: raw U -> tf32 hi/lo operand tiles (+ codes -> fp32) (2-3 stages)
-//   warp 20    : TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 16-19: epilogue: TMEM (double-buffered accumulators) -> split-K partials
+// Persistent, warp-specialised (448 threads, one CTA per SM):
+//   warp 13    : TMA issuer, streams raw tiles (U 8 KB, P, codes, 1/lambda) through a smem ring
+//   warps 0-7  : producers: raw U -> tf32 hi/lo operand tiles (+ codes -> fp32) (2-3 stages)
+//   warp 12    : TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 8-11 : epilogue: TMEM (double-buffered accumulators) -> split-K partials
 // Work unit = (128-row/col block, reduction split); partials are summed in a fixed order
 // by the consumer (deterministic, no float atomics).
 #include <cuda.h>
@@ -40,13 +41,13 @@ constexpr int kProdWarps = kProd / 32;
 constexpr int kMmaWarp = kProdWarps + 4;
 constexpr int kTmaWarp = kProdWarps + 5;
 constexpr int kThreads = (kProdWarps + 6) * 32;
-constexpr int kPer = BM * BK / 4 / kProd;        // float4 of U per producer thread per k-block
+constexpr int kPer = BM * BK / 4 / kProd;        // 4-element groups of U per producer thread per k-block
 #ifndef LRQMM_OPST
 #define LRQMM_OPST 2
 #endif
 constexpr int OPST_MAX = LRQMM_OPST;
 constexpr int kATile = BM * BK * 4;    // 16 KB operand tile (hi or lo)
-constexpr int kRawTile = BM * BK * 4;  // 16 KB raw U tile
+constexpr int kRawTile = BM * BK * 2;  // 8 KB raw U tile (Q15)
 constexpr int kRawCodes = BM * BK;     // 4 KB raw code tile (dual)
 template <int kMode, int NA, bool kDual>
 struct Cfg {
@@ -115,6 +116,16 @@ LRQMM_DEV void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32
       : "memory");
 }
 LRQMM_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+LRQMM_DEV uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+// two Q15 residual fractions (packed int16) -> fp32 (exact)
+LRQMM_DEV float2 u_unfix(uint32_t w) {
+  constexpr float s = 1.f / kUScale;
+  return make_float2((float)(int16_t)(w & 0xffffu) * s, (float)(int16_t)(w >> 16) * s);
+}
 LRQMM_DEV uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
@@ -243,9 +254,12 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
           const int f = tid + kProd * q;
+          // raw U: ROW [BM rows][BK] int16 (64 B rows), COL [BK rows][BM] int16 (256 B rows)
           const uint32_t ro =
-              kMode == 0 ? (uint32_t)((f >> 3) * 128 + (f & 7) * 16) : (uint32_t)((f >> 5) * 512 + (f & 31) * 16);
-          xv[q] = lds128(raw + ro);
+              kMode == 0 ? (uint32_t)((f >> 3) * 64 + (f & 7) * 8) : (uint32_t)((f >> 5) * 256 + (f & 31) * 8);
+          const uint2 w = lds64(raw + ro);
+          const float2 u01 = u_unfix(w.x), u23 = u_unfix(w.y);
+          xv[q] = make_float4(u01.x, u01.y, u23.x, u23.y);
           if (kDual) cw[q] = lds_u32(raw + C::kOffCodes + (f >> 3) * 32 + (f & 7) * 4);
         }
         float4 pb1[kPBper], pb2[kPBper];
@@ -451,8 +465,8 @@ static int run_tc(const SideView& s, const float* P1, const float* P2, int W, fl
   a.out2 = ns == 1 ? OUT2 : partial + ns * a.nout * W;
   alignas(64) TcMaps maps;
   memset(&maps, 0, sizeof(maps));
-  if (kMode == 0) encode_map_2d(&maps.u, 1, s.U, (uint64_t)s.K, (uint64_t)s.rows, (uint64_t)s.ldu * 4, BK, BM);
-  else encode_map_2d(&maps.u, 1, s.U, (uint64_t)s.K, (uint64_t)s.rows, (uint64_t)s.ldu * 4, BM, BK);
+  if (kMode == 0) encode_map_2d(&maps.u, 2, s.U, (uint64_t)s.K, (uint64_t)s.rows, (uint64_t)s.ldu * 2, BK, BM);
+  else encode_map_2d(&maps.u, 2, s.U, (uint64_t)s.K, (uint64_t)s.rows, (uint64_t)s.ldu * 2, BM, BK);
   // P tiles [BK rows][WN cols]; columns >= W and rows past the end are zero-filled by TMA
   encode_map_2d(&maps.p1, 1, P1, (uint64_t)W, (uint64_t)rlen, (uint64_t)W * 4, C::WN, BK);
   if (kDual) {
@@ -479,7 +493,7 @@ static int run_tc(const SideView& s, const float* P1, const float* P2, int W, fl
   return (int)ns;
 }
 
-// U (K1's residual fractions) is TMA-addressable by construction (ldu % 4 == 0).  Returns the
+// U (K1's residual fractions) is TMA-addressable by construction (ldu % 8 == 0).  Returns the
 // number of split-K partials; with reduce1 == false and a result > 1, OUT1 is left as
 // partials at `partial` (summed by the fused Gram kernel).
 int launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
