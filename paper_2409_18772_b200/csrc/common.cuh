@@ -112,6 +112,14 @@ LRQMM_DEV void tma_load_1d(void* smem_dst, const void* desc, uint64_t* bar, int 
       : "memory");
 }
 
+// plain bulk copy global -> shared (16-byte aligned, bytes % 16 == 0), completes on an mbarrier
+LRQMM_DEV void bulk_load(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // ------------------------------------------------------------------ tcgen05
 LRQMM_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 LRQMM_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }

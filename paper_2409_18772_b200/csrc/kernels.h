@@ -51,11 +51,13 @@ struct SideView {
 // tcgen05 kind::tf32 (3-term split) passes, deterministic split-K partials; return the split count.
 // With reduce1 == false and > 1 splits, OUT1 stays as partials at `partial` (consumed by the fused
 // Gram kernel).  ROW: OUT1 = R P1 (rows x W); dual (P2 != null): OUT2 = X~ P2.  P is K x W (ld W).
+// img: scratch for the pre-split B operand images, >= 2 * tc_img_bytes(max(rows, K), W) bytes.
 int launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
-                        float* partial, int64_t partial_elems, bool reduce1, cudaStream_t st);
+                        float* partial, int64_t partial_elems, bool reduce1, uint8_t* img, cudaStream_t st);
 // COL: OUT = R^T P; P is rows x W, OUT is K x W.
 int launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t partial_elems,
-                        bool reduce1, cudaStream_t st);
+                        bool reduce1, uint8_t* img, cudaStream_t st);
+int64_t tc_img_bytes(int64_t n, int W);
 
 // OUT[i, :] = IN[i, :] S (fp64 S, fp64 accumulation, fp32 out); IN and OUT ld W, S W x W
 void launch_apply64(const float* IN, const double* S, int64_t n, int W, float* OUT, cudaStream_t st);
@@ -135,6 +137,8 @@ struct GemmArgs {
 };
 int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB);  // returns 0 on success
 // 2D TMA map (no swizzle), dims {inner, outer} elements of fp32 (dtype_f32=1) or u8; returns 0 on success
+int encode_map_2d_sw(void* map, int dtype, const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
+                     uint32_t box_inner, uint32_t box_outer, int swizzle_bytes /* 0, 32, 64, 128 */);
 int encode_map_2d(void* map, int dtype_f32 /* 1 f32, 2 16-bit, 0 8-bit */, const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
                   uint32_t box_inner, uint32_t box_outer);
 int encode_map_1d_f32(void* map, const void* base, uint64_t n, uint32_t box);

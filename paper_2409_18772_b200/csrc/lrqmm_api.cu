@@ -24,6 +24,7 @@ struct Side {
   int64_t rows = 0;
   int64_t ldu = 0;
   int16_t* U = nullptr;      // rows x ldu residual fraction u = lambda x - code, Q15 (written by K1)
+  uint8_t* img = nullptr;    // pre-split tf32 B operand images of the passes (skinny_tc.cu)
   int8_t* codes = nullptr;   // rows x Kp
   float* lam = nullptr;      // rows
   float* inv_lam = nullptr;  // rows, RN(1/lambda)
@@ -163,7 +164,7 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   for (auto& s : h->s) {
     cudaFree(s.codes); cudaFree(s.lam); cudaFree(s.inv_lam); cudaFree(s.row_amax); cudaFree(s.lam_scalar); cudaFree(s.Om);
     cudaFree(s.Y); cudaFree(s.Q0); cudaFree(s.Z); cudaFree(s.Q1); cudaFree(s.Gp); cudaFree(s.G);
-    cudaFree(s.gpart); cudaFree(s.counter); cudaFree(s.T64); cudaFree(s.VW); cudaFree(s.U);
+    cudaFree(s.gpart); cudaFree(s.counter); cudaFree(s.T64); cudaFree(s.VW); cudaFree(s.U); cudaFree(s.img);
   }
   cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->partial); cudaFree(h->Gcross); cudaFree(h->gpart_cross);
   cudaFree(h->counter_cross); cudaFree(h->VWbM); cudaFree(h->err_flag);
@@ -210,7 +211,8 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
       ok = ok && dalloc(&s.U, s.rows * s.ldu) && dalloc(&s.Om, K * h->W) && dalloc(&s.Y, s.rows * h->W) && dalloc(&s.Q0, s.rows * h->W) &&
            dalloc(&s.Z, K * h->W) && dalloc(&s.Q1, K * h->W) && dalloc(&s.Gp, s.rows * h->W) &&
            dalloc(&s.G, (int64_t)h->W * h->W) && dalloc(&s.gpart, (int64_t)kGramMaxBlocks * h->W * h->W) &&
-           dalloc(&s.counter, 1) && dalloc(&s.T64, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W);
+           dalloc(&s.counter, 1) && dalloc(&s.T64, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W) &&
+           dalloc(&s.img, 2 * tc_img_bytes(std::max<int64_t>(s.rows, K), h->W));
     }
   }
   if (h->W > 0) {
@@ -385,13 +387,14 @@ lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const 
   // S1: Y = R Omega   (Algorithm 1 sampling)
   for (int sd = 0; sd < 2; ++sd)
     nsp[sd] = launch_tc_proj_rows(view(h, sd), h->s[sd].Om, Ys[sd], nullptr, nullptr, W, part_of(h, sd),
-                                  part_elems(h), false, h->st);
+                                  part_elems(h), false, h->s[sd].img, h->st);
   for (int it = 0; it < h->cfg.power_iters; ++it) {
     // O1: Q0 = orth(Y)   (Y rows of A are sharded across ranks)
     if ((e = gram_step(h, Ys, rows, nsp, 0, Q0s, true)) != LRQMM_OK) return e;
     // S2: Z = R^T Q0  (reduction over rows; the A side is summed over ranks before its Gram)
     for (int sd = 0; sd < 2; ++sd)
-      nsp[sd] = launch_tc_proj_cols(view(h, sd), Q0s[sd], Zs[sd], W, part_of(h, sd), part_elems(h), multi, h->st);
+      nsp[sd] = launch_tc_proj_cols(view(h, sd), Q0s[sd], Zs[sd], W, part_of(h, sd), part_elems(h), multi,
+                                      h->s[sd].img, h->st);
     if (multi) {
       if ((e = allreduce_f32(h, Zs[0], (size_t)K * W)) != LRQMM_OK) return e;
       nsp[0] = nsp[1] = 1;
@@ -403,14 +406,14 @@ lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const 
     if (it + 1 < h->cfg.power_iters) {
       for (int sd = 0; sd < 2; ++sd)
         nsp[sd] = launch_tc_proj_rows(view(h, sd), Q1s[sd], Ys[sd], nullptr, nullptr, W, part_of(h, sd),
-                                      part_elems(h), false, h->st);
+                                      part_elems(h), false, h->s[sd].img, h->st);
     }
   }
   // S3 + cross: W_X = R_X Q1_X and G'_X = X~ Q1_other in one pass over X
   //   (Algorithm 1 on R^T: B = Q1^T R^T = W^T; RC1/RC2 skinny products)
   for (int sd = 0; sd < 2; ++sd)
     nsp[sd] = launch_tc_proj_rows(view(h, sd), Q1s[sd], Ys[sd], Q1s[1 - sd], h->s[sd].Gp, W, part_of(h, sd),
-                                  part_elems(h), false, h->st);
+                                  part_elems(h), false, h->s[sd].img, h->st);
   // T: W = sum(partials), truncation to rank r via eig(W^T W) (Algorithm 1)
   if ((e = gram_step(h, Ys, rows, nsp, 1, nullptr, true)) != LRQMM_OK) return e;
   // V_B^T V_A core: Q1_B^T Q1_A (fp64, W x W) -> Mab, VWb Mab
@@ -599,13 +602,15 @@ extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx
   const int64_t ldu = ((int64_t)K + 7) / 8 * 8;
   const int64_t pe = (int64_t)16 << 20;
   int16_t* U = nullptr;
+  uint8_t* img = nullptr;
   float *lam = nullptr, *inv = nullptr, *partial = nullptr;
   int8_t* codes = nullptr;
   int* flag = nullptr;
   bool ok = cudaMalloc(&U, sizeof(int16_t) * rows * ldu) == cudaSuccess &&
             cudaMalloc(&lam, sizeof(float) * rows) == cudaSuccess && cudaMalloc(&inv, sizeof(float) * rows) == cudaSuccess &&
             cudaMalloc(&codes, (size_t)rows * Kp) == cudaSuccess && cudaMalloc(&flag, sizeof(int)) == cudaSuccess &&
-            cudaMalloc(&partial, sizeof(float) * pe) == cudaSuccess;
+            cudaMalloc(&partial, sizeof(float) * pe) == cudaSuccess &&
+            cudaMalloc(&img, 2 * tc_img_bytes(rows > K ? rows : K, W)) == cudaSuccess;
   cudaError_t e = cudaErrorMemoryAllocation;
   if (ok) {
     cudaMemsetAsync(flag, 0, sizeof(int), st);
@@ -614,13 +619,13 @@ extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx
     q.codes = codes; q.lam = lam; q.inv_lam = inv; q.lam_fixed = nullptr; q.err_flag = flag; q.U = U; q.ldu = ldu;
     launch_quantize(q, st);
     SideView v{U, ldu, rows, K, codes, Kp, lam, inv};
-    if (mode == 0) launch_tc_proj_rows(v, P, OUT, nullptr, nullptr, W, partial, pe, true, st);
-    else if (mode == 1) launch_tc_proj_cols(v, P, OUT, W, partial, pe, true, st);
-    else launch_tc_proj_rows(v, P, OUT, P2, OUT2, W, partial, pe, true, st);
+    if (mode == 0) launch_tc_proj_rows(v, P, OUT, nullptr, nullptr, W, partial, pe, true, img, st);
+    else if (mode == 1) launch_tc_proj_cols(v, P, OUT, W, partial, pe, true, img, st);
+    else launch_tc_proj_rows(v, P, OUT, P2, OUT2, W, partial, pe, true, img, st);
     e = cudaStreamSynchronize(st);
     if (e == cudaSuccess) e = cudaGetLastError();
   }
-  cudaFree(U); cudaFree(lam); cudaFree(inv); cudaFree(codes); cudaFree(flag); cudaFree(partial);
+  cudaFree(U); cudaFree(lam); cudaFree(inv); cudaFree(codes); cudaFree(flag); cudaFree(partial); cudaFree(img);
   return e == cudaSuccess ? LRQMM_OK : (ok ? LRQMM_ERR_CUDA : LRQMM_ERR_ALLOC);
 }
 

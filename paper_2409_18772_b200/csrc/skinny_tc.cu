@@ -1,27 +1,42 @@
 // K2/K3 on the 5th-gen tensor cores: the RSVD passes over the quantization
 // residual (Algorithm 1 sampling / power iteration / projection, PAPER.md:124-140,
 // reading #11) and the cross products of Algorithm 2, computed as
-// tcgen05.mma kind::tf32 with a 3-term split (x = hi + lo, hi = tf32(x)):
-//     U P ~= U_hi P_hi + U_hi P_lo + U_lo P_hi                 (fp32-grade)
-// U is the residual fraction u = lambda x - code written by K1 (R = diag(1/lambda) U) in Q15
-// fixed point, so every pass streams 2 B per element from HBM — this kernel's roofline — and
-// the producer warps only widen u to fp32 and split it into tf32 hi/lo operand tiles (exact:
-// u16 / 2^15 has <= 16 significant bits, hi keeps 11, lo the rest).
+// tcgen05.mma kind::f16 (bf16 in, fp32 accumulate) on EXACT integer/float splits:
+//   U is the residual fraction u = lambda x - code written by K1 (R = diag(1/lambda) U) as the
+//   Q15 integer i = RN(2^15 u) = 256 h + l  (h = i >> 8, l = i & 255): 256 h and l are exact in
+//   bf16.  P = b1 + b2 + b3 with b1 = bf16(P), b2 = bf16(P - b1), b3 = bf16(P - b1 - b2) (to 2^-27).
+//     2^15 U P = (256 h) [b1 b2 b3] + l [b1 b2]   (dropped: l b3 < 2^-24 relative) (fp32-grade)
+//   Each k16 step is TWO instructions, N-stacked: A_h x [B1|B2|B3] (N = 3 W') and A_l x [B1|B2]
+//   (N = 2 W') into the same accumulator column groups; the epilogue sums the three groups.
+//   (tcgen05.mma costs max(~46, N/2) cycles per instruction at M = 128 (tools/mma_rate.cu), so
+//   wide N keeps the pass under its HBM time; the 3xTF32 form needed 12 N = 32 MMAs per k-block.)
+// Every pass streams 2 B of U per element from HBM — this kernel's roofline.
 //
 //   ROW mode  OUT1[i,:] = (1/lambda_i) sum_j U[i,j] P1[j,:]      (S1: Y = R Omega, S3: W = R Q1)
 //             OUT2[i,:] = (1/lambda_i) sum_j C[i,j] P2[j,:]      (dual: A~ Q1_other, codes exact in tf32)
-//             A operand = U tile, K-major SW128; B = P tile, MN-major SW128_BASE32B.
 //   COL mode  OUT[j,:]  = sum_i U[i,j] (P[i,:] / lambda_i)       (S2: Z = R^T Q0)
-//             A operand = U tile, MN-major SW128_BASE32B (U's natural layout); B as above.
+//
+// Operand placement (the design point of this kernel):
+//   A (the streamed U tile, M = 128 rows (ROW) / 128 columns (COL) of R, K = 32 per k-block)
+//     lives in TENSOR MEMORY: producer warps split u into (256 h, l) bf16 pairs and tcgen05.st
+//     them straight into TMEM columns; tcgen05.mma reads A from TMEM.  No shared-memory operand
+//     tiles and no generic->async proxy fence on the per-k-block path.
+//   B (P, K x W, tiny and shared by every CTA) is split into b1/b2/b3 ONCE per pass by
+//     k_prep_img into a global image that is byte-for-byte the K-major SWIZZLE_64B smem layout
+//     the MMA reads (rows [0,W') b1, [W',2W') b2, [2W',3W') b3); a bulk copy lands each
+//     k-block's image in the ring slot.
 //
 // Persistent, warp-specialised (448 threads, one CTA per SM):
-//   warp 13    : TMA issuer, streams raw tiles (U 8 KB, P, codes, 1/lambda) through a smem ring
-//   warps 0-7  : producers: raw U -> tf32 hi/lo operand tiles (+ codes -> fp32) (2-3 stages)
+//   warps 0-7  : producers: raw U (smem) -> bf16 (256 h, l) in TMEM (+ codes -> bf16 for dual);
+//                warp w owns TMEM lane quarter w % 4 and k-columns [16 (w / 4), +16)
+//   warps 8-11 : epilogue: TMEM accumulators (double-buffered) -> split-K partials
 //   warp 12    : TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 8-11 : epilogue: TMEM (double-buffered accumulators) -> split-K partials
+//   warp 13    : TMA issuer: U tile, B image(s), codes tile through an smem ring
 // Work unit = (128-row/col block, reduction split); partials are summed in a fixed order
 // by the consumer (deterministic, no float atomics).
 #include <cuda.h>
+
+#include <cuda_bf16.h>
 
 #include <cstring>
 
@@ -33,43 +48,38 @@ namespace lrqmm {
 namespace tcp {
 constexpr int BM = 128;  // output rows (ROW) / output cols (COL) per unit
 constexpr int BK = 32;   // reduction elements per k-block
-#ifndef LRQMM_PROD
-#define LRQMM_PROD 256
-#endif
-constexpr int kProd = LRQMM_PROD;  // producer threads
-constexpr int kProdWarps = kProd / 32;
+constexpr int kProdWarps = 8;
 constexpr int kMmaWarp = kProdWarps + 4;
 constexpr int kTmaWarp = kProdWarps + 5;
 constexpr int kThreads = (kProdWarps + 6) * 32;
-constexpr int kPer = BM * BK / 4 / kProd;        // 4-element groups of U per producer thread per k-block
-#ifndef LRQMM_OPST
-#define LRQMM_OPST 2
-#endif
-constexpr int OPST_MAX = LRQMM_OPST;
-constexpr int kATile = BM * BK * 4;    // 16 KB operand tile (hi or lo)
-constexpr int kRawTile = BM * BK * 2;  // 8 KB raw U tile (Q15)
-constexpr int kRawCodes = BM * BK;     // 4 KB raw code tile (dual)
+constexpr int kColsPerThr = BK / (kProdWarps / 4);  // 16 k-values of A per producer thread
+constexpr int kRawU = BM * BK * 2;                  // 8 KB raw U tile (Q15)
+constexpr int kRawCodes = BM * BK;                  // 4 KB raw code tile (dual)
 template <int kMode, int NA, bool kDual>
 struct Cfg {
-  static constexpr int WN = 32 * NA;
-  static constexpr int kBTile = BK * WN * 4;  // operand B tile (hi or lo)
-  static constexpr int kStage = (kDual ? 3 : 2) * kATile + (kDual ? 4 : 2) * kBTile;
-  // raw slot: U tile | P1 tile [BK][WN] | P2 tile | codes tile (dual) | 1/lambda[BK] (COL)
-  static constexpr int kRawP = BK * WN * 4;
-  static constexpr int kOffP2 = kRawTile + kRawP;
-  static constexpr int kOffCodes = kRawTile + (kDual ? 2 : 1) * kRawP;
-  static constexpr int kOffInv = kOffCodes + (kDual ? kRawCodes : 0);
-  static constexpr int kRawBytes = kOffInv + (kMode == 1 ? BK * 4 : 0);
+  static constexpr int WN = 32 * NA;          // W' (W rounded up to 32)
+  static constexpr int kBRows = 3 * WN;       // b1 | b2 | b3
+  static constexpr int kImg = kBRows * BK * 2;  // one k-block image: kBRows rows x 64 B
+  // raw slot: U tile | B image | B2 image (dual) | codes (dual)
+  static constexpr int kOffB = kRawU;
+  static constexpr int kOffB2 = kOffB + kImg;
+  static constexpr int kOffCodes = kOffB + (kDual ? 2 : 1) * kImg;
+  static constexpr int kRawBytes = kOffCodes + (kDual ? kRawCodes : 0);
   static constexpr int kRawSlot = (kRawBytes + 1023) / 1024 * 1024;
-  static constexpr int kBudget = 220 * 1024;
-  static constexpr bool fits(int op, int raw) { return op * kStage + raw * kRawSlot <= kBudget; }
-  static constexpr int OPST = fits(OPST_MAX, 3) ? OPST_MAX : (fits(2, 2) ? 2 : 1);
-  static constexpr int kRawSt = fits(OPST, 4) ? 4 : (fits(OPST, 3) ? 3 : 2);
-  static constexpr int kSmem = kRawSt * kRawSlot + OPST * kStage + 256 + 1024;
+  static constexpr int kBudget = 200 * 1024;
+  static constexpr int kRawSt = kBudget / kRawSlot >= 8 ? 8 : kBudget / kRawSlot;
+  static constexpr int kSmem = kRawSt * kRawSlot + 256 + 1024;
+  static_assert(kRawSt >= 3, "ring depth");
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
-  static constexpr int kAccCols = (kDual ? 2 : 1) * WN;  // per accumulator buffer
-  static constexpr uint32_t kTmemCols =
-      2 * kAccCols <= 32 ? 32 : (2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : 256));
+  // TMEM: accumulator buffer(s) of 3 W' (x2 dual) columns, then OPST A stages of
+  // (256 h, l[, codes]) x 16 columns (32 bf16 per lane per k-block each)
+  static constexpr int kAccCols = (kDual ? 2 : 1) * kBRows;
+  static constexpr int kAStage = (kDual ? 3 : 2) * (BK / 2);
+  static constexpr int kAccBufs = (2 * kAccCols + 2 * kAStage <= 512) ? 2 : 1;
+  static constexpr int OPST = (kAccBufs * kAccCols + 4 * kAStage <= 512)   ? 4
+                              : (kAccBufs * kAccCols + 3 * kAStage <= 512) ? 3
+                                                                           : 2;
+  static_assert(kAccBufs * kAccCols + OPST * kAStage <= 512, "TMEM budget");
 };
 }  // namespace tcp
 
@@ -80,70 +90,97 @@ struct TcArgs {
   int W;
   float* out1;  // partial base: split s at out + s * (nout * W)
   float* out2;
+  const uint8_t* img1;  // B images, one per global k-block
+  const uint8_t* img2;
   int64_t nout;   // rows (ROW) or K (COL)
   int64_t chunk;  // reduction elements per split (multiple of BK)
   int nblk, nsplit;
 };
 
 struct TcMaps {
-  CUtensorMap u, p1, p2, codes, inv;
+  CUtensorMap u, codes;
 };
 
-LRQMM_DEV float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
-
-// tf32 operands: K-major uses SWIZZLE_128B (type 2); MN-major must use
-// SWIZZLE_128B_BASE32B (type 1: 32 MN x 4 K atoms of 512 B, 32-byte chunks XOR row),
-// the only MN-major layout the tensor core accepts for 32-bit operands (probed on B200).
-LRQMM_DEV uint64_t desc_sw128(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t type) {
+// K-major SWIZZLE_64B descriptor (layout type 4): rows of 64 B, 8-row atoms of 512 B (SBO)
+LRQMM_DEV uint64_t desc_sw64(uint32_t addr) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)((512u >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1u << 46;
-  d |= (uint64_t)type << 61;
+  d |= (uint64_t)4u << 61;
   return d;
 }
-// kind::tf32, D f32, M = 128, N = n; a_mn / b_mn: operand is MN-major
-__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t n, uint32_t a_mn, uint32_t b_mn) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (a_mn << 15) | (b_mn << 16) | ((n >> 3) << 17) | ((128u >> 4) << 24);
+// kind::f16: D f32, A = B = bf16, both K-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_bf16(uint32_t n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((128u >> 4) << 24);
 }
-LRQMM_DEV void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+// D[tmem] (+)= A[tmem] * B[smem]
+LRQMM_DEV void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
-LRQMM_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-LRQMM_DEV uint2 lds64(uint32_t addr) {
-  uint2 v;
-  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
+LRQMM_DEV void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+LRQMM_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+LRQMM_DEV uint32_t lds_u16(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr) : "memory");
   return v;
 }
-// two Q15 residual fractions (packed int16) -> fp32 (exact)
-LRQMM_DEV float2 u_unfix(uint32_t w) {
-  constexpr float s = 1.f / kUScale;
-  return make_float2((float)(int16_t)(w & 0xffffu) * s, (float)(int16_t)(w >> 16) * s);
-}
-LRQMM_DEV uint32_t lds_u32(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+LRQMM_DEV uint4 lds128u(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+               : "memory");
   return v;
+}
+// two bf16 (first = lower k) packed into one 32-bit TMEM column word
+LRQMM_DEV uint32_t pack_bf16x2(float first, float second) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(first, second);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+// Q15 integers i0, i1 (consecutive k) -> (256 h0, 256 h1) and (l0, l1) as bf16 pairs (exact)
+LRQMM_DEV void split_q15(int i0, int i1, uint32_t& hw, uint32_t& lw) {
+  hw = pack_bf16x2((float)(i0 & ~255), (float)(i1 & ~255));
+  lw = pack_bf16x2((float)(i0 & 255), (float)(i1 & 255));
 }
 
-// byte offset of element (mn, k) in an MN-major SW128_BASE32B tile with nA 32-wide MN atoms
-// (LBO = 512 B between MN atoms, SBO = nA * 512 B between 4-deep K groups)
-LRQMM_DEV uint32_t off_mn(int mn, int k, int nA) {
-  const int row = k & 3;
-  return (uint32_t)((k >> 2) * (nA * 512) + (mn >> 5) * 512 + row * 128 + ((((mn & 31) >> 3) ^ row) << 5) +
-                    ((mn & 7) << 2));
+// byte offset of element (n, k), k < 32, in a K-major SWIZZLE_64B tile of bf16 rows
+__host__ __device__ inline uint32_t off_k64(int n, int k) {
+  return (uint32_t)((n >> 3) * 512 + (n & 7) * 64 + ((((k >> 3) ^ ((n & 7) >> 1)) & 3) << 4) + (k & 7) * 2);
 }
-// byte offset of element (mn, k) in a K-major SW128 tile (rows of 32 fp32)
-LRQMM_DEV uint32_t off_k(int mn, int k) {
-  const int row = mn & 7;
-  const int chunk = k >> 2;
-  return (uint32_t)((mn >> 3) * 1024 + row * 128 + ((chunk ^ row) << 4) + ((k & 3) << 2));
+
+// B image: for every k-block g of P (n x W, ld W), optionally row-scaled, the bf16 splits
+// b1 | b2 | b3 of P[32 g : 32 g + 32, :]^T in the smem byte layout above; rows >= n and
+// columns >= W are zero.  One thread per element.
+template <int NA>
+__global__ void __launch_bounds__(256) k_prep_img(const float* __restrict__ P, int64_t n, int W,
+                                                  const float* __restrict__ scale, int64_t nkb,
+                                                  uint8_t* __restrict__ img) {
+  constexpr int WN = 32 * NA;
+  constexpr int kImg = 3 * WN * tcp::BK * 2;
+  const int64_t total = nkb * tcp::BK * WN;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / WN;
+    const int c = (int)(e % WN);
+    const float v = (j < n && c < W) ? (scale ? P[j * W + c] * scale[j] : P[j * W + c]) : 0.f;
+    const __nv_bfloat16 b1 = __float2bfloat16_rn(v);
+    const float r1 = v - __bfloat162float(b1);
+    const __nv_bfloat16 b2 = __float2bfloat16_rn(r1);
+    const __nv_bfloat16 b3 = __float2bfloat16_rn(r1 - __bfloat162float(b2));
+    uint8_t* base = img + (j / tcp::BK) * kImg;
+    const int k = (int)(j % tcp::BK);
+    *reinterpret_cast<__nv_bfloat16*>(base + off_k64(c, k)) = b1;
+    *reinterpret_cast<__nv_bfloat16*>(base + off_k64(WN + c, k)) = b2;
+    *reinterpret_cast<__nv_bfloat16*>(base + off_k64(2 * WN + c, k)) = b3;
+  }
 }
 
 template <int kMode, int NA, bool kDual>
@@ -151,21 +188,19 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   using namespace tcp;
   using C = Cfg<kMode, NA, kDual>;
   constexpr int WN = C::WN;
-  constexpr int kBTile = C::kBTile;
-  constexpr int kStage = C::kStage;
   constexpr int RST = C::kRawSt;
   constexpr int OPST = C::OPST;
+  constexpr int NACC = C::kAccBufs;
   constexpr int kRawSlot = C::kRawSlot;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sRaw = smem;                  // RST raw slots (TMA)
-  uint8_t* sOp = smem + RST * kRawSlot;  // OPST x kStage operand tiles
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sOp + OPST * kStage);
+  uint8_t* sRaw = smem;  // RST raw slots (TMA)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sRaw + RST * kRawSlot);
   uint64_t* rfull = bars;            // RST
   uint64_t* rempty = bars + RST;     // RST
-  uint64_t* ofull = bars + 2 * RST;  // OPST
-  uint64_t* oempty = ofull + OPST;   // OPST
-  uint64_t* tfull = oempty + OPST;   // 2
+  uint64_t* afull = bars + 2 * RST;  // OPST
+  uint64_t* aempty = afull + OPST;   // OPST
+  uint64_t* tfull = aempty + OPST;   // 2
   uint64_t* tempty = tfull + 2;      // 2
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -176,11 +211,11 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   if (tid == 0) {
     for (int s = 0; s < RST; ++s) {
       mbar_init(&rfull[s], 1);
-      mbar_init(&rempty[s], kProdWarps);  // one elected arrival per producer warp
+      mbar_init(&rempty[s], kProdWarps + 1);  // producer warps (U read) + MMA commit (B read)
     }
     for (int s = 0; s < OPST; ++s) {
-      mbar_init(&ofull[s], kProdWarps);
-      mbar_init(&oempty[s], 1);
+      mbar_init(&afull[s], kProdWarps);
+      mbar_init(&aempty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -188,11 +223,12 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
     }
     fence_mbar_init();
   }
-  if (warp == kMmaWarp) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t tA0 = tmem + NACC * C::kAccCols;  // first A stage column
 
   auto unit_range = [&](int u, int& blk, int& split, int64_t& r0, int& nkb) {
     blk = u % a.nblk;
@@ -206,11 +242,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
     // ------------------------------------------------------ TMA: raw tiles
     if (lane == 0) {
       tma_prefetch_desc(&maps.u);
-      tma_prefetch_desc(&maps.p1);
-      if (kDual) {
-        tma_prefetch_desc(&maps.p2);
-        tma_prefetch_desc(&maps.codes);
-      }
+      if (kDual) tma_prefetch_desc(&maps.codes);
       int it = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         int blk, split, nkb;
@@ -224,20 +256,22 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
           const int k0 = (int)(r0 + (int64_t)kb * BK);
           if (kMode == 0) tma_load_2d(slot, &maps.u, &rfull[s], k0, blk * BM);
           else tma_load_2d(slot, &maps.u, &rfull[s], blk * BM, k0);
-          tma_load_2d(slot + kRawTile, &maps.p1, &rfull[s], 0, k0);
+          const int64_t g = k0 / BK;
+          bulk_load(slot + C::kOffB, a.img1 + g * C::kImg, C::kImg, &rfull[s]);
           if (kDual) {
-            tma_load_2d(slot + C::kOffP2, &maps.p2, &rfull[s], 0, k0);
+            bulk_load(slot + C::kOffB2, a.img2 + g * C::kImg, C::kImg, &rfull[s]);
             tma_load_2d(slot + C::kOffCodes, &maps.codes, &rfull[s], k0, blk * BM);
           }
-          if (kMode == 1) tma_load_1d(slot + C::kOffInv, &maps.inv, &rfull[s], k0);
         }
       }
     }
     __syncwarp();
   } else if (warp < kProdWarps) {
     // ------------------------------------------------------------ producers
-    constexpr int kPB4 = BK * WN / 4;
-    constexpr int kPBper = (kPB4 + kProd - 1) / kProd;
+    const int q = warp & 3;       // TMEM lane quarter of this warp
+    const int hh = warp >> 2;     // k half [16 hh, 16 hh + 16) of the k-block
+    const int m = q * 32 + lane;  // A row (TMEM lane) of this thread
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     int it = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       int blk, split, nkb;
@@ -245,133 +279,90 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       unit_range(u, blk, split, r0, nkb);
       for (int kb = 0; kb < nkb; ++kb, ++it) {
         const int rs = it % RST;
-        const int os = it % OPST;
-        // raw slot -> registers, then release the slot
+        const int as = it % OPST;
         mbar_wait(&rfull[rs], (it / RST) & 1);
         const uint32_t raw = smem_u32(sRaw) + rs * kRawSlot;
-        float4 xv[kPer];
-        uint32_t cw[kPer];
+        uint32_t hw[8], lw[8];
+        if (kMode == 0) {
+          // ROW: U tile [128 rows][32] int16, 64-byte rows, TMA SWIZZLE_64B (16-byte chunk c of row
+          // r stored at chunk c ^ ((r >> 1) & 3)); this thread reads chunks 2 hh, 2 hh + 1 of row m
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-          const int f = tid + kProd * q;
-          // raw U: ROW [BM rows][BK] int16 (64 B rows), COL [BK rows][BM] int16 (256 B rows)
-          const uint32_t ro =
-              kMode == 0 ? (uint32_t)((f >> 3) * 64 + (f & 7) * 8) : (uint32_t)((f >> 5) * 256 + (f & 31) * 8);
-          const uint2 w = lds64(raw + ro);
-          const float2 u01 = u_unfix(w.x), u23 = u_unfix(w.y);
-          xv[q] = make_float4(u01.x, u01.y, u23.x, u23.y);
-          if (kDual) cw[q] = lds_u32(raw + C::kOffCodes + (f >> 3) * 32 + (f & 7) * 4);
-        }
-        float4 pb1[kPBper], pb2[kPBper];
+          for (int h = 0; h < 2; ++h) {
+            const int c = 2 * hh + h;
+            const uint4 w = lds128u(raw + m * 64 + ((c ^ ((m >> 1) & 3)) << 4));
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int q = 0; q < kPBper; ++q) {
-          const int e = tid + kProd * q;
-          if (e < kPB4) {
-            pb1[q] = lds128(raw + kRawTile + e * 16);
-            if (kDual) pb2[q] = lds128(raw + C::kOffP2 + e * 16);
-            if (kMode == 1) {  // COL: R^T Q0 = U^T diag(1/lambda) Q0 -> scale the B rows by 1/lambda_i
-              const float il = lds32(raw + C::kOffInv + 4 * (e / (WN / 4)));
-              pb1[q] = make_float4(pb1[q].x * il, pb1[q].y * il, pb1[q].z * il, pb1[q].w * il);
-            }
+            for (int t = 0; t < 4; ++t)
+              split_q15((int)(int16_t)(ws[t] & 0xffffu), (int)(int16_t)(ws[t] >> 16), hw[h * 4 + t], lw[h * 4 + t]);
+          }
+        } else {
+          // COL: U tile [32 rows i][128 cols] int16 (256-byte rows); A row m = column m of R
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int i0 = hh * kColsPerThr + 2 * t;
+            split_q15((int)(int16_t)lds_u16(raw + i0 * 256 + m * 2), (int)(int16_t)lds_u16(raw + (i0 + 1) * 256 + m * 2),
+                      hw[t], lw[t]);
           }
         }
-        // operand stage
-        mbar_wait(&oempty[os], ((it / OPST) & 1) ^ 1);
-        const uint32_t st = smem_u32(sOp) + os * kStage;
-        const uint32_t sAhi = st;
-        const uint32_t sAlo = st + kATile;
-        const uint32_t sAc = st + 2 * kATile;
-        const uint32_t sBhi = st + (kDual ? 3 : 2) * kATile;
-        const uint32_t sBlo = sBhi + kBTile;
-        const uint32_t sB2hi = sBlo + kBTile;
-        const uint32_t sB2lo = sB2hi + kBTile;
+        uint32_t cw[8];
+        if (kDual) {
+          // codes tile [128 rows][32] int8, 32-byte rows, TMA SWIZZLE_32B (chunk c ^ ((r >> 2) & 1))
+          const uint4 w = lds128u(raw + C::kOffCodes + m * 32 + ((hh ^ ((m >> 2) & 1)) << 4));
+          const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int q = 0; q < kPBper; ++q) {
-          const int e = tid + kProd * q;
-          if (e < kPB4) {
-            const int pj = e / (WN / 4), pc = (e % (WN / 4)) * 4;
-            const uint32_t off = off_mn(pc, pj, NA);
-            const float4 h1 = make_float4(tf32_hi(pb1[q].x), tf32_hi(pb1[q].y), tf32_hi(pb1[q].z), tf32_hi(pb1[q].w));
-            sts128(sBhi + off, h1);
-            sts128(sBlo + off, make_float4(pb1[q].x - h1.x, pb1[q].y - h1.y, pb1[q].z - h1.z, pb1[q].w - h1.w));
-            if (kDual) {
-              const float4 h2 = make_float4(tf32_hi(pb2[q].x), tf32_hi(pb2[q].y), tf32_hi(pb2[q].z), tf32_hi(pb2[q].w));
-              sts128(sB2hi + off, h2);
-              sts128(sB2lo + off, make_float4(pb2[q].x - h2.x, pb2[q].y - h2.y, pb2[q].z - h2.z, pb2[q].w - h2.w));
-            }
+          for (int t = 0; t < 8; ++t) {
+            const uint32_t b = ws[t >> 1] >> (16 * (t & 1));
+            cw[t] = pack_bf16x2((float)(int8_t)(b & 0xffu), (float)(int8_t)((b >> 8) & 0xffu));
           }
         }
-#pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-          const int f = tid + kProd * q;
-          const uint32_t off = kMode == 0 ? off_k(f >> 3, (f & 7) * 4) : off_mn((f & 31) * 4, f >> 5, 4);
-          const float4 uv = xv[q];
-          const float4 h = make_float4(tf32_hi(uv.x), tf32_hi(uv.y), tf32_hi(uv.z), tf32_hi(uv.w));
-          sts128(sAhi + off, h);
-          sts128(sAlo + off, make_float4(uv.x - h.x, uv.y - h.y, uv.z - h.z, uv.w - h.w));
-          if (kDual) {
-            const uint32_t w = cw[q];
-            sts128(sAc + off, make_float4((float)(int8_t)(w & 0xff), (float)(int8_t)((w >> 8) & 0xff),
-                                          (float)(int8_t)((w >> 16) & 0xff), (float)(int8_t)(w >> 24)));
-          }
-        }
-        // one proxy fence orders this thread's operand-tile writes before the MMA (async proxy)
-        // reads them AND its raw-slot reads before the TMA (async proxy) refills the slot; a
-        // release without the fence let TMA overwrite rows before they were read on B200.
-        fence_proxy_async_smem();
+        mbar_wait(&aempty[as], ((it / OPST) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tA = tA0 + as * C::kAStage + lane_off + hh * 8;
+        tmem_st8(tA, hw);
+        tmem_st8(tA + 16, lw);
+        if (kDual) tmem_st8(tA + 32, cw);
+        tmem_st_wait();
+        tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(&ofull[os]);
-          mbar_arrive(&rempty[rs]);
+          mbar_arrive(&afull[as]);
+          mbar_arrive(&rempty[rs]);  // U consumed (its values are in TMEM)
         }
       }
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(WN, kMode == 1 ? 1u : 0u, 1u);
-      // descriptors of stage 0 at k-step 0; other stages / k-steps differ only in the start
-      // address field (addr >> 4 in the low 14 bits, no carry below 256 KB of smem)
-      constexpr uint32_t lboA = kMode == 0 ? 16 : 512, sboA = kMode == 0 ? 1024 : 2048, tA = kMode == 0 ? 2 : 1;
-      constexpr uint32_t kAStep = kMode == 0 ? 32 : 4096;  // bytes per 8-deep k-step (K-major / MN-major)
-      const uint32_t st0 = smem_u32(sOp);
-      const uint64_t dA0 = desc_sw128(st0, lboA, sboA, tA);
-      const uint64_t dB0 = desc_sw128(st0 + (kDual ? 3 : 2) * kATile, 512, NA * 512, 1);
+      constexpr uint32_t id3 = idesc_bf16(3 * WN), id2 = idesc_bf16(2 * WN);
+      const uint64_t dB0 = desc_sw64(smem_u32(sRaw) + C::kOffB);
       int it = 0, lu = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
         int blk, split, nkb;
         int64_t r0;
         unit_range(u, blk, split, r0, nkb);
-        const int acc = lu & 1;
-        mbar_wait(&tempty[acc], ((lu >> 1) & 1) ^ 1);
+        const int acc = NACC == 2 ? (lu & 1) : 0;
+        const uint32_t tph = NACC == 2 ? ((lu >> 1) & 1) : (lu & 1);
+        mbar_wait(&tempty[acc], tph ^ 1);
         tc_fence_after();
         const uint32_t d1 = tmem + acc * C::kAccCols;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int os = it % OPST;
-          mbar_wait(&ofull[os], (it / OPST) & 1);
+          const int rs = it % RST;
+          const int as = it % OPST;
+          mbar_wait(&afull[as], (it / OPST) & 1);
+          mbar_wait(&rfull[rs], (it / RST) & 1);  // B image landed
           tc_fence_after();
-          const uint64_t so = (uint64_t)((os * kStage) >> 4);
+          const uint64_t so = (uint64_t)((rs * kRawSlot) >> 4);
+          const uint32_t aS = tA0 + as * C::kAStage;
 #pragma unroll
-          for (int k = 0; k < BK / 8; ++k) {
-            const uint64_t aoff = so + ((k * kAStep) >> 4);
-            const uint64_t boff = so + ((k * (NA * 1024)) >> 4);
-            const uint64_t dAhi = dA0 + aoff;
-            const uint64_t dAlo = dA0 + aoff + (kATile >> 4);
-            const uint64_t dBhi = dB0 + boff;
-            const uint64_t dBlo = dB0 + boff + (kBTile >> 4);
+          for (int k = 0; k < 2; ++k) {
+            const uint64_t dB = dB0 + so + ((k * 32) >> 4);  // 16 bf16 along K inside the 64-byte row
             const uint32_t acc0 = (kb | k) != 0 ? 1u : 0u;
-            umma_tf32(d1, dAhi, dBhi, idesc, acc0);
-            umma_tf32(d1, dAhi, dBlo, idesc, 1u);
-            umma_tf32(d1, dAlo, dBhi, idesc, 1u);
-            if (kDual) {
-              const uint64_t dAc = dA0 + aoff + ((2 * kATile) >> 4);
-              const uint64_t dB2hi = dB0 + boff + ((2 * kBTile) >> 4);
-              const uint64_t dB2lo = dB0 + boff + ((3 * kBTile) >> 4);
-              umma_tf32(d1 + WN, dAc, dB2hi, idesc, acc0);
-              umma_tf32(d1 + WN, dAc, dB2lo, idesc, 1u);
-            }
+            umma_bf16_ts(d1, aS + k * 8, dB, id3, acc0);         // (256 h) x [b1 | b2 | b3]
+            umma_bf16_ts(d1, aS + 16 + k * 8, dB, id2, 1u);      // l x [b1 | b2]
+            if (kDual) umma_bf16_ts(d1 + 3 * WN, aS + 32 + k * 8, dB + (C::kImg >> 4), id3, acc0);  // codes x P2
           }
-          umma_commit(&oempty[os]);
+          umma_commit(&aempty[as]);
+          umma_commit(&rempty[rs]);
         }
         umma_commit(&tfull[acc]);
       }
@@ -385,28 +376,35 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       int blk, split, nkb;
       int64_t r0;
       unit_range(u, blk, split, r0, nkb);
-      const int acc = lu & 1;
-      mbar_wait(&tfull[acc], (lu >> 1) & 1);
+      const int acc = NACC == 2 ? (lu & 1) : 0;
+      const uint32_t tph = NACC == 2 ? ((lu >> 1) & 1) : (lu & 1);
+      mbar_wait(&tfull[acc], tph);
       tc_fence_after();
       const int64_t orow = (int64_t)blk * BM + quad * 32 + lane;
       const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + acc * C::kAccCols;
-      // ROW: rows of R (and of X~) carry 1/lambda_i; COL already folded it into B
+      // ROW: rows of R (and of X~) carry 1/lambda_i; COL folded it into the B image.  U is Q15.
       float inv_row = 1.f;
       if (kMode == 0) inv_row = orow < a.rows ? __ldg(a.inv_lam + orow) : 1.f;
       float* out1 = a.out1 + (int64_t)split * a.nout * a.W;
       float* out2 = kDual ? a.out2 + (int64_t)split * a.nout * a.W : nullptr;
-#pragma unroll
+#pragma unroll 1
       for (int h = 0; h < NA * (kDual ? 2 : 1); ++h) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(trow + h * 32, v);
-        tmem_ld_wait();
         const bool second = kDual && h >= NA;
         const int cbase = (second ? h - NA : h) * 32;
+        const uint32_t tg = trow + (second ? 3 * WN : 0) + cbase;
+        uint32_t v0[32], v1[32], v2[32];
+        tmem_ld_32x32b_x32(tg, v0);
+        tmem_ld_32x32b_x32(tg + WN, v1);
+        tmem_ld_32x32b_x32(tg + 2 * WN, v2);
+        tmem_ld_wait();
+        const float sc = second ? inv_row : inv_row * (1.f / kUScale);
         if (orow < a.nout) {
           float* o = (second ? out2 : out1) + orow * a.W;
 #pragma unroll
           for (int c = 0; c < 32; ++c)
-            if (cbase + c < a.W) o[cbase + c] = __fmul_rn(__uint_as_float(v[c]), inv_row);
+            if (cbase + c < a.W)
+              o[cbase + c] =
+                  __fmul_rn((__uint_as_float(v0[c]) + __uint_as_float(v1[c])) + __uint_as_float(v2[c]), sc);
         }
       }
       tc_fence_before();
@@ -416,7 +414,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   __syncthreads();
   if (warp == kMmaWarp) {
     tc_fence_after();
-    tmem_free<C::kTmemCols>(tmem);
+    tmem_free<512>(tmem);
   }
 }
 
@@ -428,9 +426,23 @@ __global__ void k_reduce_splits_tc(const float* __restrict__ part, int nsplit, i
   }
 }
 
+int64_t tc_img_bytes(int64_t n, int W) {
+  const int WN = W <= 32 ? 32 : 64;
+  return (n + tcp::BK - 1) / tcp::BK * (3 * WN * tcp::BK * 2);
+}
+
+template <int NA>
+static void prep_img(const float* P, int64_t n, int W, const float* scale, uint8_t* img, cudaStream_t st) {
+  const int64_t nkb = (n + tcp::BK - 1) / tcp::BK;
+  const int64_t total = nkb * tcp::BK * (32 * NA);
+  const int g = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+  k_prep_img<NA><<<g, 256, 0, st>>>(P, n, W, scale, nkb, img);
+  ++launch_counter();
+}
+
 template <int kMode, int NA, bool kDual>
 static int run_tc(const SideView& s, const float* P1, const float* P2, int W, float* OUT1, float* OUT2, float* partial,
-                  int64_t pe, bool reduce1, cudaStream_t st) {
+                  int64_t pe, bool reduce1, uint8_t* img, cudaStream_t st) {
   using namespace tcp;
   using C = Cfg<kMode, NA, kDual>;
   static bool attr = false;
@@ -449,6 +461,12 @@ static int run_tc(const SideView& s, const float* P1, const float* P2, int W, fl
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t nblk = (a.nout + BM - 1) / BM;
   const int64_t rlen = kMode == 0 ? (int64_t)s.K : s.rows;
+  // B images of P1 (and P2) over the reduction dimension; COL folds 1/lambda_i into P's rows
+  const int64_t ib = tc_img_bytes(rlen, W);
+  prep_img<NA>(P1, rlen, W, kMode == 1 ? s.inv_lam : nullptr, img, st);
+  if (kDual) prep_img<NA>(P2, rlen, W, nullptr, img + ib, st);
+  a.img1 = img;
+  a.img2 = img + ib;
   // enough units for ~6 per SM (the persistent grid balances them), each >= 8 k-blocks
   int64_t ns = (6LL * nsm + nblk - 1) / nblk;
   const int64_t maxs = (rlen + 8 * BK - 1) / (8 * BK);
@@ -465,15 +483,12 @@ static int run_tc(const SideView& s, const float* P1, const float* P2, int W, fl
   a.out2 = ns == 1 ? OUT2 : partial + ns * a.nout * W;
   alignas(64) TcMaps maps;
   memset(&maps, 0, sizeof(maps));
-  if (kMode == 0) encode_map_2d(&maps.u, 2, s.U, (uint64_t)s.K, (uint64_t)s.rows, (uint64_t)s.ldu * 2, BK, BM);
-  else encode_map_2d(&maps.u, 2, s.U, (uint64_t)s.K, (uint64_t)s.rows, (uint64_t)s.ldu * 2, BM, BK);
-  // P tiles [BK rows][WN cols]; columns >= W and rows past the end are zero-filled by TMA
-  encode_map_2d(&maps.p1, 1, P1, (uint64_t)W, (uint64_t)rlen, (uint64_t)W * 4, C::WN, BK);
-  if (kDual) {
-    encode_map_2d(&maps.p2, 1, P2, (uint64_t)W, (uint64_t)rlen, (uint64_t)W * 4, C::WN, BK);
-    encode_map_2d(&maps.codes, 0, s.codes, (uint64_t)s.Kp, (uint64_t)s.rows, (uint64_t)s.Kp, BK, BM);
-  }
-  if (kMode == 1) encode_map_1d_f32(&maps.inv, s.inv_lam, (uint64_t)s.rows, BK);
+  if (kMode == 0)
+    encode_map_2d_sw(&maps.u, 2, s.U, (uint64_t)s.K, (uint64_t)s.rows, (uint64_t)s.ldu * 2, BK, BM, 64);
+  else
+    encode_map_2d_sw(&maps.u, 2, s.U, (uint64_t)s.K, (uint64_t)s.rows, (uint64_t)s.ldu * 2, BM, BK, 0);
+  if (kDual)
+    encode_map_2d_sw(&maps.codes, 0, s.codes, (uint64_t)s.Kp, (uint64_t)s.rows, (uint64_t)s.Kp, BK, BM, 32);
   const int64_t units = nblk * ns;
   const int grid = (int)(units < nsm ? units : nsm);
   k_tc_proj<kMode, NA, kDual><<<grid, kThreads, C::kSmem, st>>>(maps, a);
@@ -497,21 +512,21 @@ static int run_tc(const SideView& s, const float* P1, const float* P2, int W, fl
 // number of split-K partials; with reduce1 == false and a result > 1, OUT1 is left as
 // partials at `partial` (summed by the fused Gram kernel).
 int launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
-                        float* partial, int64_t pe, bool reduce1, cudaStream_t st) {
+                        float* partial, int64_t pe, bool reduce1, uint8_t* img, cudaStream_t st) {
   if (s.rows == 0 || s.K == 0) return 0;
   if (W <= 32) {
-    if (P2) return run_tc<0, 1, true>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, st);
-    return run_tc<0, 1, false>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, st);
+    if (P2) return run_tc<0, 1, true>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
+    return run_tc<0, 1, false>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
   }
-  if (P2) return run_tc<0, 2, true>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, st);
-  return run_tc<0, 2, false>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, st);
+  if (P2) return run_tc<0, 2, true>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
+  return run_tc<0, 2, false>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
 }
 
 int launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t pe, bool reduce1,
-                        cudaStream_t st) {
+                        uint8_t* img, cudaStream_t st) {
   if (s.K == 0 || s.rows == 0) return 0;
-  if (W <= 32) return run_tc<1, 1, false>(s, P, nullptr, W, OUT, nullptr, partial, pe, reduce1, st);
-  return run_tc<1, 2, false>(s, P, nullptr, W, OUT, nullptr, partial, pe, reduce1, st);
+  if (W <= 32) return run_tc<1, 1, false>(s, P, nullptr, W, OUT, nullptr, partial, pe, reduce1, img, st);
+  return run_tc<1, 2, false>(s, P, nullptr, W, OUT, nullptr, partial, pe, reduce1, img, st);
 }
 
 }  // namespace lrqmm
