@@ -8,8 +8,9 @@
 //     2^15 U P = (256 h) [b1 b2 b3] + l [b1 b2]   (dropped: l b3 < 2^-24 relative) (fp32-grade)
 //   Each k16 step is TWO instructions, N-stacked: A_h x [B1|B2|B3] (N = 3 W') and A_l x [B1|B2]
 //   (N = 2 W') into the same accumulator column groups; the epilogue sums the three groups.
-//   (tcgen05.mma costs max(~46, N/2) cycles per instruction at M = 128 (tools/mma_rate.cu), so
-//   wide N keeps the pass under its HBM time; the 3xTF32 form needed 12 N = 32 MMAs per k-block.)
+//   (tcgen05.mma costs max(~46-59, N/2) cycles per instruction at M = 128 plus ~45 per commit
+//   (tools/mma_rate.cu), so wide N and 64-deep k-blocks (8 MMAs per commit) keep the single
+//   issuing thread under the pass's HBM time; 3xTF32 needed 12 N = 32 MMAs per 32-deep k-block.)
 // Every pass streams 2 B of U per element from HBM — this kernel's roofline.
 //
 //   ROW mode  OUT1[i,:] = (1/lambda_i) sum_j U[i,j] P1[j,:]      (S1: Y = R Omega, S3: W = R Q1)
@@ -17,21 +18,23 @@
 //   COL mode  OUT[j,:]  = sum_i U[i,j] (P[i,:] / lambda_i)       (S2: Z = R^T Q0)
 //
 // Operand placement (the design point of this kernel):
-//   A (the streamed U tile, M = 128 rows (ROW) / 128 columns (COL) of R, K = 32 per k-block)
+//   A (the streamed U tile, M = 128 rows (ROW) / 128 columns (COL) of R, K = 64 per k-block)
 //     lives in TENSOR MEMORY: producer warps split u into (256 h, l) bf16 pairs and tcgen05.st
 //     them straight into TMEM columns; tcgen05.mma reads A from TMEM.  No shared-memory operand
 //     tiles and no generic->async proxy fence on the per-k-block path.
 //   B (P, K x W, tiny and shared by every CTA) is split into b1/b2/b3 ONCE per pass by
-//     k_prep_img into a global image that is byte-for-byte the K-major SWIZZLE_64B smem layout
+//     k_prep_img into a global image that is byte-for-byte the K-major SWIZZLE_128B smem layout
 //     the MMA reads (rows [0,W') b1, [W',2W') b2, [2W',3W') b3); a bulk copy lands each
 //     k-block's image in the ring slot.
 //
-// Persistent, warp-specialised (448 threads, one CTA per SM):
-//   warps 0-7  : producers: raw U (smem) -> bf16 (256 h, l) in TMEM (+ codes -> bf16 for dual);
-//                warp w owns TMEM lane quarter w % 4 and k-columns [16 (w / 4), +16)
-//   warps 8-11 : epilogue: TMEM accumulators (double-buffered) -> split-K partials
-//   warp 12    : TMEM allocator + single-thread tcgen05.mma issuer
-//   warp 13    : TMA issuer: U tile, B image(s), codes tile through an smem ring
+// Persistent, warp-specialised (704 threads, one CTA per SM):
+//   warps 0-15 : producers: raw U (smem) -> bf16 (256 h, l) in TMEM (+ codes -> bf16 for dual);
+//                warp w owns TMEM lane quarter w % 4 and k-values [16 (w / 4), +16) of each k-block
+//   warps 16-19: epilogue: TMEM accumulators -> registers (releases the buffer) -> split-K partials
+//   warp 20    : TMEM allocator + single-thread tcgen05.mma issuer
+//   warp 21    : TMA issuer: U tile, B image(s), codes tile
+// Slot s of the S-deep ring owns raw smem slot s AND TMEM A stage s: one MMA commit (free[s])
+// releases both; producers never wait on it (the TMA refill of slot s already did).
 // Work unit = (128-row/col block, reduction split); partials are summed in a fixed order
 // by the consumer (deterministic, no float atomics).
 #include <cuda.h>
@@ -47,39 +50,41 @@ namespace lrqmm {
 
 namespace tcp {
 constexpr int BM = 128;  // output rows (ROW) / output cols (COL) per unit
-constexpr int BK = 32;   // reduction elements per k-block
-constexpr int kProdWarps = 8;
+constexpr int BK = 64;   // reduction elements per k-block
+constexpr int kProdWarps = 16;
 constexpr int kMmaWarp = kProdWarps + 4;
 constexpr int kTmaWarp = kProdWarps + 5;
 constexpr int kThreads = (kProdWarps + 6) * 32;
 constexpr int kColsPerThr = BK / (kProdWarps / 4);  // 16 k-values of A per producer thread
-constexpr int kRawU = BM * BK * 2;                  // 8 KB raw U tile (Q15)
-constexpr int kRawCodes = BM * BK;                  // 4 KB raw code tile (dual)
+constexpr int kWords = kColsPerThr / 2;             // 8 TMEM columns per A part per thread
+constexpr int kRawU = BM * BK * 2;                  // 16 KB raw U tile (Q15)
+constexpr int kRawCodes = BM * BK;                  // 8 KB raw code tile (dual)
 template <int kMode, int NA, bool kDual>
 struct Cfg {
-  static constexpr int WN = 32 * NA;          // W' (W rounded up to 32)
-  static constexpr int kBRows = 3 * WN;       // b1 | b2 | b3
-  static constexpr int kImg = kBRows * BK * 2;  // one k-block image: kBRows rows x 64 B
+  static constexpr int WN = 32 * NA;              // W' (W rounded up to 32)
+  static constexpr int kBRows = 3 * WN;           // b1 | b2 | b3
+  static constexpr int kImg = kBRows * BK * 2;    // one k-block image: kBRows rows x 128 B
+  static constexpr int kCodesN = NA == 1 ? 3 * WN : 2 * WN;  // codes x [b1|b2|b3] (x [b1|b2] at W' = 64)
   // raw slot: U tile | B image | B2 image (dual) | codes (dual)
   static constexpr int kOffB = kRawU;
   static constexpr int kOffB2 = kOffB + kImg;
   static constexpr int kOffCodes = kOffB + (kDual ? 2 : 1) * kImg;
   static constexpr int kRawBytes = kOffCodes + (kDual ? kRawCodes : 0);
   static constexpr int kRawSlot = (kRawBytes + 1023) / 1024 * 1024;
-  static constexpr int kBudget = 200 * 1024;
-  static constexpr int kRawSt = kBudget / kRawSlot >= 8 ? 8 : kBudget / kRawSlot;
-  static constexpr int kSmem = kRawSt * kRawSlot + 256 + 1024;
-  static_assert(kRawSt >= 3, "ring depth");
-  static_assert(kSmem <= 227 * 1024, "shared memory budget");
-  // TMEM: accumulator buffer(s) of 3 W' (x2 dual) columns, then OPST A stages of
-  // (256 h, l[, codes]) x 16 columns (32 bf16 per lane per k-block each)
-  static constexpr int kAccCols = (kDual ? 2 : 1) * kBRows;
+  // TMEM: accumulator buffer(s), then one A stage per ring slot: (256 h, l[, codes]) x 32 columns
+  static constexpr int kAccCols = kBRows + (kDual ? kCodesN : 0);
   static constexpr int kAStage = (kDual ? 3 : 2) * (BK / 2);
-  static constexpr int kAccBufs = (2 * kAccCols + 2 * kAStage <= 512) ? 2 : 1;
-  static constexpr int OPST = (kAccBufs * kAccCols + 4 * kAStage <= 512)   ? 4
-                              : (kAccBufs * kAccCols + 3 * kAStage <= 512) ? 3
-                                                                           : 2;
-  static_assert(kAccBufs * kAccCols + OPST * kAStage <= 512, "TMEM budget");
+  static constexpr int kAccBufs = (2 * kAccCols + 4 * kAStage <= 512) ? 2 : 1;
+  static constexpr int kTmemS = (512 - kAccBufs * kAccCols) / kAStage;
+  static constexpr int kSmemS = (200 * 1024) / kRawSlot;
+  static constexpr int S0 = kTmemS < kSmemS ? kTmemS : kSmemS;
+  static constexpr int S = S0 > 6 ? 6 : S0;
+  static_assert(S >= 2, "ring depth");
+  static constexpr int kSmem = S * kRawSlot + 256 + 1024;
+  static_assert(kSmem <= 227 * 1024, "shared memory budget");
+  static_assert(kAccBufs * kAccCols + S * kAStage <= 512, "TMEM budget");
+  static constexpr int kOutCols = NA * 32 * (kDual ? 2 : 1);  // outputs per row
+  static constexpr bool kEarlyRelease = kOutCols <= 64;       // accumulators fit in registers
 };
 }  // namespace tcp
 
@@ -101,14 +106,14 @@ struct TcMaps {
   CUtensorMap u, codes;
 };
 
-// K-major SWIZZLE_64B descriptor (layout type 4): rows of 64 B, 8-row atoms of 512 B (SBO)
-LRQMM_DEV uint64_t desc_sw64(uint32_t addr) {
+// K-major SWIZZLE_128B descriptor (layout type 2): rows of 128 B, 8-row atoms of 1024 B (SBO)
+LRQMM_DEV uint64_t desc_sw128k(uint32_t addr) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFFu);
   d |= (uint64_t)1u << 16;
-  d |= (uint64_t)((512u >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)((1024u >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1u << 46;
-  d |= (uint64_t)4u << 61;
+  d |= (uint64_t)2u << 61;
   return d;
 }
 // kind::f16: D f32, A = B = bf16, both K-major, M = 128, N = n
@@ -124,7 +129,7 @@ LRQMM_DEV void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, ui
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
-LRQMM_DEV void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+LRQMM_DEV void tmem_st(uint32_t taddr, const uint32_t (&v)[8]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
                "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                : "memory");
@@ -152,34 +157,48 @@ LRQMM_DEV void split_q15(int i0, int i1, uint32_t& hw, uint32_t& lw) {
   lw = pack_bf16x2((float)(i0 & 255), (float)(i1 & 255));
 }
 
-// byte offset of element (n, k), k < 32, in a K-major SWIZZLE_64B tile of bf16 rows
-__host__ __device__ inline uint32_t off_k64(int n, int k) {
-  return (uint32_t)((n >> 3) * 512 + (n & 7) * 64 + ((((k >> 3) ^ ((n & 7) >> 1)) & 3) << 4) + (k & 7) * 2);
+// byte offset of element (n, k), k < 64, in a K-major SWIZZLE_128B tile of bf16 rows (128 B)
+__host__ __device__ inline uint32_t off_k128(int n, int k) {
+  return (uint32_t)((n >> 3) * 1024 + (n & 7) * 128 + ((((k >> 3) ^ (n & 7)) & 7) << 4) + (k & 7) * 2);
 }
 
 // B image: for every k-block g of P (n x W, ld W), optionally row-scaled, the bf16 splits
-// b1 | b2 | b3 of P[32 g : 32 g + 32, :]^T in the smem byte layout above; rows >= n and
-// columns >= W are zero.  One thread per element.
+// b1 | b2 | b3 of P[64 g : 64 g + 64, :]^T in the smem byte layout above; rows >= n and
+// columns >= W are zero.  One thread per (column, 8 consecutive k): three 16-byte stores.
 template <int NA>
 __global__ void __launch_bounds__(256) k_prep_img(const float* __restrict__ P, int64_t n, int W,
                                                   const float* __restrict__ scale, int64_t nkb,
                                                   uint8_t* __restrict__ img) {
   constexpr int WN = 32 * NA;
   constexpr int kImg = 3 * WN * tcp::BK * 2;
-  const int64_t total = nkb * tcp::BK * WN;
+  constexpr int kChunks = tcp::BK / 8;
+  const int64_t total = nkb * kChunks * WN;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e / WN;
-    const int c = (int)(e % WN);
-    const float v = (j < n && c < W) ? (scale ? P[j * W + c] * scale[j] : P[j * W + c]) : 0.f;
-    const __nv_bfloat16 b1 = __float2bfloat16_rn(v);
-    const float r1 = v - __bfloat162float(b1);
-    const __nv_bfloat16 b2 = __float2bfloat16_rn(r1);
-    const __nv_bfloat16 b3 = __float2bfloat16_rn(r1 - __bfloat162float(b2));
-    uint8_t* base = img + (j / tcp::BK) * kImg;
-    const int k = (int)(j % tcp::BK);
-    *reinterpret_cast<__nv_bfloat16*>(base + off_k64(c, k)) = b1;
-    *reinterpret_cast<__nv_bfloat16*>(base + off_k64(WN + c, k)) = b2;
-    *reinterpret_cast<__nv_bfloat16*>(base + off_k64(2 * WN + c, k)) = b3;
+    const int c = (int)(e % WN);  // consecutive threads: consecutive columns (coalesced reads)
+    const int64_t rest = e / WN;
+    const int ch = (int)(rest % kChunks);
+    const int64_t g = rest / kChunks;
+    uint32_t w1[4], w2[4], w3[4];
+#pragma unroll
+    for (int t = 0; t < 8; t += 2) {
+      float b1[2], b2[2], b3[2];
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        const int64_t j = g * tcp::BK + ch * 8 + t + d;
+        const float v = (j < n && c < W) ? (scale ? P[j * W + c] * scale[j] : P[j * W + c]) : 0.f;
+        b1[d] = __bfloat162float(__float2bfloat16_rn(v));
+        const float r1 = v - b1[d];
+        b2[d] = __bfloat162float(__float2bfloat16_rn(r1));
+        b3[d] = r1 - b2[d];
+      }
+      w1[t / 2] = pack_bf16x2(b1[0], b1[1]);
+      w2[t / 2] = pack_bf16x2(b2[0], b2[1]);
+      w3[t / 2] = pack_bf16x2(b3[0], b3[1]);
+    }
+    uint8_t* base = img + g * kImg;
+    *reinterpret_cast<uint4*>(base + off_k128(c, ch * 8)) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+    *reinterpret_cast<uint4*>(base + off_k128(WN + c, ch * 8)) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+    *reinterpret_cast<uint4*>(base + off_k128(2 * WN + c, ch * 8)) = make_uint4(w3[0], w3[1], w3[2], w3[3]);
   }
 }
 
@@ -188,20 +207,18 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   using namespace tcp;
   using C = Cfg<kMode, NA, kDual>;
   constexpr int WN = C::WN;
-  constexpr int RST = C::kRawSt;
-  constexpr int OPST = C::OPST;
+  constexpr int S = C::S;
   constexpr int NACC = C::kAccBufs;
   constexpr int kRawSlot = C::kRawSlot;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sRaw = smem;  // RST raw slots (TMA)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sRaw + RST * kRawSlot);
-  uint64_t* rfull = bars;            // RST
-  uint64_t* rempty = bars + RST;     // RST
-  uint64_t* afull = bars + 2 * RST;  // OPST
-  uint64_t* aempty = afull + OPST;   // OPST
-  uint64_t* tfull = aempty + OPST;   // 2
-  uint64_t* tempty = tfull + 2;      // 2
+  uint8_t* sRaw = smem;  // S raw slots (TMA)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sRaw + S * kRawSlot);
+  uint64_t* full = bars;           // S: TMA landed
+  uint64_t* afull = bars + S;      // S: A stage written (producer warps)
+  uint64_t* freeb = bars + 2 * S;  // S: MMA done with slot (raw smem + TMEM A stage)
+  uint64_t* tfull = bars + 3 * S;  // 2
+  uint64_t* tempty = tfull + 2;    // 2
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -209,13 +226,10 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   const int nunits = a.nblk * a.nsplit;
 
   if (tid == 0) {
-    for (int s = 0; s < RST; ++s) {
-      mbar_init(&rfull[s], 1);
-      mbar_init(&rempty[s], kProdWarps + 1);  // producer warps (U read) + MMA commit (B read)
-    }
-    for (int s = 0; s < OPST; ++s) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
       mbar_init(&afull[s], kProdWarps);
-      mbar_init(&aempty[s], 1);
+      mbar_init(&freeb[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -228,7 +242,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tA0 = tmem + NACC * C::kAccCols;  // first A stage column
+  const uint32_t tA0 = tmem + NACC * C::kAccCols;  // A stage of slot 0
 
   auto unit_range = [&](int u, int& blk, int& split, int64_t& r0, int& nkb) {
     blk = u % a.nblk;
@@ -249,18 +263,18 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
         int64_t r0;
         unit_range(u, blk, split, r0, nkb);
         for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % RST;
-          mbar_wait(&rempty[s], ((it / RST) & 1) ^ 1);
+          const int s = it % S;
+          mbar_wait(&freeb[s], ((it / S) & 1) ^ 1);
           uint8_t* slot = sRaw + s * kRawSlot;
-          mbar_arrive_expect_tx(&rfull[s], C::kRawBytes);
+          mbar_arrive_expect_tx(&full[s], C::kRawBytes);
           const int k0 = (int)(r0 + (int64_t)kb * BK);
-          if (kMode == 0) tma_load_2d(slot, &maps.u, &rfull[s], k0, blk * BM);
-          else tma_load_2d(slot, &maps.u, &rfull[s], blk * BM, k0);
+          if (kMode == 0) tma_load_2d(slot, &maps.u, &full[s], k0, blk * BM);
+          else tma_load_2d(slot, &maps.u, &full[s], blk * BM, k0);
           const int64_t g = k0 / BK;
-          bulk_load(slot + C::kOffB, a.img1 + g * C::kImg, C::kImg, &rfull[s]);
+          bulk_load(slot + C::kOffB, a.img1 + g * C::kImg, C::kImg, &full[s]);
           if (kDual) {
-            bulk_load(slot + C::kOffB2, a.img2 + g * C::kImg, C::kImg, &rfull[s]);
-            tma_load_2d(slot + C::kOffCodes, &maps.codes, &rfull[s], k0, blk * BM);
+            bulk_load(slot + C::kOffB2, a.img2 + g * C::kImg, C::kImg, &full[s]);
+            tma_load_2d(slot + C::kOffCodes, &maps.codes, &full[s], k0, blk * BM);
           }
         }
       }
@@ -269,7 +283,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   } else if (warp < kProdWarps) {
     // ------------------------------------------------------------ producers
     const int q = warp & 3;       // TMEM lane quarter of this warp
-    const int hh = warp >> 2;     // k half [16 hh, 16 hh + 16) of the k-block
+    const int hh = warp >> 2;     // k-values [16 hh, 16 hh + 16) of the k-block
     const int m = q * 32 + lane;  // A row (TMEM lane) of this thread
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     int it = 0;
@@ -278,63 +292,61 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       int64_t r0;
       unit_range(u, blk, split, r0, nkb);
       for (int kb = 0; kb < nkb; ++kb, ++it) {
-        const int rs = it % RST;
-        const int as = it % OPST;
-        mbar_wait(&rfull[rs], (it / RST) & 1);
-        const uint32_t raw = smem_u32(sRaw) + rs * kRawSlot;
-        uint32_t hw[8], lw[8];
+        const int s = it % S;
+        // full[s] of this round implies free[s] of the previous round (the TMA waited on it), so
+        // TMEM A stage s is no longer read by the MMA
+        mbar_wait(&full[s], (it / S) & 1);
+        tc_fence_after();
+        const uint32_t raw = smem_u32(sRaw) + s * kRawSlot;
+        uint32_t hw[kWords], lw[kWords];
         if (kMode == 0) {
-          // ROW: U tile [128 rows][32] int16, 64-byte rows, TMA SWIZZLE_64B (16-byte chunk c of row
-          // r stored at chunk c ^ ((r >> 1) & 3)); this thread reads chunks 2 hh, 2 hh + 1 of row m
+          // ROW: U tile [128 rows][64] int16, 128-byte rows, TMA SWIZZLE_128B (16-byte chunk c of
+          // row r stored at chunk c ^ (r & 7)); this thread reads chunks 2 hh, 2 hh + 1 of row m
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int c = 2 * hh + h;
-            const uint4 w = lds128u(raw + m * 64 + ((c ^ ((m >> 1) & 3)) << 4));
+            const uint4 w = lds128u(raw + m * 128 + ((c ^ (m & 7)) << 4));
             const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (int t = 0; t < 4; ++t)
               split_q15((int)(int16_t)(ws[t] & 0xffffu), (int)(int16_t)(ws[t] >> 16), hw[h * 4 + t], lw[h * 4 + t]);
           }
         } else {
-          // COL: U tile [32 rows i][128 cols] int16 (256-byte rows); A row m = column m of R
+          // COL: U tile [64 rows i][128 cols] int16 (256-byte rows); A row m = column m of R
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
+          for (int t = 0; t < kWords; ++t) {
             const int i0 = hh * kColsPerThr + 2 * t;
             split_q15((int)(int16_t)lds_u16(raw + i0 * 256 + m * 2), (int)(int16_t)lds_u16(raw + (i0 + 1) * 256 + m * 2),
                       hw[t], lw[t]);
           }
         }
-        uint32_t cw[8];
+        uint32_t cw[kWords];
         if (kDual) {
-          // codes tile [128 rows][32] int8, 32-byte rows, TMA SWIZZLE_32B (chunk c ^ ((r >> 2) & 1))
-          const uint4 w = lds128u(raw + C::kOffCodes + m * 32 + ((hh ^ ((m >> 2) & 1)) << 4));
+          // codes tile [128 rows][64] int8, 64-byte rows, TMA SWIZZLE_64B (chunk c ^ ((r >> 1) & 3));
+          // this thread's 16 codes are chunk hh of row m
+          const uint4 w = lds128u(raw + C::kOffCodes + m * 64 + ((hh ^ ((m >> 1) & 3)) << 4));
           const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const uint32_t b = ws[t >> 1] >> (16 * (t & 1));
-            cw[t] = pack_bf16x2((float)(int8_t)(b & 0xffu), (float)(int8_t)((b >> 8) & 0xffu));
+          for (int t = 0; t < kWords; ++t) {
+            const uint32_t bb = ws[t >> 1] >> (16 * (t & 1));
+            cw[t] = pack_bf16x2((float)(int8_t)(bb & 0xffu), (float)(int8_t)((bb >> 8) & 0xffu));
           }
         }
-        mbar_wait(&aempty[as], ((it / OPST) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t tA = tA0 + as * C::kAStage + lane_off + hh * 8;
-        tmem_st8(tA, hw);
-        tmem_st8(tA + 16, lw);
-        if (kDual) tmem_st8(tA + 32, cw);
+        const uint32_t tA = tA0 + s * C::kAStage + lane_off + hh * kWords;
+        tmem_st(tA, hw);
+        tmem_st(tA + BK / 2, lw);
+        if (kDual) tmem_st(tA + BK, cw);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&afull[as]);
-          mbar_arrive(&rempty[rs]);  // U consumed (its values are in TMEM)
-        }
+        if (lane == 0) mbar_arrive(&afull[s]);
       }
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t id3 = idesc_bf16(3 * WN), id2 = idesc_bf16(2 * WN);
-      const uint64_t dB0 = desc_sw64(smem_u32(sRaw) + C::kOffB);
+      constexpr uint32_t id3 = idesc_bf16(3 * WN), id2 = idesc_bf16(2 * WN), idc = idesc_bf16(C::kCodesN);
+      const uint64_t dB0 = desc_sw128k(smem_u32(sRaw) + C::kOffB);
       int it = 0, lu = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
         int blk, split, nkb;
@@ -346,23 +358,21 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
         tc_fence_after();
         const uint32_t d1 = tmem + acc * C::kAccCols;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int rs = it % RST;
-          const int as = it % OPST;
-          mbar_wait(&afull[as], (it / OPST) & 1);
-          mbar_wait(&rfull[rs], (it / RST) & 1);  // B image landed
+          const int s = it % S;
+          mbar_wait(&afull[s], (it / S) & 1);
+          mbar_wait(&full[s], (it / S) & 1);  // B image landed (already true: producers saw it)
           tc_fence_after();
-          const uint64_t so = (uint64_t)((rs * kRawSlot) >> 4);
-          const uint32_t aS = tA0 + as * C::kAStage;
+          const uint64_t dB = dB0 + (uint64_t)((s * kRawSlot) >> 4);
+          const uint32_t aS = tA0 + s * C::kAStage;
 #pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const uint64_t dB = dB0 + so + ((k * 32) >> 4);  // 16 bf16 along K inside the 64-byte row
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t dBk = dB + (uint64_t)((k * 32) >> 4);  // 16 bf16 along K inside the 128-byte row
             const uint32_t acc0 = (kb | k) != 0 ? 1u : 0u;
-            umma_bf16_ts(d1, aS + k * 8, dB, id3, acc0);         // (256 h) x [b1 | b2 | b3]
-            umma_bf16_ts(d1, aS + 16 + k * 8, dB, id2, 1u);      // l x [b1 | b2]
-            if (kDual) umma_bf16_ts(d1 + 3 * WN, aS + 32 + k * 8, dB + (C::kImg >> 4), id3, acc0);  // codes x P2
+            umma_bf16_ts(d1, aS + k * 8, dBk, id3, acc0);          // (256 h) x [b1 | b2 | b3]
+            umma_bf16_ts(d1, aS + BK / 2 + k * 8, dBk, id2, 1u);   // l x [b1 | b2]
+            if (kDual) umma_bf16_ts(d1 + 3 * WN, aS + BK + k * 8, dBk + (C::kImg >> 4), idc, acc0);  // codes x P2
           }
-          umma_commit(&aempty[as]);
-          umma_commit(&rempty[rs]);
+          umma_commit(&freeb[s]);
         }
         umma_commit(&tfull[acc]);
       }
@@ -387,28 +397,54 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       if (kMode == 0) inv_row = orow < a.rows ? __ldg(a.inv_lam + orow) : 1.f;
       float* out1 = a.out1 + (int64_t)split * a.nout * a.W;
       float* out2 = kDual ? a.out2 + (int64_t)split * a.nout * a.W : nullptr;
-#pragma unroll 1
-      for (int h = 0; h < NA * (kDual ? 2 : 1); ++h) {
-        const bool second = kDual && h >= NA;
-        const int cbase = (second ? h - NA : h) * 32;
-        const uint32_t tg = trow + (second ? 3 * WN : 0) + cbase;
-        uint32_t v0[32], v1[32], v2[32];
+      constexpr int NG = NA * (kDual ? 2 : 1);  // 32-column output groups per row
+      // group g: columns [32 g', +32) of OUT1 (g < NA) or OUT2; the sum of its 3 (2) accumulator groups
+      auto load_group = [&](int g, float (&o)[32]) {
+        const bool second = kDual && g >= NA;
+        const int cb = (second ? g - NA : g) * 32;
+        const uint32_t tg = trow + (second ? 3 * WN : 0) + cb;
+        uint32_t v0[32], v1[32];
         tmem_ld_32x32b_x32(tg, v0);
         tmem_ld_32x32b_x32(tg + WN, v1);
-        tmem_ld_32x32b_x32(tg + 2 * WN, v2);
         tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) o[c] = __uint_as_float(v0[c]) + __uint_as_float(v1[c]);
+        if (!second || C::kCodesN == 3 * WN) {
+          tmem_ld_32x32b_x32(tg + 2 * WN, v0);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) o[c] += __uint_as_float(v0[c]);
+        }
+      };
+      auto store_group = [&](int g, const float (&o)[32]) {
+        const bool second = kDual && g >= NA;
+        const int cb = (second ? g - NA : g) * 32;
         const float sc = second ? inv_row : inv_row * (1.f / kUScale);
         if (orow < a.nout) {
-          float* o = (second ? out2 : out1) + orow * a.W;
+          float* op = (second ? out2 : out1) + orow * a.W;
 #pragma unroll
           for (int c = 0; c < 32; ++c)
-            if (cbase + c < a.W)
-              o[cbase + c] =
-                  __fmul_rn((__uint_as_float(v0[c]) + __uint_as_float(v1[c])) + __uint_as_float(v2[c]), sc);
+            if (cb + c < a.W) op[cb + c] = __fmul_rn(o[c], sc);
         }
+      };
+      if constexpr (C::kEarlyRelease) {
+        float o[NG][32];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) load_group(g, o[g]);
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);  // accumulator buffer free: the next unit's MMAs may start
+#pragma unroll
+        for (int g = 0; g < NG; ++g) store_group(g, o[g]);
+      } else {
+#pragma unroll 1
+        for (int g = 0; g < NG; ++g) {
+          float o[32];
+          load_group(g, o);
+          store_group(g, o);
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
     }
   }
   __syncthreads();
@@ -434,7 +470,7 @@ int64_t tc_img_bytes(int64_t n, int W) {
 template <int NA>
 static void prep_img(const float* P, int64_t n, int W, const float* scale, uint8_t* img, cudaStream_t st) {
   const int64_t nkb = (n + tcp::BK - 1) / tcp::BK;
-  const int64_t total = nkb * tcp::BK * (32 * NA);
+  const int64_t total = nkb * (tcp::BK / 8) * (32 * NA);
   const int g = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
   k_prep_img<NA><<<g, 256, 0, st>>>(P, n, W, scale, nkb, img);
   ++launch_counter();
@@ -484,11 +520,11 @@ static int run_tc(const SideView& s, const float* P1, const float* P2, int W, fl
   alignas(64) TcMaps maps;
   memset(&maps, 0, sizeof(maps));
   if (kMode == 0)
-    encode_map_2d_sw(&maps.u, 2, s.U, (uint64_t)s.K, (uint64_t)s.rows, (uint64_t)s.ldu * 2, BK, BM, 64);
+    encode_map_2d_sw(&maps.u, 2, s.U, (uint64_t)s.K, (uint64_t)s.rows, (uint64_t)s.ldu * 2, BK, BM, 128);
   else
     encode_map_2d_sw(&maps.u, 2, s.U, (uint64_t)s.K, (uint64_t)s.rows, (uint64_t)s.ldu * 2, BM, BK, 0);
   if (kDual)
-    encode_map_2d_sw(&maps.codes, 0, s.codes, (uint64_t)s.Kp, (uint64_t)s.rows, (uint64_t)s.Kp, BK, BM, 32);
+    encode_map_2d_sw(&maps.codes, 0, s.codes, (uint64_t)s.Kp, (uint64_t)s.rows, (uint64_t)s.Kp, BK, BM, 64);
   const int64_t units = nblk * ns;
   const int grid = (int)(units < nsm ? units : nsm);
   k_tc_proj<kMode, NA, kDual><<<grid, kThreads, C::kSmem, st>>>(maps, a);

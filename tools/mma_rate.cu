@@ -17,15 +17,18 @@ __device__ uint64_t desc_k(uint32_t addr) {  // K-major SW128, SBO 1024
   return d;
 }
 
-template <int V, int NACC>
+template <int V, int NACC, int ROT, int COMMIT>
 __global__ void rate(int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar;
+  __shared__ uint64_t cb[2];
   __shared__ uint32_t slot;
-  for (int i = threadIdx.x; i < 65536 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < 110000 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
+    mbar_init(&cb[0], 1);
+    mbar_init(&cb[1], 1);
     fence_mbar_init();
   }
   if (threadIdx.x < 32) tmem_alloc<512>(&slot);
@@ -47,21 +50,26 @@ __global__ void rate(int iters, unsigned long long* out) {
     for (int i = 0; i < iters; ++i) {
       const uint32_t acc = i > 0;
       const uint32_t tmd = tm + (uint32_t)((i % NACC) * 64);
+      const uint64_t dBv = dB + (uint64_t)(ROT ? ((i & 7) * 6144) >> 4 : 0);  // rotate B over 8 ring slots
       if (V == 0 || V == 7)
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
-                     ::"r"(tmd), "r"(ta), "l"(dB), "r"(id), "r"(acc) : "memory");
+                     ::"r"(tmd), "r"(ta), "l"(dBv), "r"(id), "r"(acc) : "memory");
       else if (V == 1)
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
-                     ::"r"(tmd), "l"(dA), "l"(dB), "r"(id), "r"(acc) : "memory");
+                     ::"r"(tmd), "l"(dA), "l"(dBv), "r"(id), "r"(acc) : "memory");
       else if (V == 2 || V == 3 || V == 4)
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
-                     ::"r"(tmd), "r"(ta), "l"(dB), "r"(id), "r"(acc) : "memory");
+                     ::"r"(tmd), "r"(ta), "l"(dBv), "r"(id), "r"(acc) : "memory");
       else if (V == 5)
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-                     ::"r"(tmd), "l"(dA), "l"(dB), "r"(id), "r"(acc) : "memory");
+                     ::"r"(tmd), "l"(dA), "l"(dBv), "r"(id), "r"(acc) : "memory");
       else
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
-                     ::"r"(tmd), "l"(dA), "l"(dB), "r"(idi8), "r"(acc) : "memory");
+                     ::"r"(tmd), "l"(dA), "l"(dBv), "r"(idi8), "r"(acc) : "memory");
+      if (COMMIT && (i & 3) == 3) {
+        umma_commit(&cb[0]);
+        umma_commit(&cb[1]);
+      }
     }
     umma_commit(&bar);
     mbar_wait(&bar, 0);
@@ -72,12 +80,12 @@ __global__ void rate(int iters, unsigned long long* out) {
   if (threadIdx.x < 32) tmem_free<512>(tm);
 }
 
-template <int V, int NACC = 1>
+template <int V, int NACC = 1, int ROT = 0, int COMMIT = 0>
 void run(const char* name, unsigned long long* d) {
-  cudaFuncSetAttribute(rate<V, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+  cudaFuncSetAttribute(rate<V, NACC, ROT, COMMIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120000);
   const int iters = 4096;
-  rate<V, NACC><<<148, 128, 70000>>>(iters, d);
-  rate<V, NACC><<<148, 128, 70000>>>(iters, d);
+  rate<V, NACC, ROT, COMMIT><<<148, 128, 120000>>>(iters, d);
+  rate<V, NACC, ROT, COMMIT><<<148, 128, 120000>>>(iters, d);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -103,5 +111,11 @@ int main() {
   run<2, 4>("bf16  A=tmem N=32 4 accumulators", d);
   run<5, 4>("bf16  A=smem N=32 4 accumulators", d);
   run<3, 4>("bf16  A=tmem N=96 4 accumulators", d);
+  run<3, 1, 1>("bf16  A=tmem N=96 B rotating", d);
+  run<2, 1, 1>("bf16  A=tmem N=32 B rotating", d);
+  run<4, 1, 1>("bf16  A=tmem N=160 B rotating", d);
+  run<5, 1, 1>("bf16  A=smem N=32 B rotating", d);
+  run<3, 1, 1, 1>("bf16  A=tmem N=96 rot + 2 commits/4", d);
+  run<2, 1, 1, 1>("bf16  A=tmem N=32 rot + 2 commits/4", d);
   return 0;
 }
