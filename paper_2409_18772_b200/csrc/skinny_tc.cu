@@ -27,14 +27,18 @@
 //     the MMA reads (rows [0,W') b1, [W',2W') b2, [2W',3W') b3); a bulk copy lands each
 //     k-block's image in the ring slot.
 //
-// Persistent, warp-specialised (704 threads, one CTA per SM):
+// Persistent, warp-specialised (736 threads, one CTA per SM):
 //   warps 0-15 : producers: raw U (smem) -> bf16 (256 h, l) in TMEM (+ codes -> bf16 for dual);
 //                warp w owns TMEM lane quarter w % 4 and k-values [16 (w / 4), +16) of each k-block
 //   warps 16-19: epilogue: TMEM accumulators -> registers (releases the buffer) -> split-K partials
 //   warp 20    : TMEM allocator + single-thread tcgen05.mma issuer
-//   warp 21    : TMA issuer: U tile, B image(s), codes tile
-// Slot s of the S-deep ring owns raw smem slot s AND TMEM A stage s: one MMA commit (free[s])
-// releases both; producers never wait on it (the TMA refill of slot s already did).
+//   warp 21    : TMA issuer: U (+ codes) tiles into the U ring
+//   warp 22    : bulk-copy issuer: B images into the B ring (its own thread, so that waiting for
+//                the MMA to free a B slot never stalls the U prefetch)
+// Two rings: the U ring (raw U [+ codes] tiles, RU deep) is released by the producer warps once
+// the values are in TMEM; the B ring (B images, SB deep) shares its index with the TMEM A stages
+// and is released by one MMA commit (free[s]).  So HBM prefetch depth does not depend on the MMA
+// completion latency.
 // Work unit = (128-row/col block, reduction split); partials are summed in a fixed order
 // by the consumer (deterministic, no float atomics).
 #include <cuda.h>
@@ -53,8 +57,9 @@ constexpr int BM = 128;  // output rows (ROW) / output cols (COL) per unit
 constexpr int BK = 64;   // reduction elements per k-block
 constexpr int kProdWarps = 16;
 constexpr int kMmaWarp = kProdWarps + 4;
-constexpr int kTmaWarp = kProdWarps + 5;
-constexpr int kThreads = (kProdWarps + 6) * 32;
+constexpr int kTmaWarp = kProdWarps + 5;   // U (+ codes) tiles
+constexpr int kBWarp = kProdWarps + 6;     // B images
+constexpr int kThreads = (kProdWarps + 7) * 32;
 constexpr int kColsPerThr = BK / (kProdWarps / 4);  // 16 k-values of A per producer thread
 constexpr int kWords = kColsPerThr / 2;             // 8 TMEM columns per A part per thread
 constexpr int kRawU = BM * BK * 2;                  // 16 KB raw U tile (Q15)
@@ -65,22 +70,24 @@ struct Cfg {
   static constexpr int kBRows = 3 * WN;           // b1 | b2 | b3
   static constexpr int kImg = kBRows * BK * 2;    // one k-block image: kBRows rows x 128 B
   static constexpr int kCodesN = NA == 1 ? 3 * WN : 2 * WN;  // codes x [b1|b2|b3] (x [b1|b2] at W' = 64)
-  // raw slot: U tile | B image | B2 image (dual) | codes (dual)
-  static constexpr int kOffB = kRawU;
-  static constexpr int kOffB2 = kOffB + kImg;
-  static constexpr int kOffCodes = kOffB + (kDual ? 2 : 1) * kImg;
-  static constexpr int kRawBytes = kOffCodes + (kDual ? kRawCodes : 0);
-  static constexpr int kRawSlot = (kRawBytes + 1023) / 1024 * 1024;
+  // U slot: U tile | codes (dual);  B slot: B image | B2 image (dual)
+  static constexpr int kOffCodes = kRawU;
+  static constexpr int kUBytes = kRawU + (kDual ? kRawCodes : 0);
+  static constexpr int kUSlot = (kUBytes + 1023) / 1024 * 1024;
+  static constexpr int kBBytes = (kDual ? 2 : 1) * kImg;
+  static constexpr int kBSlot = (kBBytes + 1023) / 1024 * 1024;
   // TMEM: accumulator buffer(s), then one A stage per ring slot: (256 h, l[, codes]) x 32 columns
   static constexpr int kAccCols = kBRows + (kDual ? kCodesN : 0);
   static constexpr int kAStage = (kDual ? 3 : 2) * (BK / 2);
   static constexpr int kAccBufs = (2 * kAccCols + 4 * kAStage <= 512) ? 2 : 1;
   static constexpr int kTmemS = (512 - kAccBufs * kAccCols) / kAStage;
-  static constexpr int kSmemS = (200 * 1024) / kRawSlot;
-  static constexpr int S0 = kTmemS < kSmemS ? kTmemS : kSmemS;
-  static constexpr int S = S0 > 6 ? 6 : S0;
-  static_assert(S >= 2, "ring depth");
-  static constexpr int kSmem = S * kRawSlot + 256 + 1024;
+  static constexpr int SB = kTmemS > 4 ? 4 : kTmemS;  // B ring = TMEM A stages
+  static_assert(SB >= 2, "B ring depth");
+  static constexpr int RU0 = (200 * 1024 - SB * kBSlot) / kUSlot;
+  static constexpr int RU = RU0 > 8 ? 8 : RU0;  // U ring
+  static_assert(RU >= 3, "U ring depth");
+  static constexpr int S = SB;
+  static constexpr int kSmem = RU * kUSlot + SB * kBSlot + 256 + 1024;
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
   static_assert(kAccBufs * kAccCols + S * kAStage <= 512, "TMEM budget");
   static constexpr int kOutCols = NA * 32 * (kDual ? 2 : 1);  // outputs per row
@@ -207,17 +214,20 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   using namespace tcp;
   using C = Cfg<kMode, NA, kDual>;
   constexpr int WN = C::WN;
-  constexpr int S = C::S;
+  constexpr int S = C::SB;
+  constexpr int RU = C::RU;
   constexpr int NACC = C::kAccBufs;
-  constexpr int kRawSlot = C::kRawSlot;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sRaw = smem;  // S raw slots (TMA)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sRaw + S * kRawSlot);
-  uint64_t* full = bars;           // S: TMA landed
-  uint64_t* afull = bars + S;      // S: A stage written (producer warps)
-  uint64_t* freeb = bars + 2 * S;  // S: MMA done with slot (raw smem + TMEM A stage)
-  uint64_t* tfull = bars + 3 * S;  // 2
+  uint8_t* sU = smem;                     // RU U slots (TMA)
+  uint8_t* sB = smem + RU * C::kUSlot;    // S B-image slots (bulk copies)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + S * C::kBSlot);
+  uint64_t* ufull = bars;               // RU: U tile landed
+  uint64_t* uempty = bars + RU;         // RU: U slot consumed (producer warps)
+  uint64_t* full = bars + 2 * RU;       // S: B image landed
+  uint64_t* afull = full + S;           // S: A stage written (producer warps)
+  uint64_t* freeb = full + 2 * S;       // S: MMA done with B slot + TMEM A stage
+  uint64_t* tfull = full + 3 * S;       // 2
   uint64_t* tempty = tfull + 2;    // 2
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -226,6 +236,10 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   const int nunits = a.nblk * a.nsplit;
 
   if (tid == 0) {
+    for (int s = 0; s < RU; ++s) {
+      mbar_init(&ufull[s], 1);
+      mbar_init(&uempty[s], kProdWarps);
+    }
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&afull[s], kProdWarps);
@@ -263,19 +277,34 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
         int64_t r0;
         unit_range(u, blk, split, r0, nkb);
         for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % S;
-          mbar_wait(&freeb[s], ((it / S) & 1) ^ 1);
-          uint8_t* slot = sRaw + s * kRawSlot;
-          mbar_arrive_expect_tx(&full[s], C::kRawBytes);
+          const int su = it % RU;
           const int k0 = (int)(r0 + (int64_t)kb * BK);
-          if (kMode == 0) tma_load_2d(slot, &maps.u, &full[s], k0, blk * BM);
-          else tma_load_2d(slot, &maps.u, &full[s], blk * BM, k0);
-          const int64_t g = k0 / BK;
-          bulk_load(slot + C::kOffB, a.img1 + g * C::kImg, C::kImg, &full[s]);
-          if (kDual) {
-            bulk_load(slot + C::kOffB2, a.img2 + g * C::kImg, C::kImg, &full[s]);
-            tma_load_2d(slot + C::kOffCodes, &maps.codes, &full[s], k0, blk * BM);
-          }
+          mbar_wait(&uempty[su], ((it / RU) & 1) ^ 1);
+          uint8_t* us = sU + su * C::kUSlot;
+          mbar_arrive_expect_tx(&ufull[su], C::kUBytes);
+          if (kMode == 0) tma_load_2d(us, &maps.u, &ufull[su], k0, blk * BM);
+          else tma_load_2d(us, &maps.u, &ufull[su], blk * BM, k0);
+          if (kDual) tma_load_2d(us + C::kOffCodes, &maps.codes, &ufull[su], k0, blk * BM);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kBWarp) {
+    // ------------------------------------------------ bulk copies: B images
+    if (lane == 0) {
+      int it = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        int blk, split, nkb;
+        int64_t r0;
+        unit_range(u, blk, split, r0, nkb);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % S;
+          const int64_t g = (r0 + (int64_t)kb * BK) / BK;
+          mbar_wait(&freeb[s], ((it / S) & 1) ^ 1);
+          uint8_t* bs = sB + s * C::kBSlot;
+          mbar_arrive_expect_tx(&full[s], C::kBBytes);
+          bulk_load(bs, a.img1 + g * C::kImg, C::kImg, &full[s]);
+          if (kDual) bulk_load(bs + C::kImg, a.img2 + g * C::kImg, C::kImg, &full[s]);
         }
       }
     }
@@ -292,12 +321,10 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       int64_t r0;
       unit_range(u, blk, split, r0, nkb);
       for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int su = it % RU;
         const int s = it % S;
-        // full[s] of this round implies free[s] of the previous round (the TMA waited on it), so
-        // TMEM A stage s is no longer read by the MMA
-        mbar_wait(&full[s], (it / S) & 1);
-        tc_fence_after();
-        const uint32_t raw = smem_u32(sRaw) + s * kRawSlot;
+        mbar_wait(&ufull[su], (it / RU) & 1);
+        const uint32_t raw = smem_u32(sU) + su * C::kUSlot;
         uint32_t hw[kWords], lw[kWords];
         if (kMode == 0) {
           // ROW: U tile [128 rows][64] int16, 128-byte rows, TMA SWIZZLE_128B (16-byte chunk c of
@@ -332,21 +359,28 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
             cw[t] = pack_bf16x2((float)(int8_t)(bb & 0xffu), (float)(int8_t)((bb >> 8) & 0xffu));
           }
         }
+        // full[s] of this round implies free[s] of the previous round (the TMA waited on it before
+        // refilling B slot s), so TMEM A stage s is no longer read by the MMA
+        mbar_wait(&full[s], (it / S) & 1);
+        tc_fence_after();
         const uint32_t tA = tA0 + s * C::kAStage + lane_off + hh * kWords;
         tmem_st(tA, hw);
         tmem_st(tA + BK / 2, lw);
         if (kDual) tmem_st(tA + BK, cw);
-        tmem_st_wait();
+        tmem_st_wait();  // the U values are consumed: the TMA may refill the U slot
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&afull[s]);
+        if (lane == 0) {
+          mbar_arrive(&afull[s]);
+          mbar_arrive(&uempty[su]);
+        }
       }
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t id3 = idesc_bf16(3 * WN), id2 = idesc_bf16(2 * WN), idc = idesc_bf16(C::kCodesN);
-      const uint64_t dB0 = desc_sw128k(smem_u32(sRaw) + C::kOffB);
+      const uint64_t dB0 = desc_sw128k(smem_u32(sB));
       int it = 0, lu = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
         int blk, split, nkb;
@@ -362,7 +396,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
           mbar_wait(&afull[s], (it / S) & 1);
           mbar_wait(&full[s], (it / S) & 1);  // B image landed (already true: producers saw it)
           tc_fence_after();
-          const uint64_t dB = dB0 + (uint64_t)((s * kRawSlot) >> 4);
+          const uint64_t dB = dB0 + (uint64_t)((s * C::kBSlot) >> 4);
           const uint32_t aS = tA0 + s * C::kAStage;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
