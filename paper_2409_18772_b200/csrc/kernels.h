@@ -24,8 +24,10 @@ struct QuantArgs {
   float* inv_lam;         // rows: RN(1/lambda) (written unless lam_fixed)
   const float* lam_fixed; // device scalar (per-tensor mode) or nullptr
   int* err_flag;          // bit 0: non-finite input
-  int16_t* U;             // rows x ldu residual fraction u = lambda x - code, Q15 fixed point (or nullptr)
-  int64_t ldu;            // multiple of 8, >= K
+  uint8_t* U;             // residual fraction u = lambda x - code as Q15 i = RN(2^15 u) = 256 h + l in two
+                          // byte planes: h (int8) at U, l (uint8) at U + uplane; rows x ldu each (or nullptr)
+  int64_t ldu;            // multiple of 16, >= K
+  int64_t uplane;         // bytes between the h and l planes
 };
 void launch_quantize(const QuantArgs& a, cudaStream_t st);
 void launch_tensor_scale(const float* X, int64_t ldx, int64_t rows, int K, int qmax, float* row_amax,
@@ -34,12 +36,14 @@ void launch_tensor_scale(const float* X, int64_t ldx, int64_t rows, int K, int q
 // ------------------------------------------------- K2/K3 skinny residual products
 // The passes stream the residual fraction u = lambda x - code written by K1 (R = u / lambda,
 // Alg. 2) and, for the cross products, the codes (X~ = code / lambda, line 352).
-// u is stored as int16 Q15: u16 = clamp(RN(u * 2^15), +-32767) (|u| < 1 for every rounding mode;
-// |u16 / 2^15 - u| <= 2^-16, 2^-15 where u rounds past the clamp).  Half the bytes of fp32 on the three RSVD passes that stream it
-// (reading #28); u16 / 2^15 is exact in fp32 and splits exactly into tf32 hi + lo.
+// u is stored as Q15: i = clamp(RN(u * 2^15), +-32767) (|u| < 1 for every rounding mode;
+// |i / 2^15 - u| <= 2^-16, 2^-15 where u rounds past the clamp), split into the bytes
+// i = 256 h + l (h = i >> 8 signed, l = i & 255 unsigned) stored as two planes, so the RSVD
+// passes feed them to kind::i8 MMAs straight from TMA (reading #28).  2 B per element.
 constexpr float kUScale = 32768.f;
 struct SideView {
-  const int16_t* U;      // rows x ldu, u in Q15 fixed point (kUScale)
+  const uint8_t* Uh;     // rows x ldu int8 (h)
+  const uint8_t* Ul;     // rows x ldu uint8 (l)
   int64_t ldu;
   int64_t rows;
   int K;
@@ -51,7 +55,7 @@ struct SideView {
 // tcgen05 kind::tf32 (3-term split) passes, deterministic split-K partials; return the split count.
 // With reduce1 == false and > 1 splits, OUT1 stays as partials at `partial` (consumed by the fused
 // Gram kernel).  ROW: OUT1 = R P1 (rows x W); dual (P2 != null): OUT2 = X~ P2.  P is K x W (ld W).
-// img: scratch for the pre-split B operand images, >= 2 * tc_img_bytes(max(rows, K), W) bytes.
+// img: scratch for the B operand images + column scales, >= 2 * tc_img_bytes(max(rows, K), W) bytes.
 int launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
                         float* partial, int64_t partial_elems, bool reduce1, uint8_t* img, cudaStream_t st);
 // COL: OUT = R^T P; P is rows x W, OUT is K x W.

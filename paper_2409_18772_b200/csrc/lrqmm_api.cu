@@ -23,7 +23,7 @@ constexpr int kMaxWidth = 64;
 struct Side {
   int64_t rows = 0;
   int64_t ldu = 0;
-  int16_t* U = nullptr;      // rows x ldu residual fraction u = lambda x - code, Q15 (written by K1)
+  uint8_t* U = nullptr;      // residual fraction u = lambda x - code, Q15 as h | l byte planes (written by K1)
   uint8_t* img = nullptr;    // pre-split tf32 B operand images of the passes (skinny_tc.cu)
   int8_t* codes = nullptr;   // rows x Kp
   float* lam = nullptr;      // rows
@@ -207,8 +207,8 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
     ok = ok && dalloc(&s.codes, s.rows * h->Kp) && dalloc(&s.lam, s.rows) && dalloc(&s.inv_lam, s.rows) && dalloc(&s.row_amax, s.rows) &&
          dalloc(&s.lam_scalar, 1);
     if (h->W > 0) {
-      s.ldu = (K + 7) / 8 * 8;
-      ok = ok && dalloc(&s.U, s.rows * s.ldu) && dalloc(&s.Om, K * h->W) && dalloc(&s.Y, s.rows * h->W) && dalloc(&s.Q0, s.rows * h->W) &&
+      s.ldu = h->Kp;
+      ok = ok && dalloc(&s.U, 2 * s.rows * s.ldu) && dalloc(&s.Om, K * h->W) && dalloc(&s.Y, s.rows * h->W) && dalloc(&s.Q0, s.rows * h->W) &&
            dalloc(&s.Z, K * h->W) && dalloc(&s.Q1, K * h->W) && dalloc(&s.Gp, s.rows * h->W) &&
            dalloc(&s.G, (int64_t)h->W * h->W) && dalloc(&s.gpart, (int64_t)kGramMaxBlocks * h->W * h->W) &&
            dalloc(&s.counter, 1) && dalloc(&s.T64, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W) &&
@@ -294,6 +294,7 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
   a.err_flag = h->err_flag;
   a.U = s.U;  // residual fractions for the RSVD passes (rank > 0 only)
   a.ldu = s.ldu;
+  a.uplane = s.rows * s.ldu;
   if (s.rows > 0) launch_quantize(a, h->st);
   record(h, side == LRQMM_SIDE_A ? 1 : 3);
   lrqmm_status_t e = check_launch(h);
@@ -305,7 +306,8 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
 
 static SideView view(lrqmm_handle_t h, int sd) {
   SideView v;
-  v.U = h->s[sd].U;
+  v.Uh = h->s[sd].U;
+  v.Ul = h->s[sd].U ? h->s[sd].U + h->s[sd].rows * h->s[sd].ldu : nullptr;
   v.ldu = h->s[sd].ldu;
   v.rows = h->s[sd].rows;
   v.K = (int)h->cfg.k;
@@ -599,14 +601,14 @@ extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx
                                            float* OUT2, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int Kp = (int)roundup(K > 0 ? K : 1, 128);
-  const int64_t ldu = ((int64_t)K + 7) / 8 * 8;
+  const int64_t ldu = Kp;
   const int64_t pe = (int64_t)16 << 20;
-  int16_t* U = nullptr;
+  uint8_t* U = nullptr;
   uint8_t* img = nullptr;
   float *lam = nullptr, *inv = nullptr, *partial = nullptr;
   int8_t* codes = nullptr;
   int* flag = nullptr;
-  bool ok = cudaMalloc(&U, sizeof(int16_t) * rows * ldu) == cudaSuccess &&
+  bool ok = cudaMalloc(&U, 2 * rows * ldu) == cudaSuccess &&
             cudaMalloc(&lam, sizeof(float) * rows) == cudaSuccess && cudaMalloc(&inv, sizeof(float) * rows) == cudaSuccess &&
             cudaMalloc(&codes, (size_t)rows * Kp) == cudaSuccess && cudaMalloc(&flag, sizeof(int)) == cudaSuccess &&
             cudaMalloc(&partial, sizeof(float) * pe) == cudaSuccess &&
@@ -616,9 +618,9 @@ extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx
     cudaMemsetAsync(flag, 0, sizeof(int), st);
     QuantArgs q{};
     q.X = X; q.ldx = ldx; q.rows = rows; q.K = K; q.Kp = Kp; q.qmax = (1 << (bits - 1)) - 1; q.mode = rounding;
-    q.codes = codes; q.lam = lam; q.inv_lam = inv; q.lam_fixed = nullptr; q.err_flag = flag; q.U = U; q.ldu = ldu;
+    q.codes = codes; q.lam = lam; q.inv_lam = inv; q.lam_fixed = nullptr; q.err_flag = flag; q.U = U; q.ldu = ldu; q.uplane = rows * ldu;
     launch_quantize(q, st);
-    SideView v{U, ldu, rows, K, codes, Kp, lam, inv};
+    SideView v{U, U + rows * ldu, ldu, rows, K, codes, Kp, lam, inv};
     if (mode == 0) launch_tc_proj_rows(v, P, OUT, nullptr, nullptr, W, partial, pe, true, img, st);
     else if (mode == 1) launch_tc_proj_cols(v, P, OUT, W, partial, pe, true, img, st);
     else launch_tc_proj_rows(v, P, OUT, P2, OUT2, W, partial, pe, true, img, st);

@@ -54,7 +54,9 @@ LRQMM_DEV int u_fix(float u) {
   const int q = __float2int_rn(u * kUScale);
   return q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
 }
-LRQMM_DEV uint32_t pack_u16(int a, int b) { return ((uint32_t)a & 0xffffu) | ((uint32_t)b << 16); }
+LRQMM_DEV uint32_t pack_bytes(int a, int b, int c, int d) {
+  return ((uint32_t)a & 0xffu) | (((uint32_t)b & 0xffu) << 8) | (((uint32_t)c & 0xffu) << 16) | ((uint32_t)d << 24);
+}
 
 // TPR threads cooperate on one row; each holds VPT float4 of it.  Row length
 // covered: TPR*VPT*4 >= Kp.  kFixedLam: lambda given (per-tensor mode), no amax.
@@ -63,7 +65,7 @@ __global__ void __launch_bounds__(256) k1_quantize(const float* __restrict__ X, 
                                                    int qmax, int mode, int8_t* __restrict__ codes,
                                                    float* __restrict__ lam_out, float* __restrict__ inv_out,
                                                    const float* __restrict__ lam_in, int* __restrict__ err_flag,
-                                                   int16_t* __restrict__ U, int64_t ldu) {
+                                                   uint8_t* __restrict__ U, int64_t ldu, int64_t uplane) {
   constexpr int kRowsPerCta = 256 / TPR;
   constexpr int kWarpsPerRow = TPR / 32;
   __shared__ float red[8];
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(256) k1_quantize(const float* __restrict__ X, 
         inv_out[row] = __frcp_rn(lam);
       }
       uint32_t* crow = reinterpret_cast<uint32_t*>(codes + row * (int64_t)Kp);
-      int16_t* urow = U ? U + row * ldu : nullptr;
+      uint8_t* urow = U ? U + row * ldu : nullptr;
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
         const int col = (sub + i * TPR) * 4;
@@ -130,9 +132,10 @@ __global__ void __launch_bounds__(256) k1_quantize(const float* __restrict__ X, 
           crow[col >> 2] = pack4(c0, c1, c2, c3);
           // residual fraction u = lambda x - code (R = u / lambda, Alg. 2), exactly rounded
           if (urow && col < ldu) {
-            const uint32_t u01 = pack_u16(u_fix(__fmaf_rn(lam, v[i].x, -(float)c0)), u_fix(__fmaf_rn(lam, v[i].y, -(float)c1)));
-            const uint32_t u23 = pack_u16(u_fix(__fmaf_rn(lam, v[i].z, -(float)c2)), u_fix(__fmaf_rn(lam, v[i].w, -(float)c3)));
-            __stcg(reinterpret_cast<uint2*>(urow + col), make_uint2(u01, u23));
+            const int i0 = u_fix(__fmaf_rn(lam, v[i].x, -(float)c0)), i1 = u_fix(__fmaf_rn(lam, v[i].y, -(float)c1));
+            const int i2 = u_fix(__fmaf_rn(lam, v[i].z, -(float)c2)), i3 = u_fix(__fmaf_rn(lam, v[i].w, -(float)c3));
+            __stcg(reinterpret_cast<uint32_t*>(urow + col), pack_bytes(i0 >> 8, i1 >> 8, i2 >> 8, i3 >> 8));
+            __stcg(reinterpret_cast<uint32_t*>(urow + uplane + col), pack_bytes(i0, i1, i2, i3));
           }
         }
       }
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(256) k1_quantize_long(const float* __restrict_
                                                         int Kp, int qmax, int mode, int8_t* __restrict__ codes,
                                                         float* __restrict__ lam_out, float* __restrict__ inv_out,
                                                         const float* __restrict__ lam_in, int* __restrict__ err_flag,
-                                                        int16_t* __restrict__ U, int64_t ldu) {
+                                                        uint8_t* __restrict__ U, int64_t ldu, int64_t uplane) {
   __shared__ float red[8];
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
     const float* xr = X + row * ldx;
@@ -230,7 +233,11 @@ __global__ void __launch_bounds__(256) k1_quantize_long(const float* __restrict_
       const float x = c < K ? xr[c] : 0.f;
       const int8_t q = code_of(lam, x, mode, qmax);
       crow[c] = q;
-      if (U && c < ldu) U[row * ldu + c] = (int16_t)u_fix(__fmaf_rn(lam, x, -(float)q));
+      if (U && c < ldu) {
+        const int iu = u_fix(__fmaf_rn(lam, x, -(float)q));
+        U[row * ldu + c] = (uint8_t)(iu >> 8);
+        U[uplane + row * ldu + c] = (uint8_t)(iu & 255);
+      }
     }
   }
 }
@@ -243,7 +250,7 @@ static void launch_k1_t(const QuantArgs& a, bool vec, bool fixed, cudaStream_t s
   if (grid < 1) grid = 1;
 #define K1_LAUNCH(V, F)                                                                                  \
   k1_quantize<TPR, VPT, V, F><<<grid, 256, 0, st>>>(a.X, a.ldx, a.rows, a.K, a.Kp, a.qmax, a.mode, a.codes, \
-                                                    a.lam, a.inv_lam, a.lam_fixed, a.err_flag, a.U, a.ldu)
+                                                    a.lam, a.inv_lam, a.lam_fixed, a.err_flag, a.U, a.ldu, a.uplane)
   if (vec) {
     if (fixed) K1_LAUNCH(true, true); else K1_LAUNCH(true, false);
   } else {
@@ -270,7 +277,7 @@ void launch_quantize(const QuantArgs& a, cudaStream_t st) {
   else {
     int grid = a.rows < 148 * 16 ? (int)a.rows : 148 * 16;
     k1_quantize_long<<<grid, 256, 0, st>>>(a.X, a.ldx, a.rows, a.K, a.Kp, a.qmax, a.mode, a.codes, a.lam,
-                                           a.inv_lam, a.lam_fixed, a.err_flag, a.U, a.ldu); ++launch_counter();
+                                           a.inv_lam, a.lam_fixed, a.err_flag, a.U, a.ldu, a.uplane); ++launch_counter();
   }
 }
 
