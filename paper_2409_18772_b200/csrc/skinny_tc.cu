@@ -27,6 +27,7 @@
 //   warps 2-5 : epilogue: TMEM accumulators -> registers (buffer released) -> split-K partials
 // Work unit = (128-row/col block, reduction split); partials are summed in a fixed order by the
 // consumer (deterministic, no float atomics).
+#include <cooperative_groups.h>
 #include <cuda.h>
 
 #include <cstring>
@@ -109,70 +110,141 @@ __host__ __device__ inline uint32_t off_k128(int n, int k) {
   return (uint32_t)((n >> 3) * 1024 + (n & 7) * 128 + ((((k >> 4) ^ (n & 7)) & 7) << 4) + (k & 15));
 }
 
-// per-column max |P_jc * scale_j| (as float bits; non-negative floats order like unsigned ints)
-__global__ void __launch_bounds__(256) k_colmax(const float* __restrict__ P, int64_t n, int W,
-                                                const float* __restrict__ scale, unsigned* __restrict__ colmax) {
-  __shared__ unsigned sm[64];
-  if (threadIdx.x < 64) sm[threadIdx.x] = 0u;
-  __syncthreads();
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * W; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e / W;
-    const float v = fabsf(scale ? P[e] * scale[j] : P[e]);
-    atomicMax(&sm[e % W], __float_as_uint(v));
-  }
-  __syncthreads();
-  if (threadIdx.x < W && sm[threadIdx.x]) atomicMax(&colmax[threadIdx.x], sm[threadIdx.x]);
-}
-
 // s_c = 2^e with max_j |P_jc| s_c in [32, 64) (1 for a zero column)
 LRQMM_DEV float col_scale(unsigned cmax_bits) {
-  const float m = __uint_as_float(cmax_bits);
-  if (!(m > 0.f)) return 1.f;
-  int ex;
-  frexpf(m, &ex);  // m = f 2^ex, f in [0.5, 1)
-  return ldexpf(1.f, 6 - ex);
+  // m = f 2^(E - 126) with f in [0.5, 1) for biased exponent E: s = 2^(6 - (E - 126)) = 2^(132 - E)
+  const int E = (int)((cmax_bits >> 23) & 0xffu);
+  if (E == 0) return 1.f;  // zero (or subnormal) column
+  int e = 259 - E;          // biased exponent of s
+  e = e > 254 ? 254 : e;
+  return __uint_as_float((unsigned)e << 23);
 }
 
-// B image: for every k-block g of P (n x W, ld W), optionally row-scaled, the int8 pieces
-// p1 | p2 | p3 of s_c P[128 g : 128 g + 128, c] in the K-major SWIZZLE_128B layout above (rows
-// [0,W') p1, [W',2W') p2, [2W',3W') p3); rows >= n and columns >= W are zero.  Also writes
-// cinv[c] = 1 / s_c.  One thread per (column, 16 consecutive k): three 16-byte stores.
+struct PrepJob {
+  const float* P;       // n x W, ld W
+  const float* scale;   // per-row scale (COL: 1/lambda) or nullptr
+  uint8_t* img;         // nkb images
+  unsigned* colmax;     // 64 (scratch)
+  float* cinv;          // 64: 1 / s_c
+};
+struct PrepJobs {
+  PrepJob j[2];
+  int njobs;
+  int64_t n, nkb;
+  int W;
+};
+
+// B images (one cooperative launch for the one or two operands of a pass):
+//   phase 1  colmax_c = max_j |P_jc scale_j| (float bits: non-negative floats order like uints)
+//   phase 2  for every k-block g, the int8 pieces p1 | p2 | p3 of s_c P[128 g : 128 g + 128, c]
+//            in the K-major SWIZZLE_128B layout above (rows [0,W') p1, [W',2W') p2, [2W',3W') p3),
+//            rows >= n and columns >= W zero; cinv_c = 1 / s_c.
+// One thread per (column, 16 consecutive k) in phase 2: three 16-byte stores.
+#ifdef LRQMM_PREP_TIMING
+__device__ unsigned long long g_prep_t[8];
+LRQMM_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PREP_T(i) if (blockIdx.x == 0 && threadIdx.x == 0) g_prep_t[i] = gtime();
+#else
+#define PREP_T(i)
+#endif
 template <int NA>
-__global__ void __launch_bounds__(256) k_prep_img(const float* __restrict__ P, int64_t n, int W,
-                                                  const float* __restrict__ scale, int64_t nkb,
-                                                  const unsigned* __restrict__ colmax, uint8_t* __restrict__ img,
-                                                  float* __restrict__ cinv) {
+__global__ void __launch_bounds__(256) k_prep_img(PrepJobs jb) {
+  PREP_T(0)
+  namespace cg = cooperative_groups;
   constexpr int WN = 32 * NA;
   constexpr int kImg = 3 * WN * tcp::BK;
   constexpr int kChunks = tcp::BK / 16;
-  if (blockIdx.x == 0 && threadIdx.x < WN)
-    cinv[threadIdx.x] = threadIdx.x < W ? 1.f / col_scale(colmax[threadIdx.x]) : 0.f;
-  const int64_t total = nkb * kChunks * WN;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e % WN);  // consecutive threads: consecutive columns (coalesced reads)
-    const int64_t rest = e / WN;
-    const int ch = (int)(rest % kChunks);
-    const int64_t g = rest / kChunks;
-    const float sc = c < W ? col_scale(colmax[c]) : 1.f;
-    uint32_t w1[4] = {0, 0, 0, 0}, w2[4] = {0, 0, 0, 0}, w3[4] = {0, 0, 0, 0};
+  __shared__ unsigned sm[2][64];
+  const int W = jb.W;
+  const int64_t n = jb.n;
+  if (threadIdx.x < 128) sm[threadIdx.x >> 6][threadIdx.x & 63] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x < 128 && (int)(threadIdx.x >> 6) < jb.njobs)
+    jb.j[threadIdx.x >> 6].colmax[threadIdx.x & 63] = 0u;
+  PREP_T(1)
+  cg::this_grid().sync();
+  PREP_T(2)
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  {
+    // thread = (row lane, column c): a running max in a register, one shared atomic at the end
+    constexpr int kRowsPerBlk = 256 / WN;
+    const int c = threadIdx.x % WN;
+    const int64_t rstride = (int64_t)gridDim.x * kRowsPerBlk;
+    for (int q = 0; q < jb.njobs; ++q) {
+      const PrepJob& J = jb.j[q];
+      float m = 0.f;
+      if (c < W) {
+        int64_t j = (int64_t)blockIdx.x * kRowsPerBlk + threadIdx.x / WN;
+        for (; j + 3 * rstride < n; j += 4 * rstride) {  // 4 independent loads in flight
+          float v[4];
 #pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const int64_t j = g * tcp::BK + ch * 16 + t;
-      const float v = (j < n && c < W) ? (scale ? P[j * W + c] * scale[j] : P[j * W + c]) * sc : 0.f;
-      const float p1 = rintf(v);
-      const float r1 = (v - p1) * 128.f;  // exact: |v| < 64, power-of-two scaling
-      const float p2 = rintf(r1);
-      const float p3 = rintf((r1 - p2) * 128.f);
-      const int sh = 8 * (t & 3);
-      w1[t >> 2] |= ((uint32_t)(int)p1 & 0xffu) << sh;
-      w2[t >> 2] |= ((uint32_t)(int)p2 & 0xffu) << sh;
-      w3[t >> 2] |= ((uint32_t)(int)p3 & 0xffu) << sh;
+          for (int t = 0; t < 4; ++t) {
+            const int64_t jj = j + t * rstride;
+            v[t] = fabsf(J.scale ? J.P[jj * W + c] * J.scale[jj] : J.P[jj * W + c]);
+          }
+          m = fmaxf(m, fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])));
+        }
+        for (; j < n; j += rstride) m = fmaxf(m, fabsf(J.scale ? J.P[j * W + c] * J.scale[j] : J.P[j * W + c]));
+      }
+      if (m > 0.f) atomicMax(&sm[q][c], __float_as_uint(m));
     }
-    uint8_t* base = img + g * kImg;
-    *reinterpret_cast<uint4*>(base + off_k128(c, ch * 16)) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
-    *reinterpret_cast<uint4*>(base + off_k128(WN + c, ch * 16)) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
-    *reinterpret_cast<uint4*>(base + off_k128(2 * WN + c, ch * 16)) = make_uint4(w3[0], w3[1], w3[2], w3[3]);
   }
+  __syncthreads();
+  if (threadIdx.x < 128) {
+    const int q = threadIdx.x >> 6, c = threadIdx.x & 63;
+    if (q < jb.njobs && c < W && sm[q][c]) atomicMax(&jb.j[q].colmax[c], sm[q][c]);
+  }
+  PREP_T(3)
+  cg::this_grid().sync();
+  PREP_T(4)
+  for (int q = 0; q < jb.njobs; ++q) {
+    const PrepJob& J = jb.j[q];
+    if (blockIdx.x == 0 && threadIdx.x < WN)
+      J.cinv[threadIdx.x] = (int)threadIdx.x < W ? 1.f / col_scale(J.colmax[threadIdx.x]) : 0.f;
+    const int64_t total = jb.nkb * kChunks * WN;
+    for (int64_t e = t0; e < total; e += gstride) {
+      const int c = (int)(e % WN);  // consecutive threads: consecutive columns (coalesced reads)
+      const int64_t rest = e / WN;
+      const int ch = (int)(rest % kChunks);
+      const int64_t g = rest / kChunks;
+      const bool cok = c < W;
+      const float sc = cok ? col_scale(J.colmax[c]) : 0.f;  // 0 zeroes columns >= W
+      const bool hs = J.scale != nullptr;
+      const float* sp = hs ? J.scale : J.P;
+      // unconditional (clamped) loads so that all 16 are in flight together
+      float x[16], y[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        int64_t j = g * tcp::BK + ch * 16 + t;
+        j = j < n ? j : n - 1;
+        x[t] = __ldg(J.P + j * W + (cok ? c : 0));
+        y[t] = __ldg(sp + (hs ? j : 0));
+      }
+      uint32_t w1[4] = {0, 0, 0, 0}, w2[4] = {0, 0, 0, 0}, w3[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int64_t j = g * tcp::BK + ch * 16 + t;
+        const float v = j < n ? (hs ? x[t] * y[t] : x[t]) * sc : 0.f;
+        const float p1 = rintf(v);
+        const float r1 = (v - p1) * 128.f;  // exact: |v| < 64, power-of-two scaling
+        const float p2 = rintf(r1);
+        const float p3 = rintf((r1 - p2) * 128.f);
+        const int sh = 8 * (t & 3);
+        w1[t >> 2] |= ((uint32_t)(int)p1 & 0xffu) << sh;
+        w2[t >> 2] |= ((uint32_t)(int)p2 & 0xffu) << sh;
+        w3[t >> 2] |= ((uint32_t)(int)p3 & 0xffu) << sh;
+      }
+      uint8_t* base = J.img + g * kImg;
+      *reinterpret_cast<uint4*>(base + off_k128(c, ch * 16)) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+      *reinterpret_cast<uint4*>(base + off_k128(WN + c, ch * 16)) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+      *reinterpret_cast<uint4*>(base + off_k128(2 * WN + c, ch * 16)) = make_uint4(w3[0], w3[1], w3[2], w3[3]);
+    }
+  }
+  PREP_T(5)
 }
 
 template <int kMode, int NA, bool kDual>
@@ -401,21 +473,34 @@ int64_t tc_img_bytes(int64_t n, int W) {
 }
 
 template <int NA>
-static void prep_img(const float* P, int64_t n, int W, const float* scale, uint8_t* img, float** cinv_out,
-                     cudaStream_t st) {
+static void prep_imgs(const float* P1, const float* P2, int64_t n, int W, const float* scale1, uint8_t* img1,
+                      uint8_t* img2, float** cinv1, float** cinv2, cudaStream_t st) {
   const int64_t nkb = (n + tcp::BK - 1) / tcp::BK;
-  uint8_t* tailp = img + nkb * (3 * 32 * NA * tcp::BK);
-  unsigned* colmax = reinterpret_cast<unsigned*>(tailp);
-  float* cinv = reinterpret_cast<float*>(tailp + 256);
-  cudaMemsetAsync(colmax, 0, 256, st);
-  const int64_t ne = n * W;
-  const int gm = (int)((ne + 255) / 256 < 1024 ? (ne + 255) / 256 : 1024);
-  k_colmax<<<gm > 0 ? gm : 1, 256, 0, st>>>(P, n, W, scale, colmax);
-  const int64_t total = nkb * (tcp::BK / 16) * (32 * NA);
-  const int g = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
-  k_prep_img<NA><<<g > 0 ? g : 1, 256, 0, st>>>(P, n, W, scale, nkb, colmax, img, cinv);
-  launch_counter() += 2;
-  *cinv_out = cinv;
+  PrepJobs jb{};
+  jb.n = n;
+  jb.nkb = nkb;
+  jb.W = W;
+  jb.njobs = P2 ? 2 : 1;
+  const float* Ps[2] = {P1, P2};
+  uint8_t* imgs[2] = {img1, img2};
+  for (int q = 0; q < jb.njobs; ++q) {
+    uint8_t* tailp = imgs[q] + nkb * (3 * 32 * NA * tcp::BK);
+    jb.j[q] = PrepJob{Ps[q], q == 0 ? scale1 : nullptr, imgs[q], reinterpret_cast<unsigned*>(tailp),
+                      reinterpret_cast<float*>(tailp + 256)};
+  }
+  *cinv1 = jb.j[0].cinv;
+  *cinv2 = jb.j[jb.njobs - 1].cinv;
+  static int grid = 0;
+  if (!grid) {
+    int dev = 0, nsm = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_prep_img<NA>, 256, 0);
+    grid = nsm * (per < 4 ? (per < 1 ? 1 : per) : 4);
+  }
+  void* args[] = {&jb};
+  cudaLaunchCooperativeKernel((const void*)k_prep_img<NA>, dim3(grid), dim3(256), args, 0, st);
+  ++launch_counter();
 }
 
 template <int kMode, int NA, bool kDual>
@@ -443,8 +528,8 @@ static int run_tc(const SideView& s, const float* P1, const float* P2, int W, fl
   const int64_t ib = tc_img_bytes(rlen, W);
   float* cinv1 = nullptr;
   float* cinv2 = nullptr;
-  prep_img<NA>(P1, rlen, W, kMode == 1 ? s.inv_lam : nullptr, img, &cinv1, st);
-  if (kDual) prep_img<NA>(P2, rlen, W, nullptr, img + ib, &cinv2, st);
+  prep_imgs<NA>(P1, kDual ? P2 : nullptr, rlen, W, kMode == 1 ? s.inv_lam : nullptr, img, img + ib, &cinv1, &cinv2,
+                st);
   a.img1 = img;
   a.img2 = img + ib;
   a.cinv1 = cinv1;
@@ -513,3 +598,9 @@ int launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, fl
 }
 
 }  // namespace lrqmm
+
+#ifdef LRQMM_PREP_TIMING
+extern "C" int lrqmm_debug_prep_times(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, lrqmm::g_prep_t, sizeof(unsigned long long) * 8);
+}
+#endif
