@@ -5,43 +5,45 @@
 // to Kp = roundup(K,128)) and lambda (rows fp32).  Each row is read from HBM once:
 // it stays in registers between the amax reduction and the rounding pass.
 //
-// Bit-exact rounding on the exact product lambda*x (reading #4):
-//   p = RN(lambda*x), e = fma(lambda, x, -p) is the exact error of the product, and
-//   floor(lambda*x) = floorf(p) - (p == floorf(p) && (e < 0 || (p == 0 && x < 0))).
-// RN is monotone and integers / half-integers are fp32-representable below 2^23,
-// so p lies in the same unit interval as the exact product except when p itself
-// is an integer (floor/trunc) or a half-integer (nearest); e decides those.
+// Bit-exact rounding on the exact product lambda*x (reading #4), on the FMA pipe:
+//   n = fma(lambda, x, 1.5 2^23) - 1.5 2^23 (integer bits) is RN_int(lambda x) of the EXACT product
+//   (|lambda x| <= qmax (1 + 2^-23) < 2^22, so the sum lies where the fp32 ulp is 1; ties to even),
+//   d = fma(lambda, x, -n) has the sign of the exact lambda x - n, so
+//   floor = n - (d < 0), ceil = n + (d > 0), trunc = floor / ceil by sign, nearest = n.
+//   (d underflows to 0 only for n = 0 with |lambda x| < 2^-149: then x decides floor.)
 #include "common.cuh"
 #include "kernels.h"
 
 namespace lrqmm {
 
-LRQMM_DEV int round_exact(float lam, float x, int mode) {
-  const float p = __fmul_rn(lam, x);
-  const float e = __fmaf_rn(lam, x, -p);
-  if (mode == kRoundFloor) {
-    float f = floorf(p);
-    if (p == f && (e < 0.f || (p == 0.f && x < 0.f))) f -= 1.f;
-    return static_cast<int>(f);
-  } else if (mode == kRoundTrunc) {
-    float t = truncf(p);
-    if (p == t && p != 0.f) {
-      if (p > 0.f && e < 0.f) t -= 1.f;
-      if (p < 0.f && e > 0.f) t += 1.f;
-    }
-    return static_cast<int>(t);
-  } else {  // nearest, ties to even, decided on the exact product
-    float r = rintf(p);
-    const float fl = floorf(p);
-    if (p - fl == 0.5f && e != 0.f) r = (e > 0.f) ? fl + 1.f : fl;
-    return static_cast<int>(r);
-  }
+constexpr float kMagic = 12582912.f;  // 1.5 2^23
+constexpr int kMagicBits = 0x4B400000;
+
+LRQMM_DEV int code_int(float lam, float x, int mode) {
+  const int n = __float_as_int(__fmaf_rn(lam, x, kMagic)) - kMagicBits;
+  if (mode == kRoundNearest) return n;
+  const float d = __fmaf_rn(lam, x, -(float)n);
+  if (mode == kRoundFloor) return n - ((d < 0.f || (d == 0.f && n == 0 && x < 0.f)) ? 1 : 0);
+  return x >= 0.f ? n - (d < 0.f ? 1 : 0) : n + (d > 0.f ? 1 : 0);  // trunc
 }
 
 LRQMM_DEV int8_t code_of(float lam, float x, int mode, int qmax) {
-  int c = round_exact(lam, x, mode);
+  int c = code_int(lam, x, mode);
   c = c > qmax ? qmax : (c < -qmax ? -qmax : c);
   return static_cast<int8_t>(c);
+}
+
+// Q15 residual fraction i = clamp(RN(2^15 (lambda x - code)), +-32767) with ONE rounding of the exact
+// value: RN_int(2^15 lambda x) - 2^15 code (lam32k = 2^15 lambda, exact unless it overflows, see
+// k1 callers: rows with lambda > 2^100 take the two-step form).
+LRQMM_DEV int u_q15(float lam32k, float x, int code) {
+  int i = __float_as_int(__fmaf_rn(lam32k, x, kMagic)) - kMagicBits - 32768 * code;
+  return i > 32767 ? 32767 : (i < -32767 ? -32767 : i);
+}
+LRQMM_DEV int u_q15_slow(float lam, float x, int code) {
+  const float u = __fmaf_rn(lam, x, -(float)code);  // |u| < 1, |error| <= 2^-24
+  int i = __float2int_rn(u * 32768.f);
+  return i > 32767 ? 32767 : (i < -32767 ? -32767 : i);
 }
 
 LRQMM_DEV uint32_t pack4(int8_t a, int8_t b, int8_t c, int8_t d) {
@@ -49,11 +51,6 @@ LRQMM_DEV uint32_t pack4(int8_t a, int8_t b, int8_t c, int8_t d) {
          ((uint32_t)(uint8_t)d << 24);
 }
 
-// residual fraction u (exact fp32, |u| < 1) -> Q15: clamp(RN(u * 2^15), +-32767); the scaling is exact
-LRQMM_DEV int u_fix(float u) {
-  const int q = __float2int_rn(u * kUScale);
-  return q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
-}
 LRQMM_DEV uint32_t pack_bytes(int a, int b, int c, int d) {
   return ((uint32_t)a & 0xffu) | (((uint32_t)b & 0xffu) << 8) | (((uint32_t)c & 0xffu) << 16) | ((uint32_t)d << 24);
 }
@@ -132,8 +129,14 @@ __global__ void __launch_bounds__(256) k1_quantize(const float* __restrict__ X, 
           crow[col >> 2] = pack4(c0, c1, c2, c3);
           // residual fraction u = lambda x - code (R = u / lambda, Alg. 2), exactly rounded
           if (urow && col < ldu) {
-            const int i0 = u_fix(__fmaf_rn(lam, v[i].x, -(float)c0)), i1 = u_fix(__fmaf_rn(lam, v[i].y, -(float)c1));
-            const int i2 = u_fix(__fmaf_rn(lam, v[i].z, -(float)c2)), i3 = u_fix(__fmaf_rn(lam, v[i].w, -(float)c3));
+            int i0, i1, i2, i3;
+            if (lam < 0x1p100f) {
+              const float l32 = lam * 32768.f;
+              i0 = u_q15(l32, v[i].x, c0); i1 = u_q15(l32, v[i].y, c1); i2 = u_q15(l32, v[i].z, c2); i3 = u_q15(l32, v[i].w, c3);
+            } else {
+              i0 = u_q15_slow(lam, v[i].x, c0); i1 = u_q15_slow(lam, v[i].y, c1);
+              i2 = u_q15_slow(lam, v[i].z, c2); i3 = u_q15_slow(lam, v[i].w, c3);
+            }
             __stcg(reinterpret_cast<uint32_t*>(urow + col), pack_bytes(i0 >> 8, i1 >> 8, i2 >> 8, i3 >> 8));
             __stcg(reinterpret_cast<uint32_t*>(urow + uplane + col), pack_bytes(i0, i1, i2, i3));
           }
@@ -234,12 +237,162 @@ __global__ void __launch_bounds__(256) k1_quantize_long(const float* __restrict_
       const int8_t q = code_of(lam, x, mode, qmax);
       crow[c] = q;
       if (U && c < ldu) {
-        const int iu = u_fix(__fmaf_rn(lam, x, -(float)q));
+        const int iu = lam < 0x1p100f ? u_q15(lam * 32768.f, x, q) : u_q15_slow(lam, x, q);
         U[row * ldu + c] = (uint8_t)(iu >> 8);
         U[uplane + row * ldu + c] = (uint8_t)(iu & 255);
       }
     }
   }
+}
+
+// Persistent TMA-pipelined K1 (rows of up to ~24K floats, K % 4 == 0, 16-byte aligned rows):
+// a producer warp bulk-copies whole rows into an NS-deep shared-memory ring while 16 consumer
+// warps quantize the previous ones, so HBM reads never wait for the reduce / round / store
+// phases.  Same arithmetic as k1_quantize: the row is read from smem once into registers.
+namespace k1t {
+constexpr int kCons = 512;                 // consumer threads (16 warps)
+constexpr int kThreads = kCons + 32;       // + producer warp
+constexpr int kSmemBudget = 200 * 1024;
+}  // namespace k1t
+
+template <int VPT, bool kFixedLam>
+__global__ void __launch_bounds__(k1t::kThreads, 1)
+    k1_quantize_tma(const float* __restrict__ X, int64_t ldx, int rows, int K, int Kp, int qmax, int mode,
+                    int8_t* __restrict__ codes, float* __restrict__ lam_out, float* __restrict__ inv_out,
+                    const float* __restrict__ lam_in, int* __restrict__ err_flag, uint8_t* __restrict__ U,
+                    int64_t ldu, int64_t uplane, int ns, int slot_bytes) {
+  using namespace k1t;
+  extern __shared__ __align__(128) uint8_t smem_k1[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_k1);
+  uint64_t* empty = full + ns;
+  __shared__ float red[2][16];
+  uint8_t* ring = smem_k1 + 1024;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCons / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t row_bytes = (uint32_t)K * 4u;
+  if (warp == kCons / 32) {
+    // ------------------------------------------------------------- producer
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, ++it) {
+        const int s = it % ns;
+        mbar_wait(&empty[s], ((it / ns) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], row_bytes);
+        bulk_load(ring + (size_t)s * slot_bytes, X + r * ldx, row_bytes, &full[s]);
+      }
+    }
+    return;
+  }
+  // --------------------------------------------------------------- consumers
+  int it = 0;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, ++it) {
+    const int s = it % ns;
+    mbar_wait(&full[s], (it / ns) & 1);
+    const uint32_t base = smem_u32(ring + (size_t)s * slot_bytes);
+    float4 v[VPT];
+    float amax = 0.f;
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int col = (tid + i * kCons) * 4;
+      v[i] = col < K ? lds128(base + (uint32_t)col * 4u) : make_float4(0.f, 0.f, 0.f, 0.f);
+      bad |= !(isfinite(v[i].x) && isfinite(v[i].y) && isfinite(v[i].z) && isfinite(v[i].w));
+      amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
+    }
+    // the row is in registers (amax depends on every value): hand the slot back to the producer
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (bad) atomicOr(err_flag, 1);
+    float lam;
+    if (kFixedLam) {
+      lam = lam_in[0];
+    } else {
+      amax = warp_max(amax);
+      if (lane == 0) red[it & 1][warp] = amax;
+      asm volatile("bar.sync 1, %0;" ::"n"(kCons) : "memory");
+      float m = red[it & 1][0];
+#pragma unroll
+      for (int w = 1; w < kCons / 32; ++w) m = fmaxf(m, red[it & 1][w]);
+      // lambda = RN32(qmax / amax) (IEEE division), 1 for an all-zero row.
+      lam = (m == 0.f) ? 1.f : __fdiv_rn(static_cast<float>(qmax), m);
+      if (tid == 0) {
+        lam_out[r] = lam;
+        inv_out[r] = __frcp_rn(lam);
+      }
+    }
+    uint32_t* crow = reinterpret_cast<uint32_t*>(codes + r * (int64_t)Kp);
+    uint8_t* urow = U ? U + r * ldu : nullptr;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int col = (tid + i * kCons) * 4;
+      if (col < Kp) {
+        // padded columns (K <= col < Kp) hold x = 0 -> code 0, u = 0
+        const int8_t c0 = code_of(lam, v[i].x, mode, qmax), c1 = code_of(lam, v[i].y, mode, qmax);
+        const int8_t c2 = code_of(lam, v[i].z, mode, qmax), c3 = code_of(lam, v[i].w, mode, qmax);
+        crow[col >> 2] = pack4(c0, c1, c2, c3);
+        if (urow) {
+          int i0, i1, i2, i3;
+          if (lam < 0x1p100f) {
+            const float l32 = lam * 32768.f;
+            i0 = u_q15(l32, v[i].x, c0); i1 = u_q15(l32, v[i].y, c1); i2 = u_q15(l32, v[i].z, c2); i3 = u_q15(l32, v[i].w, c3);
+          } else {
+            i0 = u_q15_slow(lam, v[i].x, c0); i1 = u_q15_slow(lam, v[i].y, c1);
+            i2 = u_q15_slow(lam, v[i].z, c2); i3 = u_q15_slow(lam, v[i].w, c3);
+          }
+          __stcg(reinterpret_cast<uint32_t*>(urow + col), pack_bytes(i0 >> 8, i1 >> 8, i2 >> 8, i3 >> 8));
+          __stcg(reinterpret_cast<uint32_t*>(urow + uplane + col), pack_bytes(i0, i1, i2, i3));
+        }
+      }
+    }
+  }
+}
+
+template <int VPT>
+static bool launch_k1_tma_t(const QuantArgs& a, bool fixed, cudaStream_t st) {
+  const int slot = (a.K * 4 + 1023) / 1024 * 1024;
+  int ns = k1t::kSmemBudget / slot;
+  if (ns > 8) ns = 8;
+  if (ns < 2) return false;
+  const int smem = 1024 + ns * slot;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = (int)(a.rows < nsm ? a.rows : nsm);
+  if (fixed) {
+    cudaFuncSetAttribute(k1_quantize_tma<VPT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k1_quantize_tma<VPT, true><<<grid, k1t::kThreads, smem, st>>>(a.X, a.ldx, (int)a.rows, a.K, a.Kp, a.qmax, a.mode,
+                                                                  a.codes, a.lam, a.inv_lam, a.lam_fixed, a.err_flag,
+                                                                  a.U, a.ldu, a.uplane, ns, slot);
+  } else {
+    cudaFuncSetAttribute(k1_quantize_tma<VPT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k1_quantize_tma<VPT, false><<<grid, k1t::kThreads, smem, st>>>(a.X, a.ldx, (int)a.rows, a.K, a.Kp, a.qmax, a.mode,
+                                                                   a.codes, a.lam, a.inv_lam, a.lam_fixed, a.err_flag,
+                                                                   a.U, a.ldu, a.uplane, ns, slot);
+  }
+  ++launch_counter();
+  return true;
+}
+
+// TMA path: rows 16-byte aligned (bulk copies) and at least ~4K columns (enough bytes per copy)
+static bool launch_k1_tma(const QuantArgs& a, bool fixed, cudaStream_t st) {
+  if ((reinterpret_cast<uintptr_t>(a.X) & 15) != 0 || a.ldx % 4 != 0 || a.K % 4 != 0 || a.K < 4096) return false;
+  const int Kp = a.Kp;
+  constexpr int C4 = k1t::kCons * 4;
+  if (Kp <= C4 * 2) return launch_k1_tma_t<2>(a, fixed, st);
+  if (Kp <= C4 * 4) return launch_k1_tma_t<4>(a, fixed, st);
+  if (Kp <= C4 * 8) return launch_k1_tma_t<8>(a, fixed, st);
+  if (Kp <= C4 * 12) return launch_k1_tma_t<12>(a, fixed, st);
+  return false;
 }
 
 template <int TPR, int VPT>
@@ -265,6 +418,9 @@ void launch_quantize(const QuantArgs& a, cudaStream_t st) {
   const bool vec = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
   const bool fixed = a.lam_fixed != nullptr;
   const int Kp = a.Kp;
+#ifndef LRQMM_K1_NO_TMA
+  if (launch_k1_tma(a, fixed, st)) return;
+#endif
   if (Kp <= 32 * 4 * 1) launch_k1_t<32, 1>(a, vec, fixed, st);
   else if (Kp <= 32 * 4 * 2) launch_k1_t<32, 2>(a, vec, fixed, st);
   else if (Kp <= 32 * 4 * 4) launch_k1_t<32, 4>(a, vec, fixed, st);

@@ -24,14 +24,14 @@ def rel(a, b):
 
 def side(rows, K, dist="normal", bits=4, seed=0):
     """Oracle codes / scales and the residual AS THE PASSES SEE IT: K1 stores the residual fraction
-    u = fp32(lambda x - code) in Q15 fixed point (kernels.h kUScale, reading #28), so the
-    stage reference is R_q = (RN(u 2^15) / 2^15) / lambda, within 2^-16 / lambda (2^-15 where u rounds past the clamp) of the oracle's R."""
+    u = lambda x - code in Q15 fixed point (kernels.h kUScale, reading #28), so the
+    stage reference is R_q = (RN(2^15 (lambda x - code)) / 2^15) / lambda, within 2^-16 / lambda (2^-15 where u rounds past the clamp) of the oracle's R."""
     X = S.gen_matrix(dist, rows, K, seed)
     codes, lam = O.quantize(X, bits)
     R = O.residual(X, codes, lam)
     lam64 = lam.astype(np.float64)[:, None]
-    u = (lam64 * X.astype(np.float64) - codes).astype(np.float32).astype(np.float64)
-    u16 = np.clip(np.rint(u * 32768.0), -32767, 32767)
+    # one rounding of the exact value: lambda x is exact in fp64 (24 + 24 bits), 2^15 scaling exact
+    u16 = np.clip(np.rint((lam64 * X.astype(np.float64) - codes) * 32768.0), -32767, 32767)
     Rq = u16 / 32768.0 / lam64
     assert np.all(np.abs(Rq - R) <= 2.0 ** -15 / lam64 * (1 + 1e-9))  # 2^-16, 2^-15 at the clamp u -> 1
     return X, codes, lam, Rq

@@ -9,7 +9,7 @@ bad = 0; tot = 0
 for rep in range(3):
   for (rows, K, W) in [(257, 4096, 40), (2048, 4096, 24), (128, 4096, 40), (257, 4096, 32), (1000, 2048, 64)]:
     X = S.gen_matrix("normal", rows, K, rep); codes, lam = O.quantize(X, 4); l64 = lam.astype(np.float64)[:, None]
-    u = (l64 * X - codes).astype(np.float32).astype(np.float64); R = np.clip(np.rint(u * 32768), -32767, 32767) / 32768 / l64  # Q15 as stored
+    R = np.clip(np.rint((l64 * X - codes) * 32768), -32767, 32767) / 32768 / l64  # Q15 as stored
     P = np.random.default_rng(1).standard_normal((K, W)).astype(np.float32)
     ref = R @ P
     for mode in (0, 1):
