@@ -245,6 +245,36 @@ __global__ void __launch_bounds__(256) k1_quantize_long(const float* __restrict_
   }
 }
 
+// ---- lean per-element arithmetic of the TMA K1 (same exact results as code_of / u_q15) ----
+// code: directed-rounding FMA of the exact product into the magic range (ulp 1):
+//   floor = RD(lambda x + 1.5 2^23) - 1.5 2^23, trunc = RD / RU by the sign of x, nearest = RN.
+template <int kMode>
+LRQMM_DEV int code_fast(float lam, float x, int qmax) {
+  int c;
+  if (kMode == kRoundFloor) {
+    c = __float_as_int(__fmaf_rd(lam, x, kMagic)) - kMagicBits;
+    c = c < -qmax ? -qmax : c;  // floor only overshoots downwards (lambda amax may exceed qmax by an ulp)
+  } else if (kMode == kRoundTrunc) {
+    c = __float_as_int(x >= 0.f ? __fmaf_rd(lam, x, kMagic) : __fmaf_ru(lam, x, kMagic)) - kMagicBits;
+  } else {
+    c = __float_as_int(__fmaf_rn(lam, x, kMagic)) - kMagicBits;
+  }
+  return c;
+}
+// Q15 of lambda x - c (one rounding), clamped on the side the mode can overshoot
+template <int kMode>
+LRQMM_DEV int q15_fast(float lam32k, float x, int c) {
+  int i = __float_as_int(__fmaf_rn(lam32k, x, kMagic)) - kMagicBits - (c << 15);
+  if (kMode == kRoundFloor) return i > 32767 ? 32767 : i;
+  return i > 32767 ? 32767 : (i < -32767 ? -32767 : i);
+}
+LRQMM_DEV uint32_t bytes4(int a, int b, int c, int d) {  // low bytes of a..d (PRMT)
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+LRQMM_DEV uint32_t hbytes4(int a, int b, int c, int d) {  // byte 1 of a..d
+  return __byte_perm(__byte_perm(a, b, 0x0051), __byte_perm(c, d, 0x0051), 0x5410);
+}
+
 // Persistent TMA-pipelined K1 (rows of up to ~24K floats, K % 4 == 0, 16-byte aligned rows):
 // a producer warp bulk-copies whole rows into an NS-deep shared-memory ring while 16 consumer
 // warps quantize the previous ones, so HBM reads never wait for the reduce / round / store
@@ -255,7 +285,7 @@ constexpr int kThreads = kCons + 32;       // + producer warp
 constexpr int kSmemBudget = 200 * 1024;
 }  // namespace k1t
 
-template <int VPT, bool kFixedLam>
+template <int VPT, bool kFixedLam, int kMode>
 __global__ void __launch_bounds__(k1t::kThreads, 1)
     k1_quantize_tma(const float* __restrict__ X, int64_t ldx, int rows, int K, int Kp, int qmax, int mode,
                     int8_t* __restrict__ codes, float* __restrict__ lam_out, float* __restrict__ inv_out,
@@ -297,15 +327,18 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
     mbar_wait(&full[s], (it / ns) & 1);
     const uint32_t base = smem_u32(ring + (size_t)s * slot_bytes);
     float4 v[VPT];
-    float amax = 0.f;
-    bool bad = false;
+    float amax = 0.f, chk = 0.f;  // chk = sum x * 0: NaN iff some x is NaN or Inf
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int col = (tid + i * kCons) * 4;
       v[i] = col < K ? lds128(base + (uint32_t)col * 4u) : make_float4(0.f, 0.f, 0.f, 0.f);
-      bad |= !(isfinite(v[i].x) && isfinite(v[i].y) && isfinite(v[i].z) && isfinite(v[i].w));
+      chk = __fmaf_rn(v[i].x, 0.f, chk);
+      chk = __fmaf_rn(v[i].y, 0.f, chk);
+      chk = __fmaf_rn(v[i].z, 0.f, chk);
+      chk = __fmaf_rn(v[i].w, 0.f, chk);
       amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
     }
+    const bool bad = chk != chk;
     // the row is in registers (amax depends on every value): hand the slot back to the producer
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -329,25 +362,27 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
     }
     uint32_t* crow = reinterpret_cast<uint32_t*>(codes + r * (int64_t)Kp);
     uint8_t* urow = U ? U + r * ldu : nullptr;
+    const bool fast = lam < 0x1p100f;  // 2^15 lambda representable (always, but for rows of ~1e-28)
+    const float l32 = lam * 32768.f;
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int col = (tid + i * kCons) * 4;
       if (col < Kp) {
         // padded columns (K <= col < Kp) hold x = 0 -> code 0, u = 0
-        const int8_t c0 = code_of(lam, v[i].x, mode, qmax), c1 = code_of(lam, v[i].y, mode, qmax);
-        const int8_t c2 = code_of(lam, v[i].z, mode, qmax), c3 = code_of(lam, v[i].w, mode, qmax);
-        crow[col >> 2] = pack4(c0, c1, c2, c3);
+        const int c0 = code_fast<kMode>(lam, v[i].x, qmax), c1 = code_fast<kMode>(lam, v[i].y, qmax);
+        const int c2 = code_fast<kMode>(lam, v[i].z, qmax), c3 = code_fast<kMode>(lam, v[i].w, qmax);
+        crow[col >> 2] = bytes4(c0, c1, c2, c3);
         if (urow) {
           int i0, i1, i2, i3;
-          if (lam < 0x1p100f) {
-            const float l32 = lam * 32768.f;
-            i0 = u_q15(l32, v[i].x, c0); i1 = u_q15(l32, v[i].y, c1); i2 = u_q15(l32, v[i].z, c2); i3 = u_q15(l32, v[i].w, c3);
+          if (fast) {
+            i0 = q15_fast<kMode>(l32, v[i].x, c0); i1 = q15_fast<kMode>(l32, v[i].y, c1);
+            i2 = q15_fast<kMode>(l32, v[i].z, c2); i3 = q15_fast<kMode>(l32, v[i].w, c3);
           } else {
             i0 = u_q15_slow(lam, v[i].x, c0); i1 = u_q15_slow(lam, v[i].y, c1);
             i2 = u_q15_slow(lam, v[i].z, c2); i3 = u_q15_slow(lam, v[i].w, c3);
           }
-          __stcg(reinterpret_cast<uint32_t*>(urow + col), pack_bytes(i0 >> 8, i1 >> 8, i2 >> 8, i3 >> 8));
-          __stcg(reinterpret_cast<uint32_t*>(urow + uplane + col), pack_bytes(i0, i1, i2, i3));
+          __stcg(reinterpret_cast<uint32_t*>(urow + col), hbytes4(i0, i1, i2, i3));
+          __stcg(reinterpret_cast<uint32_t*>(urow + uplane + col), bytes4(i0, i1, i2, i3));
         }
       }
     }
@@ -368,17 +403,23 @@ static bool launch_k1_tma_t(const QuantArgs& a, bool fixed, cudaStream_t st) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   const int grid = (int)(a.rows < nsm ? a.rows : nsm);
+#define K1T_LAUNCH(F, M)                                                                                         \
+  do {                                                                                                           \
+    cudaFuncSetAttribute(k1_quantize_tma<VPT, F, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);        \
+    k1_quantize_tma<VPT, F, M><<<grid, k1t::kThreads, smem, st>>>(a.X, a.ldx, (int)a.rows, a.K, a.Kp, a.qmax,   \
+                                                                  a.mode, a.codes, a.lam, a.inv_lam, a.lam_fixed, \
+                                                                  a.err_flag, a.U, a.ldu, a.uplane, ns, slot);   \
+  } while (0)
   if (fixed) {
-    cudaFuncSetAttribute(k1_quantize_tma<VPT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k1_quantize_tma<VPT, true><<<grid, k1t::kThreads, smem, st>>>(a.X, a.ldx, (int)a.rows, a.K, a.Kp, a.qmax, a.mode,
-                                                                  a.codes, a.lam, a.inv_lam, a.lam_fixed, a.err_flag,
-                                                                  a.U, a.ldu, a.uplane, ns, slot);
+    if (a.mode == kRoundFloor) K1T_LAUNCH(true, kRoundFloor);
+    else if (a.mode == kRoundTrunc) K1T_LAUNCH(true, kRoundTrunc);
+    else K1T_LAUNCH(true, kRoundNearest);
   } else {
-    cudaFuncSetAttribute(k1_quantize_tma<VPT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k1_quantize_tma<VPT, false><<<grid, k1t::kThreads, smem, st>>>(a.X, a.ldx, (int)a.rows, a.K, a.Kp, a.qmax, a.mode,
-                                                                   a.codes, a.lam, a.inv_lam, a.lam_fixed, a.err_flag,
-                                                                   a.U, a.ldu, a.uplane, ns, slot);
+    if (a.mode == kRoundFloor) K1T_LAUNCH(false, kRoundFloor);
+    else if (a.mode == kRoundTrunc) K1T_LAUNCH(false, kRoundTrunc);
+    else K1T_LAUNCH(false, kRoundNearest);
   }
+#undef K1T_LAUNCH
   ++launch_counter();
   return true;
 }
