@@ -22,6 +22,11 @@ extern "C" {
 lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx, int64_t rows, int K, int bits, int rounding,
                                 const float* P, const float* P2, int W, float* OUT, float* OUT2, void* stream);
 
+/* GEMM kernel selection for later calls in this process: 0 = automatic (CTA-pair kernel for
+ * M, N >= 512), 1 = one-CTA kernel (K6), 2 = CTA-pair kernel (K7).  Lets the tests run both
+ * kernels on the same shapes.  Returns INVALID_ARGUMENT for other values. */
+lrqmm_status_t lrqmm_debug_set_gemm_variant(int variant);
+
 /* Small solvers (K4) on Y (n x W):
  *   op 0: G = Y^T Y (fp64, W x W)
  *   op 1: G = Y^T Y, T = orthonormalising transform (Y T has orthonormal columns)

@@ -64,11 +64,12 @@ struct G6Params {
   int vec_ok;
 };
 
+template <int kGM = g6::kGroupM>
 LRQMM_DEV void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
-  const int per_group = g6::kGroupM * num_n;
+  const int per_group = kGM * num_n;
   const int group = t / per_group;
-  const int first_m = group * g6::kGroupM;
-  const int gsize = min(g6::kGroupM, num_m - first_m);
+  const int first_m = group * kGM;
+  const int gsize = min(kGM, num_m - first_m);
   const int in = t % per_group;
   mb = first_m + in % gsize;
   nb = in / gsize;
@@ -312,6 +313,301 @@ __global__ void __launch_bounds__(g6::kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// K7 — the same GEMM + epilogue on CTA PAIRS (cluster of 2, tcgen05.mma.cta_group::2):
+// a pair owns a 256 x 256 output tile; CTA r loads A rows [256 mb + 128 r, +128) and B^T rows
+// [256 nb + 128 r, +128) (32 KB per 128-deep stage instead of 48 KB), the leader (r = 0) issues
+// one M = 256, N = 256, K = 32 MMA per step that reads both CTAs' shared memory, and each CTA's
+// TMEM receives its own 128 rows x 256 columns, so the epilogue is the one of K6.  Per SM this
+// halves the MMA instructions, commits and B bytes per unit of tensor work.
+//   full[s]  (leader)   : both CTAs' TMA bytes (expect_tx set by the leader's producer)
+//   empty[s] (each CTA) : multicast commit from the leader's MMA
+//   tfull[a] (each CTA) : multicast commit at the end of a tile
+//   tempty[a] (leader)  : 128 epilogue threads of EACH CTA (peer arrives remotely)
+namespace g7 {
+constexpr int BM = 128;  // rows per CTA (256 per pair)
+constexpr int BN = 256;  // output columns per pair tile
+constexpr int BNH = 128; // B^T rows loaded per CTA
+constexpr int BK = 128;
+constexpr int UK = 32;
+constexpr int kThreads = 192;
+constexpr int kEpiThreads = 128;
+constexpr int kABytes = BM * BK;
+constexpr int kBBytes = BNH * BK;
+constexpr int kStageBytes = kABytes + kBBytes;  // 32 KB per CTA
+#ifndef LRQMM_L2HINT7
+#define LRQMM_L2HINT7 1  // A panels evict_last (reused by the next waves of the raster group)
+#endif
+#ifndef LRQMM_PAIR_RELEASE
+#define LRQMM_PAIR_RELEASE 0  // one commit per two stages (measured slower: less buffering)
+#endif
+#ifndef LRQMM_GROUPM7
+#define LRQMM_GROUPM7 8
+#endif
+constexpr int kGroupM = LRQMM_GROUPM7;  // pair-tile rows (256 A rows each) per raster group
+__host__ __device__ constexpr int extra_bytes(int r2) { return BN * r2 * 4 + BN * 4 + 256 + 1024; }
+__host__ __device__ constexpr int stages_for(int r2) {  // even: stages are released in pairs
+  return ((232448 - extra_bytes(r2)) / kStageBytes > 6 ? 6 : (232448 - extra_bytes(r2)) / kStageBytes) & ~1;
+}
+__host__ __device__ constexpr int smem_bytes(int r2) { return stages_for(r2) * kStageBytes + extra_bytes(r2); }
+}  // namespace g7
+
+LRQMM_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+LRQMM_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same offset in CTA `rank` of the cluster
+LRQMM_DEV uint32_t mapa_cta(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+LRQMM_DEV void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// 2SM TMA: data lands in this CTA's smem, complete_tx goes to the barrier at `mbar_cluster`
+LRQMM_DEV void tma_load_2d_2sm(void* smem_dst, const void* desc, uint32_t mbar_cluster, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(mbar_cluster), "r"(x), "r"(y)
+      : "memory");
+}
+LRQMM_DEV void tma_load_2d_2sm_hint(void* smem_dst, const void* desc, uint32_t mbar_cluster, int x, int y,
+                                    uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(mbar_cluster), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+LRQMM_DEV void umma_i8_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// warp-collective forms: the whole (converged) warp executes them, one elected lane issues, so the
+// operands stay warp-uniform and no per-instruction elect loop is generated
+LRQMM_DEV void umma_i8_2sm_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+LRQMM_DEV void umma_commit_2sm_mc_warp(uint32_t bar_addr) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\t.reg .pred e;\n\tmov.b16 m, 3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          bar_addr)
+      : "memory");
+}
+LRQMM_DEV void umma_commit_2sm_mc(uint64_t* bar) {  // arrive on `bar` in both CTAs of the pair
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+template <int kR2>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
+    k7_gemm_i8_2sm(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, G6Params p) {
+  using namespace g7;
+  constexpr int STAGES = stages_for(kR2);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * kABytes;
+  float* sLB = reinterpret_cast<float*>(smem + STAGES * kStageBytes);  // BN x kR2
+  float* sSB = sLB + BN * kR2;                                           // BN : 1/lambda_b
+  const uint32_t sLBa = smem_u32(sLB), sSBa = smem_u32(sSB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sSB + BN);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int num_tiles = p.num_m * p.num_n;  // pair tiles (256 x 256)
+  const bool pair_rel = LRQMM_PAIR_RELEASE && (p.num_kb & 1) == 0;  // a tile always starts on an even stage
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mapA);
+    tma_prefetch_desc(&mapB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * kEpiThreads);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t full0 = mapa_cta(smem_u32(full), 0);  // leader's full[0]
+#if LRQMM_L2HINT7
+      const uint64_t polA = l2_policy_evict_last();
+#endif
+      for (int t = pair; t < num_tiles; t += npairs) {
+        int mb, nb;
+        tile_coords<g7::kGroupM>(t, p.num_m, p.num_n, mb, nb);
+        const int arow = mb * (2 * BM) + (int)rank * BM;
+        const int brow = nb * BN + (int)rank * BNH;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          // with an even k-block count, stages are released in pairs (one MMA commit per two)
+          if (!pair_rel) mbar_wait(&empty[stage], phase ^ 1);
+          else if ((stage & 1) == 0) mbar_wait(&empty[stage >> 1], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
+          const uint32_t fb = full0 + stage * 8;
+#if LRQMM_L2HINT7
+          tma_load_2d_2sm_hint(sA + stage * kABytes, &mapA, fb, kb * BK, arow, polA);
+#else
+          tma_load_2d_2sm(sA + stage * kABytes, &mapA, fb, kb * BK, arow);
+#endif
+          tma_load_2d_2sm(sB + stage * kBBytes, &mapB, fb, kb * BK, brow);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ UMMA issuer (leader only)
+    // The whole warp runs the loop (warp-uniform operands); one elected lane issues each op.
+    if (leader) {
+      constexpr uint32_t idesc = make_idesc_i8(2 * BM, BN);
+      // descriptors differ only in the start-address field (addr >> 4, no carry below 256 KB)
+      const uint64_t dA0 = make_sw128_kmajor_desc(smem_u32(sA));
+      const uint64_t dB0 = make_sw128_kmajor_desc(smem_u32(sB));
+      const uint32_t empty_a = smem_u32(empty), tfull_a = smem_u32(tfull);
+      int stage = 0;
+      uint32_t phase = 0;
+      int lt = 0;
+      for (int t = pair; t < num_tiles; t += npairs, ++lt) {
+        const int acc = lt & 1;
+        const uint32_t acc_phase = (lt >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = dA0 + (uint64_t)((stage * kABytes) >> 4);
+          const uint64_t bd = dB0 + (uint64_t)((stage * kBBytes) >> 4);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            umma_i8_2sm_warp(d_tmem, ad + (uint64_t)((k * UK) >> 4), bd + (uint64_t)((k * UK) >> 4), idesc,
+                             (kb | k) != 0 ? 1u : 0u);
+          // frees this stage (or the pair (stage - 1, stage)) in both CTAs
+          if (!pair_rel) umma_commit_2sm_mc_warp(empty_a + 8 * stage);
+          else if (stage & 1) umma_commit_2sm_mc_warp(empty_a + 8 * (stage >> 1));
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_2sm_mc_warp(tfull_a + 8 * acc);  // both halves of the accumulator ready
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------------------------------------------------------- epilogue (both CTAs)
+    const int et = threadIdx.x - 64;  // 0..127
+    const int quad = warp & 3;
+    const uint32_t tempty0 = mapa_cta(smem_u32(tempty), 0);
+    int lt = 0;
+    for (int t = pair; t < num_tiles; t += npairs, ++lt) {
+      int mb, nb;
+      tile_coords<g7::kGroupM>(t, p.num_m, p.num_n, mb, nb);
+      const int acc = lt & 1;
+      const uint32_t acc_phase = (lt >> 1) & 1;
+      const int64_t row = (int64_t)mb * (2 * BM) + (int64_t)rank * BM + quad * 32 + lane;
+      const int n0 = nb * BN;
+      float sa = 0.f;
+      float la[kR2 > 0 ? kR2 : 1];
+#pragma unroll
+      for (int l = 0; l < (kR2 > 0 ? kR2 : 1); ++l) la[l] = 0.f;
+      if (p.epi == 1) {
+        epi_bar();
+        for (int j = et; j < BN; j += kEpiThreads) {
+          const int col = n0 + j;
+          const float v = col < p.N ? __ldg(p.inv_b + col) : 0.f;
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(sSBa + 4 * j), "f"(v) : "memory");
+        }
+        if constexpr (kR2 > 0) {
+          const float4* src = reinterpret_cast<const float4*>(p.LB + (int64_t)n0 * kR2);
+          const int total4 = BN * kR2 / 4;
+          const int valid4 = (int)((p.N - n0 < BN ? p.N - n0 : (int64_t)BN) * kR2 / 4);
+          for (int e = et; e < total4; e += kEpiThreads)
+            sts128(sLBa + 16 * e, e < valid4 ? __ldg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+        if (row < p.M) {
+          sa = p.alpha * __ldg(p.inv_a + row);
+          if constexpr (kR2 > 0) {
+            const float4* lr = reinterpret_cast<const float4*>(p.LA + row * kR2);
+#pragma unroll
+            for (int l = 0; l < kR2; l += 4) {
+              const float4 v = __ldg(lr + (l >> 2));
+              la[l] = p.alpha * v.x; la[l + 1] = p.alpha * v.y; la[l + 2] = p.alpha * v.z; la[l + 3] = p.alpha * v.w;
+            }
+          }
+        }
+        epi_bar();
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      uint32_t ra[8], rb[8];
+      tmem_ld_32x32b_x8(t_row, ra);
+#pragma unroll 1
+      for (int g = 0; g < BN / 8; g += 2) {
+        tmem_ld_wait();
+        tmem_ld_32x32b_x8(t_row + (g + 1) * 8, rb);
+        epilogue_group<kR2>(p, ra, row, n0 + g * 8, g * 8, sa, la, sLBa, sSBa);
+        tmem_ld_wait();
+        if (g + 2 < BN / 8) tmem_ld_32x32b_x8(t_row + (g + 2) * 8, ra);
+        epilogue_group<kR2>(p, rb, row, n0 + (g + 1) * 8, (g + 1) * 8, sa, la, sLBa, sSBa);
+      }
+      tc_fence_before();
+      mbar_arrive_remote(tempty0 + acc * 8);  // the leader's tempty[acc] (local arrive on the leader)
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // no CTA leaves while its peer may still signal it
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(512) : "memory");
+  }
+}
+
 // ------------------------------------------------------------------- host side
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -391,9 +687,25 @@ int encode_map_1d_f32(void* map, const void* base, uint64_t n, uint32_t box) {
   return r == CUDA_SUCCESS ? 0 : 2;
 }
 
+int& gemm_variant() {  // 0 auto, 1 force one-CTA K6, 2 force CTA-pair K7 (test hook)
+  static int v = 0;
+  return v;
+}
+
+static bool use_2sm(int64_t M, int64_t N) {
+  if (gemm_variant() == 1) return false;
+  if (gemm_variant() == 2) return true;
+  return M >= 512 && N >= 512;
+}
+
+// mapA/mapB hold the K6 maps (box rows 128 / 256); mapA2/mapB2 the K7 maps (128 / 128)
 int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB) {
-  if (encode_codes_map(reinterpret_cast<CUtensorMap*>(mapA), g.A, g.M, g.Kp, g6::BM)) return 1;
-  if (encode_codes_map(reinterpret_cast<CUtensorMap*>(mapB), g.B, g.N, g.Kp, g6::BN)) return 1;
+  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(mapA);
+  CUtensorMap* n = reinterpret_cast<CUtensorMap*>(mapB);
+  if (encode_codes_map(m, g.A, g.M, g.Kp, g6::BM)) return 1;
+  if (encode_codes_map(n, g.B, g.N, g.Kp, g6::BN)) return 1;
+  if (encode_codes_map(m + 1, g.A, g.M, g.Kp, g7::BM)) return 1;
+  if (encode_codes_map(n + 1, g.B, g.N, g.Kp, g7::BNH)) return 1;
   return 0;
 }
 
@@ -407,6 +719,24 @@ static void launch_t(const G6Params& p, const CUtensorMap* mA, const CUtensorMap
     attr = true;
   }
   k6_gemm_i8<kR2><<<grid, g6::kThreads, kSmem, st>>>(*mA, *mB, p); ++launch_counter();
+}
+
+template <int kR2>
+static void launch_t7(G6Params p, const CUtensorMap* mA, const CUtensorMap* mB, int nsm, cudaStream_t st) {
+  constexpr int kSmem = g7::smem_bytes(kR2);
+  static_assert(kSmem <= 232448, "shared memory budget");
+  static_assert(g7::stages_for(kR2) >= 3, "stages");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k7_gemm_i8_2sm<kR2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    attr = true;
+  }
+  p.num_m = (int)((p.M + 2 * g7::BM - 1) / (2 * g7::BM));
+  p.num_n = (int)((p.N + g7::BN - 1) / g7::BN);
+  const int tiles = p.num_m * p.num_n;
+  int pairs = nsm / 2;
+  if (tiles < pairs) pairs = tiles;
+  k7_gemm_i8_2sm<kR2><<<2 * pairs, g7::kThreads, kSmem, st>>>(*mA, *mB, p); ++launch_counter();
 }
 
 void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStream_t st) {
@@ -437,6 +767,21 @@ void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStre
   const CUtensorMap* mA = reinterpret_cast<const CUtensorMap*>(mapA);
   const CUtensorMap* mB = reinterpret_cast<const CUtensorMap*>(mapB);
   const int r2 = g.epi == 0 ? 0 : g.R2;
+  if (use_2sm(g.M, g.N)) {
+    switch (r2) {
+      case 0: launch_t7<0>(p, mA + 1, mB + 1, nsm, st); break;
+      case 8: launch_t7<8>(p, mA + 1, mB + 1, nsm, st); break;
+      case 16: launch_t7<16>(p, mA + 1, mB + 1, nsm, st); break;
+      case 24: launch_t7<24>(p, mA + 1, mB + 1, nsm, st); break;
+      case 32: launch_t7<32>(p, mA + 1, mB + 1, nsm, st); break;
+      case 40: launch_t7<40>(p, mA + 1, mB + 1, nsm, st); break;
+      case 48: launch_t7<48>(p, mA + 1, mB + 1, nsm, st); break;
+      case 56: launch_t7<56>(p, mA + 1, mB + 1, nsm, st); break;
+      case 64: launch_t7<64>(p, mA + 1, mB + 1, nsm, st); break;
+      default: break;
+    }
+    return;
+  }
   switch (r2) {
     case 0: launch_t<0>(p, mA, mB, grid, st); break;
     case 8: launch_t<8>(p, mA, mB, grid, st); break;

@@ -139,7 +139,9 @@ struct GemmArgs {
   int32_t* Cint;         // M x N (ldd)
   int64_t ldd;
 };
-int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB);  // returns 0 on success
+// mapA / mapB: arrays of two CUtensorMap (one-CTA and CTA-pair box shapes); returns 0 on success
+int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB);
+int& gemm_variant();  // 0 auto (CTA pairs when M, N >= 512), 1 one-CTA K6, 2 CTA-pair K7
 // 2D TMA map (no swizzle), dims {inner, outer} elements of fp32 (dtype_f32=1) or u8; returns 0 on success
 int encode_map_2d_sw(void* map, int dtype, const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
                      uint32_t box_inner, uint32_t box_outer, int swizzle_bytes /* 0, 32, 64, 128 */);

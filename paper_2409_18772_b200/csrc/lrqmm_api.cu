@@ -61,8 +61,8 @@ struct lrqmm_handle_s {
   int* counter_cross = nullptr;
   float* VWbM = nullptr;     // W x W
   int* err_flag = nullptr;
-  alignas(64) CUtensorMap mapA;
-  alignas(64) CUtensorMap mapB;
+  alignas(64) CUtensorMap mapA[2];  // [0] one-CTA GEMM boxes, [1] CTA-pair GEMM boxes
+  alignas(64) CUtensorMap mapB[2];
   cudaEvent_t ev[8] = {};
   ncclComm_t comm = nullptr;
   // run_host buffers
@@ -235,7 +235,7 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
   g.M = std::max<int64_t>(cfg->m, 1);
   g.N = std::max<int64_t>(cfg->n, 1);
   g.Kp = h->Kp;
-  if (gemm_prepare_maps(g, &h->mapA, &h->mapB) != 0) {
+  if (gemm_prepare_maps(g, h->mapA, h->mapB) != 0) {
     lrqmm_destroy(h);
     return LRQMM_ERR_CUDA;
   }
@@ -459,7 +459,7 @@ static lrqmm_status_t run_gemm(lrqmm_handle_t h, int epi, float alpha, float bet
   g.D = D;
   g.Cint = Cint;
   g.ldd = ldd;
-  launch_gemm(g, &h->mapA, &h->mapB, h->st);
+  launch_gemm(g, h->mapA, h->mapB, h->st);
   return check_launch(h);
 }
 
@@ -629,6 +629,12 @@ extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx
   }
   cudaFree(U); cudaFree(lam); cudaFree(inv); cudaFree(codes); cudaFree(flag); cudaFree(partial); cudaFree(img);
   return e == cudaSuccess ? LRQMM_OK : (ok ? LRQMM_ERR_CUDA : LRQMM_ERR_ALLOC);
+}
+
+extern "C" lrqmm_status_t lrqmm_debug_set_gemm_variant(int variant) {
+  if (variant < 0 || variant > 2) return LRQMM_ERR_INVALID_ARGUMENT;
+  gemm_variant() = variant;
+  return LRQMM_OK;
 }
 
 extern "C" lrqmm_status_t lrqmm_debug_small(int op, const float* Y, int64_t n, int W, int r, double* G, float* T,

@@ -32,7 +32,7 @@ EXPORTS = (
     "lrqmm_gemm_int32", "lrqmm_get_factors", "lrqmm_get_correction", "lrqmm_correction_width",
     "lrqmm_get_timings", "lrqmm_launch_count", "lrqmm_status_string",
 )
-DEBUG_EXPORTS = ("lrqmm_debug_proj", "lrqmm_debug_small")
+DEBUG_EXPORTS = ("lrqmm_debug_proj", "lrqmm_debug_small", "lrqmm_debug_set_gemm_variant")
 
 
 class LrqmmError(RuntimeError):
@@ -85,6 +85,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         # test hooks (include/lrqmm_debug.h)
         "lrqmm_debug_proj": (I, [I, P, I64, I64, I, I, I, P, P, I, P, P, P]),
         "lrqmm_debug_small": (I, [I, P, I64, I, I, P, P, P]),
+        "lrqmm_debug_set_gemm_variant": (I, [I]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -15,6 +15,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from paper_2409_18772_b200 import SIDE_A, SIDE_B, Lrqmm, LrqmmError  # noqa: E402
+from paper_2409_18772_b200 import lrqmm as L  # noqa: E402
 
 DEV = "cuda:0"
 TOL_D = 1e-4
@@ -100,10 +101,20 @@ def test_nonfinite_is_reported():
         assert ei.value.code == 5
 
 
-# ------------------------------------------------------------ K6 int GEMM
+# ------------------------------------------------------------ K6 / K7 int GEMM
+@pytest.fixture(params=[1, 2], ids=["gemm1cta", "gemm2cta"])
+def gemm_variant(request):
+    """Runs the test with the one-CTA GEMM (K6) and the CTA-pair GEMM (K7) forced."""
+    lib = L.load_library()
+    assert lib.lrqmm_debug_set_gemm_variant(request.param) == 0
+    yield request.param
+    lib.lrqmm_debug_set_gemm_variant(0)
+
+
 @pytest.mark.parametrize("bits", [4, 8])
-@pytest.mark.parametrize("shape", [(128, 256, 128), (300, 520, 1000), (1024, 768, 4096), (37, 1000, 147)])
-def test_int32_accumulators_bit_exact(bits, shape):
+@pytest.mark.parametrize("shape", [(128, 256, 128), (300, 520, 1000), (1024, 768, 4096), (37, 1000, 147),
+                                   (700, 300, 256), (2304, 2560, 384)])
+def test_int32_accumulators_bit_exact(bits, shape, gemm_variant):
     M, N, K = shape
     A, Bt, _, _ = S.problem(M, N, K, 1, s=2)
     out = run_gpu(A, Bt, bits, 0, 0)
@@ -114,7 +125,7 @@ def test_int32_accumulators_bit_exact(bits, shape):
     assert np.array_equal(out["c_int"].astype(np.int64), O.int_gemm(ca, cb))
 
 
-def test_int32_extreme_values_int8():
+def test_int32_extreme_values_int8(gemm_variant):
     # all codes at +-qmax: the largest |acc| for this K
     M, N, K = 256, 256, 8192
     A = np.ones((M, K), np.float32)
@@ -151,7 +162,7 @@ def test_lrqmm_matches_oracle(bits, dist, shape, r, p):
 
 @pytest.mark.parametrize("q", [1, 2])
 @pytest.mark.parametrize("r,p", [(1, 0), (32, 5), (20, 20)])
-def test_lrqmm_rank_and_power_iters(q, r, p):
+def test_lrqmm_rank_and_power_iters(q, r, p, gemm_variant):
     A, Bt, OmA, OmB = S.problem(320, 300, 640, r + p, s=5, dist="u01")
     ref = O.lrqmm(A, Bt, 4, r, OmA, OmB, q=q)
     check_d(A, Bt, run_gpu(A, Bt, 4, r, p, OmA, OmB, q=q), ref)
@@ -165,7 +176,7 @@ def test_direct_quant_modes_match_oracle():
         assert O.relative_error(ref, out["D"]) <= 1e-6
 
 
-def test_alpha_beta():
+def test_alpha_beta(gemm_variant):
     A, Bt, OmA, OmB = S.problem(256, 256, 384, 13, s=2)
     D0 = np.random.default_rng(0).standard_normal((256, 256)).astype(np.float32)
     ref = O.lrqmm(A, Bt, 4, 8, OmA, OmB, alpha=1.5, beta=-0.5, D=D0)
