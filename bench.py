@@ -37,6 +37,8 @@ CONFIGS = {
     "c2i8": (4096, 4096, 4096, 8, 16, 5, "normal", "square 4096^3 int8 rank 16 (p=5, q=1) Gaussian, configs[1]"),
     "c1": (256, 256, 256, 4, 8, 5, "normal", "square 256^3 int4 rank 8 (p=5, q=1) Gaussian, configs[0]"),
     "c5": (4096, 32768, 32768, 4, 32, 5, "normal", "32768^3 int4 rank 32 row-sharded (4096 rows/rank), configs[4]"),
+    # configs[3]: the 53 ResNet-50 convolutions as im2col GEMMs at batch 256 (synth.resnet50_convs)
+    "c4": (None, None, None, 4, 16, 5, "relu_normal", "ResNet-50 conv layers as im2col GEMMs, batch 256, 4-bit, configs[3]"),
 }
 METRIC = "effective TOPS (2MNK/t) of the LRQMM hot path; overhead vs bare int8 GEMM; rel. Frobenius error vs direct quant"
 REF_ROWS = 256  # oracle row sample per reference / cpu_baseline step
@@ -230,6 +232,73 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------ configs[3]: ResNet-50 suite
+def run_resnet(args, ws, rank, local):
+    """All 53 ResNet-50 convolutions as im2col GEMMs at batch 256 (A: post-ReLU activations,
+    B: Kaiming-normal random-init weights), int4, r = 16, p = 5: per-layer device time of the full
+    LRQMM call sequence, bare int8 GEMM time and error on 64 sampled rows; suite effective TOPS."""
+    import torch
+
+    import synth as S
+    from paper_2409_18772_b200 import SIDE_A, SIDE_B, Lrqmm
+
+    _, _, _, bits, r, p, dist_name, label = CONFIGS["c4"]
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    layers = S.resnet50_convs(256)
+    out, t_all, t_bare_all, ops_all = [], 0.0, 0.0, 0.0
+    steps = max(1, min(args.steps, 5))
+    for li, (name, M, K, N, _) in enumerate(layers):
+        A = S.gen_matrix_torch(dist_name, M, K, 100 + 2 * li + 7919 * rank, device=dev)
+        Bt = S.gen_matrix_torch("normal", N, K, 101 + 2 * li, device=dev, scale=(2.0 / K) ** 0.5)
+        OmA = torch.from_numpy(S.gen_omega(K, r + p, 1000 + 2 * li)).to(dev)
+        OmB = torch.from_numpy(S.gen_omega(K, r + p, 1001 + 2 * li)).to(dev)
+        D = torch.empty((M, N), device=dev)
+        C = torch.empty((M, N), dtype=torch.int32, device=dev)
+        with Lrqmm(M, N, K, bits, r, p, 1, "floor", "row", device=local, stream=stream) as h:
+            def step():
+                h.quantize(SIDE_A, A); h.quantize(SIDE_B, Bt); h.rsvd_residual(OmA, OmB); h.gemm(D)
+            for _ in range(max(args.warmup, 1)):
+                step()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(steps):
+                step()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            t = e0.elapsed_time(e1) / 1e3 / steps
+            h.gemm_int32(C)
+            torch.cuda.synchronize(dev)
+            e0.record(stream)
+            for _ in range(steps):
+                h.gemm_int32(C)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            tb = e0.elapsed_time(e1) / 1e3 / steps
+            step()
+            h.sync()
+            rows = torch.arange(0, M, max(1, M // 64), device=dev)[:64]
+            Cx = A[rows].double() @ Bt.double().T
+            err = float(torch.linalg.norm(D[rows].double() - Cx) / torch.linalg.norm(Cx))
+        ops = 2.0 * M * N * K
+        out.append({"layer": name, "M": M, "K": K, "N": N, "ms": t * 1e3, "bare_int8_ms": tb * 1e3,
+                    "overhead_vs_bare": t / tb, "tops": ops / t / 1e12, "rel_fro_error": err})
+        t_all += t; t_bare_all += tb; ops_all += ops
+        del A, Bt, D, C
+        torch.cuda.empty_cache()
+    if rank == 0:
+        line = {"metric": METRIC, "value": ops_all / t_all / 1e12, "unit": "TOPS", "n_gpus": ws, "steps": steps,
+                "warmup": args.warmup, "ms_per_step": t_all * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "int8", "data": "synthetic (post-ReLU normal activations, Kaiming weights)",
+                "config": {"workload": label, "layers": len(layers), "bits": bits, "rank": r, "oversample": p,
+                           "batch": 256},
+                "overhead_vs_bare_int8": t_all / t_bare_all, "bare_int8_tops": ops_all / t_bare_all / 1e12,
+                "layers": out}
+        print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------ main
 def main():
     args = parse()
@@ -248,6 +317,9 @@ def main():
     import synth as S
     from paper_2409_18772_b200 import SIDE_A, SIDE_B, Lrqmm, get_unique_id
 
+    if args.config == "c4":
+        run_resnet(args, ws, rank, local)
+        return
     cfg = CONFIGS[args.config]
     Mloc, N, K, bits, r, p, dist_name, label = cfg
     kk = r + p

@@ -89,7 +89,7 @@ typedef struct {
 lrqmm_status_t lrqmm_get_unique_id(unsigned char out[128]);
 
 /* Host.  Validates cfg, allocates all device workspace (codes M x Kp and N x Kp int8 with
- * Kp = roundup(K,128), scales, RSVD panels, correction factors), builds the NCCL
+ * Kp = roundup(K,16), scales, RSVD panels, correction factors), builds the NCCL
  * communicator when world_size > 1 (collective across ranks).  Errors: INVALID_ARGUMENT,
  * SHAPE, RANK, OVERFLOW, UNSUPPORTED, ALLOC, CUDA, NCCL. */
 lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out);

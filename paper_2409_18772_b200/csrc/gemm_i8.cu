@@ -744,7 +744,7 @@ void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStre
   G6Params p;
   p.M = g.M;
   p.N = g.N;
-  p.num_kb = g.Kp / g6::BK;
+  p.num_kb = (g.Kp + g6::BK - 1) / g6::BK;  // the last box is zero-filled past Kp
   p.num_m = (int)((g.M + g6::BM - 1) / g6::BM);
   p.num_n = (int)((g.N + g6::BN - 1) / g6::BN);
   p.epi = g.epi;

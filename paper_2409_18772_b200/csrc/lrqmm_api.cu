@@ -194,7 +194,9 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
   h->cfg.nccl_unique_id = nullptr;
   h->st = reinterpret_cast<cudaStream_t>(cfg->stream);
   h->qmax = (1 << (cfg->bits - 1)) - 1;
-  h->Kp = (int)roundup(std::max<int64_t>(cfg->k, 1), 128);
+  // codes / residual-plane row stride: 16-byte multiple (TMA); the kernels' 128-deep boxes read
+  // past it as zeros (out-of-bounds fill), so no 128-column padding is stored
+  h->Kp = (int)roundup(std::max<int64_t>(cfg->k, 1), 16);
   h->r = cfg->rank;
   h->kk = cfg->rank > 0 ? cfg->rank + cfg->oversample : 0;
   h->W = h->kk > 0 ? (int)roundup(h->kk, 8) : 0;
@@ -600,7 +602,7 @@ extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx
                                            int rounding, const float* P, const float* P2, int W, float* OUT,
                                            float* OUT2, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int Kp = (int)roundup(K > 0 ? K : 1, 128);
+  const int Kp = (int)roundup(K > 0 ? K : 1, 16);
   const int64_t ldu = Kp;
   const int64_t pe = (int64_t)16 << 20;
   uint8_t* U = nullptr;

@@ -2,7 +2,7 @@
 // scales; floor rounding of Eq. get_ra2).
 //
 // One side X (rows x K fp32, row stride ldx) -> codes (rows x Kp int8, zero padded
-// to Kp = roundup(K,128)) and lambda (rows fp32).  Each row is read from HBM once:
+// to Kp = roundup(K,16)) and lambda (rows fp32).  Each row is read from HBM once:
 // it stays in registers between the amax reduction and the rounding pass.
 //
 // Bit-exact rounding on the exact product lambda*x (reading #4), on the FMA pipe:

@@ -527,9 +527,24 @@ template <int W>
 __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
   extern __shared__ double dyn[];
   const SmallJob jb = jobs.j[blockIdx.y];
-  double (*sY)[kN + 1] = reinterpret_cast<double (*)[kN + 1]>(dyn);  // kFRows x (kN+1), fp64 (converted once)
+  constexpr int kLd = W + 2;                      // fp64 row stride: 16-byte aligned rows
+  double (*sY)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);  // kFRows x kLd, fp64 (converted once)
   __shared__ int ticket;
-  const int npairs = W * W;
+  constexpr int npairs = W * W;
+  // Gram in 4 x 4 register tiles: tile (a, c), a <= c, of T x T tiles; G row groups per block
+  constexpr int T = W / 4;
+  constexpr int U = T * (T + 1) / 2;
+  constexpr int G = 256 / U;
+  int ta = 0, tc = 0;
+  const int tu = threadIdx.x % U, tg = threadIdx.x / U;
+  const bool gram_thread = threadIdx.x < U * G;
+  {
+    int u = tu;
+    for (int a = 0; a < T; ++a) {
+      if (u < T - a) { ta = a; tc = a + u; break; }
+      u -= T - a;
+    }
+  }
   const int64_t rpb = (jb.n + gridDim.x - 1) / gridDim.x;
   const int64_t r_begin = (int64_t)blockIdx.x * rpb;
   const int64_t r_end = (jb.n < r_begin + rpb) ? jb.n : r_begin + rpb;
@@ -578,27 +593,40 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
       }
     }
     __syncthreads();
+    if (gram_thread) {
+      for (int i = tg; i < nr; i += G) {
+        const double2 x0 = *reinterpret_cast<const double2*>(&sY[i][4 * ta]);
+        const double2 x1 = *reinterpret_cast<const double2*>(&sY[i][4 * ta + 2]);
+        const double2 y0 = *reinterpret_cast<const double2*>(&sY[i][4 * tc]);
+        const double2 y1 = *reinterpret_cast<const double2*>(&sY[i][4 * tc + 2]);
+        const double xa[4] = {x0.x, x0.y, x1.x, x1.y}, yc[4] = {y0.x, y0.y, y1.x, y1.y};
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int pr = threadIdx.x + 256 * q;
-      if (pr < npairs) {
-        const int a = pr / W, c = pr % W;
-        double t0 = 0.0, t1 = 0.0;
-        int i = 0;
-        for (; i + 1 < nr; i += 2) {
-          t0 = fma(sY[i][a], sY[i][c], t0);
-          t1 = fma(sY[i + 1][a], sY[i + 1][c], t1);
-        }
-        if (i < nr) t0 = fma(sY[i][a], sY[i][c], t0);
-        acc[q] += t0 + t1;
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[p * 4 + q] = fma(xa[p], yc[q], acc[p * 4 + q]);
       }
     }
   }
-  double* part = jb.gpart + (int64_t)blockIdx.x * npairs;
+  // fixed-order reduction of the G row groups of each tile, then the block partial (both halves)
+  __syncthreads();
+  double (*red)[16] = reinterpret_cast<double (*)[16]>(dyn);  // (G * U) x 16
+  if (gram_thread)
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int pr = threadIdx.x + 256 * q;
-    if (pr < npairs) part[pr] = acc[q];
+    for (int q = 0; q < 16; ++q) red[tg * U + tu][q] = acc[q];
+  __syncthreads();
+  double* part = jb.gpart + (int64_t)blockIdx.x * npairs;
+  for (int e = threadIdx.x; e < U * 16; e += 256) {
+    const int u = e / 16, q = e % 16;
+    double sum = 0.0;
+    for (int g = 0; g < G; ++g) sum += red[g * U + u][q];
+    int a = 0, c = 0, uu = u;
+    for (int aa = 0; aa < T; ++aa) {
+      if (uu < T - aa) { a = aa; c = aa + uu; break; }
+      uu -= T - aa;
+    }
+    const int i = 4 * a + q / 4, j = 4 * c + q % 4;
+    part[i * W + j] = sum;  // diagonal tiles: (p, q) and (q, p) hold bitwise-equal sums
+    part[j * W + i] = sum;
   }
   __threadfence();
   __syncthreads();
@@ -650,8 +678,9 @@ static void fused_t(const SmallJobs& jobs, int mode, int64_t nb, cudaStream_t st
 void launch_fused_small(const SmallJobs& jobs, int W, int mode, cudaStream_t st) {
   int64_t nmax = 0;
   for (int i = 0; i < jobs.n; ++i) nmax = jobs.j[i].n > nmax ? jobs.j[i].n : nmax;
-  // ~4 row chunks per block keeps the last-block reduction short (<= 64 partials at 16K rows)
+  // ~4 row chunks per block, at most 2 blocks per SM: the last block sums <= 296 partials
   int64_t nb = (nmax + 4 * kFRows - 1) / (4 * kFRows);
+  if (nb > 296) nb = 296;
   if (nb > kGramMaxBlocks) nb = kGramMaxBlocks;
   if (nb < 1) nb = 1;
   switch (W) {
