@@ -38,7 +38,8 @@ CONFIGS = {
     "c1": (256, 256, 256, 4, 8, 5, "normal", "square 256^3 int4 rank 8 (p=5, q=1) Gaussian, configs[0]"),
     "c5": (4096, 32768, 32768, 4, 32, 5, "normal", "32768^3 int4 rank 32 row-sharded (4096 rows/rank), configs[4]"),
     # configs[3]: the 53 ResNet-50 convolutions as im2col GEMMs at batch 256 (synth.resnet50_convs)
-    "c4": (None, None, None, 4, 16, 5, "relu_normal", "ResNet-50 conv layers as im2col GEMMs, batch 256, 4-bit, configs[3]"),
+    "c4": (None, None, None, 4, 20, 5, "relu_normal",
+           "ResNet-50 conv layers as im2col GEMMs, batch 256, 4-bit, rank 20 (PAPER.md:822), configs[3]"),
 }
 METRIC = "effective TOPS (2MNK/t) of the LRQMM hot path; overhead vs bare int8 GEMM; rel. Frobenius error vs direct quant"
 REF_ROWS = 256  # oracle row sample per reference / cpu_baseline step
@@ -232,6 +233,30 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------ HBM roofline inputs
+def hbm_peak() -> float:
+    peaks, _ = load_peaks()
+    return float(peaks["hbm_gbs"])
+
+
+def hbm_bytes_quantize(rows: int, K: int, rank: bool) -> float:
+    """Algorithmic HBM bytes of K1 per side: read x (4 B), write codes (1 B) and, with rank > 0, the
+    Q15 residual planes (2 B) per element."""
+    return rows * K * (4 + 1 + (2 if rank else 0))
+
+
+def hbm_bytes_rsvd(rows: int, K: int) -> float:
+    """Algorithmic HBM bytes of one side's three RSVD passes: S1 and S2 stream the 2-byte residual,
+    S3 the residual + the 1-byte codes (the sketch panels are L2-sized at these shapes)."""
+    return rows * K * (2 + 2 + 3)
+
+
+def hbm_bytes_step(M: int, N: int, K: int, k: int) -> float:
+    """Whole-step algorithmic HBM bytes: quantize + RSVD both sides, GEMM operands + fp32 D."""
+    return (hbm_bytes_quantize(M, K, True) + hbm_bytes_quantize(N, K, True) + hbm_bytes_rsvd(M, K)
+            + hbm_bytes_rsvd(N, K) + (M + N) * K + 4.0 * M * N)
+
+
 # ------------------------------------------------------ configs[3]: ResNet-50 suite
 def run_resnet(args, ws, rank, local):
     """All 53 ResNet-50 convolutions as im2col GEMMs at batch 256 (A: post-ReLU activations,
@@ -247,7 +272,7 @@ def run_resnet(args, ws, rank, local):
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
     layers = S.resnet50_convs(256)
-    out, t_all, t_bare_all, ops_all = [], 0.0, 0.0, 0.0
+    out, t_all, t_bare_all, ops_all, hbm_all = [], 0.0, 0.0, 0.0, 0.0
     steps = max(1, min(args.steps, 5))
     for li, (name, M, K, N, _) in enumerate(layers):
         A = S.gen_matrix_torch(dist_name, M, K, 100 + 2 * li + 7919 * rank, device=dev)
@@ -283,9 +308,11 @@ def run_resnet(args, ws, rank, local):
             Cx = A[rows].double() @ Bt.double().T
             err = float(torch.linalg.norm(D[rows].double() - Cx) / torch.linalg.norm(Cx))
         ops = 2.0 * M * N * K
+        hbm = hbm_bytes_step(M, N, K, r + p)
         out.append({"layer": name, "M": M, "K": K, "N": N, "ms": t * 1e3, "bare_int8_ms": tb * 1e3,
-                    "overhead_vs_bare": t / tb, "tops": ops / t / 1e12, "rel_fro_error": err})
-        t_all += t; t_bare_all += tb; ops_all += ops
+                    "overhead_vs_bare": t / tb, "tops": ops / t / 1e12, "rel_fro_error": err,
+                    "hbm_gbs": hbm / t / 1e9, "hbm_frac": hbm / t / 1e9 / hbm_peak()})
+        t_all += t; t_bare_all += tb; ops_all += ops; hbm_all += hbm
         del A, Bt, D, C
         torch.cuda.empty_cache()
     if rank == 0:
@@ -295,6 +322,9 @@ def run_resnet(args, ws, rank, local):
                 "config": {"workload": label, "layers": len(layers), "bits": bits, "rank": r, "oversample": p,
                            "batch": 256},
                 "overhead_vs_bare_int8": t_all / t_bare_all, "bare_int8_tops": ops_all / t_bare_all / 1e12,
+                "hbm_roofline": {"bytes": hbm_all, "gbs": hbm_all / t_all / 1e9, "peak_gbs": hbm_peak(),
+                                 "frac": hbm_all / t_all / 1e9 / hbm_peak(),
+                                 "note": "algorithmic bytes of the whole LRQMM call per layer (bench.hbm_bytes_step)"},
                 "layers": out}
         print(json.dumps(line), flush=True)
 
@@ -514,9 +544,18 @@ def main():
                      "peak_note": f"int8 dense = 2 x {peak_src} bf16 burst ({peaks['bf16_tflops']} TFLOP/s; guide nominal "
                                   "ratio 4.5/2.25); the bf16 sustained figure is power-capped below this "
                                   "kernel's clock"},
+        "hbm_roofline": {
+            "peak_gbs": hbm_peak(), "peak_note": "MEASURED_PEAKS.json hbm_gbs (copy)",
+            "quantize_AB": {"bytes": hbm_bytes_quantize(Mloc, K, r > 0) + hbm_bytes_quantize(N, K, r > 0),
+                            "gbs": (hbm_bytes_quantize(Mloc, K, r > 0) + hbm_bytes_quantize(N, K, r > 0)) / t_quant / 1e9},
+            "rsvd_residual": {"bytes": hbm_bytes_rsvd(Mloc, K) + hbm_bytes_rsvd(N, K),
+                              "gbs": (hbm_bytes_rsvd(Mloc, K) + hbm_bytes_rsvd(N, K)) / t_rsvd / 1e9},
+        },
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    for ph in ("quantize_AB", "rsvd_residual"):
+        line["hbm_roofline"][ph]["frac"] = line["hbm_roofline"][ph]["gbs"] / line["hbm_roofline"]["peak_gbs"]
     if cpu:
         line["cpu_baseline"] = cpu
     if e2e:
