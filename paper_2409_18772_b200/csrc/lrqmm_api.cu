@@ -65,6 +65,13 @@ struct lrqmm_handle_s {
   alignas(64) CUtensorMap mapB[2];
   cudaEvent_t ev[8] = {};
   ncclComm_t comm = nullptr;
+  // rsvd_residual as a CUDA graph: captured once on a private stream (the caller's stream may be
+  // the legacy default stream, which cannot be captured), then launched onto the caller's stream
+  cudaStream_t cap_st = nullptr;
+  cudaGraphExec_t rsvd_exec = nullptr;
+  int rsvd_calls = 0;
+  int64_t rsvd_graph_kernels = 0;
+  bool graph_off = false;
   // run_host buffers
   float *hA = nullptr, *hB = nullptr, *hOmA = nullptr, *hOmB = nullptr, *hD = nullptr;
 };
@@ -171,6 +178,8 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   cudaFree(h->hA); cudaFree(h->hB); cudaFree(h->hOmA); cudaFree(h->hOmB); cudaFree(h->hD);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
+  if (h->rsvd_exec) cudaGraphExecDestroy(h->rsvd_exec);
+  if (h->cap_st) cudaStreamDestroy(h->cap_st);
   if (h->comm) ncclCommDestroy(h->comm);
   delete h;
   return LRQMM_OK;
@@ -364,22 +373,11 @@ static lrqmm_status_t gram_step(lrqmm_handle_t h, float* const Y[2], const int64
   return check_launch(h);
 }
 
-lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const float* omegaB, int64_t ldo) {
-  if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
-  if (h->sticky != LRQMM_OK) return h->sticky;
-  if (h->r == 0) return LRQMM_ERR_STATE;
-  if ((h->state & 3) != 3) return LRQMM_ERR_STATE;
-  if (!omegaA || !omegaB || ldo < h->kk) return LRQMM_ERR_INVALID_ARGUMENT;
-  cudaSetDevice(h->cfg.device);
+// Everything after the Omega copy: ~30 launches on handle-owned buffers only (graph-capturable).
+static lrqmm_status_t rsvd_body(lrqmm_handle_t h) {
   const int W = h->W;
   const int64_t K = h->cfg.k;
   const bool multi = h->cfg.world_size > 1;
-  record(h, 4);
-  // sketch Omega (K x kk, caller layout) -> zero-padded K x W
-  const float* om[2] = {omegaA, omegaB};
-  for (int sd = 0; sd < 2; ++sd)
-    LQ_CUDA(cudaMemcpy2DAsync(h->s[sd].Om, sizeof(float) * W, om[sd], sizeof(float) * ldo, sizeof(float) * h->kk, K,
-                              cudaMemcpyDeviceToDevice, h->st));
   const int64_t rows[2] = {h->s[0].rows, h->s[1].rows};
   const int64_t kdim[2] = {K, K};
   float* Ys[2] = {h->s[0].Y, h->s[1].Y};
@@ -436,6 +434,62 @@ lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const 
   launch_apply_small(h->s[0].Gp, h->s[1].VW, nullptr, nullptr, rows[0], W, W, r, h->LA, h->R2, r, h->st);   // A~ V_B
   launch_apply_small(h->s[1].Gp, h->s[0].VW, YB, h->VWbM, rows[1], W, W, r, h->LB, h->R2, 0, h->st);        // B~^T V_A + U_B S_B M
   launch_apply_small(YB, h->s[1].VW, nullptr, nullptr, rows[1], W, W, r, h->LB, h->R2, r, h->st);           // U_B S_B
+  return check_launch(h);
+}
+
+
+lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const float* omegaB, int64_t ldo) {
+  if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (h->sticky != LRQMM_OK) return h->sticky;
+  if (h->r == 0) return LRQMM_ERR_STATE;
+  if ((h->state & 3) != 3) return LRQMM_ERR_STATE;
+  if (!omegaA || !omegaB || ldo < h->kk) return LRQMM_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(h->cfg.device);
+  const int W = h->W;
+  const int64_t K = h->cfg.k;
+  const bool multi = h->cfg.world_size > 1;
+  record(h, 4);
+  // sketch Omega (K x kk, caller layout) -> zero-padded K x W
+  const float* om[2] = {omegaA, omegaB};
+  for (int sd = 0; sd < 2; ++sd)
+    LQ_CUDA(cudaMemcpy2DAsync(h->s[sd].Om, sizeof(float) * W, om[sd], sizeof(float) * ldo, sizeof(float) * h->kk, K,
+                              cudaMemcpyDeviceToDevice, h->st));
+  lrqmm_status_t e = LRQMM_OK;
+  // graphs: single-rank handles (NCCL collectives stay eagerly enqueued), not disabled by env
+  const bool use_graph = !h->graph_off && !multi && !getenv("LRQMM_NO_GRAPH");
+  if (h->rsvd_exec) {
+    LQ_CUDA(cudaGraphLaunch(h->rsvd_exec, h->st));
+    launch_counter() += h->rsvd_graph_kernels;
+  } else if (use_graph && h->rsvd_calls >= 1) {
+    // capture on the private stream (function attributes were set by the eager first call)
+    if (!h->cap_st && cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking) != cudaSuccess) h->graph_off = true;
+    cudaGraph_t g = nullptr;
+    bool ok = !h->graph_off && cudaStreamBeginCapture(h->cap_st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      const int64_t k0 = launch_counter();
+      cudaStream_t user = h->st;
+      h->st = h->cap_st;
+      e = rsvd_body(h);
+      h->st = user;
+      h->rsvd_graph_kernels = launch_counter() - k0;
+      launch_counter() = k0;
+      ok = cudaStreamEndCapture(h->cap_st, &g) == cudaSuccess && e == LRQMM_OK && g != nullptr &&
+           cudaGraphInstantiate(&h->rsvd_exec, g, 0) == cudaSuccess;
+      if (g) cudaGraphDestroy(g);
+    }
+    cudaGetLastError();  // a failed capture must not leave a sticky launch error behind
+    if (ok) {
+      LQ_CUDA(cudaGraphLaunch(h->rsvd_exec, h->st));
+      launch_counter() += h->rsvd_graph_kernels;
+    } else {
+      h->graph_off = true;
+      if (h->rsvd_exec) { cudaGraphExecDestroy(h->rsvd_exec); h->rsvd_exec = nullptr; }
+      if ((e = rsvd_body(h)) != LRQMM_OK) return e;
+    }
+  } else {
+    if ((e = rsvd_body(h)) != LRQMM_OK) return e;
+  }
+  ++h->rsvd_calls;
   record(h, 5);
   if ((e = check_launch(h)) != LRQMM_OK) return e;
   h->state |= 4;

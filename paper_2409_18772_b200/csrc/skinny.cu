@@ -8,53 +8,82 @@ namespace lrqmm {
 [[maybe_unused]] static int clamp_grid(int64_t want) { return (int)(want < 148 * 32 ? (want < 1 ? 1 : want) : 148 * 32); }
 
 // ----------------------------------------------------- small right-multiplies
-// One thread per row: the row's W inputs in registers, the small matrix broadcast from shared
-// memory (every lane reads the same element), all outputs of the row accumulated in registers.
+// Blocks of 128 rows: the rows are staged through shared memory with coalesced 16-byte loads,
+// each thread then multiplies ITS row (in registers) by the small matrix (broadcast from shared
+// memory), and the results go back through shared memory to coalesced stores.
+constexpr int kApRows = 128;
+// staging row stride in floats for W columns: W + 4 keeps per-thread 16-byte row reads
+// conflict-free (8 consecutive threads hit 8 distinct 16-byte bank groups)
+__host__ __device__ constexpr int ap_ld(int w) { return w + 4; }
+
+template <int W>
+LRQMM_DEV void stage_rows_in(const float* __restrict__ src, int64_t i0, int nr, float* sm) {
+  constexpr int L = ap_ld(W);
+  const float4* s4 = reinterpret_cast<const float4*>(src + i0 * W);
+  for (int e = threadIdx.x; e < nr * (W / 4); e += blockDim.x) {
+    const int r = e / (W / 4), c = e % (W / 4);
+    *reinterpret_cast<float4*>(sm + r * L + 4 * c) = __ldg(s4 + e);
+  }
+}
+
 // OUT[i, col0 + o] = sum_c IN1[i,c] S1[c,o] (+ sum_c IN2[i,c] S2[c,o]),  o < nout (<= W)
 template <int W>
-__global__ void __launch_bounds__(128) k_apply_small(const float* __restrict__ IN1, const float* __restrict__ S1,
-                                                     const float* __restrict__ IN2, const float* __restrict__ S2,
-                                                     int64_t n, int ldS, int nout, float* __restrict__ OUT,
-                                                     int64_t ldo, int col0) {
-  __shared__ float s1[W * W];
-  __shared__ float s2[W * W];
+__global__ void __launch_bounds__(kApRows) k_apply_small(const float* __restrict__ IN1, const float* __restrict__ S1,
+                                                         const float* __restrict__ IN2, const float* __restrict__ S2,
+                                                         int64_t n, int ldS, int nout, float* __restrict__ OUT,
+                                                         int64_t ldo, int col0) {
+  constexpr int L = ap_ld(W);
+  extern __shared__ __align__(16) float apsm[];
+  float* sin1 = apsm;                    // kApRows x L
+  float* sin2 = sin1 + kApRows * L;      // kApRows x L
+  float* s1 = sin2 + kApRows * L;        // W x W
+  float* s2 = s1 + W * W;                // W x W
   for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
     const int c = e / W, o = e % W;
     s1[e] = o < nout ? S1[c * ldS + o] : 0.f;
     s2[e] = (IN2 && o < nout) ? S2[c * ldS + o] : 0.f;
   }
-  __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float x[W];
-    const float4* r1 = reinterpret_cast<const float4*>(IN1 + i * W);
-#pragma unroll
-    for (int c = 0; c < W / 4; ++c) {
-      const float4 v = __ldg(r1 + c);
-      x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
-    }
+  for (int64_t i0 = (int64_t)blockIdx.x * kApRows; i0 < n; i0 += (int64_t)gridDim.x * kApRows) {
+    const int nr = (int)(n - i0 < kApRows ? n - i0 : kApRows);
+    __syncthreads();
+    stage_rows_in<W>(IN1, i0, nr, sin1);
+    if (IN2) stage_rows_in<W>(IN2, i0, nr, sin2);
+    __syncthreads();
     float acc[W];
 #pragma unroll
     for (int o = 0; o < W; ++o) acc[o] = 0.f;
+    if (threadIdx.x < nr) {
 #pragma unroll
-    for (int c = 0; c < W; ++c)
+      for (int c4 = 0; c4 < W / 4; ++c4) {
+        const float4 v = *reinterpret_cast<const float4*>(sin1 + threadIdx.x * L + 4 * c4);
+        const float xs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int o = 0; o < W; ++o) acc[o] = fmaf(x[c], s1[c * W + o], acc[o]);
-    if (IN2) {
-      const float4* r2 = reinterpret_cast<const float4*>(IN2 + i * W);
+        for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int c = 0; c < W / 4; ++c) {
-        const float4 v = __ldg(r2 + c);
-        x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
+          for (int o = 0; o < W; ++o) acc[o] = fmaf(xs[j], s1[(4 * c4 + j) * W + o], acc[o]);
       }
+      if (IN2) {
 #pragma unroll
-      for (int c = 0; c < W; ++c)
+        for (int c4 = 0; c4 < W / 4; ++c4) {
+          const float4 v = *reinterpret_cast<const float4*>(sin2 + threadIdx.x * L + 4 * c4);
+          const float xs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int o = 0; o < W; ++o) acc[o] = fmaf(x[c], s2[c * W + o], acc[o]);
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int o = 0; o < W; ++o) acc[o] = fmaf(xs[j], s2[(4 * c4 + j) * W + o], acc[o]);
+        }
+      }
     }
-    float* out = OUT + i * ldo + col0;
+    __syncthreads();  // sin1 is reused as the output staging buffer
+    if (threadIdx.x < nr) {
 #pragma unroll
-    for (int o = 0; o < W; ++o)
-      if (o < nout) out[o] = acc[o];
+      for (int o = 0; o < W; ++o) sin1[threadIdx.x * L + o] = acc[o];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * nout; e += blockDim.x) {
+      const int r = e / nout, o = e % nout;
+      OUT[(i0 + r) * ldo + col0 + o] = sin1[r * L + o];
+    }
   }
 }
 
@@ -63,53 +92,84 @@ static int grid_rows(int64_t n, int per) {
   return (int)(want < 148 * 16 ? (want < 1 ? 1 : want) : 148 * 16);
 }
 
+template <int W>
+static void apply_small_t(const float* IN1, const float* S1, const float* IN2, const float* S2, int64_t n, int ldS,
+                          int nout, float* OUT, int64_t ldo, int col0, cudaStream_t st) {
+  constexpr int smem = (2 * kApRows * ap_ld(W) + 2 * W * W) * (int)sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_apply_small<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  k_apply_small<W><<<grid_rows(n, kApRows), kApRows, smem, st>>>(IN1, S1, IN2, S2, n, ldS, nout, OUT, ldo, col0);
+}
+
 void launch_apply_small(const float* IN1, const float* S1, const float* IN2, const float* S2, int64_t n, int W,
                         int ldS, int nout, float* OUT, int64_t ldo, int col0, cudaStream_t st) {
   if (n == 0 || nout == 0) return;
-  const int g = grid_rows(n, 128);
-#define AS_CASE(w) \
-  case w: k_apply_small<w><<<g, 128, 0, st>>>(IN1, S1, IN2, S2, n, ldS, nout, OUT, ldo, col0); break;
+#define AS_CASE(w) case w: apply_small_t<w>(IN1, S1, IN2, S2, n, ldS, nout, OUT, ldo, col0, st); break;
   switch (W) { AS_CASE(8) AS_CASE(16) AS_CASE(24) AS_CASE(32) AS_CASE(40) AS_CASE(48) AS_CASE(56) AS_CASE(64) default: break; }
 #undef AS_CASE
   ++launch_counter();
 }
 
 // OUT = IN S with S in fp64 and fp64 accumulation (orthonormalisation: keeps Q orthonormal to
-// fp32 rounding instead of cond(IN) * eps32).  One thread per row, as above.
+// fp32 rounding instead of cond(IN) * eps32).  Same staging as above.
 template <int W>
-__global__ void __launch_bounds__(128) k_apply64(const float* __restrict__ IN, const double* __restrict__ S, int64_t n,
-                                                 float* __restrict__ OUT) {
-  __shared__ double s[W * W];
+__global__ void __launch_bounds__(kApRows) k_apply64(const float* __restrict__ IN, const double* __restrict__ S, int64_t n,
+                                                     float* __restrict__ OUT) {
+  constexpr int L = ap_ld(W);
+  extern __shared__ __align__(16) double apsm64[];
+  double* s = apsm64;                                      // W x W
+  float* sin = reinterpret_cast<float*>(apsm64 + W * W);   // kApRows x L
   for (int e = threadIdx.x; e < W * W; e += blockDim.x) s[e] = S[e];
-  __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float x[W];
-    const float4* r = reinterpret_cast<const float4*>(IN + i * W);
-#pragma unroll
-    for (int c = 0; c < W / 4; ++c) {
-      const float4 v = __ldg(r + c);
-      x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
-    }
+  for (int64_t i0 = (int64_t)blockIdx.x * kApRows; i0 < n; i0 += (int64_t)gridDim.x * kApRows) {
+    const int nr = (int)(n - i0 < kApRows ? n - i0 : kApRows);
+    __syncthreads();
+    stage_rows_in<W>(IN, i0, nr, sin);
+    __syncthreads();
     double acc[W];
 #pragma unroll
     for (int o = 0; o < W; ++o) acc[o] = 0.0;
+    if (threadIdx.x < nr) {
 #pragma unroll
-    for (int c = 0; c < W; ++c) {
-      const double xc = (double)x[c];
+      for (int c4 = 0; c4 < W / 4; ++c4) {
+        const float4 v = *reinterpret_cast<const float4*>(sin + threadIdx.x * L + 4 * c4);
+        const double xs[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
 #pragma unroll
-      for (int o = 0; o < W; ++o) acc[o] = fma(xc, s[c * W + o], acc[o]);
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int o = 0; o < W; ++o) acc[o] = fma(xs[j], s[(4 * c4 + j) * W + o], acc[o]);
+      }
     }
-    float4* out = reinterpret_cast<float4*>(OUT + i * W);
+    __syncthreads();
+    if (threadIdx.x < nr) {
 #pragma unroll
-    for (int c = 0; c < W / 4; ++c)
-      out[c] = make_float4((float)acc[4 * c], (float)acc[4 * c + 1], (float)acc[4 * c + 2], (float)acc[4 * c + 3]);
+      for (int o = 0; o < W; ++o) sin[threadIdx.x * L + o] = (float)acc[o];
+    }
+    __syncthreads();
+    float4* o4 = reinterpret_cast<float4*>(OUT + i0 * W);
+    for (int e = threadIdx.x; e < nr * (W / 4); e += blockDim.x) {
+      const int r = e / (W / 4), c = e % (W / 4);
+      o4[e] = *reinterpret_cast<const float4*>(sin + r * L + 4 * c);
+    }
   }
+}
+
+template <int W>
+static void apply64_t(const float* IN, const double* S, int64_t n, float* OUT, cudaStream_t st) {
+  constexpr int smem = W * W * (int)sizeof(double) + kApRows * ap_ld(W) * (int)sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_apply64<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  k_apply64<W><<<grid_rows(n, kApRows), kApRows, smem, st>>>(IN, S, n, OUT);
 }
 
 void launch_apply64(const float* IN, const double* S, int64_t n, int W, float* OUT, cudaStream_t st) {
   if (n == 0) return;
-  const int g = grid_rows(n, 128);
-#define A64_CASE(w) case w: k_apply64<w><<<g, 128, 0, st>>>(IN, S, n, OUT); break;
+#define A64_CASE(w) case w: apply64_t<w>(IN, S, n, OUT, st); break;
   switch (W) { A64_CASE(8) A64_CASE(16) A64_CASE(24) A64_CASE(32) A64_CASE(40) A64_CASE(48) A64_CASE(56) A64_CASE(64) default: break; }
 #undef A64_CASE
   ++launch_counter();

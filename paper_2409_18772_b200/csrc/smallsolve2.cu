@@ -522,9 +522,11 @@ __global__ void __launch_bounds__(32) k_warp_chol(EigJobs jobs) {
 //   phase 2 (last block by ticket): fixed-order sum of the Gram partials -> G, then the
 //                         pivoted CholQR transform (mode 0) or the truncation eigenvectors
 //                         (mode 1), or nothing (mode 2: G must first be summed across ranks).
-constexpr int kFRows = 64;
+// rows per shared-memory chunk: as many as the 66.5 KB dynamic buffer holds in fp64
+__host__ __device__ constexpr int frows(int w) { return w <= 24 ? 256 : (w <= 48 ? 128 : 64); }
 template <int W>
 __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
+  constexpr int kFRows = frows(W);
   extern __shared__ double dyn[];
   const SmallJob jb = jobs.j[blockIdx.y];
   constexpr int kLd = W + 2;                      // fp64 row stride: 16-byte aligned rows
@@ -678,8 +680,9 @@ static void fused_t(const SmallJobs& jobs, int mode, int64_t nb, cudaStream_t st
 void launch_fused_small(const SmallJobs& jobs, int W, int mode, cudaStream_t st) {
   int64_t nmax = 0;
   for (int i = 0; i < jobs.n; ++i) nmax = jobs.j[i].n > nmax ? jobs.j[i].n : nmax;
-  // ~4 row chunks per block, at most 2 blocks per SM: the last block sums <= 296 partials
-  int64_t nb = (nmax + 4 * kFRows - 1) / (4 * kFRows);
+  // ~2 row chunks per block, at most 2 blocks per SM: the last block sums <= 296 partials
+  const int fr = frows(W);
+  int64_t nb = (nmax + 2 * fr - 1) / (2 * fr);
   if (nb > 296) nb = 296;
   if (nb > kGramMaxBlocks) nb = kGramMaxBlocks;
   if (nb < 1) nb = 1;

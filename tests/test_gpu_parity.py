@@ -212,3 +212,20 @@ def test_run_host_e2e_matches_device_path():
     with Lrqmm(256, 192, 320, 4, 8, 5) as h:
         h.run_host(A, Bt, np.ascontiguousarray(OmA[:, :13]), np.ascontiguousarray(OmB[:, :13]), D)
     assert O.relative_error(ref, D) <= TOL_D
+
+
+def test_repeated_calls_reuse_handle():
+    """One handle, four calls with different A, B^T and Omega: the second call captures the RSVD
+    as a CUDA graph, the later ones replay it (lrqmm_api.cu); every call must match the oracle."""
+    M, N, K, r, p = 384, 320, 768, 8, 5
+    with Lrqmm(M, N, K, 4, r, p) as h:
+        for call in range(4):
+            A, Bt, OmA, OmB = S.problem(M, N, K, r + p, s=20 + call, dist=["normal", "u01", "exp4", "normal"][call])
+            ref = O.lrqmm(A, Bt, 4, r, OmA, OmB, q=1)
+            h.quantize(SIDE_A, cu(A))
+            h.quantize(SIDE_B, cu(Bt))
+            h.rsvd_residual(cu(OmA), cu(OmB))
+            D = torch.empty((M, N), device=DEV)
+            h.gemm(D)
+            h.sync()
+            check_d(A, Bt, {"D": D.cpu().numpy().astype(np.float64)}, ref)
