@@ -106,8 +106,18 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
  * correction factors L_A = [U_A S_A | A_F V_B], L_B = [B_F^T V_A + U_B S_B (V_B^T V_A) | U_B S_B]
  * (Alg. 2).  omegaA / omegaB: k x (r+p) fp32 sketches (ld ldo >= r+p), the
  * Gaussian test matrices of Algorithm 1, supplied by the caller so that a
- * CPU reference can use the same draws.  Requires rank > 0 and both sides quantized. */
+ * CPU reference can use the same draws.  Requires rank > 0 and both sides quantized.
+ * Static-B (weight-resident) mode: omegaB == NULL reuses B's RSVD factors computed by
+ * lrqmm_rsvd_residual_b (or by the last full call for the same quantized B) and runs only the
+ * A side plus the one A-dependent B term B_F^T V_A (a pass over B's codes); the result is the
+ * same correction as a full call with that omegaB.  STATE if B's factors are not resident.
+ * Repeated calls on a handle are replayed from a CUDA graph captured on the second call. */
 lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const float* omegaB, int64_t ldo);
+
+/* Static-B preparation: RSVD of B's residual only (range finder, W_B = R_B Q1_B, truncation),
+ * kept resident in the handle until B is quantized again.  omegaB as above.  Requires rank > 0
+ * and B quantized.  SURVEY §8(f) f2 ("B broadcast once" / weights deployment). */
+lrqmm_status_t lrqmm_rsvd_residual_b(lrqmm_handle_t h, const float* omegaB, int64_t ldo);
 
 /* D = alpha * (C_int / (lambda_A lambda_B) + L_A L_B^T) + beta * D  (Alg. 2,
  * 369, 372), one tcgen05 int8 GEMM with the correction in its epilogue.  D is m x n (ld ldd);

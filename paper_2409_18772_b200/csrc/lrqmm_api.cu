@@ -68,9 +68,9 @@ struct lrqmm_handle_s {
   // rsvd_residual as a CUDA graph: captured once on a private stream (the caller's stream may be
   // the legacy default stream, which cannot be captured), then launched onto the caller's stream
   cudaStream_t cap_st = nullptr;
-  cudaGraphExec_t rsvd_exec = nullptr;
-  int rsvd_calls = 0;
-  int64_t rsvd_graph_kernels = 0;
+  cudaGraphExec_t rsvd_exec[3] = {};  // per rsvd_body kind
+  int rsvd_calls[3] = {};
+  int64_t rsvd_graph_kernels[3] = {};
   bool graph_off = false;
   // run_host buffers
   float *hA = nullptr, *hB = nullptr, *hOmA = nullptr, *hOmB = nullptr, *hD = nullptr;
@@ -178,7 +178,8 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   cudaFree(h->hA); cudaFree(h->hB); cudaFree(h->hOmA); cudaFree(h->hOmB); cudaFree(h->hD);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
-  if (h->rsvd_exec) cudaGraphExecDestroy(h->rsvd_exec);
+  for (auto& x : h->rsvd_exec)
+    if (x) cudaGraphExecDestroy(x);
   if (h->cap_st) cudaStreamDestroy(h->cap_st);
   if (h->comm) ncclCommDestroy(h->comm);
   delete h;
@@ -312,6 +313,7 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
   if (e != LRQMM_OK) return e;
   h->state |= (side == LRQMM_SIDE_A ? 1 : 2);
   h->state &= ~4;
+  if (side == LRQMM_SIDE_B) h->state &= ~8;  // resident B factors belong to the previous B
   return LRQMM_OK;
 }
 
@@ -349,32 +351,37 @@ static int64_t part_elems(lrqmm_handle_t h) { return h->partial_elems / 2; }
 // After a skinny pass left Y_s as nsp[s] split partials: Y = sum(partials), G = Y^T Y, then
 // mode 0: CholQR transform T64 -> Q = Y T64 (fp64 accumulation); mode 1: truncation VW.
 // On a row-sharded A (world > 1, a_sharded) G_A is summed across ranks before the solve.
+// sides: bit 0 = A, bit 1 = B
 static lrqmm_status_t gram_step(lrqmm_handle_t h, float* const Y[2], const int64_t n[2], const int nsp[2], int mode,
-                                float* const Q[2], bool a_sharded) {
+                                float* const Q[2], bool a_sharded, int sides = 3) {
   const int W = h->W;
-  const bool ranks = a_sharded && h->cfg.world_size > 1;
+  const bool ranks = a_sharded && h->cfg.world_size > 1 && (sides & 1);
   SmallJobs j{};
-  j.n = 2;
+  j.n = 0;
   for (int sd = 0; sd < 2; ++sd)
-    j.j[sd] = SmallJob{Y[sd], part_of(h, sd), nsp[sd], n[sd], h->s[sd].G, h->s[sd].gpart, h->s[sd].counter,
-                       h->s[sd].T64, h->s[sd].VW, h->r};
+    if (sides & (1 << sd))
+      j.j[j.n++] = SmallJob{Y[sd], part_of(h, sd), nsp[sd], n[sd], h->s[sd].G, h->s[sd].gpart, h->s[sd].counter,
+                            h->s[sd].T64, h->s[sd].VW, h->r};
   launch_fused_small(j, W, ranks ? 2 : mode, h->st);
   if (ranks) {
     lrqmm_status_t e = allreduce_f64(h, h->s[0].G, (size_t)W * W);
     if (e != LRQMM_OK) return e;
     EigJobs ej{};
-    ej.n = 2;
-    for (int sd = 0; sd < 2; ++sd) ej.j[sd] = EigJob{h->s[sd].G, h->s[sd].VW, h->s[sd].T64, h->r};
+    ej.n = 0;
+    for (int sd = 0; sd < 2; ++sd)
+      if (sides & (1 << sd)) ej.j[ej.n++] = EigJob{h->s[sd].G, h->s[sd].VW, h->s[sd].T64, h->r};
     if (mode == 0) launch_chol_orth(ej, W, h->st);
     else launch_eig_warp(ej, W, h->st);
   }
   if (mode == 0)
-    for (int sd = 0; sd < 2; ++sd) launch_apply64(Y[sd], h->s[sd].T64, n[sd], W, Q[sd], h->st);
+    for (int sd = 0; sd < 2; ++sd)
+      if (sides & (1 << sd)) launch_apply64(Y[sd], h->s[sd].T64, n[sd], W, Q[sd], h->st);
   return check_launch(h);
 }
 
-// Everything after the Omega copy: ~30 launches on handle-owned buffers only (graph-capturable).
-static lrqmm_status_t rsvd_body(lrqmm_handle_t h) {
+// Range finder of the selected sides (Algorithm 1 with q power steps, reading #11):
+// S1 Y = R Omega; q x [O1 Q0 = orth(Y); S2 Z = R^T Q0; O2 Q1 = orth(Z)].  Leaves Q1 (K x W).
+static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides) {
   const int W = h->W;
   const int64_t K = h->cfg.k;
   const bool multi = h->cfg.world_size > 1;
@@ -384,40 +391,43 @@ static lrqmm_status_t rsvd_body(lrqmm_handle_t h) {
   float* Q0s[2] = {h->s[0].Q0, h->s[1].Q0};
   float* Zs[2] = {h->s[0].Z, h->s[1].Z};
   float* Q1s[2] = {h->s[0].Q1, h->s[1].Q1};
-  int nsp[2];
+  int nsp[2] = {1, 1};
   lrqmm_status_t e;
   // S1: Y = R Omega   (Algorithm 1 sampling)
   for (int sd = 0; sd < 2; ++sd)
-    nsp[sd] = launch_tc_proj_rows(view(h, sd), h->s[sd].Om, Ys[sd], nullptr, nullptr, W, part_of(h, sd),
-                                  part_elems(h), false, h->s[sd].img, h->st);
+    if (sides & (1 << sd))
+      nsp[sd] = launch_tc_proj_rows(view(h, sd), h->s[sd].Om, Ys[sd], nullptr, nullptr, W, part_of(h, sd),
+                                    part_elems(h), false, h->s[sd].img, h->st);
   for (int it = 0; it < h->cfg.power_iters; ++it) {
     // O1: Q0 = orth(Y)   (Y rows of A are sharded across ranks)
-    if ((e = gram_step(h, Ys, rows, nsp, 0, Q0s, true)) != LRQMM_OK) return e;
+    if ((e = gram_step(h, Ys, rows, nsp, 0, Q0s, true, sides)) != LRQMM_OK) return e;
     // S2: Z = R^T Q0  (reduction over rows; the A side is summed over ranks before its Gram)
     for (int sd = 0; sd < 2; ++sd)
-      nsp[sd] = launch_tc_proj_cols(view(h, sd), Q0s[sd], Zs[sd], W, part_of(h, sd), part_elems(h), multi,
+      if (sides & (1 << sd))
+        nsp[sd] = launch_tc_proj_cols(view(h, sd), Q0s[sd], Zs[sd], W, part_of(h, sd), part_elems(h), multi,
                                       h->s[sd].img, h->st);
     if (multi) {
-      if ((e = allreduce_f32(h, Zs[0], (size_t)K * W)) != LRQMM_OK) return e;
-      nsp[0] = nsp[1] = 1;
-      // side B was reduced too (multi -> reduce1), both Z are final
+      if ((sides & 1) && (e = allreduce_f32(h, Zs[0], (size_t)K * W)) != LRQMM_OK) return e;
+      nsp[0] = nsp[1] = 1;  // multi -> reduce1: both Z are final
     }
     // O2: Q1 = orth(Z) (fp64 Gram + Cholesky, transform applied with fp64 accumulation, so Q1 is
     // orthonormal to fp32 rounding); K rows are replicated on every rank
-    if ((e = gram_step(h, Zs, kdim, nsp, 0, Q1s, false)) != LRQMM_OK) return e;
+    if ((e = gram_step(h, Zs, kdim, nsp, 0, Q1s, false, sides)) != LRQMM_OK) return e;
     if (it + 1 < h->cfg.power_iters) {
       for (int sd = 0; sd < 2; ++sd)
-        nsp[sd] = launch_tc_proj_rows(view(h, sd), Q1s[sd], Ys[sd], nullptr, nullptr, W, part_of(h, sd),
-                                      part_elems(h), false, h->s[sd].img, h->st);
+        if (sides & (1 << sd))
+          nsp[sd] = launch_tc_proj_rows(view(h, sd), Q1s[sd], Ys[sd], nullptr, nullptr, W, part_of(h, sd),
+                                        part_elems(h), false, h->s[sd].img, h->st);
     }
   }
-  // S3 + cross: W_X = R_X Q1_X and G'_X = X~ Q1_other in one pass over X
-  //   (Algorithm 1 on R^T: B = Q1^T R^T = W^T; RC1/RC2 skinny products)
-  for (int sd = 0; sd < 2; ++sd)
-    nsp[sd] = launch_tc_proj_rows(view(h, sd), Q1s[sd], Ys[sd], Q1s[1 - sd], h->s[sd].Gp, W, part_of(h, sd),
-                                  part_elems(h), false, h->s[sd].img, h->st);
-  // T: W = sum(partials), truncation to rank r via eig(W^T W) (Algorithm 1 lines 139-140)
-  if ((e = gram_step(h, Ys, rows, nsp, 1, nullptr, true)) != LRQMM_OK) return e;
+  return check_launch(h);
+}
+
+// Cross core and factor assembly (Algorithm 2 lines 361-366 folded into two rank-2r factors):
+// needs W_X (= Y_X), VW_X, Q1_X of both sides and G'_A = A~ Q1_B, G'_B = B~ Q1_A.
+static lrqmm_status_t assemble(lrqmm_handle_t h) {
+  const int W = h->W;
+  const int64_t K = h->cfg.k;
   // V_B^T V_A core: Q1_B^T Q1_A (fp64, W x W) -> Mab, VWb Mab
   {
     GramJobs j{};
@@ -426,8 +436,8 @@ static lrqmm_status_t rsvd_body(lrqmm_handle_t h) {
     launch_gram_jobs(j, W, h->st);
   }
   launch_cross_small(h->Gcross, h->s[0].VW, h->s[1].VW, W, h->r, h->VWbM, h->st);
-  // F: factor assembly (Algorithm 2 lines 361-366 folded into two rank-2r factors)
   const int r = h->r;
+  const int64_t rows[2] = {h->s[0].rows, h->s[1].rows};
   float* YA = h->s[0].Y;
   float* YB = h->s[1].Y;
   launch_apply_small(YA, h->s[0].VW, nullptr, nullptr, rows[0], W, W, r, h->LA, h->R2, 0, h->st);          // U_A S_A
@@ -437,30 +447,47 @@ static lrqmm_status_t rsvd_body(lrqmm_handle_t h) {
   return check_launch(h);
 }
 
-
-lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const float* omegaB, int64_t ldo) {
-  if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
-  if (h->sticky != LRQMM_OK) return h->sticky;
-  if (h->r == 0) return LRQMM_ERR_STATE;
-  if ((h->state & 3) != 3) return LRQMM_ERR_STATE;
-  if (!omegaA || !omegaB || ldo < h->kk) return LRQMM_ERR_INVALID_ARGUMENT;
-  cudaSetDevice(h->cfg.device);
+// kind 0: both sides (full);  kind 1: static-B (A side + the A-dependent B term; B's W_B, VW_B,
+// Q1_B resident);  kind 2: B side only (prepare the resident B factors).
+// All of it is on handle-owned buffers only (graph-capturable).
+static lrqmm_status_t rsvd_body(lrqmm_handle_t h, int kind) {
   const int W = h->W;
-  const int64_t K = h->cfg.k;
-  const bool multi = h->cfg.world_size > 1;
-  record(h, 4);
-  // sketch Omega (K x kk, caller layout) -> zero-padded K x W
-  const float* om[2] = {omegaA, omegaB};
-  for (int sd = 0; sd < 2; ++sd)
-    LQ_CUDA(cudaMemcpy2DAsync(h->s[sd].Om, sizeof(float) * W, om[sd], sizeof(float) * ldo, sizeof(float) * h->kk, K,
-                              cudaMemcpyDeviceToDevice, h->st));
+  const int64_t rows[2] = {h->s[0].rows, h->s[1].rows};
+  float* Ys[2] = {h->s[0].Y, h->s[1].Y};
+  float* Q1s[2] = {h->s[0].Q1, h->s[1].Q1};
+  const int sides = kind == 0 ? 3 : (kind == 1 ? 1 : 2);
+  lrqmm_status_t e;
+  if ((e = rsvd_chain(h, sides)) != LRQMM_OK) return e;
+  int nsp[2] = {1, 1};
+  // S3 (+ cross): W_X = R_X Q1_X, and G'_X = X~ Q1_other in the same pass over X when the other
+  //   side's Q1 is current (Algorithm 1 on R^T: B = Q1^T R^T = W^T; RC1/RC2 skinny
+  //   products)
+  for (int sd = 0; sd < 2; ++sd) {
+    if (!(sides & (1 << sd))) continue;
+    const bool cross = kind != 2;
+    nsp[sd] = launch_tc_proj_rows(view(h, sd), Q1s[sd], Ys[sd], cross ? Q1s[1 - sd] : nullptr,
+                                  cross ? h->s[sd].Gp : nullptr, W, part_of(h, sd), part_elems(h), false,
+                                  h->s[sd].img, h->st);
+  }
+  // T: W = sum(partials), truncation to rank r via eig(W^T W) (Algorithm 1 lines 139-140)
+  if ((e = gram_step(h, Ys, rows, nsp, 1, nullptr, true, sides)) != LRQMM_OK) return e;
+  if (kind == 2) return check_launch(h);
+  // static-B: the only A-dependent B-side term, G'_B = B~ Q1_A (a codes-only pass over B)
+  if (kind == 1)
+    launch_tc_proj_codes(view(h, 1), Q1s[0], h->s[1].Gp, W, part_of(h, 1), part_elems(h), h->s[1].img, h->st);
+  return assemble(h);
+}
+
+// Runs rsvd_body(kind), captured as a CUDA graph on the second call of that kind and replayed after.
+static lrqmm_status_t run_rsvd(lrqmm_handle_t h, int kind) {
   lrqmm_status_t e = LRQMM_OK;
+  const bool multi = h->cfg.world_size > 1;
   // graphs: single-rank handles (NCCL collectives stay eagerly enqueued), not disabled by env
-  const bool use_graph = !h->graph_off && !multi && !getenv("LRQMM_NO_GRAPH");
-  if (h->rsvd_exec) {
-    LQ_CUDA(cudaGraphLaunch(h->rsvd_exec, h->st));
-    launch_counter() += h->rsvd_graph_kernels;
-  } else if (use_graph && h->rsvd_calls >= 1) {
+  const bool use_graph = kind != 2 && !h->graph_off && !multi && !getenv("LRQMM_NO_GRAPH");
+  if (use_graph && h->rsvd_exec[kind]) {
+    LQ_CUDA(cudaGraphLaunch(h->rsvd_exec[kind], h->st));
+    launch_counter() += h->rsvd_graph_kernels[kind];
+  } else if (use_graph && h->rsvd_calls[kind] >= 1) {
     // capture on the private stream (function attributes were set by the eager first call)
     if (!h->cap_st && cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking) != cudaSuccess) h->graph_off = true;
     cudaGraph_t g = nullptr;
@@ -469,30 +496,68 @@ lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const 
       const int64_t k0 = launch_counter();
       cudaStream_t user = h->st;
       h->st = h->cap_st;
-      e = rsvd_body(h);
+      e = rsvd_body(h, kind);
       h->st = user;
-      h->rsvd_graph_kernels = launch_counter() - k0;
+      h->rsvd_graph_kernels[kind] = launch_counter() - k0;
       launch_counter() = k0;
       ok = cudaStreamEndCapture(h->cap_st, &g) == cudaSuccess && e == LRQMM_OK && g != nullptr &&
-           cudaGraphInstantiate(&h->rsvd_exec, g, 0) == cudaSuccess;
+           cudaGraphInstantiate(&h->rsvd_exec[kind], g, 0) == cudaSuccess;
       if (g) cudaGraphDestroy(g);
     }
     cudaGetLastError();  // a failed capture must not leave a sticky launch error behind
     if (ok) {
-      LQ_CUDA(cudaGraphLaunch(h->rsvd_exec, h->st));
-      launch_counter() += h->rsvd_graph_kernels;
+      LQ_CUDA(cudaGraphLaunch(h->rsvd_exec[kind], h->st));
+      launch_counter() += h->rsvd_graph_kernels[kind];
     } else {
       h->graph_off = true;
-      if (h->rsvd_exec) { cudaGraphExecDestroy(h->rsvd_exec); h->rsvd_exec = nullptr; }
-      if ((e = rsvd_body(h)) != LRQMM_OK) return e;
+      if (h->rsvd_exec[kind]) { cudaGraphExecDestroy(h->rsvd_exec[kind]); h->rsvd_exec[kind] = nullptr; }
+      if ((e = rsvd_body(h, kind)) != LRQMM_OK) return e;
     }
   } else {
-    if ((e = rsvd_body(h)) != LRQMM_OK) return e;
+    if ((e = rsvd_body(h, kind)) != LRQMM_OK) return e;
   }
-  ++h->rsvd_calls;
+  ++h->rsvd_calls[kind];
+  return check_launch(h);
+}
+
+static lrqmm_status_t copy_omega(lrqmm_handle_t h, int sd, const float* om, int64_t ldo) {
+  LQ_CUDA(cudaMemcpy2DAsync(h->s[sd].Om, sizeof(float) * h->W, om, sizeof(float) * ldo, sizeof(float) * h->kk,
+                            h->cfg.k, cudaMemcpyDeviceToDevice, h->st));
+  return LRQMM_OK;
+}
+
+lrqmm_status_t lrqmm_rsvd_residual_b(lrqmm_handle_t h, const float* omegaB, int64_t ldo) {
+  if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (h->sticky != LRQMM_OK) return h->sticky;
+  if (h->r == 0) return LRQMM_ERR_STATE;
+  if (!(h->state & 2)) return LRQMM_ERR_STATE;
+  if (!omegaB || ldo < h->kk) return LRQMM_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(h->cfg.device);
+  lrqmm_status_t e;
+  if ((e = copy_omega(h, 1, omegaB, ldo)) != LRQMM_OK) return e;
+  if ((e = run_rsvd(h, 2)) != LRQMM_OK) return e;
+  h->state |= 8;   // B's factors resident
+  h->state &= ~4;  // the correction itself still needs an A side
+  return LRQMM_OK;
+}
+
+lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const float* omegaB, int64_t ldo) {
+  if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (h->sticky != LRQMM_OK) return h->sticky;
+  if (h->r == 0) return LRQMM_ERR_STATE;
+  if ((h->state & 3) != 3) return LRQMM_ERR_STATE;
+  if (!omegaA || ldo < h->kk) return LRQMM_ERR_INVALID_ARGUMENT;
+  const bool static_b = omegaB == nullptr;  // reuse the resident B factors (lrqmm_rsvd_residual_b)
+  if (static_b && !(h->state & 8)) return LRQMM_ERR_STATE;
+  cudaSetDevice(h->cfg.device);
+  record(h, 4);
+  lrqmm_status_t e;
+  // sketches Omega (K x kk, caller layout) -> zero-padded K x W
+  if ((e = copy_omega(h, 0, omegaA, ldo)) != LRQMM_OK) return e;
+  if (!static_b && (e = copy_omega(h, 1, omegaB, ldo)) != LRQMM_OK) return e;
+  if ((e = run_rsvd(h, static_b ? 1 : 0)) != LRQMM_OK) return e;
   record(h, 5);
-  if ((e = check_launch(h)) != LRQMM_OK) return e;
-  h->state |= 4;
+  h->state |= 4 | 8;  // correction ready; B's factors (W_B, VW_B, Q1_B) are current either way
   return LRQMM_OK;
 }
 

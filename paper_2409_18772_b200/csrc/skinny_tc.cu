@@ -45,17 +45,20 @@ constexpr int kMmaWarp = 1;
 constexpr int kThreads = 192;
 constexpr int kPlane = BM * BK;  // 16 KB: one h, l or codes tile
 constexpr int64_t kMaxChunk = 65536;  // |l p| <= 255 * 64: int32 accumulation exact up to 131072 terms
-template <int kMode, int NA, bool kDual>
+// kVar: 0 = residual (h, l) only, 1 = residual + codes ("dual"), 2 = codes only
+template <int kMode, int NA, int kVar>
 struct Cfg {
+  static constexpr bool kHasU = kVar != 2;
+  static constexpr bool kHasC = kVar != 0;
   static constexpr int WN = 32 * NA;            // W' (W rounded up to 32)
   static constexpr int kBRows = 3 * WN;         // p1 | p2 | p3
   static constexpr int kImg = kBRows * BK;      // one k-block image: kBRows rows x 128 B
-  // stage: h | l | B image [| codes | B2 image]
+  // stage: [h | l | B image] [codes | B2 image]
   static constexpr int kOffL = kPlane;
   static constexpr int kOffB = 2 * kPlane;
-  static constexpr int kOffC = kOffB + kImg;
+  static constexpr int kOffC = kHasU ? kOffB + kImg : 0;
   static constexpr int kOffB2 = kOffC + kPlane;
-  static constexpr int kStageBytes = kDual ? kOffB2 + kImg : kOffB + kImg;
+  static constexpr int kStageBytes = kHasC ? kOffB2 + kImg : kOffB + kImg;
   static constexpr int kStage = (kStageBytes + 1023) / 1024 * 1024;
   static constexpr int S0 = (216 * 1024) / kStage;
   static constexpr int S = S0 > 6 ? 6 : S0;
@@ -63,7 +66,8 @@ struct Cfg {
   static constexpr int kSmem = S * kStage + 256 + 1024;
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
   // TMEM accumulator: H (3 W') | L (2 W') [| C (3 W')], int32
-  static constexpr int kAccCols = 5 * WN + (kDual ? 3 * WN : 0);
+  static constexpr int kOffAccC = kHasU ? 5 * WN : 0;  // C accumulator columns
+  static constexpr int kAccCols = kOffAccC + (kHasC ? 3 * WN : 0);
   static constexpr int kAccBufs = 2 * kAccCols <= 512 ? 2 : 1;
   static_assert(kAccBufs * kAccCols <= 512, "TMEM budget");
 };
@@ -247,10 +251,11 @@ __global__ void __launch_bounds__(256) k_prep_img(PrepJobs jb) {
   PREP_T(5)
 }
 
-template <int kMode, int NA, bool kDual>
+template <int kMode, int NA, int kVar>
 __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_constant__ TcMaps maps, TcArgs a) {
   using namespace tcp;
-  using C = Cfg<kMode, NA, kDual>;
+  using C = Cfg<kMode, NA, kVar>;
+  constexpr bool kHasU = C::kHasU, kHasC = C::kHasC;
   constexpr int WN = C::WN;
   constexpr int S = C::S;
   constexpr int NACC = C::kAccBufs;
@@ -295,9 +300,11 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   if (warp == kTmaWarp) {
     // ------------------------------------------------------ TMA producer
     if (lane == 0) {
-      tma_prefetch_desc(&maps.uh);
-      tma_prefetch_desc(&maps.ul);
-      if (kDual) tma_prefetch_desc(&maps.codes);
+      if (kHasU) {
+        tma_prefetch_desc(&maps.uh);
+        tma_prefetch_desc(&maps.ul);
+      }
+      if (kHasC) tma_prefetch_desc(&maps.codes);
       int it = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         int blk, split, nkb;
@@ -309,16 +316,18 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
           mbar_wait(&freeb[s], ((it / S) & 1) ^ 1);
           uint8_t* st = smem + s * C::kStage;
           mbar_arrive_expect_tx(&full[s], C::kStageBytes);
-          if (kMode == 0) {
-            tma_load_2d(st, &maps.uh, &full[s], k0, blk * BM);
-            tma_load_2d(st + C::kOffL, &maps.ul, &full[s], k0, blk * BM);
-          } else {
-            tma_load_2d(st, &maps.uh, &full[s], blk * BM, k0);
-            tma_load_2d(st + C::kOffL, &maps.ul, &full[s], blk * BM, k0);
-          }
           const int64_t g = k0 / BK;
-          bulk_load(st + C::kOffB, a.img1 + g * C::kImg, C::kImg, &full[s]);
-          if (kDual) {
+          if (kHasU) {
+            if (kMode == 0) {
+              tma_load_2d(st, &maps.uh, &full[s], k0, blk * BM);
+              tma_load_2d(st + C::kOffL, &maps.ul, &full[s], k0, blk * BM);
+            } else {
+              tma_load_2d(st, &maps.uh, &full[s], blk * BM, k0);
+              tma_load_2d(st + C::kOffL, &maps.ul, &full[s], blk * BM, k0);
+            }
+            bulk_load(st + C::kOffB, a.img1 + g * C::kImg, C::kImg, &full[s]);
+          }
+          if (kHasC) {
             tma_load_2d(st + C::kOffC, &maps.codes, &full[s], k0, blk * BM);
             bulk_load(st + C::kOffB2, a.img2 + g * C::kImg, C::kImg, &full[s]);
           }
@@ -345,7 +354,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
         tc_fence_after();
         const uint32_t dH = tmem + acc * C::kAccCols;
         const uint32_t dL = dH + 3 * WN;
-        const uint32_t dC = dH + 5 * WN;
+        const uint32_t dC = dH + C::kOffAccC;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % S;
           mbar_wait(&full[s], (it / S) & 1);
@@ -354,11 +363,13 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
 #pragma unroll
           for (int k = 0; k < BK / 32; ++k) {
             const uint32_t acc0 = (kb | k) != 0 ? 1u : 0u;
-            const uint64_t dA = ds + ((k * kAStep) >> 4);
-            const uint64_t dB = ds + ((C::kOffB + k * 32) >> 4);
-            umma_i8(dH, dA, dB, idH, acc0);                          // h x [p1 | p2 | p3]
-            umma_i8(dL, dA + (C::kOffL >> 4), dB, idL, acc0);        // l x [p1 | p2]
-            if (kDual)
+            if (kHasU) {
+              const uint64_t dA = ds + ((k * kAStep) >> 4);
+              const uint64_t dB = ds + ((C::kOffB + k * 32) >> 4);
+              umma_i8(dH, dA, dB, idH, acc0);                          // h x [p1 | p2 | p3]
+              umma_i8(dL, dA + (C::kOffL >> 4), dB, idL, acc0);        // l x [p1 | p2]
+            }
+            if (kHasC)
               umma_i8(dC, ds + ((C::kOffC + k * 32) >> 4), ds + ((C::kOffB2 + k * 32) >> 4), idC, acc0);
           }
           umma_commit(&freeb[s]);
@@ -383,10 +394,11 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + acc * C::kAccCols;
       float inv_row = 1.f;  // ROW: rows of R and X~ carry 1/lambda_i (COL folded it into P)
       if (kMode == 0) inv_row = orow < a.rows ? __ldg(a.inv_lam + orow) : 1.f;
-      constexpr int NG = NA * (kDual ? 2 : 1);  // 32-column output groups per row
+      constexpr int GU = kHasU ? NA : 0;       // output groups of the residual product
+      constexpr int NG = GU + (kHasC ? NA : 0);  // 32-column output groups per row
       float o[NG][32];
 #pragma unroll
-      for (int g = 0; g < NA; ++g) {
+      for (int g = 0; g < GU; ++g) {
         // 256 (H1 + H2 2^-7 + H3 2^-14) + L1 + L2 2^-7, then 2^-15 / lambda / s_c
         uint32_t v[32];
         const uint32_t tH = trow + g * 32, tL = trow + 3 * WN + g * 32;
@@ -411,42 +423,44 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
 #pragma unroll
         for (int c = 0; c < 32; ++c) o[g][c] += (float)(int)v[c];
       }
-      if (kDual) {
+      if (kHasC) {
 #pragma unroll
         for (int g = 0; g < NA; ++g) {
           uint32_t v[32];
-          const uint32_t tC = trow + 5 * WN + g * 32;
+          const uint32_t tC = trow + C::kOffAccC + g * 32;
           tmem_ld_32x32b_x32(tC + 2 * WN, v);
           tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < 32; ++c) o[NA + g][c] = (float)(int)v[c] * 0x1p-14f;
+          for (int c = 0; c < 32; ++c) o[GU + g][c] = (float)(int)v[c] * 0x1p-14f;
           tmem_ld_32x32b_x32(tC + WN, v);
           tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < 32; ++c) o[NA + g][c] += (float)(int)v[c] * 0x1p-7f;
+          for (int c = 0; c < 32; ++c) o[GU + g][c] += (float)(int)v[c] * 0x1p-7f;
           tmem_ld_32x32b_x32(tC, v);
           tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < 32; ++c) o[NA + g][c] += (float)(int)v[c];
+          for (int c = 0; c < 32; ++c) o[GU + g][c] += (float)(int)v[c];
         }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);  // accumulator buffer free: the next unit's MMAs may start
       if (orow < a.nout) {
-        float* o1 = a.out1 + (int64_t)split * a.nout * a.W + orow * a.W;
-        const float s1 = inv_row * (1.f / kUScale);
+        if (kHasU) {
+          float* o1 = a.out1 + (int64_t)split * a.nout * a.W + orow * a.W;
+          const float s1 = inv_row * (1.f / kUScale);
 #pragma unroll
-        for (int g = 0; g < NA; ++g)
+          for (int g = 0; g < GU; ++g)
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (g * 32 + c < a.W) o1[g * 32 + c] = o[g][c] * (s1 * __ldg(a.cinv1 + g * 32 + c));
-        if (kDual) {
+            for (int c = 0; c < 32; ++c)
+              if (g * 32 + c < a.W) o1[g * 32 + c] = o[g][c] * (s1 * __ldg(a.cinv1 + g * 32 + c));
+        }
+        if (kHasC) {
           float* o2 = a.out2 + (int64_t)split * a.nout * a.W + orow * a.W;
 #pragma unroll
           for (int g = 0; g < NA; ++g)
 #pragma unroll
             for (int c = 0; c < 32; ++c)
-              if (g * 32 + c < a.W) o2[g * 32 + c] = o[NA + g][c] * (inv_row * __ldg(a.cinv2 + g * 32 + c));
+              if (g * 32 + c < a.W) o2[g * 32 + c] = o[GU + g][c] * (inv_row * __ldg(a.cinv2 + g * 32 + c));
         }
       }
     }
@@ -503,14 +517,15 @@ static void prep_imgs(const float* P1, const float* P2, int64_t n, int W, const 
   ++launch_counter();
 }
 
-template <int kMode, int NA, bool kDual>
+template <int kMode, int NA, int kVar>
 static int run_tc(const SideView& s, const float* P1, const float* P2, int W, float* OUT1, float* OUT2, float* partial,
                   int64_t pe, bool reduce1, uint8_t* img, cudaStream_t st) {
   using namespace tcp;
-  using C = Cfg<kMode, NA, kDual>;
+  using C = Cfg<kMode, NA, kVar>;
+  constexpr bool kHasU = C::kHasU, kHasC = C::kHasC;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_tc_proj<kMode, NA, kDual>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaFuncSetAttribute(k_tc_proj<kMode, NA, kVar>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr = true;
   }
   TcArgs a{};
@@ -528,18 +543,24 @@ static int run_tc(const SideView& s, const float* P1, const float* P2, int W, fl
   const int64_t ib = tc_img_bytes(rlen, W);
   float* cinv1 = nullptr;
   float* cinv2 = nullptr;
-  prep_imgs<NA>(P1, kDual ? P2 : nullptr, rlen, W, kMode == 1 ? s.inv_lam : nullptr, img, img + ib, &cinv1, &cinv2,
-                st);
-  a.img1 = img;
-  a.img2 = img + ib;
-  a.cinv1 = cinv1;
-  a.cinv2 = kDual ? cinv2 : cinv1;
+  if (kVar == 2) {  // codes only: P2 is the single operand
+    prep_imgs<NA>(P2, nullptr, rlen, W, nullptr, img, img + ib, &cinv2, &cinv1, st);
+    a.img1 = a.img2 = img;
+    a.cinv1 = a.cinv2 = cinv2;
+  } else {
+    prep_imgs<NA>(P1, kHasC ? P2 : nullptr, rlen, W, kMode == 1 ? s.inv_lam : nullptr, img, img + ib, &cinv1,
+                  &cinv2, st);
+    a.img1 = img;
+    a.img2 = img + ib;
+    a.cinv1 = cinv1;
+    a.cinv2 = kHasC ? cinv2 : cinv1;
+  }
   // enough units for ~6 per SM (the persistent grid balances them), each >= 4 k-blocks, and a
   // chunk short enough for exact int32 accumulation
   int64_t ns = (6LL * nsm + nblk - 1) / nblk;
   const int64_t maxs = (rlen + 4 * BK - 1) / (4 * BK);
   if (ns > maxs) ns = maxs;
-  const int64_t per = a.nout * W * (kDual ? 2 : 1);
+  const int64_t per = a.nout * W * (kVar == 1 ? 2 : 1);
   if (ns > 1 && ns * per > pe) ns = pe / per;
   const int64_t mins = (rlen + kMaxChunk - 1) / kMaxChunk;
   if (ns < mins) ns = mins;
@@ -550,26 +571,28 @@ static int run_tc(const SideView& s, const float* P1, const float* P2, int W, fl
   a.nblk = (int)nblk;
   a.nsplit = (int)ns;
   a.out1 = ns == 1 ? OUT1 : partial;
-  a.out2 = ns == 1 ? OUT2 : partial + ns * a.nout * W;
+  a.out2 = ns == 1 ? OUT2 : (kVar == 2 ? partial : partial + ns * a.nout * W);
   alignas(64) TcMaps maps;
   memset(&maps, 0, sizeof(maps));
   const uint64_t ld = (uint64_t)s.ldu;
-  encode_map_2d_sw(&maps.uh, 0, s.Uh, (uint64_t)s.K, (uint64_t)s.rows, ld, BK, BM, 128);
-  encode_map_2d_sw(&maps.ul, 0, s.Ul, (uint64_t)s.K, (uint64_t)s.rows, ld, BK, BM, 128);
-  if (kDual) encode_map_2d_sw(&maps.codes, 0, s.codes, (uint64_t)s.Kp, (uint64_t)s.rows, (uint64_t)s.Kp, BK, BM, 128);
+  if (kHasU) {
+    encode_map_2d_sw(&maps.uh, 0, s.Uh, (uint64_t)s.K, (uint64_t)s.rows, ld, BK, BM, 128);
+    encode_map_2d_sw(&maps.ul, 0, s.Ul, (uint64_t)s.K, (uint64_t)s.rows, ld, BK, BM, 128);
+  }
+  if (kHasC) encode_map_2d_sw(&maps.codes, 0, s.codes, (uint64_t)s.Kp, (uint64_t)s.rows, (uint64_t)s.Kp, BK, BM, 128);
   const int64_t units = nblk * ns;
   const int grid = (int)(units < nsm ? units : nsm);
-  k_tc_proj<kMode, NA, kDual><<<grid, kThreads, C::kSmem, st>>>(maps, a);
+  k_tc_proj<kMode, NA, kVar><<<grid, kThreads, C::kSmem, st>>>(maps, a);
   ++launch_counter();
   if (ns > 1) {
     const int64_t n = a.nout * W;
     const int g = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
-    if (reduce1) {
+    if (reduce1 && kHasU) {
       k_reduce_splits_tc<<<g, 256, 0, st>>>(partial, (int)ns, n, OUT1);
       ++launch_counter();
     }
-    if (kDual) {
-      k_reduce_splits_tc<<<g, 256, 0, st>>>(partial + ns * a.nout * W, (int)ns, n, OUT2);
+    if (kHasC) {
+      k_reduce_splits_tc<<<g, 256, 0, st>>>(kVar == 2 ? partial : partial + ns * a.nout * W, (int)ns, n, OUT2);
       ++launch_counter();
     }
   }
@@ -583,18 +606,27 @@ int launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const f
                         float* partial, int64_t pe, bool reduce1, uint8_t* img, cudaStream_t st) {
   if (s.rows == 0 || s.K == 0) return 0;
   if (W <= 32) {
-    if (P2) return run_tc<0, 1, true>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
-    return run_tc<0, 1, false>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
+    if (P2) return run_tc<0, 1, 1>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
+    return run_tc<0, 1, 0>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
   }
-  if (P2) return run_tc<0, 2, true>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
-  return run_tc<0, 2, false>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
+  if (P2) return run_tc<0, 2, 1>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
+  return run_tc<0, 2, 0>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
 }
 
 int launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t pe, bool reduce1,
                         uint8_t* img, cudaStream_t st) {
   if (s.K == 0 || s.rows == 0) return 0;
-  if (W <= 32) return run_tc<1, 1, false>(s, P, nullptr, W, OUT, nullptr, partial, pe, reduce1, img, st);
-  return run_tc<1, 2, false>(s, P, nullptr, W, OUT, nullptr, partial, pe, reduce1, img, st);
+  if (W <= 32) return run_tc<1, 1, 0>(s, P, nullptr, W, OUT, nullptr, partial, pe, reduce1, img, st);
+  return run_tc<1, 2, 0>(s, P, nullptr, W, OUT, nullptr, partial, pe, reduce1, img, st);
+}
+
+// OUT = X~ P (codes only, rows x W; X~ = code / lambda): the A-dependent term B~ Q1_A of the
+// static-B mode (lrqmm_rsvd_residual with omegaB == NULL).  1 byte of codes per element.
+int launch_tc_proj_codes(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t pe,
+                         uint8_t* img, cudaStream_t st) {
+  if (s.rows == 0 || s.K == 0) return 0;
+  if (W <= 32) return run_tc<0, 1, 2>(s, nullptr, P, W, nullptr, OUT, partial, pe, true, img, st);
+  return run_tc<0, 2, 2>(s, nullptr, P, W, nullptr, OUT, partial, pe, true, img, st);
 }
 
 }  // namespace lrqmm

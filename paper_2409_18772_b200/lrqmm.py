@@ -30,7 +30,7 @@ EXPORTS = (
     "lrqmm_get_unique_id", "lrqmm_create", "lrqmm_quantize", "lrqmm_rsvd_residual", "lrqmm_gemm",
     "lrqmm_destroy", "lrqmm_sync", "lrqmm_run_host", "lrqmm_get_codes", "lrqmm_get_scales",
     "lrqmm_gemm_int32", "lrqmm_get_factors", "lrqmm_get_correction", "lrqmm_correction_width",
-    "lrqmm_get_timings", "lrqmm_launch_count", "lrqmm_status_string",
+    "lrqmm_get_timings", "lrqmm_launch_count", "lrqmm_status_string", "lrqmm_rsvd_residual_b",
 )
 DEBUG_EXPORTS = ("lrqmm_debug_proj", "lrqmm_debug_small", "lrqmm_debug_set_gemm_variant")
 
@@ -69,6 +69,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lrqmm_create": (I, [ctypes.POINTER(Config), ctypes.POINTER(P)]),
         "lrqmm_quantize": (I, [P, I, P, I64]),
         "lrqmm_rsvd_residual": (I, [P, P, P, I64]),
+        "lrqmm_rsvd_residual_b": (I, [P, P, I64]),
         "lrqmm_gemm": (I, [P, F, F, P, I64]),
         "lrqmm_destroy": (I, [P]),
         "lrqmm_sync": (I, [P]),
@@ -147,9 +148,14 @@ class Lrqmm:
         """X: float32 cuda tensor (rows x k), any row stride."""
         _check(self.lib.lrqmm_quantize(self.h, side, _ptr(X), _ld(X)), "lrqmm_quantize")
 
-    def rsvd_residual(self, omega_a, omega_b):
-        assert omega_a.stride(0) == omega_b.stride(0)
+    def rsvd_residual(self, omega_a, omega_b=None):
+        """omega_b None: static-B mode (B's factors from rsvd_residual_b / the last full call)."""
+        assert omega_b is None or omega_a.stride(0) == omega_b.stride(0)
         _check(self.lib.lrqmm_rsvd_residual(self.h, _ptr(omega_a), _ptr(omega_b), _ld(omega_a)), "lrqmm_rsvd_residual")
+
+    def rsvd_residual_b(self, omega_b):
+        """Static-B preparation: B's RSVD once, resident until B is quantized again."""
+        _check(self.lib.lrqmm_rsvd_residual_b(self.h, _ptr(omega_b), _ld(omega_b)), "lrqmm_rsvd_residual_b")
 
     def gemm(self, D, alpha: float = 1.0, beta: float = 0.0):
         _check(self.lib.lrqmm_gemm(self.h, alpha, beta, _ptr(D), _ld(D)), "lrqmm_gemm")

@@ -229,3 +229,41 @@ def test_repeated_calls_reuse_handle():
             h.gemm(D)
             h.sync()
             check_d(A, Bt, {"D": D.cpu().numpy().astype(np.float64)}, ref)
+
+
+def test_static_b_mode_matches_full_oracle():
+    """Static-B: B quantized + RSVD'd once (rsvd_residual_b), then three A's reuse it
+    (rsvd_residual with omega_b=None).  Each result must match the oracle's full Algorithm 2 with the
+    same Omega_B; quantizing B again invalidates the resident factors."""
+    M, N, K, r, p = 400, 288, 640, 10, 5
+    _, Bt, _, OmB = S.problem(M, N, K, r + p, s=40, dist="exp4")
+    with Lrqmm(M, N, K, 4, r, p) as h:
+        h.quantize(SIDE_B, cu(Bt))
+        h.rsvd_residual_b(cu(OmB))
+        for call in range(3):
+            A, _, OmA, _ = S.problem(M, N, K, r + p, s=41 + call, dist=["normal", "u01", "exp4"][call])
+            ref = O.lrqmm(A, Bt, 4, r, OmA, OmB, q=1)
+            h.quantize(SIDE_A, cu(A))
+            h.rsvd_residual(cu(OmA))
+            D = torch.empty((M, N), device=DEV)
+            h.gemm(D)
+            h.sync()
+            check_d(A, Bt, {"D": D.cpu().numpy().astype(np.float64)}, ref)
+        h.quantize(SIDE_B, cu(Bt))
+        with pytest.raises(LrqmmError) as ei:
+            h.rsvd_residual(cu(OmA))
+        assert ei.value.code == 6  # LRQMM_ERR_STATE
+
+
+def test_full_call_makes_b_resident():
+    M, N, K, r, p = 256, 256, 512, 8, 5
+    A, Bt, OmA, OmB = S.problem(M, N, K, r + p, s=50)
+    A2, _, OmA2, _ = S.problem(M, N, K, r + p, s=51, dist="u01")
+    ref2 = O.lrqmm(A2, Bt, 4, r, OmA2, OmB, q=1)
+    with Lrqmm(M, N, K, 4, r, p) as h:
+        h.quantize(SIDE_A, cu(A)); h.quantize(SIDE_B, cu(Bt)); h.rsvd_residual(cu(OmA), cu(OmB))
+        h.quantize(SIDE_A, cu(A2)); h.rsvd_residual(cu(OmA2))
+        D = torch.empty((M, N), device=DEV)
+        h.gemm(D)
+        h.sync()
+        check_d(A2, Bt, {"D": D.cpu().numpy().astype(np.float64)}, ref2)
