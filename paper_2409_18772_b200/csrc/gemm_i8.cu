@@ -62,6 +62,7 @@ struct G6Params {
   int32_t* Cint;
   int64_t ldd;
   int vec_ok;
+  int* sched;  // K7: global tile counter (atomicAdd), zeroed before the launch
 };
 
 template <int kGM = g6::kGroupM>
@@ -335,6 +336,7 @@ constexpr int kEpiThreads = 128;
 constexpr int kABytes = BM * BK;
 constexpr int kBBytes = BNH * BK;
 constexpr int kStageBytes = kABytes + kBBytes;  // 32 KB per CTA
+constexpr int kTR = 4;  // tile-index ring depth (dynamic scheduler -> MMA, epilogues, peer producer)
 #ifndef LRQMM_L2HINT7
 #define LRQMM_L2HINT7 1  // A panels evict_last (reused by the next waves of the raster group)
 #endif
@@ -437,7 +439,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = bars + 2 * STAGES + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  uint64_t* tfull_t = bars + 2 * STAGES + 4;  // kTR: tile index published (both CTAs)
+  uint64_t* tempty_t = tfull_t + kTR;         // kTR: tile index consumed (leader, 4 arrivals)
+  int* tile_ring = reinterpret_cast<int*>(tempty_t + kTR);  // kTR tile indices (both CTAs)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + kTR);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -457,6 +462,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * kEpiThreads);
+    }
+    for (int q = 0; q < kTR; ++q) {
+      mbar_init(&tfull_t[q], 1);
+      mbar_init(&tempty_t[q], 4);  // leader MMA, leader epilogue, peer producer, peer epilogue
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -480,7 +489,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
 #if LRQMM_L2HINT7
       const uint64_t polA = l2_policy_evict_last();
 #endif
-      for (int t = pair; t < num_tiles; t += npairs) {
+      const uint32_t tfull_peer = mapa_cta(smem_u32(tfull_t), 1);
+      const uint32_t ring_peer = mapa_cta(smem_u32(tile_ring), 1);
+      const uint32_t tempty_lead = mapa_cta(smem_u32(tempty_t), 0);
+      for (int lt = 0;; ++lt) {
+        const int q = lt % kTR;
+        const uint32_t qph = (lt / kTR) & 1;
+        int t;
+        if (leader) {
+          // dynamic schedule: in-flight tiles always form one contiguous window of indices, so
+          // the raster groups' L2 working set stays bounded however the pairs drift
+          mbar_wait(&tempty_t[q], qph ^ 1);
+          t = atomicAdd(p.sched, 1);
+          tile_ring[q] = t;
+          asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(ring_peer + 4 * q), "r"(t) : "memory");
+          mbar_arrive(&tfull_t[q]);
+          mbar_arrive_remote(tfull_peer + 8 * q);
+        } else {
+          mbar_wait(&tfull_t[q], qph);
+          t = tile_ring[q];
+          mbar_arrive_remote(tempty_lead + 8 * q);
+        }
+        if (t >= num_tiles) break;
         int mb, nb;
         tile_coords<g7::kGroupM>(t, p.num_m, p.num_n, mb, nb);
         const int arow = mb * (2 * BM) + (int)rank * BM;
@@ -513,8 +543,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
       const uint32_t empty_a = smem_u32(empty), tfull_a = smem_u32(tfull);
       int stage = 0;
       uint32_t phase = 0;
-      int lt = 0;
-      for (int t = pair; t < num_tiles; t += npairs, ++lt) {
+      for (int lt = 0;; ++lt) {
+        const int q = lt % kTR;
+        mbar_wait(&tfull_t[q], (lt / kTR) & 1);
+        const int t = tile_ring[q];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_t[q]);
+        if (t >= num_tiles) break;
         const int acc = lt & 1;
         const uint32_t acc_phase = (lt >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -543,8 +578,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
     const int et = threadIdx.x - 64;  // 0..127
     const int quad = warp & 3;
     const uint32_t tempty0 = mapa_cta(smem_u32(tempty), 0);
-    int lt = 0;
-    for (int t = pair; t < num_tiles; t += npairs, ++lt) {
+    const uint32_t tempty_t0 = mapa_cta(smem_u32(tempty_t), 0);
+    for (int lt = 0;; ++lt) {
+      const int q = lt % kTR;
+      mbar_wait(&tfull_t[q], (lt / kTR) & 1);
+      const int t = tile_ring[q];
+      epi_bar();  // every epilogue thread has read the index
+      if (et == 0) mbar_arrive_remote(tempty_t0 + 8 * q);
+      if (t >= num_tiles) break;
       int mb, nb;
       tile_coords<g7::kGroupM>(t, p.num_m, p.num_n, mb, nb);
       const int acc = lt & 1;
@@ -692,8 +733,8 @@ int& gemm_variant() {  // 0 auto, 1 force one-CTA K6, 2 force CTA-pair K7 (test 
   return v;
 }
 
-static bool use_2sm(int64_t M, int64_t N) {
-  if (gemm_variant() == 1) return false;
+static bool use_2sm(int64_t M, int64_t N, const int* sched) {
+  if (!sched || gemm_variant() == 1) return false;
   if (gemm_variant() == 2) return true;
   return M >= 512 && N >= 512;
 }
@@ -736,6 +777,7 @@ static void launch_t7(G6Params p, const CUtensorMap* mA, const CUtensorMap* mB, 
   const int tiles = p.num_m * p.num_n;
   int pairs = nsm / 2;
   if (tiles < pairs) pairs = tiles;
+  cudaMemsetAsync(p.sched, 0, sizeof(int), st);
   k7_gemm_i8_2sm<kR2><<<2 * pairs, g7::kThreads, kSmem, st>>>(*mA, *mB, p); ++launch_counter();
 }
 
@@ -757,6 +799,7 @@ void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStre
   p.D = g.D;
   p.Cint = g.Cint;
   p.ldd = g.ldd;
+  p.sched = g.sched;
   const void* outp = g.epi == 0 ? (const void*)g.Cint : (const void*)g.D;
   p.vec_ok = ((reinterpret_cast<uintptr_t>(outp) & 15) == 0) && (g.ldd % 4 == 0);
   int dev = 0, nsm = 148;
@@ -767,7 +810,7 @@ void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStre
   const CUtensorMap* mA = reinterpret_cast<const CUtensorMap*>(mapA);
   const CUtensorMap* mB = reinterpret_cast<const CUtensorMap*>(mapB);
   const int r2 = g.epi == 0 ? 0 : g.R2;
-  if (use_2sm(g.M, g.N)) {
+  if (use_2sm(g.M, g.N, g.sched)) {
     switch (r2) {
       case 0: launch_t7<0>(p, mA + 1, mB + 1, nsm, st); break;
       case 8: launch_t7<8>(p, mA + 1, mB + 1, nsm, st); break;

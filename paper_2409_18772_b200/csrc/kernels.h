@@ -141,6 +141,7 @@ struct GemmArgs {
   float* D;              // M x N (ldd)
   int32_t* Cint;         // M x N (ldd)
   int64_t ldd;
+  int* sched;            // device int: dynamic tile counter of the CTA-pair GEMM (zeroed per launch)
 };
 // mapA / mapB: arrays of two CUtensorMap (one-CTA and CTA-pair box shapes); returns 0 on success
 int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB);

@@ -61,6 +61,7 @@ struct lrqmm_handle_s {
   int* counter_cross = nullptr;
   float* VWbM = nullptr;     // W x W
   int* err_flag = nullptr;
+  int* sched = nullptr;  // CTA-pair GEMM tile counter
   alignas(64) CUtensorMap mapA[2];  // [0] one-CTA GEMM boxes, [1] CTA-pair GEMM boxes
   alignas(64) CUtensorMap mapB[2];
   cudaEvent_t ev[8] = {};
@@ -174,7 +175,7 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
     cudaFree(s.gpart); cudaFree(s.counter); cudaFree(s.T64); cudaFree(s.VW); cudaFree(s.U); cudaFree(s.img);
   }
   cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->partial); cudaFree(h->Gcross); cudaFree(h->gpart_cross);
-  cudaFree(h->counter_cross); cudaFree(h->VWbM); cudaFree(h->err_flag);
+  cudaFree(h->counter_cross); cudaFree(h->VWbM); cudaFree(h->err_flag); cudaFree(h->sched);
   cudaFree(h->hA); cudaFree(h->hB); cudaFree(h->hOmA); cudaFree(h->hOmB); cudaFree(h->hD);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
@@ -236,7 +237,7 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
          dalloc(&h->gpart_cross, (int64_t)kGramMaxBlocks * h->W * h->W) && dalloc(&h->counter_cross, 1) &&
          dalloc(&h->VWbM, (int64_t)h->W * h->W);
   }
-  ok = ok && dalloc(&h->err_flag, 4);
+  ok = ok && dalloc(&h->err_flag, 4) && dalloc(&h->sched, 1);
   if (!ok) {
     lrqmm_destroy(h);
     return LRQMM_ERR_ALLOC;
@@ -580,6 +581,7 @@ static lrqmm_status_t run_gemm(lrqmm_handle_t h, int epi, float alpha, float bet
   g.D = D;
   g.Cint = Cint;
   g.ldd = ldd;
+  g.sched = h->sched;
   launch_gemm(g, h->mapA, h->mapB, h->st);
   return check_launch(h);
 }
