@@ -466,9 +466,10 @@ def main():
         h.sync()
         nrm = torch.linalg.norm(Cex)
         errs["lrqmm"] = float(torch.linalg.norm(D[rows].double() - Cex) / nrm)
-        for name, rnd, gran in (("dq_paper_trunc_tensor", "trunc", "tensor"), ("dq_nearest_row", "nearest", "row"),
-                                ("dq_floor_row", "floor", "row")):
-            with Lrqmm(Mloc, N, K, bits, 0, 0, 1, rnd, gran, device=local, stream=stream) as hq:
+        for name, rnd, gran, qt in (("dq_paper_trunc_tensor", "trunc", "tensor", 0), ("dq_nearest_row", "nearest", "row", 0),
+                                    ("dq_floor_row", "floor", "row", 0), ("qt110_trunc_tensor", "trunc", "tensor", 3),
+                                    ("qt111_trunc_tensor", "trunc", "tensor", 4)):
+            with Lrqmm(Mloc, N, K, bits, 0, 0, 1, rnd, gran, device=local, stream=stream, qt_terms=qt) as hq:
                 hq.quantize(SIDE_A, A); hq.quantize(SIDE_B, Bt); hq.gemm(D); hq.sync()
             errs[name] = float(torch.linalg.norm(D[rows].double() - Cex) / nrm)
         del Cex

@@ -82,6 +82,11 @@ typedef struct {
   int device;      /* CUDA device ordinal */
   void* stream;    /* cudaStream_t (NULL = legacy default stream) */
   int enable_timing; /* record per-phase CUDA events (lrqmm_get_timings) */
+  int qt_terms;      /* 0, or QuantTensor compensation instead of LRQMM (requires rank == 0): 3 = QT(1,1,0),
+                        4 = QT(1,1,1) of Eq. gemm_r_split.  quantize then also re-quantizes
+                        the fp32 residual fp32(x - code/lambda) with its own scales (same bits, rounding,
+                        granularity; the paper's QT columns use trunc + per-tensor, reading #27) and
+                        gemm returns alpha (A_q B_q + A_q R_Bq + R_Aq B_q [+ R_Aq R_Bq]) + beta D */
 } lrqmm_config_t;
 
 /* Host.  128-byte NCCL unique id for a world_size > 1 communicator (call on rank 0,

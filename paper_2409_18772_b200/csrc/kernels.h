@@ -30,6 +30,9 @@ struct QuantArgs {
   int64_t uplane;         // bytes between the h and l planes
 };
 void launch_quantize(const QuantArgs& a, cudaStream_t st);
+// QT: R = fp32(X - code / lambda) (rows x K, dense), fp64 arithmetic as the oracle
+void launch_resid_f32(const float* X, int64_t ldx, const int8_t* codes, int Kp, const float* lam, int64_t rows, int K,
+                      float* R, cudaStream_t st);
 void launch_tensor_scale(const float* X, int64_t ldx, int64_t rows, int K, int qmax, float* row_amax,
                          float* lam_rows, float* inv_rows, float* lam_scalar, int* err_flag, cudaStream_t st);
 

@@ -24,7 +24,11 @@ struct Side {
   int64_t rows = 0;
   int64_t ldu = 0;
   uint8_t* U = nullptr;      // residual fraction u = lambda x - code, Q15 as h | l byte planes (written by K1)
-  uint8_t* img = nullptr;    // pre-split tf32 B operand images of the passes (skinny_tc.cu)
+  uint8_t* img = nullptr;    // B operand images of the RSVD passes (skinny_tc.cu)
+  // QuantTensor (cfg.qt_terms > 0): fp32 residual and its re-quantization
+  float* R32 = nullptr;      // rows x K
+  int8_t* rcodes = nullptr;  // rows x Kp
+  float *rlam = nullptr, *rinv = nullptr, *rrow_amax = nullptr, *rlam_scalar = nullptr;
   int8_t* codes = nullptr;   // rows x Kp
   float* lam = nullptr;      // rows
   float* inv_lam = nullptr;  // rows, RN(1/lambda)
@@ -64,6 +68,8 @@ struct lrqmm_handle_s {
   int* sched = nullptr;  // CTA-pair GEMM tile counter
   alignas(64) CUtensorMap mapA[2];  // [0] one-CTA GEMM boxes, [1] CTA-pair GEMM boxes
   alignas(64) CUtensorMap mapB[2];
+  alignas(64) CUtensorMap mapRA[2];  // QT: maps of the residual codes
+  alignas(64) CUtensorMap mapRB[2];
   cudaEvent_t ev[8] = {};
   ncclComm_t comm = nullptr;
   // rsvd_residual as a CUDA graph: captured once on a private stream (the caller's stream may be
@@ -162,6 +168,8 @@ static lrqmm_status_t validate(const lrqmm_config_t* c) {
     // r + p <= min(rows, K) of each side (A: global rows checked per shard)
     if (kk > c->k || kk > c->n || (c->world_size == 1 && kk > c->m)) return LRQMM_ERR_RANK;
   }
+  if (c->qt_terms != 0 && c->qt_terms != 3 && c->qt_terms != 4) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (c->qt_terms != 0 && c->rank != 0) return LRQMM_ERR_UNSUPPORTED;  // QT and LRQMM are alternatives
   return LRQMM_OK;
 }
 
@@ -173,6 +181,7 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
     cudaFree(s.codes); cudaFree(s.lam); cudaFree(s.inv_lam); cudaFree(s.row_amax); cudaFree(s.lam_scalar); cudaFree(s.Om);
     cudaFree(s.Y); cudaFree(s.Q0); cudaFree(s.Z); cudaFree(s.Q1); cudaFree(s.Gp); cudaFree(s.G);
     cudaFree(s.gpart); cudaFree(s.counter); cudaFree(s.T64); cudaFree(s.VW); cudaFree(s.U); cudaFree(s.img);
+    cudaFree(s.R32); cudaFree(s.rcodes); cudaFree(s.rlam); cudaFree(s.rinv); cudaFree(s.rrow_amax); cudaFree(s.rlam_scalar);
   }
   cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->partial); cudaFree(h->Gcross); cudaFree(h->gpart_cross);
   cudaFree(h->counter_cross); cudaFree(h->VWbM); cudaFree(h->err_flag); cudaFree(h->sched);
@@ -227,6 +236,9 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
            dalloc(&s.counter, 1) && dalloc(&s.T64, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W) &&
            dalloc(&s.img, 2 * tc_img_bytes(std::max<int64_t>(s.rows, K), h->W));
     }
+    if (cfg->qt_terms > 0)
+      ok = ok && dalloc(&s.R32, s.rows * K) && dalloc(&s.rcodes, s.rows * h->Kp) && dalloc(&s.rlam, s.rows) &&
+           dalloc(&s.rinv, s.rows) && dalloc(&s.rrow_amax, s.rows) && dalloc(&s.rlam_scalar, 1);
   }
   if (h->W > 0) {
     const int64_t maxrows = std::max<int64_t>({cfg->m, cfg->n, K});
@@ -251,6 +263,14 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
   if (gemm_prepare_maps(g, h->mapA, h->mapB) != 0) {
     lrqmm_destroy(h);
     return LRQMM_ERR_CUDA;
+  }
+  if (cfg->qt_terms > 0) {
+    g.A = h->s[0].rcodes;
+    g.B = h->s[1].rcodes;
+    if (gemm_prepare_maps(g, h->mapRA, h->mapRB) != 0) {
+      lrqmm_destroy(h);
+      return LRQMM_ERR_CUDA;
+    }
   }
   if (cfg->enable_timing) {
     for (auto& e : h->ev)
@@ -309,6 +329,23 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
   a.ldu = s.ldu;
   a.uplane = s.rows * s.ldu;
   if (s.rows > 0) launch_quantize(a, h->st);
+  if (h->cfg.qt_terms > 0 && s.rows > 0 && h->cfg.k > 0) {
+    // QuantTensor: r = fp32(x - code/lambda), re-quantized with its own scale(s) (Eq. gemm_r_split)
+    const int K = (int)h->cfg.k;
+    launch_resid_f32(X, ldx, s.codes, h->Kp, s.lam, s.rows, K, s.R32, h->st);
+    if (h->cfg.granularity == LRQMM_SCALE_PER_TENSOR)
+      launch_tensor_scale(s.R32, K, s.rows, K, h->qmax, s.rrow_amax, s.rlam, s.rinv, s.rlam_scalar, h->err_flag,
+                          h->st);
+    QuantArgs b = a;
+    b.X = s.R32;
+    b.ldx = K;
+    b.codes = s.rcodes;
+    b.lam = s.rlam;
+    b.inv_lam = s.rinv;
+    b.lam_fixed = h->cfg.granularity == LRQMM_SCALE_PER_TENSOR ? s.rlam_scalar : nullptr;
+    b.U = nullptr;
+    launch_quantize(b, h->st);
+  }
   record(h, side == LRQMM_SIDE_A ? 1 : 3);
   lrqmm_status_t e = check_launch(h);
   if (e != LRQMM_OK) return e;
@@ -563,16 +600,18 @@ lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const 
 }
 
 static lrqmm_status_t run_gemm(lrqmm_handle_t h, int epi, float alpha, float beta, float* D, int32_t* Cint,
-                               int64_t ldd) {
+                               int64_t ldd, int qt_term = 0) {
   GemmArgs g{};
-  g.A = h->s[0].codes;
-  g.B = h->s[1].codes;
+  // QT term t (1-based): 1 = A_q B_q, 2 = A_q R_Bq, 3 = R_Aq B_q, 4 = R_Aq R_Bq (Eq. gemm_r_split)
+  const bool ra = qt_term == 3 || qt_term == 4, rb = qt_term == 2 || qt_term == 4;
+  g.A = ra ? h->s[0].rcodes : h->s[0].codes;
+  g.B = rb ? h->s[1].rcodes : h->s[1].codes;
   g.M = h->cfg.m;
   g.N = h->cfg.n;
   g.Kp = h->Kp;
   g.epi = epi;
-  g.inv_a = h->s[0].inv_lam;
-  g.inv_b = h->s[1].inv_lam;
+  g.inv_a = ra ? h->s[0].rinv : h->s[0].inv_lam;
+  g.inv_b = rb ? h->s[1].rinv : h->s[1].inv_lam;
   g.LA = h->LA;
   g.LB = h->LB;
   g.R2 = h->r > 0 ? h->R2 : 0;
@@ -582,7 +621,7 @@ static lrqmm_status_t run_gemm(lrqmm_handle_t h, int epi, float alpha, float bet
   g.Cint = Cint;
   g.ldd = ldd;
   g.sched = h->sched;
-  launch_gemm(g, h->mapA, h->mapB, h->st);
+  launch_gemm(g, ra ? h->mapRA : h->mapA, rb ? h->mapRB : h->mapB, h->st);
   return check_launch(h);
 }
 
@@ -594,7 +633,14 @@ lrqmm_status_t lrqmm_gemm(lrqmm_handle_t h, float alpha, float beta, float* D, i
   if ((!D && h->cfg.m > 0 && h->cfg.n > 0) || ldd < h->cfg.n) return LRQMM_ERR_INVALID_ARGUMENT;
   cudaSetDevice(h->cfg.device);
   record(h, 6);
-  lrqmm_status_t e = run_gemm(h, 1, alpha, beta, D, nullptr, ldd);
+  lrqmm_status_t e;
+  if (h->cfg.qt_terms > 0) {
+    // QuantTensor: the terms accumulate into D (beta chaining), alpha on every term
+    e = run_gemm(h, 1, alpha, beta, D, nullptr, ldd, 1);
+    for (int t = 2; t <= h->cfg.qt_terms && e == LRQMM_OK; ++t) e = run_gemm(h, 1, alpha, 1.f, D, nullptr, ldd, t);
+  } else {
+    e = run_gemm(h, 1, alpha, beta, D, nullptr, ldd);
+  }
   record(h, 7);
   return e;
 }

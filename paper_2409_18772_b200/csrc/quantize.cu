@@ -487,4 +487,29 @@ void launch_tensor_scale(const float* X, int64_t ldx, int64_t rows, int K, int q
   k1_tensor_scale<<<1, 1024, 0, st>>>(row_amax, (int)rows, qmax, lam_rows, inv_rows, lam_scalar); ++launch_counter();
 }
 
+// QuantTensor (Eq. gemm_r_split): the fp32 residual
+// r = fp32(x - code / lambda), formed in fp64 with a correctly rounded division and rounded once
+// to fp32 -- the GEMM operand the paper re-quantizes (oracle.qt_gemm does the same).
+__global__ void __launch_bounds__(256) k_resid_f32(const float* __restrict__ X, int64_t ldx,
+                                                   const int8_t* __restrict__ codes, int Kp,
+                                                   const float* __restrict__ lam, int64_t rows, int K,
+                                                   float* __restrict__ R) {
+  const int64_t total = rows * K;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / K;
+    const int j = (int)(e % K);
+    const double xt = __ddiv_rn((double)codes[i * Kp + j], (double)lam[i]);
+    R[e] = __double2float_rn(__dsub_rn((double)X[i * ldx + j], xt));
+  }
+}
+
+void launch_resid_f32(const float* X, int64_t ldx, const int8_t* codes, int Kp, const float* lam, int64_t rows, int K,
+                      float* R, cudaStream_t st) {
+  const int64_t total = rows * K;
+  if (total == 0) return;
+  const int g = (int)((total + 255) / 256 < 148 * 64 ? (total + 255) / 256 : 148 * 64);
+  k_resid_f32<<<g, 256, 0, st>>>(X, ldx, codes, Kp, lam, rows, K, R);
+  ++launch_counter();
+}
+
 }  // namespace lrqmm

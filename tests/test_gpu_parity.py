@@ -267,3 +267,34 @@ def test_full_call_makes_b_resident():
         h.gemm(D)
         h.sync()
         check_d(A2, Bt, {"D": D.cpu().numpy().astype(np.float64)}, ref2)
+
+
+# ------------------------------------------------ QuantTensor comparison columns
+@pytest.mark.parametrize("terms", [3, 4])
+@pytest.mark.parametrize("rounding,gran", [("trunc", "tensor"), ("floor", "row"), ("nearest", "row")])
+@pytest.mark.parametrize("bits,dist", [(4, "normal"), (8, "exp4"), (4, "u01")])
+def test_quanttensor_matches_oracle(terms, rounding, gran, bits, dist):
+    """QT(1,1,0) / QT(1,1,1) of Eq. gemm_r_split: residual re-quantized with its
+    own scale; the GPU sums 3 / 4 int8 GEMMs in fp32 (the oracle in fp64)."""
+    M, N, K = 300, 260, 900
+    A, Bt, _, _ = S.problem(M, N, K, 1, s=7, dist=dist)
+    ref = O.qt_gemm(A, Bt, bits, terms, rounding=rounding, granularity=gran)
+    with Lrqmm(M, N, K, bits, 0, 0, 1, rounding, gran, qt_terms=terms) as h:
+        h.quantize(SIDE_A, cu(A))
+        h.quantize(SIDE_B, cu(Bt))
+        D = torch.empty((M, N), device=DEV)
+        h.gemm(D)
+        h.sync()
+        d = D.cpu().numpy().astype(np.float64)
+    C = O.matmul_exact(A, Bt)
+    assert O.relative_error(ref, d) <= 1e-5
+    assert O.relative_error(C, d) <= 1.05 * O.relative_error(C, ref) + 1e-9
+
+
+def test_quanttensor_config_errors():
+    with pytest.raises(LrqmmError) as ei:
+        Lrqmm(64, 64, 64, 4, 8, 5, qt_terms=4)
+    assert ei.value.code == 10  # QT and LRQMM are alternatives
+    with pytest.raises(LrqmmError) as ei:
+        Lrqmm(64, 64, 64, 4, 0, 0, qt_terms=2)
+    assert ei.value.code == 1
