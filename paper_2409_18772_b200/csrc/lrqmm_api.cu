@@ -397,9 +397,17 @@ static lrqmm_status_t gram_step(lrqmm_handle_t h, float* const Y[2], const int64
   SmallJobs j{};
   j.n = 0;
   for (int sd = 0; sd < 2; ++sd)
-    if (sides & (1 << sd))
-      j.j[j.n++] = SmallJob{Y[sd], part_of(h, sd), nsp[sd], n[sd], h->s[sd].G, h->s[sd].gpart, h->s[sd].counter,
+    if (sides & (1 << sd)) {
+      int ns = nsp[sd];
+      // split-K partials are reduced first, in parallel over the elements (fixed order per element);
+      // the fused kernel then streams the dense Y with bulk copies
+      if (ns > 1) {
+        launch_reduce_splits(part_of(h, sd), ns, n[sd] * W, Y[sd], h->st);
+        ns = 1;
+      }
+      j.j[j.n++] = SmallJob{Y[sd], part_of(h, sd), ns, n[sd], h->s[sd].G, h->s[sd].gpart, h->s[sd].counter,
                             h->s[sd].T64, h->s[sd].VW, h->r};
+    }
   launch_fused_small(j, W, ranks ? 2 : mode, h->st);
   if (ranks) {
     lrqmm_status_t e = allreduce_f64(h, h->s[0].G, (size_t)W * W);

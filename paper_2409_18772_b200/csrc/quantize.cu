@@ -389,6 +389,168 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
   }
 }
 
+// Short rows (K < 4096, dense X): the same pipeline, but one bulk copy moves a chunk of R
+// consecutive rows (~64 KB; R K 4 is a multiple of 16 bytes) and each consumer warp owns whole
+// rows: pass 1 reduces amax from shared memory, pass 2 re-reads the row and writes codes and the
+// Q15 planes (same exact arithmetic).  kVec4: K % 4 == 0 (16-byte row alignment in the slot).
+template <bool kVec4, bool kFixedLam, int kMode>
+__global__ void __launch_bounds__(k1t::kThreads, 1)
+    k1_quantize_rows_tma(const float* __restrict__ X, int rows_full, int R, int K, int Kp, int qmax,
+                         int8_t* __restrict__ codes, float* __restrict__ lam_out, float* __restrict__ inv_out,
+                         const float* __restrict__ lam_in, int* __restrict__ err_flag, uint8_t* __restrict__ U,
+                         int64_t ldu, int64_t uplane, int ns, int slot_bytes) {
+  using namespace k1t;
+  extern __shared__ __align__(128) uint8_t smem_k1[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_k1);
+  uint64_t* empty = full + ns;
+  uint8_t* ring = smem_k1 + 1024;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int kWarps = kCons / 32;
+  if (tid == 0) {
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int nchunks = rows_full / R;
+  if (warp == kWarps) {
+    if (lane == 0) {
+      int it = 0;
+      for (int c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+        const int s = it % ns;
+        mbar_wait(&empty[s], ((it / ns) & 1) ^ 1);
+        const uint32_t bytes = (uint32_t)R * (uint32_t)K * 4u;
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_load(ring + (size_t)s * slot_bytes, X + (int64_t)c * R * K, bytes, &full[s]);
+      }
+    }
+    return;
+  }
+  int it = 0;
+  for (int c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+    const int s = it % ns;
+    mbar_wait(&full[s], (it / ns) & 1);
+    const uint8_t* slot = ring + (size_t)s * slot_bytes;
+    for (int rr = warp; rr < R; rr += kWarps) {
+      const int64_t row = (int64_t)c * R + rr;
+      const float* xr = reinterpret_cast<const float*>(slot) + (int64_t)rr * K;
+      float amax = 0.f, chk = 0.f;
+      if (kVec4) {
+        for (int f = lane; f < K / 4; f += 32) {
+          const float4 v = reinterpret_cast<const float4*>(xr)[f];
+          chk = __fmaf_rn(v.x, 0.f, __fmaf_rn(v.y, 0.f, __fmaf_rn(v.z, 0.f, __fmaf_rn(v.w, 0.f, chk))));
+          amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        }
+      } else {
+        for (int j = lane; j < K; j += 32) {
+          const float v = xr[j];
+          chk = __fmaf_rn(v, 0.f, chk);
+          amax = fmaxf(amax, fabsf(v));
+        }
+      }
+      if (chk != chk) atomicOr(err_flag, 1);
+      float lam;
+      if (kFixedLam) {
+        lam = lam_in[0];
+      } else {
+        amax = warp_max(amax);
+        lam = (amax == 0.f) ? 1.f : __fdiv_rn(static_cast<float>(qmax), amax);
+        if (lane == 0) {
+          lam_out[row] = lam;
+          inv_out[row] = __frcp_rn(lam);
+        }
+      }
+      const bool fast = lam < 0x1p100f;
+      const float l32 = lam * 32768.f;
+      int8_t* crow = codes + row * (int64_t)Kp;
+      uint8_t* urow = U ? U + row * ldu : nullptr;
+      if (kVec4) {
+        for (int f = lane; f < Kp / 4; f += 32) {
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (4 * f < K) v = reinterpret_cast<const float4*>(xr)[f];
+          const int c0 = code_fast<kMode>(lam, v.x, qmax), c1 = code_fast<kMode>(lam, v.y, qmax);
+          const int c2 = code_fast<kMode>(lam, v.z, qmax), c3 = code_fast<kMode>(lam, v.w, qmax);
+          reinterpret_cast<uint32_t*>(crow)[f] = bytes4(c0, c1, c2, c3);
+          if (urow) {
+            int i0, i1, i2, i3;
+            if (fast) {
+              i0 = q15_fast<kMode>(l32, v.x, c0); i1 = q15_fast<kMode>(l32, v.y, c1);
+              i2 = q15_fast<kMode>(l32, v.z, c2); i3 = q15_fast<kMode>(l32, v.w, c3);
+            } else {
+              i0 = u_q15_slow(lam, v.x, c0); i1 = u_q15_slow(lam, v.y, c1);
+              i2 = u_q15_slow(lam, v.z, c2); i3 = u_q15_slow(lam, v.w, c3);
+            }
+            __stcg(reinterpret_cast<uint32_t*>(urow) + f, hbytes4(i0, i1, i2, i3));
+            __stcg(reinterpret_cast<uint32_t*>(urow + uplane) + f, bytes4(i0, i1, i2, i3));
+          }
+        }
+      } else {
+        for (int j = lane; j < Kp; j += 32) {
+          const float v = j < K ? xr[j] : 0.f;
+          const int cj = code_fast<kMode>(lam, v, qmax);
+          crow[j] = (int8_t)cj;
+          if (urow) {
+            const int ij = fast ? q15_fast<kMode>(l32, v, cj) : u_q15_slow(lam, v, cj);
+            urow[j] = (uint8_t)(ij >> 8);
+            urow[uplane + j] = (uint8_t)(ij & 255);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // this warp's rows are done with the slot
+  }
+}
+
+// dense X (ldx == K), 16-byte aligned, 16 <= K < 4096: chunks of R rows per bulk copy.  Returns the
+// number of rows handled (a multiple of R); the caller quantizes the rest with the row kernels.
+static int64_t launch_k1_rows_tma(const QuantArgs& a, bool fixed, cudaStream_t st) {
+  if ((reinterpret_cast<uintptr_t>(a.X) & 15) != 0 || a.ldx != a.K || a.K < 16 || a.K >= 4096) return 0;
+  const int step = a.K % 4 == 0 ? 1 : (a.K % 2 == 0 ? 2 : 4);  // R K 4 % 16 == 0
+  int R = (16384 / a.K) / step * step;
+  if (R < step) return 0;
+  const int64_t rows_full = a.rows / R * R;
+  if (rows_full == 0 || rows_full > INT32_MAX) return 0;
+  const int slot = (R * a.K * 4 + 1023) / 1024 * 1024;
+  int ns = k1t::kSmemBudget / slot;
+  if (ns > 4) ns = 4;
+  if (ns < 2) return 0;
+  const int smem = 1024 + ns * slot;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t nchunks = rows_full / R;
+  const int grid = (int)(nchunks < nsm ? nchunks : nsm);
+  const bool v4 = a.K % 4 == 0;
+#define K1R_LAUNCH(V, F, M)                                                                                      \
+  do {                                                                                                           \
+    cudaFuncSetAttribute(k1_quantize_rows_tma<V, F, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);     \
+    k1_quantize_rows_tma<V, F, M><<<grid, k1t::kThreads, smem, st>>>(a.X, (int)rows_full, R, a.K, a.Kp, a.qmax, \
+                                                                     a.codes, a.lam, a.inv_lam, a.lam_fixed,    \
+                                                                     a.err_flag, a.U, a.ldu, a.uplane, ns, slot); \
+  } while (0)
+#define K1R_MODE(V, F)                                      \
+  do {                                                      \
+    if (a.mode == kRoundFloor) K1R_LAUNCH(V, F, kRoundFloor); \
+    else if (a.mode == kRoundTrunc) K1R_LAUNCH(V, F, kRoundTrunc); \
+    else K1R_LAUNCH(V, F, kRoundNearest);                   \
+  } while (0)
+  if (v4) {
+    if (fixed) K1R_MODE(true, true); else K1R_MODE(true, false);
+  } else {
+    if (fixed) K1R_MODE(false, true); else K1R_MODE(false, false);
+  }
+#undef K1R_MODE
+#undef K1R_LAUNCH
+  ++launch_counter();
+  return rows_full;
+}
+
 template <int VPT>
 static bool launch_k1_tma_t(const QuantArgs& a, bool fixed, cudaStream_t st) {
   const int slot = (a.K * 4 + 1023) / 1024 * 1024;
@@ -454,14 +616,38 @@ static void launch_k1_t(const QuantArgs& a, bool vec, bool fixed, cudaStream_t s
   ++launch_counter();
 }
 
+void launch_quantize_rows(const QuantArgs& a, bool fixed, cudaStream_t st);
+
 void launch_quantize(const QuantArgs& a, cudaStream_t st) {
   if (a.rows == 0) return;
-  const bool vec = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
   const bool fixed = a.lam_fixed != nullptr;
-  const int Kp = a.Kp;
 #ifndef LRQMM_K1_NO_TMA
   if (launch_k1_tma(a, fixed, st)) return;
+  {
+    const int64_t done = launch_k1_rows_tma(a, fixed, st);
+    if (done == a.rows) return;
+    if (done > 0) {  // the ragged tail rows: register-row kernels on the remaining rows
+      QuantArgs t = a;
+      t.X = a.X + done * a.ldx;
+      t.rows = a.rows - done;
+      t.codes = a.codes + done * (int64_t)a.Kp;
+      if (!fixed) {
+        t.lam = a.lam + done;
+        t.inv_lam = a.inv_lam + done;
+      }
+      if (a.U) t.U = a.U + done * a.ldu;
+      launch_quantize_rows(t, fixed, st);
+      return;
+    }
+  }
 #endif
+  launch_quantize_rows(a, fixed, st);
+}
+
+// register-row kernels (one CTA / warp group per row), any alignment / stride
+void launch_quantize_rows(const QuantArgs& a, bool fixed, cudaStream_t st) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
+  const int Kp = a.Kp;
   if (Kp <= 32 * 4 * 1) launch_k1_t<32, 1>(a, vec, fixed, st);
   else if (Kp <= 32 * 4 * 2) launch_k1_t<32, 2>(a, vec, fixed, st);
   else if (Kp <= 32 * 4 * 4) launch_k1_t<32, 4>(a, vec, fixed, st);

@@ -480,6 +480,14 @@ __global__ void k_reduce_splits_tc(const float* __restrict__ part, int nsplit, i
   }
 }
 
+// fixed-order sum of nsplit partial planes into out (n elements), grid over elements
+void launch_reduce_splits(const float* part, int nsplit, int64_t n, float* out, cudaStream_t st) {
+  if (n == 0) return;
+  const int g = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+  k_reduce_splits_tc<<<g, 256, 0, st>>>(part, nsplit, n, out);
+  ++launch_counter();
+}
+
 // one image: ceil(n / BK) k-block images, then colmax (64 x u32) and cinv (64 x f32)
 int64_t tc_img_bytes(int64_t n, int W) {
   const int WN = W <= 32 ? 32 : 64;

@@ -522,15 +522,15 @@ __global__ void __launch_bounds__(32) k_warp_chol(EigJobs jobs) {
 //   phase 2 (last block by ticket): fixed-order sum of the Gram partials -> G, then the
 //                         pivoted CholQR transform (mode 0) or the truncation eigenvectors
 //                         (mode 1), or nothing (mode 2: G must first be summed across ranks).
-// rows per shared-memory chunk: as many as the 66.5 KB dynamic buffer holds in fp64
-__host__ __device__ constexpr int frows(int w) { return w <= 24 ? 256 : (w <= 48 ? 128 : 64); }
+// rows per shared-memory chunk (fp32, two buffers in the 66.5 KB dynamic allocation)
+__host__ __device__ constexpr int frows(int w) { return w <= 32 ? 256 : 128; }
 template <int W>
 __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
   constexpr int kFRows = frows(W);
-  extern __shared__ double dyn[];
+  extern __shared__ __align__(128) double dyn[];
   const SmallJob jb = jobs.j[blockIdx.y];
-  constexpr int kLd = W + 2;                      // fp64 row stride: 16-byte aligned rows
-  double (*sY)[kLd] = reinterpret_cast<double (*)[kLd]>(dyn);  // kFRows x kLd, fp64 (converted once)
+  float* buf = reinterpret_cast<float*>(dyn);  // 2 x kFRows x W fp32 (bulk-copied chunks of Y)
+  __shared__ uint64_t ld_bar[2];
   __shared__ int ticket;
   constexpr int npairs = W * W;
   // Gram in 4 x 4 register tiles: tile (a, c), a <= c, of T x T tiles; G row groups per block
@@ -550,64 +550,47 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
   const int64_t rpb = (jb.n + gridDim.x - 1) / gridDim.x;
   const int64_t r_begin = (int64_t)blockIdx.x * rpb;
   const int64_t r_end = (jb.n < r_begin + rpb) ? jb.n : r_begin + rpb;
-  const int64_t plane = jb.n * W;
+  const int nchunk = r_end > r_begin ? (int)((r_end - r_begin + kFRows - 1) / kFRows) : 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&ld_bar[0], 1);
+    mbar_init(&ld_bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // Y is final and dense (split partials were reduced beforehand): chunk c of this block is one
+  // contiguous bulk copy, double-buffered so that chunk c+1 lands while chunk c is multiplied
+  auto issue = [&](int c) {
+    const int64_t r0 = r_begin + (int64_t)c * kFRows;
+    const int nr = (int)(r_end - r0 < kFRows ? r_end - r0 : kFRows);
+    const uint32_t bytes = (uint32_t)nr * W * 4u;
+    mbar_arrive_expect_tx(&ld_bar[c & 1], bytes);
+    bulk_load(buf + (c & 1) * kFRows * W, jb.Y + r0 * W, bytes, &ld_bar[c & 1]);
+  };
+  if (threadIdx.x == 0) {
+    if (nchunk > 0) issue(0);
+    if (nchunk > 1) issue(1);
+  }
   double acc[16];
 #pragma unroll
   for (int q = 0; q < 16; ++q) acc[q] = 0.0;
-  for (int64_t r0 = r_begin; r0 < r_end; r0 += kFRows) {
+  for (int c = 0; c < nchunk; ++c) {
+    const int64_t r0 = r_begin + (int64_t)c * kFRows;
     const int nr = (int)(r_end - r0 < kFRows ? r_end - r0 : kFRows);
-    __syncthreads();
-    // element e of the chunk: thread-strided; the split partials of several elements are
-    // loaded before any is summed (fixed summation order per element: s = 0, 1, ...)
-    const int ne = nr * W;
-    for (int e0 = threadIdx.x; e0 < ne; e0 += 256 * 4) {
-      float v[4] = {0.f, 0.f, 0.f, 0.f};
-      if (jb.nsplit > 1) {
-        for (int sp0 = 0; sp0 < jb.nsplit; sp0 += 8) {
-          float t[4][8];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int e = e0 + 256 * u;
-            const int64_t g = r0 * W + e;
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              t[u][k] = (e < ne && sp0 + k < jb.nsplit) ? __ldcg(jb.part + (sp0 + k) * plane + g) : 0.f;
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int k = 0; k < 8; ++k) v[u] += t[u][k];
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = e0 + 256 * u;
-          if (e < ne) v[u] = __ldcg(jb.Y + r0 * W + e);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int e = e0 + 256 * u;
-        if (e < ne) {
-          if (jb.nsplit > 1) jb.Y[r0 * W + e] = v[u];
-          sY[e / W][e % W] = (double)v[u];
-        }
-      }
-    }
-    __syncthreads();
+    mbar_wait(&ld_bar[c & 1], (c >> 1) & 1);
+    const float* bY = buf + (c & 1) * kFRows * W;
     if (gram_thread) {
       for (int i = tg; i < nr; i += G) {
-        const double2 x0 = *reinterpret_cast<const double2*>(&sY[i][4 * ta]);
-        const double2 x1 = *reinterpret_cast<const double2*>(&sY[i][4 * ta + 2]);
-        const double2 y0 = *reinterpret_cast<const double2*>(&sY[i][4 * tc]);
-        const double2 y1 = *reinterpret_cast<const double2*>(&sY[i][4 * tc + 2]);
-        const double xa[4] = {x0.x, x0.y, x1.x, x1.y}, yc[4] = {y0.x, y0.y, y1.x, y1.y};
+        const float4 x4 = *reinterpret_cast<const float4*>(bY + i * W + 4 * ta);
+        const float4 y4 = *reinterpret_cast<const float4*>(bY + i * W + 4 * tc);
+        const double xa[4] = {x4.x, x4.y, x4.z, x4.w}, yc[4] = {y4.x, y4.y, y4.z, y4.w};
 #pragma unroll
         for (int p = 0; p < 4; ++p)
 #pragma unroll
           for (int q = 0; q < 4; ++q) acc[p * 4 + q] = fma(xa[p], yc[q], acc[p * 4 + q]);
       }
     }
+    __syncthreads();  // every thread is done with buffer (c & 1): refill it with chunk c + 2
+    if (threadIdx.x == 0 && c + 2 < nchunk) issue(c + 2);
   }
   // fixed-order reduction of the G row groups of each tile, then the block partial (both halves)
   __syncthreads();
@@ -683,6 +666,8 @@ void launch_fused_small(const SmallJobs& jobs, int W, int mode, cudaStream_t st)
   // ~2 row chunks per block, at most 2 blocks per SM: the last block sums <= 296 partials
   const int fr = frows(W);
   int64_t nb = (nmax + 2 * fr - 1) / (2 * fr);
+  for (int i = 0; i < jobs.n; ++i)
+    if (jobs.j[i].nsplit != 1) return;  // contract: Y is reduced before the fused kernel
   if (nb > 296) nb = 296;
   if (nb > kGramMaxBlocks) nb = kGramMaxBlocks;
   if (nb < 1) nb = 1;
