@@ -398,14 +398,16 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
     k1_quantize_rows_tma(const float* __restrict__ X, int rows_full, int R, int K, int Kp, int qmax,
                          int8_t* __restrict__ codes, float* __restrict__ lam_out, float* __restrict__ inv_out,
                          const float* __restrict__ lam_in, int* __restrict__ err_flag, uint8_t* __restrict__ U,
-                         int64_t ldu, int64_t uplane, int ns, int slot_bytes) {
+                         int64_t ldu, int64_t uplane, int ns, int slot_bytes, int L) {
   using namespace k1t;
   extern __shared__ __align__(128) uint8_t smem_k1[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_k1);
   uint64_t* empty = full + ns;
   uint8_t* ring = smem_k1 + 1024;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5, lane_w = tid & 31;
   constexpr int kWarps = kCons / 32;
+  // L lanes per row (a power of two <= 32): a warp quantizes 32 / L rows at a time
+  const int sub_l = lane_w % L, grp = lane_w / L, rpw = 32 / L;
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
       mbar_init(&full[s], 1);
@@ -416,7 +418,7 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
   __syncthreads();
   const int nchunks = rows_full / R;
   if (warp == kWarps) {
-    if (lane == 0) {
+    if (lane_w == 0) {
       int it = 0;
       for (int c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
         const int s = it % ns;
@@ -433,18 +435,22 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
     const int s = it % ns;
     mbar_wait(&full[s], (it / ns) & 1);
     const uint8_t* slot = ring + (size_t)s * slot_bytes;
-    for (int rr = warp; rr < R; rr += kWarps) {
+    // uniform trip count across the warp (the lane groups' shuffles must all execute)
+    for (int rb = warp * rpw; rb < R; rb += kWarps * rpw) {
+      const int rr = rb + grp;
+      const bool active = rr < R;
+      const int lane = sub_l;
       const int64_t row = (int64_t)c * R + rr;
-      const float* xr = reinterpret_cast<const float*>(slot) + (int64_t)rr * K;
+      const float* xr = reinterpret_cast<const float*>(slot) + (int64_t)(active ? rr : 0) * K;
       float amax = 0.f, chk = 0.f;
       if (kVec4) {
-        for (int f = lane; f < K / 4; f += 32) {
+        for (int f = lane; active && f < K / 4; f += L) {
           const float4 v = reinterpret_cast<const float4*>(xr)[f];
           chk = __fmaf_rn(v.x, 0.f, __fmaf_rn(v.y, 0.f, __fmaf_rn(v.z, 0.f, __fmaf_rn(v.w, 0.f, chk))));
           amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
         }
       } else {
-        for (int j = lane; j < K; j += 32) {
+        for (int j = lane; active && j < K; j += L) {
           const float v = xr[j];
           chk = __fmaf_rn(v, 0.f, chk);
           amax = fmaxf(amax, fabsf(v));
@@ -455,19 +461,20 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
       if (kFixedLam) {
         lam = lam_in[0];
       } else {
-        amax = warp_max(amax);
+        for (int o = L >> 1; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
         lam = (amax == 0.f) ? 1.f : __fdiv_rn(static_cast<float>(qmax), amax);
-        if (lane == 0) {
+        if (active && lane == 0) {
           lam_out[row] = lam;
           inv_out[row] = __frcp_rn(lam);
         }
       }
+      if (!active) continue;
       const bool fast = lam < 0x1p100f;
       const float l32 = lam * 32768.f;
       int8_t* crow = codes + row * (int64_t)Kp;
       uint8_t* urow = U ? U + row * ldu : nullptr;
       if (kVec4) {
-        for (int f = lane; f < Kp / 4; f += 32) {
+        for (int f = lane; f < Kp / 4; f += L) {
           float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
           if (4 * f < K) v = reinterpret_cast<const float4*>(xr)[f];
           const int c0 = code_fast<kMode>(lam, v.x, qmax), c1 = code_fast<kMode>(lam, v.y, qmax);
@@ -487,7 +494,7 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
           }
         }
       } else {
-        for (int j = lane; j < Kp; j += 32) {
+        for (int j = lane; j < Kp; j += L) {
           const float v = j < K ? xr[j] : 0.f;
           const int cj = code_fast<kMode>(lam, v, qmax);
           crow[j] = (int8_t)cj;
@@ -500,7 +507,7 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);  // this warp's rows are done with the slot
+    if (lane_w == 0) mbar_arrive(&empty[s]);  // this warp's rows are done with the slot
   }
 }
 
@@ -527,12 +534,15 @@ static int64_t launch_k1_rows_tma(const QuantArgs& a, bool fixed, cudaStream_t s
   const int64_t nchunks = rows_full / R;
   const int grid = (int)(nchunks < nsm ? nchunks : nsm);
   const bool v4 = a.K % 4 == 0;
+  int L = 32;  // lanes per row: the smallest power of two covering the row's float4s (vec4 path)
+  if (v4)
+    while (L > 1 && L / 2 >= a.K / 4) L /= 2;
 #define K1R_LAUNCH(V, F, M)                                                                                      \
   do {                                                                                                           \
     cudaFuncSetAttribute(k1_quantize_rows_tma<V, F, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);     \
     k1_quantize_rows_tma<V, F, M><<<grid, k1t::kThreads, smem, st>>>(a.X, (int)rows_full, R, a.K, a.Kp, a.qmax, \
                                                                      a.codes, a.lam, a.inv_lam, a.lam_fixed,    \
-                                                                     a.err_flag, a.U, a.ldu, a.uplane, ns, slot); \
+                                                                     a.err_flag, a.U, a.ldu, a.uplane, ns, slot, L); \
   } while (0)
 #define K1R_MODE(V, F)                                      \
   do {                                                      \

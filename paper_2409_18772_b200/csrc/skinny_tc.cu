@@ -480,11 +480,42 @@ __global__ void k_reduce_splits_tc(const float* __restrict__ part, int nsplit, i
   }
 }
 
-// fixed-order sum of nsplit partial planes into out (n elements), grid over elements
+// many splits: 32 consecutive elements x 8 split groups per block (coalesced 128-byte rows),
+// group g sums splits g, g + 8, ... in order, then the 8 group sums are added in order
+__global__ void __launch_bounds__(256) k_reduce_splits_wide(const float* __restrict__ part, int nsplit, int64_t n,
+                                                            float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const int e_l = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * 32 + e_l;
+  float acc = 0.f;
+  if (e < n) {
+    int s = g;
+    for (; s + 24 < nsplit; s += 32) {  // 4 independent loads in flight, summed in split order
+      const float a0 = __ldcg(part + (int64_t)s * n + e), a1 = __ldcg(part + (int64_t)(s + 8) * n + e);
+      const float a2 = __ldcg(part + (int64_t)(s + 16) * n + e), a3 = __ldcg(part + (int64_t)(s + 24) * n + e);
+      acc += a0; acc += a1; acc += a2; acc += a3;
+    }
+    for (; s < nsplit; s += 8) acc += __ldcg(part + (int64_t)s * n + e);
+  }
+  red[g][e_l] = acc;
+  __syncthreads();
+  if (g == 0 && e < n) {
+    float t = red[0][e_l];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) t += red[k][e_l];
+    out[e] = t;
+  }
+}
+
+// fixed-order sum of nsplit partial planes into out (n elements)
 void launch_reduce_splits(const float* part, int nsplit, int64_t n, float* out, cudaStream_t st) {
   if (n == 0) return;
-  const int g = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
-  k_reduce_splits_tc<<<g, 256, 0, st>>>(part, nsplit, n, out);
+  if (nsplit > 16) {
+    k_reduce_splits_wide<<<(unsigned)((n + 31) / 32), 256, 0, st>>>(part, nsplit, n, out);
+  } else {
+    const int g = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+    k_reduce_splits_tc<<<g, 256, 0, st>>>(part, nsplit, n, out);
+  }
   ++launch_counter();
 }
 
@@ -568,6 +599,7 @@ static int run_tc(const SideView& s, const float* P1, const float* P2, int W, fl
   int64_t ns = (6LL * nsm + nblk - 1) / nblk;
   const int64_t maxs = (rlen + 4 * BK - 1) / (4 * BK);
   if (ns > maxs) ns = maxs;
+  if (ns > 256) ns = 256;  // few output blocks (short K in COL mode): bound the partials to reduce
   const int64_t per = a.nout * W * (kVar == 1 ? 2 : 1);
   if (ns > 1 && ns * per > pe) ns = pe / per;
   const int64_t mins = (rlen + kMaxChunk - 1) / kMaxChunk;
@@ -595,14 +627,9 @@ static int run_tc(const SideView& s, const float* P1, const float* P2, int W, fl
   if (ns > 1) {
     const int64_t n = a.nout * W;
     const int g = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
-    if (reduce1 && kHasU) {
-      k_reduce_splits_tc<<<g, 256, 0, st>>>(partial, (int)ns, n, OUT1);
-      ++launch_counter();
-    }
-    if (kHasC) {
-      k_reduce_splits_tc<<<g, 256, 0, st>>>(kVar == 2 ? partial : partial + ns * a.nout * W, (int)ns, n, OUT2);
-      ++launch_counter();
-    }
+    (void)g;
+    if (reduce1 && kHasU) launch_reduce_splits(partial, (int)ns, n, OUT1, st);
+    if (kHasC) launch_reduce_splits(kVar == 2 ? partial : partial + ns * a.nout * W, (int)ns, n, OUT2, st);
   }
   return (int)ns;
 }
