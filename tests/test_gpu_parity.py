@@ -298,3 +298,42 @@ def test_quanttensor_config_errors():
     with pytest.raises(LrqmmError) as ei:
         Lrqmm(64, 64, 64, 4, 0, 0, qt_terms=2)
     assert ei.value.code == 1
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("r,p", [(32, 32), (30, 2), (8, 24)])
+def test_widest_sketch_w64(r, p):
+    """r + p up to 64 (W = 64: the NA = 2 pass kernels, 2-group epilogues, 64-wide solves)."""
+    A, Bt, OmA, OmB = S.problem(384, 320, 700, r + p, s=60, dist="normal")
+    ref = O.lrqmm(A, Bt, 4, r, OmA, OmB, q=1)
+    check_d(A, Bt, run_gpu(A, Bt, 4, r, p, OmA, OmB), ref)
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 200, 300), (200, 1, 300), (130, 150, 1), (130, 150, 7), (129, 257, 16)])
+def test_degenerate_shapes_direct_quant(M, N, K):
+    """Single rows / columns, K below one 16-byte code row and below one 128-deep MMA step."""
+    A, Bt, _, _ = S.problem(M, N, K, 1, s=61, dist="u11")
+    out = run_gpu(A, Bt, 8, 0, 0)
+    ca, la = O.quantize(A, 8)
+    cb, lb = O.quantize(Bt, 8)
+    assert np.array_equal(out["codes_a"].astype(np.int64), ca)
+    assert np.array_equal(out["c_int"].astype(np.int64), O.int_gemm(ca, cb))
+    ref = O.lrqmm(A, Bt, 8, 0)
+    assert O.relative_error(ref, out["D"]) <= 1e-6
+
+
+def test_rank_at_the_limit():
+    """r + p = min(rows, K) with r at its cap of 32: the largest sketch accepted."""
+    M, N, K, r, p = 300, 280, 40, 32, 8
+    A, Bt, OmA, OmB = S.problem(M, N, K, r + p, s=62, dist="exp4")
+    ref = O.lrqmm(A, Bt, 4, r, OmA, OmB, q=1)
+    check_d(A, Bt, run_gpu(A, Bt, 4, r, p, OmA, OmB), ref)
+
+
+def test_empty_problem_is_a_no_op():
+    with Lrqmm(0, 64, 128, 4, 0, 0) as h:
+        h.quantize(SIDE_A, torch.empty((0, 128), device=DEV))
+        h.quantize(SIDE_B, cu(S.gen_matrix("normal", 64, 128, 1)))
+        D = torch.empty((0, 64), device=DEV)
+        h.gemm(D)
+        h.sync()
