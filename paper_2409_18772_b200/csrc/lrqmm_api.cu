@@ -233,7 +233,7 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
       ok = ok && dalloc(&s.U, 2 * s.rows * s.ldu) && dalloc(&s.Om, K * h->W) && dalloc(&s.Y, s.rows * h->W) && dalloc(&s.Q0, s.rows * h->W) &&
            dalloc(&s.Z, K * h->W) && dalloc(&s.Q1, K * h->W) && dalloc(&s.Gp, s.rows * h->W) &&
            dalloc(&s.G, (int64_t)h->W * h->W) && dalloc(&s.gpart, (int64_t)kGramMaxBlocks * h->W * h->W) &&
-           dalloc(&s.counter, 1) && dalloc(&s.T64, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W) &&
+           dalloc(&s.counter, 64) && dalloc(&s.T64, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W) &&
            dalloc(&s.img, 2 * tc_img_bytes(std::max<int64_t>(s.rows, K), h->W));
     }
     if (cfg->qt_terms > 0)

@@ -613,27 +613,36 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
     part[i * W + j] = sum;  // diagonal tiles: (p, q) and (q, p) hold bitwise-equal sums
     part[j * W + i] = sum;
   }
+  // two-level fixed-order reduction of the block partials: the last block of each group of 16
+  // sums its group (-> gpart[nb + g]), the last group finisher sums the groups (-> G).  Counters:
+  // counter[0] = groups done, counter[1 + g] = blocks of group g done (all re-armed to 0).
+  const int nb = (int)gridDim.x;
+  const int grp = blockIdx.x / 16, ngrp = (nb + 15) / 16;
+  const int gsize = nb - 16 * grp < 16 ? nb - 16 * grp : 16;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(jb.counter + 1 + grp, 1);
+  __syncthreads();
+  if (ticket != gsize - 1) return;
+  __threadfence();
+  for (int pr = threadIdx.x; pr < npairs; pr += 256) {
+    double a = 0.0;
+    for (int b = 16 * grp; b < 16 * grp + gsize; ++b) a += __ldcg(jb.gpart + (int64_t)b * npairs + pr);
+    jb.gpart[(int64_t)(nb + grp) * npairs + pr] = a;
+  }
+  if (threadIdx.x == 0) jb.counter[1 + grp] = 0;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) ticket = atomicAdd(jb.counter, 1);
   __syncthreads();
-  if (ticket != (int)gridDim.x - 1) return;
+  if (ticket != ngrp - 1) return;
   __threadfence();
-  const int nb = (int)gridDim.x;
   for (int pr = threadIdx.x; pr < npairs; pr += 256) {
-    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    int b = 0;
-    for (; b + 7 < nb; b += 8) {
-      double t[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) t[k] = __ldcg(jb.gpart + (int64_t)(b + k) * npairs + pr);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) a[k] += t[k];
-    }
-    for (; b < nb; ++b) a[0] += __ldcg(jb.gpart + (int64_t)b * npairs + pr);
-    jb.G[pr] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    double a = 0.0;
+    for (int g = 0; g < ngrp; ++g) a += __ldcg(jb.gpart + (int64_t)(nb + g) * npairs + pr);
+    jb.G[pr] = a;
   }
-  if (threadIdx.x == 0) *jb.counter = 0;  // re-arm for the next launch (stream ordered)
+  if (threadIdx.x == 0) jb.counter[0] = 0;  // re-arm for the next launch (stream ordered)
   __threadfence_block();
   __syncthreads();
   if constexpr (W <= 32) {
@@ -668,7 +677,7 @@ void launch_fused_small(const SmallJobs& jobs, int W, int mode, cudaStream_t st)
   int64_t nb = (nmax + 2 * fr - 1) / (2 * fr);
   for (int i = 0; i < jobs.n; ++i)
     if (jobs.j[i].nsplit != 1) return;  // contract: Y is reduced before the fused kernel
-  if (nb > 296) nb = 296;
+  if (nb > 444) nb = 444;  // three resident blocks per SM (66.5 KB each)
   if (nb > kGramMaxBlocks) nb = kGramMaxBlocks;
   if (nb < 1) nb = 1;
   switch (W) {
