@@ -25,15 +25,11 @@ namespace lrqmm {
 
 namespace g6 {
 constexpr int BM = 128;
-constexpr int BN = 256;
+constexpr int BN = 256;  // widest tile (the BN template parameter picks 64 / 128 / 256 by N)
 constexpr int BK = 128;  // bytes = int8 elements per stage (one 128B swizzle atom row)
 constexpr int UK = 32;   // K per tcgen05.mma kind::i8
-constexpr int kThreads = 192;
-constexpr int kEpiThreads = 128;
+constexpr int kEpiThreads = 128;  // one epilogue group: one warp per TMEM lane quarter
 constexpr int kABytes = BM * BK;
-constexpr int kBBytes = BN * BK;
-constexpr int kStageBytes = kABytes + kBBytes;
-constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
 #ifndef LRQMM_L2HINT
 #define LRQMM_L2HINT 2  // 1: A evict_last + B evict_first, 2: A evict_last only
 #endif
@@ -41,11 +37,28 @@ constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
 #define LRQMM_GROUPM 16
 #endif
 constexpr int kGroupM = LRQMM_GROUPM;  // tile rasterisation: M-blocks per group (L2 reuse)
-// 4 smem stages while the L_B tile fits beside them, 3 for the widest corrections
-__host__ __device__ constexpr int stages_for(int r2) { return r2 > 32 ? 3 : 4; }
-__host__ __device__ constexpr int smem_bytes(int r2) {
-  return stages_for(r2) * kStageBytes + BN * r2 * 4 + BN * 4 + 256 /*barriers*/ + 1024 /*align*/;
+__host__ __device__ constexpr int stage_bytes(int bn) { return kABytes + bn * BK; }
+__host__ __device__ constexpr int staging_bytes(int r2, int bn) { return bn * r2 * 4 + bn * 4; }
+// epilogue groups = TMEM accumulators: up to 4 (512 columns / BN), each with its own L_B /
+// 1/lambda_B staging, as long as >= 3 smem stages still fit; at least 2 accumulators always
+__host__ __device__ constexpr int fits_groups(int g, int r2, int bn) {
+  return (232448 - (g * staging_bytes(r2, bn) + 1280)) / stage_bytes(bn) >= 3;
 }
+__host__ __device__ constexpr int epi_groups(int r2, int bn) {
+  return (512 / bn >= 4 && fits_groups(4, r2, bn)) ? 4 : (fits_groups(2, r2, bn) ? 2 : 1);
+}
+__host__ __device__ constexpr int num_acc(int r2, int bn) { return epi_groups(r2, bn) < 2 ? 2 : epi_groups(r2, bn); }
+__host__ __device__ constexpr int threads_for(int r2, int bn) { return 64 + 128 * epi_groups(r2, bn); }
+__host__ __device__ constexpr int extra_bytes(int r2, int bn) {
+  return epi_groups(r2, bn) * staging_bytes(r2, bn) + 256 + 1024;
+}
+// as many smem stages as fit beside the L_B tile(s), at most 8
+__host__ __device__ constexpr int stages_for(int r2, int bn) {
+  return (232448 - extra_bytes(r2, bn)) / stage_bytes(bn) > 8 ? 8 : (232448 - extra_bytes(r2, bn)) / stage_bytes(bn);
+}
+__host__ __device__ constexpr int smem_bytes(int r2, int bn) { return stages_for(r2, bn) * stage_bytes(bn) + extra_bytes(r2, bn); }
+// accumulators of bn columns, rounded to the power-of-two allocation granule
+__host__ __device__ constexpr uint32_t tmem_cols(int cols) { return cols <= 128 ? 128 : (cols <= 256 ? 256 : 512); }
 }  // namespace g6
 
 struct G6Params {
@@ -76,7 +89,10 @@ LRQMM_DEV void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
   nb = in / gsize;
 }
 
-LRQMM_DEV void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(g6::kEpiThreads) : "memory"); }
+template <int kN = g6::kEpiThreads>
+LRQMM_DEV void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kN) : "memory"); }
+// named barrier `id` over one epilogue group (128 threads)
+LRQMM_DEV void epi_bar_id(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(g6::kEpiThreads) : "memory"); }
 
 // one 8-column group of one output row: acc (int32 from TMEM) -> D or Cint.
 // Kept small and rolled (the 256-column tile is walked in 32 groups) so the
@@ -138,24 +154,27 @@ LRQMM_DEV void epilogue_group(const G6Params& p, const uint32_t (&acc)[8], int64
   }
 }
 
-template <int kR2>
-__global__ void __launch_bounds__(g6::kThreads, 1)
+template <int kR2, int BN>
+__global__ void __launch_bounds__(g6::threads_for(kR2, BN), 1)
     k6_gemm_i8(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, G6Params p) {
-  using namespace g6;
-  constexpr int STAGES = stages_for(kR2);
+  using g6::BM; using g6::BK; using g6::UK; using g6::kABytes; using g6::kEpiThreads;
+  constexpr int kBBytes = BN * BK;
+  constexpr int kStageBytes = kABytes + kBBytes;
+  constexpr int NACC = g6::num_acc(kR2, BN);
+  constexpr uint32_t kTmemCols = g6::tmem_cols(NACC * BN);
+  constexpr int STAGES = g6::stages_for(kR2, BN);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * kABytes;
-  float* sLB = reinterpret_cast<float*>(smem + STAGES * kStageBytes);  // BN x kR2
-  float* sSB = sLB + BN * kR2;                                           // BN : 1/lambda_b
-  const uint32_t sLBa = smem_u32(sLB), sSBa = smem_u32(sSB);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sSB + BN);
+  constexpr int EG = g6::epi_groups(kR2, BN);
+  float* sLB0 = reinterpret_cast<float*>(smem + STAGES * kStageBytes);  // EG groups x (BN x kR2 | BN)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sLB0 + EG * (BN * kR2 + BN));
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
-  uint64_t* tfull = bars + 2 * STAGES;
-  uint64_t* tempty = bars + 2 * STAGES + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  uint64_t* tfull = bars + 2 * STAGES;         // NACC
+  uint64_t* tempty = tfull + NACC;             // NACC
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -168,7 +187,7 @@ __global__ void __launch_bounds__(g6::kThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiThreads);
     }
@@ -221,8 +240,8 @@ __global__ void __launch_bounds__(g6::kThreads, 1)
       uint32_t phase = 0;
       int lt = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
-        const int acc = lt & 1;
-        const uint32_t acc_phase = (lt >> 1) & 1;
+        const int acc = lt % NACC;
+        const uint32_t acc_phase = (lt / NACC) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -246,14 +265,20 @@ __global__ void __launch_bounds__(g6::kThreads, 1)
     __syncwarp();
   } else {
     // ---------------------------------------------------------------- epilogue
-    const int et = threadIdx.x - 64;  // 0..127
-    const int quad = warp & 3;        // TMEM lane quadrant this warp may access
-    int lt = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+    // two groups of 4 warps; group e owns accumulator buffer e and this CTA's tiles lt = e, e+2, ...
+    // so one group's staging (L_A rows, L_B tile: global-memory latency) overlaps the other's math
+    // (EG == 1 when two staging buffers do not fit beside 3 stages: group 0 takes every tile)
+    const int egrp = (warp - 2) >> 2;
+    const int et = threadIdx.x - 64 - 128 * egrp;  // 0..127 within the group
+    const int quad = warp & 3;                      // TMEM lane quadrant this warp may access
+    const uint32_t sLBa = smem_u32(sLB0 + (egrp < EG ? egrp : 0) * (BN * kR2 + BN));
+    const uint32_t sSBa = sLBa + 4 * BN * kR2;
+    int lt = egrp;
+    for (int t = blockIdx.x + egrp * gridDim.x; egrp < EG && t < num_tiles; t += EG * gridDim.x, lt += EG) {
       int mb, nb;
       tile_coords(t, p.num_m, p.num_n, mb, nb);
-      const int acc = lt & 1;
-      const uint32_t acc_phase = (lt >> 1) & 1;
+      const int acc = lt % NACC;
+      const uint32_t acc_phase = (lt / NACC) & 1;
       const int64_t row = (int64_t)mb * BM + quad * 32 + lane;
       const int n0 = nb * BN;
       float sa = 0.f;
@@ -262,7 +287,7 @@ __global__ void __launch_bounds__(g6::kThreads, 1)
       for (int l = 0; l < (kR2 > 0 ? kR2 : 1); ++l) la[l] = 0.f;
       if (p.epi == 1) {
         // stage this tile's column data (L_B rows, 1/lambda_b) while the mainloop runs
-        epi_bar();  // previous tile's readers are done
+        epi_bar_id(1 + egrp);  // previous tile's readers are done
         for (int j = et; j < BN; j += kEpiThreads) {
           const int col = n0 + j;
           const float v = col < p.N ? __ldg(p.inv_b + col) : 0.f;
@@ -286,7 +311,7 @@ __global__ void __launch_bounds__(g6::kThreads, 1)
             }
           }
         }
-        epi_bar();  // staged data visible to all epilogue warps
+        epi_bar_id(1 + egrp);  // staged data visible to the group
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -310,7 +335,7 @@ __global__ void __launch_bounds__(g6::kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_free<g6::kTmemCols>(tmem_base);
+    tmem_free<kTmemCols>(tmem_base);
   }
 }
 
@@ -448,7 +473,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int num_tiles = p.num_m * p.num_n;  // pair tiles (256 x 256)
   const bool pair_rel = LRQMM_PAIR_RELEASE && (p.num_kb & 1) == 0;  // a tile always starts on an even stage
 
@@ -583,7 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
       const int q = lt % kTR;
       mbar_wait(&tfull_t[q], (lt / kTR) & 1);
       const int t = tile_ring[q];
-      epi_bar();  // every epilogue thread has read the index
+      epi_bar<g7::kEpiThreads>();  // every epilogue thread has read the index
       if (et == 0) mbar_arrive_remote(tempty_t0 + 8 * q);
       if (t >= num_tiles) break;
       int mb, nb;
@@ -597,7 +621,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
 #pragma unroll
       for (int l = 0; l < (kR2 > 0 ? kR2 : 1); ++l) la[l] = 0.f;
       if (p.epi == 1) {
-        epi_bar();
+        epi_bar<g7::kEpiThreads>();
         for (int j = et; j < BN; j += kEpiThreads) {
           const int col = n0 + j;
           const float v = col < p.N ? __ldg(p.inv_b + col) : 0.f;
@@ -621,7 +645,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
             }
           }
         }
-        epi_bar();
+        epi_bar<g7::kEpiThreads>();
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -739,27 +763,41 @@ static bool use_2sm(int64_t M, int64_t N, const int* sched) {
   return M >= 512 && N >= 512;
 }
 
-// mapA/mapB hold the K6 maps (box rows 128 / 256); mapA2/mapB2 the K7 maps (128 / 128)
+// map slots: [0] K6 (A box rows 128, B 256), [1] K7 (128 / 128), [2] K6 B box 128, [3] K6 B box 64
 int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB) {
   CUtensorMap* m = reinterpret_cast<CUtensorMap*>(mapA);
   CUtensorMap* n = reinterpret_cast<CUtensorMap*>(mapB);
   if (encode_codes_map(m, g.A, g.M, g.Kp, g6::BM)) return 1;
-  if (encode_codes_map(n, g.B, g.N, g.Kp, g6::BN)) return 1;
+  if (encode_codes_map(n, g.B, g.N, g.Kp, 256)) return 1;
   if (encode_codes_map(m + 1, g.A, g.M, g.Kp, g7::BM)) return 1;
   if (encode_codes_map(n + 1, g.B, g.N, g.Kp, g7::BNH)) return 1;
+  if (encode_codes_map(n + 2, g.B, g.N, g.Kp, 128)) return 1;
+  if (encode_codes_map(n + 3, g.B, g.N, g.Kp, 64)) return 1;
   return 0;
 }
 
-template <int kR2>
-static void launch_t(const G6Params& p, const CUtensorMap* mA, const CUtensorMap* mB, int grid, cudaStream_t st) {
-  constexpr int kSmem = g6::smem_bytes(kR2);
+template <int kR2, int BN>
+static void launch_t(G6Params p, const CUtensorMap* mA, const CUtensorMap* mB, int nsm, cudaStream_t st) {
+  constexpr int kSmem = g6::smem_bytes(kR2, BN);
   static_assert(kSmem <= 232448, "shared memory budget");
+  static_assert(g6::stages_for(kR2, BN) >= 3, "stages");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k6_gemm_i8<kR2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(k6_gemm_i8<kR2, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     attr = true;
   }
-  k6_gemm_i8<kR2><<<grid, g6::kThreads, kSmem, st>>>(*mA, *mB, p); ++launch_counter();
+  p.num_n = (int)((p.N + BN - 1) / BN);
+  const int tiles = p.num_m * p.num_n;
+  const int grid = tiles < nsm ? tiles : nsm;
+  k6_gemm_i8<kR2, BN><<<grid, g6::threads_for(kR2, BN), kSmem, st>>>(*mA, *mB, p); ++launch_counter();
+}
+
+template <int kR2>
+static void launch_k6(const G6Params& p, const CUtensorMap* mA, const CUtensorMap* mB, int nsm, cudaStream_t st) {
+  // narrowest tile that covers N (no wasted MMA / epilogue columns for N = 64, 128)
+  if (p.N <= 64) launch_t<kR2, 64>(p, mA, mB + 3, nsm, st);
+  else if (p.N <= 128) launch_t<kR2, 128>(p, mA, mB + 2, nsm, st);
+  else launch_t<kR2, 256>(p, mA, mB, nsm, st);
 }
 
 template <int kR2>
@@ -825,16 +863,17 @@ void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStre
     }
     return;
   }
+  (void)grid;
   switch (r2) {
-    case 0: launch_t<0>(p, mA, mB, grid, st); break;
-    case 8: launch_t<8>(p, mA, mB, grid, st); break;
-    case 16: launch_t<16>(p, mA, mB, grid, st); break;
-    case 24: launch_t<24>(p, mA, mB, grid, st); break;
-    case 32: launch_t<32>(p, mA, mB, grid, st); break;
-    case 40: launch_t<40>(p, mA, mB, grid, st); break;
-    case 48: launch_t<48>(p, mA, mB, grid, st); break;
-    case 56: launch_t<56>(p, mA, mB, grid, st); break;
-    case 64: launch_t<64>(p, mA, mB, grid, st); break;
+    case 0: launch_k6<0>(p, mA, mB, nsm, st); break;
+    case 8: launch_k6<8>(p, mA, mB, nsm, st); break;
+    case 16: launch_k6<16>(p, mA, mB, nsm, st); break;
+    case 24: launch_k6<24>(p, mA, mB, nsm, st); break;
+    case 32: launch_k6<32>(p, mA, mB, nsm, st); break;
+    case 40: launch_k6<40>(p, mA, mB, nsm, st); break;
+    case 48: launch_k6<48>(p, mA, mB, nsm, st); break;
+    case 56: launch_k6<56>(p, mA, mB, nsm, st); break;
+    case 64: launch_k6<64>(p, mA, mB, nsm, st); break;
     default: break;
   }
 }

@@ -148,7 +148,7 @@ struct GemmArgs {
   int64_t ldd;
   int* sched;            // device int: dynamic tile counter of the CTA-pair GEMM (zeroed per launch)
 };
-// mapA / mapB: arrays of two CUtensorMap (one-CTA and CTA-pair box shapes); returns 0 on success
+// mapA / mapB: arrays of four CUtensorMap (one-CTA, CTA-pair and narrow-N box shapes); 0 on success
 int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB);
 int& gemm_variant();  // 0 auto (CTA pairs when M, N >= 512), 1 one-CTA K6, 2 CTA-pair K7
 // 2D TMA map (no swizzle), dims {inner, outer} elements of fp32 (dtype_f32=1) or u8; returns 0 on success

@@ -66,10 +66,10 @@ struct lrqmm_handle_s {
   float* VWbM = nullptr;     // W x W
   int* err_flag = nullptr;
   int* sched = nullptr;  // CTA-pair GEMM tile counter
-  alignas(64) CUtensorMap mapA[2];  // [0] one-CTA GEMM boxes, [1] CTA-pair GEMM boxes
-  alignas(64) CUtensorMap mapB[2];
-  alignas(64) CUtensorMap mapRA[2];  // QT: maps of the residual codes
-  alignas(64) CUtensorMap mapRB[2];
+  alignas(64) CUtensorMap mapA[4];  // GEMM map slots (gemm_i8.cu gemm_prepare_maps)
+  alignas(64) CUtensorMap mapB[4];
+  alignas(64) CUtensorMap mapRA[4];  // QT: maps of the residual codes
+  alignas(64) CUtensorMap mapRB[4];
   cudaEvent_t ev[8] = {};
   ncclComm_t comm = nullptr;
   // rsvd_residual as a CUDA graph: captured once on a private stream (the caller's stream may be
