@@ -58,6 +58,19 @@ struct SideView {
 // tcgen05 kind::tf32 (3-term split) passes, deterministic split-K partials; return the split count.
 // With reduce1 == false and > 1 splits, OUT1 stays as partials at `partial` (consumed by the fused
 // Gram kernel).  ROW: OUT1 = R P1 (rows x W); dual (P2 != null): OUT2 = X~ P2.  P is K x W (ld W).
+// One RSVD pass over one or two sides in a single launch (skinny_tc.cu launch_tc_pass).
+struct TcPassSide {
+  SideView view;
+  const float* P1;   // ROW/DUAL/COL operand
+  const float* P2;   // DUAL/CODES operand
+  float* OUT1;
+  float* OUT2;
+  float* partial;    // split-K partial scratch of this side
+  int64_t pe;        // its capacity in floats
+  uint8_t* img;      // >= 2 * tc_img_bytes(max(rows, K), W) bytes
+};
+enum { kPassRow = 0, kPassDual = 1, kPassCol = 2, kPassCodes = 3 };
+void launch_tc_pass(int kind, int nsides, const TcPassSide* sides, int W, bool reduce1, int* ns_out, cudaStream_t st);
 // img: scratch for the B operand images + column scales, >= 2 * tc_img_bytes(max(rows, K), W) bytes.
 int launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
                         float* partial, int64_t partial_elems, bool reduce1, uint8_t* img, cudaStream_t st);

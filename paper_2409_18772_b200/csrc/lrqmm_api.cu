@@ -386,6 +386,22 @@ static lrqmm_status_t allreduce_f32(lrqmm_handle_t h, float* buf, size_t n) {
 static float* part_of(lrqmm_handle_t h, int sd) { return h->partial + sd * (h->partial_elems / 2); }
 static int64_t part_elems(lrqmm_handle_t h) { return h->partial_elems / 2; }
 
+// One RSVD pass over the selected sides, both in a single launch (launch_tc_pass).
+static void pass_sides(lrqmm_handle_t h, int kind, int sides, const float* const P1[2], const float* const P2[2],
+                       float* const O1[2], float* const O2[2], bool reduce1, int nsp[2]) {
+  TcPassSide ps[2];
+  int idx[2], n = 0;
+  for (int sd = 0; sd < 2; ++sd)
+    if (sides & (1 << sd)) {
+      ps[n] = TcPassSide{view(h, sd), P1 ? P1[sd] : nullptr, P2 ? P2[sd] : nullptr, O1 ? O1[sd] : nullptr,
+                         O2 ? O2[sd] : nullptr, part_of(h, sd), part_elems(h), h->s[sd].img};
+      idx[n++] = sd;
+    }
+  int ns[2] = {0, 0};
+  launch_tc_pass(kind, n, ps, h->W, reduce1, ns, h->st);
+  for (int i = 0; i < n; ++i) nsp[idx[i]] = ns[i];
+}
+
 // After a skinny pass left Y_s as nsp[s] split partials: Y = sum(partials), G = Y^T Y, then
 // mode 0: CholQR transform T64 -> Q = Y T64 (fp64 accumulation); mode 1: truncation VW.
 // On a row-sharded A (world > 1, a_sharded) G_A is summed across ranks before the solve.
@@ -440,18 +456,13 @@ static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides) {
   int nsp[2] = {1, 1};
   lrqmm_status_t e;
   // S1: Y = R Omega   (Algorithm 1 sampling)
-  for (int sd = 0; sd < 2; ++sd)
-    if (sides & (1 << sd))
-      nsp[sd] = launch_tc_proj_rows(view(h, sd), h->s[sd].Om, Ys[sd], nullptr, nullptr, W, part_of(h, sd),
-                                    part_elems(h), false, h->s[sd].img, h->st);
+  const float* Oms[2] = {h->s[0].Om, h->s[1].Om};
+  pass_sides(h, kPassRow, sides, Oms, nullptr, Ys, nullptr, false, nsp);
   for (int it = 0; it < h->cfg.power_iters; ++it) {
     // O1: Q0 = orth(Y)   (Y rows of A are sharded across ranks)
     if ((e = gram_step(h, Ys, rows, nsp, 0, Q0s, true, sides)) != LRQMM_OK) return e;
     // S2: Z = R^T Q0  (reduction over rows; the A side is summed over ranks before its Gram)
-    for (int sd = 0; sd < 2; ++sd)
-      if (sides & (1 << sd))
-        nsp[sd] = launch_tc_proj_cols(view(h, sd), Q0s[sd], Zs[sd], W, part_of(h, sd), part_elems(h), multi,
-                                      h->s[sd].img, h->st);
+    pass_sides(h, kPassCol, sides, Q0s, nullptr, Zs, nullptr, multi, nsp);
     if (multi) {
       if ((sides & 1) && (e = allreduce_f32(h, Zs[0], (size_t)K * W)) != LRQMM_OK) return e;
       nsp[0] = nsp[1] = 1;  // multi -> reduce1: both Z are final
@@ -460,10 +471,7 @@ static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides) {
     // orthonormal to fp32 rounding); K rows are replicated on every rank
     if ((e = gram_step(h, Zs, kdim, nsp, 0, Q1s, false, sides)) != LRQMM_OK) return e;
     if (it + 1 < h->cfg.power_iters) {
-      for (int sd = 0; sd < 2; ++sd)
-        if (sides & (1 << sd))
-          nsp[sd] = launch_tc_proj_rows(view(h, sd), Q1s[sd], Ys[sd], nullptr, nullptr, W, part_of(h, sd),
-                                        part_elems(h), false, h->s[sd].img, h->st);
+      pass_sides(h, kPassRow, sides, Q1s, nullptr, Ys, nullptr, false, nsp);
     }
   }
   return check_launch(h);
@@ -508,12 +516,12 @@ static lrqmm_status_t rsvd_body(lrqmm_handle_t h, int kind) {
   // S3 (+ cross): W_X = R_X Q1_X, and G'_X = X~ Q1_other in the same pass over X when the other
   //   side's Q1 is current (Algorithm 1 on R^T: B = Q1^T R^T = W^T; RC1/RC2 skinny
   //   products)
-  for (int sd = 0; sd < 2; ++sd) {
-    if (!(sides & (1 << sd))) continue;
-    const bool cross = kind != 2;
-    nsp[sd] = launch_tc_proj_rows(view(h, sd), Q1s[sd], Ys[sd], cross ? Q1s[1 - sd] : nullptr,
-                                  cross ? h->s[sd].Gp : nullptr, W, part_of(h, sd), part_elems(h), false,
-                                  h->s[sd].img, h->st);
+  if (kind != 2) {
+    const float* other[2] = {Q1s[1], Q1s[0]};
+    float* Gps[2] = {h->s[0].Gp, h->s[1].Gp};
+    pass_sides(h, kPassDual, sides, Q1s, other, Ys, Gps, false, nsp);
+  } else {
+    pass_sides(h, kPassRow, sides, Q1s, nullptr, Ys, nullptr, false, nsp);
   }
   // T: W = sum(partials), truncation to rank r via eig(W^T W) (Algorithm 1)
   if ((e = gram_step(h, Ys, rows, nsp, 1, nullptr, true, sides)) != LRQMM_OK) return e;

@@ -92,6 +92,14 @@ struct TcArgs {
 struct TcMaps {
   CUtensorMap uh, ul, codes;
 };
+// one launch covers both sides of the RSVD: units [0, units0) are side 0's, the rest side 1's
+struct TcArgs2 {
+  TcArgs a[2];
+  int units0, units;
+};
+struct TcMaps2 {
+  TcMaps m[2];
+};
 
 // SWIZZLE_128B smem descriptor (layout type 2); K-major: rows of 128 B, 8-row atoms (SBO 1024);
 // MN-major (int8, M = 128 = one atom): rows along K, 8-row groups 1024 B apart (SBO)
@@ -130,47 +138,33 @@ struct PrepJob {
   uint8_t* img;         // nkb images
   unsigned* colmax;     // 64 (scratch)
   float* cinv;          // 64: 1 / s_c
-};
-struct PrepJobs {
-  PrepJob j[2];
-  int njobs;
   int64_t n, nkb;
+};
+constexpr int kMaxPrep = 4;
+struct PrepJobs {
+  PrepJob j[kMaxPrep];
+  int njobs;
   int W;
 };
 
-// B images (one cooperative launch for the one or two operands of a pass):
+// B images (one cooperative launch for all operands of a pass, both sides):
 //   phase 1  colmax_c = max_j |P_jc scale_j| (float bits: non-negative floats order like uints)
 //   phase 2  for every k-block g, the int8 pieces p1 | p2 | p3 of s_c P[128 g : 128 g + 128, c]
 //            in the K-major SWIZZLE_128B layout above (rows [0,W') p1, [W',2W') p2, [2W',3W') p3),
 //            rows >= n and columns >= W zero; cinv_c = 1 / s_c.
 // One thread per (column, 16 consecutive k) in phase 2: three 16-byte stores.
-#ifdef LRQMM_PREP_TIMING
-__device__ unsigned long long g_prep_t[8];
-LRQMM_DEV unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define PREP_T(i) if (blockIdx.x == 0 && threadIdx.x == 0) g_prep_t[i] = gtime();
-#else
-#define PREP_T(i)
-#endif
 template <int NA>
 __global__ void __launch_bounds__(256) k_prep_img(PrepJobs jb) {
-  PREP_T(0)
   namespace cg = cooperative_groups;
   constexpr int WN = 32 * NA;
   constexpr int kImg = 3 * WN * tcp::BK;
   constexpr int kChunks = tcp::BK / 16;
-  __shared__ unsigned sm[2][64];
+  __shared__ unsigned sm[kMaxPrep][64];
   const int W = jb.W;
-  const int64_t n = jb.n;
-  if (threadIdx.x < 128) sm[threadIdx.x >> 6][threadIdx.x & 63] = 0u;
-  if (blockIdx.x == 0 && threadIdx.x < 128 && (int)(threadIdx.x >> 6) < jb.njobs)
-    jb.j[threadIdx.x >> 6].colmax[threadIdx.x & 63] = 0u;
-  PREP_T(1)
+  for (int e = threadIdx.x; e < kMaxPrep * 64; e += blockDim.x) sm[e >> 6][e & 63] = 0u;
+  if (blockIdx.x == 0)
+    for (int e = threadIdx.x; e < jb.njobs * 64; e += blockDim.x) jb.j[e >> 6].colmax[e & 63] = 0u;
   cg::this_grid().sync();
-  PREP_T(2)
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   {
@@ -180,6 +174,7 @@ __global__ void __launch_bounds__(256) k_prep_img(PrepJobs jb) {
     const int64_t rstride = (int64_t)gridDim.x * kRowsPerBlk;
     for (int q = 0; q < jb.njobs; ++q) {
       const PrepJob& J = jb.j[q];
+      const int64_t n = J.n;
       float m = 0.f;
       if (c < W) {
         int64_t j = (int64_t)blockIdx.x * kRowsPerBlk + threadIdx.x / WN;
@@ -198,18 +193,17 @@ __global__ void __launch_bounds__(256) k_prep_img(PrepJobs jb) {
     }
   }
   __syncthreads();
-  if (threadIdx.x < 128) {
-    const int q = threadIdx.x >> 6, c = threadIdx.x & 63;
-    if (q < jb.njobs && c < W && sm[q][c]) atomicMax(&jb.j[q].colmax[c], sm[q][c]);
+  for (int e = threadIdx.x; e < jb.njobs * 64; e += blockDim.x) {
+    const int q = e >> 6, c = e & 63;
+    if (c < W && sm[q][c]) atomicMax(&jb.j[q].colmax[c], sm[q][c]);
   }
-  PREP_T(3)
   cg::this_grid().sync();
-  PREP_T(4)
   for (int q = 0; q < jb.njobs; ++q) {
     const PrepJob& J = jb.j[q];
+    const int64_t n = J.n;
     if (blockIdx.x == 0 && threadIdx.x < WN)
       J.cinv[threadIdx.x] = (int)threadIdx.x < W ? 1.f / col_scale(J.colmax[threadIdx.x]) : 0.f;
-    const int64_t total = jb.nkb * kChunks * WN;
+    const int64_t total = J.nkb * kChunks * WN;
     for (int64_t e = t0; e < total; e += gstride) {
       const int c = (int)(e % WN);  // consecutive threads: consecutive columns (coalesced reads)
       const int64_t rest = e / WN;
@@ -248,11 +242,11 @@ __global__ void __launch_bounds__(256) k_prep_img(PrepJobs jb) {
       *reinterpret_cast<uint4*>(base + off_k128(2 * WN + c, ch * 16)) = make_uint4(w3[0], w3[1], w3[2], w3[3]);
     }
   }
-  PREP_T(5)
 }
 
 template <int kMode, int NA, int kVar>
-__global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_constant__ TcMaps maps, TcArgs a) {
+__global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_constant__ TcMaps2 maps,
+                                                                 const __grid_constant__ TcArgs2 args) {
   using namespace tcp;
   using C = Cfg<kMode, NA, kVar>;
   constexpr bool kHasU = C::kHasU, kHasC = C::kHasC;
@@ -269,8 +263,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t r_len = kMode == 0 ? (int64_t)a.K : a.rows;
-  const int nunits = a.nblk * a.nsplit;
+  const int nunits = args.units;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -289,9 +282,13 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  auto unit_range = [&](int u, int& blk, int& split, int64_t& r0, int& nkb) {
-    blk = u % a.nblk;
-    split = u / a.nblk;
+  auto unit_range = [&](int u, int& side, int& blk, int& split, int64_t& r0, int& nkb) {
+    side = u >= args.units0 ? 1 : 0;
+    const TcArgs& a = args.a[side];
+    const int lu = u - (side ? args.units0 : 0);
+    const int64_t r_len = kMode == 0 ? (int64_t)a.K : a.rows;
+    blk = lu % a.nblk;
+    split = lu / a.nblk;
     r0 = (int64_t)split * a.chunk;
     const int64_t r1 = r0 + a.chunk < r_len ? r0 + a.chunk : r_len;
     nkb = (int)((r1 - r0 + BK - 1) / BK);
@@ -300,16 +297,20 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   if (warp == kTmaWarp) {
     // ------------------------------------------------------ TMA producer
     if (lane == 0) {
-      if (kHasU) {
-        tma_prefetch_desc(&maps.uh);
-        tma_prefetch_desc(&maps.ul);
+      for (int sd = 0; sd < 2; ++sd) {
+        if (kHasU) {
+          tma_prefetch_desc(&maps.m[sd].uh);
+          tma_prefetch_desc(&maps.m[sd].ul);
+        }
+        if (kHasC) tma_prefetch_desc(&maps.m[sd].codes);
       }
-      if (kHasC) tma_prefetch_desc(&maps.codes);
       int it = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        int blk, split, nkb;
+        int side, blk, split, nkb;
         int64_t r0;
-        unit_range(u, blk, split, r0, nkb);
+        unit_range(u, side, blk, split, r0, nkb);
+        const TcArgs& a = args.a[side];
+        const TcMaps& mp = maps.m[side];
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % S;
           const int k0 = (int)(r0 + (int64_t)kb * BK);
@@ -319,16 +320,16 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
           const int64_t g = k0 / BK;
           if (kHasU) {
             if (kMode == 0) {
-              tma_load_2d(st, &maps.uh, &full[s], k0, blk * BM);
-              tma_load_2d(st + C::kOffL, &maps.ul, &full[s], k0, blk * BM);
+              tma_load_2d(st, &mp.uh, &full[s], k0, blk * BM);
+              tma_load_2d(st + C::kOffL, &mp.ul, &full[s], k0, blk * BM);
             } else {
-              tma_load_2d(st, &maps.uh, &full[s], blk * BM, k0);
-              tma_load_2d(st + C::kOffL, &maps.ul, &full[s], blk * BM, k0);
+              tma_load_2d(st, &mp.uh, &full[s], blk * BM, k0);
+              tma_load_2d(st + C::kOffL, &mp.ul, &full[s], blk * BM, k0);
             }
             bulk_load(st + C::kOffB, a.img1 + g * C::kImg, C::kImg, &full[s]);
           }
           if (kHasC) {
-            tma_load_2d(st + C::kOffC, &maps.codes, &full[s], k0, blk * BM);
+            tma_load_2d(st + C::kOffC, &mp.codes, &full[s], k0, blk * BM);
             bulk_load(st + C::kOffB2, a.img2 + g * C::kImg, C::kImg, &full[s]);
           }
         }
@@ -345,9 +346,9 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       const uint64_t d0 = desc_sw128(smem_u32(smem));
       int it = 0, lu = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
-        int blk, split, nkb;
+        int side, blk, split, nkb;
         int64_t r0;
-        unit_range(u, blk, split, r0, nkb);
+        unit_range(u, side, blk, split, r0, nkb);
         const int acc = NACC == 2 ? (lu & 1) : 0;
         const uint32_t tph = NACC == 2 ? ((lu >> 1) & 1) : (lu & 1);
         mbar_wait(&tempty[acc], tph ^ 1);
@@ -383,9 +384,10 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
     const int quad = warp & 3;
     int lu = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
-      int blk, split, nkb;
+      int side, blk, split, nkb;
       int64_t r0;
-      unit_range(u, blk, split, r0, nkb);
+      unit_range(u, side, blk, split, r0, nkb);
+      const TcArgs& a = args.a[side];
       const int acc = NACC == 2 ? (lu & 1) : 0;
       const uint32_t tph = NACC == 2 ? ((lu >> 1) & 1) : (lu & 1);
       mbar_wait(&tfull[acc], tph);
@@ -526,23 +528,7 @@ int64_t tc_img_bytes(int64_t n, int W) {
 }
 
 template <int NA>
-static void prep_imgs(const float* P1, const float* P2, int64_t n, int W, const float* scale1, uint8_t* img1,
-                      uint8_t* img2, float** cinv1, float** cinv2, cudaStream_t st) {
-  const int64_t nkb = (n + tcp::BK - 1) / tcp::BK;
-  PrepJobs jb{};
-  jb.n = n;
-  jb.nkb = nkb;
-  jb.W = W;
-  jb.njobs = P2 ? 2 : 1;
-  const float* Ps[2] = {P1, P2};
-  uint8_t* imgs[2] = {img1, img2};
-  for (int q = 0; q < jb.njobs; ++q) {
-    uint8_t* tailp = imgs[q] + nkb * (3 * 32 * NA * tcp::BK);
-    jb.j[q] = PrepJob{Ps[q], q == 0 ? scale1 : nullptr, imgs[q], reinterpret_cast<unsigned*>(tailp),
-                      reinterpret_cast<float*>(tailp + 256)};
-  }
-  *cinv1 = jb.j[0].cinv;
-  *cinv2 = jb.j[jb.njobs - 1].cinv;
+static void launch_prep(PrepJobs& jb, cudaStream_t st) {
   static int grid = 0;
   if (!grid) {
     int dev = 0, nsm = 148, per = 1;
@@ -556,9 +542,10 @@ static void prep_imgs(const float* P1, const float* P2, int64_t n, int W, const 
   ++launch_counter();
 }
 
+// One pass over one or two sides: a single prep launch builds every B image, then ONE k_tc_proj
+// launch processes the units of both sides (units [0, units0) are side 0's).
 template <int kMode, int NA, int kVar>
-static int run_tc(const SideView& s, const float* P1, const float* P2, int W, float* OUT1, float* OUT2, float* partial,
-                  int64_t pe, bool reduce1, uint8_t* img, cudaStream_t st) {
+static void run_tc(int nsides, const TcPassSide* sides, int W, bool reduce1, int* ns_out, cudaStream_t st) {
   using namespace tcp;
   using C = Cfg<kMode, NA, kVar>;
   constexpr bool kHasU = C::kHasU, kHasC = C::kHasC;
@@ -567,107 +554,146 @@ static int run_tc(const SideView& s, const float* P1, const float* P2, int W, fl
     cudaFuncSetAttribute(k_tc_proj<kMode, NA, kVar>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr = true;
   }
-  TcArgs a{};
-  a.rows = s.rows;
-  a.K = s.K;
-  a.inv_lam = s.inv_lam;
-  a.W = W;
-  a.nout = kMode == 0 ? s.rows : (int64_t)s.K;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t nblk = (a.nout + BM - 1) / BM;
-  const int64_t rlen = kMode == 0 ? (int64_t)s.K : s.rows;
-  // B images of P1 (and P2) over the reduction dimension; COL folds 1/lambda_i into P's rows
-  const int64_t ib = tc_img_bytes(rlen, W);
-  float* cinv1 = nullptr;
-  float* cinv2 = nullptr;
-  if (kVar == 2) {  // codes only: P2 is the single operand
-    prep_imgs<NA>(P2, nullptr, rlen, W, nullptr, img, img + ib, &cinv2, &cinv1, st);
-    a.img1 = a.img2 = img;
-    a.cinv1 = a.cinv2 = cinv2;
-  } else {
-    prep_imgs<NA>(P1, kHasC ? P2 : nullptr, rlen, W, kMode == 1 ? s.inv_lam : nullptr, img, img + ib, &cinv1,
-                  &cinv2, st);
-    a.img1 = img;
-    a.img2 = img + ib;
-    a.cinv1 = cinv1;
-    a.cinv2 = kHasC ? cinv2 : cinv1;
-  }
-  // enough units for ~6 per SM (the persistent grid balances them), each >= 4 k-blocks, and a
-  // chunk short enough for exact int32 accumulation
-  int64_t ns = (6LL * nsm + nblk - 1) / nblk;
-  const int64_t maxs = (rlen + 4 * BK - 1) / (4 * BK);
-  if (ns > maxs) ns = maxs;
-  if (ns > 256) ns = 256;  // few output blocks (short K in COL mode): bound the partials to reduce
-  const int64_t per = a.nout * W * (kVar == 1 ? 2 : 1);
-  if (ns > 1 && ns * per > pe) ns = pe / per;
-  const int64_t mins = (rlen + kMaxChunk - 1) / kMaxChunk;
-  if (ns < mins) ns = mins;
-  if (ns < 1) ns = 1;
-  a.chunk = ((rlen + ns - 1) / ns + BK - 1) / BK * BK;
-  ns = (rlen + a.chunk - 1) / a.chunk;
-  if (ns < 1) ns = 1;
-  a.nblk = (int)nblk;
-  a.nsplit = (int)ns;
-  a.out1 = ns == 1 ? OUT1 : partial;
-  a.out2 = ns == 1 ? OUT2 : (kVar == 2 ? partial : partial + ns * a.nout * W);
-  alignas(64) TcMaps maps;
+  TcArgs2 args{};
+  alignas(64) TcMaps2 maps;
   memset(&maps, 0, sizeof(maps));
-  const uint64_t ld = (uint64_t)s.ldu;
-  if (kHasU) {
-    encode_map_2d_sw(&maps.uh, 0, s.Uh, (uint64_t)s.K, (uint64_t)s.rows, ld, BK, BM, 128);
-    encode_map_2d_sw(&maps.ul, 0, s.Ul, (uint64_t)s.K, (uint64_t)s.rows, ld, BK, BM, 128);
+  PrepJobs jb{};
+  jb.W = W;
+  int jfirst[2] = {0, 0};
+  int64_t units[2] = {0, 0};
+  for (int sd = 0; sd < nsides; ++sd) {
+    const SideView& s = sides[sd].view;
+    TcArgs& a = args.a[sd];
+    a.rows = s.rows;
+    a.K = s.K;
+    a.inv_lam = s.inv_lam;
+    a.W = W;
+    a.nout = kMode == 0 ? s.rows : (int64_t)s.K;
+    const int64_t nblk = (a.nout + BM - 1) / BM;
+    const int64_t rlen = kMode == 0 ? (int64_t)s.K : s.rows;
+    // B images over the reduction dimension (COL folds 1/lambda_i into P's rows)
+    const int64_t nkb = (rlen + BK - 1) / BK;
+    const int64_t ib = tc_img_bytes(rlen, W);
+    auto add_job = [&](const float* P, const float* scale, uint8_t* img) {
+      uint8_t* tailp = img + nkb * (3 * 32 * NA * BK);
+      jb.j[jb.njobs++] = PrepJob{P,   scale, img, reinterpret_cast<unsigned*>(tailp), reinterpret_cast<float*>(tailp + 256),
+                                 rlen, nkb};
+    };
+    jfirst[sd] = jb.njobs;
+    if (kVar == 2) {
+      add_job(sides[sd].P2, nullptr, sides[sd].img);
+      a.img1 = a.img2 = sides[sd].img;
+      a.cinv1 = a.cinv2 = jb.j[jfirst[sd]].cinv;
+    } else {
+      add_job(sides[sd].P1, kMode == 1 ? s.inv_lam : nullptr, sides[sd].img);
+      a.img1 = sides[sd].img;
+      a.cinv1 = jb.j[jfirst[sd]].cinv;
+      if (kHasC) {
+        add_job(sides[sd].P2, nullptr, sides[sd].img + ib);
+        a.img2 = sides[sd].img + ib;
+        a.cinv2 = jb.j[jfirst[sd] + 1].cinv;
+      } else {
+        a.img2 = a.img1;
+        a.cinv2 = a.cinv1;
+      }
+    }
+    // enough units for ~6 per SM (the persistent grid balances them), each >= 4 k-blocks, and a
+    // chunk short enough for exact int32 accumulation
+    int64_t ns = (6LL * nsm + nblk - 1) / nblk;
+    const int64_t maxs = (rlen + 4 * BK - 1) / (4 * BK);
+    if (ns > maxs) ns = maxs;
+    if (ns > 256) ns = 256;  // few output blocks (short K in COL mode): bound the partials to reduce
+    const int64_t per = a.nout * W * (kVar == 1 ? 2 : 1);
+    if (ns > 1 && ns * per > sides[sd].pe) ns = sides[sd].pe / per;
+    const int64_t mins = (rlen + kMaxChunk - 1) / kMaxChunk;
+    if (ns < mins) ns = mins;
+    if (ns < 1) ns = 1;
+    a.chunk = ((rlen + ns - 1) / ns + BK - 1) / BK * BK;
+    ns = (rlen + a.chunk - 1) / a.chunk;
+    if (ns < 1) ns = 1;
+    a.nblk = (int)nblk;
+    a.nsplit = (int)ns;
+    float* part = sides[sd].partial;
+    a.out1 = ns == 1 ? sides[sd].OUT1 : part;
+    a.out2 = ns == 1 ? sides[sd].OUT2 : (kVar == 2 ? part : part + ns * a.nout * W);
+    const uint64_t ld = (uint64_t)s.ldu;
+    if (kHasU) {
+      encode_map_2d_sw(&maps.m[sd].uh, 0, s.Uh, (uint64_t)s.K, (uint64_t)s.rows, ld, BK, BM, 128);
+      encode_map_2d_sw(&maps.m[sd].ul, 0, s.Ul, (uint64_t)s.K, (uint64_t)s.rows, ld, BK, BM, 128);
+    }
+    if (kHasC)
+      encode_map_2d_sw(&maps.m[sd].codes, 0, s.codes, (uint64_t)s.Kp, (uint64_t)s.rows, (uint64_t)s.Kp, BK, BM, 128);
+    units[sd] = nblk * ns;
+    ns_out[sd] = (int)ns;
   }
-  if (kHasC) encode_map_2d_sw(&maps.codes, 0, s.codes, (uint64_t)s.Kp, (uint64_t)s.rows, (uint64_t)s.Kp, BK, BM, 128);
-  const int64_t units = nblk * ns;
-  const int grid = (int)(units < nsm ? units : nsm);
-  k_tc_proj<kMode, NA, kVar><<<grid, kThreads, C::kSmem, st>>>(maps, a);
+  launch_prep<NA>(jb, st);
+  args.units0 = (int)units[0];
+  args.units = (int)(units[0] + units[1]);
+  const int grid = (int)(args.units < nsm ? args.units : nsm);
+  k_tc_proj<kMode, NA, kVar><<<grid, kThreads, C::kSmem, st>>>(maps, args);
   ++launch_counter();
-  if (ns > 1) {
+  for (int sd = 0; sd < nsides; ++sd) {
+    const int ns = ns_out[sd];
+    if (ns <= 1) continue;
+    const TcArgs& a = args.a[sd];
     const int64_t n = a.nout * W;
-    const int g = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
-    (void)g;
-    if (reduce1 && kHasU) launch_reduce_splits(partial, (int)ns, n, OUT1, st);
-    if (kHasC) launch_reduce_splits(kVar == 2 ? partial : partial + ns * a.nout * W, (int)ns, n, OUT2, st);
+    float* part = sides[sd].partial;
+    if (reduce1 && kHasU) launch_reduce_splits(part, ns, n, sides[sd].OUT1, st);
+    if (kHasC) launch_reduce_splits(kVar == 2 ? part : part + (int64_t)ns * a.nout * W, ns, n, sides[sd].OUT2, st);
   }
-  return (int)ns;
 }
 
-// U (K1's residual planes) is TMA-addressable by construction (ldu % 16 == 0).  Returns the
-// number of split-K partials; with reduce1 == false and a result > 1, OUT1 is left as
-// partials at `partial` (summed by the fused Gram kernel).
+// kind: kPassRow (OUT1 = R P1), kPassDual (+ OUT2 = X~ P2), kPassCol (OUT1 = R^T P1), kPassCodes
+// (OUT2 = X~ P2 only, always reduced).  Sides with no rows or no K are skipped.  ns_out[i]: the
+// split-K partial count of sides[i] (0 if skipped); with reduce1 == false and ns > 1 the U result
+// stays as partials at sides[i].partial.
+void launch_tc_pass(int kind, int nsides, const TcPassSide* sides_in, int W, bool reduce1, int* ns_out,
+                    cudaStream_t st) {
+  TcPassSide sides[2];
+  int map[2], n = 0;
+  for (int i = 0; i < nsides; ++i) {
+    ns_out[i] = 0;
+    if (sides_in[i].view.rows > 0 && sides_in[i].view.K > 0) { map[n] = i; sides[n++] = sides_in[i]; }
+  }
+  if (n == 0) return;
+  int ns[2] = {0, 0};
+  const bool wide = W > 32;
+  switch (kind) {
+    case kPassRow: wide ? run_tc<0, 2, 0>(n, sides, W, reduce1, ns, st) : run_tc<0, 1, 0>(n, sides, W, reduce1, ns, st); break;
+    case kPassDual: wide ? run_tc<0, 2, 1>(n, sides, W, reduce1, ns, st) : run_tc<0, 1, 1>(n, sides, W, reduce1, ns, st); break;
+    case kPassCol: wide ? run_tc<1, 2, 0>(n, sides, W, reduce1, ns, st) : run_tc<1, 1, 0>(n, sides, W, reduce1, ns, st); break;
+    default: wide ? run_tc<0, 2, 2>(n, sides, W, true, ns, st) : run_tc<0, 1, 2>(n, sides, W, true, ns, st); break;
+  }
+  for (int i = 0; i < n; ++i) ns_out[map[i]] = ns[i];
+}
+
+// single-side forms (test hooks)
 int launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
                         float* partial, int64_t pe, bool reduce1, uint8_t* img, cudaStream_t st) {
-  if (s.rows == 0 || s.K == 0) return 0;
-  if (W <= 32) {
-    if (P2) return run_tc<0, 1, 1>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
-    return run_tc<0, 1, 0>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
-  }
-  if (P2) return run_tc<0, 2, 1>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
-  return run_tc<0, 2, 0>(s, P1, P2, W, OUT1, OUT2, partial, pe, reduce1, img, st);
+  TcPassSide sd{s, P1, P2, OUT1, OUT2, partial, pe, img};
+  int ns = 0;
+  launch_tc_pass(P2 ? kPassDual : kPassRow, 1, &sd, W, reduce1, &ns, st);
+  return ns;
 }
 
 int launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t pe, bool reduce1,
                         uint8_t* img, cudaStream_t st) {
-  if (s.K == 0 || s.rows == 0) return 0;
-  if (W <= 32) return run_tc<1, 1, 0>(s, P, nullptr, W, OUT, nullptr, partial, pe, reduce1, img, st);
-  return run_tc<1, 2, 0>(s, P, nullptr, W, OUT, nullptr, partial, pe, reduce1, img, st);
+  TcPassSide sd{s, P, nullptr, OUT, nullptr, partial, pe, img};
+  int ns = 0;
+  launch_tc_pass(kPassCol, 1, &sd, W, reduce1, &ns, st);
+  return ns;
 }
 
-// OUT = X~ P (codes only, rows x W; X~ = code / lambda): the A-dependent term B~ Q1_A of the
-// static-B mode (lrqmm_rsvd_residual with omegaB == NULL).  1 byte of codes per element.
 int launch_tc_proj_codes(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t pe,
                          uint8_t* img, cudaStream_t st) {
-  if (s.rows == 0 || s.K == 0) return 0;
-  if (W <= 32) return run_tc<0, 1, 2>(s, nullptr, P, W, nullptr, OUT, partial, pe, true, img, st);
-  return run_tc<0, 2, 2>(s, nullptr, P, W, nullptr, OUT, partial, pe, true, img, st);
+  TcPassSide sd{s, nullptr, P, nullptr, OUT, partial, pe, img};
+  int ns = 0;
+  launch_tc_pass(kPassCodes, 1, &sd, W, true, &ns, st);
+  return ns;
 }
 
 }  // namespace lrqmm
 
-#ifdef LRQMM_PREP_TIMING
-extern "C" int lrqmm_debug_prep_times(unsigned long long* out) {
-  return (int)cudaMemcpyFromSymbol(out, lrqmm::g_prep_t, sizeof(unsigned long long) * 8);
-}
-#endif
