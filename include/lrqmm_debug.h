@@ -30,7 +30,8 @@ lrqmm_status_t lrqmm_debug_set_gemm_variant(int variant);
 /* Small solvers (K4) on Y (n x W):
  *   op 0: G = Y^T Y (fp64, W x W)
  *   op 1: G = Y^T Y, T = orthonormalising transform (Y T has orthonormal columns)
- *   op 2: G = Y^T Y, T[:, 0:r] = top-r eigenvectors of G (descending), rest 0     */
+ *   op 2: G = Y^T Y, T[:, 0:r] = top-r eigenvectors of G (descending), rest 0
+ *   op 3, 4: as ops 1, 2 through the fused Gram + solve kernel the RSVD runs        */
 lrqmm_status_t lrqmm_debug_small(int op, const float* Y, int64_t n, int W, int r, double* G, float* T, void* stream);
 
 #ifdef __cplusplus

@@ -75,6 +75,8 @@ struct lrqmm_handle_s {
   // rsvd_residual as a CUDA graph: captured once on a private stream (the caller's stream may be
   // the legacy default stream, which cannot be captured), then launched onto the caller's stream
   cudaStream_t cap_st = nullptr;
+  cudaStream_t side_st = nullptr;                      // forked branch (cross Gram || truncation)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaGraphExec_t rsvd_exec[3] = {};  // per rsvd_body kind
   int rsvd_calls[3] = {};
   int64_t rsvd_graph_kernels[3] = {};
@@ -191,6 +193,9 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   for (auto& x : h->rsvd_exec)
     if (x) cudaGraphExecDestroy(x);
   if (h->cap_st) cudaStreamDestroy(h->cap_st);
+  if (h->side_st) cudaStreamDestroy(h->side_st);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->comm) ncclCommDestroy(h->comm);
   delete h;
   return LRQMM_OK;
@@ -479,16 +484,29 @@ static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides) {
 
 // Cross core and factor assembly (Algorithm 2 lines 361-366 folded into two rank-2r factors):
 // needs W_X (= Y_X), VW_X, Q1_X of both sides and G'_A = A~ Q1_B, G'_B = B~ Q1_A.
+// V_B^T V_A core: Gcross = Q1_B^T Q1_A (fp64, W x W).  Independent of the truncation, so it runs
+// on a forked branch (side stream, event fork/join; captured into the graph as a parallel branch)
+// while the one-CTA-per-side eigensolver occupies two SMs.
+static lrqmm_status_t fork_cross_gram(lrqmm_handle_t h) {
+  if (!h->side_st) {
+    if (cudaStreamCreateWithFlags(&h->side_st, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess)
+      return LRQMM_ERR_CUDA;
+  }
+  LQ_CUDA(cudaEventRecord(h->ev_fork, h->st));
+  LQ_CUDA(cudaStreamWaitEvent(h->side_st, h->ev_fork, 0));
+  GramJobs j{};
+  j.n = 1;
+  j.j[0] = GramJob{h->s[1].Q1, h->s[0].Q1, h->cfg.k, h->Gcross, h->gpart_cross, h->counter_cross};
+  launch_gram_jobs(j, h->W, h->side_st);
+  LQ_CUDA(cudaEventRecord(h->ev_join, h->side_st));
+  return LRQMM_OK;
+}
+
 static lrqmm_status_t assemble(lrqmm_handle_t h) {
   const int W = h->W;
-  const int64_t K = h->cfg.k;
-  // V_B^T V_A core: Q1_B^T Q1_A (fp64, W x W) -> Mab, VWb Mab
-  {
-    GramJobs j{};
-    j.n = 1;
-    j.j[0] = GramJob{h->s[1].Q1, h->s[0].Q1, K, h->Gcross, h->gpart_cross, h->counter_cross};
-    launch_gram_jobs(j, W, h->st);
-  }
+  LQ_CUDA(cudaStreamWaitEvent(h->st, h->ev_join, 0));  // Gcross (fork_cross_gram)
   launch_cross_small(h->Gcross, h->s[0].VW, h->s[1].VW, W, h->r, h->VWbM, h->st);
   const int r = h->r;
   const int64_t rows[2] = {h->s[0].rows, h->s[1].rows};
@@ -523,6 +541,7 @@ static lrqmm_status_t rsvd_body(lrqmm_handle_t h, int kind) {
   } else {
     pass_sides(h, kPassRow, sides, Q1s, nullptr, Ys, nullptr, false, nsp);
   }
+  if (kind != 2 && (e = fork_cross_gram(h)) != LRQMM_OK) return e;
   // T: W = sum(partials), truncation to rank r via eig(W^T W) (Algorithm 1)
   if ((e = gram_step(h, Ys, rows, nsp, 1, nullptr, true, sides)) != LRQMM_OK) return e;
   if (kind == 2) return check_launch(h);
@@ -828,8 +847,23 @@ extern "C" lrqmm_status_t lrqmm_debug_small(int op, const float* Y, int64_t n, i
   double* part = nullptr;
   int* counter = nullptr;
   if (cudaMalloc(&part, sizeof(double) * kGramMaxBlocks * W * W) != cudaSuccess) return LRQMM_ERR_ALLOC;
-  if (cudaMalloc(&counter, sizeof(int)) != cudaSuccess) return LRQMM_ERR_ALLOC;
-  cudaMemsetAsync(counter, 0, sizeof(int), st);
+  if (cudaMalloc(&counter, 64 * sizeof(int)) != cudaSuccess) return LRQMM_ERR_ALLOC;
+  cudaMemsetAsync(counter, 0, 64 * sizeof(int), st);
+  if (op == 3 || op == 4) {
+    // the fused Gram + solve kernel of the RSVD (mode 0 CholQR transform, mode 1 truncation), x reps
+    double* T64 = nullptr;
+    if (cudaMalloc(&T64, sizeof(double) * W * W) != cudaSuccess) return LRQMM_ERR_ALLOC;
+    SmallJobs j{};
+    j.n = 1;
+    j.j[0] = SmallJob{const_cast<float*>(Y), nullptr, 1, n, G, part, counter, T64, T, r};
+    launch_fused_small(j, W, op - 3, st);
+    if (op == 3) launch_f64_to_f32(T64, T, (int64_t)W * W, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(part);
+    cudaFree(counter);
+    cudaFree(T64);
+    return e == cudaSuccess ? LRQMM_OK : LRQMM_ERR_CUDA;
+  }
   GramJobs gj{};
   gj.n = 1;
   gj.j[0] = GramJob{Y, Y, n, G, part, counter};
