@@ -76,7 +76,20 @@ struct G6Params {
   int64_t ldd;
   int vec_ok;
   int* sched;  // K7: global tile counter (atomicAdd), zeroed before the launch
+  int group_m;  // K7: pair-tile rows per raster group
+  int polA, polB;  // K7: L2 policies of the A / B loads (l2_policy kinds)
 };
+
+// raster with a runtime group height (K7)
+LRQMM_DEV void tile_coords_rt(int t, int gm, int num_m, int num_n, int& mb, int& nb) {
+  const int per_group = gm * num_n;
+  const int group = t / per_group;
+  const int first_m = group * gm;
+  const int gsize = min(gm, num_m - first_m);
+  const int in = t % per_group;
+  mb = first_m + in % gsize;
+  nb = in / gsize;
+}
 
 template <int kGM = g6::kGroupM>
 LRQMM_DEV void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
@@ -510,9 +523,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t full0 = mapa_cta(smem_u32(full), 0);  // leader's full[0]
-#if LRQMM_L2HINT7
-      const uint64_t polA = l2_policy_evict_last();
-#endif
+      const uint64_t polA = l2_policy(p.polA), polB = l2_policy(p.polB);
       const uint32_t tfull_peer = mapa_cta(smem_u32(tfull_t), 1);
       const uint32_t ring_peer = mapa_cta(smem_u32(tile_ring), 1);
       const uint32_t tempty_lead = mapa_cta(smem_u32(tempty_t), 0);
@@ -536,7 +547,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
         }
         if (t >= num_tiles) break;
         int mb, nb;
-        tile_coords<g7::kGroupM>(t, p.num_m, p.num_n, mb, nb);
+        tile_coords_rt(t, p.group_m, p.num_m, p.num_n, mb, nb);
         const int arow = mb * (2 * BM) + (int)rank * BM;
         const int brow = nb * BN + (int)rank * BNH;
         for (int kb = 0; kb < p.num_kb; ++kb) {
@@ -545,12 +556,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
           else if ((stage & 1) == 0) mbar_wait(&empty[stage >> 1], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
           const uint32_t fb = full0 + stage * 8;
-#if LRQMM_L2HINT7
           tma_load_2d_2sm_hint(sA + stage * kABytes, &mapA, fb, kb * BK, arow, polA);
-#else
-          tma_load_2d_2sm(sA + stage * kABytes, &mapA, fb, kb * BK, arow);
-#endif
-          tma_load_2d_2sm(sB + stage * kBBytes, &mapB, fb, kb * BK, brow);
+          tma_load_2d_2sm_hint(sB + stage * kBBytes, &mapB, fb, kb * BK, brow, polB);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -611,7 +618,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
       if (et == 0) mbar_arrive_remote(tempty_t0 + 8 * q);
       if (t >= num_tiles) break;
       int mb, nb;
-      tile_coords<g7::kGroupM>(t, p.num_m, p.num_n, mb, nb);
+      tile_coords_rt(t, p.group_m, p.num_m, p.num_n, mb, nb);
       const int acc = lt & 1;
       const uint32_t acc_phase = (lt >> 1) & 1;
       const int64_t row = (int64_t)mb * (2 * BM) + (int64_t)rank * BM + quad * 32 + lane;
@@ -815,6 +822,19 @@ static void launch_t7(G6Params p, const CUtensorMap* mA, const CUtensorMap* mB, 
   const int tiles = p.num_m * p.num_n;
   int pairs = nsm / 2;
   if (tiles < pairs) pairs = tiles;
+  // raster group / L2 policies (defaults measured best; LRQMM_G7_{GROUP,POLA,POLB} override them
+  // for experiments)
+  static int group = -1, pola = 2, polb = 1;  // A evict_last, B evict_first (c3: -4.6% GEMM time)
+  if (group < 0) {
+    const char* e = getenv("LRQMM_G7_GROUP");
+    group = e ? atoi(e) : g7::kGroupM;
+    if (group < 1) group = 1;
+    if ((e = getenv("LRQMM_G7_POLA"))) pola = atoi(e);
+    if ((e = getenv("LRQMM_G7_POLB"))) polb = atoi(e);
+  }
+  p.group_m = group;
+  p.polA = pola;
+  p.polB = polb;
   cudaMemsetAsync(p.sched, 0, sizeof(int), st);
   k7_gemm_i8_2sm<kR2><<<2 * pairs, g7::kThreads, kSmem, st>>>(*mA, *mB, p); ++launch_counter();
 }
