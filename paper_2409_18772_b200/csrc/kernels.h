@@ -68,6 +68,8 @@ struct TcPassSide {
   float* partial;    // split-K partial scratch of this side
   int64_t pe;        // its capacity in floats
   uint8_t* img;      // >= 2 * tc_img_bytes(max(rows, K), W) bytes
+  const unsigned* cmax1;  // column maxima (float bits) of |P1 scale| / |P2| from their producer, or nullptr
+  const unsigned* cmax2;
 };
 enum { kPassRow = 0, kPassDual = 1, kPassCol = 2, kPassCodes = 3 };
 void launch_tc_pass(int kind, int nsides, const TcPassSide* sides, int W, bool reduce1, int* ns_out, cudaStream_t st);
@@ -86,6 +88,39 @@ int launch_tc_proj_codes(const SideView& s, const float* P, float* OUT, int W, f
 
 // OUT[i, :] = IN[i, :] S (fp64 S, fp64 accumulation, fp32 out); IN and OUT ld W, S W x W
 void launch_apply64(const float* IN, const double* S, int64_t n, int W, float* OUT, cudaStream_t st);
+// multi-job forms (one launch): OUT = IN S per job
+struct Apply64Job {
+  const float* IN;
+  const double* S;
+  int64_t n;
+  float* OUT;
+  unsigned* cmax;       // if set: atomicMax of the float bits of |OUT[i, c] * cscale[i]| per column c
+  const float* cscale;  // (zeroed beforehand; cscale nullptr = 1)
+};
+struct Apply64Jobs {
+  Apply64Job j[2];
+  int n;
+  int first[3];  // block ranges (set by the launcher)
+};
+void launch_apply64_jobs(const Apply64Jobs& jobs, int W, cudaStream_t st);
+constexpr int kMaxApply = 4;
+struct ApplyJob {
+  const float* IN1;
+  const float* S1;
+  const float* IN2;
+  const float* S2;
+  int64_t n;
+  int ldS, nout;
+  float* OUT;
+  int64_t ldo;
+  int col0;
+};
+struct ApplyJobs {
+  ApplyJob j[kMaxApply];
+  int n;
+  int first[kMaxApply + 1];
+};
+void launch_apply_jobs(const ApplyJobs& jobs, int W, cudaStream_t st);
 // OUT[i, col0 + o] = sum_c IN1[i,c] S1[c,o] (+ sum_c IN2[i,c] S2[c,o]), o < nout; IN ld W, S ld ldS, OUT ld ldo
 void launch_apply_small(const float* IN1, const float* S1, const float* IN2, const float* S2, int64_t n, int W,
                         int ldS, int nout, float* OUT, int64_t ldo, int col0, cudaStream_t st);
@@ -132,6 +167,7 @@ struct SmallJob {
   double* T64;
   float* T;
   int r;
+  unsigned* cmax;      // zeroed by the last block (the next apply64 accumulates column maxima into it)
 };
 struct SmallJobs {
   SmallJob j[2];

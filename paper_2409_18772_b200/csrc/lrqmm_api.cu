@@ -43,6 +43,8 @@ struct Side {
   double* G = nullptr;       // W x W
   double* gpart = nullptr;   // kGramMaxBlocks x W x W Gram partials
   int* counter = nullptr;    // Gram last-block ticket
+  unsigned* cmax0 = nullptr; // column maxima of |Q0 / lambda| (COL pass image), written by apply64
+  unsigned* cmax1 = nullptr; // column maxima of |Q1| (ROW / dual / codes pass images)
   double* T64 = nullptr;     // W x W  (orth transform, fp64)
   float* VW = nullptr;       // W x W  (first r columns: truncation)
 };
@@ -182,7 +184,7 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   for (auto& s : h->s) {
     cudaFree(s.codes); cudaFree(s.lam); cudaFree(s.inv_lam); cudaFree(s.row_amax); cudaFree(s.lam_scalar); cudaFree(s.Om);
     cudaFree(s.Y); cudaFree(s.Q0); cudaFree(s.Z); cudaFree(s.Q1); cudaFree(s.Gp); cudaFree(s.G);
-    cudaFree(s.gpart); cudaFree(s.counter); cudaFree(s.T64); cudaFree(s.VW); cudaFree(s.U); cudaFree(s.img);
+    cudaFree(s.gpart); cudaFree(s.cmax0); cudaFree(s.cmax1); cudaFree(s.counter); cudaFree(s.T64); cudaFree(s.VW); cudaFree(s.U); cudaFree(s.img);
     cudaFree(s.R32); cudaFree(s.rcodes); cudaFree(s.rlam); cudaFree(s.rinv); cudaFree(s.rrow_amax); cudaFree(s.rlam_scalar);
   }
   cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->partial); cudaFree(h->Gcross); cudaFree(h->gpart_cross);
@@ -238,7 +240,7 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
       ok = ok && dalloc(&s.U, 2 * s.rows * s.ldu) && dalloc(&s.Om, K * h->W) && dalloc(&s.Y, s.rows * h->W) && dalloc(&s.Q0, s.rows * h->W) &&
            dalloc(&s.Z, K * h->W) && dalloc(&s.Q1, K * h->W) && dalloc(&s.Gp, s.rows * h->W) &&
            dalloc(&s.G, (int64_t)h->W * h->W) && dalloc(&s.gpart, (int64_t)kGramMaxBlocks * h->W * h->W) &&
-           dalloc(&s.counter, 64) && dalloc(&s.T64, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W) &&
+           dalloc(&s.counter, 64) && dalloc(&s.cmax0, 64) && dalloc(&s.cmax1, 64) && dalloc(&s.T64, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W) &&
            dalloc(&s.img, 2 * tc_img_bytes(std::max<int64_t>(s.rows, K), h->W));
     }
     if (cfg->qt_terms > 0)
@@ -392,14 +394,17 @@ static float* part_of(lrqmm_handle_t h, int sd) { return h->partial + sd * (h->p
 static int64_t part_elems(lrqmm_handle_t h) { return h->partial_elems / 2; }
 
 // One RSVD pass over the selected sides, both in a single launch (launch_tc_pass).
+// cm1 / cm2: column maxima of P1 / P2 from their producer (apply64), or nullptr (computed by the prep)
 static void pass_sides(lrqmm_handle_t h, int kind, int sides, const float* const P1[2], const float* const P2[2],
-                       float* const O1[2], float* const O2[2], bool reduce1, int nsp[2]) {
+                       float* const O1[2], float* const O2[2], bool reduce1, int nsp[2],
+                       const unsigned* const cm1[2] = nullptr, const unsigned* const cm2[2] = nullptr) {
   TcPassSide ps[2];
   int idx[2], n = 0;
   for (int sd = 0; sd < 2; ++sd)
     if (sides & (1 << sd)) {
       ps[n] = TcPassSide{view(h, sd), P1 ? P1[sd] : nullptr, P2 ? P2[sd] : nullptr, O1 ? O1[sd] : nullptr,
-                         O2 ? O2[sd] : nullptr, part_of(h, sd), part_elems(h), h->s[sd].img};
+                         O2 ? O2[sd] : nullptr, part_of(h, sd), part_elems(h), h->s[sd].img,
+                         cm1 ? cm1[sd] : nullptr, cm2 ? cm2[sd] : nullptr};
       idx[n++] = sd;
     }
   int ns[2] = {0, 0};
@@ -411,8 +416,10 @@ static void pass_sides(lrqmm_handle_t h, int kind, int sides, const float* const
 // mode 0: CholQR transform T64 -> Q = Y T64 (fp64 accumulation); mode 1: truncation VW.
 // On a row-sharded A (world > 1, a_sharded) G_A is summed across ranks before the solve.
 // sides: bit 0 = A, bit 1 = B
+// which (mode 0): 0 = the result is Q0 (its COL-pass image needs max |Q0 / lambda| per column),
+// 1 = Q1 (max |Q1|); apply64 accumulates those maxima into cmax0 / cmax1.
 static lrqmm_status_t gram_step(lrqmm_handle_t h, float* const Y[2], const int64_t n[2], const int nsp[2], int mode,
-                                float* const Q[2], bool a_sharded, int sides = 3) {
+                                float* const Q[2], bool a_sharded, int sides = 3, int which = 1) {
   const int W = h->W;
   const bool ranks = a_sharded && h->cfg.world_size > 1 && (sides & 1);
   SmallJobs j{};
@@ -427,7 +434,8 @@ static lrqmm_status_t gram_step(lrqmm_handle_t h, float* const Y[2], const int64
         ns = 1;
       }
       j.j[j.n++] = SmallJob{Y[sd], part_of(h, sd), ns, n[sd], h->s[sd].G, h->s[sd].gpart, h->s[sd].counter,
-                            h->s[sd].T64, h->s[sd].VW, h->r};
+                            h->s[sd].T64, h->s[sd].VW, h->r,
+                            mode == 1 ? nullptr : (which == 0 ? h->s[sd].cmax0 : h->s[sd].cmax1)};
     }
   launch_fused_small(j, W, ranks ? 2 : mode, h->st);
   if (ranks) {
@@ -440,9 +448,14 @@ static lrqmm_status_t gram_step(lrqmm_handle_t h, float* const Y[2], const int64
     if (mode == 0) launch_chol_orth(ej, W, h->st);
     else launch_eig_warp(ej, W, h->st);
   }
-  if (mode == 0)
+  if (mode == 0) {
+    Apply64Jobs aj{};
     for (int sd = 0; sd < 2; ++sd)
-      if (sides & (1 << sd)) launch_apply64(Y[sd], h->s[sd].T64, n[sd], W, Q[sd], h->st);
+      if (sides & (1 << sd))
+        aj.j[aj.n++] = Apply64Job{Y[sd], h->s[sd].T64, n[sd], Q[sd], which == 0 ? h->s[sd].cmax0 : h->s[sd].cmax1,
+                                  which == 0 ? h->s[sd].inv_lam : nullptr};
+    launch_apply64_jobs(aj, W, h->st);
+  }
   return check_launch(h);
 }
 
@@ -459,24 +472,26 @@ static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides) {
   float* Zs[2] = {h->s[0].Z, h->s[1].Z};
   float* Q1s[2] = {h->s[0].Q1, h->s[1].Q1};
   int nsp[2] = {1, 1};
+  const unsigned* cm0[2] = {h->s[0].cmax0, h->s[1].cmax0};
+  const unsigned* cm1[2] = {h->s[0].cmax1, h->s[1].cmax1};
   lrqmm_status_t e;
   // S1: Y = R Omega   (Algorithm 1 sampling)
   const float* Oms[2] = {h->s[0].Om, h->s[1].Om};
   pass_sides(h, kPassRow, sides, Oms, nullptr, Ys, nullptr, false, nsp);
   for (int it = 0; it < h->cfg.power_iters; ++it) {
     // O1: Q0 = orth(Y)   (Y rows of A are sharded across ranks)
-    if ((e = gram_step(h, Ys, rows, nsp, 0, Q0s, true, sides)) != LRQMM_OK) return e;
+    if ((e = gram_step(h, Ys, rows, nsp, 0, Q0s, true, sides, 0)) != LRQMM_OK) return e;
     // S2: Z = R^T Q0  (reduction over rows; the A side is summed over ranks before its Gram)
-    pass_sides(h, kPassCol, sides, Q0s, nullptr, Zs, nullptr, multi, nsp);
+    pass_sides(h, kPassCol, sides, Q0s, nullptr, Zs, nullptr, multi, nsp, cm0);
     if (multi) {
       if ((sides & 1) && (e = allreduce_f32(h, Zs[0], (size_t)K * W)) != LRQMM_OK) return e;
       nsp[0] = nsp[1] = 1;  // multi -> reduce1: both Z are final
     }
     // O2: Q1 = orth(Z) (fp64 Gram + Cholesky, transform applied with fp64 accumulation, so Q1 is
     // orthonormal to fp32 rounding); K rows are replicated on every rank
-    if ((e = gram_step(h, Zs, kdim, nsp, 0, Q1s, false, sides)) != LRQMM_OK) return e;
+    if ((e = gram_step(h, Zs, kdim, nsp, 0, Q1s, false, sides, 1)) != LRQMM_OK) return e;
     if (it + 1 < h->cfg.power_iters) {
-      pass_sides(h, kPassRow, sides, Q1s, nullptr, Ys, nullptr, false, nsp);
+      pass_sides(h, kPassRow, sides, Q1s, nullptr, Ys, nullptr, false, nsp, cm1);
     }
   }
   return check_launch(h);
@@ -512,10 +527,13 @@ static lrqmm_status_t assemble(lrqmm_handle_t h) {
   const int64_t rows[2] = {h->s[0].rows, h->s[1].rows};
   float* YA = h->s[0].Y;
   float* YB = h->s[1].Y;
-  launch_apply_small(YA, h->s[0].VW, nullptr, nullptr, rows[0], W, W, r, h->LA, h->R2, 0, h->st);          // U_A S_A
-  launch_apply_small(h->s[0].Gp, h->s[1].VW, nullptr, nullptr, rows[0], W, W, r, h->LA, h->R2, r, h->st);   // A~ V_B
-  launch_apply_small(h->s[1].Gp, h->s[0].VW, YB, h->VWbM, rows[1], W, W, r, h->LB, h->R2, 0, h->st);        // B~^T V_A + U_B S_B M
-  launch_apply_small(YB, h->s[1].VW, nullptr, nullptr, rows[1], W, W, r, h->LB, h->R2, r, h->st);           // U_B S_B
+  ApplyJobs aj{};
+  aj.n = 4;
+  aj.j[0] = ApplyJob{YA, h->s[0].VW, nullptr, nullptr, rows[0], W, r, h->LA, h->R2, 0};        // U_A S_A
+  aj.j[1] = ApplyJob{h->s[0].Gp, h->s[1].VW, nullptr, nullptr, rows[0], W, r, h->LA, h->R2, r}; // A~ V_B
+  aj.j[2] = ApplyJob{h->s[1].Gp, h->s[0].VW, YB, h->VWbM, rows[1], W, r, h->LB, h->R2, 0};      // B~^T V_A + U_B S_B M
+  aj.j[3] = ApplyJob{YB, h->s[1].VW, nullptr, nullptr, rows[1], W, r, h->LB, h->R2, r};         // U_B S_B
+  launch_apply_jobs(aj, W, h->st);
   return check_launch(h);
 }
 
@@ -534,20 +552,26 @@ static lrqmm_status_t rsvd_body(lrqmm_handle_t h, int kind) {
   // S3 (+ cross): W_X = R_X Q1_X, and G'_X = X~ Q1_other in the same pass over X when the other
   //   side's Q1 is current (Algorithm 1 on R^T: B = Q1^T R^T = W^T; RC1/RC2 skinny
   //   products)
+  const unsigned* cm1[2] = {h->s[0].cmax1, h->s[1].cmax1};
+  const unsigned* cm1o[2] = {h->s[1].cmax1, h->s[0].cmax1};
   if (kind != 2) {
     const float* other[2] = {Q1s[1], Q1s[0]};
     float* Gps[2] = {h->s[0].Gp, h->s[1].Gp};
-    pass_sides(h, kPassDual, sides, Q1s, other, Ys, Gps, false, nsp);
+    pass_sides(h, kPassDual, sides, Q1s, other, Ys, Gps, false, nsp, cm1, cm1o);
   } else {
-    pass_sides(h, kPassRow, sides, Q1s, nullptr, Ys, nullptr, false, nsp);
+    pass_sides(h, kPassRow, sides, Q1s, nullptr, Ys, nullptr, false, nsp, cm1);
   }
   if (kind != 2 && (e = fork_cross_gram(h)) != LRQMM_OK) return e;
   // T: W = sum(partials), truncation to rank r via eig(W^T W) (Algorithm 1)
   if ((e = gram_step(h, Ys, rows, nsp, 1, nullptr, true, sides)) != LRQMM_OK) return e;
   if (kind == 2) return check_launch(h);
   // static-B: the only A-dependent B-side term, G'_B = B~ Q1_A (a codes-only pass over B)
-  if (kind == 1)
-    launch_tc_proj_codes(view(h, 1), Q1s[0], h->s[1].Gp, W, part_of(h, 1), part_elems(h), h->s[1].img, h->st);
+  if (kind == 1) {
+    float* Gps[2] = {nullptr, h->s[1].Gp};
+    const float* qa[2] = {nullptr, Q1s[0]};
+    const unsigned* cma[2] = {nullptr, h->s[0].cmax1};
+    pass_sides(h, kPassCodes, 2, nullptr, qa, nullptr, Gps, true, nsp, nullptr, cma);
+  }
   return assemble(h);
 }
 
@@ -855,7 +879,7 @@ extern "C" lrqmm_status_t lrqmm_debug_small(int op, const float* Y, int64_t n, i
     if (cudaMalloc(&T64, sizeof(double) * W * W) != cudaSuccess) return LRQMM_ERR_ALLOC;
     SmallJobs j{};
     j.n = 1;
-    j.j[0] = SmallJob{const_cast<float*>(Y), nullptr, 1, n, G, part, counter, T64, T, r};
+    j.j[0] = SmallJob{const_cast<float*>(Y), nullptr, 1, n, G, part, counter, T64, T, r, nullptr};
     launch_fused_small(j, W, op - 3, st);
     if (op == 3) launch_f64_to_f32(T64, T, (int64_t)W * W, st);
     cudaError_t e = cudaStreamSynchronize(st);

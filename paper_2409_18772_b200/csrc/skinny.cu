@@ -26,28 +26,32 @@ LRQMM_DEV void stage_rows_in(const float* __restrict__ src, int64_t i0, int nr, 
   }
 }
 
-// OUT[i, col0 + o] = sum_c IN1[i,c] S1[c,o] (+ sum_c IN2[i,c] S2[c,o]),  o < nout (<= W)
+// OUT[i, col0 + o] = sum_c IN1[i,c] S1[c,o] (+ sum_c IN2[i,c] S2[c,o]),  o < nout (<= W).
+// Up to kMaxApply jobs per launch: job q owns blocks [first[q], first[q+1]) and walks its rows.
 template <int W>
-__global__ void __launch_bounds__(kApRows) k_apply_small(const float* __restrict__ IN1, const float* __restrict__ S1,
-                                                         const float* __restrict__ IN2, const float* __restrict__ S2,
-                                                         int64_t n, int ldS, int nout, float* __restrict__ OUT,
-                                                         int64_t ldo, int col0) {
+__global__ void __launch_bounds__(kApRows) k_apply_small(const ApplyJobs jobs) {
   constexpr int L = ap_ld(W);
   extern __shared__ __align__(16) float apsm[];
+  int q = 0;
+  while (q + 1 < jobs.n && (int)blockIdx.x >= jobs.first[q + 1]) ++q;
+  const ApplyJob& J = jobs.j[q];
+  const int b0 = jobs.first[q], nb = jobs.first[q + 1] - b0;
   float* sin1 = apsm;                    // kApRows x L
   float* sin2 = sin1 + kApRows * L;      // kApRows x L
   float* s1 = sin2 + kApRows * L;        // W x W
   float* s2 = s1 + W * W;                // W x W
+  const int nout = J.nout;
   for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
     const int c = e / W, o = e % W;
-    s1[e] = o < nout ? S1[c * ldS + o] : 0.f;
-    s2[e] = (IN2 && o < nout) ? S2[c * ldS + o] : 0.f;
+    s1[e] = o < nout ? J.S1[c * J.ldS + o] : 0.f;
+    s2[e] = (J.IN2 && o < nout) ? J.S2[c * J.ldS + o] : 0.f;
   }
-  for (int64_t i0 = (int64_t)blockIdx.x * kApRows; i0 < n; i0 += (int64_t)gridDim.x * kApRows) {
+  const int64_t n = J.n;
+  for (int64_t i0 = (int64_t)(blockIdx.x - b0) * kApRows; i0 < n; i0 += (int64_t)nb * kApRows) {
     const int nr = (int)(n - i0 < kApRows ? n - i0 : kApRows);
     __syncthreads();
-    stage_rows_in<W>(IN1, i0, nr, sin1);
-    if (IN2) stage_rows_in<W>(IN2, i0, nr, sin2);
+    stage_rows_in<W>(J.IN1, i0, nr, sin1);
+    if (J.IN2) stage_rows_in<W>(J.IN2, i0, nr, sin2);
     __syncthreads();
     float acc[W];
 #pragma unroll
@@ -62,7 +66,7 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const float* __restrict
 #pragma unroll
           for (int o = 0; o < W; ++o) acc[o] = fmaf(xs[j], s1[(4 * c4 + j) * W + o], acc[o]);
       }
-      if (IN2) {
+      if (J.IN2) {
 #pragma unroll
         for (int c4 = 0; c4 < W / 4; ++c4) {
           const float4 v = *reinterpret_cast<const float4*>(sin2 + threadIdx.x * L + 4 * c4);
@@ -82,51 +86,77 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const float* __restrict
     __syncthreads();
     for (int e = threadIdx.x; e < nr * nout; e += blockDim.x) {
       const int r = e / nout, o = e % nout;
-      OUT[(i0 + r) * ldo + col0 + o] = sin1[r * L + o];
+      J.OUT[(i0 + r) * J.ldo + J.col0 + o] = sin1[r * L + o];
     }
   }
 }
 
-static int grid_rows(int64_t n, int per) {
-  const int64_t want = (n + per - 1) / per;
-  return (int)(want < 148 * 16 ? (want < 1 ? 1 : want) : 148 * 16);
+// blocks per job: one 128-row block each, or (when that exceeds the cap) an even share of the cap
+static int assign_blocks(const int64_t* n, int njobs, int* first) {
+  const int64_t cap = 148 * 16;
+  int64_t rb[kMaxApply], tot = 0;
+  for (int q = 0; q < njobs; ++q) { rb[q] = (n[q] + kApRows - 1) / kApRows; if (rb[q] < 1) rb[q] = 1; tot += rb[q]; }
+  const int64_t it = (tot + cap - 1) / cap;
+  first[0] = 0;
+  for (int q = 0; q < njobs; ++q) first[q + 1] = first[q] + (int)((rb[q] + it - 1) / it);
+  return first[njobs];
 }
 
 template <int W>
-static void apply_small_t(const float* IN1, const float* S1, const float* IN2, const float* S2, int64_t n, int ldS,
-                          int nout, float* OUT, int64_t ldo, int col0, cudaStream_t st) {
+static void apply_small_t(ApplyJobs& jobs, cudaStream_t st) {
   constexpr int smem = (2 * kApRows * ap_ld(W) + 2 * W * W) * (int)sizeof(float);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_apply_small<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  k_apply_small<W><<<grid_rows(n, kApRows), kApRows, smem, st>>>(IN1, S1, IN2, S2, n, ldS, nout, OUT, ldo, col0);
+  int64_t n[kMaxApply];
+  for (int q = 0; q < jobs.n; ++q) n[q] = jobs.j[q].n;
+  const int grid = assign_blocks(n, jobs.n, jobs.first);
+  k_apply_small<W><<<grid, kApRows, smem, st>>>(jobs);
 }
 
-void launch_apply_small(const float* IN1, const float* S1, const float* IN2, const float* S2, int64_t n, int W,
-                        int ldS, int nout, float* OUT, int64_t ldo, int col0, cudaStream_t st) {
-  if (n == 0 || nout == 0) return;
-#define AS_CASE(w) case w: apply_small_t<w>(IN1, S1, IN2, S2, n, ldS, nout, OUT, ldo, col0, st); break;
+void launch_apply_jobs(const ApplyJobs& in, int W, cudaStream_t st) {
+  ApplyJobs jobs{};
+  for (int q = 0; q < in.n; ++q)
+    if (in.j[q].n > 0 && in.j[q].nout > 0) jobs.j[jobs.n++] = in.j[q];
+  if (jobs.n == 0) return;
+#define AS_CASE(w) case w: apply_small_t<w>(jobs, st); break;
   switch (W) { AS_CASE(8) AS_CASE(16) AS_CASE(24) AS_CASE(32) AS_CASE(40) AS_CASE(48) AS_CASE(56) AS_CASE(64) default: break; }
 #undef AS_CASE
   ++launch_counter();
 }
 
+void launch_apply_small(const float* IN1, const float* S1, const float* IN2, const float* S2, int64_t n, int W,
+                        int ldS, int nout, float* OUT, int64_t ldo, int col0, cudaStream_t st) {
+  ApplyJobs j{};
+  j.n = 1;
+  j.j[0] = ApplyJob{IN1, S1, IN2, S2, n, ldS, nout, OUT, ldo, col0};
+  launch_apply_jobs(j, W, st);
+}
+
 // OUT = IN S with S in fp64 and fp64 accumulation (orthonormalisation: keeps Q orthonormal to
-// fp32 rounding instead of cond(IN) * eps32).  Same staging as above.
+// fp32 rounding instead of cond(IN) * eps32).  Same staging as above; one launch for both sides.
 template <int W>
-__global__ void __launch_bounds__(kApRows) k_apply64(const float* __restrict__ IN, const double* __restrict__ S, int64_t n,
-                                                     float* __restrict__ OUT) {
+__global__ void __launch_bounds__(kApRows) k_apply64(const Apply64Jobs jobs) {
   constexpr int L = ap_ld(W);
   extern __shared__ __align__(16) double apsm64[];
+  const int q = (jobs.n > 1 && (int)blockIdx.x >= jobs.first[1]) ? 1 : 0;
+  const Apply64Job& J = jobs.j[q];
+  const int b0 = jobs.first[q], nb = jobs.first[q + 1] - b0;
   double* s = apsm64;                                      // W x W
   float* sin = reinterpret_cast<float*>(apsm64 + W * W);   // kApRows x L
-  for (int e = threadIdx.x; e < W * W; e += blockDim.x) s[e] = S[e];
-  for (int64_t i0 = (int64_t)blockIdx.x * kApRows; i0 < n; i0 += (int64_t)gridDim.x * kApRows) {
+  for (int e = threadIdx.x; e < W * W; e += blockDim.x) s[e] = J.S[e];
+  unsigned run[(W + 31) / 32];  // lane c: running column max of column c (+32)
+#pragma unroll
+  for (int u = 0; u < (W + 31) / 32; ++u) run[u] = 0u;
+  __shared__ unsigned bmax[64];
+  if (threadIdx.x < 64) bmax[threadIdx.x] = 0u;
+  const int64_t n = J.n;
+  for (int64_t i0 = (int64_t)(blockIdx.x - b0) * kApRows; i0 < n; i0 += (int64_t)nb * kApRows) {
     const int nr = (int)(n - i0 < kApRows ? n - i0 : kApRows);
     __syncthreads();
-    stage_rows_in<W>(IN, i0, nr, sin);
+    stage_rows_in<W>(J.IN, i0, nr, sin);
     __syncthreads();
     double acc[W];
 #pragma unroll
@@ -147,32 +177,62 @@ __global__ void __launch_bounds__(kApRows) k_apply64(const float* __restrict__ I
 #pragma unroll
       for (int o = 0; o < W; ++o) sin[threadIdx.x * L + o] = (float)acc[o];
     }
+    if (J.cmax) {
+      // column maxima of |OUT * cscale| for the next pass's B image (same fp32 product as there)
+      const float cs = (J.cscale && threadIdx.x < nr) ? J.cscale[i0 + threadIdx.x] : 1.f;
+#pragma unroll
+      for (int o = 0; o < W; ++o) {
+        const unsigned b = threadIdx.x < nr ? __float_as_uint(fabsf((float)acc[o] * cs)) : 0u;
+        const unsigned m = __reduce_max_sync(0xffffffffu, b);
+        if ((threadIdx.x & 31) == (o & 31)) run[o >> 5] = max(run[o >> 5], m);
+      }
+    }
     __syncthreads();
-    float4* o4 = reinterpret_cast<float4*>(OUT + i0 * W);
+    float4* o4 = reinterpret_cast<float4*>(J.OUT + i0 * W);
     for (int e = threadIdx.x; e < nr * (W / 4); e += blockDim.x) {
       const int r = e / (W / 4), c = e % (W / 4);
       o4[e] = *reinterpret_cast<const float4*>(sin + r * L + 4 * c);
     }
   }
+  if (J.cmax) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int u = 0; u < (W + 31) / 32; ++u)
+      if (32 * u + lane < W && run[u]) atomicMax(&bmax[32 * u + lane], run[u]);
+    __syncthreads();
+    if (threadIdx.x < W && bmax[threadIdx.x]) atomicMax(J.cmax + threadIdx.x, bmax[threadIdx.x]);
+  }
 }
 
 template <int W>
-static void apply64_t(const float* IN, const double* S, int64_t n, float* OUT, cudaStream_t st) {
+static void apply64_t(Apply64Jobs& jobs, cudaStream_t st) {
   constexpr int smem = W * W * (int)sizeof(double) + kApRows * ap_ld(W) * (int)sizeof(float);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_apply64<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  k_apply64<W><<<grid_rows(n, kApRows), kApRows, smem, st>>>(IN, S, n, OUT);
+  int64_t n[2] = {jobs.j[0].n, jobs.n > 1 ? jobs.j[1].n : 0};
+  const int grid = assign_blocks(n, jobs.n, jobs.first);
+  k_apply64<W><<<grid, kApRows, smem, st>>>(jobs);
 }
 
-void launch_apply64(const float* IN, const double* S, int64_t n, int W, float* OUT, cudaStream_t st) {
-  if (n == 0) return;
-#define A64_CASE(w) case w: apply64_t<w>(IN, S, n, OUT, st); break;
+void launch_apply64_jobs(const Apply64Jobs& in, int W, cudaStream_t st) {
+  Apply64Jobs jobs{};
+  for (int q = 0; q < in.n; ++q)
+    if (in.j[q].n > 0) jobs.j[jobs.n++] = in.j[q];
+  if (jobs.n == 0) return;
+#define A64_CASE(w) case w: apply64_t<w>(jobs, st); break;
   switch (W) { A64_CASE(8) A64_CASE(16) A64_CASE(24) A64_CASE(32) A64_CASE(40) A64_CASE(48) A64_CASE(56) A64_CASE(64) default: break; }
 #undef A64_CASE
   ++launch_counter();
+}
+
+void launch_apply64(const float* IN, const double* S, int64_t n, int W, float* OUT, cudaStream_t st) {
+  Apply64Jobs j{};
+  j.n = 1;
+  j.j[0] = Apply64Job{IN, S, n, OUT, nullptr, nullptr};
+  launch_apply64_jobs(j, W, st);
 }
 
 __global__ void k_f64_to_f32(const double* __restrict__ in, float* __restrict__ out, int64_t n) {

@@ -139,6 +139,7 @@ struct PrepJob {
   unsigned* colmax;     // 64 (scratch)
   float* cinv;          // 64: 1 / s_c
   int64_t n, nkb;
+  const unsigned* cmax_in;  // column maxima supplied by P's producer (apply64), or nullptr
 };
 constexpr int kMaxPrep = 4;
 struct PrepJobs {
@@ -153,20 +154,23 @@ struct PrepJobs {
 //            in the K-major SWIZZLE_128B layout above (rows [0,W') p1, [W',2W') p2, [2W',3W') p3),
 //            rows >= n and columns >= W zero; cinv_c = 1 / s_c.
 // One thread per (column, 16 consecutive k) in phase 2: three 16-byte stores.
-template <int NA>
+// kHaveMax: every job's column maxima come from P's producer (cmax_in): no phase 1, no grid
+// synchronisation, an ordinary launch.
+template <int NA, bool kHaveMax>
 __global__ void __launch_bounds__(256) k_prep_img(PrepJobs jb) {
   namespace cg = cooperative_groups;
   constexpr int WN = 32 * NA;
   constexpr int kImg = 3 * WN * tcp::BK;
   constexpr int kChunks = tcp::BK / 16;
-  __shared__ unsigned sm[kMaxPrep][64];
   const int W = jb.W;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if constexpr (!kHaveMax) {
+  __shared__ unsigned sm[kMaxPrep][64];
   for (int e = threadIdx.x; e < kMaxPrep * 64; e += blockDim.x) sm[e >> 6][e & 63] = 0u;
   if (blockIdx.x == 0)
     for (int e = threadIdx.x; e < jb.njobs * 64; e += blockDim.x) jb.j[e >> 6].colmax[e & 63] = 0u;
   cg::this_grid().sync();
-  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   {
     // thread = (row lane, column c): a running max in a register, one shared atomic at the end
     constexpr int kRowsPerBlk = 256 / WN;
@@ -198,11 +202,13 @@ __global__ void __launch_bounds__(256) k_prep_img(PrepJobs jb) {
     if (c < W && sm[q][c]) atomicMax(&jb.j[q].colmax[c], sm[q][c]);
   }
   cg::this_grid().sync();
+  }
   for (int q = 0; q < jb.njobs; ++q) {
     const PrepJob& J = jb.j[q];
     const int64_t n = J.n;
+    const unsigned* cmax = kHaveMax ? J.cmax_in : J.colmax;
     if (blockIdx.x == 0 && threadIdx.x < WN)
-      J.cinv[threadIdx.x] = (int)threadIdx.x < W ? 1.f / col_scale(J.colmax[threadIdx.x]) : 0.f;
+      J.cinv[threadIdx.x] = (int)threadIdx.x < W ? 1.f / col_scale(__ldcg(cmax + threadIdx.x)) : 0.f;
     const int64_t total = J.nkb * kChunks * WN;
     for (int64_t e = t0; e < total; e += gstride) {
       const int c = (int)(e % WN);  // consecutive threads: consecutive columns (coalesced reads)
@@ -210,7 +216,7 @@ __global__ void __launch_bounds__(256) k_prep_img(PrepJobs jb) {
       const int ch = (int)(rest % kChunks);
       const int64_t g = rest / kChunks;
       const bool cok = c < W;
-      const float sc = cok ? col_scale(J.colmax[c]) : 0.f;  // 0 zeroes columns >= W
+      const float sc = cok ? col_scale(__ldcg(cmax + c)) : 0.f;  // 0 zeroes columns >= W
       const bool hs = J.scale != nullptr;
       const float* sp = hs ? J.scale : J.P;
       // unconditional (clamped) loads so that all 16 are in flight together
@@ -529,16 +535,30 @@ int64_t tc_img_bytes(int64_t n, int W) {
 
 template <int NA>
 static void launch_prep(PrepJobs& jb, cudaStream_t st) {
-  static int grid = 0;
+  static int grid = 0, nsm = 148;
   if (!grid) {
-    int dev = 0, nsm = 148, per = 1;
+    int dev = 0, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_prep_img<NA>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_prep_img<NA, false>, 256, 0);
     grid = nsm * (per < 4 ? (per < 1 ? 1 : per) : 4);
   }
-  void* args[] = {&jb};
-  cudaLaunchCooperativeKernel((const void*)k_prep_img<NA>, dim3(grid), dim3(256), args, 0, st);
+  bool have = true;
+  int64_t work = 0;
+  for (int q = 0; q < jb.njobs; ++q) {
+    have = have && jb.j[q].cmax_in != nullptr;
+    work += jb.j[q].nkb * (tcp::BK / 16) * 32 * NA;
+  }
+  if (have) {
+    // one (column, 16 rows) item per thread, up to 8 blocks per SM
+    int64_t g = (work + 255) / 256;
+    if (g > 8 * nsm) g = 8 * nsm;
+    if (g < 1) g = 1;
+    k_prep_img<NA, true><<<(int)g, 256, 0, st>>>(jb);
+  } else {
+    void* args[] = {&jb};
+    cudaLaunchCooperativeKernel((const void*)k_prep_img<NA, false>, dim3(grid), dim3(256), args, 0, st);
+  }
   ++launch_counter();
 }
 
@@ -577,22 +597,22 @@ static void run_tc(int nsides, const TcPassSide* sides, int W, bool reduce1, int
     // B images over the reduction dimension (COL folds 1/lambda_i into P's rows)
     const int64_t nkb = (rlen + BK - 1) / BK;
     const int64_t ib = tc_img_bytes(rlen, W);
-    auto add_job = [&](const float* P, const float* scale, uint8_t* img) {
+    auto add_job = [&](const float* P, const float* scale, uint8_t* img, const unsigned* cmax) {
       uint8_t* tailp = img + nkb * (3 * 32 * NA * BK);
-      jb.j[jb.njobs++] = PrepJob{P,   scale, img, reinterpret_cast<unsigned*>(tailp), reinterpret_cast<float*>(tailp + 256),
-                                 rlen, nkb};
+      jb.j[jb.njobs++] = PrepJob{P,    scale, img, reinterpret_cast<unsigned*>(tailp), reinterpret_cast<float*>(tailp + 256),
+                                 rlen, nkb, cmax};
     };
     jfirst[sd] = jb.njobs;
     if (kVar == 2) {
-      add_job(sides[sd].P2, nullptr, sides[sd].img);
+      add_job(sides[sd].P2, nullptr, sides[sd].img, sides[sd].cmax2);
       a.img1 = a.img2 = sides[sd].img;
       a.cinv1 = a.cinv2 = jb.j[jfirst[sd]].cinv;
     } else {
-      add_job(sides[sd].P1, kMode == 1 ? s.inv_lam : nullptr, sides[sd].img);
+      add_job(sides[sd].P1, kMode == 1 ? s.inv_lam : nullptr, sides[sd].img, sides[sd].cmax1);
       a.img1 = sides[sd].img;
       a.cinv1 = jb.j[jfirst[sd]].cinv;
       if (kHasC) {
-        add_job(sides[sd].P2, nullptr, sides[sd].img + ib);
+        add_job(sides[sd].P2, nullptr, sides[sd].img + ib, sides[sd].cmax2);
         a.img2 = sides[sd].img + ib;
         a.cinv2 = jb.j[jfirst[sd] + 1].cinv;
       } else {
@@ -673,7 +693,7 @@ void launch_tc_pass(int kind, int nsides, const TcPassSide* sides_in, int W, boo
 // single-side forms (test hooks)
 int launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
                         float* partial, int64_t pe, bool reduce1, uint8_t* img, cudaStream_t st) {
-  TcPassSide sd{s, P1, P2, OUT1, OUT2, partial, pe, img};
+  TcPassSide sd{s, P1, P2, OUT1, OUT2, partial, pe, img, nullptr, nullptr};
   int ns = 0;
   launch_tc_pass(P2 ? kPassDual : kPassRow, 1, &sd, W, reduce1, &ns, st);
   return ns;
@@ -681,7 +701,7 @@ int launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const f
 
 int launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t pe, bool reduce1,
                         uint8_t* img, cudaStream_t st) {
-  TcPassSide sd{s, P, nullptr, OUT, nullptr, partial, pe, img};
+  TcPassSide sd{s, P, nullptr, OUT, nullptr, partial, pe, img, nullptr, nullptr};
   int ns = 0;
   launch_tc_pass(kPassCol, 1, &sd, W, reduce1, &ns, st);
   return ns;
@@ -689,7 +709,7 @@ int launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, fl
 
 int launch_tc_proj_codes(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t pe,
                          uint8_t* img, cudaStream_t st) {
-  TcPassSide sd{s, nullptr, P, nullptr, OUT, partial, pe, img};
+  TcPassSide sd{s, nullptr, P, nullptr, OUT, partial, pe, img, nullptr, nullptr};
   int ns = 0;
   launch_tc_pass(kPassCodes, 1, &sd, W, true, &ns, st);
   return ns;

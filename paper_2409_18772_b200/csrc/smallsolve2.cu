@@ -715,6 +715,7 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
     jb.G[pr] = a;
   }
   if (threadIdx.x == 0) jb.counter[0] = 0;  // re-arm for the next launch (stream ordered)
+  if (jb.cmax && threadIdx.x < 64) jb.cmax[threadIdx.x] = 0u;  // the next apply64's column maxima
   __threadfence_block();
   __syncthreads();
   if constexpr (W <= 32) {
