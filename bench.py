@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--b-sharded", action="store_true",
+                    help="N > 1: also column-shard B over the ranks (SURVEY §8(e)(ii); codes, scales and L_B "
+                         "allgathered) instead of replicating it")
     return ap.parse_args()
 
 
@@ -370,12 +373,14 @@ def main():
         import torch.distributed as dist
 
         uid = broadcast_unique_id(get_unique_id() if rank == 0 else None, ws, rank, dev)
+    bsh = args.b_sharded and ws > 1
     h = Lrqmm(Mloc, N, K, bits, r, p, 1, "floor", "row", world_size=ws, world_rank=rank, unique_id=uid,
-              device=local, stream=stream, enable_timing=False)
+              device=local, stream=stream, enable_timing=False, b_sharded=bsh)
+    Bt_mine = Bt[h.b_rows[0]:h.b_rows[1]]  # this rank's rows of B^T (all of them unless --b-sharded)
 
     def step():
         h.quantize(SIDE_A, A)
-        h.quantize(SIDE_B, Bt)
+        h.quantize(SIDE_B, Bt_mine)
         h.rsvd_residual(OmA, OmB)
         h.gemm(D)
 
@@ -398,7 +403,7 @@ def main():
             ev = evs[i]
             ev[0].record(stream)
             h.quantize(SIDE_A, A)
-            h.quantize(SIDE_B, Bt)
+            h.quantize(SIDE_B, Bt_mine)
             ev[1].record(stream)
             h.rsvd_residual(OmA, OmB)
             ev[2].record(stream)
@@ -479,11 +484,11 @@ def main():
     e2e = None
     if not args.no_e2e:
         hA = torch.empty((Mloc, K), dtype=torch.float32, pin_memory=True)
-        hB = torch.empty((N, K), dtype=torch.float32, pin_memory=True)
+        hB = torch.empty((Bt_mine.shape[0], K), dtype=torch.float32, pin_memory=True)
         hOa = torch.empty((K, kk), dtype=torch.float32, pin_memory=True)
         hOb = torch.empty((K, kk), dtype=torch.float32, pin_memory=True)
         hD = torch.empty((Mloc, N), dtype=torch.float32, pin_memory=True)
-        hA.copy_(A); hB.copy_(Bt); hOa.copy_(OmA); hOb.copy_(OmB)
+        hA.copy_(A); hB.copy_(Bt_mine); hOa.copy_(OmA); hOb.copy_(OmB)
         npA, npB, npOa, npOb, npD = hA.numpy(), hB.numpy(), hOa.numpy(), hOb.numpy(), hD.numpy()
         h.run_host(npA, npB, npOa, npOb, npD)
         barrier(ws)
@@ -492,7 +497,7 @@ def main():
             h.run_host(npA, npB, npOa, npOb, npD)
         t_e2e = (time.perf_counter() - t0) / args.e2e_steps
         t_e2e = max_over_ranks(t_e2e, ws, dev)
-        h2d = 4 * (Mloc * K + N * K + 2 * K * kk)
+        h2d = 4 * (Mloc * K + Bt_mine.shape[0] * K + 2 * K * kk)
         d2h = 4 * Mloc * N
         e2e = {"value": 2.0 * Mloc * ws * N * K / t_e2e / 1e12, "unit": "TOPS", "h2d_bytes_per_step": h2d * ws,
                "d2h_bytes_per_step": d2h * ws, "ms_per_step": t_e2e * 1e3,
@@ -550,7 +555,8 @@ def main():
         "config": {"workload": label, "M": Mtot, "M_per_gpu": Mloc, "N": N, "K": K, "bits": bits, "rank": r,
                    "oversample": p, "power_iters": 1, "rounding": "floor", "scales": "per-row A / per-col B",
                    "l2": "inputs 2 GiB fp32/GPU > 126 MB L2 (no flush)",
-                   "parallelism": f"row-shard A x{ws}, B replicated" if ws > 1 else "single GPU"},
+                   "parallelism": (f"row-shard A x{ws}, B column-sharded x{ws} (allgather)" if bsh else
+                                   f"row-shard A x{ws}, B replicated") if ws > 1 else "single GPU"},
         "overhead_vs_bare_int8": t_step / t_bare,
         "overhead_vs_direct_quant": t_step / t_dq,
         "ms": {"bare_int8_gemm": t_bare * 1e3, "direct_quant_pipeline": t_dq * 1e3, "quantize_AB": t_quant * 1e3,

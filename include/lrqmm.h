@@ -87,6 +87,12 @@ typedef struct {
                         the fp32 residual fp32(x - code/lambda) with its own scales (same bits, rounding,
                         granularity; the paper's QT columns use trunc + per-tensor, reading #27) and
                         gemm returns alpha (A_q B_q + A_q R_Bq + R_Aq B_q [+ R_Aq R_Bq]) + beta D */
+  int b_sharded;     /* 0: every rank holds all of B^T (n rows).  1 (world_size > 1): B is column-sharded
+                        (SURVEY §8(e)(ii)): rank i holds rows [i*nb, min(n, (i+1)*nb)) of B^T, nb = ceil(n /
+                        world_size), and quantize(SIDE_B) takes that shard; B's RSVD reduces its Gram matrices
+                        and Z_B across ranks like A's, and the B codes, scales and correction factor L_B are
+                        allgathered (in place, NCCL) so that every rank's GEMM covers all n columns.  The
+                        inspection calls return this rank's rows of B.  Not with qt_terms. */
 } lrqmm_config_t;
 
 /* Host.  128-byte NCCL unique id for a world_size > 1 communicator (call on rank 0,

@@ -74,6 +74,14 @@ struct lrqmm_handle_s {
   alignas(64) CUtensorMap mapRB[4];
   cudaEvent_t ev[8] = {};
   ncclComm_t comm = nullptr;
+  // B column-sharded over the ranks (cfg.b_sharded): this rank owns rows
+  // [b_lo, b_lo + s[1].rows) of B^T inside blocks of b_blk rows; s[1].codes / lam / inv_lam and LB
+  // point at the rank's slice of the full (ws * b_blk row) buffers below, which the GEMM reads
+  // after the in-place allgathers.
+  bool bsh = false;
+  int64_t b_blk = 0, b_lo = 0;
+  int8_t* codes_b_full = nullptr;
+  float *lam_b_full = nullptr, *inv_b_full = nullptr, *LB_full = nullptr;
   // rsvd_residual as a CUDA graph: captured once on a private stream (the caller's stream may be
   // the legacy default stream, which cannot be captured), then launched onto the caller's stream
   cudaStream_t cap_st = nullptr;
@@ -174,6 +182,8 @@ static lrqmm_status_t validate(const lrqmm_config_t* c) {
   }
   if (c->qt_terms != 0 && c->qt_terms != 3 && c->qt_terms != 4) return LRQMM_ERR_INVALID_ARGUMENT;
   if (c->qt_terms != 0 && c->rank != 0) return LRQMM_ERR_UNSUPPORTED;  // QT and LRQMM are alternatives
+  if (c->b_sharded != 0 && c->b_sharded != 1) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (c->b_sharded && c->world_size > 1 && c->qt_terms != 0) return LRQMM_ERR_UNSUPPORTED;
   return LRQMM_OK;
 }
 
@@ -181,6 +191,12 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   if (!h) return LRQMM_OK;
   cudaSetDevice(h->cfg.device);
   if (h->st) cudaStreamSynchronize(h->st);
+  if (h->bsh) {  // side B's codes / scales / LB are slices of the full buffers
+    h->s[1].codes = h->codes_b_full;
+    h->s[1].lam = h->lam_b_full;
+    h->s[1].inv_lam = h->inv_b_full;
+    h->LB = h->LB_full;
+  }
   for (auto& s : h->s) {
     cudaFree(s.codes); cudaFree(s.lam); cudaFree(s.inv_lam); cudaFree(s.row_amax); cudaFree(s.lam_scalar); cudaFree(s.Om);
     cudaFree(s.Y); cudaFree(s.Q0); cudaFree(s.Z); cudaFree(s.Q1); cudaFree(s.Gp); cudaFree(s.G);
@@ -230,10 +246,19 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
   h->R2 = h->r > 0 ? (int)roundup(2 * h->r, 8) : 0;
   h->s[0].rows = cfg->m;
   h->s[1].rows = cfg->n;
+  h->bsh = cfg->b_sharded && cfg->world_size > 1;
+  if (h->bsh) {
+    h->b_blk = (cfg->n + cfg->world_size - 1) / cfg->world_size;
+    h->b_lo = h->b_blk * cfg->world_rank;
+    h->s[1].rows = std::max<int64_t>(0, std::min<int64_t>(h->b_blk, cfg->n - h->b_lo));
+  }
   const int64_t K = cfg->k;
+  const int64_t nfull = h->bsh ? h->b_blk * cfg->world_size : cfg->n;  // rows of the GEMM's B buffers
   bool ok = true;
-  for (auto& s : h->s) {
-    ok = ok && dalloc(&s.codes, s.rows * h->Kp) && dalloc(&s.lam, s.rows) && dalloc(&s.inv_lam, s.rows) && dalloc(&s.row_amax, s.rows) &&
+  for (int sd = 0; sd < 2; ++sd) {
+    Side& s = h->s[sd];
+    const int64_t cr = sd == 1 ? nfull : s.rows;  // codes / scales rows
+    ok = ok && dalloc(&s.codes, cr * h->Kp) && dalloc(&s.lam, cr) && dalloc(&s.inv_lam, cr) && dalloc(&s.row_amax, s.rows) &&
          dalloc(&s.lam_scalar, 1);
     if (h->W > 0) {
       s.ldu = h->Kp;
@@ -251,7 +276,7 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
     const int64_t maxrows = std::max<int64_t>({cfg->m, cfg->n, K});
     // split-K / split-row partials: <= 2 outputs x ~4 waves of splits, bounded at 64 MiB
     h->partial_elems = std::min<int64_t>((int64_t)16 << 20, 2 * 32 * maxrows * h->W);
-    ok = ok && dalloc(&h->LA, cfg->m * h->R2) && dalloc(&h->LB, cfg->n * h->R2) &&
+    ok = ok && dalloc(&h->LA, cfg->m * h->R2) && dalloc(&h->LB, nfull * h->R2) &&
          dalloc(&h->partial, h->partial_elems) && dalloc(&h->Gcross, (int64_t)h->W * h->W) &&
          dalloc(&h->gpart_cross, (int64_t)kGramMaxBlocks * h->W * h->W) && dalloc(&h->counter_cross, 1) &&
          dalloc(&h->VWbM, (int64_t)h->W * h->W);
@@ -261,9 +286,19 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
     lrqmm_destroy(h);
     return LRQMM_ERR_ALLOC;
   }
+  h->codes_b_full = h->s[1].codes;
+  h->lam_b_full = h->s[1].lam;
+  h->inv_b_full = h->s[1].inv_lam;
+  h->LB_full = h->LB;
+  if (h->bsh) {  // this rank's slices
+    h->s[1].codes += h->b_lo * h->Kp;
+    h->s[1].lam += h->b_lo;
+    h->s[1].inv_lam += h->b_lo;
+    if (h->LB) h->LB += h->b_lo * h->R2;
+  }
   GemmArgs g{};
   g.A = h->s[0].codes;
-  g.B = h->s[1].codes;
+  g.B = h->codes_b_full;
   g.M = std::max<int64_t>(cfg->m, 1);
   g.N = std::max<int64_t>(cfg->n, 1);
   g.Kp = h->Kp;
@@ -306,6 +341,8 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
 static void record(lrqmm_handle_t h, int i) {
   if (h->cfg.enable_timing) cudaEventRecord(h->ev[i], h->st);
 }
+
+static lrqmm_status_t allgather_b(lrqmm_handle_t h, void* full, size_t per_row_bytes);
 
 lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* X, int64_t ldx) {
   if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
@@ -353,6 +390,13 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
     b.U = nullptr;
     launch_quantize(b, h->st);
   }
+  if (side == LRQMM_SIDE_B && h->bsh) {
+    // every rank's GEMM multiplies by all of B: gather the codes and scales of the other shards
+    lrqmm_status_t g;
+    if ((g = allgather_b(h, h->codes_b_full, (size_t)h->Kp)) != LRQMM_OK) return g;
+    if ((g = allgather_b(h, h->lam_b_full, sizeof(float))) != LRQMM_OK) return g;
+    if ((g = allgather_b(h, h->inv_b_full, sizeof(float))) != LRQMM_OK) return g;
+  }
   record(h, side == LRQMM_SIDE_A ? 1 : 3);
   lrqmm_status_t e = check_launch(h);
   if (e != LRQMM_OK) return e;
@@ -387,6 +431,15 @@ static lrqmm_status_t allreduce_f32(lrqmm_handle_t h, float* buf, size_t n) {
   LQ_NCCL(ncclAllReduce(buf, buf, n, ncclFloat32, ncclSum, h->comm, h->st));
   return LRQMM_OK;
 }
+// B column-sharded: in-place allgather of the rank blocks (b_blk rows each) of a full-B buffer
+static lrqmm_status_t allgather_b(lrqmm_handle_t h, void* full, size_t per_row_bytes) {
+  const size_t cnt = (size_t)h->b_blk * per_row_bytes;
+  char* base = reinterpret_cast<char*>(full);
+  LQ_NCCL(ncclAllGather(base + cnt * h->cfg.world_rank, base, cnt, ncclInt8, h->comm, h->st));
+  return LRQMM_OK;
+}
+// side sd's rows are sharded over the ranks (A always when world > 1; B when b_sharded)
+static bool side_sharded(lrqmm_handle_t h, int sd) { return h->cfg.world_size > 1 && (sd == 0 || h->bsh); }
 
 // Split-K partial regions: one half of the partial buffer per side, so side A's partials can
 // wait for the fused Gram kernel while side B's pass runs.
@@ -421,7 +474,7 @@ static void pass_sides(lrqmm_handle_t h, int kind, int sides, const float* const
 static lrqmm_status_t gram_step(lrqmm_handle_t h, float* const Y[2], const int64_t n[2], const int nsp[2], int mode,
                                 float* const Q[2], bool a_sharded, int sides = 3, int which = 1) {
   const int W = h->W;
-  const bool ranks = a_sharded && h->cfg.world_size > 1 && (sides & 1);
+  const bool ranks = a_sharded && ((side_sharded(h, 0) && (sides & 1)) || (side_sharded(h, 1) && (sides & 2)));
   SmallJobs j{};
   j.n = 0;
   for (int sd = 0; sd < 2; ++sd)
@@ -439,8 +492,11 @@ static lrqmm_status_t gram_step(lrqmm_handle_t h, float* const Y[2], const int64
     }
   launch_fused_small(j, W, ranks ? 2 : mode, h->st);
   if (ranks) {
-    lrqmm_status_t e = allreduce_f64(h, h->s[0].G, (size_t)W * W);
-    if (e != LRQMM_OK) return e;
+    for (int sd = 0; sd < 2; ++sd)
+      if ((sides & (1 << sd)) && side_sharded(h, sd)) {
+        lrqmm_status_t e = allreduce_f64(h, h->s[sd].G, (size_t)W * W);
+        if (e != LRQMM_OK) return e;
+      }
     EigJobs ej{};
     ej.n = 0;
     for (int sd = 0; sd < 2; ++sd)
@@ -484,7 +540,9 @@ static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides) {
     // S2: Z = R^T Q0  (reduction over rows; the A side is summed over ranks before its Gram)
     pass_sides(h, kPassCol, sides, Q0s, nullptr, Zs, nullptr, multi, nsp, cm0);
     if (multi) {
-      if ((sides & 1) && (e = allreduce_f32(h, Zs[0], (size_t)K * W)) != LRQMM_OK) return e;
+      for (int sd = 0; sd < 2; ++sd)
+        if ((sides & (1 << sd)) && side_sharded(h, sd) && (e = allreduce_f32(h, Zs[sd], (size_t)K * W)) != LRQMM_OK)
+          return e;
       nsp[0] = nsp[1] = 1;  // multi -> reduce1: both Z are final
     }
     // O2: Q1 = orth(Z) (fp64 Gram + Cholesky, transform applied with fp64 accumulation, so Q1 is
@@ -534,6 +592,10 @@ static lrqmm_status_t assemble(lrqmm_handle_t h) {
   aj.j[2] = ApplyJob{h->s[1].Gp, h->s[0].VW, YB, h->VWbM, rows[1], W, r, h->LB, h->R2, 0};      // B~^T V_A + U_B S_B M
   aj.j[3] = ApplyJob{YB, h->s[1].VW, nullptr, nullptr, rows[1], W, r, h->LB, h->R2, r};         // U_B S_B
   launch_apply_jobs(aj, W, h->st);
+  if (h->bsh) {  // the epilogue of every rank's GEMM reads all rows of L_B
+    lrqmm_status_t e = allgather_b(h, h->LB_full, sizeof(float) * h->R2);
+    if (e != LRQMM_OK) return e;
+  }
   return check_launch(h);
 }
 
@@ -664,15 +726,15 @@ static lrqmm_status_t run_gemm(lrqmm_handle_t h, int epi, float alpha, float bet
   // QT term t (1-based): 1 = A_q B_q, 2 = A_q R_Bq, 3 = R_Aq B_q, 4 = R_Aq R_Bq (Eq. gemm_r_split)
   const bool ra = qt_term == 3 || qt_term == 4, rb = qt_term == 2 || qt_term == 4;
   g.A = ra ? h->s[0].rcodes : h->s[0].codes;
-  g.B = rb ? h->s[1].rcodes : h->s[1].codes;
+  g.B = rb ? h->s[1].rcodes : h->codes_b_full;
   g.M = h->cfg.m;
   g.N = h->cfg.n;
   g.Kp = h->Kp;
   g.epi = epi;
   g.inv_a = ra ? h->s[0].rinv : h->s[0].inv_lam;
-  g.inv_b = rb ? h->s[1].rinv : h->s[1].inv_lam;
+  g.inv_b = rb ? h->s[1].rinv : h->inv_b_full;
   g.LA = h->LA;
-  g.LB = h->LB;
+  g.LB = h->LB_full;
   g.R2 = h->r > 0 ? h->R2 : 0;
   g.alpha = alpha;
   g.beta = beta;
@@ -733,16 +795,17 @@ lrqmm_status_t lrqmm_run_host(lrqmm_handle_t h, const float* A_host, const float
   if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
   if (h->sticky != LRQMM_OK) return h->sticky;
   const int64_t m = h->cfg.m, n = h->cfg.n, k = h->cfg.k, kk = h->kk;
-  if ((!A_host && m * k > 0) || (!Bt_host && n * k > 0) || (!D_host && m * n > 0)) return LRQMM_ERR_INVALID_ARGUMENT;
+  const int64_t nb = h->s[1].rows;  // rows of B^T on this rank (all of them unless b_sharded)
+  if ((!A_host && m * k > 0) || (!Bt_host && nb * k > 0) || (!D_host && m * n > 0)) return LRQMM_ERR_INVALID_ARGUMENT;
   if (h->r > 0 && (!omegaA_host || !omegaB_host)) return LRQMM_ERR_INVALID_ARGUMENT;
   cudaSetDevice(h->cfg.device);
   if (!h->hA) {
-    bool ok = dalloc(&h->hA, m * k) && dalloc(&h->hB, n * k) && dalloc(&h->hD, m * n);
+    bool ok = dalloc(&h->hA, m * k) && dalloc(&h->hB, nb * k) && dalloc(&h->hD, m * n);
     if (ok && kk > 0) ok = dalloc(&h->hOmA, k * kk) && dalloc(&h->hOmB, k * kk);
     if (!ok) return fail(h, LRQMM_ERR_ALLOC);
   }
   LQ_CUDA(cudaMemcpyAsync(h->hA, A_host, sizeof(float) * m * k, cudaMemcpyHostToDevice, h->st));
-  LQ_CUDA(cudaMemcpyAsync(h->hB, Bt_host, sizeof(float) * n * k, cudaMemcpyHostToDevice, h->st));
+  LQ_CUDA(cudaMemcpyAsync(h->hB, Bt_host, sizeof(float) * nb * k, cudaMemcpyHostToDevice, h->st));
   if (kk > 0) {
     LQ_CUDA(cudaMemcpyAsync(h->hOmA, omegaA_host, sizeof(float) * k * kk, cudaMemcpyHostToDevice, h->st));
     LQ_CUDA(cudaMemcpyAsync(h->hOmB, omegaB_host, sizeof(float) * k * kk, cudaMemcpyHostToDevice, h->st));

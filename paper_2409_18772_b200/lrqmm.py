@@ -48,7 +48,7 @@ class Config(ctypes.Structure):
         ("power_iters", ctypes.c_int), ("rounding", ctypes.c_int), ("granularity", ctypes.c_int),
         ("world_size", ctypes.c_int), ("world_rank", ctypes.c_int),
         ("nccl_unique_id", ctypes.c_void_p), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
-        ("enable_timing", ctypes.c_int), ("qt_terms", ctypes.c_int),
+        ("enable_timing", ctypes.c_int), ("qt_terms", ctypes.c_int), ("b_sharded", ctypes.c_int),
     ]
 
 
@@ -123,13 +123,18 @@ class Lrqmm:
     def __init__(self, m: int, n: int, k: int, bits: int = 4, rank: int = 16, oversample: int = 5,
                  power_iters: int = 1, rounding: str = "floor", granularity: str = "row",
                  world_size: int = 1, world_rank: int = 0, unique_id: bytes | None = None,
-                 device: int = 0, stream=None, enable_timing: bool = False, qt_terms: int = 0):
+                 device: int = 0, stream=None, enable_timing: bool = False, qt_terms: int = 0,
+                 b_sharded: bool = False):
         import torch
 
         lib = load_library()
         self.lib = lib
         self.m, self.n, self.k = m, n, k
         self.bits, self.rank, self.oversample = bits, rank, oversample
+        # rows of B^T this rank holds (b_sharded: blocks of ceil(n / world_size) rows)
+        blk = -(-n // world_size) if (b_sharded and world_size > 1) else n
+        lo = blk * world_rank if (b_sharded and world_size > 1) else 0
+        self.b_rows = (lo, max(0, min(n, lo + blk)))
         self.device = device
         if stream is None:
             stream = torch.cuda.current_stream(device)
@@ -137,7 +142,8 @@ class Lrqmm:
         self._uid = (ctypes.c_ubyte * 128).from_buffer_copy(unique_id) if unique_id else None
         cfg = Config(m, n, k, bits, rank, oversample, power_iters, ROUND[rounding], GRAN[granularity],
                      world_size, world_rank, ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None,
-                     device, ctypes.c_void_p(stream.cuda_stream), 1 if enable_timing else 0, qt_terms)
+                     device, ctypes.c_void_p(stream.cuda_stream), 1 if enable_timing else 0, qt_terms,
+                     1 if b_sharded else 0)
         h = ctypes.c_void_p()
         _check(lib.lrqmm_create(ctypes.byref(cfg), ctypes.byref(h)), "lrqmm_create")
         self.h = h

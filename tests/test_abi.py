@@ -58,6 +58,9 @@ def _cfg(**kw):
     (dict(power_iters=0), 10),                # q >= 1 required (reading #10)
     (dict(rounding=7), 1),
     (dict(world_size=2, world_rank=0), 1),    # multi-rank needs a unique id
+    (dict(b_sharded=2), 1),                   # b_sharded is 0 or 1
+    (dict(rank=0, qt_terms=3, b_sharded=1, world_size=2,
+          nccl_unique_id=ctypes.cast(ctypes.create_string_buffer(128), ctypes.c_void_p)), 10),  # QT not B-sharded
 ])
 def test_create_validates_on_host(lib, kw, code):
     h = ctypes.c_void_p()

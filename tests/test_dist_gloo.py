@@ -121,6 +121,70 @@ def test_sharded_rsvd_matches_oracle(tmp_path, M, K, bits, r, p, q):
         np.testing.assert_allclose(np.abs(V_r.T @ V), np.eye(V.shape[1]), atol=1e-8)
 
 
+def _allgather_blocks(x: np.ndarray, blk: int) -> np.ndarray:
+    """In-place allgather of equal blocks of `blk` rows (the last rank's block zero-padded), as
+    liblrqmm's allgather_b does for the B codes, scales and L_B."""
+    pad = np.zeros((blk,) + x.shape[1:], dtype=x.dtype)
+    pad[: x.shape[0]] = x
+    out = [torch.zeros_like(torch.from_numpy(pad)) for _ in range(WS)]
+    dist.all_gather(out, torch.from_numpy(pad))
+    return np.concatenate([o.numpy() for o in out])
+
+
+def _worker_bsh(rank, port, M, N, K, bits, r, p, q, out_dir):
+    """B column-sharded mode (cfg.b_sharded): A rows AND B^T rows sharded; both
+    RSVDs reduce their Grams and Z across ranks; the B codes, scales and L_B are allgathered in
+    blocks of ceil(N / ws) rows; each rank then forms its rows of D against all N columns."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WS)
+    try:
+        import bench
+
+        A = S.gen_matrix("normal", M, K, 21)
+        Bt = S.gen_matrix("normal", N, K, 22)
+        OmA, OmB = S.gen_omega(K, r + p, 23), S.gen_omega(K, r + p, 24)
+        lo, hi = bench.row_shard(M, WS, rank)
+        blk = -(-N // WS)
+        blo, bhi = blk * rank, min(N, blk * (rank + 1))
+        ca, la = O.quantize(A[lo:hi], bits, "floor", "row")
+        cb, lb = O.quantize(Bt[blo:bhi], bits, "floor", "row")
+        RA = O.residual(A[lo:hi], ca, la)
+        RB = O.residual(Bt[blo:bhi], cb, lb)
+        USa, Va = _sharded_rsvd(RA, OmA, r, q)
+        USb, Vb = _sharded_rsvd(RB, OmB, r, q)
+        # factor assembly on local rows (Alg. 2 lines 361-366 folded into L_A, L_B)
+        Af = O.dequantize(ca, la)
+        Btf = O.dequantize(cb, lb)
+        LA = np.hstack([USa, Af @ Vb])
+        LB = np.hstack([Btf @ Va + USb @ (Vb.T @ Va), USb])
+        # allgathers: every rank's GEMM covers all N columns
+        cb_all = _allgather_blocks(cb, blk)[:N]
+        lb_all = _allgather_blocks(lb, blk)[:N]
+        LB_all = _allgather_blocks(LB, blk)[:N]
+        D = O.dequant_result(O.int_gemm(ca, cb_all), la, lb_all) + LA @ LB_all.T
+        np.save(os.path.join(out_dir, f"d_{rank}.npy"), D)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("M,N,K,bits,r,p,q", [(64, 90, 80, 4, 4, 3, 1), (50, 77, 64, 8, 5, 3, 1)])
+def test_b_sharded_schedule_matches_oracle(tmp_path, M, N, K, bits, r, p, q):
+    port = _free_port()
+    mp.spawn(_worker_bsh, args=(port, M, N, K, bits, r, p, q, str(tmp_path)), nprocs=WS, join=True)
+    import bench
+
+    A = S.gen_matrix("normal", M, K, 21)
+    Bt = S.gen_matrix("normal", N, K, 22)
+    ref = O.lrqmm(A, Bt, bits, r, S.gen_omega(K, r + p, 23), S.gen_omega(K, r + p, 24), q=q)
+    for rank in range(WS):
+        lo, hi = bench.row_shard(M, WS, rank)
+        D = np.load(tmp_path / f"d_{rank}.npy")
+        assert D.shape == (hi - lo, N)
+        np.testing.assert_allclose(D, ref[lo:hi], rtol=0, atol=1e-9 * np.abs(ref).max())
+
+
 def test_row_shard_covers_rows():
     import bench
 
