@@ -159,8 +159,12 @@ def rsvd(R: np.ndarray, omega: np.ndarray, r: int, q: int = 1):
                          USigma = Y V_W, V = Q1 V_W        (SVD of B)
       else:              USigma = Y,     V = Q1
     """
-    if q < 1:
-        raise ValueError("variant (b) needs q >= 1 (reading #10)")
+    if q == 0:
+        # Algorithm 1 itself with Q from one sampling pass (reading #30): Q = orth(R Omega),
+        # B = Q^* R, SVD(B), U = Q U' (PAPER.md:124-140), truncated to rank r
+        return rsvd_spec_variant(R, omega, r, 0)
+    if q < 0:
+        raise ValueError("q >= 0")
     R = np.asarray(R, dtype=np.float64)
     Om = np.asarray(omega, dtype=np.float64)
     Y = R @ Om

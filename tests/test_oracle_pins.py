@@ -392,3 +392,28 @@ def test_negative_control_wrong_rounding_fails_table_pin(golden_tables):
     C = O.matmul_exact(A, Bt)
     e = O.relative_error(C, O.direct_quant(A, Bt, 4, rounding="nearest", granularity="tensor"))
     assert e < golden_tables[("u01", 4)]["dq"] / 10
+
+
+def test_rsvd_q0_is_algorithm1_on_the_sampled_basis():
+    """q = 0 (reading #30): Algorithm 1 on Q = orth(R Omega).  Pins: (i) R of
+    exact rank <= k is recovered exactly (Q spans range(R) almost surely, so Q Q^T R = R);
+    (ii) the rank-r result is the Eckart-Young truncation of the PROJECTION Q Q^T R (SVD of B =
+    Q^T R, computed here independently through the Gram of the projection); (iii) a structured
+    sketch whose first column is all ones captures a constant (mean) residual exactly."""
+    rng = np.random.default_rng(41)
+    R = rng.standard_normal((30, 4)) @ rng.standard_normal((4, 25))
+    US, V = O.rsvd(R, rng.standard_normal((25, 6)), 6, 0)
+    np.testing.assert_allclose(US @ V.T, R, atol=1e-10 * np.abs(R).max())
+    R = rng.standard_normal((40, 33))
+    Om = rng.standard_normal((33, 9))
+    US, V = O.rsvd(R, Om, 4, 0)
+    Q, _ = np.linalg.qr(R @ Om)
+    P = Q @ (Q.T @ R)
+    w, E = np.linalg.eigh(P.T @ P)           # right singular vectors of the projection
+    E4 = E[:, np.argsort(-w)[:4]]
+    np.testing.assert_allclose(US @ V.T, P @ E4 @ E4.T, atol=1e-9 * np.abs(P).max())
+    Rc = np.full((20, 16), 0.37)             # floor-rounding residual mean: a constant matrix
+    Om = rng.standard_normal((16, 3))
+    Om[:, 0] = 1.0
+    US, V = O.rsvd(Rc, Om, 1, 0)
+    np.testing.assert_allclose(US @ V.T, Rc, atol=1e-12)
