@@ -464,6 +464,7 @@ def main():
 
     # accuracy on a row sample (exact product in fp64 for 256 rows)
     errs = {}
+    q0_variant = None
     if rank == 0:
         rows = torch.arange(0, Mloc, max(1, Mloc // 256), device=dev)[:256]
         Cex = A[rows].double() @ Bt.double().T
@@ -477,6 +478,29 @@ def main():
             with Lrqmm(Mloc, N, K, bits, 0, 0, 1, rnd, gran, device=local, stream=stream, qt_terms=qt) as hq:
                 hq.quantize(SIDE_A, A); hq.quantize(SIDE_B, Bt); hq.gemm(D); hq.sync()
             errs[name] = float(torch.linalg.norm(D[rows].double() - Cex) / nrm)
+        # labelled variant (reading #30): q = 0 with a structured sketch (first column
+        # all ones): two passes over R plus a codes-only pass instead of q = 1's three R passes
+        if r > 0:
+            OmA1, OmB1 = OmA.clone(), OmB.clone()
+            OmA1[:, 0] = 1.0
+            OmB1[:, 0] = 1.0
+            with Lrqmm(Mloc, N, K, bits, r, p, 0, "floor", "row", device=local, stream=stream) as h0:
+                def step_q0():
+                    h0.quantize(SIDE_A, A); h0.quantize(SIDE_B, Bt); h0.rsvd_residual(OmA1, OmB1); h0.gemm(D)
+                for _ in range(3):
+                    step_q0()
+                h0.sync()
+                q0s, q0e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                q0s.record(stream)
+                for _ in range(args.steps):
+                    step_q0()
+                q0e.record(stream)
+                h0.sync()
+                t_q0 = q0s.elapsed_time(q0e) / 1e3 / args.steps
+                errs["lrqmm_q0_ones_sketch"] = float(torch.linalg.norm(D[rows].double() - Cex) / nrm)
+                q0_variant = {"ms_per_step": t_q0 * 1e3, "value": 2.0 * Mloc * N * K / t_q0 / 1e12, "unit": "TOPS",
+                              "note": "power_iters=0 + Omega[:,0]=1 (SURVEY f4 / E3 (c), reading #30): labelled variant, "
+                                      "not the paper's q; error in rel_fro_error.lrqmm_q0_ones_sketch"}
         del Cex
 
     # end to end through the C ABI with pinned HOST buffers: every rank runs lrqmm_run_host on its
@@ -562,6 +586,7 @@ def main():
         "ms": {"bare_int8_gemm": t_bare * 1e3, "direct_quant_pipeline": t_dq * 1e3, "quantize_AB": t_quant * 1e3,
                "rsvd_residual": t_rsvd * 1e3, "gemm_fused_epilogue": t_gemm * 1e3},
         "bare_int8_tops": 2.0 * Mloc * N * K / t_bare / 1e12,
+        "variant_q0_ones_sketch": q0_variant,
         "static_b": None if t_static is None else {
             "ms_per_step": t_static * 1e3, "value": ops / t_static / 1e12, "unit": "TOPS",
             "overhead_vs_bare_int8": t_static / t_bare,

@@ -50,7 +50,7 @@ typedef enum {
   LRQMM_ERR_CUDA = 7,
   LRQMM_ERR_NCCL = 8,
   LRQMM_ERR_ALLOC = 9,
-  LRQMM_ERR_UNSUPPORTED = 10      /* e.g. power_iters < 1, bits not in {4, 8}, not an sm_100 device */
+  LRQMM_ERR_UNSUPPORTED = 10      /* e.g. power_iters < 0, bits not in {4, 8}, not an sm_100 device */
 } lrqmm_status_t;
 
 typedef enum { LRQMM_SIDE_A = 0, LRQMM_SIDE_B = 1 } lrqmm_side_t;
@@ -73,7 +73,10 @@ typedef struct {
   int bits;        /* N of Eq. quantA: 4 or 8; codes in [-qmax, qmax], qmax = 2^(N-1)-1, stored as int8 */
   int rank;        /* r >= 0; 0 = direct quantization (no residual correction) */
   int oversample;  /* p >= 0; sketch width k = r + p <= 64 */
-  int power_iters; /* q >= 1 (reading #10) */
+  int power_iters; /* q >= 0: power iterations of the range finder (reading #10: q = 1 for LRQMM's accuracy).
+                      q = 0 is Algorithm 1 on the sampled basis Q = orth(R Omega) (two passes over R plus a
+                      codes-only pass; reading #30) -- with a structured sketch whose first column is all ones
+                      it matches q = 1's accuracy, a labelled variant */
   int rounding;    /* lrqmm_round_t */
   int granularity; /* lrqmm_gran_t */
   int world_size;  /* >= 1; ranks that row-shard A */

@@ -174,7 +174,7 @@ static lrqmm_status_t validate(const lrqmm_config_t* c) {
   const int64_t qmax = (1 << (c->bits - 1)) - 1;
   if (c->k * qmax * qmax > (int64_t)INT32_MAX) return LRQMM_ERR_OVERFLOW;  // reading #24
   if (c->rank > 0) {
-    if (c->power_iters < 1) return LRQMM_ERR_UNSUPPORTED;  // reading #10
+    if (c->power_iters < 0) return LRQMM_ERR_UNSUPPORTED;  // q = 0: Algorithm 1 on orth(R Omega), reading #30
     const int64_t kk = (int64_t)c->rank + c->oversample;
     if (kk > kMaxWidth || c->rank > 32) return LRQMM_ERR_RANK;
     // r + p <= min(rows, K) of each side (A: global rows checked per shard)
@@ -531,6 +531,18 @@ static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides) {
   const unsigned* cm0[2] = {h->s[0].cmax0, h->s[1].cmax0};
   const unsigned* cm1[2] = {h->s[0].cmax1, h->s[1].cmax1};
   lrqmm_status_t e;
+  if (h->cfg.power_iters == 0) {
+    // q = 0 (reading #30): S1 Y = R Omega; O1 Q0 = orth(Y); S2 Z = R^T Q0 = B^T of Algorithm 1
+    // (B = Q0^* R).  Z goes to the Q1 buffer (the K-side factor), reduced.
+    const float* Oms[2] = {h->s[0].Om, h->s[1].Om};
+    pass_sides(h, kPassRow, sides, Oms, nullptr, Ys, nullptr, false, nsp);
+    if ((e = gram_step(h, Ys, rows, nsp, 0, Q0s, true, sides, 0)) != LRQMM_OK) return e;
+    pass_sides(h, kPassCol, sides, Q0s, nullptr, Q1s, nullptr, true, nsp, cm0);
+    for (int sd = 0; sd < 2; ++sd)
+      if ((sides & (1 << sd)) && side_sharded(h, sd) && (e = allreduce_f32(h, Q1s[sd], (size_t)K * W)) != LRQMM_OK)
+        return e;
+    return check_launch(h);
+  }
   // S1: Y = R Omega   (Algorithm 1 sampling)
   const float* Oms[2] = {h->s[0].Om, h->s[1].Om};
   pass_sides(h, kPassRow, sides, Oms, nullptr, Ys, nullptr, false, nsp);
@@ -583,8 +595,9 @@ static lrqmm_status_t assemble(lrqmm_handle_t h) {
   launch_cross_small(h->Gcross, h->s[0].VW, h->s[1].VW, W, h->r, h->VWbM, h->st);
   const int r = h->r;
   const int64_t rows[2] = {h->s[0].rows, h->s[1].rows};
-  float* YA = h->s[0].Y;
-  float* YB = h->s[1].Y;
+  // row-side factor: W = R Q1 (q >= 1), or the orthonormal Q0 (q = 0: R_k = Q0 B, B = Z^T)
+  float* YA = h->cfg.power_iters == 0 ? h->s[0].Q0 : h->s[0].Y;
+  float* YB = h->cfg.power_iters == 0 ? h->s[1].Q0 : h->s[1].Y;
   ApplyJobs aj{};
   aj.n = 4;
   aj.j[0] = ApplyJob{YA, h->s[0].VW, nullptr, nullptr, rows[0], W, r, h->LA, h->R2, 0};        // U_A S_A
@@ -611,6 +624,22 @@ static lrqmm_status_t rsvd_body(lrqmm_handle_t h, int kind) {
   lrqmm_status_t e;
   if ((e = rsvd_chain(h, sides)) != LRQMM_OK) return e;
   int nsp[2] = {1, 1};
+  if (h->cfg.power_iters == 0) {
+    const int64_t kdim[2] = {h->cfg.k, h->cfg.k};
+    if (kind != 2) {
+      // cross products G'_X = X~ Z_other (codes-only pass over both sides; both are needed even when
+      // B's factors are resident, since Z_A is new)
+      const float* other[2] = {Q1s[1], Q1s[0]};
+      float* Gps[2] = {h->s[0].Gp, h->s[1].Gp};
+      pass_sides(h, kPassCodes, 3, nullptr, other, nullptr, Gps, true, nsp);
+      if ((e = fork_cross_gram(h)) != LRQMM_OK) return e;
+    }
+    // truncation: SVD of B = Z^T through eig(Z^T Z) (Algorithm 1); Z is replicated
+    int one[2] = {1, 1};
+    if ((e = gram_step(h, Q1s, kdim, one, 1, nullptr, false, sides)) != LRQMM_OK) return e;
+    if (kind == 2) return check_launch(h);
+    return assemble(h);
+  }
   // S3 (+ cross): W_X = R_X Q1_X, and G'_X = X~ Q1_other in the same pass over X when the other
   //   side's Q1 is current (Algorithm 1 on R^T: B = Q1^T R^T = W^T; RC1/RC2 skinny
   //   products)

@@ -55,7 +55,7 @@ def _cfg(**kw):
     (dict(m=-1), 2),
     (dict(rank=40, oversample=30), 3),        # r + p > 64
     (dict(rank=60, oversample=10, k=32), 3),  # r + p > K
-    (dict(power_iters=0), 10),                # q >= 1 required (reading #10)
+    (dict(power_iters=-1), 10),               # q >= 0 required (readings #10, #30)
     (dict(rounding=7), 1),
     (dict(world_size=2, world_rank=0), 1),    # multi-rank needs a unique id
     (dict(b_sharded=2), 1),                   # b_sharded is 0 or 1

@@ -269,6 +269,41 @@ def test_full_call_makes_b_resident():
         check_d(A2, Bt, {"D": D.cpu().numpy().astype(np.float64)}, ref2)
 
 
+# ------------------------------------- q = 0 / structured-sketch 2-pass RSVD
+@pytest.mark.parametrize("ones_col", [False, True])
+@pytest.mark.parametrize("dist,bits,shape,r,p", [("u01", 4, (320, 300, 640), 8, 5), ("exp4", 8, (257, 390, 1000), 16, 5),
+                                                ("normal", 4, (500, 130, 777), 4, 0), ("pois10", 4, (129, 520, 300), 32, 5)])
+def test_q0_rsvd_matches_oracle(ones_col, dist, bits, shape, r, p, gemm_variant):
+    """power_iters = 0 (reading #30): Algorithm 1 on Q = orth(R Omega), with a
+    Gaussian sketch or the structured sketch whose first column is all ones."""
+    M, N, K = shape
+    A, Bt, OmA, OmB = S.problem(M, N, K, r + p, s=60, dist=dist)
+    if ones_col:
+        OmA[:, 0] = 1.0
+        OmB[:, 0] = 1.0
+    ref = O.lrqmm(A, Bt, bits, r, OmA, OmB, q=0)
+    check_d(A, Bt, run_gpu(A, Bt, bits, r, p, OmA, OmB, q=0), ref)
+
+
+def test_q0_static_b_matches_oracle():
+    M, N, K, r, p = 300, 256, 512, 10, 5
+    _, Bt, _, OmB = S.problem(M, N, K, r + p, s=61, dist="u01")
+    OmB[:, 0] = 1.0
+    with Lrqmm(M, N, K, 4, r, p, 0) as h:
+        h.quantize(SIDE_B, cu(Bt))
+        h.rsvd_residual_b(cu(OmB))
+        for call in range(2):
+            A, _, OmA, _ = S.problem(M, N, K, r + p, s=62 + call, dist="exp4")
+            OmA[:, 0] = 1.0
+            ref = O.lrqmm(A, Bt, 4, r, OmA, OmB, q=0)
+            h.quantize(SIDE_A, cu(A))
+            h.rsvd_residual(cu(OmA))
+            D = torch.empty((M, N), device=DEV)
+            h.gemm(D)
+            h.sync()
+            check_d(A, Bt, {"D": D.cpu().numpy().astype(np.float64)}, ref)
+
+
 # ------------------------------------------------ QuantTensor comparison columns (SURVEY f1)
 @pytest.mark.parametrize("terms", [3, 4])
 @pytest.mark.parametrize("rounding,gran", [("trunc", "tensor"), ("floor", "row"), ("nearest", "row")])
