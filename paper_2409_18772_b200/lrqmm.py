@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblrqmm.so")
+# LRQMM_LIB: another build of this library (A/B timing of two builds in one session, tools/ab.sh)
+LIB_PATH = os.environ.get("LRQMM_LIB") or os.path.join(_HERE, "liblrqmm.so")
 
 SIDE_A, SIDE_B = 0, 1
 ROUND = {"floor": 0, "trunc": 1, "nearest": 2}
