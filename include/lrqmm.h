@@ -116,6 +116,28 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out);
  * buffer, so X is not referenced after this call's work completes in stream order. */
 lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* X, int64_t ldx);
 
+/* Convolution geometry for lrqmm_quantize_im2col (NHWC input, square or rectangular windows). */
+typedef struct {
+  int64_t batch;
+  int H, W, C;             /* input height, width, channels */
+  int kh, kw;              /* window */
+  int stride_h, stride_w;  /* >= 1 */
+  int pad_h, pad_w;        /* >= 0, zero padding */
+  int dil_h, dil_w;        /* >= 1 */
+} lrqmm_conv_t;
+
+/* Implicit-im2col quantization: the same as lrqmm_quantize on the im2col matrix
+ * of a convolution, without materialising it.  X (device, fp32) is the NHWC input
+ * [batch][H][W][C], dense; the side's matrix has rows r = (b, ho, wo) in that order (Ho = (H + 2 pad_h
+ * - dil_h (kh - 1) - 1) / stride_h + 1, likewise Wo) and columns k = (i kw + j) C + c, element
+ * X[b][ho stride_h - pad_h + i dil_h][wo stride_w - pad_w + j dil_w][c] (0 outside the image).  The
+ * weights passed as the other side must use the same k order (B^T row = one output channel,
+ * [kh][kw][C] flattened).  Codes, lambda and residual planes are bit-identical to lrqmm_quantize of
+ * the explicit matrix.  Errors: LRQMM_ERR_SHAPE if batch Ho Wo != the side's rows or kh kw C != k;
+ * LRQMM_ERR_INVALID_ARGUMENT for a null X or a bad geometry; LRQMM_ERR_UNSUPPORTED with per-tensor
+ * scales or qt_terms.  Stream-ordered like lrqmm_quantize. */
+lrqmm_status_t lrqmm_quantize_im2col(lrqmm_handle_t h, lrqmm_side_t side, const float* X, const lrqmm_conv_t* conv);
+
 /* RSVD of both residuals (Alg. 2) and assembly of the
  * correction factors L_A = [U_A S_A | A_F V_B], L_B = [B_F^T V_A + U_B S_B (V_B^T V_A) | U_B S_B]
  * (Alg. 2).  omegaA / omegaB: k x (r+p) fp32 sketches (ld ldo >= r+p), the

@@ -299,3 +299,27 @@ def frobenius_norm(X) -> float:
 def relative_error(C_exact, C_approx) -> float:
     """||C - C~||_F / ||C||_F, PAPER.md:687."""
     return frobenius_norm(np.asarray(C_exact, np.float64) - np.asarray(C_approx, np.float64)) / frobenius_norm(C_exact)
+
+
+# ---------------------------------------------------------------------------
+# im2col of an NHWC convolution input (SURVEY f3: the conv-layer workloads of PAPER.md:822 as
+# GEMMs).  Test infrastructure: the explicit matrix whose quantization lrqmm_quantize_im2col
+# must reproduce bit for bit.
+# ---------------------------------------------------------------------------
+def im2col_nhwc(X, kh: int, kw: int, stride=(1, 1), pad=(0, 0), dilation=(1, 1)) -> np.ndarray:
+    """Rows (b, ho, wo), columns (i, j, c): element X[b, ho*sh - ph + i*dh, wo*sw - pw + j*dw, c],
+    zero outside the image (zero padding)."""
+    X = np.asarray(X)
+    B, H, W, C = X.shape
+    sh, sw = stride
+    ph, pw = pad
+    dh, dw = dilation
+    Ho = (H + 2 * ph - dh * (kh - 1) - 1) // sh + 1
+    Wo = (W + 2 * pw - dw * (kw - 1) - 1) // sw + 1
+    Xp = np.zeros((B, H + 2 * ph, W + 2 * pw, C), dtype=X.dtype)
+    Xp[:, ph:ph + H, pw:pw + W, :] = X
+    out = np.empty((B, Ho, Wo, kh, kw, C), dtype=X.dtype)
+    for i in range(kh):
+        for j in range(kw):
+            out[:, :, :, i, j, :] = Xp[:, i * dh: i * dh + sh * (Ho - 1) + 1: sh, j * dw: j * dw + sw * (Wo - 1) + 1: sw, :]
+    return out.reshape(B * Ho * Wo, kh * kw * C)

@@ -30,6 +30,11 @@ struct QuantArgs {
   int64_t uplane;         // bytes between the h and l planes
 };
 void launch_quantize(const QuantArgs& a, cudaStream_t st);
+// implicit im2col of an NHWC convolution input: rows (b, ho, wo), K = kh kw C
+struct ConvGeom {
+  int batch, H, W, C, kh, kw, sh, sw, ph, pw, dh, dw, Ho, Wo;
+};
+void launch_quantize_im2col(const QuantArgs& a, const ConvGeom& g, cudaStream_t st);
 // QT: R = fp32(X - code / lambda) (rows x K, dense), fp64 arithmetic as the oracle
 void launch_resid_f32(const float* X, int64_t ldx, const int8_t* codes, int Kp, const float* lam, int64_t rows, int K,
                       float* R, cudaStream_t st);

@@ -406,6 +406,56 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
   return LRQMM_OK;
 }
 
+lrqmm_status_t lrqmm_quantize_im2col(lrqmm_handle_t h, lrqmm_side_t side, const float* X, const lrqmm_conv_t* cv) {
+  if (!h || !cv) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (h->sticky != LRQMM_OK) return h->sticky;
+  if (side != LRQMM_SIDE_A && side != LRQMM_SIDE_B) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (h->cfg.granularity == LRQMM_SCALE_PER_TENSOR || h->cfg.qt_terms > 0) return LRQMM_ERR_UNSUPPORTED;
+  if (cv->batch < 0 || cv->H < 1 || cv->W < 1 || cv->C < 1 || cv->kh < 1 || cv->kw < 1 || cv->stride_h < 1 ||
+      cv->stride_w < 1 || cv->pad_h < 0 || cv->pad_w < 0 || cv->dil_h < 1 || cv->dil_w < 1)
+    return LRQMM_ERR_INVALID_ARGUMENT;
+  const int64_t eh = (int64_t)cv->dil_h * (cv->kh - 1) + 1, ew = (int64_t)cv->dil_w * (cv->kw - 1) + 1;
+  const int64_t Ho = (cv->H + 2LL * cv->pad_h - eh) / cv->stride_h + 1, Wo = (cv->W + 2LL * cv->pad_w - ew) / cv->stride_w + 1;
+  if (cv->H + 2LL * cv->pad_h < eh || cv->W + 2LL * cv->pad_w < ew) return LRQMM_ERR_INVALID_ARGUMENT;
+  Side& s = h->s[side];
+  if (cv->batch * Ho * Wo != s.rows || (int64_t)cv->kh * cv->kw * cv->C != h->cfg.k) return LRQMM_ERR_SHAPE;
+  if (!X && s.rows > 0) return LRQMM_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(h->cfg.device);
+  record(h, side == LRQMM_SIDE_A ? 0 : 2);
+  QuantArgs a;
+  a.X = X;
+  a.ldx = h->cfg.k;
+  a.rows = s.rows;
+  a.K = (int)h->cfg.k;
+  a.Kp = h->Kp;
+  a.qmax = h->qmax;
+  a.mode = h->cfg.rounding;
+  a.codes = s.codes;
+  a.lam = s.lam;
+  a.inv_lam = s.inv_lam;
+  a.lam_fixed = nullptr;
+  a.err_flag = h->err_flag;
+  a.U = s.U;
+  a.ldu = s.ldu;
+  a.uplane = s.rows * s.ldu;
+  ConvGeom g{(int)cv->batch, cv->H, cv->W, cv->C, cv->kh, cv->kw, cv->stride_h, cv->stride_w, cv->pad_h, cv->pad_w,
+             cv->dil_h, cv->dil_w, (int)Ho, (int)Wo};
+  launch_quantize_im2col(a, g, h->st);
+  if (side == LRQMM_SIDE_B && h->bsh) {
+    lrqmm_status_t e;
+    if ((e = allgather_b(h, h->codes_b_full, (size_t)h->Kp)) != LRQMM_OK) return e;
+    if ((e = allgather_b(h, h->lam_b_full, sizeof(float))) != LRQMM_OK) return e;
+    if ((e = allgather_b(h, h->inv_b_full, sizeof(float))) != LRQMM_OK) return e;
+  }
+  record(h, side == LRQMM_SIDE_A ? 1 : 3);
+  lrqmm_status_t e = check_launch(h);
+  if (e != LRQMM_OK) return e;
+  h->state |= (side == LRQMM_SIDE_A ? 1 : 2);
+  h->state &= ~4;
+  if (side == LRQMM_SIDE_B) h->state &= ~8;
+  return LRQMM_OK;
+}
+
 static SideView view(lrqmm_handle_t h, int sd) {
   SideView v;
   v.Uh = h->s[sd].U;

@@ -674,6 +674,113 @@ void launch_quantize_rows(const QuantArgs& a, bool fixed, cudaStream_t st) {
   }
 }
 
+// ------------------------------------------------------------ implicit im2col
+// K1 on the im2col matrix of a convolution without materialising it: row (b, ho, wo), column
+// k = (i kw + j) C + c reads X[b, ho sh - ph + i dh, wo sw - pw + j dw, c] of the NHWC input (zero
+// outside the image).  One warp per row: pass 1 the row amax, pass 2 (the same elements, now in
+// L1 / L2) codes and the Q15 residual planes, with the exact arithmetic of k1_quantize_tma.  A
+// 3x3 window reads each activation ~9 times, so HBM sees the activations once (L2 reuse across
+// neighbouring rows) instead of the 9x larger fp32 im2col matrix.
+// kVec: C % 4 == 0 -> each lane handles 4 consecutive channels of one (i, j) tap (16-byte loads).
+template <int kMode, bool kVec>
+__global__ void __launch_bounds__(256) k1_quantize_im2col(const float* __restrict__ X, const ConvGeom g, int K, int Kp,
+                                                          int qmax, int8_t* __restrict__ codes, float* __restrict__ lam_out,
+                                                          float* __restrict__ inv_out, int* __restrict__ err_flag,
+                                                          uint8_t* __restrict__ U, int64_t ldu, int64_t uplane, int64_t rows) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  auto tap = [&](int64_t b, int hb, int wb, int k, float* v) {
+    // the 4 (kVec) or 1 elements of column k of this row
+    const int seg = k / g.C, c = k - seg * g.C;
+    const int i = seg / g.kw, j = seg - i * g.kw;
+    const int hi = hb + i * g.dh, wi = wb + j * g.dw;
+    const bool in = k < K && hi >= 0 && hi < g.H && wi >= 0 && wi < g.W;
+    const float* p = X + (((b * g.H + hi) * g.W + wi) * g.C + c);
+    if (kVec) {
+      const float4 t = in ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    } else {
+      v[0] = in ? __ldg(p) : 0.f;
+    }
+  };
+  constexpr int E = kVec ? 4 : 1;
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows; row += nw) {
+    const int wo = (int)(row % g.Wo);
+    const int64_t t = row / g.Wo;
+    const int ho = (int)(t % g.Ho);
+    const int64_t b = t / g.Ho;
+    const int hb = ho * g.sh - g.ph, wb = wo * g.sw - g.pw;
+    float amax = 0.f, chk = 0.f;  // chk = sum x * 0: NaN iff some x is NaN or Inf
+    for (int k = lane * E; k < K; k += 32 * E) {
+      float v[4];
+      tap(b, hb, wb, k, v);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        chk = __fmaf_rn(v[e], 0.f, chk);
+        amax = fmaxf(amax, fabsf(v[e]));
+      }
+    }
+    if (chk != chk) atomicOr(err_flag, 1);
+    amax = warp_max(amax);
+    // lambda = RN32(qmax / amax) (IEEE division), 1 for an all-zero row
+    const float lam = (amax == 0.f) ? 1.f : __fdiv_rn(static_cast<float>(qmax), amax);
+    if (lane == 0) {
+      lam_out[row] = lam;
+      inv_out[row] = __frcp_rn(lam);
+    }
+    const bool fast = lam < 0x1p100f;
+    const float l32 = lam * 32768.f;
+    int8_t* crow = codes + row * (int64_t)Kp;
+    uint8_t* urow = U ? U + row * ldu : nullptr;
+    for (int k = lane * E; k < Kp; k += 32 * E) {
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (k < K) tap(b, hb, wb, k, v);  // padded columns: x = 0 -> code 0, u = 0
+      int c[4], q[4];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        c[e] = code_fast<kMode>(lam, v[e], qmax);
+        q[e] = fast ? q15_fast<kMode>(l32, v[e], c[e]) : u_q15_slow(lam, v[e], c[e]);
+      }
+      if (kVec) {
+        *reinterpret_cast<uint32_t*>(crow + k) = bytes4(c[0], c[1], c[2], c[3]);
+        if (urow) {
+          __stcg(reinterpret_cast<uint32_t*>(urow + k), hbytes4(q[0], q[1], q[2], q[3]));
+          __stcg(reinterpret_cast<uint32_t*>(urow + uplane + k), bytes4(q[0], q[1], q[2], q[3]));
+        }
+      } else {
+        crow[k] = (int8_t)c[0];
+        if (urow) {
+          urow[k] = (uint8_t)(q[0] >> 8);
+          urow[uplane + k] = (uint8_t)(q[0] & 255);
+        }
+      }
+    }
+  }
+}
+
+template <bool kVec>
+static void im2col_t(const QuantArgs& a, const ConvGeom& g, cudaStream_t st) {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int64_t blocks = (a.rows + 7) / 8;
+  if (blocks > 16LL * nsm) blocks = 16LL * nsm;
+  const int gb = (int)(blocks < 1 ? 1 : blocks);
+#define IM_ARGS a.X, g, a.K, a.Kp, a.qmax, a.codes, a.lam, a.inv_lam, a.err_flag, a.U, a.ldu, a.uplane, a.rows
+  if (a.mode == kRoundFloor) k1_quantize_im2col<kRoundFloor, kVec><<<gb, 256, 0, st>>>(IM_ARGS);
+  else if (a.mode == kRoundTrunc) k1_quantize_im2col<kRoundTrunc, kVec><<<gb, 256, 0, st>>>(IM_ARGS);
+  else k1_quantize_im2col<kRoundNearest, kVec><<<gb, 256, 0, st>>>(IM_ARGS);
+#undef IM_ARGS
+  ++launch_counter();
+}
+
+void launch_quantize_im2col(const QuantArgs& a, const ConvGeom& g, cudaStream_t st) {
+  if (a.rows == 0) return;
+  const bool vec = g.C % 4 == 0 && (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
+  if (vec) im2col_t<true>(a, g, st);
+  else im2col_t<false>(a, g, st);
+}
+
 void launch_tensor_scale(const float* X, int64_t ldx, int64_t rows, int K, int qmax, float* row_amax, float* lam_rows,
                          float* inv_rows, float* lam_scalar, int* err_flag, cudaStream_t st) {
   if (rows > 0) {

@@ -32,6 +32,7 @@ EXPORTS = (
     "lrqmm_destroy", "lrqmm_sync", "lrqmm_run_host", "lrqmm_get_codes", "lrqmm_get_scales",
     "lrqmm_gemm_int32", "lrqmm_get_factors", "lrqmm_get_correction", "lrqmm_correction_width",
     "lrqmm_get_timings", "lrqmm_launch_count", "lrqmm_status_string", "lrqmm_rsvd_residual_b",
+    "lrqmm_quantize_im2col",
 )
 DEBUG_EXPORTS = ("lrqmm_debug_proj", "lrqmm_debug_small", "lrqmm_debug_set_gemm_variant")
 
@@ -40,6 +41,15 @@ class LrqmmError(RuntimeError):
     def __init__(self, code: int, where: str):
         self.code = code
         super().__init__(f"{where}: {STATUS.get(code, code)}")
+
+
+class ConvGeom(ctypes.Structure):
+    """lrqmm_conv_t (NHWC convolution geometry for quantize_im2col)."""
+    _fields_ = [
+        ("batch", ctypes.c_int64), ("H", ctypes.c_int), ("W", ctypes.c_int), ("C", ctypes.c_int),
+        ("kh", ctypes.c_int), ("kw", ctypes.c_int), ("stride_h", ctypes.c_int), ("stride_w", ctypes.c_int),
+        ("pad_h", ctypes.c_int), ("pad_w", ctypes.c_int), ("dil_h", ctypes.c_int), ("dil_w", ctypes.c_int),
+    ]
 
 
 class Config(ctypes.Structure):
@@ -69,6 +79,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lrqmm_get_unique_id": (I, [P]),
         "lrqmm_create": (I, [ctypes.POINTER(Config), ctypes.POINTER(P)]),
         "lrqmm_quantize": (I, [P, I, P, I64]),
+        "lrqmm_quantize_im2col": (I, [P, I, P, ctypes.POINTER(ConvGeom)]),
         "lrqmm_rsvd_residual": (I, [P, P, P, I64]),
         "lrqmm_rsvd_residual_b": (I, [P, P, I64]),
         "lrqmm_gemm": (I, [P, F, F, P, I64]),
@@ -154,6 +165,16 @@ class Lrqmm:
     def quantize(self, side: int, X):
         """X: float32 cuda tensor (rows x k), any row stride."""
         _check(self.lib.lrqmm_quantize(self.h, side, _ptr(X), _ld(X)), "lrqmm_quantize")
+
+    def quantize_im2col(self, side: int, X, kh: int, kw: int, stride=1, pad=0, dilation=1):
+        """X: float32 cuda tensor [batch, H, W, C] (NHWC, dense); the side's matrix is its im2col
+        (rows (b, ho, wo), columns (i, j, c)) without materialising it."""
+        st = stride if isinstance(stride, tuple) else (stride, stride)
+        pd = pad if isinstance(pad, tuple) else (pad, pad)
+        dl = dilation if isinstance(dilation, tuple) else (dilation, dilation)
+        assert X.dim() == 4 and X.is_contiguous()
+        g = ConvGeom(X.shape[0], X.shape[1], X.shape[2], X.shape[3], kh, kw, st[0], st[1], pd[0], pd[1], dl[0], dl[1])
+        _check(self.lib.lrqmm_quantize_im2col(self.h, side, _ptr(X), ctypes.byref(g)), "lrqmm_quantize_im2col")
 
     def rsvd_residual(self, omega_a, omega_b=None):
         """omega_b None: static-B mode (B's factors from rsvd_residual_b / the last full call)."""

@@ -372,3 +372,73 @@ def test_empty_problem_is_a_no_op():
         D = torch.empty((0, 64), device=DEV)
         h.gemm(D)
         h.sync()
+
+
+# --------------------------------------------- implicit-im2col quantization
+@pytest.mark.parametrize("geom", [
+    # (batch, H, W, C, kh, kw, stride, pad, dil, Cout)
+    (2, 14, 14, 64, 3, 3, 1, 1, 1, 64),     # ResNet 3x3 (C % 4 == 0: 16-byte taps)
+    (2, 15, 15, 32, 3, 3, 2, 1, 1, 48),     # strided 3x3, odd size
+    (1, 23, 23, 3, 7, 7, 2, 3, 1, 16),      # the 7x7 stem (C = 3: scalar taps)
+    (2, 9, 9, 16, 1, 1, 2, 0, 1, 40),       # 1x1 strided downsample
+    (1, 12, 10, 8, 3, 3, 1, 2, 2, 24),      # dilated
+])
+@pytest.mark.parametrize("bits,rounding", [(4, "floor"), (8, "nearest"), (4, "trunc")])
+def test_quantize_im2col_matches_explicit(geom, bits, rounding):
+    B, H, W, C, kh, kw, s, p, d, Co = geom
+    rng = np.random.default_rng(91)
+    X = np.maximum(rng.standard_normal((B, H, W, C)), 0).astype(np.float32)  # post-ReLU activations
+    A = O.im2col_nhwc(X, kh, kw, (s, s), (p, p), (d, d))
+    M, K = A.shape
+    Wt = (rng.standard_normal((Co, K)) * np.sqrt(2.0 / K)).astype(np.float32)
+    r, pp = (4, 3) if rounding == "floor" else (0, 0)
+    OmA, OmB = S.gen_omega(K, r + pp, 92), S.gen_omega(K, r + pp, 93)
+    with Lrqmm(M, Co, K, bits, r, pp, 1, rounding, "row") as h:
+        h.quantize_im2col(SIDE_A, cu(X), kh, kw, s, p, d)
+        h.quantize(SIDE_B, cu(Wt))
+        ca, la = h.codes(SIDE_A).cpu().numpy(), h.scales(SIDE_A).cpu().numpy()
+        if r > 0:
+            h.rsvd_residual(cu(OmA), cu(OmB))
+        D = torch.empty((M, Co), device=DEV)
+        h.gemm(D)
+        h.sync()
+        d_gpu = D.cpu().numpy().astype(np.float64)
+    ref, parts = O.lrqmm(A, Wt, bits, r, OmA if r else None, OmB if r else None, q=1, rounding=rounding,
+                         return_parts=True)
+    assert np.array_equal(ca.astype(np.int64), parts["codes_a"])
+    assert np.array_equal(la.view(np.uint32), parts["lam_a"].view(np.uint32))
+    check_d(A, Wt, {"D": d_gpu}, ref)
+
+
+def test_quantize_im2col_residual_planes_match_explicit():
+    """The Q15 residual planes (what the RSVD passes read) are byte-identical to K1 on the explicit
+    matrix: the RSVD factors of both handles agree to the last bit."""
+    rng = np.random.default_rng(94)
+    X = np.maximum(rng.standard_normal((2, 10, 10, 32)), 0).astype(np.float32)
+    A = O.im2col_nhwc(X, 3, 3, (1, 1), (1, 1), (1, 1))
+    M, K = A.shape
+    Wt = rng.standard_normal((24, K)).astype(np.float32)
+    OmA, OmB = cu(S.gen_omega(K, 13, 95)), cu(S.gen_omega(K, 13, 96))
+    outs = []
+    for implicit in (False, True):
+        with Lrqmm(M, 24, K, 4, 8, 5) as h:
+            if implicit:
+                h.quantize_im2col(SIDE_A, cu(X), 3, 3, 1, 1, 1)
+            else:
+                h.quantize(SIDE_A, cu(A))
+            h.quantize(SIDE_B, cu(Wt))
+            h.rsvd_residual(OmA, OmB)
+            D = torch.empty((M, 24), device=DEV)
+            h.gemm(D)
+            h.sync()
+            outs.append(D.cpu().numpy())
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+
+
+def test_quantize_im2col_shape_errors():
+    X = torch.zeros((1, 8, 8, 4), device=DEV)
+    with Lrqmm(64, 8, 36, 4, 0, 0) as h:
+        with pytest.raises(LrqmmError) as ei:
+            h.quantize_im2col(SIDE_A, X, 3, 3, 1, 0, 1)   # 6 x 6 outputs = 36 rows != 64
+        assert ei.value.code == 2
+        h.quantize_im2col(SIDE_A, X, 3, 3, 1, 1, 1)       # 8 x 8 = 64 rows, K = 36

@@ -417,3 +417,31 @@ def test_rsvd_q0_is_algorithm1_on_the_sampled_basis():
     Om[:, 0] = 1.0
     US, V = O.rsvd(Rc, Om, 1, 0)
     np.testing.assert_allclose(US @ V.T, Rc, atol=1e-12)
+
+
+def test_im2col_is_the_convolution_as_a_gemm():
+    """im2col_nhwc pinned to the textbook definition of a 2-D convolution (direct loops) and to
+    torch's conv2d (an independent library routine), with stride, padding and dilation."""
+    import torch
+    rng = np.random.default_rng(7)
+    for (B, H, W, C, kh, kw, s, p, d, Co) in [(2, 7, 6, 3, 3, 3, 1, 1, 1, 4), (1, 9, 9, 5, 3, 2, 2, 1, 1, 3),
+                                              (2, 8, 7, 2, 3, 3, 2, 2, 2, 2), (1, 5, 5, 4, 1, 1, 2, 0, 1, 3)]:
+        X = rng.standard_normal((B, H, W, C))
+        Wt = rng.standard_normal((Co, kh, kw, C))
+        M = O.im2col_nhwc(X, kh, kw, (s, s), (p, p), (d, d))
+        Y = M @ Wt.reshape(Co, -1).T
+        Ho = (H + 2 * p - d * (kh - 1) - 1) // s + 1
+        Wo = (W + 2 * p - d * (kw - 1) - 1) // s + 1
+        ref = np.zeros((B, Ho, Wo, Co))
+        for b in range(B):
+            for ho in range(Ho):
+                for wo in range(Wo):
+                    for i in range(kh):
+                        for j in range(kw):
+                            hi, wi = ho * s - p + i * d, wo * s - p + j * d
+                            if 0 <= hi < H and 0 <= wi < W:
+                                ref[b, ho, wo] += Wt[:, i, j, :] @ X[b, hi, wi, :]
+        np.testing.assert_allclose(Y.reshape(B, Ho, Wo, Co), ref, atol=1e-12)
+        t = torch.nn.functional.conv2d(torch.from_numpy(X).permute(0, 3, 1, 2), torch.from_numpy(Wt).permute(0, 3, 1, 2),
+                                       stride=s, padding=p, dilation=d)
+        np.testing.assert_allclose(Y.reshape(B, Ho, Wo, Co), t.permute(0, 2, 3, 1).numpy(), atol=1e-12)
