@@ -261,6 +261,22 @@ def hbm_bytes_step(M: int, N: int, K: int, k: int) -> float:
 
 
 # ------------------------------------------------------ configs[3]: ResNet-50 suite
+def im2col_rows(X, g, rows):
+    """Explicit im2col rows (b, ho, wo) -> (i, j, c) of an NHWC tensor, for the error sample only."""
+    import torch
+
+    s, p, kh, kw = g["stride"], g["pad"], g["kh"], g["kw"]
+    Xp = torch.nn.functional.pad(X, (0, 0, p, p, p, p))
+    Ho = (g["H"] + 2 * p - kh) // s + 1
+    Wo = (g["W"] + 2 * p - kw) // s + 1
+    out = []
+    for r in rows.tolist():
+        b, rem = divmod(r, Ho * Wo)
+        ho, wo = divmod(rem, Wo)
+        out.append(Xp[b, ho * s: ho * s + kh, wo * s: wo * s + kw, :].reshape(-1))
+    return torch.stack(out)
+
+
 def run_resnet(args, ws, rank, local):
     """All 53 ResNet-50 convolutions as im2col GEMMs at batch 256 (A: post-ReLU activations,
     B: Kaiming-normal random-init weights), int4, r = 16, p = 5: per-layer device time of the full
@@ -275,18 +291,31 @@ def run_resnet(args, ws, rank, local):
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
     layers = S.resnet50_convs(256)
+    geoms = dict(S.resnet50_conv_geoms(256))
     out, t_all, t_bare_all, ops_all, hbm_all = [], 0.0, 0.0, 0.0, 0.0
     steps = max(1, min(args.steps, 5))
     for li, (name, M, K, N, _) in enumerate(layers):
-        A = S.gen_matrix_torch(dist_name, M, K, 100 + 2 * li + 7919 * rank, device=dev)
+        g = geoms[name]
+        # post-ReLU NHWC activations; windowed / strided layers quantize their im2col implicitly
+        # (lrqmm_quantize_im2col), 1x1 stride-1 layers use the activations as A directly
+        X = S.gen_matrix_torch(dist_name, g["batch"] * g["H"] * g["W"], g["C"], 100 + 2 * li + 7919 * rank, device=dev)
+        X = X.view(g["batch"], g["H"], g["W"], g["C"])
+        implicit = g["kh"] * g["kw"] > 1 or g["stride"] > 1
+        A = None if implicit else X.view(M, K)
         Bt = S.gen_matrix_torch("normal", N, K, 101 + 2 * li, device=dev, scale=(2.0 / K) ** 0.5)
         OmA = torch.from_numpy(S.gen_omega(K, r + p, 1000 + 2 * li)).to(dev)
         OmB = torch.from_numpy(S.gen_omega(K, r + p, 1001 + 2 * li)).to(dev)
         D = torch.empty((M, N), device=dev)
         C = torch.empty((M, N), dtype=torch.int32, device=dev)
         with Lrqmm(M, N, K, bits, r, p, 1, "floor", "row", device=local, stream=stream) as h:
+            def quant_a():
+                if implicit:
+                    h.quantize_im2col(SIDE_A, X, g["kh"], g["kw"], g["stride"], g["pad"])
+                else:
+                    h.quantize(SIDE_A, A)
+
             def step():
-                h.quantize(SIDE_A, A); h.quantize(SIDE_B, Bt); h.rsvd_residual(OmA, OmB); h.gemm(D)
+                quant_a(); h.quantize(SIDE_B, Bt); h.rsvd_residual(OmA, OmB); h.gemm(D)
             for _ in range(max(args.warmup, 1)):
                 step()
             torch.cuda.synchronize(dev)
@@ -308,20 +337,24 @@ def run_resnet(args, ws, rank, local):
             step()
             h.sync()
             rows = torch.arange(0, M, max(1, M // 64), device=dev)[:64]
-            Cx = A[rows].double() @ Bt.double().T
+            Cx = im2col_rows(X, g, rows).double() @ Bt.double().T
             err = float(torch.linalg.norm(D[rows].double() - Cx) / torch.linalg.norm(Cx))
         ops = 2.0 * M * N * K
-        hbm = hbm_bytes_step(M, N, K, r + p)
+        # implicit im2col: K1 reads the activations once (L2 reuse across windows), not M x K floats
+        hbm = hbm_bytes_step(M, N, K, r + p) - (4.0 * M * K - 4.0 * X.numel() if implicit else 0.0)
         out.append({"layer": name, "M": M, "K": K, "N": N, "ms": t * 1e3, "bare_int8_ms": tb * 1e3,
                     "overhead_vs_bare": t / tb, "tops": ops / t / 1e12, "rel_fro_error": err,
                     "hbm_gbs": hbm / t / 1e9, "hbm_frac": hbm / t / 1e9 / hbm_peak()})
         t_all += t; t_bare_all += tb; ops_all += ops; hbm_all += hbm
-        del A, Bt, D, C
+        out[-1]["a_input"] = "implicit im2col" if implicit else "activations"
+        del A, X, Bt, D, C
         torch.cuda.empty_cache()
     if rank == 0:
         line = {"metric": METRIC, "value": ops_all / t_all / 1e12, "unit": "TOPS", "n_gpus": ws, "steps": steps,
                 "warmup": args.warmup, "ms_per_step": t_all * 1e3, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "int8", "data": "synthetic (post-ReLU normal activations, Kaiming weights)",
+                "vs_baseline": None, "dtype": "int8",
+                "data": "synthetic (post-ReLU normal NHWC activations, Kaiming weights); windowed / strided layers "
+                        "quantized by implicit im2col (lrqmm_quantize_im2col)",
                 "config": {"workload": label, "layers": len(layers), "bits": bits, "rank": r, "oversample": p,
                            "batch": 256},
                 "overhead_vs_bare_int8": t_all / t_bare_all, "bare_int8_tops": ops_all / t_bare_all / 1e12,

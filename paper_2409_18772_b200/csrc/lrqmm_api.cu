@@ -419,6 +419,7 @@ lrqmm_status_t lrqmm_quantize_im2col(lrqmm_handle_t h, lrqmm_side_t side, const 
   if (cv->H + 2LL * cv->pad_h < eh || cv->W + 2LL * cv->pad_w < ew) return LRQMM_ERR_INVALID_ARGUMENT;
   Side& s = h->s[side];
   if (cv->batch * Ho * Wo != s.rows || (int64_t)cv->kh * cv->kw * cv->C != h->cfg.k) return LRQMM_ERR_SHAPE;
+  if (s.rows > INT32_MAX || (int64_t)cv->H * cv->W * cv->C > INT32_MAX) return LRQMM_ERR_SHAPE;  // 32-bit indexing
   if (!X && s.rows > 0) return LRQMM_ERR_INVALID_ARGUMENT;
   cudaSetDevice(h->cfg.device);
   record(h, side == LRQMM_SIDE_A ? 0 : 2);

@@ -681,44 +681,75 @@ void launch_quantize_rows(const QuantArgs& a, bool fixed, cudaStream_t st) {
 // L1 / L2) codes and the Q15 residual planes, with the exact arithmetic of k1_quantize_tma.  A
 // 3x3 window reads each activation ~9 times, so HBM sees the activations once (L2 reuse across
 // neighbouring rows) instead of the 9x larger fp32 im2col matrix.
-// kVec: C % 4 == 0 -> each lane handles 4 consecutive channels of one (i, j) tap (16-byte loads).
-template <int kMode, bool kVec>
+// kVec: C % 4 == 0 -> each lane handles groups of 4 consecutive channels of one (i, j) tap
+// (16-byte loads).  Each pass issues VPT independent group loads per lane before using them
+// (memory-level parallelism); rows of K <= 32 E VPT stay in registers between amax and rounding.
+template <int kMode, bool kVec, int VPT>
 __global__ void __launch_bounds__(256) k1_quantize_im2col(const float* __restrict__ X, const ConvGeom g, int K, int Kp,
                                                           int qmax, int8_t* __restrict__ codes, float* __restrict__ lam_out,
                                                           float* __restrict__ inv_out, int* __restrict__ err_flag,
-                                                          uint8_t* __restrict__ U, int64_t ldu, int64_t uplane, int64_t rows) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  auto tap = [&](int64_t b, int hb, int wb, int k, float* v) {
-    // the 4 (kVec) or 1 elements of column k of this row
-    const int seg = k / g.C, c = k - seg * g.C;
-    const int i = seg / g.kw, j = seg - i * g.kw;
-    const int hi = hb + i * g.dh, wi = wb + j * g.dw;
-    const bool in = k < K && hi >= 0 && hi < g.H && wi >= 0 && wi < g.W;
-    const float* p = X + (((b * g.H + hi) * g.W + wi) * g.C + c);
-    if (kVec) {
-      const float4 t = in ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-    } else {
-      v[0] = in ? __ldg(p) : 0.f;
-    }
-  };
+                                                          uint8_t* __restrict__ U, int64_t ldu, int64_t uplane, int rows) {
   constexpr int E = kVec ? 4 : 1;
-  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows; row += nw) {
-    const int wo = (int)(row % g.Wo);
-    const int64_t t = row / g.Wo;
-    const int ho = (int)(t % g.Ho);
-    const int64_t b = t / g.Ho;
+  constexpr int SPAN = 32 * E * VPT;  // row elements per batch
+  const int lane = threadIdx.x & 31;
+  const int G = g.C / E;  // element groups per tap
+  // this lane's first group q = lane: tap / channel group / (i, j); a step of 32 groups moves
+  // d_tap taps and d_cg groups (with a carry when the channel group wraps)
+  const int l_tap = lane / G, l_cg = lane - l_tap * G, l_i = l_tap / g.kw, l_j = l_tap - l_i * g.kw;
+  const int d_tap = 32 / G, d_cg = 32 - d_tap * G;
+  const int img = g.H * g.W * g.C;  // < 2^31 (checked by the launcher)
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows; row += nw) {
+    const int t = row / g.Wo;
+    const int wo = row - t * g.Wo;
+    const int b = t / g.Ho;
+    const int ho = t - b * g.Ho;
     const int hb = ho * g.sh - g.ph, wb = wo * g.sw - g.pw;
-    float amax = 0.f, chk = 0.f;  // chk = sum x * 0: NaN iff some x is NaN or Inf
-    for (int k = lane * E; k < K; k += 32 * E) {
-      float v[4];
-      tap(b, hb, wb, k, v);
+    const float* xb = X + (int64_t)b * img;
+    int st_cg, st_i, st_j;
+    auto reset = [&]() { st_cg = l_cg; st_i = l_i; st_j = l_j; };
+    auto step = [&]() {
+      int dt = d_tap;
+      st_cg += d_cg;
+      if (st_cg >= G) { st_cg -= G; ++dt; }
+      st_j += dt;
+      while (st_j >= g.kw) { st_j -= g.kw; ++st_i; }
+    };
+    // VPT groups of this lane for the batch starting at column k0 (0 outside the image / past K)
+    auto load = [&](int k0, float (&v)[VPT][4]) {
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        chk = __fmaf_rn(v[e], 0.f, chk);
-        amax = fmaxf(amax, fabsf(v[e]));
+      for (int u = 0; u < VPT; ++u) {
+        if (k0 + u * 32 * E >= K) {  // warp-uniform: the rest of the batch is past the row
+#pragma unroll
+          for (int e = 0; e < 4; ++e) v[u][e] = 0.f;
+          continue;
+        }
+        const int k = k0 + (u * 32 + lane) * E;
+        const int hi = hb + st_i * g.dh, wi = wb + st_j * g.dw;
+        const bool in = k < K && (unsigned)hi < (unsigned)g.H && (unsigned)wi < (unsigned)g.W;
+        const float* p = xb + ((hi * g.W + wi) * g.C + st_cg * E);
+        if (kVec) {
+          const float4 q = in ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[u][0] = q.x; v[u][1] = q.y; v[u][2] = q.z; v[u][3] = q.w;
+        } else {
+          v[u][0] = in ? __ldg(p) : 0.f;
+        }
+        step();
       }
+    };
+    reset();
+    float v[VPT][4];
+    float amax = 0.f, chk = 0.f;  // chk = sum x * 0: NaN iff some x is NaN or Inf
+    const bool one = K <= SPAN;   // the whole row in registers
+    for (int k0 = 0; k0 < K; k0 += SPAN) {
+      load(k0, v);
+#pragma unroll
+      for (int u = 0; u < VPT; ++u)
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          chk = __fmaf_rn(v[u][e], 0.f, chk);
+          amax = fmaxf(amax, fabsf(v[u][e]));
+        }
     }
     if (chk != chk) atomicOr(err_flag, 1);
     amax = warp_max(amax);
@@ -730,28 +761,34 @@ __global__ void __launch_bounds__(256) k1_quantize_im2col(const float* __restric
     }
     const bool fast = lam < 0x1p100f;
     const float l32 = lam * 32768.f;
-    int8_t* crow = codes + row * (int64_t)Kp;
-    uint8_t* urow = U ? U + row * ldu : nullptr;
-    for (int k = lane * E; k < Kp; k += 32 * E) {
-      float v[4] = {0.f, 0.f, 0.f, 0.f};
-      if (k < K) tap(b, hb, wb, k, v);  // padded columns: x = 0 -> code 0, u = 0
-      int c[4], q[4];
+    int8_t* crow = codes + (int64_t)row * Kp;
+    uint8_t* urow = U ? U + (int64_t)row * ldu : nullptr;
+    if (!one) reset();
+    for (int k0 = 0; k0 < Kp; k0 += SPAN) {
+      if (!one) load(k0, v);  // second pass (L1 / L2); padded columns load as 0 -> code 0, u = 0
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        c[e] = code_fast<kMode>(lam, v[e], qmax);
-        q[e] = fast ? q15_fast<kMode>(l32, v[e], c[e]) : u_q15_slow(lam, v[e], c[e]);
-      }
-      if (kVec) {
-        *reinterpret_cast<uint32_t*>(crow + k) = bytes4(c[0], c[1], c[2], c[3]);
-        if (urow) {
-          __stcg(reinterpret_cast<uint32_t*>(urow + k), hbytes4(q[0], q[1], q[2], q[3]));
-          __stcg(reinterpret_cast<uint32_t*>(urow + uplane + k), bytes4(q[0], q[1], q[2], q[3]));
+      for (int u = 0; u < VPT; ++u) {
+        if (k0 + u * 32 * E >= Kp) break;
+        const int k = k0 + (u * 32 + lane) * E;
+        if (k >= Kp) continue;
+        int c[4], q[4];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          c[e] = code_fast<kMode>(lam, v[u][e], qmax);
+          q[e] = fast ? q15_fast<kMode>(l32, v[u][e], c[e]) : u_q15_slow(lam, v[u][e], c[e]);
         }
-      } else {
-        crow[k] = (int8_t)c[0];
-        if (urow) {
-          urow[k] = (uint8_t)(q[0] >> 8);
-          urow[uplane + k] = (uint8_t)(q[0] & 255);
+        if (kVec) {
+          *reinterpret_cast<uint32_t*>(crow + k) = bytes4(c[0], c[1], c[2], c[3]);
+          if (urow) {
+            __stcg(reinterpret_cast<uint32_t*>(urow + k), hbytes4(q[0], q[1], q[2], q[3]));
+            __stcg(reinterpret_cast<uint32_t*>(urow + uplane + k), bytes4(q[0], q[1], q[2], q[3]));
+          }
+        } else {
+          crow[k] = (int8_t)c[0];
+          if (urow) {
+            urow[k] = (uint8_t)(q[0] >> 8);
+            urow[uplane + k] = (uint8_t)(q[0] & 255);
+          }
         }
       }
     }
@@ -766,10 +803,11 @@ static void im2col_t(const QuantArgs& a, const ConvGeom& g, cudaStream_t st) {
   int64_t blocks = (a.rows + 7) / 8;
   if (blocks > 16LL * nsm) blocks = 16LL * nsm;
   const int gb = (int)(blocks < 1 ? 1 : blocks);
-#define IM_ARGS a.X, g, a.K, a.Kp, a.qmax, a.codes, a.lam, a.inv_lam, a.err_flag, a.U, a.ldu, a.uplane, a.rows
-  if (a.mode == kRoundFloor) k1_quantize_im2col<kRoundFloor, kVec><<<gb, 256, 0, st>>>(IM_ARGS);
-  else if (a.mode == kRoundTrunc) k1_quantize_im2col<kRoundTrunc, kVec><<<gb, 256, 0, st>>>(IM_ARGS);
-  else k1_quantize_im2col<kRoundNearest, kVec><<<gb, 256, 0, st>>>(IM_ARGS);
+#define IM_ARGS a.X, g, a.K, a.Kp, a.qmax, a.codes, a.lam, a.inv_lam, a.err_flag, a.U, a.ldu, a.uplane, (int)a.rows
+  constexpr int VPT = kVec ? 8 : 8;
+  if (a.mode == kRoundFloor) k1_quantize_im2col<kRoundFloor, kVec, VPT><<<gb, 256, 0, st>>>(IM_ARGS);
+  else if (a.mode == kRoundTrunc) k1_quantize_im2col<kRoundTrunc, kVec, VPT><<<gb, 256, 0, st>>>(IM_ARGS);
+  else k1_quantize_im2col<kRoundNearest, kVec, VPT><<<gb, 256, 0, st>>>(IM_ARGS);
 #undef IM_ARGS
   ++launch_counter();
 }

@@ -101,6 +101,27 @@ def gen_matrix_torch(dist: str, rows: int, cols: int, seed: int, device="cuda", 
 # Shapes only: torchvision resnet50 topology at 224x224 input.
 # Returns (name, M = batch*Ho*Wo, K = Cin*kh*kw, N = Cout, kh*kw) per conv.
 # ---------------------------------------------------------------------------
+def resnet50_conv_geoms(batch: int = 256):
+    """The 53 convolutions of resnet50_convs with their NHWC geometry (torchvision v1.5: stride on the
+    3x3): (name, dict(batch, H, W, C, kh, kw, stride, pad, Cout)); im2col rows = batch Ho Wo,
+    K = kh kw C, N = Cout (same order and sizes as resnet50_convs)."""
+    g = [("conv1", dict(batch=batch, H=224, W=224, C=3, kh=7, kw=7, stride=2, pad=3, Cout=64))]
+    spec = [(64, 3, 256, 56), (128, 4, 512, 28), (256, 6, 1024, 14), (512, 3, 2048, 7)]
+    cin, hw_in = 64, 56
+    for li, (width, blocks, cout, hw) in enumerate(spec, start=1):
+        for b in range(blocks):
+            hin = hw_in if b == 0 else hw
+            s2 = hin // hw  # 2 on the first block of layers 2-4, else 1
+            g.append((f"layer{li}.{b}.conv1", dict(batch=batch, H=hin, W=hin, C=cin, kh=1, kw=1, stride=1, pad=0, Cout=width)))
+            g.append((f"layer{li}.{b}.conv2", dict(batch=batch, H=hin, W=hin, C=width, kh=3, kw=3, stride=s2, pad=1, Cout=width)))
+            g.append((f"layer{li}.{b}.conv3", dict(batch=batch, H=hw, W=hw, C=width, kh=1, kw=1, stride=1, pad=0, Cout=cout)))
+            if b == 0:
+                g.append((f"layer{li}.{b}.downsample", dict(batch=batch, H=hin, W=hin, C=cin, kh=1, kw=1, stride=s2, pad=0, Cout=cout)))
+            cin = cout
+        hw_in = hw
+    return g
+
+
 def resnet50_convs(batch: int = 256):
     layers = []
     layers.append(("conv1", batch * 112 * 112, 3 * 7 * 7, 64, 49))
