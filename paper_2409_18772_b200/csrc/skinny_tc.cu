@@ -620,9 +620,15 @@ static void run_tc(int nsides, const TcPassSide* sides, int W, bool reduce1, int
         a.cinv2 = a.cinv1;
       }
     }
-    // enough units for ~6 per SM (the persistent grid balances them), each >= 4 k-blocks, and a
+    // enough units for ~3 per SM (the persistent grid balances them), each >= 4 k-blocks, and a
     // chunk short enough for exact int32 accumulation
-    int64_t ns = (6LL * nsm + nblk - 1) / nblk;
+    static int waves = 0;  // work units per SM (LRQMM_TC_WAVES overrides, for sweeps)
+    if (!waves) {
+      const char* e = getenv("LRQMM_TC_WAVES");
+      waves = e ? atoi(e) : 3;  // c3 sweep (tools/waves_sweep.sh): 3 -> RSVD 867 us vs 911 at 6
+      if (waves < 1) waves = 1;
+    }
+    int64_t ns = ((int64_t)waves * nsm + nblk - 1) / nblk;
     const int64_t maxs = (rlen + 4 * BK - 1) / (4 * BK);
     if (ns > maxs) ns = maxs;
     if (ns > 256) ns = 256;  // few output blocks (short K in COL mode): bound the partials to reduce
