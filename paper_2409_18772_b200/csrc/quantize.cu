@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
 // rows: pass 1 reduces amax from shared memory, pass 2 re-reads the row and writes codes and the
 // Q15 planes (same exact arithmetic).  kVec4: K % 4 == 0 (16-byte row alignment in the slot).
 template <bool kVec4, bool kFixedLam, int kMode>
-__global__ void __launch_bounds__(k1t::kThreads, 1)
+__global__ void __launch_bounds__(k1t::kThreads, 2)
     k1_quantize_rows_tma(const float* __restrict__ X, int rows_full, int R, int K, int Kp, int qmax,
                          int8_t* __restrict__ codes, float* __restrict__ lam_out, float* __restrict__ inv_out,
                          const float* __restrict__ lam_in, int* __restrict__ err_flag, uint8_t* __restrict__ U,
@@ -516,13 +516,14 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
 static int64_t launch_k1_rows_tma(const QuantArgs& a, bool fixed, cudaStream_t st) {
   if ((reinterpret_cast<uintptr_t>(a.X) & 15) != 0 || a.ldx != a.K || a.K < 16 || a.K >= 4096) return 0;
   const int step = a.K % 4 == 0 ? 1 : (a.K % 2 == 0 ? 2 : 4);  // R K 4 % 16 == 0
-  int R = (16384 / a.K) / step * step;
+  // ~32 KB chunks, 3 slots: two CTAs per SM (34 warps) hide the per-row amax -> lambda -> round chain
+  int R = (8192 / a.K) / step * step;
   if (R < step) return 0;
   const int64_t rows_full = a.rows / R * R;
   if (rows_full == 0 || rows_full > INT32_MAX) return 0;
   const int slot = (R * a.K * 4 + 1023) / 1024 * 1024;
-  int ns = k1t::kSmemBudget / slot;
-  if (ns > 4) ns = 4;
+  int ns = (k1t::kSmemBudget / 2) / slot;
+  if (ns > 3) ns = 3;
   if (ns < 2) return 0;
   const int smem = 1024 + ns * slot;
   static int nsm = 0;
@@ -532,7 +533,7 @@ static int64_t launch_k1_rows_tma(const QuantArgs& a, bool fixed, cudaStream_t s
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   const int64_t nchunks = rows_full / R;
-  const int grid = (int)(nchunks < nsm ? nchunks : nsm);
+  const int grid = (int)(nchunks < 2 * nsm ? nchunks : 2 * nsm);
   const bool v4 = a.K % 4 == 0;
   int L = 32;  // lanes per row: the smallest power of two covering the row's float4s (vec4 path)
   if (v4)
