@@ -92,7 +92,6 @@ int launch_tc_proj_codes(const SideView& s, const float* P, float* OUT, int W, f
                          uint8_t* img, cudaStream_t st);
 
 // OUT[i, :] = IN[i, :] S (fp64 S, fp64 accumulation, fp32 out); IN and OUT ld W, S W x W
-void launch_apply64(const float* IN, const double* S, int64_t n, int W, float* OUT, cudaStream_t st);
 // multi-job forms (one launch): OUT = IN S per job
 struct Apply64Job {
   const float* IN;
@@ -211,8 +210,7 @@ int encode_map_2d_sw(void* map, int dtype, const void* base, uint64_t inner, uin
 int encode_map_2d(void* map, int dtype_f32 /* 1 f32, 2 16-bit, 0 8-bit */, const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
                   uint32_t box_inner, uint32_t box_outer);
 int encode_map_1d_f32(void* map, const void* base, uint64_t n, uint32_t box);
-// out[i] = RN(1 / in[i])
-void launch_recip(const float* in, float* out, int64_t n, cudaStream_t st);
+
 void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t st);
 void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStream_t st);
 

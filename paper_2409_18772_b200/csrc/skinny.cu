@@ -228,12 +228,6 @@ void launch_apply64_jobs(const Apply64Jobs& in, int W, cudaStream_t st) {
   ++launch_counter();
 }
 
-void launch_apply64(const float* IN, const double* S, int64_t n, int W, float* OUT, cudaStream_t st) {
-  Apply64Jobs j{};
-  j.n = 1;
-  j.j[0] = Apply64Job{IN, S, n, OUT, nullptr, nullptr};
-  launch_apply64_jobs(j, W, st);
-}
 
 __global__ void k_f64_to_f32(const double* __restrict__ in, float* __restrict__ out, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -245,15 +239,5 @@ void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t st)
   ++launch_counter();
 }
 
-__global__ void k_recip(const float* __restrict__ in, float* __restrict__ out, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = __frcp_rn(in[i]);
-}
-
-void launch_recip(const float* in, float* out, int64_t n, cudaStream_t st) {
-  if (n == 0) return;
-  k_recip<<<clamp_grid((n + 255) / 256), 256, 0, st>>>(in, out, n);
-  ++launch_counter();
-}
 
 }  // namespace lrqmm
