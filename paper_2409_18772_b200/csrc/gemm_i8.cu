@@ -711,21 +711,6 @@ static int encode_codes_map(CUtensorMap* map, const int8_t* base, int64_t rows, 
 }
 
 // generic 2D tiled map: dims {inner, outer}, row stride in bytes, box {box_inner, box_outer}
-int encode_map_2d(void* map, int dtype_f32, const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
-                  uint32_t box_inner, uint32_t box_outer) {
-  PFN_encodeTiled enc = get_encode();
-  if (!enc) return 1;
-  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)stride_bytes};
-  cuuint32_t box[2] = {box_inner, box_outer};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(reinterpret_cast<CUtensorMap*>(map), dtype_f32 == 1 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
-                   : (dtype_f32 == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8),
-                   2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? 0 : 2;
-}
-
 int encode_map_2d_sw(void* map, int dtype, const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
                      uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
   PFN_encodeTiled enc = get_encode();
@@ -743,19 +728,6 @@ int encode_map_2d_sw(void* map, int dtype, const void* base, uint64_t inner, uin
                                               : CU_TENSOR_MAP_DATA_TYPE_UINT8;
   CUresult r = enc(reinterpret_cast<CUtensorMap*>(map), dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? 0 : 2;
-}
-
-int encode_map_1d_f32(void* map, const void* base, uint64_t n, uint32_t box) {
-  PFN_encodeTiled enc = get_encode();
-  if (!enc) return 1;
-  cuuint64_t dims[1] = {(cuuint64_t)n};
-  cuuint64_t strides[1] = {0};
-  cuuint32_t bx[1] = {box};
-  cuuint32_t estr[1] = {1};
-  CUresult r = enc(reinterpret_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<void*>(base), dims,
-                   strides, bx, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : 2;
 }
 
