@@ -20,9 +20,17 @@ template <int W>
 LRQMM_DEV void stage_rows_in(const float* __restrict__ src, int64_t i0, int nr, float* sm) {
   constexpr int L = ap_ld(W);
   const float4* s4 = reinterpret_cast<const float4*>(src + i0 * W);
-  for (int e = threadIdx.x; e < nr * (W / 4); e += blockDim.x) {
-    const int r = e / (W / 4), c = e % (W / 4);
-    *reinterpret_cast<float4*>(sm + r * L + 4 * c) = __ldg(s4 + e);
+  // all of the tile's loads issue before the first store (W / 4 float4 per thread in flight)
+  float4 v[W / 4];
+#pragma unroll
+  for (int u = 0; u < W / 4; ++u) {
+    const int e = threadIdx.x + u * kApRows;
+    if (e < nr * (W / 4)) v[u] = __ldg(s4 + e);
+  }
+#pragma unroll
+  for (int u = 0; u < W / 4; ++u) {
+    const int e = threadIdx.x + u * kApRows;
+    if (e < nr * (W / 4)) *reinterpret_cast<float4*>(sm + (e / (W / 4)) * L + 4 * (e % (W / 4))) = v[u];
   }
 }
 
@@ -47,6 +55,7 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const ApplyJobs jobs) {
     s2[e] = (J.IN2 && o < nout) ? J.S2[c * J.ldS + o] : 0.f;
   }
   const int64_t n = J.n;
+  const bool vec_out = nout % 4 == 0 && J.col0 % 4 == 0 && J.ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(J.OUT) & 15) == 0;
   for (int64_t i0 = (int64_t)(blockIdx.x - b0) * kApRows; i0 < n; i0 += (int64_t)nb * kApRows) {
     const int nr = (int)(n - i0 < kApRows ? n - i0 : kApRows);
     __syncthreads();
@@ -78,15 +87,18 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const ApplyJobs jobs) {
         }
       }
     }
-    __syncthreads();  // sin1 is reused as the output staging buffer
+    // outputs straight from registers: this thread's row, 16-byte stores when aligned
     if (threadIdx.x < nr) {
+      float* orow = J.OUT + (i0 + threadIdx.x) * J.ldo + J.col0;
+      if (vec_out) {
 #pragma unroll
-      for (int o = 0; o < W; ++o) sin1[threadIdx.x * L + o] = acc[o];
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < nr * nout; e += blockDim.x) {
-      const int r = e / nout, o = e % nout;
-      J.OUT[(i0 + r) * J.ldo + J.col0 + o] = sin1[r * L + o];
+        for (int o4 = 0; o4 < W / 4; ++o4)
+          if (4 * o4 < nout) *reinterpret_cast<float4*>(orow + 4 * o4) = make_float4(acc[4 * o4], acc[4 * o4 + 1], acc[4 * o4 + 2], acc[4 * o4 + 3]);
+      } else {
+#pragma unroll
+        for (int o = 0; o < W; ++o)
+          if (o < nout) orow[o] = acc[o];
+      }
     }
   }
 }
@@ -172,10 +184,11 @@ __global__ void __launch_bounds__(kApRows) k_apply64(const Apply64Jobs jobs) {
           for (int o = 0; o < W; ++o) acc[o] = fma(xs[j], s[(4 * c4 + j) * W + o], acc[o]);
       }
     }
-    __syncthreads();
-    if (threadIdx.x < nr) {
+    if (threadIdx.x < nr) {  // outputs straight from registers (16-byte stores of this thread's row)
+      float4* orow = reinterpret_cast<float4*>(J.OUT + (i0 + threadIdx.x) * W);
 #pragma unroll
-      for (int o = 0; o < W; ++o) sin[threadIdx.x * L + o] = (float)acc[o];
+      for (int o4 = 0; o4 < W / 4; ++o4)
+        orow[o4] = make_float4((float)acc[4 * o4], (float)acc[4 * o4 + 1], (float)acc[4 * o4 + 2], (float)acc[4 * o4 + 3]);
     }
     if (J.cmax) {
       // column maxima of |OUT * cscale| for the next pass's B image (same fp32 product as there)
@@ -186,12 +199,6 @@ __global__ void __launch_bounds__(kApRows) k_apply64(const Apply64Jobs jobs) {
         const unsigned m = __reduce_max_sync(0xffffffffu, b);
         if ((threadIdx.x & 31) == (o & 31)) run[o >> 5] = max(run[o >> 5], m);
       }
-    }
-    __syncthreads();
-    float4* o4 = reinterpret_cast<float4*>(J.OUT + i0 * W);
-    for (int e = threadIdx.x; e < nr * (W / 4); e += blockDim.x) {
-      const int r = e / (W / 4), c = e % (W / 4);
-      o4[e] = *reinterpret_cast<const float4*>(sin + r * L + 4 * c);
     }
   }
   if (J.cmax) {
