@@ -442,3 +442,49 @@ def test_quantize_im2col_shape_errors():
             h.quantize_im2col(SIDE_A, X, 3, 3, 1, 0, 1)   # 6 x 6 outputs = 36 rows != 64
         assert ei.value.code == 2
         h.quantize_im2col(SIDE_A, X, 3, 3, 1, 1, 1)       # 8 x 8 = 64 rows, K = 36
+
+
+# --------------------------------------------------------------- feature combinations
+@pytest.mark.parametrize("rounding,gran", [("trunc", "tensor"), ("nearest", "row")])
+def test_q0_with_other_roundings_and_granularities(rounding, gran):
+    A, Bt, OmA, OmB = S.problem(300, 260, 520, 13, s=70, dist="exp4")
+    OmA[:, 0] = 1.0
+    OmB[:, 0] = 1.0
+    ref = O.lrqmm(A, Bt, 4, 8, OmA, OmB, q=0, rounding=rounding, granularity=gran)
+    check_d(A, Bt, run_gpu(A, Bt, 4, 8, 5, OmA, OmB, q=0, rounding=rounding, gran=gran), ref)
+
+
+def test_b_sharded_flag_is_inert_on_one_rank():
+    """cfg.b_sharded with world_size == 1: B is not split (bit-identical D)."""
+    A, Bt, OmA, OmB = S.problem(256, 300, 512, 13, s=71)
+    outs = []
+    for bsh in (False, True):
+        with Lrqmm(256, 300, 512, 4, 8, 5, b_sharded=bsh) as h:
+            assert h.b_rows == (0, 300)
+            h.quantize(SIDE_A, cu(A)); h.quantize(SIDE_B, cu(Bt))
+            h.rsvd_residual(cu(OmA[:, :13]), cu(OmB[:, :13]))
+            D = torch.empty((256, 300), device=DEV)
+            h.gemm(D)
+            h.sync()
+            outs.append(D.cpu().numpy())
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+
+
+def test_im2col_with_static_b_and_q0():
+    """Implicit-im2col activations against resident (static-B) weights, q = 0 sketch."""
+    rng = np.random.default_rng(72)
+    X = np.maximum(rng.standard_normal((2, 12, 12, 16)), 0).astype(np.float32)
+    A = O.im2col_nhwc(X, 3, 3, (1, 1), (1, 1), (1, 1))
+    M, K = A.shape
+    Wt = (rng.standard_normal((40, K)) * np.sqrt(2.0 / K)).astype(np.float32)
+    OmA, OmB = S.gen_omega(K, 13, 73), S.gen_omega(K, 13, 74)
+    ref = O.lrqmm(A, Wt, 4, 8, OmA, OmB, q=0)
+    with Lrqmm(M, 40, K, 4, 8, 5, 0) as h:
+        h.quantize(SIDE_B, cu(Wt))
+        h.rsvd_residual_b(cu(OmB))
+        h.quantize_im2col(SIDE_A, cu(X), 3, 3, 1, 1, 1)
+        h.rsvd_residual(cu(OmA))
+        D = torch.empty((M, 40), device=DEV)
+        h.gemm(D)
+        h.sync()
+        check_d(A, Wt, {"D": D.cpu().numpy().astype(np.float64)}, ref)
