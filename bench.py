@@ -292,7 +292,7 @@ def run_resnet(args, ws, rank, local):
     stream = torch.cuda.current_stream(dev)
     layers = S.resnet50_convs(256)
     geoms = dict(S.resnet50_conv_geoms(256))
-    out, t_all, t_bare_all, ops_all, hbm_all = [], 0.0, 0.0, 0.0, 0.0
+    out, t_all, t_bare_all, ops_all, hbm_all, t_static_all = [], 0.0, 0.0, 0.0, 0.0, 0.0
     steps = max(1, min(args.steps, 5))
     for li, (name, M, K, N, _) in enumerate(layers):
         g = geoms[name]
@@ -334,6 +334,22 @@ def run_resnet(args, ws, rank, local):
             e1.record(stream)
             torch.cuda.synchronize(dev)
             tb = e0.elapsed_time(e1) / 1e3 / steps
+            # weight-resident deployment (static-B): B quantized + RSVD'd once, per call
+            # only the activation side, the A-dependent B term and the GEMM
+            h.quantize(SIDE_B, Bt)
+            h.rsvd_residual_b(OmB)
+
+            def step_static():
+                quant_a(); h.rsvd_residual(OmA); h.gemm(D)
+            for _ in range(2):
+                step_static()
+            torch.cuda.synchronize(dev)
+            e0.record(stream)
+            for _ in range(steps):
+                step_static()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ts = e0.elapsed_time(e1) / 1e3 / steps
             step()
             h.sync()
             rows = torch.arange(0, M, max(1, M // 64), device=dev)[:64]
@@ -342,10 +358,10 @@ def run_resnet(args, ws, rank, local):
         ops = 2.0 * M * N * K
         # implicit im2col: K1 reads the activations once (L2 reuse across windows), not M x K floats
         hbm = hbm_bytes_step(M, N, K, r + p) - (4.0 * M * K - 4.0 * X.numel() if implicit else 0.0)
-        out.append({"layer": name, "M": M, "K": K, "N": N, "ms": t * 1e3, "bare_int8_ms": tb * 1e3,
+        out.append({"layer": name, "M": M, "K": K, "N": N, "ms": t * 1e3, "static_b_ms": ts * 1e3, "bare_int8_ms": tb * 1e3,
                     "overhead_vs_bare": t / tb, "tops": ops / t / 1e12, "rel_fro_error": err,
                     "hbm_gbs": hbm / t / 1e9, "hbm_frac": hbm / t / 1e9 / hbm_peak()})
-        t_all += t; t_bare_all += tb; ops_all += ops; hbm_all += hbm
+        t_all += t; t_bare_all += tb; ops_all += ops; hbm_all += hbm; t_static_all += ts
         out[-1]["a_input"] = "implicit im2col" if implicit else "activations"
         del A, X, Bt, D, C
         torch.cuda.empty_cache()
@@ -358,6 +374,10 @@ def run_resnet(args, ws, rank, local):
                 "config": {"workload": label, "layers": len(layers), "bits": bits, "rank": r, "oversample": p,
                            "batch": 256},
                 "overhead_vs_bare_int8": t_all / t_bare_all, "bare_int8_tops": ops_all / t_bare_all / 1e12,
+                "static_b": {"ms_per_step": t_static_all * 1e3, "value": ops_all / t_static_all / 1e12, "unit": "TOPS",
+                             "overhead_vs_bare_int8": t_static_all / t_bare_all,
+                             "note": "weight-resident deployment (SURVEY f2): per layer quantize(A) + rsvd_residual(omega_a) "
+                                     "+ gemm with B's codes and factors from lrqmm_rsvd_residual_b"},
                 "hbm_roofline": {"bytes": hbm_all, "gbs": hbm_all / t_all / 1e9, "peak_gbs": hbm_peak(),
                                  "frac": hbm_all / t_all / 1e9 / hbm_peak(),
                                  "note": "algorithmic bytes of the whole LRQMM call per layer (bench.hbm_bytes_step)"},
