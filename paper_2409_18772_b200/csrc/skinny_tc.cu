@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   constexpr int S = C::S;
   constexpr int NACC = C::kAccBufs;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ float cinv_s[2][2][64];  // [side][P1 / P2][column]
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStage);
   uint64_t* full = bars;          // S: stage landed (TMA tx)
@@ -388,6 +389,13 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   } else {
     // -------------------------------------------------------------- epilogue
     const int quad = warp & 3;
+    // the per-column scales 1/s_c of both sides' P1 / P2 (written by the prep launch), once
+    for (int e = threadIdx.x - 2 * 32; e < 4 * 64; e += 128) {
+      const int sd = e >> 7, which = (e >> 6) & 1, c = e & 63;
+      const TcArgs& a = args.a[sd];
+      cinv_s[sd][which][c] = (sd == 0 || args.units > args.units0) && c < a.W ? (which ? a.cinv2[c] : a.cinv1[c]) : 0.f;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
     int lu = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
       int side, blk, split, nkb;
@@ -452,23 +460,31 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);  // accumulator buffer free: the next unit's MMAs may start
+      // this thread's output row: 16-byte stores (W is a multiple of 8, rows are 32-byte aligned),
+      // per-column scales from shared memory
       if (orow < a.nout) {
         if (kHasU) {
-          float* o1 = a.out1 + (int64_t)split * a.nout * a.W + orow * a.W;
+          float4* o1 = reinterpret_cast<float4*>(a.out1 + (int64_t)split * a.nout * a.W + orow * a.W);
           const float s1 = inv_row * (1.f / kUScale);
+          const float* cs = cinv_s[side][0];
 #pragma unroll
           for (int g = 0; g < GU; ++g)
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-              if (g * 32 + c < a.W) o1[g * 32 + c] = o[g][c] * (s1 * __ldg(a.cinv1 + g * 32 + c));
+            for (int c = 0; c < 32; c += 4)
+              if (g * 32 + c < a.W)
+                o1[(g * 32 + c) >> 2] = make_float4(o[g][c] * (s1 * cs[g * 32 + c]), o[g][c + 1] * (s1 * cs[g * 32 + c + 1]),
+                                                    o[g][c + 2] * (s1 * cs[g * 32 + c + 2]), o[g][c + 3] * (s1 * cs[g * 32 + c + 3]));
         }
         if (kHasC) {
-          float* o2 = a.out2 + (int64_t)split * a.nout * a.W + orow * a.W;
+          float4* o2 = reinterpret_cast<float4*>(a.out2 + (int64_t)split * a.nout * a.W + orow * a.W);
+          const float* cs = cinv_s[side][1];
 #pragma unroll
           for (int g = 0; g < NA; ++g)
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-              if (g * 32 + c < a.W) o2[g * 32 + c] = o[GU + g][c] * (inv_row * __ldg(a.cinv2 + g * 32 + c));
+            for (int c = 0; c < 32; c += 4)
+              if (g * 32 + c < a.W)
+                o2[(g * 32 + c) >> 2] = make_float4(o[GU + g][c] * (inv_row * cs[g * 32 + c]), o[GU + g][c + 1] * (inv_row * cs[g * 32 + c + 1]),
+                                                    o[GU + g][c + 2] * (inv_row * cs[g * 32 + c + 2]), o[GU + g][c + 3] * (inv_row * cs[g * 32 + c + 3]));
         }
       }
     }
