@@ -117,6 +117,21 @@ def _ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
 
 
+def _arg(t, dtype: str, device: int, name: str) -> int:
+    """Device pointer of a caller tensor after checking what the C ABI assumes (a CUDA tensor of
+    torch.<dtype> on the handle's device); raises ValueError instead of passing a wrong pointer."""
+    import torch
+
+    if t is None:
+        return 0
+    dtype = getattr(torch, dtype)
+    if not t.is_cuda or t.device.index != device:
+        raise ValueError(f"{name}: expected a tensor on cuda:{device}, got {t.device}")
+    if t.dtype != dtype:
+        raise ValueError(f"{name}: expected {dtype}, got {t.dtype}")
+    return int(t.data_ptr())
+
+
 def _ld(t) -> int:
     assert t.dim() == 2 and t.stride(1) == 1, "row-major with unit column stride expected"
     return int(t.stride(0))
@@ -164,7 +179,7 @@ class Lrqmm:
     # ---- the five calls of the boundary ----
     def quantize(self, side: int, X):
         """X: float32 cuda tensor (rows x k), any row stride."""
-        _check(self.lib.lrqmm_quantize(self.h, side, _ptr(X), _ld(X)), "lrqmm_quantize")
+        _check(self.lib.lrqmm_quantize(self.h, side, _arg(X, "float32", self.device, "X"), _ld(X)), "lrqmm_quantize")
 
     def quantize_im2col(self, side: int, X, kh: int, kw: int, stride=1, pad=0, dilation=1):
         """X: float32 cuda tensor [batch, H, W, C] (NHWC, dense); the side's matrix is its im2col
@@ -174,19 +189,23 @@ class Lrqmm:
         dl = dilation if isinstance(dilation, tuple) else (dilation, dilation)
         assert X.dim() == 4 and X.is_contiguous()
         g = ConvGeom(X.shape[0], X.shape[1], X.shape[2], X.shape[3], kh, kw, st[0], st[1], pd[0], pd[1], dl[0], dl[1])
-        _check(self.lib.lrqmm_quantize_im2col(self.h, side, _ptr(X), ctypes.byref(g)), "lrqmm_quantize_im2col")
+        _check(self.lib.lrqmm_quantize_im2col(self.h, side, _arg(X, "float32", self.device, "X"), ctypes.byref(g)),
+               "lrqmm_quantize_im2col")
 
     def rsvd_residual(self, omega_a, omega_b=None):
         """omega_b None: static-B mode (B's factors from rsvd_residual_b / the last full call)."""
         assert omega_b is None or omega_a.stride(0) == omega_b.stride(0)
-        _check(self.lib.lrqmm_rsvd_residual(self.h, _ptr(omega_a), _ptr(omega_b), _ld(omega_a)), "lrqmm_rsvd_residual")
+        _check(self.lib.lrqmm_rsvd_residual(self.h, _arg(omega_a, "float32", self.device, "omega_a"),
+                                            _arg(omega_b, "float32", self.device, "omega_b"), _ld(omega_a)),
+               "lrqmm_rsvd_residual")
 
     def rsvd_residual_b(self, omega_b):
         """Static-B preparation: B's RSVD once, resident until B is quantized again."""
-        _check(self.lib.lrqmm_rsvd_residual_b(self.h, _ptr(omega_b), _ld(omega_b)), "lrqmm_rsvd_residual_b")
+        _check(self.lib.lrqmm_rsvd_residual_b(self.h, _arg(omega_b, "float32", self.device, "omega_b"), _ld(omega_b)),
+               "lrqmm_rsvd_residual_b")
 
     def gemm(self, D, alpha: float = 1.0, beta: float = 0.0):
-        _check(self.lib.lrqmm_gemm(self.h, alpha, beta, _ptr(D), _ld(D)), "lrqmm_gemm")
+        _check(self.lib.lrqmm_gemm(self.h, alpha, beta, _arg(D, "float32", self.device, "D"), _ld(D)), "lrqmm_gemm")
         return D
 
     def close(self):
@@ -211,7 +230,7 @@ class Lrqmm:
         _check(self.lib.lrqmm_sync(self.h), "lrqmm_sync")
 
     def gemm_int32(self, C):
-        _check(self.lib.lrqmm_gemm_int32(self.h, _ptr(C), _ld(C)), "lrqmm_gemm_int32")
+        _check(self.lib.lrqmm_gemm_int32(self.h, _arg(C, "int32", self.device, "C"), _ld(C)), "lrqmm_gemm_int32")
         return C
 
     def codes(self, side: int):

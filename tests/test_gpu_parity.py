@@ -488,3 +488,14 @@ def test_im2col_with_static_b_and_q0():
         h.gemm(D)
         h.sync()
         check_d(A, Wt, {"D": D.cpu().numpy().astype(np.float64)}, ref)
+
+
+def test_binding_rejects_wrong_tensors():
+    """The binding checks device and dtype before handing a pointer to the C ABI."""
+    with Lrqmm(64, 64, 64, 4, 4, 2) as h:
+        with pytest.raises(ValueError):
+            h.quantize(SIDE_A, torch.zeros((64, 64)))                               # host tensor
+        with pytest.raises(ValueError):
+            h.quantize(SIDE_A, torch.zeros((64, 64), dtype=torch.float64, device=DEV))
+        with pytest.raises(ValueError):
+            h.gemm_int32(torch.zeros((64, 64), device=DEV))                          # needs int32
