@@ -682,6 +682,12 @@ void launch_quantize_rows(const QuantArgs& a, bool fixed, cudaStream_t st) {
 // L1 / L2) codes and the Q15 residual planes, with the exact arithmetic of k1_quantize_tma.  A
 // 3x3 window reads each activation ~9 times, so HBM sees the activations once (L2 reuse across
 // neighbouring rows) instead of the 9x larger fp32 im2col matrix.
+// max with NaN propagation (PTX max.NaN): lets one reduction carry both amax and the non-finite test
+LRQMM_DEV float fmax_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
 // kVec: C % 4 == 0 -> each lane handles groups of 4 consecutive channels of one (i, j) tap
 // (16-byte loads).  Each pass issues VPT independent group loads per lane before using them
 // (memory-level parallelism); rows of K <= 32 E VPT stay in registers between amax and rounding.
@@ -740,19 +746,16 @@ __global__ void __launch_bounds__(256) k1_quantize_im2col(const float* __restric
     };
     reset();
     float v[VPT][4];
-    float amax = 0.f, chk = 0.f;  // chk = sum x * 0: NaN iff some x is NaN or Inf
-    const bool one = K <= SPAN;   // the whole row in registers
+    float amax = 0.f;            // NaN-propagating max: NaN if any x is NaN, Inf if any is infinite
+    const bool one = K <= SPAN;  // the whole row in registers
     for (int k0 = 0; k0 < K; k0 += SPAN) {
       load(k0, v);
 #pragma unroll
       for (int u = 0; u < VPT; ++u)
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          chk = __fmaf_rn(v[u][e], 0.f, chk);
-          amax = fmaxf(amax, fabsf(v[u][e]));
-        }
+        for (int e = 0; e < E; ++e) amax = fmax_nan(amax, fabsf(v[u][e]));
     }
-    if (chk != chk) atomicOr(err_flag, 1);
+    if (!(amax <= 3.402823466e38f)) atomicOr(err_flag, 1);
     amax = warp_max(amax);
     // lambda = RN32(qmax / amax) (IEEE division), 1 for an all-zero row
     const float lam = (amax == 0.f) ? 1.f : __fdiv_rn(static_cast<float>(qmax), amax);
@@ -773,10 +776,18 @@ __global__ void __launch_bounds__(256) k1_quantize_im2col(const float* __restric
         const int k = k0 + (u * 32 + lane) * E;
         if (k >= Kp) continue;
         int c[4], q[4];
+        if (fast) {  // row-uniform: one form per row, not both and a select
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          c[e] = code_fast<kMode>(lam, v[u][e], qmax);
-          q[e] = fast ? q15_fast<kMode>(l32, v[u][e], c[e]) : u_q15_slow(lam, v[u][e], c[e]);
+          for (int e = 0; e < E; ++e) {
+            c[e] = code_fast<kMode>(lam, v[u][e], qmax);
+            q[e] = q15_fast<kMode>(l32, v[u][e], c[e]);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            c[e] = code_fast<kMode>(lam, v[u][e], qmax);
+            q[e] = u_q15_slow(lam, v[u][e], c[e]);
+          }
         }
         if (kVec) {
           *reinterpret_cast<uint32_t*>(crow + k) = bytes4(c[0], c[1], c[2], c[3]);

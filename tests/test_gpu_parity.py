@@ -499,3 +499,13 @@ def test_binding_rejects_wrong_tensors():
             h.quantize(SIDE_A, torch.zeros((64, 64), dtype=torch.float64, device=DEV))
         with pytest.raises(ValueError):
             h.gemm_int32(torch.zeros((64, 64), device=DEV))                          # needs int32
+
+
+def test_quantize_im2col_reports_nonfinite():
+    X = torch.zeros((1, 6, 6, 4), device=DEV)
+    X[0, 2, 3, 1] = float("nan")
+    with Lrqmm(36, 8, 36, 4, 0, 0) as h:
+        h.quantize_im2col(SIDE_A, X, 3, 3, 1, 1, 1)
+        with pytest.raises(LrqmmError) as ei:
+            h.sync()
+        assert ei.value.code == 5  # LRQMM_ERR_NONFINITE
