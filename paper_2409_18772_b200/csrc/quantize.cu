@@ -46,6 +46,13 @@ LRQMM_DEV int u_q15_slow(float lam, float x, int code) {
   return i > 32767 ? 32767 : (i < -32767 ? -32767 : i);
 }
 
+// max with NaN propagation (PTX max.NaN): lets one reduction carry both amax and the non-finite test
+LRQMM_DEV float fmax_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+
 LRQMM_DEV uint32_t pack4(int8_t a, int8_t b, int8_t c, int8_t d) {
   return (uint32_t)(uint8_t)a | ((uint32_t)(uint8_t)b << 8) | ((uint32_t)(uint8_t)c << 16) |
          ((uint32_t)(uint8_t)d << 24);
@@ -442,21 +449,19 @@ __global__ void __launch_bounds__(k1t::kThreads, 2)
       const int lane = sub_l;
       const int64_t row = (int64_t)c * R + rr;
       const float* xr = reinterpret_cast<const float*>(slot) + (int64_t)(active ? rr : 0) * K;
-      float amax = 0.f, chk = 0.f;
+      float amax = 0.f;  // NaN-propagating: NaN / Inf if the row holds one (non-finite test below)
       if (kVec4) {
         for (int f = lane; active && f < K / 4; f += L) {
           const float4 v = reinterpret_cast<const float4*>(xr)[f];
-          chk = __fmaf_rn(v.x, 0.f, __fmaf_rn(v.y, 0.f, __fmaf_rn(v.z, 0.f, __fmaf_rn(v.w, 0.f, chk))));
-          amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+          amax = fmax_nan(amax, fmax_nan(fmax_nan(fabsf(v.x), fabsf(v.y)), fmax_nan(fabsf(v.z), fabsf(v.w))));
         }
       } else {
         for (int j = lane; active && j < K; j += L) {
           const float v = xr[j];
-          chk = __fmaf_rn(v, 0.f, chk);
-          amax = fmaxf(amax, fabsf(v));
+          amax = fmax_nan(amax, fabsf(v));
         }
       }
-      if (chk != chk) atomicOr(err_flag, 1);
+      if (!(amax <= 3.402823466e38f)) atomicOr(err_flag, 1);
       float lam;
       if (kFixedLam) {
         lam = lam_in[0];
@@ -682,12 +687,6 @@ void launch_quantize_rows(const QuantArgs& a, bool fixed, cudaStream_t st) {
 // L1 / L2) codes and the Q15 residual planes, with the exact arithmetic of k1_quantize_tma.  A
 // 3x3 window reads each activation ~9 times, so HBM sees the activations once (L2 reuse across
 // neighbouring rows) instead of the 9x larger fp32 im2col matrix.
-// max with NaN propagation (PTX max.NaN): lets one reduction carry both amax and the non-finite test
-LRQMM_DEV float fmax_nan(float a, float b) {
-  float d;
-  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
-  return d;
-}
 // kVec: C % 4 == 0 -> each lane handles groups of 4 consecutive channels of one (i, j) tap
 // (16-byte loads).  Each pass issues VPT independent group loads per lane before using them
 // (memory-level parallelism); rows of K <= 32 E VPT stay in registers between amax and rounding.
