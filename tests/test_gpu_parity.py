@@ -382,6 +382,8 @@ def test_empty_problem_is_a_no_op():
     (1, 23, 23, 3, 7, 7, 2, 3, 1, 16),      # the 7x7 stem (C = 3: scalar taps)
     (2, 9, 9, 16, 1, 1, 2, 0, 1, 40),       # 1x1 strided downsample
     (1, 12, 10, 8, 3, 3, 1, 2, 2, 24),      # dilated
+    (2, 11, 10, 3, 3, 3, 1, 2, 2, 8),       # dilated, C = 3 (scalar per-tap stepping)
+    (2, 9, 13, 5, 5, 3, 1, 0, 1, 12),       # C = 5, rectangular input, no padding (scalar spans)
 ])
 @pytest.mark.parametrize("bits,rounding", [(4, "floor"), (8, "nearest"), (4, "trunc")])
 def test_quantize_im2col_matches_explicit(geom, bits, rounding):
