@@ -175,6 +175,15 @@ lrqmm_status_t lrqmm_sync(lrqmm_handle_t h);
 lrqmm_status_t lrqmm_run_host(lrqmm_handle_t h, const float* A_host, const float* Bt_host, const float* omegaA_host,
                               const float* omegaB_host, float alpha, float* D_host);
 
+/* Asynchronous form of lrqmm_run_host for a stream of calls: returns once the work is enqueued.
+ * Inputs are staged through two device slots on a copy-in stream and D leaves through a copy-out
+ * stream, so the host->device copy of call i+1 and the device->host copy of call i overlap each
+ * other and the compute (PCIe is full duplex).  Host buffers must be pinned and must stay valid
+ * (inputs unmodified, D unread) until lrqmm_sync, which waits for all three streams.  The
+ * quantize / RSVD / GEMM work stays in call order on the handle stream. */
+lrqmm_status_t lrqmm_run_host_async(lrqmm_handle_t h, const float* A_host, const float* Bt_host,
+                                    const float* omegaA_host, const float* omegaB_host, float alpha, float* D_host);
+
 /* ---- inspection (parity tests); async device-to-device copies on the handle stream ---- */
 /* codes of a side: rows x k int8 into dst (ld >= k) */
 lrqmm_status_t lrqmm_get_codes(lrqmm_handle_t h, lrqmm_side_t side, signed char* dst, int64_t ld);

@@ -93,6 +93,13 @@ struct lrqmm_handle_s {
   bool graph_off = false;
   // run_host buffers
   float *hA = nullptr, *hB = nullptr, *hOmA = nullptr, *hOmB = nullptr, *hD = nullptr;
+  // lrqmm_run_host_async: double-buffered device staging, copy-in / copy-out streams, events
+  struct Slot {
+    float *A = nullptr, *B = nullptr, *OmA = nullptr, *OmB = nullptr, *D = nullptr;
+    cudaEvent_t in = nullptr, consumed = nullptr, done = nullptr, out = nullptr;
+  } slot[2];
+  int next_slot = 0;
+  cudaStream_t cin = nullptr, cout = nullptr;
 };
 
 #define LQ_CUDA(call)                                                                          \
@@ -206,6 +213,13 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->partial); cudaFree(h->Gcross); cudaFree(h->gpart_cross);
   cudaFree(h->counter_cross); cudaFree(h->VWbM); cudaFree(h->err_flag); cudaFree(h->sched);
   cudaFree(h->hA); cudaFree(h->hB); cudaFree(h->hOmA); cudaFree(h->hOmB); cudaFree(h->hD);
+  for (auto& sl : h->slot) {
+    cudaFree(sl.A); cudaFree(sl.B); cudaFree(sl.OmA); cudaFree(sl.OmB); cudaFree(sl.D);
+    for (cudaEvent_t e : {sl.in, sl.consumed, sl.done, sl.out})
+      if (e) cudaEventDestroy(e);
+  }
+  if (h->cin) cudaStreamDestroy(h->cin);
+  if (h->cout) cudaStreamDestroy(h->cout);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   for (auto& x : h->rsvd_exec)
@@ -859,6 +873,8 @@ lrqmm_status_t lrqmm_sync(lrqmm_handle_t h) {
   if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
   cudaSetDevice(h->cfg.device);
   if (cudaStreamSynchronize(h->st) != cudaSuccess) return fail(h, LRQMM_ERR_CUDA);
+  if (h->cin && cudaStreamSynchronize(h->cin) != cudaSuccess) return fail(h, LRQMM_ERR_CUDA);
+  if (h->cout && cudaStreamSynchronize(h->cout) != cudaSuccess) return fail(h, LRQMM_ERR_CUDA);
   if (h->sticky != LRQMM_OK) return h->sticky;
   int flag = 0;
   if (cudaMemcpy(&flag, h->err_flag, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return fail(h, LRQMM_ERR_CUDA);
@@ -897,6 +913,54 @@ lrqmm_status_t lrqmm_run_host(lrqmm_handle_t h, const float* A_host, const float
   if ((e = lrqmm_gemm(h, alpha, 0.f, h->hD, n)) != LRQMM_OK) return e;
   LQ_CUDA(cudaMemcpyAsync(D_host, h->hD, sizeof(float) * m * n, cudaMemcpyDeviceToHost, h->st));
   return lrqmm_sync(h);
+}
+
+lrqmm_status_t lrqmm_run_host_async(lrqmm_handle_t h, const float* A_host, const float* Bt_host,
+                                    const float* omegaA_host, const float* omegaB_host, float alpha, float* D_host) {
+  if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (h->sticky != LRQMM_OK) return h->sticky;
+  const int64_t m = h->cfg.m, n = h->cfg.n, k = h->cfg.k, kk = h->kk;
+  const int64_t nb = h->s[1].rows;
+  if ((!A_host && m * k > 0) || (!Bt_host && nb * k > 0) || (!D_host && m * n > 0)) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (h->r > 0 && (!omegaA_host || !omegaB_host)) return LRQMM_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(h->cfg.device);
+  if (!h->cin) {
+    bool ok = cudaStreamCreateWithFlags(&h->cin, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&h->cout, cudaStreamNonBlocking) == cudaSuccess;
+    for (auto& sl : h->slot) {
+      ok = ok && dalloc(&sl.A, m * k) && dalloc(&sl.B, nb * k) && dalloc(&sl.D, m * n);
+      if (ok && kk > 0) ok = dalloc(&sl.OmA, k * kk) && dalloc(&sl.OmB, k * kk);
+      for (cudaEvent_t* e : {&sl.in, &sl.consumed, &sl.done, &sl.out})
+        ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
+    }
+    if (!ok) return fail(h, LRQMM_ERR_ALLOC);
+  }
+  auto& sl = h->slot[h->next_slot];
+  h->next_slot ^= 1;
+  // copy-in stream: this slot's inputs may be overwritten once the call two steps back consumed them
+  LQ_CUDA(cudaStreamWaitEvent(h->cin, sl.consumed, 0));
+  LQ_CUDA(cudaMemcpyAsync(sl.A, A_host, sizeof(float) * m * k, cudaMemcpyHostToDevice, h->cin));
+  LQ_CUDA(cudaMemcpyAsync(sl.B, Bt_host, sizeof(float) * nb * k, cudaMemcpyHostToDevice, h->cin));
+  if (kk > 0) {
+    LQ_CUDA(cudaMemcpyAsync(sl.OmA, omegaA_host, sizeof(float) * k * kk, cudaMemcpyHostToDevice, h->cin));
+    LQ_CUDA(cudaMemcpyAsync(sl.OmB, omegaB_host, sizeof(float) * k * kk, cudaMemcpyHostToDevice, h->cin));
+  }
+  LQ_CUDA(cudaEventRecord(sl.in, h->cin));
+  // compute (handle stream)
+  LQ_CUDA(cudaStreamWaitEvent(h->st, sl.in, 0));
+  lrqmm_status_t e;
+  if ((e = lrqmm_quantize(h, LRQMM_SIDE_A, sl.A, k)) != LRQMM_OK) return e;
+  if ((e = lrqmm_quantize(h, LRQMM_SIDE_B, sl.B, k)) != LRQMM_OK) return e;
+  if (h->r > 0 && (e = lrqmm_rsvd_residual(h, sl.OmA, sl.OmB, kk)) != LRQMM_OK) return e;
+  LQ_CUDA(cudaEventRecord(sl.consumed, h->st));  // the slot's inputs are no longer read
+  LQ_CUDA(cudaStreamWaitEvent(h->st, sl.out, 0));  // the slot's D was copied out by its last user
+  if ((e = lrqmm_gemm(h, alpha, 0.f, sl.D, n)) != LRQMM_OK) return e;
+  LQ_CUDA(cudaEventRecord(sl.done, h->st));
+  // copy-out stream
+  LQ_CUDA(cudaStreamWaitEvent(h->cout, sl.done, 0));
+  LQ_CUDA(cudaMemcpyAsync(D_host, sl.D, sizeof(float) * m * n, cudaMemcpyDeviceToHost, h->cout));
+  LQ_CUDA(cudaEventRecord(sl.out, h->cout));
+  return check_launch(h);
 }
 
 lrqmm_status_t lrqmm_get_codes(lrqmm_handle_t h, lrqmm_side_t side, signed char* dst, int64_t ld) {

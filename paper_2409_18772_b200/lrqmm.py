@@ -32,7 +32,7 @@ EXPORTS = (
     "lrqmm_destroy", "lrqmm_sync", "lrqmm_run_host", "lrqmm_get_codes", "lrqmm_get_scales",
     "lrqmm_gemm_int32", "lrqmm_get_factors", "lrqmm_get_correction", "lrqmm_correction_width",
     "lrqmm_get_timings", "lrqmm_launch_count", "lrqmm_status_string", "lrqmm_rsvd_residual_b",
-    "lrqmm_quantize_im2col",
+    "lrqmm_quantize_im2col", "lrqmm_run_host_async",
 )
 DEBUG_EXPORTS = ("lrqmm_debug_proj", "lrqmm_debug_small", "lrqmm_debug_set_gemm_variant")
 
@@ -86,6 +86,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lrqmm_destroy": (I, [P]),
         "lrqmm_sync": (I, [P]),
         "lrqmm_run_host": (I, [P, P, P, P, P, F, P]),
+        "lrqmm_run_host_async": (I, [P, P, P, P, P, F, P]),
         "lrqmm_get_codes": (I, [P, I, P, I64]),
         "lrqmm_get_scales": (I, [P, I, P]),
         "lrqmm_gemm_int32": (I, [P, P, I64]),
@@ -283,6 +284,15 @@ class Lrqmm:
             return None if a is None else ctypes.c_void_p(a.ctypes.data)
         _check(self.lib.lrqmm_run_host(self.h, hp(A), hp(Bt), hp(omega_a), hp(omega_b), alpha, hp(D)),
                "lrqmm_run_host")
+        return D
+
+    def run_host_async(self, A: np.ndarray, Bt: np.ndarray, omega_a: np.ndarray | None,
+                       omega_b: np.ndarray | None, D: np.ndarray, alpha: float = 1.0):
+        """Enqueue one call (pinned host arrays, valid until sync()); copies overlap across calls."""
+        def hp(a):
+            return None if a is None else ctypes.c_void_p(a.ctypes.data)
+        _check(self.lib.lrqmm_run_host_async(self.h, hp(A), hp(Bt), hp(omega_a), hp(omega_b), alpha, hp(D)),
+               "lrqmm_run_host_async")
         return D
 
 

@@ -511,3 +511,24 @@ def test_quantize_im2col_reports_nonfinite():
         with pytest.raises(LrqmmError) as ei:
             h.sync()
         assert ei.value.code == 5  # LRQMM_ERR_NONFINITE
+
+
+def test_run_host_async_pipeline_matches_sync():
+    """Three pipelined host calls with different inputs (both staging slots, overlapping copies)
+    give exactly the synchronous path's D for each."""
+    M, N, K, r, p = 384, 320, 512, 8, 5
+    probs = [S.problem(M, N, K, r + p, s=80 + i, dist=["normal", "u01", "exp4"][i]) for i in range(3)]
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
+    with Lrqmm(M, N, K, 4, r, p) as h:
+        refs = []
+        for A, Bt, OmA, OmB in probs:
+            D = pin(np.zeros((M, N), np.float32))
+            h.run_host(pin(A), pin(Bt), pin(OmA[:, :r + p]), pin(OmB[:, :r + p]), D)
+            refs.append(D.copy())
+        ins = [(pin(A), pin(Bt), pin(OmA[:, :r + p]), pin(OmB[:, :r + p])) for A, Bt, OmA, OmB in probs]
+        outs = [pin(np.zeros((M, N), np.float32)) for _ in range(3)]
+        for (a, b, oa, ob), D in zip(ins, outs):
+            h.run_host_async(a, b, oa, ob, D)
+        h.sync()
+    for D, ref in zip(outs, refs):
+        assert np.array_equal(D.view(np.uint32), ref.view(np.uint32))
