@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--b-sharded", action="store_true",
                     help="N > 1: also column-shard B over the ranks (SURVEY §8(e)(ii); codes, scales and L_B "
                          "allgathered) instead of replicating it")
