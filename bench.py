@@ -477,6 +477,9 @@ def main():
     t_step = e0.elapsed_time(e1) / 1e3 / args.steps
     ph = np.array([[ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])] for ev in evs]) / 1e3
     t_quant, t_rsvd, t_gemm = [float(x) for x in ph.mean(axis=0)]
+    per_step = ph.sum(axis=1)  # event-to-event time of each timed step (s)
+    step_stats = {"median_ms": float(np.median(per_step)) * 1e3, "min_ms": float(per_step.min()) * 1e3,
+                  "max_ms": float(per_step.max()) * 1e3, "steps": int(per_step.size)}
     t_step = max_over_ranks(t_step, ws, dev)
 
     # bare int8 GEMM (same tcgen05 kernel, int32 epilogue): the overhead denominator
@@ -647,6 +650,7 @@ def main():
                                    f"row-shard A x{ws}, B replicated") if ws > 1 else "single GPU"},
         "overhead_vs_bare_int8": t_step / t_bare,
         "overhead_vs_direct_quant": t_step / t_dq,
+        "step_stats": step_stats,
         "ms": {"bare_int8_gemm": t_bare * 1e3, "direct_quant_pipeline": t_dq * 1e3, "quantize_AB": t_quant * 1e3,
                "rsvd_residual": t_rsvd * 1e3, "gemm_fused_epilogue": t_gemm * 1e3},
         "bare_int8_tops": 2.0 * Mloc * N * K / t_bare / 1e12,
