@@ -183,7 +183,7 @@ def row_shard(M_total: int, ws: int, rank: int) -> tuple[int, int]:
 
 
 # ------------------------------------------------------------ oracle legs
-def oracle_sample(cfg, seed_base=0, rows=REF_ROWS, b_rows=None):
+def oracle_sample(cfg, seed_base=0, rows=REF_ROWS, b_rows=None, phases=None):
     """Time the fp64 oracle (as it stands) on a bounded row sample of the workload:
     the first `rows` rows of A against the first `b_rows` rows of B^T (all by default; the B-side
     quantize + RSVD is the sample's dominant cost).  Returns (seconds, ops_sampled)."""
@@ -201,6 +201,22 @@ def oracle_sample(cfg, seed_base=0, rows=REF_ROWS, b_rows=None):
     t0 = time.perf_counter()
     O.lrqmm(A, Bt, bits, r, OmA, OmB, q=1)
     dt = time.perf_counter() - t0
+    if phases is not None:
+        # the oracle's own steps one by one on the same sample: wall clock per phase
+        def timed(name, f):
+            t = time.perf_counter()
+            out = f()
+            phases[name] = time.perf_counter() - t
+            return out
+        ca, la = timed("quantize_A", lambda: O.quantize(A, bits))
+        cb, lb = timed("quantize_B", lambda: O.quantize(Bt, bits))
+        RA = O.residual(A, ca, la)
+        RB = O.residual(Bt, cb, lb)
+        timed("rsvd_A", lambda: O.rsvd(RA, OmA, r, 1))
+        timed("rsvd_B", lambda: O.rsvd(RB, OmB, r, 1))
+        c = timed("int_gemm", lambda: O.int_gemm(ca, cb))
+        timed("dequant", lambda: O.dequant_result(c, la, lb))
+        timed("C_exact", lambda: O.matmul_exact(A, Bt))
     del A, Bt
     return dt, 2.0 * rows * N * K
 
@@ -625,10 +641,12 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
-        dt, sops = oracle_sample(cfg)
+        phases = {}
+        dt, sops = oracle_sample(cfg, phases=phases)
         cpu = {"value": sops / dt / 1e12, "unit": "TOPS", "cores": cpu_cores(), "kind": "oracle",
                "sample": f"NumPy fp64 oracle on the first {REF_ROWS} rows of A x full B^T ({N}x{K}), "
-                         f"incl. full quantize + RSVD of B; {dt:.1f} s"}
+                         f"incl. full quantize + RSVD of B; {dt:.1f} s",
+               "phases_s": {k: round(v, 4) for k, v in phases.items()}}
 
     line = {
         "metric": METRIC,
