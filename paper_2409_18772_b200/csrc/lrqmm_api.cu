@@ -45,6 +45,7 @@ struct Side {
   int* counter = nullptr;    // Gram last-block ticket
   unsigned* cmax0 = nullptr; // column maxima of |Q0 / lambda| (COL pass image), written by apply64
   unsigned* cmax1 = nullptr; // column maxima of |Q1| (ROW / dual / codes pass images)
+  unsigned* cmaxOm = nullptr;  // column maxima of |Omega| (S1 pass image), from the Omega copy
   double* T64 = nullptr;     // W x W  (orth transform, fp64)
   float* VW = nullptr;       // W x W  (first r columns: truncation)
 };
@@ -207,7 +208,7 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   for (auto& s : h->s) {
     cudaFree(s.codes); cudaFree(s.lam); cudaFree(s.inv_lam); cudaFree(s.row_amax); cudaFree(s.lam_scalar); cudaFree(s.Om);
     cudaFree(s.Y); cudaFree(s.Q0); cudaFree(s.Z); cudaFree(s.Q1); cudaFree(s.Gp); cudaFree(s.G);
-    cudaFree(s.gpart); cudaFree(s.cmax0); cudaFree(s.cmax1); cudaFree(s.counter); cudaFree(s.T64); cudaFree(s.VW); cudaFree(s.U); cudaFree(s.img);
+    cudaFree(s.gpart); cudaFree(s.cmaxOm); cudaFree(s.cmax0); cudaFree(s.cmax1); cudaFree(s.counter); cudaFree(s.T64); cudaFree(s.VW); cudaFree(s.U); cudaFree(s.img);
     cudaFree(s.R32); cudaFree(s.rcodes); cudaFree(s.rlam); cudaFree(s.rinv); cudaFree(s.rrow_amax); cudaFree(s.rlam_scalar);
   }
   cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->partial); cudaFree(h->Gcross); cudaFree(h->gpart_cross);
@@ -279,7 +280,7 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
       ok = ok && dalloc(&s.U, 2 * s.rows * s.ldu) && dalloc(&s.Om, K * h->W) && dalloc(&s.Y, s.rows * h->W) && dalloc(&s.Q0, s.rows * h->W) &&
            dalloc(&s.Z, K * h->W) && dalloc(&s.Q1, K * h->W) && dalloc(&s.Gp, s.rows * h->W) &&
            dalloc(&s.G, (int64_t)h->W * h->W) && dalloc(&s.gpart, (int64_t)kGramMaxBlocks * h->W * h->W) &&
-           dalloc(&s.counter, 64) && dalloc(&s.cmax0, 64) && dalloc(&s.cmax1, 64) && dalloc(&s.T64, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W) &&
+           dalloc(&s.counter, 64) && dalloc(&s.cmax0, 64) && dalloc(&s.cmax1, 64) && dalloc(&s.cmaxOm, 64) && dalloc(&s.T64, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W) &&
            dalloc(&s.img, 2 * tc_img_bytes(std::max<int64_t>(s.rows, K), h->W));
     }
     if (cfg->qt_terms > 0)
@@ -600,7 +601,8 @@ static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides) {
     // q = 0 (reading #30): S1 Y = R Omega; O1 Q0 = orth(Y); S2 Z = R^T Q0 = B^T of Algorithm 1
     // (B = Q0^* R).  Z goes to the Q1 buffer (the K-side factor), reduced.
     const float* Oms[2] = {h->s[0].Om, h->s[1].Om};
-    pass_sides(h, kPassRow, sides, Oms, nullptr, Ys, nullptr, false, nsp);
+    const unsigned* cmo[2] = {h->s[0].cmaxOm, h->s[1].cmaxOm};
+    pass_sides(h, kPassRow, sides, Oms, nullptr, Ys, nullptr, false, nsp, cmo);
     if ((e = gram_step(h, Ys, rows, nsp, 0, Q0s, true, sides, 0)) != LRQMM_OK) return e;
     pass_sides(h, kPassCol, sides, Q0s, nullptr, Q1s, nullptr, true, nsp, cm0);
     for (int sd = 0; sd < 2; ++sd)
@@ -610,7 +612,8 @@ static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides) {
   }
   // S1: Y = R Omega   (Algorithm 1 sampling)
   const float* Oms[2] = {h->s[0].Om, h->s[1].Om};
-  pass_sides(h, kPassRow, sides, Oms, nullptr, Ys, nullptr, false, nsp);
+  const unsigned* cmo[2] = {h->s[0].cmaxOm, h->s[1].cmaxOm};
+  pass_sides(h, kPassRow, sides, Oms, nullptr, Ys, nullptr, false, nsp, cmo);
   for (int it = 0; it < h->cfg.power_iters; ++it) {
     // O1: Q0 = orth(Y)   (Y rows of A are sharded across ranks)
     if ((e = gram_step(h, Ys, rows, nsp, 0, Q0s, true, sides, 0)) != LRQMM_OK) return e;
@@ -774,9 +777,8 @@ static lrqmm_status_t run_rsvd(lrqmm_handle_t h, int kind) {
 }
 
 static lrqmm_status_t copy_omega(lrqmm_handle_t h, int sd, const float* om, int64_t ldo) {
-  LQ_CUDA(cudaMemcpy2DAsync(h->s[sd].Om, sizeof(float) * h->W, om, sizeof(float) * ldo, sizeof(float) * h->kk,
-                            h->cfg.k, cudaMemcpyDeviceToDevice, h->st));
-  return LRQMM_OK;
+  launch_copy_omega(om, ldo, (int)h->kk, h->cfg.k, h->W, h->s[sd].Om, h->s[sd].cmaxOm, h->st);
+  return check_launch(h);
 }
 
 lrqmm_status_t lrqmm_rsvd_residual_b(lrqmm_handle_t h, const float* omegaB, int64_t ldo) {

@@ -236,6 +236,40 @@ void launch_apply64_jobs(const Apply64Jobs& in, int W, cudaStream_t st) {
 }
 
 
+// Omega (K x kk, caller layout, ld ldo) -> the handle's zero-padded K x W copy, plus the column
+// maxima of |Omega| (float bits; cmax zeroed beforehand) for the S1 pass's B image, so that prep
+// needs no reduction phase of its own.  Thread = (row lane, column c); one atomicMax per column
+// per block (order-independent: deterministic).
+__global__ void __launch_bounds__(256) k_copy_omega(const float* __restrict__ src, int64_t ldo, int kk, int64_t K, int W,
+                                                    float* __restrict__ dst, unsigned* __restrict__ cmax) {
+  __shared__ unsigned bm[64];
+  if (threadIdx.x < 64) bm[threadIdx.x] = 0u;
+  __syncthreads();
+  const int rpb = blockDim.x / W;  // rows per block iteration
+  const int c = threadIdx.x % W, r0 = threadIdx.x / W;
+  unsigned m = 0u;
+  if (r0 < rpb)
+    for (int64_t row = (int64_t)blockIdx.x * rpb + r0; row < K; row += (int64_t)gridDim.x * rpb) {
+      const float v = c < kk ? src[row * ldo + c] : 0.f;
+      dst[row * W + c] = v;
+      m = max(m, __float_as_uint(fabsf(v)));
+    }
+  if (r0 < rpb && m) atomicMax(&bm[c], m);
+  __syncthreads();
+  if (threadIdx.x < W && bm[threadIdx.x]) atomicMax(cmax + threadIdx.x, bm[threadIdx.x]);
+}
+
+void launch_copy_omega(const float* src, int64_t ldo, int kk, int64_t K, int W, float* dst, unsigned* cmax,
+                       cudaStream_t st) {
+  cudaMemsetAsync(cmax, 0, 64 * sizeof(unsigned), st);
+  if (K == 0 || W == 0) return;
+  const int rpb = 256 / W;
+  int64_t g = (K + rpb - 1) / rpb;
+  if (g > 148 * 4) g = 148 * 4;
+  k_copy_omega<<<(int)g, 256, 0, st>>>(src, ldo, kk, K, W, dst, cmax);
+  ++launch_counter();
+}
+
 __global__ void k_f64_to_f32(const double* __restrict__ in, float* __restrict__ out, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (float)in[i];
