@@ -739,7 +739,10 @@ int& gemm_variant() {  // 0 auto, 1 force one-CTA K6, 2 force CTA-pair K7 (test 
 static bool use_2sm(int64_t M, int64_t N, const int* sched) {
   if (!sched || gemm_variant() == 1) return false;
   if (gemm_variant() == 2) return true;
-  return M >= 512 && N >= 512;
+  // CTA pairs need enough 256 x 256 tiles to fill 74 pairs for several waves: below ~512 of them
+  // (c2, 4096^2: 256) the one-CTA kernel's 2x more, smaller tiles balance better (measured 87 vs
+  // 96 us at 4096^3 fused, tools/gemm_variants.py)
+  return M >= 512 && N >= 512 && ((M + 255) / 256) * ((N + 255) / 256) >= 512;
 }
 
 // map slots: [0] K6 (A box rows 128, B 256), [1] K7 (128 / 128), [2] K6 B box 128, [3] K6 B box 64
