@@ -23,7 +23,7 @@ lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx, int64_t r
                                 const float* P, const float* P2, int W, float* OUT, float* OUT2, void* stream);
 
 /* GEMM kernel selection for later calls in this process: 0 = automatic (CTA-pair kernel for
- * M, N >= 512), 1 = one-CTA kernel (K6), 2 = CTA-pair kernel (K7).  Lets the tests run both
+ * M, N >= 512 and >= 512 256x256 tiles), 1 = one-CTA kernel (K6), 2 = CTA-pair kernel (K7).  Lets the tests run both
  * kernels on the same shapes.  Returns INVALID_ARGUMENT for other values. */
 lrqmm_status_t lrqmm_debug_set_gemm_variant(int variant);
 

@@ -203,7 +203,7 @@ struct GemmArgs {
 };
 // mapA / mapB: arrays of four CUtensorMap (one-CTA, CTA-pair and narrow-N box shapes); 0 on success
 int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB);
-int& gemm_variant();  // 0 auto (CTA pairs when M, N >= 512), 1 one-CTA K6, 2 CTA-pair K7
+int& gemm_variant();  // 0 auto (CTA pairs when M, N >= 512 and >= 512 pair tiles), 1 one-CTA K6, 2 CTA-pair K7
 // 2D TMA map, dims {inner, outer} elements of u8 (dtype 0), fp32 (1) or u16 (2); returns 0 on success
 int encode_map_2d_sw(void* map, int dtype, const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
                      uint32_t box_inner, uint32_t box_outer, int swizzle_bytes /* 0, 32, 64, 128 */);
