@@ -680,7 +680,8 @@ def main():
         "rel_fro_error": errs,
         "roofline": {"bound": "tensor",
                      "kernel": ("k7_gemm_i8_2sm (CTA-pair tcgen05.mma.cta_group::2 kind::i8 + fused LRQMM epilogue)"
-                                if Mloc >= 512 and N >= 512 else "k6_gemm_i8 (tcgen05 kind::i8 + fused LRQMM epilogue)"),
+                                if Mloc >= 512 and N >= 512 and ((Mloc + 255) // 256) * ((N + 255) // 256) >= 512
+                                else "k6_gemm_i8 (tcgen05 kind::i8 + fused LRQMM epilogue)"),  # gemm_i8.cu use_pair rule
                      "achieved": gemm_tops, "peak": int8_peak, "unit": "TFLOP/s", "frac": gemm_tops / int8_peak,
                      "traffic": traffic,
                      "peak_note": f"int8 dense = 2 x {peak_src} bf16 burst ({peaks['bf16_tflops']} TFLOP/s; guide nominal "

@@ -15,6 +15,18 @@ namespace lrqmm {
 
 constexpr int kWarp = 32;
 
+// Programmatic dependent launch (PDL). Every kernel launched through launch_pdl() starts with
+// pdl_enter(): it waits until the preceding kernel on the stream has completed and its writes
+// are visible (griddepcontrol.wait; a no-op when the launch carried no PDL attribute), then
+// lets the next kernel begin launching (griddepcontrol.launch_dependents). Waiting first keeps
+// at most two kernels of a chain resident; the gain is that the next kernel's launch and CTA
+// rasterisation overlap this kernel's tail instead of following its completion. Only eager
+// launches use it (see launch_pdl): inside the captured rsvd graph it measured slower.
+LRQMM_DEV void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 LRQMM_DEV float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -2,6 +2,8 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cstdlib>
+#include <utility>
 
 namespace lrqmm {
 
@@ -9,6 +11,34 @@ namespace lrqmm {
 inline int64_t& launch_counter() {
   static int64_t c = 0;
   return c;
+}
+
+// PDL on (LRQMM_NO_PDL unset): eager launches made through launch_pdl() carry
+// cudaLaunchAttributeProgrammaticStreamSerialization; the kernel must begin with pdl_enter().
+// Launches being captured into a graph do not: the graph already hides launch latency, and the
+// early-resident dependents then only compete for SMs (c2 rsvd_residual 246 -> 264 us with PDL
+// edges in the graph; eager, multi-rank path 289 -> 261 us with PDL; tools/ab_pdl.sh).
+inline bool pdl_enabled() {
+  static const bool on = getenv("LRQMM_NO_PDL") == nullptr;
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (pdl_enabled()) cudaStreamIsCapturing(st, &cap);
+  cfg.numAttrs = (pdl_enabled() && cap == cudaStreamCaptureStatusNone) ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 enum { kRoundFloor = 0, kRoundTrunc = 1, kRoundNearest = 2 };

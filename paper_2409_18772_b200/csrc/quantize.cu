@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(256) k1_quantize(const float* __restrict__ X, 
                                                    float* __restrict__ lam_out, float* __restrict__ inv_out,
                                                    const float* __restrict__ lam_in, int* __restrict__ err_flag,
                                                    uint8_t* __restrict__ U, int64_t ldu, int64_t uplane) {
+  ::lrqmm::pdl_enter();
   constexpr int kRowsPerCta = 256 / TPR;
   constexpr int kWarpsPerRow = TPR / 32;
   __shared__ float red[8];
@@ -156,6 +157,7 @@ __global__ void __launch_bounds__(256) k1_quantize(const float* __restrict__ X, 
 // Per-tensor mode step 1: per-row amax (also non-finite detection).
 __global__ void __launch_bounds__(256) k1_row_amax(const float* __restrict__ X, int64_t ldx, int rows, int K,
                                                    float* __restrict__ amax_out, int* __restrict__ err_flag) {
+  ::lrqmm::pdl_enter();
   __shared__ float red[8];
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
     const float* xr = X + row * ldx;
@@ -183,6 +185,7 @@ __global__ void __launch_bounds__(256) k1_row_amax(const float* __restrict__ X, 
 __global__ void __launch_bounds__(1024) k1_tensor_scale(const float* __restrict__ row_amax, int rows, int qmax,
                                                         float* __restrict__ lam_rows, float* __restrict__ inv_rows,
                                                         float* __restrict__ lam_scalar) {
+  ::lrqmm::pdl_enter();
   __shared__ float red[32];
   __shared__ float lam_s;
   float m = 0.f;
@@ -211,6 +214,7 @@ __global__ void __launch_bounds__(256) k1_quantize_long(const float* __restrict_
                                                         float* __restrict__ lam_out, float* __restrict__ inv_out,
                                                         const float* __restrict__ lam_in, int* __restrict__ err_flag,
                                                         uint8_t* __restrict__ U, int64_t ldu, int64_t uplane) {
+  ::lrqmm::pdl_enter();
   __shared__ float red[8];
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
     const float* xr = X + row * ldx;
@@ -298,6 +302,7 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
                     int8_t* __restrict__ codes, float* __restrict__ lam_out, float* __restrict__ inv_out,
                     const float* __restrict__ lam_in, int* __restrict__ err_flag, uint8_t* __restrict__ U,
                     int64_t ldu, int64_t uplane, int ns, int slot_bytes) {
+  ::lrqmm::pdl_enter();
   using namespace k1t;
   extern __shared__ __align__(128) uint8_t smem_k1[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_k1);
@@ -406,6 +411,7 @@ __global__ void __launch_bounds__(k1t::kThreads, 2)
                          int8_t* __restrict__ codes, float* __restrict__ lam_out, float* __restrict__ inv_out,
                          const float* __restrict__ lam_in, int* __restrict__ err_flag, uint8_t* __restrict__ U,
                          int64_t ldu, int64_t uplane, int ns, int slot_bytes, int L) {
+  ::lrqmm::pdl_enter();
   using namespace k1t;
   extern __shared__ __align__(128) uint8_t smem_k1[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_k1);
@@ -546,7 +552,7 @@ static int64_t launch_k1_rows_tma(const QuantArgs& a, bool fixed, cudaStream_t s
 #define K1R_LAUNCH(V, F, M)                                                                                      \
   do {                                                                                                           \
     cudaFuncSetAttribute(k1_quantize_rows_tma<V, F, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);     \
-    k1_quantize_rows_tma<V, F, M><<<grid, k1t::kThreads, smem, st>>>(a.X, (int)rows_full, R, a.K, a.Kp, a.qmax, \
+    launch_pdl(k1_quantize_rows_tma<V, F, M>, grid, k1t::kThreads, smem, st, a.X, (int)rows_full, R, a.K, a.Kp, a.qmax, \
                                                                      a.codes, a.lam, a.inv_lam, a.lam_fixed,    \
                                                                      a.err_flag, a.U, a.ldu, a.uplane, ns, slot, L); \
   } while (0)
@@ -584,7 +590,7 @@ static bool launch_k1_tma_t(const QuantArgs& a, bool fixed, cudaStream_t st) {
 #define K1T_LAUNCH(F, M)                                                                                         \
   do {                                                                                                           \
     cudaFuncSetAttribute(k1_quantize_tma<VPT, F, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);        \
-    k1_quantize_tma<VPT, F, M><<<grid, k1t::kThreads, smem, st>>>(a.X, a.ldx, (int)a.rows, a.K, a.Kp, a.qmax,   \
+    launch_pdl(k1_quantize_tma<VPT, F, M>, grid, k1t::kThreads, smem, st, a.X, a.ldx, (int)a.rows, a.K, a.Kp, a.qmax,   \
                                                                   a.mode, a.codes, a.lam, a.inv_lam, a.lam_fixed, \
                                                                   a.err_flag, a.U, a.ldu, a.uplane, ns, slot);   \
   } while (0)
@@ -621,7 +627,7 @@ static void launch_k1_t(const QuantArgs& a, bool vec, bool fixed, cudaStream_t s
   int grid = (int)(ctas < 148 * 64 ? ctas : 148 * 64);
   if (grid < 1) grid = 1;
 #define K1_LAUNCH(V, F)                                                                                  \
-  k1_quantize<TPR, VPT, V, F><<<grid, 256, 0, st>>>(a.X, a.ldx, a.rows, a.K, a.Kp, a.qmax, a.mode, a.codes, \
+  launch_pdl(k1_quantize<TPR, VPT, V, F>, grid, 256, 0, st, a.X, a.ldx, a.rows, a.K, a.Kp, a.qmax, a.mode, a.codes, \
                                                     a.lam, a.inv_lam, a.lam_fixed, a.err_flag, a.U, a.ldu, a.uplane)
   if (vec) {
     if (fixed) K1_LAUNCH(true, true); else K1_LAUNCH(true, false);
@@ -675,7 +681,7 @@ void launch_quantize_rows(const QuantArgs& a, bool fixed, cudaStream_t st) {
   else if (Kp <= 256 * 4 * 32) launch_k1_t<256, 32>(a, vec, fixed, st);
   else {
     int grid = a.rows < 148 * 16 ? (int)a.rows : 148 * 16;
-    k1_quantize_long<<<grid, 256, 0, st>>>(a.X, a.ldx, a.rows, a.K, a.Kp, a.qmax, a.mode, a.codes, a.lam,
+    launch_pdl(k1_quantize_long, grid, 256, 0, st, a.X, a.ldx, a.rows, a.K, a.Kp, a.qmax, a.mode, a.codes, a.lam,
                                            a.inv_lam, a.lam_fixed, a.err_flag, a.U, a.ldu, a.uplane); ++launch_counter();
   }
 }
@@ -695,6 +701,7 @@ __global__ void __launch_bounds__(256) k1_quantize_im2col(const float* __restric
                                                           int qmax, int8_t* __restrict__ codes, float* __restrict__ lam_out,
                                                           float* __restrict__ inv_out, int* __restrict__ err_flag,
                                                           uint8_t* __restrict__ U, int64_t ldu, int64_t uplane, int rows) {
+  ::lrqmm::pdl_enter();
   constexpr int E = kVec ? 4 : 1;
   constexpr int SPAN = 32 * E * VPT;  // row elements per batch
   const int lane = threadIdx.x & 31;
@@ -816,9 +823,9 @@ static void im2col_t(const QuantArgs& a, const ConvGeom& g, cudaStream_t st) {
   const int gb = (int)(blocks < 1 ? 1 : blocks);
 #define IM_ARGS a.X, g, a.K, a.Kp, a.qmax, a.codes, a.lam, a.inv_lam, a.err_flag, a.U, a.ldu, a.uplane, (int)a.rows
   constexpr int VPT = kVec ? 8 : 8;
-  if (a.mode == kRoundFloor) k1_quantize_im2col<kRoundFloor, kVec, VPT><<<gb, 256, 0, st>>>(IM_ARGS);
-  else if (a.mode == kRoundTrunc) k1_quantize_im2col<kRoundTrunc, kVec, VPT><<<gb, 256, 0, st>>>(IM_ARGS);
-  else k1_quantize_im2col<kRoundNearest, kVec, VPT><<<gb, 256, 0, st>>>(IM_ARGS);
+  if (a.mode == kRoundFloor) launch_pdl(k1_quantize_im2col<kRoundFloor, kVec, VPT>, gb, 256, 0, st, IM_ARGS);
+  else if (a.mode == kRoundTrunc) launch_pdl(k1_quantize_im2col<kRoundTrunc, kVec, VPT>, gb, 256, 0, st, IM_ARGS);
+  else launch_pdl(k1_quantize_im2col<kRoundNearest, kVec, VPT>, gb, 256, 0, st, IM_ARGS);
 #undef IM_ARGS
   ++launch_counter();
 }
@@ -834,9 +841,9 @@ void launch_tensor_scale(const float* X, int64_t ldx, int64_t rows, int K, int q
                          float* inv_rows, float* lam_scalar, int* err_flag, cudaStream_t st) {
   if (rows > 0) {
     int grid = rows < 148 * 16 ? (int)rows : 148 * 16;
-    k1_row_amax<<<grid, 256, 0, st>>>(X, ldx, (int)rows, K, row_amax, err_flag); ++launch_counter();
+    launch_pdl(k1_row_amax, grid, 256, 0, st, X, ldx, (int)rows, K, row_amax, err_flag); ++launch_counter();
   }
-  k1_tensor_scale<<<1, 1024, 0, st>>>(row_amax, (int)rows, qmax, lam_rows, inv_rows, lam_scalar); ++launch_counter();
+  launch_pdl(k1_tensor_scale, 1, 1024, 0, st, row_amax, (int)rows, qmax, lam_rows, inv_rows, lam_scalar); ++launch_counter();
 }
 
 // QuantTensor (Eq. gemm_r_split): the fp32 residual
@@ -846,6 +853,7 @@ __global__ void __launch_bounds__(256) k_resid_f32(const float* __restrict__ X, 
                                                    const int8_t* __restrict__ codes, int Kp,
                                                    const float* __restrict__ lam, int64_t rows, int K,
                                                    float* __restrict__ R) {
+  ::lrqmm::pdl_enter();
   const int64_t total = rows * K;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / K;
@@ -860,7 +868,7 @@ void launch_resid_f32(const float* X, int64_t ldx, const int8_t* codes, int Kp, 
   const int64_t total = rows * K;
   if (total == 0) return;
   const int g = (int)((total + 255) / 256 < 148 * 64 ? (total + 255) / 256 : 148 * 64);
-  k_resid_f32<<<g, 256, 0, st>>>(X, ldx, codes, Kp, lam, rows, K, R);
+  launch_pdl(k_resid_f32, g, 256, 0, st, X, ldx, codes, Kp, lam, rows, K, R);
   ++launch_counter();
 }
 

@@ -38,6 +38,7 @@ LRQMM_DEV void stage_rows_in(const float* __restrict__ src, int64_t i0, int nr, 
 // Up to kMaxApply jobs per launch: job q owns blocks [first[q], first[q+1]) and walks its rows.
 template <int W>
 __global__ void __launch_bounds__(kApRows) k_apply_small(const ApplyJobs jobs) {
+  ::lrqmm::pdl_enter();
   constexpr int L = ap_ld(W);
   extern __shared__ __align__(16) float apsm[];
   int q = 0;
@@ -125,7 +126,7 @@ static void apply_small_t(ApplyJobs& jobs, cudaStream_t st) {
   int64_t n[kMaxApply];
   for (int q = 0; q < jobs.n; ++q) n[q] = jobs.j[q].n;
   const int grid = assign_blocks(n, jobs.n, jobs.first);
-  k_apply_small<W><<<grid, kApRows, smem, st>>>(jobs);
+  launch_pdl(k_apply_small<W>, grid, kApRows, smem, st, jobs);
 }
 
 void launch_apply_jobs(const ApplyJobs& in, int W, cudaStream_t st) {
@@ -151,6 +152,7 @@ void launch_apply_small(const float* IN1, const float* S1, const float* IN2, con
 // fp32 rounding instead of cond(IN) * eps32).  Same staging as above; one launch for both sides.
 template <int W>
 __global__ void __launch_bounds__(kApRows) k_apply64(const Apply64Jobs jobs) {
+  ::lrqmm::pdl_enter();
   constexpr int L = ap_ld(W);
   extern __shared__ __align__(16) double apsm64[];
   const int q = (jobs.n > 1 && (int)blockIdx.x >= jobs.first[1]) ? 1 : 0;
@@ -221,7 +223,7 @@ static void apply64_t(Apply64Jobs& jobs, cudaStream_t st) {
   }
   int64_t n[2] = {jobs.j[0].n, jobs.n > 1 ? jobs.j[1].n : 0};
   const int grid = assign_blocks(n, jobs.n, jobs.first);
-  k_apply64<W><<<grid, kApRows, smem, st>>>(jobs);
+  launch_pdl(k_apply64<W>, grid, kApRows, smem, st, jobs);
 }
 
 void launch_apply64_jobs(const Apply64Jobs& in, int W, cudaStream_t st) {
@@ -242,6 +244,7 @@ void launch_apply64_jobs(const Apply64Jobs& in, int W, cudaStream_t st) {
 // per block (order-independent: deterministic).
 __global__ void __launch_bounds__(256) k_copy_omega(const float* __restrict__ src, int64_t ldo, int kk, int64_t K, int W,
                                                     float* __restrict__ dst, unsigned* __restrict__ cmax) {
+  ::lrqmm::pdl_enter();
   __shared__ unsigned bm[64];
   if (threadIdx.x < 64) bm[threadIdx.x] = 0u;
   __syncthreads();
@@ -266,17 +269,18 @@ void launch_copy_omega(const float* src, int64_t ldo, int kk, int64_t K, int W, 
   const int rpb = 256 / W;
   int64_t g = (K + rpb - 1) / rpb;
   if (g > 148 * 4) g = 148 * 4;
-  k_copy_omega<<<(int)g, 256, 0, st>>>(src, ldo, kk, K, W, dst, cmax);
+  launch_pdl(k_copy_omega, (int)g, 256, 0, st, src, ldo, kk, K, W, dst, cmax);
   ++launch_counter();
 }
 
 __global__ void k_f64_to_f32(const double* __restrict__ in, float* __restrict__ out, int64_t n) {
+  ::lrqmm::pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (float)in[i];
 }
 void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t st) {
   if (n == 0) return;
-  k_f64_to_f32<<<clamp_grid((n + 255) / 256), 256, 0, st>>>(in, out, n);
+  launch_pdl(k_f64_to_f32, clamp_grid((n + 255) / 256), 256, 0, st, in, out, n);
   ++launch_counter();
 }
 

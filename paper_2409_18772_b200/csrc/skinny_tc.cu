@@ -158,6 +158,7 @@ struct PrepJobs {
 // synchronisation, an ordinary launch.
 template <int NA, bool kHaveMax>
 __global__ void __launch_bounds__(256) k_prep_img(PrepJobs jb) {
+  ::lrqmm::pdl_enter();
   namespace cg = cooperative_groups;
   constexpr int WN = 32 * NA;
   constexpr int kImg = 3 * WN * tcp::BK;
@@ -253,6 +254,7 @@ __global__ void __launch_bounds__(256) k_prep_img(PrepJobs jb) {
 template <int kMode, int NA, int kVar>
 __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_constant__ TcMaps2 maps,
                                                                  const __grid_constant__ TcArgs2 args) {
+  ::lrqmm::pdl_enter();
   using namespace tcp;
   using C = Cfg<kMode, NA, kVar>;
   constexpr bool kHasU = C::kHasU, kHasC = C::kHasC;
@@ -497,6 +499,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
 }
 
 __global__ void k_reduce_splits_tc(const float* __restrict__ part, int nsplit, int64_t n, float* __restrict__ out) {
+  ::lrqmm::pdl_enter();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     float acc = 0.f;
     for (int s = 0; s < nsplit; ++s) acc += part[(int64_t)s * n + e];
@@ -508,6 +511,7 @@ __global__ void k_reduce_splits_tc(const float* __restrict__ part, int nsplit, i
 // group g sums splits g, g + 8, ... in order, then the 8 group sums are added in order
 __global__ void __launch_bounds__(256) k_reduce_splits_wide(const float* __restrict__ part, int nsplit, int64_t n,
                                                             float* __restrict__ out) {
+  ::lrqmm::pdl_enter();
   __shared__ float red[8][33];
   const int e_l = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int64_t e = (int64_t)blockIdx.x * 32 + e_l;
@@ -535,10 +539,10 @@ __global__ void __launch_bounds__(256) k_reduce_splits_wide(const float* __restr
 void launch_reduce_splits(const float* part, int nsplit, int64_t n, float* out, cudaStream_t st) {
   if (n == 0) return;
   if (nsplit > 16) {
-    k_reduce_splits_wide<<<(unsigned)((n + 31) / 32), 256, 0, st>>>(part, nsplit, n, out);
+    launch_pdl(k_reduce_splits_wide, (unsigned)((n + 31) / 32), 256, 0, st, part, nsplit, n, out);
   } else {
     const int g = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
-    k_reduce_splits_tc<<<g, 256, 0, st>>>(part, nsplit, n, out);
+    launch_pdl(k_reduce_splits_tc, g, 256, 0, st, part, nsplit, n, out);
   }
   ++launch_counter();
 }
@@ -570,7 +574,7 @@ static void launch_prep(PrepJobs& jb, cudaStream_t st) {
     int64_t g = (work + 255) / 256;
     if (g > 8 * nsm) g = 8 * nsm;
     if (g < 1) g = 1;
-    k_prep_img<NA, true><<<(int)g, 256, 0, st>>>(jb);
+    launch_pdl(k_prep_img<NA, true>, (int)g, 256, 0, st, jb);
   } else {
     void* args[] = {&jb};
     cudaLaunchCooperativeKernel((const void*)k_prep_img<NA, false>, dim3(grid), dim3(256), args, 0, st);
@@ -675,7 +679,7 @@ static void run_tc(int nsides, const TcPassSide* sides, int W, bool reduce1, int
   args.units0 = (int)units[0];
   args.units = (int)(units[0] + units[1]);
   const int grid = (int)(args.units < nsm ? args.units : nsm);
-  k_tc_proj<kMode, NA, kVar><<<grid, kThreads, C::kSmem, st>>>(maps, args);
+  launch_pdl(k_tc_proj<kMode, NA, kVar>, grid, kThreads, C::kSmem, st, maps, args);
   ++launch_counter();
   for (int sd = 0; sd < nsides; ++sd) {
     const int ns = ns_out[sd];

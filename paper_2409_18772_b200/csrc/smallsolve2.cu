@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(32) k_warp_chol(EigJobs jobs);
 constexpr int kGramRows = 32;
 template <int W>
 __global__ void __launch_bounds__(256) k_gram(GramJobs jobs) {
+  ::lrqmm::pdl_enter();
   const GramJob jb = jobs.j[blockIdx.y];
   const int npairs = W * W;
   __shared__ double s1[kGramRows][kN + 1];
@@ -117,14 +118,14 @@ void launch_gram_jobs(const GramJobs& jobs, int W, cudaStream_t st) {
   if (nb < 1) nb = 1;
 
   switch (W) {
-    case 8: k_gram<8><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
-    case 16: k_gram<16><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
-    case 24: k_gram<24><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
-    case 32: k_gram<32><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
-    case 40: k_gram<40><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
-    case 48: k_gram<48><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
-    case 56: k_gram<56><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
-    case 64: k_gram<64><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st>>>(jobs); break;
+    case 8: launch_pdl(k_gram<8>, dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st, jobs); break;
+    case 16: launch_pdl(k_gram<16>, dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st, jobs); break;
+    case 24: launch_pdl(k_gram<24>, dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st, jobs); break;
+    case 32: launch_pdl(k_gram<32>, dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st, jobs); break;
+    case 40: launch_pdl(k_gram<40>, dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st, jobs); break;
+    case 48: launch_pdl(k_gram<48>, dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st, jobs); break;
+    case 56: launch_pdl(k_gram<56>, dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st, jobs); break;
+    case 64: launch_pdl(k_gram<64>, dim3((unsigned)nb, (unsigned)jobs.n), 256, 0, st, jobs); break;
     default: break;
   }
 
@@ -230,6 +231,7 @@ __device__ void dev_chol_orth(const double* G, double* T64, double* dyn) {
 
 template <int n>
 __global__ void __launch_bounds__(256) k_chol_orth(EigJobs jobs) {
+  ::lrqmm::pdl_enter();
   extern __shared__ double dyn[];
   dev_chol_orth<n>(jobs.j[blockIdx.x].G, jobs.j[blockIdx.x].T64, dyn);
 }
@@ -239,14 +241,14 @@ static const int kDynSmem = 2 * kN * (kN + 1) * (int)sizeof(double);
 template <int n>
 static void chol_t(const EigJobs& jobs, cudaStream_t st) {
   if constexpr (n <= 32) {
-    k_warp_chol<n><<<jobs.n, 32, 0, st>>>(jobs);
+    launch_pdl(k_warp_chol<n>, jobs.n, 32, 0, st, jobs);
   } else {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_chol_orth<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
       attr = true;
     }
-    k_chol_orth<n><<<jobs.n, 256, kDynSmem, st>>>(jobs);
+    launch_pdl(k_chol_orth<n>, jobs.n, 256, kDynSmem, st, jobs);
   }
 }
 
@@ -460,6 +462,7 @@ __device__ void dev_eig_trunc(const double* G, float* T, int r, double* dyn) {
 
 template <int n>
 __global__ void __launch_bounds__(256) k_eig(EigJobs jobs) {
+  ::lrqmm::pdl_enter();
   extern __shared__ double dyn[];
   dev_eig_trunc<n>(jobs.j[blockIdx.x].G, jobs.j[blockIdx.x].T, jobs.j[blockIdx.x].r, dyn);
 }
@@ -472,7 +475,7 @@ static void eig_t(const EigJobs& jobs, cudaStream_t st) {
     cudaFuncSetAttribute(k_eig<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  k_eig<n><<<jobs.n, 256, smem, st>>>(jobs);
+  launch_pdl(k_eig<n>, jobs.n, 256, smem, st, jobs);
 }
 
 void launch_eig_warp(const EigJobs& jobs, int n, cudaStream_t st) {
@@ -582,6 +585,7 @@ __device__ void warp_chol_orth(const double* G, double* T64, double* sm, double*
 
 template <int n>
 __global__ void __launch_bounds__(32) k_warp_chol(EigJobs jobs) {
+  ::lrqmm::pdl_enter();
   __shared__ double buf[3][32 * 33];
   const EigJob job = jobs.j[blockIdx.x];
   warp_chol_orth<n>(job.G, job.T64, buf[0], buf[1], buf[2]);
@@ -598,6 +602,7 @@ __global__ void __launch_bounds__(32) k_warp_chol(EigJobs jobs) {
 __host__ __device__ constexpr int frows(int w) { return w <= 32 ? 256 : 128; }
 template <int W>
 __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
+  ::lrqmm::pdl_enter();
   constexpr int kFRows = frows(W);
   extern __shared__ __align__(128) double dyn[];
   const SmallJob jb = jobs.j[blockIdx.y];
@@ -739,7 +744,7 @@ static void fused_t(const SmallJobs& jobs, int mode, int64_t nb, cudaStream_t st
     cudaFuncSetAttribute(k_fused_small<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     attr = true;
   }
-  k_fused_small<W><<<dim3((unsigned)nb, (unsigned)jobs.n), 256, smem, st>>>(jobs, mode);
+  launch_pdl(k_fused_small<W>, dim3((unsigned)nb, (unsigned)jobs.n), 256, smem, st, jobs, mode);
 }
 
 void launch_fused_small(const SmallJobs& jobs, int W, int mode, cudaStream_t st) {
@@ -773,6 +778,7 @@ void launch_fused_small(const SmallJobs& jobs, int W, int mode, cudaStream_t st)
 __global__ void __launch_bounds__(256) k_cross_small(const double* __restrict__ C, const float* __restrict__ VWa,
                                                      const float* __restrict__ VWb, int n, int r,
                                                      float* __restrict__ VWbM) {
+  ::lrqmm::pdl_enter();
   __shared__ double T1[kN][kN / 2];      // C VWa  (n x r), r <= 32
   __shared__ double M[kN / 2][kN / 2];   // r x r
   const int tid = threadIdx.x;
@@ -800,7 +806,7 @@ __global__ void __launch_bounds__(256) k_cross_small(const double* __restrict__ 
 
 void launch_cross_small(const double* C, const float* VWa, const float* VWb, int n, int r, float* VWbM,
                         cudaStream_t st) {
-  k_cross_small<<<1, 256, 0, st>>>(C, VWa, VWb, n, r, VWbM); ++launch_counter();
+  launch_pdl(k_cross_small, 1, 256, 0, st, C, VWa, VWb, n, r, VWbM); ++launch_counter();
 }
 
 }  // namespace lrqmm
