@@ -231,6 +231,30 @@ def test_repeated_calls_reuse_handle():
             check_d(A, Bt, {"D": D.cpu().numpy().astype(np.float64)}, ref)
 
 
+def test_graph_replay_and_eager_pdl_agree(monkeypatch):
+    """The same call through the captured RSVD graph (plain edges) and eagerly with PDL launches
+    (LRQMM_NO_GRAPH, the multi-rank path; kernels.h launch_pdl) gives bit-identical D; both match
+    the oracle (same kernels, same order, only the launch mechanism differs)."""
+    M, N, K, r, p = 640, 384, 1536, 16, 5
+    A, Bt, OmA, OmB = S.problem(M, N, K, r + p, s=77)
+    ref = O.lrqmm(A, Bt, 4, r, OmA, OmB, q=1)
+    outs = []
+    for eager in (False, True):
+        if eager:
+            monkeypatch.setenv("LRQMM_NO_GRAPH", "1")
+        with Lrqmm(M, N, K, 4, r, p) as h:
+            for _ in range(3):  # the third call replays the graph when graphs are on
+                h.quantize(SIDE_A, cu(A))
+                h.quantize(SIDE_B, cu(Bt))
+                h.rsvd_residual(cu(OmA[:, : r + p]), cu(OmB[:, : r + p]))
+                D = torch.empty((M, N), device=DEV)
+                h.gemm(D)
+                h.sync()
+            outs.append(D.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    check_d(A, Bt, {"D": outs[1].astype(np.float64)}, ref)
+
+
 def test_static_b_mode_matches_full_oracle():
     """Static-B: B quantized + RSVD'd once (rsvd_residual_b), then three A's reuse it
     (rsvd_residual with omega_b=None).  Each result must match the oracle's full Algorithm 2 with the
