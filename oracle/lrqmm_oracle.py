@@ -17,8 +17,13 @@ Pins (all in tests/test_oracle_pins.py, `-m "not gpu"`):
   compute_scale / quantize   -> exact rational arithmetic (fractions.Fraction)
                                 and SPEC.md:141-153 examples
   int_gemm / dequant_result  -> Python-int triple loops; SPEC.md:181, 319
+  orth                       -> known-spectrum (Hadamard) matrices: the 1e-5
+                                threshold is relative to sigma_max at scales
+                                1e-12 / 1 / 1e6 (reading #12)
   rsvd                       -> full-rank recovery, exact-rank fixtures,
-                                Eckart-Young, SPEC.md:235-245 examples
+                                Eckart-Young, SPEC.md:235-245 examples; every
+                                q in {1, 2, 3} against the exact-rational
+                                projector onto span((R^T R)^q Omega)
   lrqmm                      -> exact rational (Fraction) evaluation of the
                                 projector form on 8x8, zero residual, full
                                 rank identity (Eq. gemm_r_split), rank-1

@@ -181,6 +181,37 @@ def test_orth_threshold_and_degenerate():
     assert np.allclose(Q @ (Q.T @ M), M, atol=1e-12)
 
 
+def _hadamard(n):
+    H = np.array([[1.0]])
+    while H.shape[0] < n:
+        H = np.block([[H, H], [H, -H]])
+    return H / np.sqrt(n)  # orthogonal to fp64 rounding
+
+
+@pytest.mark.parametrize("scale", [1e-12, 1.0, 1e6])
+def test_orth_threshold_is_relative_to_sigma_max(scale):
+    """Reading #12 ("orthogonal columns"): orth drops a direction
+    iff sigma < 1e-5 * sigma_max -- a RELATIVE threshold.  M = U diag(s) V^T is built with known
+    singular values from exact orthogonal (Hadamard) factors, so what must be kept is known in
+    closed form: a 1e-12-scaled full-rank matrix keeps every direction (an absolute threshold would
+    drop them all), sigma ratios 1e-4 / 1e-6 keep / drop the small direction at every scale (an
+    absolute threshold would flip one of them at 1e-12 or 1e6)."""
+    U = _hadamard(8)[:, :4]
+    V = _hadamard(4)
+    for sig, keep in (([1.0, 0.5, 0.25, 0.125], 4),        # full rank at any scale
+                      ([1.0, 0.5, 1e-4, 1e-4], 4),          # ratio 1e-4 >= 1e-5: kept
+                      ([1.0, 0.5, 1e-6, 1e-6], 2),          # ratio 1e-6 < 1e-5: dropped
+                      ([1.0, 2e-5, 5e-6, 0.0], 2)):         # straddling the threshold
+        s = np.array(sig) * scale
+        M = (U * s) @ V.T
+        Q = O.orth(M)
+        assert Q.shape == (8, keep), (sig, scale, Q.shape)
+        assert np.allclose(Q.T @ Q, np.eye(keep), atol=1e-12)
+        # span(Q) is exactly the span of the kept left singular vectors
+        Uk = U[:, :keep]
+        assert np.allclose(Q @ (Q.T @ Uk), Uk, atol=1e-10)
+
+
 def test_rsvd_spec_examples():
     rng = np.random.default_rng(0)
     # SPEC.md:235: I_5, r = 5, p = 0 -> full capture
@@ -305,11 +336,13 @@ def test_exact_rank1_residual_fixture(bits):
     assert O.relative_error(C, O.lrqmm(A, Bt, bits, 0)) > 1e-6
 
 
-def _exact_lrqmm_projector_form(A, Bt, bits, OmA, OmB):
-    """Exact rational evaluation of the same definitions (p = 0, q = 1), with
-    the projector P = Z (Z^T Z)^-1 Z^T, Z = R^T R Omega, in place of the
+def _exact_lrqmm_projector_form(A, Bt, bits, OmA, OmB, power_steps=1):
+    """Exact rational evaluation of the same definitions (p = 0, q power steps), with
+    the projector P = Z (Z^T Z)^-1 Z^T, Z = (R^T R)^q Omega, in place of the
     oracle's SVD-based orthonormalisation:  R_k = R P,
-    D = C_F + R_A,k B~ + A~ R_B,k + R_A,k R_B,k."""
+    D = C_F + R_A,k B~ + A~ R_B,k + R_A,k R_B,k.
+    Variant (b) with q power steps (reading #11; q of Eq. rsvderror) spans
+    span(Q1) = span(R^T orth(R ... R^T orth(R Omega))) = span((R^T R)^q Omega) for full-rank sketches."""
     q = O.qmax_of(bits)
 
     def side(X, Om):
@@ -324,8 +357,10 @@ def _exact_lrqmm_projector_form(A, Bt, bits, OmA, OmB):
                  for i in range(len(Xf))]
         Xt = [[Fraction(codes[i][j]) / lams[i] for j in range(len(Xf[0]))] for i in range(len(Xf))]
         R = [[Xf[i][j] - Xt[i][j] for j in range(len(Xf[0]))] for i in range(len(Xf))]
-        Y = frac_matmul(R, to_frac(Om))
-        Z = frac_matmul(frac_T(R), Y)
+        RT = frac_T(R)
+        Z = to_frac(Om)
+        for _ in range(power_steps):
+            Z = frac_matmul(RT, frac_matmul(R, Z))
         P = frac_matmul(frac_matmul(Z, frac_inv(frac_matmul(frac_T(Z), Z))), frac_T(Z))
         Rk = frac_matmul(R, P)
         return codes, lams, Xt, Rk
@@ -343,12 +378,18 @@ def _exact_lrqmm_projector_form(A, Bt, bits, OmA, OmB):
     return np.array([[float(CF[i][j] + T2[i][j] + T3[i][j] + T4[i][j]) for j in range(N)] for i in range(M)])
 
 
-@pytest.mark.parametrize("bits,dist", [(4, "normal"), (4, "u01"), (8, "exp4")])
-def test_8x8_exact_rational_brute_force(bits, dist):
+@pytest.mark.parametrize("bits,dist,q", [(4, "normal", 1), (4, "u01", 1), (8, "exp4", 1),
+                                         (4, "normal", 2), (8, "u01", 2), (4, "exp4", 3)])
+def test_8x8_exact_rational_brute_force(bits, dist, q):
     A, Bt, OmA, OmB = S.problem(8, 8, 8, 3, s=4, dist=dist)
-    exact = _exact_lrqmm_projector_form(A, Bt, bits, OmA, OmB)
-    D = O.lrqmm(A, Bt, bits, 3, OmA, OmB, q=1)
+    exact = _exact_lrqmm_projector_form(A, Bt, bits, OmA, OmB, power_steps=q)
+    D = O.lrqmm(A, Bt, bits, 3, OmA, OmB, q=q)
     assert np.max(np.abs(D - exact)) <= 1e-12 * np.max(np.abs(exact))
+    if q >= 2:
+        # the pin discriminates q: the q-1 result is far outside the tolerance (a loop that
+        # hoisted Y = R Q1 out of the power iteration would make q = 2 return the q = 1 value)
+        prev = _exact_lrqmm_projector_form(A, Bt, bits, OmA, OmB, power_steps=q - 1)
+        assert np.max(np.abs(prev - exact)) > 1e-8 * np.max(np.abs(exact))
 
 
 def test_alpha_beta_contract():
