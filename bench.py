@@ -6,9 +6,11 @@
 A step = one pass of the whole hot path over one batch of synthetic input:
 quantize(A), quantize(B), rsvd_residual, gemm (Algorithm 2).
 Default workload (N=1): BASELINE.json configs[2], 16384^3 int4, rank 16, p=5, q=1,
-Gaussian A and B.  Under torchrun (N>1) every rank holds its own 16384-row block
-of A (global M = 16384*N, weak scaling) and the same B; the A-side RSVD is
-coupled across ranks by NCCL allreduces inside liblrqmm.
+Gaussian A and B.  Under torchrun (N>1) the SAME problem is split (strong
+scaling, the north_star's 16384^3 on 8 GPUs): rank i holds M/N rows of A and,
+by default, n/N rows of B^T; the A- and B-side RSVDs are
+coupled by NCCL allreduces inside liblrqmm and the B codes / scales / L_B
+are allgathered.  `--config c5` is configs[4] (32768^3, r = 32).
 
 One JSON line on rank 0.  `value` = effective TOPS (2*M*N*K / step time, all
 ranks), inputs resident in HBM (2 GiB of fp32 inputs per GPU > 126 MB L2, so no
@@ -31,12 +33,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (M per rank, N, K, bits, rank, oversample, dist, workload label)
+    # name: (M (global; split over the ranks), N, K, bits, rank, oversample, dist, workload label)
     "c3": (16384, 16384, 16384, 4, 16, 5, "normal", "square 16384^3 int4 rank 16 (p=5, q=1) Gaussian, configs[2]"),
     "c2": (4096, 4096, 4096, 4, 16, 5, "normal", "square 4096^3 int4 rank 16 (p=5, q=1) Gaussian, configs[1]"),
     "c2i8": (4096, 4096, 4096, 8, 16, 5, "normal", "square 4096^3 int8 rank 16 (p=5, q=1) Gaussian, configs[1]"),
     "c1": (256, 256, 256, 4, 8, 5, "normal", "square 256^3 int4 rank 8 (p=5, q=1) Gaussian, configs[0]"),
-    "c5": (4096, 32768, 32768, 4, 32, 5, "normal", "32768^3 int4 rank 32 row-sharded (4096 rows/rank), configs[4]"),
+    "c5": (32768, 32768, 32768, 4, 32, 5, "normal", "32768^3 int4 rank 32 row-sharded over the GPUs, configs[4]"),
     # configs[3]: the 53 ResNet-50 convolutions as im2col GEMMs at batch 256 (synth.resnet50_convs)
     "c4": (None, None, None, 4, 20, 5, "relu_normal",
            "ResNet-50 conv layers as im2col GEMMs, batch 256, 4-bit, rank 20 (PAPER.md:822), configs[3]"),
@@ -55,9 +57,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--b-sharded", action="store_true",
-                    help="N > 1: also column-shard B over the ranks (SURVEY §8(e)(ii); codes, scales and L_B "
-                         "allgathered) instead of replicating it")
+    ap.add_argument("--b-replicated", action="store_true",
+                    help="N > 1: every rank quantizes and RSVDs all of B (SURVEY §8(e)(i)) instead of the default "
+                         "column-sharded B (§8(e)(ii): codes, scales and L_B allgathered)")
     return ap.parse_args()
 
 
@@ -232,7 +234,7 @@ def run_reference(args, ws, rank):
     cfg = CONFIGS[args.config]
     if rank != 0:
         return
-    M, N, K = cfg[0] * ws, cfg[1], cfg[2]
+    M, N, K = cfg[0], cfg[1], cfg[2]
     # bounded: a full-B sample costs ~6 s on 16 cores; beyond 12 steps + warmups the B sample
     # shrinks so that the whole run stays within ~2 minutes
     nsteps = args.warmup + args.steps
@@ -249,7 +251,7 @@ def run_reference(args, ws, rank):
               f"(of {cfg[1]}x{cfg[2]}), incl. quantize+RSVD of that B sample")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "TOPS", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg[7], "M": M, "N": N, "K": K, "bits": cfg[3], "rank": cfg[4], "oversample": cfg[5],
                    "power_iters": 1, "sample_rows": REF_ROWS},
@@ -408,6 +410,66 @@ def run_resnet(args, ws, rank, local):
         print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ e2e context
+def pcie_context(dev, nbytes_in: int, nbytes_out: int) -> dict:
+    """Achieved pinned host->device and device->host GB/s for copies of the e2e step's sizes (CUDA
+    events), and the NUMA placement of the GPU and of this process's CPUs: the e2e number is
+    PCIe-bound, so these explain its spread across boxes."""
+    import torch
+
+    out = {}
+    try:
+        n_in = min(nbytes_in, 1 << 30) // 4
+        n_out = min(nbytes_out, 1 << 30) // 4
+        h = torch.empty(max(n_in, n_out), dtype=torch.float32, pin_memory=True)
+        d = torch.empty(max(n_in, n_out), dtype=torch.float32, device=dev)
+        st = torch.cuda.current_stream(dev)
+        for name, n, fn in (("h2d_gbs", n_in, lambda n: d[:n].copy_(h[:n], non_blocking=True)),
+                            ("d2h_gbs", n_out, lambda n: h[:n].copy_(d[:n], non_blocking=True))):
+            fn(n)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(3):
+                fn(n)
+            e1.record(st)
+            torch.cuda.synchronize(dev)
+            out[name] = 3 * 4.0 * n / (e0.elapsed_time(e1) / 1e3) / 1e9
+        del h, d
+    except Exception as e:  # context only
+        out["pcie_error"] = str(e)[:120]
+    try:
+        pr = torch.cuda.get_device_properties(dev)
+        bus = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        out["gpu_pci"] = bus
+        with open(f"/sys/bus/pci/devices/{bus}/numa_node") as f:
+            out["gpu_numa_node"] = int(f.read().strip())
+    except Exception:
+        out["gpu_numa_node"] = None
+    try:
+        cpus = sorted(os.sched_getaffinity(0))
+        nodes = set()
+        base = "/sys/devices/system/node"
+        for nd in os.listdir(base):
+            if not nd.startswith("node"):
+                continue
+            txt = open(os.path.join(base, nd, "cpulist")).read().strip()
+            ids = set()
+            for part in txt.split(","):
+                if "-" in part:
+                    a, b = part.split("-")
+                    ids.update(range(int(a), int(b) + 1))
+                elif part:
+                    ids.add(int(part))
+            if ids & set(cpus):
+                nodes.add(int(nd[4:]))
+        out["process_cpu_numa_nodes"] = sorted(nodes)
+        out["process_cpus"] = len(cpus)
+    except Exception:
+        pass
+    return out
+
+
 # ------------------------------------------------------------------ main
 def main():
     args = parse()
@@ -430,29 +492,41 @@ def main():
         run_resnet(args, ws, rank, local)
         return
     cfg = CONFIGS[args.config]
-    Mloc, N, K, bits, r, p, dist_name, label = cfg
+    M, N, K, bits, r, p, dist_name, label = cfg
     kk = r + p
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
 
-    # synthetic inputs (seeded, per-rank A block), resident in HBM
-    A = S.gen_matrix_torch(dist_name, Mloc, K, 2 * 0 + 7919 * rank, device=dev)
+    # strong scaling (north_star: the one GEMM split over the GPUs): rank i owns rows [lo, hi) of A
+    # and, unless --b-replicated, rows [blo, bhi) of B^T; N=1 is the whole problem
+    lo, hi = row_shard(M, ws, rank)
+    Mloc = hi - lo
+    bsh = ws > 1 and not args.b_replicated
+    # synthetic inputs, resident in HBM: the GLOBAL A is one seeded draw, so every N sees the same
+    # problem (each rank draws it and keeps its rows; B^T likewise, all ranks hold it for the error
+    # sample and the single-rank comparison handles)
+    A_full = S.gen_matrix_torch(dist_name, M, K, 0, device=dev)
+    A = A_full[lo:hi].clone()
+    del A_full
+    torch.cuda.empty_cache()
     Bt = S.gen_matrix_torch(dist_name, N, K, 1, device=dev)
     OmA = torch.from_numpy(S.gen_omega(K, kk, 1000)).to(dev)
     OmB = torch.from_numpy(S.gen_omega(K, kk, 1001)).to(dev)
     D = torch.empty((Mloc, N), device=dev)
     Cint = torch.empty((Mloc, N), dtype=torch.int32, device=dev)
 
-    uid = None
-    if ws > 1:
-        import torch.distributed as dist
+    def handle(rank_=r, p_=p, q_=1, rounding="floor", gran="row", qt=0, multi=True):
+        """A handle with this run's sharding (multi-rank: a fresh NCCL communicator), or a
+        single-rank handle over this rank's rows and all of B (multi=False)."""
+        if multi and ws > 1:
+            uid = broadcast_unique_id(get_unique_id() if rank == 0 else None, ws, rank, dev)
+            return Lrqmm(Mloc, N, K, bits, rank_, p_, q_, rounding, gran, world_size=ws, world_rank=rank,
+                         unique_id=uid, device=local, stream=stream, b_sharded=bsh, qt_terms=qt)
+        return Lrqmm(Mloc, N, K, bits, rank_, p_, q_, rounding, gran, device=local, stream=stream, qt_terms=qt)
 
-        uid = broadcast_unique_id(get_unique_id() if rank == 0 else None, ws, rank, dev)
-    bsh = args.b_sharded and ws > 1
-    h = Lrqmm(Mloc, N, K, bits, r, p, 1, "floor", "row", world_size=ws, world_rank=rank, unique_id=uid,
-              device=local, stream=stream, enable_timing=False, b_sharded=bsh)
-    Bt_mine = Bt[h.b_rows[0]:h.b_rows[1]]  # this rank's rows of B^T (all of them unless --b-sharded)
+    h = handle()
+    Bt_mine = Bt[h.b_rows[0]:h.b_rows[1]]  # this rank's rows of B^T (all of them unless B is sharded)
 
     def step():
         h.quantize(SIDE_A, A)
@@ -470,6 +544,11 @@ def main():
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    # per-step working set (fp32 inputs, codes, residual planes, D); below 2x L2 every timed step is
+    # preceded by a 256 MiB L2 flush (outside the per-step events, which then give the step time)
+    nb_loc = h.b_rows[1] - h.b_rows[0]
+    wset = 4 * (Mloc + nb_loc) * K + 3 * (Mloc + nb_loc) * K + 4 * Mloc * N
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev) if wset < (256 << 20) else None
     h.launch_count(reset=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize(dev)
@@ -477,6 +556,8 @@ def main():
         e0.record(stream)
         for i in range(args.steps):
             ev = evs[i]
+            if flush is not None:
+                flush.fill_(float(i))
             ev[0].record(stream)
             h.quantize(SIDE_A, A)
             h.quantize(SIDE_B, Bt_mine)
@@ -496,94 +577,88 @@ def main():
     per_step = ph.sum(axis=1)  # event-to-event time of each timed step (s)
     step_stats = {"median_ms": float(np.median(per_step)) * 1e3, "min_ms": float(per_step.min()) * 1e3,
                   "max_ms": float(per_step.max()) * 1e3, "steps": int(per_step.size)}
+    if flush is not None:
+        t_step = float(per_step.mean())  # the flushes sit between the per-step events
+    del flush
     t_step = max_over_ranks(t_step, ws, dev)
 
-    # bare int8 GEMM (same tcgen05 kernel, int32 epilogue): the overhead denominator
-    for _ in range(2):
-        h.gemm_int32(Cint)
-    torch.cuda.synchronize(dev)
-    b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    b0.record(stream)
-    for _ in range(args.steps):
-        h.gemm_int32(Cint)
-    b1.record(stream)
-    torch.cuda.synchronize(dev)
-    t_bare = b0.elapsed_time(b1) / 1e3 / args.steps
-
-    # direct-quant pipeline (quantize x2 + dequant GEMM, rank 0)
-    hd = Lrqmm(Mloc, N, K, bits, 0, 0, 1, "floor", "row", device=local, stream=stream)
-    for _ in range(2):
-        hd.quantize(SIDE_A, A); hd.quantize(SIDE_B, Bt); hd.gemm(D)
-    torch.cuda.synchronize(dev)
-    b0.record(stream)
-    for _ in range(args.steps):
-        hd.quantize(SIDE_A, A); hd.quantize(SIDE_B, Bt); hd.gemm(D)
-    b1.record(stream)
-    torch.cuda.synchronize(dev)
-    t_dq = b0.elapsed_time(b1) / 1e3 / args.steps
-    hd.close()
-
-    # static-B (weight-resident): B quantized + RSVD'd once, per call only the A side
-    # (quantize A, rsvd_residual(omega_a), gemm).  Same correction as the full call.
-    t_static = None
-    if ws == 1:
-        h.quantize(SIDE_B, Bt)
-        h.rsvd_residual_b(OmB)
-        def step_static():
-            h.quantize(SIDE_A, A); h.rsvd_residual(OmA); h.gemm(D)
-        for _ in range(3):
-            step_static()
+    def timed(fn, reps, warm=2):
+        for _ in range(warm):
+            fn()
         torch.cuda.synchronize(dev)
+        barrier(ws)
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         b0.record(stream)
-        for _ in range(args.steps):
-            step_static()
+        for _ in range(reps):
+            fn()
         b1.record(stream)
         torch.cuda.synchronize(dev)
-        t_static = b0.elapsed_time(b1) / 1e3 / args.steps
+        return max_over_ranks(b0.elapsed_time(b1) / 1e3 / reps, ws, dev)
 
-    # accuracy on a row sample (exact product in fp64 for 256 rows)
-    errs = {}
+    # bare int8 GEMM of this rank's shard (same tcgen05 kernel, int32 epilogue): the overhead
+    # denominator (slowest rank)
+    t_bare = timed(lambda: h.gemm_int32(Cint), args.steps)
+
+    # direct-quant pipeline (quantize x2 + dequant GEMM, rank 0 correction off), same sharding
+    hd = handle(0, 0)
+    Bt_d = Bt[hd.b_rows[0]:hd.b_rows[1]]
+    t_dq = timed(lambda: (hd.quantize(SIDE_A, A), hd.quantize(SIDE_B, Bt_d), hd.gemm(D)), args.steps)
+    hd.close()
+
+    # static-B (weight-resident): B quantized + RSVD'd once (sharded like the
+    # full call), per call only the A side (quantize A, rsvd_residual(omega_a), gemm)
+    h.quantize(SIDE_B, Bt_mine)
+    h.rsvd_residual_b(OmB)
+    t_static = timed(lambda: (h.quantize(SIDE_A, A), h.rsvd_residual(OmA), h.gemm(D)), args.steps, warm=3)
+
+    # accuracy on a row sample of every rank (exact product in fp64), from a full call on all ranks
+    step()
+    h.sync()
+    torch.cuda.synchronize(dev)
+    rows = torch.arange(0, Mloc, max(1, Mloc // max(1, 256 // ws)), device=dev)[:max(1, 256 // ws)]
+    Cex = A[rows].double() @ Bt.double().T
+    nrm2 = float(torch.linalg.norm(Cex)) ** 2
+
+    def sampled_err():
+        e2, n2 = float(torch.linalg.norm(D[rows].double() - Cex)) ** 2, nrm2
+        if ws > 1:
+            t = torch.tensor([e2, n2], dtype=torch.float64, device=dev)
+            import torch.distributed as dist
+
+            dist.all_reduce(t)
+            e2, n2 = float(t[0]), float(t[1])
+        return (e2 / n2) ** 0.5
+
+    errs = {"lrqmm": sampled_err()}
     q0_variant = None
-    if rank == 0:
-        rows = torch.arange(0, Mloc, max(1, Mloc // 256), device=dev)[:256]
-        Cex = A[rows].double() @ Bt.double().T
-        step()
-        h.sync()
-        nrm = torch.linalg.norm(Cex)
-        errs["lrqmm"] = float(torch.linalg.norm(D[rows].double() - Cex) / nrm)
-        for name, rnd, gran, qt in (("dq_paper_trunc_tensor", "trunc", "tensor", 0), ("dq_nearest_row", "nearest", "row", 0),
-                                    ("dq_floor_row", "floor", "row", 0), ("qt110_trunc_tensor", "trunc", "tensor", 3),
-                                    ("qt111_trunc_tensor", "trunc", "tensor", 4)):
-            with Lrqmm(Mloc, N, K, bits, 0, 0, 1, rnd, gran, device=local, stream=stream, qt_terms=qt) as hq:
-                hq.quantize(SIDE_A, A); hq.quantize(SIDE_B, Bt); hq.gemm(D); hq.sync()
-            errs[name] = float(torch.linalg.norm(D[rows].double() - Cex) / nrm)
-        # labelled variant (reading #30): q = 0 with a structured sketch (first column
-        # all ones): two passes over R plus a codes-only pass instead of q = 1's three R passes
-        if r > 0:
-            OmA1, OmB1 = OmA.clone(), OmB.clone()
-            OmA1[:, 0] = 1.0
-            OmB1[:, 0] = 1.0
-            with Lrqmm(Mloc, N, K, bits, r, p, 0, "floor", "row", device=local, stream=stream) as h0:
-                def step_q0():
-                    h0.quantize(SIDE_A, A); h0.quantize(SIDE_B, Bt); h0.rsvd_residual(OmA1, OmB1); h0.gemm(D)
-                for _ in range(3):
-                    step_q0()
-                h0.sync()
-                q0s, q0e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                q0s.record(stream)
-                for _ in range(args.steps):
-                    step_q0()
-                q0e.record(stream)
-                h0.sync()
-                t_q0 = q0s.elapsed_time(q0e) / 1e3 / args.steps
-                errs["lrqmm_q0_ones_sketch"] = float(torch.linalg.norm(D[rows].double() - Cex) / nrm)
-                q0_variant = {"ms_per_step": t_q0 * 1e3, "value": 2.0 * Mloc * N * K / t_q0 / 1e12, "unit": "TOPS",
-                              "note": "power_iters=0 + Omega[:,0]=1 (SURVEY f4 / E3 (c), reading #30): labelled variant, "
-                                      "not the paper's q; error in rel_fro_error.lrqmm_q0_ones_sketch"}
-        del Cex
+    for name, rnd, gran, qt in (("dq_paper_trunc_tensor", "trunc", "tensor", 0), ("dq_nearest_row", "nearest", "row", 0),
+                                ("dq_floor_row", "floor", "row", 0), ("qt110_trunc_tensor", "trunc", "tensor", 3),
+                                ("qt111_trunc_tensor", "trunc", "tensor", 4)):
+        # per-tensor scales and QT are single-rank configurations: rank-local handles over this rank's
+        # rows and all of B (per-tensor: the rank's A shard max)
+        with handle(0, 0, 1, rnd, gran, qt, multi=(gran == "row" and qt == 0)) as hq:
+            Bq = Bt[hq.b_rows[0]:hq.b_rows[1]]
+            hq.quantize(SIDE_A, A); hq.quantize(SIDE_B, Bq); hq.gemm(D); hq.sync()
+        errs[name] = sampled_err()
+    # labelled variant (reading #30): q = 0 with a structured sketch (first column all
+    # ones): two passes over R plus a codes-only pass instead of q = 1's three R passes
+    if r > 0:
+        OmA1, OmB1 = OmA.clone(), OmB.clone()
+        OmA1[:, 0] = 1.0
+        OmB1[:, 0] = 1.0
+        with handle(r, p, 0) as h0:
+            B0 = Bt[h0.b_rows[0]:h0.b_rows[1]]
+            t_q0 = timed(lambda: (h0.quantize(SIDE_A, A), h0.quantize(SIDE_B, B0), h0.rsvd_residual(OmA1, OmB1),
+                                  h0.gemm(D)), args.steps, warm=3)
+            h0.sync()
+            errs["lrqmm_q0_ones_sketch"] = sampled_err()
+            q0_variant = {"ms_per_step": t_q0 * 1e3, "value": 2.0 * M * N * K / t_q0 / 1e12, "unit": "TOPS",
+                          "note": "power_iters=0 + Omega[:,0]=1 (SURVEY f4 / E3 (c), reading #30): labelled variant, "
+                                  "not the paper's q; error in rel_fro_error.lrqmm_q0_ones_sketch"}
+    del Cex
 
-    # end to end through the C ABI with pinned HOST buffers: every rank runs lrqmm_run_host on its
-    # own A block (H2D of A, B^T, Omega; full hot path; D2H of D); max over ranks of host wall time
+    # end to end through the C ABI with pinned HOST buffers: every rank runs lrqmm_run_host_async on
+    # its own shard (H2D of A rows, B^T rows, Omega; full hot path; D2H of D rows); max over ranks
     e2e = None
     if not args.no_e2e:
         hA = torch.empty((Mloc, K), dtype=torch.float32, pin_memory=True)
@@ -605,12 +680,15 @@ def main():
         t_e2e = max_over_ranks(t_e2e, ws, dev)
         h2d = 4 * (Mloc * K + Bt_mine.shape[0] * K + 2 * K * kk)
         d2h = 4 * Mloc * N
-        e2e = {"value": 2.0 * Mloc * ws * N * K / t_e2e / 1e12, "unit": "TOPS", "h2d_bytes_per_step": h2d * ws,
-               "d2h_bytes_per_step": d2h * ws, "ms_per_step": t_e2e * 1e3,
-               "note": "lrqmm_run_host_async (a stream of calls, synced at the end): pinned host A, B^T, Omega -> "
-                       "device, full hot path, D -> host every step; "
-                       "host wall clock, max over ranks"}
         del hA, hB, hD
+        ctx = pcie_context(dev, h2d, d2h)
+        e2e = {"value": 2.0 * M * N * K / t_e2e / 1e12, "unit": "TOPS", "h2d_bytes_per_step": h2d * ws,
+               "d2h_bytes_per_step": d2h * ws, "ms_per_step": t_e2e * 1e3,
+               "pcie": ctx,
+               "pcie_bound_ms": (h2d / ctx["h2d_gbs"] / 1e6) if ctx.get("h2d_gbs") else None,
+               "note": "lrqmm_run_host_async (a stream of calls, synced at the end): pinned host A, B^T, Omega -> "
+                       "device, full hot path, D -> host every step; host wall clock, max over ranks; "
+                       "pcie = this box's measured pinned copy rates and NUMA placement (the e2e bound)"}
 
     h.close()
     if rank != 0:
@@ -620,8 +698,7 @@ def main():
             dist.destroy_process_group()
         return
 
-    Mtot = Mloc * ws
-    ops = 2.0 * Mtot * N * K
+    ops = 2.0 * M * N * K
     peaks, peak_src = load_peaks()
     # int8 dense = 2 x the measured bf16 BURST figure (guide nominal ratio 4.5 / 2.25).  The GEMM runs
     # inside a long step, but the bf16 "sustained" figure is a power-capped clock (~1.24 GHz) that
@@ -629,13 +706,15 @@ def main():
     # figure is the larger, conservative denominator.
     int8_peak = 2.0 * float(peaks["bf16_tflops"])
     gemm_tops = 2.0 * Mloc * N * K / t_gemm / 1e12
-    traffic = None
+    traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", "gemm_ncu_summary.json")
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            if pj.get("config") == args.config:
+            if pj.get("config") == args.config and ws == 1:
                 traffic = pj.get("dram_bytes_per_launch")
+                traffic_src = (f"profiles/gemm_ncu_summary.json: one ncu --set full capture of this kernel at this "
+                               f"config ({pj.get('captured', 'round 1')}), not measured in this run")
         except Exception:
             traffic = None
 
@@ -648,6 +727,7 @@ def main():
                          f"incl. full quantize + RSVD of B; {dt:.1f} s",
                "phases_s": {k: round(v, 4) for k, v in phases.items()}}
 
+    nb = h.b_rows[1] - h.b_rows[0]
     line = {
         "metric": METRIC,
         "value": ops / t_step / 1e12,
@@ -657,13 +737,15 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": t_step * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "int8",
         "data": "synthetic",
-        "config": {"workload": label, "M": Mtot, "M_per_gpu": Mloc, "N": N, "K": K, "bits": bits, "rank": r,
+        "config": {"workload": label, "M": M, "M_per_gpu": Mloc, "N": N, "K": K, "bits": bits, "rank": r,
                    "oversample": p, "power_iters": 1, "rounding": "floor", "scales": "per-row A / per-col B",
-                   "l2": "inputs 2 GiB fp32/GPU > 126 MB L2 (no flush)",
+                   "l2": (f"per-step working set {wset / 2**20:.0f} MiB/GPU (fp32 inputs, codes, residual planes, D) "
+                          + ("> 2x the 126 MB L2: no flush" if wset >= (256 << 20) else
+                             "< 2x L2: a 256 MiB L2 flush before every timed step, outside its events")),
                    "parallelism": (f"row-shard A x{ws}, B column-sharded x{ws} (allgather)" if bsh else
                                    f"row-shard A x{ws}, B replicated") if ws > 1 else "single GPU"},
         "overhead_vs_bare_int8": t_step / t_bare,
@@ -671,34 +753,36 @@ def main():
         "step_stats": step_stats,
         "ms": {"bare_int8_gemm": t_bare * 1e3, "direct_quant_pipeline": t_dq * 1e3, "quantize_AB": t_quant * 1e3,
                "rsvd_residual": t_rsvd * 1e3, "gemm_fused_epilogue": t_gemm * 1e3},
-        "bare_int8_tops": 2.0 * Mloc * N * K / t_bare / 1e12,
+        "bare_int8_tops": ops / t_bare / 1e12,
         "variant_q0_ones_sketch": q0_variant,
-        "static_b": None if t_static is None else {
+        "static_b": {
             "ms_per_step": t_static * 1e3, "value": ops / t_static / 1e12, "unit": "TOPS",
             "overhead_vs_bare_int8": t_static / t_bare,
             "note": "weight-resident B (lrqmm_rsvd_residual_b once); per call: quantize A, rsvd_residual(omega_a), gemm"},
         "rel_fro_error": errs,
+        "rel_fro_error_note": (f"{len(rows)} sampled rows per rank vs the fp64 product of the fp32 inputs" +
+                               ("; dq_paper_trunc_tensor / qt* use rank-local single-GPU handles" if ws > 1 else "")),
         "roofline": {"bound": "tensor",
                      "kernel": ("k7_gemm_i8_2sm (CTA-pair tcgen05.mma.cta_group::2 kind::i8 + fused LRQMM epilogue)"
                                 if Mloc >= 512 and N >= 512 and ((Mloc + 255) // 256) * ((N + 255) // 256) >= 512
                                 else "k6_gemm_i8 (tcgen05 kind::i8 + fused LRQMM epilogue)"),  # gemm_i8.cu use_pair rule
                      "achieved": gemm_tops, "peak": int8_peak, "unit": "TFLOP/s", "frac": gemm_tops / int8_peak,
-                     "traffic": traffic,
+                     "traffic": traffic, "traffic_source": traffic_src,
                      "peak_note": f"int8 dense = 2 x {peak_src} bf16 burst ({peaks['bf16_tflops']} TFLOP/s; guide nominal "
                                   "ratio 4.5/2.25); the bf16 sustained figure is power-capped below this "
                                   "kernel's clock"},
         "hbm_roofline": {
             "peak_gbs": hbm_peak(), "peak_note": "MEASURED_PEAKS.json hbm_gbs (copy)",
-            "quantize_AB": {"bytes": hbm_bytes_quantize(Mloc, K, r > 0) + hbm_bytes_quantize(N, K, r > 0),
-                            "gbs": (hbm_bytes_quantize(Mloc, K, r > 0) + hbm_bytes_quantize(N, K, r > 0)) / t_quant / 1e9},
-            "rsvd_residual": {"bytes": hbm_bytes_rsvd(Mloc, K) + hbm_bytes_rsvd(N, K),
-                              "gbs": (hbm_bytes_rsvd(Mloc, K) + hbm_bytes_rsvd(N, K)) / t_rsvd / 1e9},
+            "quantize_AB": {"bytes": hbm_bytes_quantize(Mloc, K, r > 0) + hbm_bytes_quantize(nb, K, r > 0),
+                            "gbs": (hbm_bytes_quantize(Mloc, K, r > 0) + hbm_bytes_quantize(nb, K, r > 0)) / t_quant / 1e9},
+            "rsvd_residual": {"bytes": hbm_bytes_rsvd(Mloc, K) + hbm_bytes_rsvd(nb, K),
+                              "gbs": (hbm_bytes_rsvd(Mloc, K) + hbm_bytes_rsvd(nb, K)) / t_rsvd / 1e9},
         },
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    for ph in ("quantize_AB", "rsvd_residual"):
-        line["hbm_roofline"][ph]["frac"] = line["hbm_roofline"][ph]["gbs"] / line["hbm_roofline"]["peak_gbs"]
+    for ph_ in ("quantize_AB", "rsvd_residual"):
+        line["hbm_roofline"][ph_]["frac"] = line["hbm_roofline"][ph_]["gbs"] / line["hbm_roofline"]["peak_gbs"]
     if cpu:
         line["cpu_baseline"] = cpu
     if e2e:

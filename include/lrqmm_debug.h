@@ -34,6 +34,19 @@ lrqmm_status_t lrqmm_debug_set_gemm_variant(int variant);
  *   op 3, 4: as ops 1, 2 through the fused Gram + solve kernel the RSVD runs        */
 lrqmm_status_t lrqmm_debug_small(int op, const float* Y, int64_t n, int W, int r, double* G, float* T, void* stream);
 
+/* Test transport for the row-sharded path on ONE GPU: creates a handle exactly
+ * like lrqmm_create (cfg.world_size > 1, cfg.world_rank, cfg.b_sharded as documented there;
+ * cfg.nccl_unique_id is ignored) whose collectives -- the fp64 Gram and Z allreduces and the B
+ * allgathers -- run over a process-local "loopback" group instead of NCCL: every rank of `group`
+ * is a handle of this process on the same cfg.device, driven by its own host thread (and stream).
+ * Each collective synchronises the rank's stream, meets the other ranks at a host barrier (120 s
+ * timeout -> LRQMM_ERR_NCCL, sticky), sums / copies the peers' buffers in rank order on its own
+ * stream, and meets them again; no kernel waits on another rank.  The sharded schedule, buffers
+ * and kernels are the product's; only the transport differs.  Multi-rank loopback handles run
+ * the RSVD eagerly (no CUDA graph).  Errors: as lrqmm_create; INVALID_ARGUMENT if the group
+ * already holds world_size handles or another world_size / device. */
+lrqmm_status_t lrqmm_debug_create_loopback(const lrqmm_config_t* cfg, int group, lrqmm_handle_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,8 +20,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "liblrqmm.so")
-SOURCES = ["quantize.cu", "skinny.cu", "skinny_tc.cu", "smallsolve2.cu", "gemm_i8.cu", "lrqmm_api.cu"]
-HEADERS = ["common.cuh", "kernels.h"]
+SOURCES = ["quantize.cu", "skinny.cu", "skinny_tc.cu", "smallsolve2.cu", "gemm_i8.cu", "comm.cu", "lrqmm_api.cu"]
+HEADERS = ["common.cuh", "kernels.h", "comm.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

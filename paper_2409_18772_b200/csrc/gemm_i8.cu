@@ -763,11 +763,8 @@ static void launch_t(G6Params p, const CUtensorMap* mA, const CUtensorMap* mB, i
   constexpr int kSmem = g6::smem_bytes(kR2, BN);
   static_assert(kSmem <= 232448, "shared memory budget");
   static_assert(g6::stages_for(kR2, BN) >= 3, "stages");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k6_gemm_i8<kR2, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0};
+  ensure_smem(k6_gemm_i8<kR2, BN>, kSmem, attr);
   p.num_n = (int)((p.N + BN - 1) / BN);
   const int tiles = p.num_m * p.num_n;
   const int grid = tiles < nsm ? tiles : nsm;
@@ -787,11 +784,8 @@ static void launch_t7(G6Params p, const CUtensorMap* mA, const CUtensorMap* mB, 
   constexpr int kSmem = g7::smem_bytes(kR2);
   static_assert(kSmem <= 232448, "shared memory budget");
   static_assert(g7::stages_for(kR2) >= 3, "stages");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k7_gemm_i8_2sm<kR2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0};
+  ensure_smem(k7_gemm_i8_2sm<kR2>, kSmem, attr);
   p.num_m = (int)((p.M + 2 * g7::BM - 1) / (2 * g7::BM));
   p.num_n = (int)((p.N + g7::BN - 1) / g7::BN);
   const int tiles = p.num_m * p.num_n;
@@ -814,8 +808,8 @@ static void launch_t7(G6Params p, const CUtensorMap* mA, const CUtensorMap* mB, 
   k7_gemm_i8_2sm<kR2><<<2 * pairs, g7::kThreads, kSmem, st>>>(*mA, *mB, p); ++launch_counter();
 }
 
-void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStream_t st) {
-  if (g.M == 0 || g.N == 0) return;
+int launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStream_t st) {
+  if (g.M == 0 || g.N == 0) return 0;
   G6Params p;
   p.M = g.M;
   p.N = g.N;
@@ -854,9 +848,9 @@ void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStre
       case 48: launch_t7<48>(p, mA + 1, mB + 1, nsm, st); break;
       case 56: launch_t7<56>(p, mA + 1, mB + 1, nsm, st); break;
       case 64: launch_t7<64>(p, mA + 1, mB + 1, nsm, st); break;
-      default: break;
+      default: return 1;  // correction width not instantiated (the API validates 2r <= 64)
     }
-    return;
+    return 0;
   }
   (void)grid;
   switch (r2) {
@@ -869,8 +863,9 @@ void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStre
     case 48: launch_k6<48>(p, mA, mB, nsm, st); break;
     case 56: launch_k6<56>(p, mA, mB, nsm, st); break;
     case 64: launch_k6<64>(p, mA, mB, nsm, st); break;
-    default: break;
+    default: return 1;
   }
+  return 0;
 }
 
 }  // namespace lrqmm

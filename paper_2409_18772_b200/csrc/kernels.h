@@ -1,5 +1,6 @@
 // Host-side launch interfaces of the liblrqmm kernels (internal; not part of the C ABI).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cstdlib>
@@ -7,10 +8,49 @@
 
 namespace lrqmm {
 
-// number of kernels this library has launched (gpu_launches evidence for the bench)
+// Kernel launches are counted per handle (gpu_launches evidence for the bench): every C-ABI entry
+// point that launches installs its handle's counter for the calling thread (CounterScope), and the
+// launchers increment launch_counter().  Launches outside any handle (test hooks) go to a
+// thread-local fallback.
+inline int64_t*& launch_counter_slot() {
+  static thread_local int64_t* p = nullptr;
+  return p;
+}
 inline int64_t& launch_counter() {
-  static int64_t c = 0;
-  return c;
+  static thread_local int64_t fallback = 0;
+  int64_t* p = launch_counter_slot();
+  return p ? *p : fallback;
+}
+struct CounterScope {
+  int64_t* prev;
+  explicit CounterScope(int64_t* c) : prev(launch_counter_slot()) { launch_counter_slot() = c; }
+  ~CounterScope() { launch_counter_slot() = prev; }
+};
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies to the CURRENT device's copy of the
+// kernel: remember it per device ordinal (bit d of `done`), set before the bit is published.
+template <typename K>
+inline void ensure_smem(K* kernel, int bytes, std::atomic<unsigned>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned bit = 1u << (dev & 31);
+  if (!(done.load(std::memory_order_acquire) & bit)) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done.fetch_or(bit, std::memory_order_release);
+  }
+}
+// SM count of the current device (cached per ordinal)
+inline int sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int v = cache[dev & 63].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+    cache[dev & 63].store(v, std::memory_order_relaxed);
+  }
+  return v;
 }
 
 // PDL on (LRQMM_NO_PDL unset): eager launches made through launch_pdl() carry
@@ -241,7 +281,8 @@ int encode_map_2d_sw(void* map, int dtype, const void* base, uint64_t inner, uin
 void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t st);
 // Omega -> zero-padded K x W copy + column maxima of |Omega| (skinny.cu)
 void launch_copy_omega(const float* src, int64_t ldo, int kk, int64_t K, int W, float* dst, unsigned* cmax,
-                       cudaStream_t st);
-void launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStream_t st);
+                       int* err_flag, cudaStream_t st);  // err_flag bit 0: non-finite Omega
+// 0 on success, 1 if the correction width R2 has no instantiation (nothing launched)
+int launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStream_t st);
 
 }  // namespace lrqmm

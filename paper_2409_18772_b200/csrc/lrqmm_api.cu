@@ -12,6 +12,7 @@
 #include <new>
 
 #include "../../include/lrqmm.h"
+#include "comm.h"
 #include "kernels.h"
 
 using namespace lrqmm;
@@ -74,7 +75,8 @@ struct lrqmm_handle_s {
   alignas(64) CUtensorMap mapRA[4];  // QT: maps of the residual codes
   alignas(64) CUtensorMap mapRB[4];
   cudaEvent_t ev[8] = {};
-  ncclComm_t comm = nullptr;
+  Comm* comm = nullptr;   // world_size > 1: NCCL, or the test loopback (lrqmm_debug_create_loopback)
+  int64_t launches = 0;   // kernels this handle enqueued (lrqmm_launch_count)
   // B column-sharded over the ranks (cfg.b_sharded): this rank owns rows
   // [b_lo, b_lo + s[1].rows) of B^T inside blocks of b_blk rows; s[1].codes / lam / inv_lam and LB
   // point at the rank's slice of the full (ws * b_blk row) buffers below, which the GEMM reads
@@ -168,7 +170,7 @@ lrqmm_status_t lrqmm_get_unique_id(unsigned char out[128]) {
   return LRQMM_OK;
 }
 
-static lrqmm_status_t validate(const lrqmm_config_t* c) {
+static lrqmm_status_t validate(const lrqmm_config_t* c, bool loopback) {
   if (!c) return LRQMM_ERR_INVALID_ARGUMENT;
   if (c->m < 0 || c->n < 0 || c->k < 0) return LRQMM_ERR_SHAPE;
   if (c->k > INT32_MAX - 256 || c->n > INT32_MAX || c->m > ((int64_t)1 << 40)) return LRQMM_ERR_SHAPE;
@@ -177,7 +179,7 @@ static lrqmm_status_t validate(const lrqmm_config_t* c) {
   if (c->granularity < 0 || c->granularity > 1) return LRQMM_ERR_INVALID_ARGUMENT;
   if (c->rank < 0 || c->oversample < 0) return LRQMM_ERR_RANK;
   if (c->world_size < 1 || c->world_rank < 0 || c->world_rank >= c->world_size) return LRQMM_ERR_INVALID_ARGUMENT;
-  if (c->world_size > 1 && !c->nccl_unique_id) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (c->world_size > 1 && !c->nccl_unique_id && !loopback) return LRQMM_ERR_INVALID_ARGUMENT;
   if (c->world_size > 1 && c->granularity == LRQMM_SCALE_PER_TENSOR) return LRQMM_ERR_UNSUPPORTED;
   const int64_t qmax = (1 << (c->bits - 1)) - 1;
   if (c->k * qmax * qmax > (int64_t)INT32_MAX) return LRQMM_ERR_OVERFLOW;  // reading #24
@@ -198,7 +200,12 @@ static lrqmm_status_t validate(const lrqmm_config_t* c) {
 lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   if (!h) return LRQMM_OK;
   cudaSetDevice(h->cfg.device);
-  if (h->st) cudaStreamSynchronize(h->st);
+  // nothing may still read or write the handle's buffers: the handle stream (also the legacy
+  // default stream) and run_host_async's copy streams
+  cudaStreamSynchronize(h->st);
+  if (h->cin) cudaStreamSynchronize(h->cin);
+  if (h->cout) cudaStreamSynchronize(h->cout);
+  if (h->side_st) cudaStreamSynchronize(h->side_st);
   if (h->bsh) {  // side B's codes / scales / LB are slices of the full buffers
     h->s[1].codes = h->codes_b_full;
     h->s[1].lam = h->lam_b_full;
@@ -229,15 +236,16 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   if (h->side_st) cudaStreamDestroy(h->side_st);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
-  if (h->comm) ncclCommDestroy(h->comm);
+  delete h->comm;
   delete h;
   return LRQMM_OK;
 }
 
-lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
+// loopback_group >= 0: test transport (lrqmm_debug_create_loopback) instead of NCCL
+static lrqmm_status_t create_impl(const lrqmm_config_t* cfg, int loopback_group, lrqmm_handle_t* out) {
   if (!out) return LRQMM_ERR_INVALID_ARGUMENT;
   *out = nullptr;
-  lrqmm_status_t v = validate(cfg);
+  lrqmm_status_t v = validate(cfg, loopback_group >= 0);
   if (v != LRQMM_OK) return v;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) return LRQMM_ERR_CUDA;
@@ -337,12 +345,11 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
       }
   }
   if (cfg->world_size > 1) {
-    ncclUniqueId id;
-    memcpy(id.internal, cfg->nccl_unique_id, 128);
-    if (ncclCommInitRank(&h->comm, cfg->world_size, id, cfg->world_rank) != ncclSuccess) {
-      h->comm = nullptr;
+    h->comm = loopback_group >= 0 ? comm_create_loopback(loopback_group, cfg->world_size, cfg->world_rank, cfg->device)
+                                  : comm_create_nccl(cfg->world_size, cfg->world_rank, cfg->nccl_unique_id);
+    if (!h->comm) {
       lrqmm_destroy(h);
-      return LRQMM_ERR_NCCL;
+      return loopback_group >= 0 ? LRQMM_ERR_INVALID_ARGUMENT : LRQMM_ERR_NCCL;
     }
   }
   if (cudaDeviceSynchronize() != cudaSuccess) {
@@ -353,6 +360,8 @@ lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) {
   return LRQMM_OK;
 }
 
+lrqmm_status_t lrqmm_create(const lrqmm_config_t* cfg, lrqmm_handle_t* out) { return create_impl(cfg, -1, out); }
+
 static void record(lrqmm_handle_t h, int i) {
   if (h->cfg.enable_timing) cudaEventRecord(h->ev[i], h->st);
 }
@@ -361,6 +370,7 @@ static lrqmm_status_t allgather_b(lrqmm_handle_t h, void* full, size_t per_row_b
 
 lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* X, int64_t ldx) {
   if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  CounterScope counter_scope(&h->launches);
   if (h->sticky != LRQMM_OK) return h->sticky;
   if (side != LRQMM_SIDE_A && side != LRQMM_SIDE_B) return LRQMM_ERR_INVALID_ARGUMENT;
   Side& s = h->s[side];
@@ -423,6 +433,7 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
 
 lrqmm_status_t lrqmm_quantize_im2col(lrqmm_handle_t h, lrqmm_side_t side, const float* X, const lrqmm_conv_t* cv) {
   if (!h || !cv) return LRQMM_ERR_INVALID_ARGUMENT;
+  CounterScope counter_scope(&h->launches);
   if (h->sticky != LRQMM_OK) return h->sticky;
   if (side != LRQMM_SIDE_A && side != LRQMM_SIDE_B) return LRQMM_ERR_INVALID_ARGUMENT;
   if (h->cfg.granularity == LRQMM_SCALE_PER_TENSOR || h->cfg.qt_terms > 0) return LRQMM_ERR_UNSUPPORTED;
@@ -489,19 +500,17 @@ static SideView view(lrqmm_handle_t h, int sd) {
 // allreduce (sum) of an A-side quantity across the row shards
 static lrqmm_status_t allreduce_f64(lrqmm_handle_t h, double* buf, size_t n) {
   if (h->cfg.world_size == 1) return LRQMM_OK;
-  LQ_NCCL(ncclAllReduce(buf, buf, n, ncclFloat64, ncclSum, h->comm, h->st));
+  if (h->comm->allreduce(buf, n, kCommF64, h->st) != 0) return fail(h, LRQMM_ERR_NCCL);
   return LRQMM_OK;
 }
 static lrqmm_status_t allreduce_f32(lrqmm_handle_t h, float* buf, size_t n) {
   if (h->cfg.world_size == 1) return LRQMM_OK;
-  LQ_NCCL(ncclAllReduce(buf, buf, n, ncclFloat32, ncclSum, h->comm, h->st));
+  if (h->comm->allreduce(buf, n, kCommF32, h->st) != 0) return fail(h, LRQMM_ERR_NCCL);
   return LRQMM_OK;
 }
 // B column-sharded: in-place allgather of the rank blocks (b_blk rows each) of a full-B buffer
 static lrqmm_status_t allgather_b(lrqmm_handle_t h, void* full, size_t per_row_bytes) {
-  const size_t cnt = (size_t)h->b_blk * per_row_bytes;
-  char* base = reinterpret_cast<char*>(full);
-  LQ_NCCL(ncclAllGather(base + cnt * h->cfg.world_rank, base, cnt, ncclInt8, h->comm, h->st));
+  if (h->comm->allgather(full, (size_t)h->b_blk * per_row_bytes, h->st) != 0) return fail(h, LRQMM_ERR_NCCL);
   return LRQMM_OK;
 }
 // side sd's rows are sharded over the ranks (A always when world > 1; B when b_sharded)
@@ -739,7 +748,9 @@ static lrqmm_status_t run_rsvd(lrqmm_handle_t h, int kind) {
   lrqmm_status_t e = LRQMM_OK;
   const bool multi = h->cfg.world_size > 1;
   // graphs: single-rank handles (NCCL collectives stay eagerly enqueued), not disabled by env
-  const bool use_graph = kind != 2 && !h->graph_off && !multi && !getenv("LRQMM_NO_GRAPH");
+  // (NCCL collectives are captured with the kernels; the host-synchronised loopback test transport
+  // keeps multi-rank handles eager)
+  const bool use_graph = kind != 2 && !h->graph_off && (!multi || h->comm->capturable()) && !getenv("LRQMM_NO_GRAPH");
   if (use_graph && h->rsvd_exec[kind]) {
     LQ_CUDA(cudaGraphLaunch(h->rsvd_exec[kind], h->st));
     launch_counter() += h->rsvd_graph_kernels[kind];
@@ -777,12 +788,13 @@ static lrqmm_status_t run_rsvd(lrqmm_handle_t h, int kind) {
 }
 
 static lrqmm_status_t copy_omega(lrqmm_handle_t h, int sd, const float* om, int64_t ldo) {
-  launch_copy_omega(om, ldo, (int)h->kk, h->cfg.k, h->W, h->s[sd].Om, h->s[sd].cmaxOm, h->st);
+  launch_copy_omega(om, ldo, (int)h->kk, h->cfg.k, h->W, h->s[sd].Om, h->s[sd].cmaxOm, h->err_flag, h->st);
   return check_launch(h);
 }
 
 lrqmm_status_t lrqmm_rsvd_residual_b(lrqmm_handle_t h, const float* omegaB, int64_t ldo) {
   if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  CounterScope counter_scope(&h->launches);
   if (h->sticky != LRQMM_OK) return h->sticky;
   if (h->r == 0) return LRQMM_ERR_STATE;
   if (!(h->state & 2)) return LRQMM_ERR_STATE;
@@ -798,6 +810,7 @@ lrqmm_status_t lrqmm_rsvd_residual_b(lrqmm_handle_t h, const float* omegaB, int6
 
 lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const float* omegaB, int64_t ldo) {
   if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  CounterScope counter_scope(&h->launches);
   if (h->sticky != LRQMM_OK) return h->sticky;
   if (h->r == 0) return LRQMM_ERR_STATE;
   if ((h->state & 3) != 3) return LRQMM_ERR_STATE;
@@ -838,12 +851,13 @@ static lrqmm_status_t run_gemm(lrqmm_handle_t h, int epi, float alpha, float bet
   g.Cint = Cint;
   g.ldd = ldd;
   g.sched = h->sched;
-  launch_gemm(g, ra ? h->mapRA : h->mapA, rb ? h->mapRB : h->mapB, h->st);
+  if (launch_gemm(g, ra ? h->mapRA : h->mapA, rb ? h->mapRB : h->mapB, h->st) != 0) return LRQMM_ERR_UNSUPPORTED;
   return check_launch(h);
 }
 
 lrqmm_status_t lrqmm_gemm(lrqmm_handle_t h, float alpha, float beta, float* D, int64_t ldd) {
   if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  CounterScope counter_scope(&h->launches);
   if (h->sticky != LRQMM_OK) return h->sticky;
   if ((h->state & 3) != 3) return LRQMM_ERR_STATE;
   if (h->r > 0 && !(h->state & 4)) return LRQMM_ERR_STATE;
@@ -864,6 +878,7 @@ lrqmm_status_t lrqmm_gemm(lrqmm_handle_t h, float alpha, float beta, float* D, i
 
 lrqmm_status_t lrqmm_gemm_int32(lrqmm_handle_t h, int32_t* Cint, int64_t ldc) {
   if (!h) return LRQMM_ERR_INVALID_ARGUMENT;
+  CounterScope counter_scope(&h->launches);
   if (h->sticky != LRQMM_OK) return h->sticky;
   if ((h->state & 3) != 3) return LRQMM_ERR_STATE;
   if ((!Cint && h->cfg.m > 0 && h->cfg.n > 0) || ldc < h->cfg.n) return LRQMM_ERR_INVALID_ARGUMENT;
@@ -881,10 +896,7 @@ lrqmm_status_t lrqmm_sync(lrqmm_handle_t h) {
   int flag = 0;
   if (cudaMemcpy(&flag, h->err_flag, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return fail(h, LRQMM_ERR_CUDA);
   if (flag & 1) return fail(h, LRQMM_ERR_NONFINITE);
-  if (h->comm) {
-    ncclResult_t ar;
-    if (ncclCommGetAsyncError(h->comm, &ar) != ncclSuccess || ar != ncclSuccess) return fail(h, LRQMM_ERR_NCCL);
-  }
+  if (h->comm && h->comm->async_error() != 0) return fail(h, LRQMM_ERR_NCCL);
   return LRQMM_OK;
 }
 
@@ -995,6 +1007,7 @@ lrqmm_status_t lrqmm_get_correction(lrqmm_handle_t h, lrqmm_side_t side, float* 
 
 lrqmm_status_t lrqmm_get_factors(lrqmm_handle_t h, lrqmm_side_t side, float* USigma, float* V) {
   if (!h || (side != 0 && side != 1) || !USigma || !V) return LRQMM_ERR_INVALID_ARGUMENT;
+  CounterScope counter_scope(&h->launches);
   if (!(h->state & 4)) return LRQMM_ERR_STATE;
   const int64_t rows = h->s[side].rows;
   const int r = h->r;
@@ -1022,9 +1035,9 @@ lrqmm_status_t lrqmm_get_timings(lrqmm_handle_t h, double us[8]) {
 }
 
 int64_t lrqmm_launch_count(lrqmm_handle_t h, int reset) {
-  (void)h;
-  const int64_t c = launch_counter();
-  if (reset) launch_counter() = 0;
+  if (!h) return 0;
+  const int64_t c = h->launches;
+  if (reset) h->launches = 0;
   return c;
 }
 
@@ -1066,6 +1079,11 @@ extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx
   }
   cudaFree(U); cudaFree(lam); cudaFree(inv); cudaFree(codes); cudaFree(flag); cudaFree(partial); cudaFree(img);
   return e == cudaSuccess ? LRQMM_OK : (ok ? LRQMM_ERR_CUDA : LRQMM_ERR_ALLOC);
+}
+
+extern "C" lrqmm_status_t lrqmm_debug_create_loopback(const lrqmm_config_t* cfg, int group, lrqmm_handle_t* out) {
+  if (group < 0) return LRQMM_ERR_INVALID_ARGUMENT;
+  return create_impl(cfg, group, out);
 }
 
 extern "C" lrqmm_status_t lrqmm_debug_set_gemm_variant(int variant) {

@@ -537,12 +537,7 @@ static int64_t launch_k1_rows_tma(const QuantArgs& a, bool fixed, cudaStream_t s
   if (ns > 3) ns = 3;
   if (ns < 2) return 0;
   const int smem = 1024 + ns * slot;
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int nsm = sm_count();
   const int64_t nchunks = rows_full / R;
   const int grid = (int)(nchunks < 2 * nsm ? nchunks : 2 * nsm);
   const bool v4 = a.K % 4 == 0;
@@ -580,12 +575,7 @@ static bool launch_k1_tma_t(const QuantArgs& a, bool fixed, cudaStream_t st) {
   if (ns > 8) ns = 8;
   if (ns < 2) return false;
   const int smem = 1024 + ns * slot;
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int nsm = sm_count();
   const int grid = (int)(a.rows < nsm ? a.rows : nsm);
 #define K1T_LAUNCH(F, M)                                                                                         \
   do {                                                                                                           \

@@ -118,11 +118,8 @@ static int assign_blocks(const int64_t* n, int njobs, int* first) {
 template <int W>
 static void apply_small_t(ApplyJobs& jobs, cudaStream_t st) {
   constexpr int smem = (2 * kApRows * ap_ld(W) + 2 * W * W) * (int)sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_apply_small<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0};
+  ensure_smem(k_apply_small<W>, smem, attr);
   int64_t n[kMaxApply];
   for (int q = 0; q < jobs.n; ++q) n[q] = jobs.j[q].n;
   const int grid = assign_blocks(n, jobs.n, jobs.first);
@@ -216,11 +213,8 @@ __global__ void __launch_bounds__(kApRows) k_apply64(const Apply64Jobs jobs) {
 template <int W>
 static void apply64_t(Apply64Jobs& jobs, cudaStream_t st) {
   constexpr int smem = W * W * (int)sizeof(double) + kApRows * ap_ld(W) * (int)sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_apply64<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0};
+  ensure_smem(k_apply64<W>, smem, attr);
   int64_t n[2] = {jobs.j[0].n, jobs.n > 1 ? jobs.j[1].n : 0};
   const int grid = assign_blocks(n, jobs.n, jobs.first);
   launch_pdl(k_apply64<W>, grid, kApRows, smem, st, jobs);
@@ -243,7 +237,8 @@ void launch_apply64_jobs(const Apply64Jobs& in, int W, cudaStream_t st) {
 // needs no reduction phase of its own.  Thread = (row lane, column c); one atomicMax per column
 // per block (order-independent: deterministic).
 __global__ void __launch_bounds__(256) k_copy_omega(const float* __restrict__ src, int64_t ldo, int kk, int64_t K, int W,
-                                                    float* __restrict__ dst, unsigned* __restrict__ cmax) {
+                                                    float* __restrict__ dst, unsigned* __restrict__ cmax,
+                                                    int* __restrict__ err_flag) {
   ::lrqmm::pdl_enter();
   __shared__ unsigned bm[64];
   if (threadIdx.x < 64) bm[threadIdx.x] = 0u;
@@ -255,6 +250,9 @@ __global__ void __launch_bounds__(256) k_copy_omega(const float* __restrict__ sr
     for (int64_t row = (int64_t)blockIdx.x * rpb + r0; row < K; row += (int64_t)gridDim.x * rpb) {
       const float v = c < kk ? src[row * ldo + c] : 0.f;
       dst[row * W + c] = v;
+      // a NaN (0x7fc00000 > every finite |v| as bits) or Inf would own the column maximum and
+      // corrupt that column's pass image: flagged instead (LRQMM_ERR_NONFINITE at lrqmm_sync)
+      if (!isfinite(v)) atomicOr(err_flag, 1);
       m = max(m, __float_as_uint(fabsf(v)));
     }
   if (r0 < rpb && m) atomicMax(&bm[c], m);
@@ -263,13 +261,13 @@ __global__ void __launch_bounds__(256) k_copy_omega(const float* __restrict__ sr
 }
 
 void launch_copy_omega(const float* src, int64_t ldo, int kk, int64_t K, int W, float* dst, unsigned* cmax,
-                       cudaStream_t st) {
+                       int* err_flag, cudaStream_t st) {
   cudaMemsetAsync(cmax, 0, 64 * sizeof(unsigned), st);
   if (K == 0 || W == 0) return;
   const int rpb = 256 / W;
   int64_t g = (K + rpb - 1) / rpb;
   if (g > 148 * 4) g = 148 * 4;
-  launch_pdl(k_copy_omega, (int)g, 256, 0, st, src, ldo, kk, K, W, dst, cmax);
+  launch_pdl(k_copy_omega, (int)g, 256, 0, st, src, ldo, kk, K, W, dst, cmax, err_flag);
   ++launch_counter();
 }
 

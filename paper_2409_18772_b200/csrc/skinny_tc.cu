@@ -555,14 +555,15 @@ int64_t tc_img_bytes(int64_t n, int W) {
 
 template <int NA>
 static void launch_prep(PrepJobs& jb, cudaStream_t st) {
-  static int grid = 0, nsm = 148;
-  if (!grid) {
-    int dev = 0, per = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = sm_count();
+  static std::atomic<int> per_sm{0};  // co-resident blocks of the cooperative form (same on every B200)
+  int per = per_sm.load(std::memory_order_relaxed);
+  if (per <= 0) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_prep_img<NA, false>, 256, 0);
-    grid = nsm * (per < 4 ? (per < 1 ? 1 : per) : 4);
+    per = per < 4 ? (per < 1 ? 1 : per) : 4;
+    per_sm.store(per, std::memory_order_relaxed);
   }
+  const int grid = nsm * per;
   bool have = true;
   int64_t work = 0;
   for (int q = 0; q < jb.njobs; ++q) {
@@ -589,11 +590,8 @@ static void run_tc(int nsides, const TcPassSide* sides, int W, bool reduce1, int
   using namespace tcp;
   using C = Cfg<kMode, NA, kVar>;
   constexpr bool kHasU = C::kHasU, kHasC = C::kHasC;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_tc_proj<kMode, NA, kVar>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0};
+  ensure_smem(k_tc_proj<kMode, NA, kVar>, C::kSmem, attr);
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

@@ -243,11 +243,8 @@ static void chol_t(const EigJobs& jobs, cudaStream_t st) {
   if constexpr (n <= 32) {
     launch_pdl(k_warp_chol<n>, jobs.n, 32, 0, st, jobs);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_chol_orth<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
-      attr = true;
-    }
+    static std::atomic<unsigned> attr{0};
+    ensure_smem(k_chol_orth<n>, kDynSmem, attr);
     launch_pdl(k_chol_orth<n>, jobs.n, 256, kDynSmem, st, jobs);
   }
 }
@@ -470,11 +467,8 @@ __global__ void __launch_bounds__(256) k_eig(EigJobs jobs) {
 template <int n>
 static void eig_t(const EigJobs& jobs, cudaStream_t st) {
   constexpr int smem = eig_smem_bytes(n) > kDynSmem ? eig_smem_bytes(n) : kDynSmem;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_eig<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0};
+  ensure_smem(k_eig<n>, smem, attr);
   launch_pdl(k_eig<n>, jobs.n, 256, smem, st, jobs);
 }
 
@@ -739,11 +733,8 @@ static void fused_t(const SmallJobs& jobs, int mode, int64_t nb, cudaStream_t st
   // the truncation (mode 1) of the widest sketches needs more than the Y staging buffers
   constexpr int big = eig_smem_bytes(W) > kDynSmem ? eig_smem_bytes(W) : kDynSmem;
   const int smem = mode == 1 ? big : kDynSmem;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_fused_small<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0};
+  ensure_smem(k_fused_small<W>, big, attr);
   launch_pdl(k_fused_small<W>, dim3((unsigned)nb, (unsigned)jobs.n), 256, smem, st, jobs, mode);
 }
 

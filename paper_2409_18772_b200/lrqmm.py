@@ -34,7 +34,8 @@ EXPORTS = (
     "lrqmm_get_timings", "lrqmm_launch_count", "lrqmm_status_string", "lrqmm_rsvd_residual_b",
     "lrqmm_quantize_im2col", "lrqmm_run_host_async",
 )
-DEBUG_EXPORTS = ("lrqmm_debug_proj", "lrqmm_debug_small", "lrqmm_debug_set_gemm_variant")
+DEBUG_EXPORTS = ("lrqmm_debug_proj", "lrqmm_debug_small", "lrqmm_debug_set_gemm_variant",
+                 "lrqmm_debug_create_loopback")
 
 
 class LrqmmError(RuntimeError):
@@ -100,6 +101,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lrqmm_debug_proj": (I, [I, P, I64, I64, I, I, I, P, P, I, P, P, P]),
         "lrqmm_debug_small": (I, [I, P, I64, I, I, P, P, P]),
         "lrqmm_debug_set_gemm_variant": (I, [I]),
+        "lrqmm_debug_create_loopback": (I, [ctypes.POINTER(Config), I, ctypes.POINTER(P)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -133,9 +135,34 @@ def _arg(t, dtype: str, device: int, name: str) -> int:
     return int(t.data_ptr())
 
 
-def _ld(t) -> int:
-    assert t.dim() == 2 and t.stride(1) == 1, "row-major with unit column stride expected"
-    return int(t.stride(0))
+def _mat(t, dtype: str, device: int, name: str, rows: int, cols: int):
+    """(pointer, ld) of a row-major rows x cols operand (a view of a larger tensor is fine): checks
+    device and dtype (_arg), two dimensions, unit column stride and at least rows x cols elements,
+    so the kernels never read or write past the caller's tensor."""
+    if t is None:
+        return 0, max(cols, 1)
+    ptr = _arg(t, dtype, device, name)
+    if t.dim() != 2:
+        raise ValueError(f"{name}: expected a 2-D tensor, got {t.dim()}-D")
+    if t.shape[0] < rows or t.shape[1] < cols:
+        raise ValueError(f"{name}: expected at least {rows} x {cols}, got {tuple(t.shape)}")
+    if t.shape[1] > 1 and t.stride(1) != 1:
+        raise ValueError(f"{name}: row-major with unit column stride expected (strides {t.stride()})")
+    ld = int(t.stride(0)) if t.shape[0] > 1 else max(int(t.shape[1]), 1)
+    if ld < cols:
+        raise ValueError(f"{name}: row stride {ld} < {cols} columns")
+    return ptr, ld
+
+
+def _host(a, name: str, shape):
+    """Host pointer of a C-contiguous float32 NumPy array of exactly `shape` (run_host*)."""
+    if a is None:
+        return None
+    if not isinstance(a, np.ndarray) or a.dtype != np.float32 or not a.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"{name}: expected a C-contiguous float32 numpy array")
+    if tuple(a.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {a.shape}")
+    return ctypes.c_void_p(a.ctypes.data)
 
 
 def get_unique_id() -> bytes:
@@ -152,7 +179,9 @@ class Lrqmm:
                  power_iters: int = 1, rounding: str = "floor", granularity: str = "row",
                  world_size: int = 1, world_rank: int = 0, unique_id: bytes | None = None,
                  device: int = 0, stream=None, enable_timing: bool = False, qt_terms: int = 0,
-                 b_sharded: bool = False):
+                 b_sharded: bool = False, loopback_group: int | None = None):
+        """loopback_group: test transport (include/lrqmm_debug.h lrqmm_debug_create_loopback) --
+        world_size handles of this process, one host thread each, on one device, instead of NCCL."""
         import torch
 
         lib = load_library()
@@ -173,14 +202,24 @@ class Lrqmm:
                      device, ctypes.c_void_p(stream.cuda_stream), 1 if enable_timing else 0, qt_terms,
                      1 if b_sharded else 0)
         h = ctypes.c_void_p()
-        _check(lib.lrqmm_create(ctypes.byref(cfg), ctypes.byref(h)), "lrqmm_create")
+        if loopback_group is None:
+            _check(lib.lrqmm_create(ctypes.byref(cfg), ctypes.byref(h)), "lrqmm_create")
+        else:
+            _check(lib.lrqmm_debug_create_loopback(ctypes.byref(cfg), int(loopback_group), ctypes.byref(h)),
+                   "lrqmm_debug_create_loopback")
+        self.kk = rank + oversample if rank > 0 else 0
         self.h = h
         self._keep = {}
 
     # ---- the five calls of the boundary ----
+    def side_rows(self, side: int) -> int:
+        """Rows of the side's matrix on this rank: m for A, this rank's rows of B^T for B."""
+        return self.m if side == SIDE_A else self.b_rows[1] - self.b_rows[0]
+
     def quantize(self, side: int, X):
         """X: float32 cuda tensor (rows x k), any row stride."""
-        _check(self.lib.lrqmm_quantize(self.h, side, _arg(X, "float32", self.device, "X"), _ld(X)), "lrqmm_quantize")
+        ptr, ld = _mat(X, "float32", self.device, "X", self.side_rows(side), self.k)
+        _check(self.lib.lrqmm_quantize(self.h, side, ptr, ld), "lrqmm_quantize")
 
     def quantize_im2col(self, side: int, X, kh: int, kw: int, stride=1, pad=0, dilation=1):
         """X: float32 cuda tensor [batch, H, W, C] (NHWC, dense); the side's matrix is its im2col
@@ -188,25 +227,28 @@ class Lrqmm:
         st = stride if isinstance(stride, tuple) else (stride, stride)
         pd = pad if isinstance(pad, tuple) else (pad, pad)
         dl = dilation if isinstance(dilation, tuple) else (dilation, dilation)
-        assert X.dim() == 4 and X.is_contiguous()
+        if X.dim() != 4 or not X.is_contiguous():
+            raise ValueError("X: expected a contiguous 4-D NHWC tensor")
         g = ConvGeom(X.shape[0], X.shape[1], X.shape[2], X.shape[3], kh, kw, st[0], st[1], pd[0], pd[1], dl[0], dl[1])
         _check(self.lib.lrqmm_quantize_im2col(self.h, side, _arg(X, "float32", self.device, "X"), ctypes.byref(g)),
                "lrqmm_quantize_im2col")
 
     def rsvd_residual(self, omega_a, omega_b=None):
         """omega_b None: static-B mode (B's factors from rsvd_residual_b / the last full call)."""
-        assert omega_b is None or omega_a.stride(0) == omega_b.stride(0)
-        _check(self.lib.lrqmm_rsvd_residual(self.h, _arg(omega_a, "float32", self.device, "omega_a"),
-                                            _arg(omega_b, "float32", self.device, "omega_b"), _ld(omega_a)),
-               "lrqmm_rsvd_residual")
+        pa, lda = _mat(omega_a, "float32", self.device, "omega_a", self.k, self.kk)
+        pb, ldb = _mat(omega_b, "float32", self.device, "omega_b", self.k, self.kk)
+        if omega_b is not None and ldb != lda:
+            raise ValueError("omega_a and omega_b must share one row stride")
+        _check(self.lib.lrqmm_rsvd_residual(self.h, pa, pb, lda), "lrqmm_rsvd_residual")
 
     def rsvd_residual_b(self, omega_b):
         """Static-B preparation: B's RSVD once, resident until B is quantized again."""
-        _check(self.lib.lrqmm_rsvd_residual_b(self.h, _arg(omega_b, "float32", self.device, "omega_b"), _ld(omega_b)),
-               "lrqmm_rsvd_residual_b")
+        pb, ldb = _mat(omega_b, "float32", self.device, "omega_b", self.k, self.kk)
+        _check(self.lib.lrqmm_rsvd_residual_b(self.h, pb, ldb), "lrqmm_rsvd_residual_b")
 
     def gemm(self, D, alpha: float = 1.0, beta: float = 0.0):
-        _check(self.lib.lrqmm_gemm(self.h, alpha, beta, _arg(D, "float32", self.device, "D"), _ld(D)), "lrqmm_gemm")
+        ptr, ld = _mat(D, "float32", self.device, "D", self.m, self.n)
+        _check(self.lib.lrqmm_gemm(self.h, alpha, beta, ptr, ld), "lrqmm_gemm")
         return D
 
     def close(self):
@@ -231,13 +273,14 @@ class Lrqmm:
         _check(self.lib.lrqmm_sync(self.h), "lrqmm_sync")
 
     def gemm_int32(self, C):
-        _check(self.lib.lrqmm_gemm_int32(self.h, _arg(C, "int32", self.device, "C"), _ld(C)), "lrqmm_gemm_int32")
+        ptr, ld = _mat(C, "int32", self.device, "C", self.m, self.n)
+        _check(self.lib.lrqmm_gemm_int32(self.h, ptr, ld), "lrqmm_gemm_int32")
         return C
 
     def codes(self, side: int):
         import torch
 
-        rows = self.m if side == SIDE_A else self.n
+        rows = self.side_rows(side)
         out = torch.empty((rows, self.k), dtype=torch.int8, device=f"cuda:{self.device}")
         _check(self.lib.lrqmm_get_codes(self.h, side, _ptr(out), self.k), "lrqmm_get_codes")
         return out
@@ -245,7 +288,7 @@ class Lrqmm:
     def scales(self, side: int):
         import torch
 
-        rows = self.m if side == SIDE_A else self.n
+        rows = self.side_rows(side)
         out = torch.empty((rows,), dtype=torch.float32, device=f"cuda:{self.device}")
         _check(self.lib.lrqmm_get_scales(self.h, side, _ptr(out)), "lrqmm_get_scales")
         return out
@@ -253,7 +296,7 @@ class Lrqmm:
     def factors(self, side: int):
         import torch
 
-        rows = self.m if side == SIDE_A else self.n
+        rows = self.side_rows(side)
         us = torch.empty((rows, self.rank), dtype=torch.float32, device=f"cuda:{self.device}")
         v = torch.empty((self.k, self.rank), dtype=torch.float32, device=f"cuda:{self.device}")
         _check(self.lib.lrqmm_get_factors(self.h, side, _ptr(us), _ptr(v)), "lrqmm_get_factors")
@@ -262,7 +305,7 @@ class Lrqmm:
     def correction(self, side: int):
         import torch
 
-        rows = self.m if side == SIDE_A else self.n
+        rows = self.side_rows(side)
         w = self.lib.lrqmm_correction_width(self.h)
         out = torch.empty((rows, w), dtype=torch.float32, device=f"cuda:{self.device}")
         _check(self.lib.lrqmm_get_correction(self.h, side, _ptr(out)), "lrqmm_get_correction")
@@ -277,22 +320,24 @@ class Lrqmm:
         return int(self.lib.lrqmm_launch_count(self.h, 1 if reset else 0))
 
     # ---- end to end from host buffers ----
+    def _host_args(self, A, Bt, omega_a, omega_b, D):
+        if D is None:
+            raise ValueError("D: a host output array is required")
+        return (_host(A, "A", (self.m, self.k)), _host(Bt, "Bt", (self.side_rows(SIDE_B), self.k)),
+                _host(omega_a, "omega_a", (self.k, self.kk)), _host(omega_b, "omega_b", (self.k, self.kk)))
+
     def run_host(self, A: np.ndarray, Bt: np.ndarray, omega_a: np.ndarray | None, omega_b: np.ndarray | None,
                  D: np.ndarray, alpha: float = 1.0):
-        """All arrays C-contiguous float32 host arrays (pinned memory recommended)."""
-        def hp(a):
-            return None if a is None else ctypes.c_void_p(a.ctypes.data)
-        _check(self.lib.lrqmm_run_host(self.h, hp(A), hp(Bt), hp(omega_a), hp(omega_b), alpha, hp(D)),
-               "lrqmm_run_host")
+        """All arrays C-contiguous float32 host arrays of the exact shapes (pinned memory recommended)."""
+        _check(self.lib.lrqmm_run_host(self.h, *self._host_args(A, Bt, omega_a, omega_b, D), alpha,
+                                       _host(D, "D", (self.m, self.n))), "lrqmm_run_host")
         return D
 
     def run_host_async(self, A: np.ndarray, Bt: np.ndarray, omega_a: np.ndarray | None,
                        omega_b: np.ndarray | None, D: np.ndarray, alpha: float = 1.0):
         """Enqueue one call (pinned host arrays, valid until sync()); copies overlap across calls."""
-        def hp(a):
-            return None if a is None else ctypes.c_void_p(a.ctypes.data)
-        _check(self.lib.lrqmm_run_host_async(self.h, hp(A), hp(Bt), hp(omega_a), hp(omega_b), alpha, hp(D)),
-               "lrqmm_run_host_async")
+        _check(self.lib.lrqmm_run_host_async(self.h, *self._host_args(A, Bt, omega_a, omega_b, D), alpha,
+                                             _host(D, "D", (self.m, self.n))), "lrqmm_run_host_async")
         return D
 
 

@@ -525,6 +525,49 @@ def test_binding_rejects_wrong_tensors():
             h.quantize(SIDE_A, torch.zeros((64, 64), dtype=torch.float64, device=DEV))
         with pytest.raises(ValueError):
             h.gemm_int32(torch.zeros((64, 64), device=DEV))                          # needs int32
+        # shapes: undersized operands would make the kernels read / write past the tensor
+        with pytest.raises(ValueError):
+            h.quantize(SIDE_A, torch.zeros((63, 64), device=DEV))
+        with pytest.raises(ValueError):
+            h.quantize(SIDE_B, torch.zeros((64, 32), device=DEV))
+        with pytest.raises(ValueError):
+            h.quantize(SIDE_A, torch.zeros((64, 128), device=DEV)[:, ::2])          # column stride 2
+        with pytest.raises(ValueError):
+            h.gemm(torch.zeros((64, 63), device=DEV))
+        with pytest.raises(ValueError):
+            h.gemm_int32(torch.zeros((32, 64), dtype=torch.int32, device=DEV))
+        with pytest.raises(ValueError):
+            h.rsvd_residual(torch.zeros((64, 5), device=DEV), torch.zeros((64, 6), device=DEV))  # k x (r+p)
+        with pytest.raises(ValueError):
+            h.rsvd_residual_b(torch.zeros((60, 6), device=DEV))
+        ok = np.zeros((64, 64), np.float32)
+        om = np.zeros((64, 6), np.float32)
+        with pytest.raises(ValueError):
+            h.run_host(ok, ok, om, om, np.zeros((64, 64), np.float64))              # D dtype
+        with pytest.raises(ValueError):
+            h.run_host(ok, ok, om, om, np.zeros((64, 63), np.float32))              # D shape
+        with pytest.raises(ValueError):
+            h.run_host(np.asfortranarray(ok + 1), ok, om, om, ok.copy())             # not C-contiguous
+        with pytest.raises(ValueError):
+            h.run_host_async(ok, ok, om[:, :5].copy(), om, ok.copy())                # Omega width
+        # a larger tensor (a view's base) is fine: the kernels use its leading rows / columns
+        h.quantize(SIDE_A, torch.zeros((80, 96), device=DEV))
+
+
+def test_nonfinite_omega_is_reported():
+    """A NaN / Inf in the sketch would own its column's maximum and corrupt the pass image:
+    reported as LRQMM_ERR_NONFINITE like non-finite inputs (reading #7)."""
+    A, Bt, OmA, OmB = S.problem(128, 96, 160, 9, s=2)
+    for bad in (float("nan"), float("inf")):
+        OmA2 = OmA.copy()
+        OmA2[17, 3] = bad
+        with Lrqmm(128, 96, 160, 4, 4, 5) as h:
+            h.quantize(SIDE_A, cu(A))
+            h.quantize(SIDE_B, cu(Bt))
+            h.rsvd_residual(cu(OmA2), cu(OmB))
+            with pytest.raises(LrqmmError) as ei:
+                h.sync()
+            assert ei.value.code == 5
 
 
 def test_quantize_im2col_reports_nonfinite():
