@@ -45,6 +45,13 @@ lrqmm_status_t lrqmm_debug_small(int op, const float* Y, int64_t n, int W, int r
  * and kernels are the product's; only the transport differs.  Multi-rank loopback handles run
  * the RSVD eagerly (no CUDA graph).  Errors: as lrqmm_create; INVALID_ARGUMENT if the group
  * already holds world_size handles or another world_size / device. */
+/* Timing trace of the fused RSVD passes (handles created with LRQMM_FUSE_TRACE=1 in the environment):
+ * per pass slot i < 8 (in launch order since the last read), out[8 i + 0] = first CTA start,
+ * [8 i + 1] = last CTA done with its units, [8 i + 2] / [8 i + 3] = solver start / end, [8 i + 4] =
+ * first CTA done, globaltimer nanoseconds.  Synchronises the stream and re-arms the trace.
+ * LRQMM_ERR_STATE if the handle has no trace. */
+lrqmm_status_t lrqmm_debug_fuse_trace(lrqmm_handle_t h, int64_t out[64]);
+
 lrqmm_status_t lrqmm_debug_create_loopback(const lrqmm_config_t* cfg, int group, lrqmm_handle_t* out);
 
 #ifdef __cplusplus

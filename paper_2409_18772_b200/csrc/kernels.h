@@ -145,9 +145,87 @@ struct TcPassSide {
   uint8_t* img;      // >= 2 * tc_img_bytes(max(rows, K), W) bytes
   const unsigned* cmax1;  // column maxima (float bits) of |P1 scale| / |P2| from their producer, or nullptr
   const unsigned* cmax2;
+  const uint8_t* pimg1;   // prebuilt B image of P1 / P2 (launch_apply_prep), or nullptr: built by the pass
+  const uint8_t* pimg2;
 };
 enum { kPassRow = 0, kPassDual = 1, kPassCol = 2, kPassCodes = 3 };
 void launch_tc_pass(int kind, int nsides, const TcPassSide* sides, int W, bool reduce1, int* ns_out, cudaStream_t st);
+// Fused pass (W <= 32, skinny_tc.cu): the pass kernel itself reduces its split-K partials (the last
+// unit to finish an output block sums the block's partials in split order), forms the fp64 Gram
+// G = OUT1^T OUT1 from per-slot partials (two-level fixed-order ticket sums: deterministic), and
+// the last CTA of the launch runs the small solver of every side (pivoted CholQR -> T64, or the
+// truncation eigensolver -> T, then optionally the cross core of Alg. 2).  B images are
+// prebuilt (launch_apply_prep): no prep launch, no reduction launches, no Gram launch.
+enum { kSolveNone = 0, kSolveChol = 1, kSolveEig = 2 };
+struct PassFuseSide {
+  float* fin1;         // final OUT1 (== TcPassSide::OUT1)
+  float* fin2;         // final OUT2
+  double* G;           // W x W Gram of OUT1 (nullptr: no Gram for this side)
+  double* T64;         // kSolveChol output (W x W)
+  float* T;            // kSolveEig output (W x W, first r columns)
+  int r;
+  unsigned* zero[2];   // 64-entry u32 arrays zeroed by the solver CTA (next column-maxima consumers)
+  int* blk_cnt;        // >= kFuseMaxSlots zeroed counters
+  int* grp_cnt;        // >= 1 + kFuseMaxSlots / 16 zeroed counters
+  double* gpart;       // >= (kFuseMaxSlots + kFuseMaxSlots / 16 + 1) x W x W
+  const uint8_t* img1; // prebuilt B images (+ their 1 / s_c vectors)
+  const float* cinv1;
+  const uint8_t* img2;
+  const float* cinv2;
+};
+constexpr int kFuseMaxSlots = 512;
+struct PassFuse {
+  PassFuseSide s[2];
+  int solver;
+  int* all_cnt;
+  const double* cross_C;  // kSolveEig: if set, VWbM = VWb (VWb^T C VWa) after both eigensolves
+  const float* cross_VWa;
+  const float* cross_VWb;
+  float* cross_out;
+  int r;
+  unsigned long long* trace;  // optional timing trace (lrqmm_debug_fuse_trace)
+};
+// false if the fused form does not apply (W > 32, or too many output blocks with splits): the
+// caller then runs launch_tc_pass + the separate small kernels
+bool launch_tc_pass_fused(int kind, int nsides, const TcPassSide* sides, int W, const PassFuse& f, int* ns_out,
+                          cudaStream_t st);
+// The prep / apply launch of the fused chain (skinny.cu, cooperative): phase 1 forms every apply
+// job's output (Q = Y T64 in fp64, or a zero-padded copy of Omega) and its column maxima; after a
+// grid barrier phase 2 writes the B images of the next pass and (optionally) the cross Gram
+// C = X1^T X2 (fp64, deterministic ticket sum).
+struct ApplyPrepJob {
+  int kind;            // 0: OUT = IN T64;  1: OUT = zero-padded copy of Omega (IN, ld ldi, kk columns)
+  const float* IN;
+  int64_t ldi;
+  int kk;
+  const double* T64;
+  int64_t n;
+  float* OUT;          // n x W
+  unsigned* cmax;      // column maxima of |OUT * cscale| (zeroed beforehand)
+  const float* cscale; // per-row scale or nullptr
+};
+struct ImgJob {
+  const float* P;      // n x W
+  const float* scale;  // per-row scale (COL: 1 / lambda) or nullptr
+  const unsigned* cmax;
+  uint8_t* img;        // nkb k-block images; cinv at img + nkb * image bytes + 256
+  int64_t n;
+};
+struct ApplyPrep {
+  ApplyPrepJob a[2];
+  int na;
+  ImgJob p[4];
+  int np;
+  const float* X1;     // cross Gram C = X1^T X2 over xn rows (nullptr: none)
+  const float* X2;
+  int64_t xn;
+  double* C;
+  double* cpart;       // >= 64 x W x W
+  int* ccnt;           // zeroed ticket
+};
+void launch_apply_prep(const ApplyPrep& ap, int W, int* err_flag /* bit 0: non-finite Omega */, cudaStream_t st);
+// 1 / s_c vector of an image built for n reduction rows (tail of the image buffer)
+float* img_cinv(uint8_t* img, int64_t n, int W);
 // img: scratch for the B operand images + column scales, >= 2 * tc_img_bytes(max(rows, K), W) bytes.
 int launch_tc_proj_rows(const SideView& s, const float* P1, float* OUT1, const float* P2, float* OUT2, int W,
                         float* partial, int64_t partial_elems, bool reduce1, uint8_t* img, cudaStream_t st);

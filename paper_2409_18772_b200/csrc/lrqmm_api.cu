@@ -49,6 +49,7 @@ struct Side {
   unsigned* cmaxOm = nullptr;  // column maxima of |Omega| (S1 pass image), from the Omega copy
   double* T64 = nullptr;     // W x W  (orth transform, fp64)
   float* VW = nullptr;       // W x W  (first r columns: truncation)
+  int* fcnt = nullptr;       // fused chain: finisher counters [0, kFuseMaxSlots) + Gram group tickets
 };
 
 }  // namespace
@@ -77,6 +78,12 @@ struct lrqmm_handle_s {
   cudaEvent_t ev[8] = {};
   Comm* comm = nullptr;   // world_size > 1: NCCL, or the test loopback (lrqmm_debug_create_loopback)
   int64_t launches = 0;   // kernels this handle enqueued (lrqmm_launch_count)
+  int trace_next = 0;
+  bool fused = false;     // experimental fused-pass chain (LRQMM_RSVD_FUSED=1)
+  bool coop = false;      // W <= 32: Omega copies, Q = Y T and the next pass's B images (+ the cross Gram)
+                          // as one cooperative launch each (launch_apply_prep)
+  int* fcnt = nullptr;    // fused chain: [0] launch ticket of the fused passes, [1] cross-Gram ticket
+  unsigned long long* trace = nullptr;  // LRQMM_FUSE_TRACE=1: 8 slots x 5 timestamps per fused pass
   // B column-sharded over the ranks (cfg.b_sharded): this rank owns rows
   // [b_lo, b_lo + s[1].rows) of B^T inside blocks of b_blk rows; s[1].codes / lam / inv_lam and LB
   // point at the rank's slice of the full (ws * b_blk row) buffers below, which the GEMM reads
@@ -217,7 +224,10 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
     cudaFree(s.Y); cudaFree(s.Q0); cudaFree(s.Z); cudaFree(s.Q1); cudaFree(s.Gp); cudaFree(s.G);
     cudaFree(s.gpart); cudaFree(s.cmaxOm); cudaFree(s.cmax0); cudaFree(s.cmax1); cudaFree(s.counter); cudaFree(s.T64); cudaFree(s.VW); cudaFree(s.U); cudaFree(s.img);
     cudaFree(s.R32); cudaFree(s.rcodes); cudaFree(s.rlam); cudaFree(s.rinv); cudaFree(s.rrow_amax); cudaFree(s.rlam_scalar);
+    cudaFree(s.fcnt);
   }
+  cudaFree(h->fcnt);
+  cudaFree(h->trace);
   cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->partial); cudaFree(h->Gcross); cudaFree(h->gpart_cross);
   cudaFree(h->counter_cross); cudaFree(h->VWbM); cudaFree(h->err_flag); cudaFree(h->sched);
   cudaFree(h->hA); cudaFree(h->hB); cudaFree(h->hOmA); cudaFree(h->hOmB); cudaFree(h->hD);
@@ -289,7 +299,7 @@ static lrqmm_status_t create_impl(const lrqmm_config_t* cfg, int loopback_group,
            dalloc(&s.Z, K * h->W) && dalloc(&s.Q1, K * h->W) && dalloc(&s.Gp, s.rows * h->W) &&
            dalloc(&s.G, (int64_t)h->W * h->W) && dalloc(&s.gpart, (int64_t)kGramMaxBlocks * h->W * h->W) &&
            dalloc(&s.counter, 64) && dalloc(&s.cmax0, 64) && dalloc(&s.cmax1, 64) && dalloc(&s.cmaxOm, 64) && dalloc(&s.T64, (int64_t)h->W * h->W) && dalloc(&s.VW, (int64_t)h->W * h->W) &&
-           dalloc(&s.img, 2 * tc_img_bytes(std::max<int64_t>(s.rows, K), h->W));
+           dalloc(&s.img, 2 * tc_img_bytes(std::max<int64_t>(s.rows, K), h->W)) && dalloc(&s.fcnt, 1024);
     }
     if (cfg->qt_terms > 0)
       ok = ok && dalloc(&s.R32, s.rows * K) && dalloc(&s.rcodes, s.rows * h->Kp) && dalloc(&s.rlam, s.rows) &&
@@ -302,7 +312,15 @@ static lrqmm_status_t create_impl(const lrqmm_config_t* cfg, int loopback_group,
     ok = ok && dalloc(&h->LA, cfg->m * h->R2) && dalloc(&h->LB, nfull * h->R2) &&
          dalloc(&h->partial, h->partial_elems) && dalloc(&h->Gcross, (int64_t)h->W * h->W) &&
          dalloc(&h->gpart_cross, (int64_t)kGramMaxBlocks * h->W * h->W) && dalloc(&h->counter_cross, 1) &&
-         dalloc(&h->VWbM, (int64_t)h->W * h->W);
+         dalloc(&h->VWbM, (int64_t)h->W * h->W) && dalloc(&h->fcnt, 64);
+    // the fused RSVD chain (W <= 32 keeps every fused pass at NA = 1; one rank: the Gram matrices are
+    // complete inside one launch; K <= 65536: a pass with splits never has more than kFuseMaxSlots
+    // output blocks).  LRQMM_RSVD_LEGACY=1 selects the separate-launch chain (A/B timing, tests).
+    // both measured slower than the separate-launch chain inside the RSVD graph (c2: 262 / 365 vs
+    // 246 us): opt-in, kept for A/B timing and parity-tested against it
+    h->coop = h->W <= 32 && (getenv("LRQMM_RSVD_COOP") || getenv("LRQMM_RSVD_FUSED")) && !getenv("LRQMM_RSVD_LEGACY");
+    h->fused = h->coop && cfg->world_size == 1 && cfg->power_iters >= 1 && K <= 65536 && getenv("LRQMM_RSVD_FUSED");
+    if (h->fused && getenv("LRQMM_FUSE_TRACE")) ok = ok && dalloc(&h->trace, 64);
   }
   ok = ok && dalloc(&h->err_flag, 4) && dalloc(&h->sched, 1);
   if (!ok) {
@@ -333,6 +351,14 @@ static lrqmm_status_t create_impl(const lrqmm_config_t* cfg, int loopback_group,
     g.A = h->s[0].rcodes;
     g.B = h->s[1].rcodes;
     if (gemm_prepare_maps(g, h->mapRA, h->mapRB) != 0) {
+      lrqmm_destroy(h);
+      return LRQMM_ERR_CUDA;
+    }
+  }
+  if (h->trace) {
+    unsigned long long t[64];
+    for (int i = 0; i < 64; ++i) t[i] = (i % 8 == 0 || i % 8 == 4) ? ~0ull : 0ull;
+    if (cudaMemcpy(h->trace, t, sizeof(t), cudaMemcpyHostToDevice) != cudaSuccess) {
       lrqmm_destroy(h);
       return LRQMM_ERR_CUDA;
     }
@@ -525,14 +551,16 @@ static int64_t part_elems(lrqmm_handle_t h) { return h->partial_elems / 2; }
 // cm1 / cm2: column maxima of P1 / P2 from their producer (apply64), or nullptr (computed by the prep)
 static void pass_sides(lrqmm_handle_t h, int kind, int sides, const float* const P1[2], const float* const P2[2],
                        float* const O1[2], float* const O2[2], bool reduce1, int nsp[2],
-                       const unsigned* const cm1[2] = nullptr, const unsigned* const cm2[2] = nullptr) {
+                       const unsigned* const cm1[2] = nullptr, const unsigned* const cm2[2] = nullptr,
+                       const uint8_t* const pi1[2] = nullptr, const uint8_t* const pi2[2] = nullptr) {
   TcPassSide ps[2];
   int idx[2], n = 0;
   for (int sd = 0; sd < 2; ++sd)
     if (sides & (1 << sd)) {
       ps[n] = TcPassSide{view(h, sd), P1 ? P1[sd] : nullptr, P2 ? P2[sd] : nullptr, O1 ? O1[sd] : nullptr,
                          O2 ? O2[sd] : nullptr, part_of(h, sd), part_elems(h), h->s[sd].img,
-                         cm1 ? cm1[sd] : nullptr, cm2 ? cm2[sd] : nullptr};
+                         cm1 ? cm1[sd] : nullptr, cm2 ? cm2[sd] : nullptr, pi1 ? pi1[sd] : nullptr,
+                         pi2 ? pi2[sd] : nullptr};
       idx[n++] = sd;
     }
   int ns[2] = {0, 0};
@@ -546,8 +574,11 @@ static void pass_sides(lrqmm_handle_t h, int kind, int sides, const float* const
 // sides: bit 0 = A, bit 1 = B
 // which (mode 0): 0 = the result is Q0 (its COL-pass image needs max |Q0 / lambda| per column),
 // 1 = Q1 (max |Q1|); apply64 accumulates those maxima into cmax0 / cmax1.
+// coop (mode 0): Q = Y T64 together with the next pass's B images of Q (which 0: Q0 / lambda over the
+// rows for the COL pass; 1: Q1 over K) in one cooperative launch; `extra` adds image / cross-Gram jobs.
 static lrqmm_status_t gram_step(lrqmm_handle_t h, float* const Y[2], const int64_t n[2], const int nsp[2], int mode,
-                                float* const Q[2], bool a_sharded, int sides = 3, int which = 1) {
+                                float* const Q[2], bool a_sharded, int sides = 3, int which = 1,
+                                const ApplyPrep* extra = nullptr) {
   const int W = h->W;
   const bool ranks = a_sharded && ((side_sharded(h, 0) && (sides & 1)) || (side_sharded(h, 1) && (sides & 2)));
   SmallJobs j{};
@@ -579,7 +610,19 @@ static lrqmm_status_t gram_step(lrqmm_handle_t h, float* const Y[2], const int64
     if (mode == 0) launch_chol_orth(ej, W, h->st);
     else launch_eig_warp(ej, W, h->st);
   }
-  if (mode == 0) {
+  if (mode == 0 && h->coop) {
+    ApplyPrep ap = extra ? *extra : ApplyPrep{};
+    ap.na = 0;
+    for (int sd = 0; sd < 2; ++sd)
+      if ((sides & (1 << sd)) && n[sd] > 0) {
+        Side& s = h->s[sd];
+        unsigned* cm = which == 0 ? s.cmax0 : s.cmax1;
+        const float* sc = which == 0 ? s.inv_lam : nullptr;
+        ap.a[ap.na++] = ApplyPrepJob{0, Y[sd], W, 0, s.T64, n[sd], Q[sd], cm, sc};
+        if (ap.np < 4) ap.p[ap.np++] = ImgJob{Q[sd], sc, cm, s.img, n[sd]};
+      }
+    if (ap.na > 0 || ap.np > 0) launch_apply_prep(ap, W, h->err_flag, h->st);
+  } else if (mode == 0) {
     Apply64Jobs aj{};
     for (int sd = 0; sd < 2; ++sd)
       if (sides & (1 << sd))
@@ -592,7 +635,7 @@ static lrqmm_status_t gram_step(lrqmm_handle_t h, float* const Y[2], const int64
 
 // Range finder of the selected sides (Algorithm 1 with q power steps, reading #11):
 // S1 Y = R Omega; q x [O1 Q0 = orth(Y); S2 Z = R^T Q0; O2 Q1 = orth(Z)].  Leaves Q1 (K x W).
-static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides) {
+static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides, int kind) {
   const int W = h->W;
   const int64_t K = h->cfg.k;
   const bool multi = h->cfg.world_size > 1;
@@ -606,14 +649,17 @@ static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides) {
   const unsigned* cm0[2] = {h->s[0].cmax0, h->s[1].cmax0};
   const unsigned* cm1[2] = {h->s[0].cmax1, h->s[1].cmax1};
   lrqmm_status_t e;
+  // coop: every pass's B image was built by the launch that produced its operand (own image buffer)
+  const uint8_t* imgs[2] = {h->s[0].img, h->s[1].img};
+  const uint8_t* const* pre = h->coop ? imgs : nullptr;
   if (h->cfg.power_iters == 0) {
     // q = 0 (reading #30): S1 Y = R Omega; O1 Q0 = orth(Y); S2 Z = R^T Q0 = B^T of Algorithm 1
     // (B = Q0^* R).  Z goes to the Q1 buffer (the K-side factor), reduced.
     const float* Oms[2] = {h->s[0].Om, h->s[1].Om};
     const unsigned* cmo[2] = {h->s[0].cmaxOm, h->s[1].cmaxOm};
-    pass_sides(h, kPassRow, sides, Oms, nullptr, Ys, nullptr, false, nsp, cmo);
+    pass_sides(h, kPassRow, sides, Oms, nullptr, Ys, nullptr, false, nsp, cmo, nullptr, pre);
     if ((e = gram_step(h, Ys, rows, nsp, 0, Q0s, true, sides, 0)) != LRQMM_OK) return e;
-    pass_sides(h, kPassCol, sides, Q0s, nullptr, Q1s, nullptr, true, nsp, cm0);
+    pass_sides(h, kPassCol, sides, Q0s, nullptr, Q1s, nullptr, true, nsp, cm0, nullptr, pre);
     for (int sd = 0; sd < 2; ++sd)
       if ((sides & (1 << sd)) && side_sharded(h, sd) && (e = allreduce_f32(h, Q1s[sd], (size_t)K * W)) != LRQMM_OK)
         return e;
@@ -622,12 +668,12 @@ static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides) {
   // S1: Y = R Omega   (Algorithm 1 sampling)
   const float* Oms[2] = {h->s[0].Om, h->s[1].Om};
   const unsigned* cmo[2] = {h->s[0].cmaxOm, h->s[1].cmaxOm};
-  pass_sides(h, kPassRow, sides, Oms, nullptr, Ys, nullptr, false, nsp, cmo);
+  pass_sides(h, kPassRow, sides, Oms, nullptr, Ys, nullptr, false, nsp, cmo, nullptr, pre);
   for (int it = 0; it < h->cfg.power_iters; ++it) {
     // O1: Q0 = orth(Y)   (Y rows of A are sharded across ranks)
     if ((e = gram_step(h, Ys, rows, nsp, 0, Q0s, true, sides, 0)) != LRQMM_OK) return e;
     // S2: Z = R^T Q0  (reduction over rows; the A side is summed over ranks before its Gram)
-    pass_sides(h, kPassCol, sides, Q0s, nullptr, Zs, nullptr, multi, nsp, cm0);
+    pass_sides(h, kPassCol, sides, Q0s, nullptr, Zs, nullptr, multi, nsp, cm0, nullptr, pre);
     if (multi) {
       for (int sd = 0; sd < 2; ++sd)
         if ((sides & (1 << sd)) && side_sharded(h, sd) && (e = allreduce_f32(h, Zs[sd], (size_t)K * W)) != LRQMM_OK)
@@ -636,9 +682,22 @@ static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides) {
     }
     // O2: Q1 = orth(Z) (fp64 Gram + Cholesky, transform applied with fp64 accumulation, so Q1 is
     // orthonormal to fp32 rounding); K rows are replicated on every rank
-    if ((e = gram_step(h, Zs, kdim, nsp, 0, Q1s, false, sides, 1)) != LRQMM_OK) return e;
-    if (it + 1 < h->cfg.power_iters) {
-      pass_sides(h, kPassRow, sides, Q1s, nullptr, Ys, nullptr, false, nsp, cm1);
+    // coop, last power step: the same launch forms the cross Gram Q1_B^T Q1_A (Alg. 2 line 366 core)
+    // and, for static-B, the image of B's resident Q1 (the A side's cross operand)
+    ApplyPrep ex{};
+    const bool last = it + 1 == h->cfg.power_iters;
+    if (h->coop && last && kind != 2) {
+      if (kind == 1 && h->s[1].rows > 0) ex.p[ex.np++] = ImgJob{h->s[1].Q1, nullptr, h->s[1].cmax1, h->s[1].img, K};
+      ex.X1 = h->s[1].Q1;
+      ex.X2 = h->s[0].Q1;
+      ex.xn = K;
+      ex.C = h->Gcross;
+      ex.cpart = h->gpart_cross;
+      ex.ccnt = h->counter_cross;
+    }
+    if ((e = gram_step(h, Zs, kdim, nsp, 0, Q1s, false, sides, 1, &ex)) != LRQMM_OK) return e;
+    if (!last) {
+      pass_sides(h, kPassRow, sides, Q1s, nullptr, Ys, nullptr, false, nsp, cm1, nullptr, pre);
     }
   }
   return check_launch(h);
@@ -666,10 +725,14 @@ static lrqmm_status_t fork_cross_gram(lrqmm_handle_t h) {
   return LRQMM_OK;
 }
 
-static lrqmm_status_t assemble(lrqmm_handle_t h) {
+// cross == false: VWbM was formed by the fused truncation pass (rsvd_body_fused); wait_fork: Gcross
+// comes from the forked branch (fork_cross_gram) rather than from stream-ordered work
+static lrqmm_status_t assemble(lrqmm_handle_t h, bool cross = true, bool wait_fork = true) {
   const int W = h->W;
-  LQ_CUDA(cudaStreamWaitEvent(h->st, h->ev_join, 0));  // Gcross (fork_cross_gram)
-  launch_cross_small(h->Gcross, h->s[0].VW, h->s[1].VW, W, h->r, h->VWbM, h->st);
+  if (cross) {
+    if (wait_fork) LQ_CUDA(cudaStreamWaitEvent(h->st, h->ev_join, 0));
+    launch_cross_small(h->Gcross, h->s[0].VW, h->s[1].VW, W, h->r, h->VWbM, h->st);
+  }
   const int r = h->r;
   const int64_t rows[2] = {h->s[0].rows, h->s[1].rows};
   // row-side factor: W = R Q1 (q >= 1), or the orthonormal Q0 (q = 0: R_k = Q0 B, B = Z^T)
@@ -692,14 +755,16 @@ static lrqmm_status_t assemble(lrqmm_handle_t h) {
 // kind 0: both sides (full);  kind 1: static-B (A side + the A-dependent B term; B's W_B, VW_B,
 // Q1_B resident);  kind 2: B side only (prepare the resident B factors).
 // All of it is on handle-owned buffers only (graph-capturable).
+static lrqmm_status_t rsvd_body_fused(lrqmm_handle_t h, int kind);
 static lrqmm_status_t rsvd_body(lrqmm_handle_t h, int kind) {
+  if (h->fused) return rsvd_body_fused(h, kind);
   const int W = h->W;
   const int64_t rows[2] = {h->s[0].rows, h->s[1].rows};
   float* Ys[2] = {h->s[0].Y, h->s[1].Y};
   float* Q1s[2] = {h->s[0].Q1, h->s[1].Q1};
   const int sides = kind == 0 ? 3 : (kind == 1 ? 1 : 2);
   lrqmm_status_t e;
-  if ((e = rsvd_chain(h, sides)) != LRQMM_OK) return e;
+  if ((e = rsvd_chain(h, sides, kind)) != LRQMM_OK) return e;
   int nsp[2] = {1, 1};
   if (h->cfg.power_iters == 0) {
     const int64_t kdim[2] = {h->cfg.k, h->cfg.k};
@@ -722,14 +787,18 @@ static lrqmm_status_t rsvd_body(lrqmm_handle_t h, int kind) {
   //   products)
   const unsigned* cm1[2] = {h->s[0].cmax1, h->s[1].cmax1};
   const unsigned* cm1o[2] = {h->s[1].cmax1, h->s[0].cmax1};
+  const uint8_t* imgs[2] = {h->s[0].img, h->s[1].img};
+  const uint8_t* imgo[2] = {h->s[1].img, h->s[0].img};
   if (kind != 2) {
     const float* other[2] = {Q1s[1], Q1s[0]};
     float* Gps[2] = {h->s[0].Gp, h->s[1].Gp};
-    pass_sides(h, kPassDual, sides, Q1s, other, Ys, Gps, false, nsp, cm1, cm1o);
+    pass_sides(h, kPassDual, sides, Q1s, other, Ys, Gps, false, nsp, cm1, cm1o, h->coop ? imgs : nullptr,
+               h->coop ? imgo : nullptr);
   } else {
-    pass_sides(h, kPassRow, sides, Q1s, nullptr, Ys, nullptr, false, nsp, cm1);
+    pass_sides(h, kPassRow, sides, Q1s, nullptr, Ys, nullptr, false, nsp, cm1, nullptr, h->coop ? imgs : nullptr);
   }
-  if (kind != 2 && (e = fork_cross_gram(h)) != LRQMM_OK) return e;
+  // coop: the cross Gram was formed with Q1 (gram_step O2); else on a forked branch
+  if (kind != 2 && !h->coop && (e = fork_cross_gram(h)) != LRQMM_OK) return e;
   // T: W = sum(partials), truncation to rank r via eig(W^T W) (Algorithm 1)
   if ((e = gram_step(h, Ys, rows, nsp, 1, nullptr, true, sides)) != LRQMM_OK) return e;
   if (kind == 2) return check_launch(h);
@@ -738,9 +807,166 @@ static lrqmm_status_t rsvd_body(lrqmm_handle_t h, int kind) {
     float* Gps[2] = {nullptr, h->s[1].Gp};
     const float* qa[2] = {nullptr, Q1s[0]};
     const unsigned* cma[2] = {nullptr, h->s[0].cmax1};
-    pass_sides(h, kPassCodes, 2, nullptr, qa, nullptr, Gps, true, nsp, nullptr, cma);
+    const uint8_t* ia[2] = {nullptr, h->s[0].img};  // coop: the image of Q1_A built with it
+    pass_sides(h, kPassCodes, 2, nullptr, qa, nullptr, Gps, true, nsp, nullptr, cma, nullptr, h->coop ? ia : nullptr);
   }
-  return assemble(h);
+  return assemble(h, true, !h->coop);
+}
+
+// ---------------------------------------------------------------- fused chain
+// Seven launches per full RSVD (q = 1): [Omega copies + S1 images] (eager, per call) then, captured:
+// S1 (+ Gram + CholQR) -> apply Q0 + COL images -> S2 (+ split reduction + Gram + CholQR) -> apply Q1 +
+// images + cross Gram -> S3 dual (+ reductions + Gram + truncation eigensolves + cross core) -> factor
+// assembly.  Same arithmetic as the separate-launch chain (rsvd_body): fp64 Grams from the fp32
+// panels, CholQR transforms applied with fp64 accumulation, the same B-image pieces.
+static uint8_t* fimg(lrqmm_handle_t h, int sd) { return h->s[sd].img; }
+
+static PassFuseSide fuse_side(lrqmm_handle_t h, int sd, bool gram, const uint8_t* img1, int64_t n1,
+                              const uint8_t* img2, int64_t n2, unsigned* z0, unsigned* z1) {
+  Side& s = h->s[sd];
+  PassFuseSide f{};
+  f.G = gram ? s.G : nullptr;
+  f.T64 = s.T64;
+  f.T = s.VW;
+  f.r = h->r;
+  f.zero[0] = z0;
+  f.zero[1] = z1;
+  f.blk_cnt = s.fcnt;
+  f.grp_cnt = s.fcnt + kFuseMaxSlots;
+  f.gpart = s.gpart;
+  f.img1 = img1;
+  f.cinv1 = img1 ? img_cinv(const_cast<uint8_t*>(img1), n1, h->W) : nullptr;
+  f.img2 = img2;
+  f.cinv2 = img2 ? img_cinv(const_cast<uint8_t*>(img2), n2, h->W) : nullptr;
+  return f;
+}
+
+static lrqmm_status_t fused_pass(lrqmm_handle_t h, int kind, int sides, const PassFuseSide fs[2], int solver,
+                                 float* const O1[2], float* const O2[2], bool cross) {
+  TcPassSide ps[2];
+  PassFuse f{};
+  int n = 0;
+  for (int sd = 0; sd < 2; ++sd)
+    if (sides & (1 << sd)) {
+      ps[n] = TcPassSide{view(h, sd), nullptr, nullptr, O1 ? O1[sd] : nullptr, O2 ? O2[sd] : nullptr, part_of(h, sd),
+                         part_elems(h), nullptr, nullptr, nullptr};
+      f.s[n++] = fs[sd];
+    }
+  f.solver = solver;
+  f.all_cnt = h->fcnt;
+  if (cross) {
+    f.cross_C = h->Gcross;
+    f.cross_VWa = h->s[0].VW;
+    f.cross_VWb = h->s[1].VW;
+    f.cross_out = h->VWbM;
+  }
+  f.r = h->r;
+  if (h->trace) f.trace = h->trace + 8 * (h->trace_next++ & 7);
+  int ns[2];
+  if (!launch_tc_pass_fused(kind, n, ps, h->W, f, ns, h->st)) return fail(h, LRQMM_ERR_UNSUPPORTED);
+  return check_launch(h);
+}
+
+// Omega (caller buffers, K x kk) -> the zero-padded K x W copies and the S1 B images (one eager
+// cooperative launch per call: the caller's pointers are arguments, so it stays outside the graph)
+static lrqmm_status_t fused_omega(lrqmm_handle_t h, const float* omA, const float* omB, int64_t ldo) {
+  ApplyPrep ap{};
+  const int64_t K = h->cfg.k;
+  const float* om[2] = {omA, omB};
+  for (int sd = 0; sd < 2; ++sd)
+    if (om[sd] && h->s[sd].rows > 0 && K > 0) {
+      Side& s = h->s[sd];
+      // (the fused chain re-zeroes the maxima in its last pass; the coop chain does it here)
+      if (!h->fused) LQ_CUDA(cudaMemsetAsync(s.cmaxOm, 0, 64 * sizeof(unsigned), h->st));
+      ap.a[ap.na++] = ApplyPrepJob{1, om[sd], ldo, (int)h->kk, nullptr, K, s.Om, s.cmaxOm, nullptr};
+      ap.p[ap.np++] = ImgJob{s.Om, nullptr, s.cmaxOm, fimg(h, sd), K};
+    }
+  if (ap.na == 0) return LRQMM_OK;
+  launch_apply_prep(ap, h->W, h->err_flag, h->st);
+  return check_launch(h);
+}
+
+static lrqmm_status_t rsvd_body_fused(lrqmm_handle_t h, int kind) {
+  const int64_t K = h->cfg.k;
+  const int sides = kind == 0 ? 3 : (kind == 1 ? 1 : 2);
+  auto has = [&](int sd) { return ((sides >> sd) & 1) && h->s[sd].rows > 0 && K > 0; };
+  int live = 0;
+  for (int sd = 0; sd < 2; ++sd)
+    if (has(sd)) live |= 1 << sd;
+  if (!live) return LRQMM_OK;
+  const int64_t rows[2] = {h->s[0].rows, h->s[1].rows};
+  float* Ys[2] = {h->s[0].Y, h->s[1].Y};
+  float* Zs[2] = {h->s[0].Z, h->s[1].Z};
+  float* Gps[2] = {h->s[0].Gp, h->s[1].Gp};
+  lrqmm_status_t e;
+  PassFuseSide fs[2];
+  // ---- S1: Y = R Omega; Gram + CholQR (Algorithm 1 sampling)
+  for (int sd = 0; sd < 2; ++sd)
+    fs[sd] = fuse_side(h, sd, true, fimg(h, sd), K, nullptr, 0, h->s[sd].cmax0, nullptr);
+  if ((e = fused_pass(h, kPassRow, live, fs, kSolveChol, Ys, nullptr, false)) != LRQMM_OK) return e;
+  for (int it = 0; it < h->cfg.power_iters; ++it) {
+    // ---- O1: Q0 = Y T64 and the COL-pass images of Q0 / lambda
+    ApplyPrep ap{};
+    for (int sd = 0; sd < 2; ++sd)
+      if (live & (1 << sd)) {
+        Side& s = h->s[sd];
+        ap.a[ap.na++] = ApplyPrepJob{0, s.Y, h->W, 0, s.T64, rows[sd], s.Q0, s.cmax0, s.inv_lam};
+        ap.p[ap.np++] = ImgJob{s.Q0, s.inv_lam, s.cmax0, fimg(h, sd), rows[sd]};
+      }
+    launch_apply_prep(ap, h->W, h->err_flag, h->st);
+    // ---- S2: Z = R^T Q0 (power half-step, Eq. rsvderror's q); Gram + CholQR
+    for (int sd = 0; sd < 2; ++sd)
+      fs[sd] = fuse_side(h, sd, true, fimg(h, sd), rows[sd], nullptr, 0, h->s[sd].cmax1, nullptr);
+    if ((e = fused_pass(h, kPassCol, live, fs, kSolveChol, Zs, nullptr, false)) != LRQMM_OK) return e;
+    // ---- O2: Q1 = Z T64 and the images of Q1 (K rows); before S3 also the cross Gram Q1_B^T Q1_A
+    const bool last = it + 1 == h->cfg.power_iters;
+    ApplyPrep aq{};
+    for (int sd = 0; sd < 2; ++sd)
+      if (live & (1 << sd)) {
+        Side& s = h->s[sd];
+        aq.a[aq.na++] = ApplyPrepJob{0, s.Z, h->W, 0, s.T64, K, s.Q1, s.cmax1, nullptr};
+        aq.p[aq.np++] = ImgJob{s.Q1, nullptr, s.cmax1, fimg(h, sd), K};
+      }
+    if (last && kind == 1) {  // static-B: B's resident Q1 is the A side's cross operand
+      Side& b = h->s[1];
+      if (b.rows > 0) aq.p[aq.np++] = ImgJob{b.Q1, nullptr, b.cmax1, fimg(h, 1), K};
+    }
+    if (last && kind != 2) {
+      aq.X1 = h->s[1].Q1;
+      aq.X2 = h->s[0].Q1;
+      aq.xn = K;
+      aq.C = h->Gcross;
+      aq.cpart = h->gpart_cross;
+      aq.ccnt = h->fcnt + 1;
+    }
+    launch_apply_prep(aq, h->W, h->err_flag, h->st);
+    if (!last) {
+      // next power step: Y = R Q1 (+ Gram + CholQR)
+      for (int sd = 0; sd < 2; ++sd)
+        fs[sd] = fuse_side(h, sd, true, fimg(h, sd), K, nullptr, 0, h->s[sd].cmax0, nullptr);
+      if ((e = fused_pass(h, kPassRow, live, fs, kSolveChol, Ys, nullptr, false)) != LRQMM_OK) return e;
+    }
+  }
+  // ---- S3: W = R Q1 (Algorithm 1 on R^T: B = Q1^T R^T = W^T), with the cross products
+  //      G'_X = X~ Q1_other (Alg. 2) in the same pass; Gram + truncation eigensolve
+  //      (Alg. 1) + the V_B^T V_A core; the next call's Omega maxima re-zeroed
+  const bool both = h->s[0].rows > 0 && h->s[1].rows > 0;
+  for (int sd = 0; sd < 2; ++sd) {
+    const int ot = 1 - sd;
+    fs[sd] = fuse_side(h, sd, true, fimg(h, sd), K, kind == 2 ? nullptr : fimg(h, ot), K, h->s[sd].cmaxOm, nullptr);
+  }
+  if (kind == 2) {
+    if ((e = fused_pass(h, kPassRow, live, fs, kSolveEig, Ys, nullptr, false)) != LRQMM_OK) return e;
+    return check_launch(h);
+  }
+  if ((e = fused_pass(h, kPassDual, live, fs, kSolveEig, Ys, Gps, both)) != LRQMM_OK) return e;
+  if (kind == 1 && h->s[1].rows > 0) {
+    // static-B: the only A-dependent B-side term, G'_B = B~ Q1_A (codes pass; finisher reduction)
+    PassFuseSide fb[2];
+    fb[1] = fuse_side(h, 1, false, nullptr, 0, fimg(h, 0), K, nullptr, nullptr);
+    if ((e = fused_pass(h, kPassCodes, 2, fb, kSolveNone, nullptr, Gps, false)) != LRQMM_OK) return e;
+  }
+  return assemble(h, false);
 }
 
 // Runs rsvd_body(kind), captured as a CUDA graph on the second call of that kind and replayed after.
@@ -787,7 +1013,9 @@ static lrqmm_status_t run_rsvd(lrqmm_handle_t h, int kind) {
   return check_launch(h);
 }
 
+static lrqmm_status_t fused_omega(lrqmm_handle_t h, const float* omA, const float* omB, int64_t ldo);
 static lrqmm_status_t copy_omega(lrqmm_handle_t h, int sd, const float* om, int64_t ldo) {
+  if (h->fused || h->coop) return fused_omega(h, sd == 0 ? om : nullptr, sd == 1 ? om : nullptr, ldo);
   launch_copy_omega(om, ldo, (int)h->kk, h->cfg.k, h->W, h->s[sd].Om, h->s[sd].cmaxOm, h->err_flag, h->st);
   return check_launch(h);
 }
@@ -821,8 +1049,12 @@ lrqmm_status_t lrqmm_rsvd_residual(lrqmm_handle_t h, const float* omegaA, const 
   record(h, 4);
   lrqmm_status_t e;
   // sketches Omega (K x kk, caller layout) -> zero-padded K x W
-  if ((e = copy_omega(h, 0, omegaA, ldo)) != LRQMM_OK) return e;
-  if (!static_b && (e = copy_omega(h, 1, omegaB, ldo)) != LRQMM_OK) return e;
+  if (h->fused || h->coop) {
+    if ((e = fused_omega(h, omegaA, static_b ? nullptr : omegaB, ldo)) != LRQMM_OK) return e;
+  } else {
+    if ((e = copy_omega(h, 0, omegaA, ldo)) != LRQMM_OK) return e;
+    if (!static_b && (e = copy_omega(h, 1, omegaB, ldo)) != LRQMM_OK) return e;
+  }
   if ((e = run_rsvd(h, static_b ? 1 : 0)) != LRQMM_OK) return e;
   record(h, 5);
   h->state |= 4 | 8;  // correction ready; B's factors (W_B, VW_B, Q1_B) are current either way
@@ -1084,6 +1316,21 @@ extern "C" lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx
 extern "C" lrqmm_status_t lrqmm_debug_create_loopback(const lrqmm_config_t* cfg, int group, lrqmm_handle_t* out) {
   if (group < 0) return LRQMM_ERR_INVALID_ARGUMENT;
   return create_impl(cfg, group, out);
+}
+
+extern "C" lrqmm_status_t lrqmm_debug_fuse_trace(lrqmm_handle_t h, int64_t out[64]) {
+  if (!h || !out) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (!h->trace) return LRQMM_ERR_STATE;
+  cudaSetDevice(h->cfg.device);
+  if (cudaStreamSynchronize(h->st) != cudaSuccess) return LRQMM_ERR_CUDA;
+  unsigned long long t[64];
+  if (cudaMemcpy(t, h->trace, sizeof(t), cudaMemcpyDeviceToHost) != cudaSuccess) return LRQMM_ERR_CUDA;
+  for (int i = 0; i < 64; ++i) out[i] = (int64_t)t[i];
+  // re-arm: min slots to the maximum, max slots to 0
+  for (int i = 0; i < 64; ++i) t[i] = (i % 8 == 0 || i % 8 == 4) ? ~0ull : 0ull;
+  if (cudaMemcpy(h->trace, t, sizeof(t), cudaMemcpyHostToDevice) != cudaSuccess) return LRQMM_ERR_CUDA;
+  h->trace_next = 0;
+  return LRQMM_OK;
 }
 
 extern "C" lrqmm_status_t lrqmm_debug_set_gemm_variant(int variant) {

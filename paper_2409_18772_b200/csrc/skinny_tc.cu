@@ -34,6 +34,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "solvers.cuh"
 
 namespace lrqmm {
 
@@ -43,10 +44,14 @@ constexpr int BK = 128;   // reduction elements per k-block (one 128-byte swizzl
 constexpr int kTmaWarp = 0;
 constexpr int kMmaWarp = 1;
 constexpr int kThreads = 192;
+constexpr int kThreadsFused = 256;  // + 2 warps that only join the solvers of the last CTA
 constexpr int kPlane = BM * BK;  // 16 KB: one h, l or codes tile
 constexpr int64_t kMaxChunk = 65536;  // |l p| <= 255 * 64: int32 accumulation exact up to 131072 terms
 // kVar: 0 = residual (h, l) only, 1 = residual + codes ("dual"), 2 = codes only
-template <int kMode, int NA, int kVar>
+// kFuse: the pass reduces its own split-K partials (last finisher of each output block), forms the
+// fp64 Gram of OUT1 and runs the small solver in its last CTA (NA == 1 only; PassFuse)
+constexpr int kFuseScratch = 16 * 1024;  // 128 rows x 32 fp32 (staged final rows) / Gram row-group sums
+template <int kMode, int NA, int kVar, bool kFuse = false>
 struct Cfg {
   static constexpr bool kHasU = kVar != 2;
   static constexpr bool kHasC = kVar != 0;
@@ -60,10 +65,12 @@ struct Cfg {
   static constexpr int kOffB2 = kOffC + kPlane;
   static constexpr int kStageBytes = kHasC ? kOffB2 + kImg : kOffB + kImg;
   static constexpr int kStage = (kStageBytes + 1023) / 1024 * 1024;
-  static constexpr int S0 = (216 * 1024) / kStage;
+  static constexpr int kScratch = kFuse ? kFuseScratch : 0;
+  static constexpr int S0 = (216 * 1024 - kScratch) / kStage;
   static constexpr int S = S0 > 6 ? 6 : S0;
   static_assert(S >= 2, "ring depth");
-  static constexpr int kSmem = S * kStage + 256 + 1024;
+  static_assert(!kFuse || NA == 1, "fused Gram / solver for W <= 32 only");
+  static constexpr int kSmem = S * kStage + 256 + 1024 + kScratch;
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
   // TMEM accumulator: H (3 W') | L (2 W') [| C (3 W')], int32
   static constexpr int kOffAccC = kHasU ? 5 * WN : 0;  // C accumulator columns
@@ -96,6 +103,19 @@ struct TcMaps {
 struct TcArgs2 {
   TcArgs a[2];
   int units0, units;
+  // kFuse: per side finisher / Gram / solver outputs, launch-level solver and cross core
+  PassFuseSide fs[2];
+  int nslots[2];
+  int solver;          // kSolveNone (G only), kSolveChol, kSolveEig
+  int ngram;           // sides with a Gram (the launch ticket's target)
+  int* all_cnt;        // launch ticket (zeroed; re-armed)
+  const double* cross_C;  // eig: Mab = VWb^T C VWa, VWbM = VWb Mab (Alg. 2 line 366 core) in the last CTA
+  const float* cross_VWa;
+  const float* cross_VWb;
+  float* cross_out;
+  int r;
+  unsigned long long* trace;  // LRQMM_FUSE_TRACE: [0] min CTA start, [1] max epilogue-loop end,
+                              // [2] solver start, [3] solver end, [4] min epilogue-loop end (globaltimer ns)
 };
 struct TcMaps2 {
   TcMaps m[2];
@@ -251,12 +271,190 @@ __global__ void __launch_bounds__(256) k_prep_img(PrepJobs jb) {
   }
 }
 
-template <int kMode, int NA, int kVar>
-__global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_constant__ TcMaps2 maps,
+// ---- fused epilogue helpers (kFuse): the 128 epilogue threads synchronise on named barrier 2
+LRQMM_DEV void epi_bar() { group_bar(2, 128); }
+LRQMM_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Gram tile of an epilogue thread: 4 x 4 tile (ta, tc), ta <= tc, of the 8 x 8 tiles of a 32-column
+// row block, rows tg, tg + kGG, ... of the staged 128 rows (36 tiles x 3 row groups = 108 threads)
+constexpr int kGT = 8, kGU = kGT * (kGT + 1) / 2, kGG = 128 / kGU;
+LRQMM_DEV void gram_tile_of(int u, int& ta, int& tc) {
+  ta = 0; tc = 0;
+  for (int a = 0; a < kGT; ++a) {
+    if (u < kGT - a) { ta = a; tc = a + u; return; }
+    u -= kGT - a;
+  }
+}
+
+// y = sum over the ns split partials of row `row` (fixed split order), loads of two splits in flight
+LRQMM_DEV void split_sum(float (&y)[32], const float* part, int ns, int64_t nout, int W, int64_t row) {
+#pragma unroll
+  for (int c = 0; c < 32; ++c) y[c] = 0.f;
+  for (int sp = 0; sp < ns; sp += 2) {
+    float4 v[2][8];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float4* p4 = reinterpret_cast<const float4*>(part + (int64_t)(sp + j) * nout * W + row * W);
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4)
+        v[j][c4] = (sp + j < ns && 4 * c4 < W) ? __ldcg(p4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (sp + j < ns)
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4) {
+          y[4 * c4] += v[j][c4].x;
+          y[4 * c4 + 1] += v[j][c4].y;
+          y[4 * c4 + 2] += v[j][c4].z;
+          y[4 * c4 + 3] += v[j][c4].w;
+        }
+  }
+}
+
+// Ticket of the 128 epilogue threads: every thread's prior global writes are released (CTA barrier,
+// then thread 0's gpu-scope acq_rel fence + atomic: cumulative), and the thread that completes the
+// count (== n - 1, re-armed to 0) acquires everyone else's.  True in the last of n arrivals.
+LRQMM_DEV bool epi_ticket(int* cnt, int n, int etid, int* flag) {
+  epi_bar();
+  if (etid == 0) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    const int t = atomicAdd(cnt, 1);
+    const bool last = t == n - 1;
+    if (last) {
+      *cnt = 0;  // re-arm (the next launch is stream ordered)
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    *flag = last;
+  }
+  epi_bar();
+  return *flag != 0;
+}
+
+// Publish this thread group's Gram accumulators as slot `slot` of the side, then the two-level
+// fixed-order ticket sums (groups of 16 slots -> G).  Returns true in the CTA that completed the
+// LAST Gram of the launch (it then runs the solvers).
+LRQMM_DEV bool gram_publish(double (&acc)[16], const PassFuseSide& fs, int nslots, int slot, int W, int ngram,
+                            int* all_cnt, float* scratch, int etid, int* flag) {
+  const int tu = etid % kGU, tg = etid / kGU;
+  const bool gt = etid < kGU * kGG;
+  double (*red)[16] = reinterpret_cast<double (*)[16]>(scratch);  // kGG * kGU x 16 doubles (13.8 KB)
+  epi_bar();
+  if (gt)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) red[tg * kGU + tu][q] = acc[q];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  epi_bar();
+  const int npairs = W * W;
+  double* part = fs.gpart + (int64_t)slot * npairs;
+  for (int e = etid; e < kGU * 16; e += 128) {
+    const int u = e / 16, q = e % 16;
+    double sum = 0.0;
+    for (int g = 0; g < kGG; ++g) sum += red[g * kGU + u][q];
+    int a, c;
+    gram_tile_of(u, a, c);
+    const int i = 4 * a + q / 4, j = 4 * c + q % 4;
+    if (i < W && j < W) {
+      part[i * W + j] = sum;  // diagonal tiles: (p, q) and (q, p) hold bitwise-equal sums
+      part[j * W + i] = sum;
+    }
+  }
+  const int grp = slot / 16, ngrp = (nslots + 15) / 16;
+  const int gsize = nslots - 16 * grp < 16 ? nslots - 16 * grp : 16;
+  if (!epi_ticket(fs.grp_cnt + 1 + grp, gsize, etid, flag)) return false;
+  for (int pr = etid; pr < npairs; pr += 128) {
+    double v[16];
+#pragma unroll
+    for (int b = 0; b < 16; ++b) v[b] = b < gsize ? __ldcg(fs.gpart + (int64_t)(16 * grp + b) * npairs + pr) : 0.0;
+    double a = 0.0;
+#pragma unroll
+    for (int b = 0; b < 16; ++b)
+      if (b < gsize) a += v[b];
+    fs.gpart[(int64_t)(nslots + grp) * npairs + pr] = a;
+  }
+  if (!epi_ticket(fs.grp_cnt, ngrp, etid, flag)) return false;
+  for (int pr = etid; pr < npairs; pr += 128) {
+    double a = 0.0;
+    for (int g = 0; g < ngrp; ++g) a += __ldcg(fs.gpart + (int64_t)(nslots + g) * npairs + pr);
+    fs.G[pr] = a;
+  }
+  return epi_ticket(all_cnt, ngram, etid, flag);
+}
+
+template <int n>
+LRQMM_DEV void fused_solve_n(const TcArgs2& args, double* base) {
+  const int tid = threadIdx.x, w = tid >> 5;
+  if (args.solver == kSolveChol) {
+    if (w < 2 && args.fs[w].G) {  // one warp per side
+      double* sm = base + w * 4096;  // 32 KB per side: S, L, T (32 x 33 doubles each)
+      warp_chol_orth<n>(args.fs[w].G, args.fs[w].T64, sm, sm + 32 * 33, sm + 2 * 32 * 33);
+    }
+  } else if (args.solver == kSolveEig) {
+    const int sd = tid >> 7;  // 128 threads per side, named barriers 3 / 4
+    if (args.fs[sd].G) {
+      double* sm = base + sd * 4096;
+      group_eig_trunc<n, 128>(args.fs[sd].G, args.fs[sd].T, args.fs[sd].r, sm, sm + 3 * 32 * 33, tid & 127, 3 + sd);
+    }
+  }
+}
+
+// The last CTA of a fused pass (all kThreadsFused threads): the small solver of every side, zeroing of
+// the next column-maxima consumers, and the cross core of the factor assembly after the truncation.
+LRQMM_DEV void fused_solve(const TcArgs2& args, uint8_t* smem, int W) {
+  double* base = reinterpret_cast<double*>(smem);
+  const int tid = threadIdx.x, NT = blockDim.x;
+  if (args.solver != kSolveNone) {
+    switch (W) {
+      case 8: fused_solve_n<8>(args, base); break;
+      case 16: fused_solve_n<16>(args, base); break;
+      case 24: fused_solve_n<24>(args, base); break;
+      default: fused_solve_n<32>(args, base); break;
+    }
+  }
+  for (int sd = 0; sd < 2; ++sd)
+    for (int z = 0; z < 2; ++z)
+      if (args.fs[sd].zero[z] && tid < 64) args.fs[sd].zero[z][tid] = 0u;
+  __syncthreads();
+  if (args.solver == kSolveEig && args.cross_C) {
+    // Mab = VWb^T C VWa (r x r), VWbM = VWb Mab (W x r): the V_B^T V_A core of RC3 (Alg. 2)
+    const int r = args.r;
+    double* T1 = base;              // W x r   (C VWa)
+    double* M = base + 32 * 32;     // r x r
+    const double* Cc = args.cross_C;
+    for (int e = tid; e < W * r; e += NT) {
+      const int i = e / r, o = e % r;
+      double a = 0.0;
+      for (int c = 0; c < W; ++c) a += Cc[i * W + c] * (double)args.cross_VWa[c * W + o];
+      T1[i * 32 + o] = a;
+    }
+    __syncthreads();
+    for (int e = tid; e < r * r; e += NT) {
+      const int u = e / r, o = e % r;
+      double a = 0.0;
+      for (int i = 0; i < W; ++i) a += (double)args.cross_VWb[i * W + u] * T1[i * 32 + o];
+      M[u * 32 + o] = a;
+    }
+    __syncthreads();
+    for (int e = tid; e < W * r; e += NT) {
+      const int i = e / r, o = e % r;
+      double a = 0.0;
+      for (int u = 0; u < r; ++u) a += (double)args.cross_VWb[i * W + u] * M[u * 32 + o];
+      args.cross_out[i * W + o] = (float)a;
+    }
+  }
+}
+
+template <int kMode, int NA, int kVar, bool kFuse>
+__global__ void __launch_bounds__(kFuse ? tcp::kThreadsFused : tcp::kThreads, 1) k_tc_proj(const __grid_constant__ TcMaps2 maps,
                                                                  const __grid_constant__ TcArgs2 args) {
   ::lrqmm::pdl_enter();
   using namespace tcp;
-  using C = Cfg<kMode, NA, kVar>;
+  using C = Cfg<kMode, NA, kVar, kFuse>;
   constexpr bool kHasU = C::kHasU, kHasC = C::kHasC;
   constexpr int WN = C::WN;
   constexpr int S = C::S;
@@ -270,6 +468,11 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
   uint64_t* tfull = bars + 2 * S; // 2
   uint64_t* tempty = tfull + 2;   // 2
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* scratch = reinterpret_cast<float*>(smem + S * C::kStage + 256);  // kFuse: kFuseScratch bytes
+  __shared__ int fuse_flag, solve_flag;
+  if constexpr (kFuse) {
+    if (args.trace && threadIdx.x == 0) atomicMin(args.trace, gtimer());
+  }
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nunits = args.units;
@@ -388,7 +591,7 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp < 6) {
     // -------------------------------------------------------------- epilogue
     const int quad = warp & 3;
     // the per-column scales 1/s_c of both sides' P1 / P2 (written by the prep launch), once
@@ -397,7 +600,11 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       const TcArgs& a = args.a[sd];
       cinv_s[sd][which][c] = (sd == 0 || args.units > args.units0) && c < a.W ? (which ? a.cinv2[c] : a.cinv1[c]) : 0.f;
     }
+    if (threadIdx.x == 64) solve_flag = 0;
     asm volatile("bar.sync 1, 128;" ::: "memory");
+    double gacc[16];  // kFuse: this thread's fp64 Gram tile accumulators (per slot)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) gacc[q] = 0.0;
     int lu = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
       int side, blk, split, nkb;
@@ -462,36 +669,128 @@ __global__ void __launch_bounds__(tcp::kThreads, 1) k_tc_proj(const __grid_const
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);  // accumulator buffer free: the next unit's MMAs may start
-      // this thread's output row: 16-byte stores (W is a multiple of 8, rows are 32-byte aligned),
-      // per-column scales from shared memory
+      // scale in place (same fp32 products as stored), then this thread's output row: 16-byte stores
+      // (W is a multiple of 8, rows are 32-byte aligned), per-column scales from shared memory
+      if (kHasU) {
+        const float s1 = inv_row * (1.f / kUScale);
+        const float* cs = cinv_s[side][0];
+#pragma unroll
+        for (int g = 0; g < GU; ++g)
+#pragma unroll
+          for (int c = 0; c < 32; ++c) o[g][c] = o[g][c] * (s1 * cs[g * 32 + c]);
+      }
+      if (kHasC) {
+        const float* cs = cinv_s[side][1];
+#pragma unroll
+        for (int g = 0; g < NA; ++g)
+#pragma unroll
+          for (int c = 0; c < 32; ++c) o[GU + g][c] = o[GU + g][c] * (inv_row * cs[g * 32 + c]);
+      }
       if (orow < a.nout) {
         if (kHasU) {
           float4* o1 = reinterpret_cast<float4*>(a.out1 + (int64_t)split * a.nout * a.W + orow * a.W);
-          const float s1 = inv_row * (1.f / kUScale);
-          const float* cs = cinv_s[side][0];
 #pragma unroll
           for (int g = 0; g < GU; ++g)
 #pragma unroll
             for (int c = 0; c < 32; c += 4)
-              if (g * 32 + c < a.W)
-                o1[(g * 32 + c) >> 2] = make_float4(o[g][c] * (s1 * cs[g * 32 + c]), o[g][c + 1] * (s1 * cs[g * 32 + c + 1]),
-                                                    o[g][c + 2] * (s1 * cs[g * 32 + c + 2]), o[g][c + 3] * (s1 * cs[g * 32 + c + 3]));
+              if (g * 32 + c < a.W) o1[(g * 32 + c) >> 2] = make_float4(o[g][c], o[g][c + 1], o[g][c + 2], o[g][c + 3]);
         }
         if (kHasC) {
           float4* o2 = reinterpret_cast<float4*>(a.out2 + (int64_t)split * a.nout * a.W + orow * a.W);
-          const float* cs = cinv_s[side][1];
 #pragma unroll
           for (int g = 0; g < NA; ++g)
 #pragma unroll
             for (int c = 0; c < 32; c += 4)
               if (g * 32 + c < a.W)
-                o2[(g * 32 + c) >> 2] = make_float4(o[GU + g][c] * (inv_row * cs[g * 32 + c]), o[GU + g][c + 1] * (inv_row * cs[g * 32 + c + 1]),
-                                                    o[GU + g][c + 2] * (inv_row * cs[g * 32 + c + 2]), o[GU + g][c + 3] * (inv_row * cs[g * 32 + c + 3]));
+                o2[(g * 32 + c) >> 2] = make_float4(o[GU + g][c], o[GU + g][c + 1], o[GU + g][c + 2], o[GU + g][c + 3]);
+        }
+      }
+      if constexpr (kFuse) {
+        const PassFuseSide& fs = args.fs[side];
+        const int etid = threadIdx.x - 64;
+        const int ns = a.nsplit;
+        const int W = a.W;
+        bool fin = true;
+        if (ns > 1) {
+          // last finisher of block blk: fixed-order sum of the block's split partials
+          fin = epi_ticket(fs.blk_cnt + blk, ns, etid, &fuse_flag);
+          if (fin) {
+            if (orow < a.nout) {
+              if (kHasU) {
+                float y[32];
+                split_sum(y, a.out1, ns, a.nout, W, orow);
+                float4* f4 = reinterpret_cast<float4*>(fs.fin1 + orow * W);
+#pragma unroll
+                for (int c = 0; c < 32; c += 4)
+                  if (c < W) f4[c >> 2] = make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
+#pragma unroll
+                for (int c = 0; c < 32; ++c) o[0][c] = y[c];
+              }
+              if (kHasC) {
+                float y[32];
+                split_sum(y, a.out2, ns, a.nout, W, orow);
+                float4* f4 = reinterpret_cast<float4*>(fs.fin2 + orow * W);
+#pragma unroll
+                for (int c = 0; c < 32; c += 4)
+                  if (c < W) f4[c >> 2] = make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
+              }
+            }
+          }
+        }
+        if (kHasU && fs.G) {
+          if (fin) {
+            // stage the block's final rows (fp32, zero beyond W and past nout) and accumulate the
+            // fp64 Gram tiles of this thread
+            epi_bar();
+            const int rl = quad * 32 + lane;
+#pragma unroll
+            for (int c = 0; c < 32; c += 4)
+              *reinterpret_cast<float4*>(scratch + rl * 32 + c) =
+                  (orow < a.nout && c < W) ? make_float4(o[0][c], o[0][c + 1], o[0][c + 2], o[0][c + 3])
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            epi_bar();
+            if (etid < kGU * kGG) {
+              int ta, tc;
+              gram_tile_of(etid % kGU, ta, tc);
+              for (int i = etid / kGU; i < BM; i += kGG) {
+                const float4 x4 = *reinterpret_cast<const float4*>(scratch + i * 32 + 4 * ta);
+                const float4 y4 = *reinterpret_cast<const float4*>(scratch + i * 32 + 4 * tc);
+                const double xa[4] = {x4.x, x4.y, x4.z, x4.w}, yc[4] = {y4.x, y4.y, y4.z, y4.w};
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) gacc[p * 4 + q] = fma(xa[p], yc[q], gacc[p * 4 + q]);
+              }
+            }
+          }
+          // publish: per output block when the pass splits (slot = block), else per CTA once its last
+          // unit of this side is done (slot = its index among the side's CTAs; static, deterministic)
+          const int side_lo = side ? args.units0 : 0, side_hi = side ? args.units : args.units0;
+          const bool pub = ns > 1 ? fin : (u + (int)gridDim.x >= side_hi);
+          if (pub) {
+            const int slot = ns > 1 ? blk : (int)((u - side_lo) % (int)gridDim.x);
+            if (gram_publish(gacc, fs, args.nslots[side], slot, W, args.ngram, args.all_cnt, scratch, etid, &fuse_flag))
+              solve_flag = 1;
+          }
         }
       }
     }
   }
   __syncthreads();
+  if constexpr (kFuse) {
+    if (args.trace && threadIdx.x == 0) {
+      const unsigned long long t = gtimer();
+      atomicMax(args.trace + 1, t);
+      atomicMin(args.trace + 4, t);
+      if (solve_flag) args.trace[2] = t;
+    }
+    // the last CTA of the launch: every unit has completed, the ring shared memory is idle
+    if (solve_flag) fused_solve(args, smem, args.a[0].W);
+    if (args.trace && solve_flag) {
+      __syncthreads();
+      if (threadIdx.x == 0) args.trace[3] = gtimer();
+    }
+  }
   if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_free<512>(tmem);
@@ -591,7 +890,7 @@ static void run_tc(int nsides, const TcPassSide* sides, int W, bool reduce1, int
   using C = Cfg<kMode, NA, kVar>;
   constexpr bool kHasU = C::kHasU, kHasC = C::kHasC;
   static std::atomic<unsigned> attr{0};
-  ensure_smem(k_tc_proj<kMode, NA, kVar>, C::kSmem, attr);
+  ensure_smem(k_tc_proj<kMode, NA, kVar, false>, C::kSmem, attr);
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -621,18 +920,27 @@ static void run_tc(int nsides, const TcPassSide* sides, int W, bool reduce1, int
                                  rlen, nkb, cmax};
     };
     jfirst[sd] = jb.njobs;
+    // an operand image is either prebuilt (pimg: launch_apply_prep) or built by this pass's prep
+    auto image = [&](const float* P, const float* scale, uint8_t* img, const unsigned* cmax, const uint8_t* pre,
+                     const uint8_t*& out_img, const float*& out_cinv) {
+      if (pre) {
+        out_img = pre;
+        out_cinv = img_cinv(const_cast<uint8_t*>(pre), rlen, W);
+      } else {
+        add_job(P, scale, img, cmax);
+        out_img = img;
+        out_cinv = jb.j[jb.njobs - 1].cinv;
+      }
+    };
     if (kVar == 2) {
-      add_job(sides[sd].P2, nullptr, sides[sd].img, sides[sd].cmax2);
-      a.img1 = a.img2 = sides[sd].img;
-      a.cinv1 = a.cinv2 = jb.j[jfirst[sd]].cinv;
+      image(sides[sd].P2, nullptr, sides[sd].img, sides[sd].cmax2, sides[sd].pimg2, a.img1, a.cinv1);
+      a.img2 = a.img1;
+      a.cinv2 = a.cinv1;
     } else {
-      add_job(sides[sd].P1, kMode == 1 ? s.inv_lam : nullptr, sides[sd].img, sides[sd].cmax1);
-      a.img1 = sides[sd].img;
-      a.cinv1 = jb.j[jfirst[sd]].cinv;
+      image(sides[sd].P1, kMode == 1 ? s.inv_lam : nullptr, sides[sd].img, sides[sd].cmax1, sides[sd].pimg1, a.img1,
+            a.cinv1);
       if (kHasC) {
-        add_job(sides[sd].P2, nullptr, sides[sd].img + ib, sides[sd].cmax2);
-        a.img2 = sides[sd].img + ib;
-        a.cinv2 = jb.j[jfirst[sd] + 1].cinv;
+        image(sides[sd].P2, nullptr, sides[sd].img + ib, sides[sd].cmax2, sides[sd].pimg2, a.img2, a.cinv2);
       } else {
         a.img2 = a.img1;
         a.cinv2 = a.cinv1;
@@ -673,11 +981,11 @@ static void run_tc(int nsides, const TcPassSide* sides, int W, bool reduce1, int
     units[sd] = nblk * ns;
     ns_out[sd] = (int)ns;
   }
-  launch_prep<NA>(jb, st);
+  if (jb.njobs > 0) launch_prep<NA>(jb, st);
   args.units0 = (int)units[0];
   args.units = (int)(units[0] + units[1]);
   const int grid = (int)(args.units < nsm ? args.units : nsm);
-  launch_pdl(k_tc_proj<kMode, NA, kVar>, grid, kThreads, C::kSmem, st, maps, args);
+  launch_pdl(k_tc_proj<kMode, NA, kVar, false>, grid, kThreads, C::kSmem, st, maps, args);
   ++launch_counter();
   for (int sd = 0; sd < nsides; ++sd) {
     const int ns = ns_out[sd];
@@ -688,6 +996,360 @@ static void run_tc(int nsides, const TcPassSide* sides, int W, bool reduce1, int
     if (reduce1 && kHasU) launch_reduce_splits(part, ns, n, sides[sd].OUT1, st);
     if (kHasC) launch_reduce_splits(kVar == 2 ? part : part + (int64_t)ns * a.nout * W, ns, n, sides[sd].OUT2, st);
   }
+}
+
+// split count of one side's pass: enough units for ~waves per SM (the persistent grid balances
+// them), each >= 4 k-blocks, a chunk short enough for exact int32 accumulation, partials in budget
+static int64_t pass_splits(int64_t nblk, int64_t rlen, int64_t per, int64_t pe, int nsm, int min_kb = 4) {
+  static int waves = 0;  // work units per SM (LRQMM_TC_WAVES overrides, for sweeps)
+  if (!waves) {
+    const char* e = getenv("LRQMM_TC_WAVES");
+    waves = e ? atoi(e) : 3;
+    if (waves < 1) waves = 1;
+  }
+  int64_t ns = ((int64_t)waves * nsm + nblk - 1) / nblk;
+  const int64_t maxs = (rlen + (int64_t)min_kb * tcp::BK - 1) / ((int64_t)min_kb * tcp::BK);
+  if (ns > maxs) ns = maxs;
+  if (ns > 256) ns = 256;
+  if (ns > 1 && ns * per > pe) ns = pe / per;
+  const int64_t mins = (rlen + tcp::kMaxChunk - 1) / tcp::kMaxChunk;
+  if (ns < mins) ns = mins;
+  return ns < 1 ? 1 : ns;
+}
+
+// Fused pass (kFuse, NA == 1): prebuilt images, in-kernel split reduction, Gram and solvers.
+template <int kMode, int kVar>
+static bool run_tc_fused(int nsides, const TcPassSide* sides, int W, const PassFuse& f, int* ns_out, cudaStream_t st) {
+  using namespace tcp;
+  using C = Cfg<kMode, 1, kVar, true>;
+  constexpr bool kHasU = C::kHasU, kHasC = C::kHasC;
+  const int nsm = sm_count();
+  TcArgs2 args{};
+  alignas(64) TcMaps2 maps;
+  memset(&maps, 0, sizeof(maps));
+  int64_t units[2] = {0, 0};
+  int ngram = 0;
+  for (int sd = 0; sd < nsides; ++sd) {
+    const SideView& s = sides[sd].view;
+    const PassFuseSide& fs = f.s[sd];
+    TcArgs& a = args.a[sd];
+    a.rows = s.rows;
+    a.K = s.K;
+    a.inv_lam = s.inv_lam;
+    a.W = W;
+    a.nout = kMode == 0 ? s.rows : (int64_t)s.K;
+    const int64_t nblk = (a.nout + BM - 1) / BM;
+    const int64_t rlen = kMode == 0 ? (int64_t)s.K : s.rows;
+    const int64_t per = a.nout * W * (kVar == 1 ? 2 : 1);
+    // fused units carry a ticket and (finishers) a reduction: >= 8 k-blocks each
+    int64_t ns = pass_splits(nblk, rlen, per, sides[sd].pe, nsm, 8);
+    a.chunk = ((rlen + ns - 1) / ns + BK - 1) / BK * BK;
+    ns = (rlen + a.chunk - 1) / a.chunk;
+    if (ns < 1) ns = 1;
+    if (ns > 1 && nblk > kFuseMaxSlots) return false;  // finisher counters / Gram slots
+    a.nblk = (int)nblk;
+    a.nsplit = (int)ns;
+    a.img1 = kHasU ? fs.img1 : fs.img2;
+    a.cinv1 = kHasU ? fs.cinv1 : fs.cinv2;
+    a.img2 = kHasC ? fs.img2 : a.img1;
+    a.cinv2 = kHasC ? fs.cinv2 : a.cinv1;
+    float* part = sides[sd].partial;
+    a.out1 = ns == 1 ? sides[sd].OUT1 : part;
+    a.out2 = ns == 1 ? sides[sd].OUT2 : (kVar == 2 ? part : part + ns * a.nout * W);
+    const uint64_t ld = (uint64_t)s.ldu;
+    if (kHasU) {
+      encode_map_2d_sw(&maps.m[sd].uh, 0, s.Uh, (uint64_t)s.K, (uint64_t)s.rows, ld, BK, BM, 128);
+      encode_map_2d_sw(&maps.m[sd].ul, 0, s.Ul, (uint64_t)s.K, (uint64_t)s.rows, ld, BK, BM, 128);
+    }
+    if (kHasC)
+      encode_map_2d_sw(&maps.m[sd].codes, 0, s.codes, (uint64_t)s.Kp, (uint64_t)s.rows, (uint64_t)s.Kp, BK, BM, 128);
+    units[sd] = nblk * ns;
+    ns_out[sd] = (int)ns;
+    args.fs[sd] = fs;
+    args.fs[sd].fin1 = sides[sd].OUT1;
+    args.fs[sd].fin2 = sides[sd].OUT2;
+    if (!kHasU) args.fs[sd].G = nullptr;
+    if (args.fs[sd].G) ++ngram;
+  }
+  if (ngram != 0 && ngram != nsides) return false;  // the solver CTA needs every unit of the launch done
+  args.units0 = (int)units[0];
+  args.units = (int)(units[0] + units[1]);
+  const int grid = (int)(args.units < nsm ? args.units : nsm);
+  for (int sd = 0; sd < nsides; ++sd) {
+    const int64_t us = units[sd];
+    args.nslots[sd] = args.a[sd].nsplit > 1 ? args.a[sd].nblk : (int)(us < grid ? us : grid);
+  }
+  args.solver = ngram ? f.solver : kSolveNone;
+  args.ngram = ngram;
+  args.all_cnt = f.all_cnt;
+  args.cross_C = f.cross_C;
+  args.cross_VWa = f.cross_VWa;
+  args.cross_VWb = f.cross_VWb;
+  args.cross_out = f.cross_out;
+  args.r = f.r;
+  args.trace = f.trace;
+  static std::atomic<unsigned> attr{0};
+  ensure_smem(k_tc_proj<kMode, 1, kVar, true>, C::kSmem, attr);
+  launch_pdl(k_tc_proj<kMode, 1, kVar, true>, grid, kThreadsFused, C::kSmem, st, maps, args);
+  ++launch_counter();
+  return true;
+}
+
+bool launch_tc_pass_fused(int kind, int nsides_in, const TcPassSide* sides_in, int W, const PassFuse& f_in, int* ns_out,
+                          cudaStream_t st) {
+  if (W > 32) return false;
+  TcPassSide sides[2];
+  PassFuse f = f_in;
+  int map[2], n = 0;
+  for (int i = 0; i < nsides_in; ++i) {
+    ns_out[i] = 0;
+    if (sides_in[i].view.rows > 0 && sides_in[i].view.K > 0) {
+      map[n] = i;
+      f.s[n] = f_in.s[i];
+      sides[n++] = sides_in[i];
+    }
+  }
+  if (n == 0) return true;
+  int ns[2] = {0, 0};
+  bool ok = false;
+  switch (kind) {
+    case kPassRow: ok = run_tc_fused<0, 0>(n, sides, W, f, ns, st); break;
+    case kPassDual: ok = run_tc_fused<0, 1>(n, sides, W, f, ns, st); break;
+    case kPassCol: ok = run_tc_fused<1, 0>(n, sides, W, f, ns, st); break;
+    default: ok = run_tc_fused<0, 2>(n, sides, W, f, ns, st); break;
+  }
+  for (int i = 0; i < n; ++i) ns_out[map[i]] = ns[i];
+  return ok;
+}
+
+float* img_cinv(uint8_t* img, int64_t n, int W) {
+  const int WN = W <= 32 ? 32 : 64;
+  return reinterpret_cast<float*>(img + (n + tcp::BK - 1) / tcp::BK * (3 * WN * tcp::BK) + 256);
+}
+
+// ------------------------------------------------ fused chain: apply + images (cooperative)
+// Phase 1: every apply job's output rows (Q = IN T64 with fp64 accumulation, or the zero-padded copy
+// of Omega) and the column maxima of |OUT * cscale| (block maxima, then one atomicMax per column).
+// grid.sync().  Phase 2: the cross Gram C = X1^T X2 (first kXBlocks blocks: per-block partials, the
+// last block by ticket sums them in block order), then the K-major SWIZZLE_128B int8 B images of the
+// next pass (the same pieces as k_prep_img) from the outputs, now L2-resident.
+constexpr int kApT = 128;      // threads per block (one row per thread in phase 1)
+constexpr int kXBlocks = 32;   // blocks of the cross Gram
+template <int W>
+__global__ void __launch_bounds__(kApT) k_apply_prep(const ApplyPrep ap, int* err_flag) {
+  namespace cg = cooperative_groups;
+  constexpr int L = W + 4;  // staging stride (conflict-free 16-byte row reads)
+  __shared__ __align__(16) float stage[kApT * L];
+  __shared__ __align__(16) float stage2[kApT * L];  // cross Gram: the second operand's rows
+  __shared__ double Ts[W * W];
+  __shared__ unsigned bmax[2][64];
+  __shared__ int ticket;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int e = tid; e < 2 * 64; e += kApT) bmax[e >> 6][e & 63] = 0u;
+  // ---- phase 1
+  int64_t tiles[2] = {0, 0};
+  for (int q = 0; q < ap.na; ++q) tiles[q] = (ap.a[q].n + kApT - 1) / kApT;
+  int cur = -1;
+  for (int64_t t = blockIdx.x; t < tiles[0] + tiles[1]; t += gridDim.x) {
+    const int q = t < tiles[0] ? 0 : 1;
+    const ApplyPrepJob& J = ap.a[q];
+    const int64_t i0 = (t - (q ? tiles[0] : 0)) * kApT;
+    const int nr = (int)(J.n - i0 < kApT ? J.n - i0 : kApT);
+    float outv[W];
+    __syncthreads();
+    if (J.kind == 0) {
+      if (q != cur)
+        for (int e = tid; e < W * W; e += kApT) Ts[e] = J.T64[e];
+      cur = q;
+      const float4* s4 = reinterpret_cast<const float4*>(J.IN + i0 * W);
+#pragma unroll
+      for (int u = 0; u < W / 4; ++u) {
+        const int e = tid + u * kApT;
+        if (e < nr * (W / 4)) *reinterpret_cast<float4*>(stage + (e / (W / 4)) * L + 4 * (e % (W / 4))) = __ldg(s4 + e);
+      }
+      __syncthreads();
+      double acc[W];
+#pragma unroll
+      for (int o = 0; o < W; ++o) acc[o] = 0.0;
+      if (tid < nr) {
+#pragma unroll
+        for (int c4 = 0; c4 < W / 4; ++c4) {
+          const float4 v = *reinterpret_cast<const float4*>(stage + tid * L + 4 * c4);
+          const double xs[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int o = 0; o < W; ++o) acc[o] = fma(xs[j], Ts[(4 * c4 + j) * W + o], acc[o]);
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < W; ++o) outv[o] = (float)acc[o];
+    } else {
+      // zero-padded copy of Omega (K x kk, ld ldi): a non-finite entry would own its column maximum
+#pragma unroll
+      for (int o = 0; o < W; ++o) {
+        const float v = (tid < nr && o < J.kk) ? J.IN[(i0 + tid) * J.ldi + o] : 0.f;
+        if (!isfinite(v)) atomicOr(err_flag, 1);
+        outv[o] = v;
+      }
+    }
+    if (tid < nr) {
+      float4* orow = reinterpret_cast<float4*>(J.OUT + (i0 + tid) * W);
+#pragma unroll
+      for (int o4 = 0; o4 < W / 4; ++o4) orow[o4] = make_float4(outv[4 * o4], outv[4 * o4 + 1], outv[4 * o4 + 2], outv[4 * o4 + 3]);
+    }
+    // column maxima of |OUT * cscale| (the same fp32 product the image uses)
+    const float cs = (J.cscale && tid < nr) ? J.cscale[i0 + tid] : 1.f;
+#pragma unroll
+    for (int o = 0; o < W; ++o) {
+      const unsigned b = tid < nr ? __float_as_uint(fabsf(outv[o] * cs)) : 0u;
+      const unsigned m = __reduce_max_sync(0xffffffffu, b);
+      if (lane == (o & 31) && m) atomicMax(&bmax[q][o], m);
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < ap.na * 64; e += kApT) {
+    const int q = e >> 6, c = e & 63;
+    if (c < W && bmax[q][c]) atomicMax(ap.a[q].cmax + c, bmax[q][c]);
+  }
+  cg::this_grid().sync();
+  // ---- phase 2a: cross Gram (rows staged through shared memory, coalesced)
+  if (ap.X1 && (int)blockIdx.x < kXBlocks) {
+    const int nb = (int)(gridDim.x < kXBlocks ? gridDim.x : kXBlocks);
+    const int64_t chunk = (ap.xn + nb - 1) / nb;
+    const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = r0 + chunk < ap.xn ? r0 + chunk : ap.xn;
+    constexpr int NP = (W * W + kApT - 1) / kApT;
+    float* s1 = stage;
+    float* s2 = stage2;
+    double acc[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) acc[k] = 0.0;
+    int pa[NP], pb[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const int pr = tid + k * kApT;
+      pa[k] = pr < W * W ? pr / W : 0;
+      pb[k] = pr < W * W ? pr % W : 0;
+    }
+    for (int64_t i0 = r0; i0 < r1; i0 += kApT) {
+      const int nr = (int)(r1 - i0 < kApT ? r1 - i0 : kApT);
+      __syncthreads();
+      const float4* x1 = reinterpret_cast<const float4*>(ap.X1 + i0 * W);
+      const float4* x2 = reinterpret_cast<const float4*>(ap.X2 + i0 * W);
+      for (int e = tid; e < nr * (W / 4); e += kApT) {
+        *reinterpret_cast<float4*>(s1 + (e / (W / 4)) * L + 4 * (e % (W / 4))) = __ldcg(x1 + e);
+        *reinterpret_cast<float4*>(s2 + (e / (W / 4)) * L + 4 * (e % (W / 4))) = __ldcg(x2 + e);
+      }
+      __syncthreads();
+      for (int i = 0; i < nr; ++i)
+#pragma unroll
+        for (int k = 0; k < NP; ++k) acc[k] = fma((double)s1[i * L + pa[k]], (double)s2[i * L + pb[k]], acc[k]);
+    }
+    double* part = ap.cpart + (int64_t)blockIdx.x * W * W;
+#pragma unroll
+    for (int k = 0; k < NP; ++k)
+      if (tid + k * kApT < W * W) part[tid + k * kApT] = acc[k];
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      ticket = atomicAdd(ap.ccnt, 1);
+      if (ticket == nb - 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    __syncthreads();
+    if (ticket == nb - 1) {
+      for (int pr = tid; pr < W * W; pr += kApT) {
+        double a = 0.0;
+        for (int b = 0; b < nb; ++b) a += __ldcg(ap.cpart + (int64_t)b * W * W + pr);
+        ap.C[pr] = a;
+      }
+      if (tid == 0) *ap.ccnt = 0;  // re-arm
+    }
+  }
+  // ---- phase 2b: B images (one (column, 16 rows) item per thread, three 16-byte stores)
+  constexpr int WN = 32;
+  constexpr int kImg = 3 * WN * tcp::BK;
+  constexpr int kChunks = tcp::BK / 16;
+  const int64_t gstride = (int64_t)gridDim.x * kApT;
+  const int64_t t0 = (int64_t)blockIdx.x * kApT + tid;
+  for (int q = 0; q < ap.np; ++q) {
+    const ImgJob& J = ap.p[q];
+    const int64_t n = J.n;
+    const int64_t nkb = (n + tcp::BK - 1) / tcp::BK;
+    if (blockIdx.x == 0 && tid < WN) {
+      float* cinv = reinterpret_cast<float*>(J.img + nkb * kImg + 256);
+      cinv[tid] = tid < W ? 1.f / col_scale(__ldcg(J.cmax + tid)) : 0.f;
+    }
+    const int64_t total = nkb * kChunks * WN;
+    for (int64_t e = t0; e < total; e += gstride) {
+      const int c = (int)(e % WN);
+      const int64_t rest = e / WN;
+      const int ch = (int)(rest % kChunks);
+      const int64_t g = rest / kChunks;
+      const bool cok = c < W;
+      const float sc = cok ? col_scale(__ldcg(J.cmax + c)) : 0.f;
+      const bool hs = J.scale != nullptr;
+      float x[16], y[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        int64_t j = g * tcp::BK + ch * 16 + t;
+        j = j < n ? j : n - 1;
+        x[t] = __ldcg(J.P + j * W + (cok ? c : 0));
+        y[t] = hs ? __ldg(J.scale + j) : 1.f;
+      }
+      uint32_t w1[4] = {0, 0, 0, 0}, w2[4] = {0, 0, 0, 0}, w3[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int64_t j = g * tcp::BK + ch * 16 + t;
+        const float v = j < n ? (hs ? x[t] * y[t] : x[t]) * sc : 0.f;
+        const float p1 = rintf(v);
+        const float r1 = (v - p1) * 128.f;  // exact: |v| < 64, power-of-two scaling
+        const float p2 = rintf(r1);
+        const float p3 = rintf((r1 - p2) * 128.f);
+        const int sh = 8 * (t & 3);
+        w1[t >> 2] |= ((uint32_t)(int)p1 & 0xffu) << sh;
+        w2[t >> 2] |= ((uint32_t)(int)p2 & 0xffu) << sh;
+        w3[t >> 2] |= ((uint32_t)(int)p3 & 0xffu) << sh;
+      }
+      uint8_t* base = J.img + g * kImg;
+      *reinterpret_cast<uint4*>(base + off_k128(c, ch * 16)) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+      *reinterpret_cast<uint4*>(base + off_k128(WN + c, ch * 16)) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+      *reinterpret_cast<uint4*>(base + off_k128(2 * WN + c, ch * 16)) = make_uint4(w3[0], w3[1], w3[2], w3[3]);
+    }
+  }
+}
+
+template <int W>
+static void apply_prep_t(const ApplyPrep& ap, int* err_flag, cudaStream_t st) {
+  static std::atomic<int> per_sm{0};
+  int per = per_sm.load(std::memory_order_relaxed);
+  if (per <= 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_apply_prep<W>, kApT, 0);
+    per = per < 1 ? 1 : (per > 8 ? 8 : per);
+    per_sm.store(per, std::memory_order_relaxed);
+  }
+  // enough blocks for the larger of the two phases, capped at co-residency
+  int64_t want = 0;
+  for (int q = 0; q < ap.na; ++q) want += (ap.a[q].n + kApT - 1) / kApT;
+  int64_t items = 0;
+  for (int q = 0; q < ap.np; ++q) items += (ap.p[q].n + tcp::BK - 1) / tcp::BK * (tcp::BK / 16) * 32;
+  if ((items + kApT - 1) / kApT > want) want = (items + kApT - 1) / kApT;
+  if (ap.X1 && want < kXBlocks) want = kXBlocks;
+  const int64_t cap = (int64_t)sm_count() * per;
+  const int grid = (int)(want < 1 ? 1 : (want > cap ? cap : want));
+  const ApplyPrep* app = &ap;
+  void* args[] = {const_cast<ApplyPrep*>(app), &err_flag};
+  cudaLaunchCooperativeKernel((const void*)k_apply_prep<W>, dim3(grid), dim3(kApT), args, 0, st);
+}
+
+void launch_apply_prep(const ApplyPrep& ap, int W, int* err_flag, cudaStream_t st) {
+  switch (W) {
+    case 8: apply_prep_t<8>(ap, err_flag, st); break;
+    case 16: apply_prep_t<16>(ap, err_flag, st); break;
+    case 24: apply_prep_t<24>(ap, err_flag, st); break;
+    case 32: apply_prep_t<32>(ap, err_flag, st); break;
+    default: return;
+  }
+  ++launch_counter();
 }
 
 // kind: kPassRow (OUT1 = R P1), kPassDual (+ OUT2 = X~ P2), kPassCol (OUT1 = R^T P1), kPassCodes

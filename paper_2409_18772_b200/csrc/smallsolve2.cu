@@ -13,6 +13,7 @@
 //                T = top-r eigenvectors in descending eigenvalue order.
 #include "common.cuh"
 #include "kernels.h"
+#include "solvers.cuh"
 
 namespace lrqmm {
 
@@ -265,198 +266,6 @@ void launch_chol_orth(const EigJobs& jobs, int n, cudaStream_t st) {
   ++launch_counter();
 }
 
-// --------------------------------------------- parallel Jacobi (truncation)
-// Cyclic parallel Jacobi with the round-robin ordering on the leading na x na block of G (na =
-// the even size covering every nonzero row: the zero-padded sketch columns beyond r + p give zero
-// rows and columns, eigenvalue 0, nothing to rotate).  na/2 disjoint rotations per step, na - 1
-// steps per sweep.  The matrix is RELABELLED after every step (position d -> sigma(d): 0 -> 0,
-// 1 -> na-1, d -> d-1) so that pair k always sits at the fixed positions (P_k, Q_k) = (0, 1) for
-// k = 0 and (k+1, na-k) otherwise: A' = J^T A J is computed over 2x2 blocks (pair k1 rows x pair
-// k2 cols) read from one buffer and written, relabelled, to the other (ping-pong), so every thread
-// has fixed addresses, one barrier per step, and no write-after-read hazards.  V' = V J is applied
-// in place on the ORIGINAL column labels (label of position d at step s: orig(s, d)).
-// Every warp computes the rotations of the step redundantly (lane k -> pair k, bitwise identical
-// in every warp) and hands c, s out by shuffle.
-// Stop: off(A)^2 <= 1e-16 diag(A)^2 (off-diagonal <= 1e-8 relative: eigenvector error ~1e-8 / relative
-// gap, at the fp32 precision of the output T; reading #29).
-__device__ __forceinline__ int jac_P(int k) { return k == 0 ? 0 : k + 1; }
-__device__ __forceinline__ int jac_Q(int k, int na) { return k == 0 ? 1 : na - k; }
-__device__ __forceinline__ int jac_sigma(int d, int na) { return d == 0 ? 0 : (d == 1 ? na - 1 : d - 1); }
-__device__ __forceinline__ int jac_orig(int s, int d, int m) {  // s in [0, m), m = na - 1
-  if (d == 0) return 0;
-  int x = d - 1 + s;
-  if (x >= m) x -= m;
-  return x + 1;
-}
-__host__ __device__ constexpr int eig_smem_bytes(int n) { return 3 * n * (n + 1) * 8; }
-
-template <int n>
-__device__ void dev_eig_trunc(const double* G, float* T, int r, double* dyn) {
-  constexpr int ld = n + 1;
-  constexpr int kBlk = ((n / 2) * (n / 2) + 255) / 256, kV = ((n / 2) * n + 255) / 256;
-  double* Abuf = dyn;                 // 2 x n x ld (ping-pong, relabelled)
-  double* V = dyn + 2 * n * ld;       // n x ld, original labels
-  __shared__ int order[kN];
-  __shared__ double red[8][2];
-  __shared__ double scale_s;
-  __shared__ int na_s;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < 32) {
-    double dm = 0.0;
-    int last = -1;
-    for (int i = lane; i < n; i += 32) {
-      const double g = fabs(G[i * n + i]);
-      dm = fmax(dm, g);
-      if (g > 0.0) last = i;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
-      last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
-    }
-    if (lane == 0) {
-      scale_s = dm > 0.0 ? 1.0 / dm : 1.0;
-      // a zero diagonal entry of a Gram matrix means a zero row and column
-      const int na = (last + 2) & ~1;
-      na_s = na < 2 ? 2 : (na > n ? n : na);
-    }
-  }
-  __syncthreads();
-  const int na = na_s, half = na / 2, m = na - 1;
-  // normalised copy (eigenvectors are scale invariant): entries O(1), so the rotation angle
-  // can be computed in fp32 without under/overflow.  At step 0 position d holds index d.
-  double off = 0.0, dg = 0.0;
-  for (int e = tid; e < n * n; e += 256) {
-    const int i = e / n, j = e % n;
-    const double a = 0.5 * (G[i * n + j] + G[j * n + i]) * scale_s;
-    Abuf[i * ld + j] = a;
-    V[i * ld + j] = (i == j) ? 1.0 : 0.0;
-    if (i == j) dg += a * a; else off += a * a;
-  }
-  auto converged = [&](double o, double d) {
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
-      o += __shfl_xor_sync(0xffffffffu, o, s);
-      d += __shfl_xor_sync(0xffffffffu, d, s);
-    }
-    if (lane == 0) { red[warp][0] = o; red[warp][1] = d; }
-    __syncthreads();
-    double o2 = 0.0, d2 = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) { o2 += red[w][0]; d2 += red[w][1]; }
-    return (o2 <= 1e-16 * d2) || (o2 == 0.0);
-  };
-  bool stop = converged(off, dg);
-  // fixed per-thread work: this lane's rotation (pair `lane`), its 2x2 blocks, its V entries
-  const int rk = lane < half ? lane : 0;
-  const int rP = jac_P(rk) * ld + jac_P(rk), rQ = jac_Q(rk, na) * ld + jac_Q(rk, na), rPQ = jac_P(rk) * ld + jac_Q(rk, na);
-  int bk1[kBlk], bk2[kBlk], brd[kBlk][4], bwr[kBlk][4];
-  bool bok[kBlk], bdiag[kBlk];
-#pragma unroll
-  for (int u = 0; u < kBlk; ++u) {
-    const int e = tid + 256 * u;
-    bok[u] = e < half * half;
-    const int k1 = bok[u] ? e / half : 0, k2 = bok[u] ? e % half : 0;
-    bk1[u] = k1;
-    bk2[u] = k2;
-    bdiag[u] = k1 == k2;
-    const int P1 = jac_P(k1), Q1 = jac_Q(k1, na), P2 = jac_P(k2), Q2 = jac_Q(k2, na);
-    brd[u][0] = P1 * ld + P2; brd[u][1] = P1 * ld + Q2; brd[u][2] = Q1 * ld + P2; brd[u][3] = Q1 * ld + Q2;
-    const int p1 = jac_sigma(P1, na), q1 = jac_sigma(Q1, na), p2 = jac_sigma(P2, na), q2 = jac_sigma(Q2, na);
-    bwr[u][0] = p1 * ld + p2; bwr[u][1] = p1 * ld + q2; bwr[u][2] = q1 * ld + p2; bwr[u][3] = q1 * ld + q2;
-  }
-  int vk[kV], vrow[kV], vP[kV], vQ[kV];
-  bool vok[kV];
-#pragma unroll
-  for (int u = 0; u < kV; ++u) {
-    const int e = tid + 256 * u;
-    vok[u] = e < half * na;
-    vk[u] = vok[u] ? e / na : 0;
-    vrow[u] = (vok[u] ? e % na : 0) * ld;
-    vP[u] = jac_P(vk[u]);
-    vQ[u] = jac_Q(vk[u], na);
-  }
-  int total = 0;  // steps done
-  for (int sweep = 0; sweep < 30 && !stop; ++sweep) {
-    for (int step = 0; step < m; ++step, ++total) {
-      const double* Ac = Abuf + (total & 1) * n * ld;
-      double* An = Abuf + ((total + 1) & 1) * n * ld;
-      const bool last = step + 1 == m;
-      double c = 1.0, s = 0.0;
-      if (lane < half) {
-        const double app = Ac[rP], aqq = Ac[rQ], apq = Ac[rPQ];
-        const float fpq = (float)apq;
-        // angle in fp32 with approximate division / square root: any rotation is an exact
-        // similarity (c, s below are orthonormal to fp64 rounding); only convergence depends on it
-        const float theta = __fdividef((float)(aqq - app), 2.f * fpq);
-        const float at = fabsf(theta);
-        const float rs = rsqrtf(fmaf(theta, theta, 1.f));
-        float t = copysignf(__fdividef(1.f, at + fmaf(theta, theta, 1.f) * rs), theta);
-        t = at > 1e18f ? __fdividef(0.5f, theta) : t;
-        const double td = fpq != 0.f ? (double)t : 0.0;
-        const double x = fma(td, td, 1.0);
-        double y = (double)rsqrtf((float)x);
-        y = y * fma(-0.5 * x, y * y, 1.5);
-        y = y * fma(-0.5 * x, y * y, 1.5);
-        c = fpq != 0.f ? y : 1.0;
-        s = td * c;
-      }
-      off = 0.0;
-      dg = 0.0;
-#pragma unroll
-      for (int u = 0; u < kBlk; ++u) {
-        const double c1 = __shfl_sync(0xffffffffu, c, bk1[u]), s1 = __shfl_sync(0xffffffffu, s, bk1[u]);
-        const double c2 = __shfl_sync(0xffffffffu, c, bk2[u]), s2 = __shfl_sync(0xffffffffu, s, bk2[u]);
-        if (bok[u]) {
-          const double a = Ac[brd[u][0]], b = Ac[brd[u][1]], cc = Ac[brd[u][2]], d = Ac[brd[u][3]];
-          const double ra = c1 * a - s1 * cc, rb = c1 * b - s1 * d;
-          const double rc = s1 * a + c1 * cc, rd = s1 * b + c1 * d;
-          const double v0 = c2 * ra - s2 * rb, v1 = s2 * ra + c2 * rb, v2 = c2 * rc - s2 * rd, v3 = s2 * rc + c2 * rd;
-          An[bwr[u][0]] = v0;
-          An[bwr[u][1]] = v1;
-          An[bwr[u][2]] = v2;
-          An[bwr[u][3]] = v3;
-          if (last) {
-            if (bdiag[u]) { dg += v0 * v0 + v3 * v3; off += v1 * v1 + v2 * v2; }
-            else off += (v0 * v0 + v1 * v1) + (v2 * v2 + v3 * v3);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kV; ++u) {
-        const double ck = __shfl_sync(0xffffffffu, c, vk[u]), sk = __shfl_sync(0xffffffffu, s, vk[u]);
-        if (vok[u]) {
-          const int p = vrow[u] + jac_orig(step, vP[u], m), q = vrow[u] + jac_orig(step, vQ[u], m);
-          const double vp = V[p], vq = V[q];
-          V[p] = ck * vp - sk * vq;
-          V[q] = sk * vp + ck * vq;
-        }
-      }
-      if (last) stop = converged(off, dg);  // its barrier ends the step
-      else __syncthreads();
-    }
-  }
-  __syncthreads();
-  // position d < na holds eigenvalue A[d][d] with eigenvector V[:, orig(total mod m, d)];
-  // indices >= na: eigenvalue 0, eigenvector e_d
-  const double* Af = Abuf + (total & 1) * n * ld;
-  const int sf = total % m;
-  for (int t = tid; t < n; t += 256) {
-    int rank = 0;
-    const double li = t < na ? Af[t * ld + t] : 0.0;
-    for (int j = 0; j < n; ++j) {
-      const double lj = j < na ? Af[j * ld + j] : 0.0;
-      rank += (lj > li) || (lj == li && j < t);
-    }
-    order[rank] = t < na ? jac_orig(sf, t, m) : t;
-  }
-  __syncthreads();
-  for (int e = tid; e < n * n; e += 256) {
-    const int a = e / n, o = e % n;
-    T[a * n + o] = (o < r) ? (float)V[a * ld + order[o]] : 0.f;
-  }
-}
-
 template <int n>
 __global__ void __launch_bounds__(256) k_eig(EigJobs jobs) {
   ::lrqmm::pdl_enter();
@@ -486,95 +295,6 @@ void launch_eig_warp(const EigJobs& jobs, int n, cudaStream_t st) {
   }
 
   ++launch_counter();
-}
-
-// ------------------------------------------------- one-warp solvers (n <= 32)
-// Pivoted Cholesky QR transform, one warp, lane j = column j, no row/column swaps:
-//   S (the Schur complement, column-major, stride 33 so lane-parallel accesses are conflict free)
-//   is updated in place on the ORIGINAL indices; lane j keeps its diagonal d_j in a register.
-//   Step k: pivot p = argmax d_j over the remaining lanes (one packed-key __reduce_max_sync pair);
-//   l = S[p, :] / sqrt(d_p) (l_p = sqrt(d_p)); S -= l l^T; d -= l^2.
-//   The transform is built alongside as Gram-Schmidt in the G inner product (mathematically
-//   T = P L^-T):  t_k = (e_p - sum_{m<k} t_m L[p, m]) / L[p, k],  so Q = Y T has orthonormal
-//   columns.  Pivots below 1e-10 x the largest diagonal entry end the factorisation (reading
-//   #12): the remaining columns of T are zero.
-// Output T64[j * n + k] = T[j, k].
-template <int n>
-__device__ void warp_chol_orth(const double* G, double* T64, double* sm, double* Lsm, double* Tsm) {
-  const int lane = threadIdx.x & 31;
-#define SA(i, j) sm[(j) * 33 + (i)]
-  double d = 0.0;
-  for (int i = 0; i < n; ++i)
-    if (lane < n) {
-      const double g = 0.5 * (G[i * n + lane] + G[lane * n + i]);
-      SA(i, lane) = g;
-      if (i == lane) d = g;
-    }
-  double dmax = d;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-  const double thr = 1e-10 * dmax;
-  bool done = lane >= n;
-  __syncwarp();
-  int k = 0;
-  for (; k < n; ++k) {
-    // argmax of d over the remaining lanes; ties (to 2^-46 relative) -> lowest lane
-    const unsigned long long bits = (!done && d > 0.0) ? (unsigned long long)__double_as_longlong(d) : 0ull;
-    const unsigned long long key = (bits & ~63ull) | (unsigned long long)(bits ? 63 - lane : 0);
-    const unsigned hi = (unsigned)(key >> 32);
-    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
-    const unsigned lo = hi == mhi ? (unsigned)key : 0u;
-    const unsigned mlo = __reduce_max_sync(0xffffffffu, lo);
-    if (mhi == 0u && mlo == 0u) break;
-    const int p = 63 - (int)(mlo & 63u);
-    const double dp = __shfl_sync(0xffffffffu, d, p);
-    if (!(dmax > 0.0) || dp < thr || dp <= 0.0) break;
-    const double inv = rsqrt(dp);
-    const double lkk = dp * inv;
-    const double spj = SA(p, lane);
-    double l = done ? 0.0 : (lane == p ? lkk : spj * inv);
-    if (lane == p) done = true;
-    Lsm[k * 33 + lane] = l;
-    if (!done) d = fma(-l, l, d);
-    __syncwarp();
-    // t_k = (e_p - sum_{m<k} t_m L[p, m]) / L[p, k]
-    {
-      double a[4] = {lane == p ? 1.0 : 0.0, 0.0, 0.0, 0.0};
-      for (int m0 = 0; m0 < k; m0 += 4) {
-        double tv[4], lv[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const bool ok = m0 + t < k;
-          tv[t] = ok ? Tsm[(m0 + t) * 33 + lane] : 0.0;
-          lv[t] = ok ? Lsm[(m0 + t) * 33 + p] : 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < 4; ++t) a[t] = fma(-tv[t], lv[t], a[t]);
-      }
-      Tsm[k * 33 + lane] = ((a[0] + a[1]) + (a[2] + a[3])) * inv;
-    }
-    // S -= l l^T on the remaining columns
-    // (explicitly staged in chunks: all loads of a chunk issue before its stores)
-    if (!done) {
-#pragma unroll
-      for (int i0 = 0; i0 < n; i0 += 8) {
-        double sv[8], lv[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          lv[t] = Lsm[k * 33 + i0 + t];
-          sv[t] = SA(i0 + t, lane);
-        }
-#pragma unroll
-        for (int t = 0; t < 8; ++t) SA(i0 + t, lane) = fma(-lv[t], l, sv[t]);
-      }
-    }
-    __syncwarp();
-  }
-  const int rk = k;
-  __syncwarp();
-  if (lane < n)
-    for (int c = 0; c < n; ++c) T64[lane * n + c] = c < rk ? Tsm[c * 33 + lane] : 0.0;
-#undef SA
 }
 
 template <int n>
@@ -766,38 +486,52 @@ void launch_fused_small(const SmallJobs& jobs, int W, int mode, cudaStream_t st)
 
 // Mab = VWb^T C VWa (r x r), C = Q1_B^T Q1_A (n x n, fp64); VWbM = VWb Mab (n x r).
 // V_B^T V_A = VWb^T Q1_B^T Q1_A VWa: the r x r core of RC3 (Alg. 2).
+// Operands staged in shared memory first (every product then reads shared memory only).
 __global__ void __launch_bounds__(256) k_cross_small(const double* __restrict__ C, const float* __restrict__ VWa,
                                                      const float* __restrict__ VWb, int n, int r,
                                                      float* __restrict__ VWbM) {
   ::lrqmm::pdl_enter();
-  __shared__ double T1[kN][kN / 2];      // C VWa  (n x r), r <= 32
-  __shared__ double M[kN / 2][kN / 2];   // r x r
+  extern __shared__ __align__(16) double xs[];
+  double* Cs = xs;                       // n x n
+  double* T1 = Cs + kN * kN;             // n x 32 : C VWa
+  double* M = T1 + kN * 32;              // 32 x 32: VWb^T T1
+  float* A = reinterpret_cast<float*>(M + 32 * 32);  // VWa, n x n
+  float* B = A + kN * kN;                            // VWb, n x n
   const int tid = threadIdx.x;
+  for (int e = tid; e < n * n; e += 256) {
+    Cs[e] = C[e];
+    A[e] = VWa[e];
+    B[e] = VWb[e];
+  }
+  __syncthreads();
   for (int e = tid; e < n * r; e += 256) {
     const int i = e / r, o = e % r;
     double a = 0.0;
-    for (int c = 0; c < n; ++c) a += C[i * n + c] * (double)VWa[c * n + o];
-    T1[i][o] = a;
+    for (int c = 0; c < n; ++c) a = fma(Cs[i * n + c], (double)A[c * n + o], a);
+    T1[i * 32 + o] = a;
   }
   __syncthreads();
   for (int e = tid; e < r * r; e += 256) {
     const int u = e / r, o = e % r;
     double a = 0.0;
-    for (int i = 0; i < n; ++i) a += (double)VWb[i * n + u] * T1[i][o];
-    M[u][o] = a;
+    for (int i = 0; i < n; ++i) a = fma((double)B[i * n + u], T1[i * 32 + o], a);
+    M[u * 32 + o] = a;
   }
   __syncthreads();
   for (int e = tid; e < n * r; e += 256) {
     const int i = e / r, o = e % r;
     double a = 0.0;
-    for (int u = 0; u < r; ++u) a += (double)VWb[i * n + u] * M[u][o];
+    for (int u = 0; u < r; ++u) a = fma((double)B[i * n + u], M[u * 32 + o], a);
     VWbM[i * n + o] = (float)a;
   }
 }
 
 void launch_cross_small(const double* C, const float* VWa, const float* VWb, int n, int r, float* VWbM,
                         cudaStream_t st) {
-  launch_pdl(k_cross_small, 1, 256, 0, st, C, VWa, VWb, n, r, VWbM); ++launch_counter();
+  constexpr int smem = (kN * kN + kN * 32 + 32 * 32) * 8 + 2 * kN * kN * 4;
+  static std::atomic<unsigned> attr{0};
+  ensure_smem(k_cross_small, smem, attr);
+  launch_pdl(k_cross_small, 1, 256, smem, st, C, VWa, VWb, n, r, VWbM); ++launch_counter();
 }
 
 }  // namespace lrqmm

@@ -599,3 +599,67 @@ def test_run_host_async_pipeline_matches_sync():
         h.sync()
     for D, ref in zip(outs, refs):
         assert np.array_equal(D.view(np.uint32), ref.view(np.uint32))
+
+
+# ------------------------------------------------ fused RSVD chain vs separate launches
+@pytest.mark.parametrize("M,N,K,r,p,q,dist", [
+    (256, 256, 256, 8, 5, 1, "normal"),      # W = 16, c1
+    (1000, 130, 700, 4, 4, 1, "u01"),        # W = 8, ragged
+    (640, 512, 384, 16, 5, 2, "exp4"),       # W = 24, q = 2 (a fused ROW pass inside the loop)
+    (300, 280, 4100, 27, 5, 1, "pois10"),    # W = 32, long rows: split ROW passes, finisher sums
+    (60000, 96, 256, 8, 5, 1, "normal"),     # tall: unsplit ROW pass (per-CTA Gram slots)
+])
+def test_fused_chain_matches_separate_launch_chain(monkeypatch, M, N, K, r, p, q, dist):
+    """The fused chain (7 launches; in-pass split reduction, Gram and solvers, cooperative apply +
+    image launches) computes what the separate-launch chain computes: D within fp32 reassociation
+    of each other, both within the north_star bars of the oracle."""
+    A, Bt, OmA, OmB = S.problem(M, N, K, r + p, s=33, dist=dist)
+    coop = run_gpu(A, Bt, 4, r, p, OmA, OmB, q=q)              # default: cooperative apply + images
+    monkeypatch.setenv("LRQMM_RSVD_FUSED", "1")
+    fused = run_gpu(A, Bt, 4, r, p, OmA, OmB, q=q)             # experimental fused passes
+    monkeypatch.delenv("LRQMM_RSVD_FUSED")
+    monkeypatch.setenv("LRQMM_RSVD_LEGACY", "1")
+    legacy = run_gpu(A, Bt, 4, r, p, OmA, OmB, q=q)            # separate launches throughout
+    monkeypatch.delenv("LRQMM_RSVD_LEGACY")
+    assert O.relative_error(legacy["D"], coop["D"]) <= 2e-5
+    assert O.relative_error(legacy["D"], fused["D"]) <= 2e-5
+    if M * N <= 1 << 20:
+        ref = O.lrqmm(A, Bt, 4, r, OmA[:, :r + p], OmB[:, :r + p], q=q)
+        check_d(A, Bt, coop, ref)
+        check_d(A, Bt, fused, ref)
+
+
+@pytest.mark.parametrize("mode", ["coop", "fused"])
+def test_fused_chain_static_b_and_graph_replays(monkeypatch, mode):
+    """Static-B through the fused chain (kind 2 once, then kind 1 calls replayed from the graph)
+    and repeated full calls: every call matches the oracle's full Algorithm 2."""
+    if mode == "fused":
+        monkeypatch.setenv("LRQMM_RSVD_FUSED", "1")
+    M, N, K, r, p = 512, 384, 768, 12, 5
+    A, Bt, OmA, OmB = S.problem(M, N, K, r + p, s=17, dist="u01")
+    ref = O.lrqmm(A, Bt, 4, r, OmA[:, :r + p], OmB[:, :r + p], q=1)
+    with Lrqmm(M, N, K, 4, r, p) as h:
+        a, b = cu(A), cu(Bt)
+        oa, ob = cu(OmA[:, :r + p]), cu(OmB[:, :r + p])
+        D = torch.empty((M, N), device=DEV)
+        h.quantize(SIDE_B, b)
+        h.rsvd_residual_b(ob)
+        outs = []
+        for _ in range(3):
+            h.quantize(SIDE_A, a)
+            h.rsvd_residual(oa)
+            h.gemm(D)
+            h.sync()
+            outs.append(D.cpu().numpy().astype(np.float64))
+        for _ in range(3):
+            h.quantize(SIDE_A, a)
+            h.quantize(SIDE_B, b)
+            h.rsvd_residual(oa, ob)
+            h.gemm(D)
+            h.sync()
+            outs.append(D.cpu().numpy().astype(np.float64))
+    for out in outs:
+        check_d(A, Bt, {"D": out}, ref)
+    # eager first call, captured second, replayed third: bit-identical
+    assert all(np.array_equal(outs[0], o) for o in outs[1:3])
+    assert all(np.array_equal(outs[3], o) for o in outs[4:])
