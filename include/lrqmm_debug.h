@@ -45,6 +45,14 @@ lrqmm_status_t lrqmm_debug_small(int op, const float* Y, int64_t n, int W, int r
  * and kernels are the product's; only the transport differs.  Multi-rank loopback handles run
  * the RSVD eagerly (no CUDA graph).  Errors: as lrqmm_create; INVALID_ARGUMENT if the group
  * already holds world_size handles or another world_size / device. */
+/* GPU negative control: makes later calls in this process run with a deliberate defect that the
+ * parity tests must detect (tests/test_gpu_negative_control.py): 1 = the other rounding mode in K1
+ * (floor <-> nearest), 2 = lambda of row 0 one ulp off after each quantize, 3 = the GEMM epilogue
+ * without the low-rank correction (D = direct quantization), 4 = the RC3 core V_B^T V_A zeroed in the
+ * factor assembly (Alg. 2 line 366 dropped).  0 restores the product path.  INVALID_ARGUMENT
+ * otherwise. */
+lrqmm_status_t lrqmm_debug_inject_fault(int kind);
+
 /* Timing trace of the fused RSVD passes (handles created with LRQMM_FUSE_TRACE=1 in the environment):
  * per pass slot i < 8 (in launch order since the last read), out[8 i + 0] = first CTA start,
  * [8 i + 1] = last CTA done with its units, [8 i + 2] / [8 i + 3] = solver start / end, [8 i + 4] =

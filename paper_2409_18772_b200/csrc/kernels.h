@@ -357,6 +357,8 @@ int encode_map_2d_sw(void* map, int dtype, const void* base, uint64_t inner, uin
                      uint32_t box_inner, uint32_t box_outer, int swizzle_bytes /* 0, 32, 64, 128 */);
 
 void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t st);
+// negative-control hook: flips the lowest mantissa bit of p[0] (skinny.cu)
+void launch_flip_lsb(float* p, cudaStream_t st);
 // Omega -> zero-padded K x W copy + column maxima of |Omega| (skinny.cu)
 void launch_copy_omega(const float* src, int64_t ldo, int kk, int64_t K, int W, float* dst, unsigned* cmax,
                        int* err_flag, cudaStream_t st);  // err_flag bit 0: non-finite Omega

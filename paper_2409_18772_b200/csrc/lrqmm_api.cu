@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -125,6 +126,11 @@ struct lrqmm_handle_s {
     ncclResult_t r_ = (call);                             \
     if (r_ != ncclSuccess) return fail(h, LRQMM_ERR_NCCL); \
   } while (0)
+
+// GPU negative control (lrqmm_debug_inject_fault): a deliberate defect in the product path that the
+// parity tests must catch.  0 = none.
+static std::atomic<int> g_fault{0};
+enum { kFaultNone = 0, kFaultRounding = 1, kFaultLambdaUlp = 2, kFaultNoCorrection = 3, kFaultDropRC3 = 4 };
 
 static lrqmm_status_t fail(lrqmm_handle_t h, lrqmm_status_t s) {
   if (h && h->sticky == LRQMM_OK) h->sticky = s;
@@ -415,6 +421,7 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
   a.Kp = h->Kp;
   a.qmax = h->qmax;
   a.mode = h->cfg.rounding;
+  if (g_fault.load() == kFaultRounding) a.mode = a.mode == kRoundNearest ? kRoundFloor : kRoundNearest;
   a.codes = s.codes;
   a.lam = s.lam;
   a.inv_lam = s.inv_lam;
@@ -424,6 +431,7 @@ lrqmm_status_t lrqmm_quantize(lrqmm_handle_t h, lrqmm_side_t side, const float* 
   a.ldu = s.ldu;
   a.uplane = s.rows * s.ldu;
   if (s.rows > 0) launch_quantize(a, h->st);
+  if (g_fault.load() == kFaultLambdaUlp && s.rows > 0) launch_flip_lsb(s.lam, h->st);  // lambda_0 one ulp off
   if (h->cfg.qt_terms > 0 && s.rows > 0 && h->cfg.k > 0) {
     // QuantTensor: r = fp32(x - code/lambda), re-quantized with its own scale(s) (Eq. gemm_r_split)
     const int K = (int)h->cfg.k;
@@ -735,6 +743,7 @@ static lrqmm_status_t assemble(lrqmm_handle_t h, bool cross = true, bool wait_fo
   }
   const int r = h->r;
   const int64_t rows[2] = {h->s[0].rows, h->s[1].rows};
+  if (g_fault.load() == kFaultDropRC3) LQ_CUDA(cudaMemsetAsync(h->VWbM, 0, sizeof(float) * W * W, h->st));
   // row-side factor: W = R Q1 (q >= 1), or the orthonormal Q0 (q = 0: R_k = Q0 B, B = Z^T)
   float* YA = h->cfg.power_iters == 0 ? h->s[0].Q0 : h->s[0].Y;
   float* YB = h->cfg.power_iters == 0 ? h->s[1].Q0 : h->s[1].Y;
@@ -1076,7 +1085,7 @@ static lrqmm_status_t run_gemm(lrqmm_handle_t h, int epi, float alpha, float bet
   g.inv_b = rb ? h->s[1].rinv : h->inv_b_full;
   g.LA = h->LA;
   g.LB = h->LB_full;
-  g.R2 = h->r > 0 ? h->R2 : 0;
+  g.R2 = (h->r > 0 && g_fault.load() != kFaultNoCorrection) ? h->R2 : 0;
   g.alpha = alpha;
   g.beta = beta;
   g.D = D;
@@ -1330,6 +1339,12 @@ extern "C" lrqmm_status_t lrqmm_debug_fuse_trace(lrqmm_handle_t h, int64_t out[6
   for (int i = 0; i < 64; ++i) t[i] = (i % 8 == 0 || i % 8 == 4) ? ~0ull : 0ull;
   if (cudaMemcpy(h->trace, t, sizeof(t), cudaMemcpyHostToDevice) != cudaSuccess) return LRQMM_ERR_CUDA;
   h->trace_next = 0;
+  return LRQMM_OK;
+}
+
+extern "C" lrqmm_status_t lrqmm_debug_inject_fault(int kind) {
+  if (kind < kFaultNone || kind > kFaultDropRC3) return LRQMM_ERR_INVALID_ARGUMENT;
+  g_fault.store(kind);
   return LRQMM_OK;
 }
 

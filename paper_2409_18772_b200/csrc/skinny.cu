@@ -276,6 +276,12 @@ __global__ void k_f64_to_f32(const double* __restrict__ in, float* __restrict__ 
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (float)in[i];
 }
+__global__ void k_flip_lsb(float* p) { *p = __uint_as_float(__float_as_uint(*p) ^ 1u); }
+void launch_flip_lsb(float* p, cudaStream_t st) {
+  k_flip_lsb<<<1, 1, 0, st>>>(p);
+  ++launch_counter();
+}
+
 void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t st) {
   if (n == 0) return;
   launch_pdl(k_f64_to_f32, clamp_grid((n + 255) / 256), 256, 0, st, in, out, n);

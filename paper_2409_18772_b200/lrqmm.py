@@ -35,7 +35,7 @@ EXPORTS = (
     "lrqmm_quantize_im2col", "lrqmm_run_host_async",
 )
 DEBUG_EXPORTS = ("lrqmm_debug_proj", "lrqmm_debug_small", "lrqmm_debug_set_gemm_variant",
-                 "lrqmm_debug_create_loopback", "lrqmm_debug_fuse_trace")
+                 "lrqmm_debug_create_loopback", "lrqmm_debug_fuse_trace", "lrqmm_debug_inject_fault")
 
 
 class LrqmmError(RuntimeError):
@@ -103,6 +103,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lrqmm_debug_set_gemm_variant": (I, [I]),
         "lrqmm_debug_create_loopback": (I, [ctypes.POINTER(Config), I, ctypes.POINTER(P)]),
         "lrqmm_debug_fuse_trace": (I, [P, ctypes.POINTER(ctypes.c_int64)]),
+        "lrqmm_debug_inject_fault": (I, [I]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
