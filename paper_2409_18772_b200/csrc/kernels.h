@@ -235,6 +235,18 @@ int launch_tc_proj_cols(const SideView& s, const float* P, float* OUT, int W, fl
 int64_t tc_img_bytes(int64_t n, int W);
 // OUT = sum over nsplit partial planes (fixed order), parallel over the n elements
 void launch_reduce_splits(const float* part, int nsplit, int64_t n, float* out, cudaStream_t st);
+struct ReduceJob {
+  const float* part;
+  int nsplit;
+  int64_t n;
+  float* out;
+};
+struct ReduceJobs {
+  ReduceJob j[4];
+  int n;
+};
+// up to 4 reductions (jobs with nsplit <= 1 skipped) in as few launches as possible
+void launch_reduce_jobs(const ReduceJobs& jobs, cudaStream_t st);
 // OUT = X~ P (rows x W) over the codes only (static-B mode's B~ Q1_A); always fully reduced
 int launch_tc_proj_codes(const SideView& s, const float* P, float* OUT, int W, float* partial, int64_t partial_elems,
                          uint8_t* img, cudaStream_t st);

@@ -591,15 +591,15 @@ static lrqmm_status_t gram_step(lrqmm_handle_t h, float* const Y[2], const int64
   const bool ranks = a_sharded && ((side_sharded(h, 0) && (sides & 1)) || (side_sharded(h, 1) && (sides & 2)));
   SmallJobs j{};
   j.n = 0;
+  // split-K partials are reduced first, in parallel over the elements (fixed order per element; both
+  // sides in one launch); the fused kernel then streams the dense Y with bulk copies
+  ReduceJobs rj{};
+  for (int sd = 0; sd < 2; ++sd)
+    if ((sides & (1 << sd)) && nsp[sd] > 1) rj.j[rj.n++] = ReduceJob{part_of(h, sd), nsp[sd], n[sd] * W, Y[sd]};
+  launch_reduce_jobs(rj, h->st);
   for (int sd = 0; sd < 2; ++sd)
     if (sides & (1 << sd)) {
-      int ns = nsp[sd];
-      // split-K partials are reduced first, in parallel over the elements (fixed order per element);
-      // the fused kernel then streams the dense Y with bulk copies
-      if (ns > 1) {
-        launch_reduce_splits(part_of(h, sd), ns, n[sd] * W, Y[sd], h->st);
-        ns = 1;
-      }
+      const int ns = 1;
       j.j[j.n++] = SmallJob{Y[sd], part_of(h, sd), ns, n[sd], h->s[sd].G, h->s[sd].gpart, h->s[sd].counter,
                             h->s[sd].T64, h->s[sd].VW, h->r,
                             mode == 1 ? nullptr : (which == 0 ? h->s[sd].cmax0 : h->s[sd].cmax1)};

@@ -834,6 +834,40 @@ __global__ void __launch_bounds__(256) k_reduce_splits_wide(const float* __restr
   }
 }
 
+// several reductions in one launch (blockIdx.y = job), each the same fixed split order as above
+__global__ void k_reduce_splits_multi(const ReduceJobs jobs) {
+  ::lrqmm::pdl_enter();
+  const ReduceJob& J = jobs.j[blockIdx.y];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < J.n; e += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < J.nsplit; ++s) acc += J.part[(int64_t)s * J.n + e];
+    J.out[e] = acc;
+  }
+}
+
+void launch_reduce_jobs(const ReduceJobs& in, cudaStream_t st) {
+  ReduceJobs jobs{};
+  int64_t nmax = 0;
+  for (int q = 0; q < in.n; ++q) {
+    const ReduceJob& J = in.j[q];
+    if (J.n == 0 || J.nsplit <= 1) continue;
+    if (J.nsplit > 16) {  // long split lists: the coalesced split-group kernel, one launch each
+      launch_reduce_splits(J.part, J.nsplit, J.n, J.out, st);
+      continue;
+    }
+    jobs.j[jobs.n++] = J;
+    nmax = J.n > nmax ? J.n : nmax;
+  }
+  if (jobs.n == 0) return;
+  if (jobs.n == 1) {
+    launch_reduce_splits(jobs.j[0].part, jobs.j[0].nsplit, jobs.j[0].n, jobs.j[0].out, st);
+    return;
+  }
+  const int g = (int)((nmax + 255) / 256 < 4096 ? (nmax + 255) / 256 : 4096);
+  launch_pdl(k_reduce_splits_multi, dim3((unsigned)g, (unsigned)jobs.n), 256, 0, st, jobs);
+  ++launch_counter();
+}
+
 // fixed-order sum of nsplit partial planes into out (n elements)
 void launch_reduce_splits(const float* part, int nsplit, int64_t n, float* out, cudaStream_t st) {
   if (n == 0) return;
@@ -987,15 +1021,17 @@ static void run_tc(int nsides, const TcPassSide* sides, int W, bool reduce1, int
   const int grid = (int)(args.units < nsm ? args.units : nsm);
   launch_pdl(k_tc_proj<kMode, NA, kVar, false>, grid, kThreads, C::kSmem, st, maps, args);
   ++launch_counter();
+  ReduceJobs rj{};
   for (int sd = 0; sd < nsides; ++sd) {
     const int ns = ns_out[sd];
     if (ns <= 1) continue;
     const TcArgs& a = args.a[sd];
     const int64_t n = a.nout * W;
     float* part = sides[sd].partial;
-    if (reduce1 && kHasU) launch_reduce_splits(part, ns, n, sides[sd].OUT1, st);
-    if (kHasC) launch_reduce_splits(kVar == 2 ? part : part + (int64_t)ns * a.nout * W, ns, n, sides[sd].OUT2, st);
+    if (reduce1 && kHasU) rj.j[rj.n++] = ReduceJob{part, ns, n, sides[sd].OUT1};
+    if (kHasC) rj.j[rj.n++] = ReduceJob{kVar == 2 ? part : part + (int64_t)ns * a.nout * W, ns, n, sides[sd].OUT2};
   }
+  launch_reduce_jobs(rj, st);  // both sides' reductions in one launch
 }
 
 // split count of one side's pass: enough units for ~waves per SM (the persistent grid balances

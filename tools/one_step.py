@@ -21,8 +21,10 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--bare", action="store_true")
+    ap.add_argument("--rank", type=int, default=None)
     a = ap.parse_args()
     M, N, K, bits, r, p, dist, _ = CONFIGS[a.config]
+    r = a.rank if a.rank is not None else r
     dev = torch.device("cuda:0")
     A = S.gen_matrix_torch(dist, M, K, 0, device=dev)
     Bt = S.gen_matrix_torch(dist, N, K, 1, device=dev)
