@@ -22,9 +22,11 @@ extern "C" {
 lrqmm_status_t lrqmm_debug_proj(int mode, const float* X, int64_t ldx, int64_t rows, int K, int bits, int rounding,
                                 const float* P, const float* P2, int W, float* OUT, float* OUT2, void* stream);
 
-/* GEMM kernel selection for later calls in this process: 0 = automatic (CTA-pair kernel for
- * M, N >= 512 and >= 512 256x256 tiles), 1 = one-CTA kernel (K6), 2 = CTA-pair kernel (K7).  Lets the tests run both
- * kernels on the same shapes.  Returns INVALID_ARGUMENT for other values. */
+/* GEMM kernel selection for later calls in this process: 0 = automatic (CTA-pair kernel K7 for
+ * M, N >= 512 and >= 512 256x256 tiles; otherwise the one-CTA K8 with the tensor-core correction when
+ * rank > 0, K6 when rank == 0), 1 = one-CTA K6 with the FFMA correction epilogue, 2 = CTA-pair K7,
+ * 3 = K8 (rank > 0).  Lets the tests run every kernel on the same shapes.  INVALID_ARGUMENT for
+ * other values. */
 lrqmm_status_t lrqmm_debug_set_gemm_variant(int variant);
 
 /* Small solvers (K4) on Y (n x W):

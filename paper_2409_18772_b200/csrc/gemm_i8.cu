@@ -17,6 +17,7 @@
 //   warps 2..5 : epilogue (TMEM -> registers -> dequant + rank-2r FFMA -> global), TMEM double-buffered
 //                so the epilogue of tile t overlaps the mainloop of tile t+1.
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -350,6 +351,251 @@ __global__ void __launch_bounds__(g6::threads_for(kR2, BN), 1)
     tc_fence_after();
     tmem_free<kTmemCols>(tmem_base);
   }
+}
+
+static int encode_codes_map(CUtensorMap* map, const int8_t* base, int64_t rows, int Kp, int box_rows);
+
+// ------------------------------------------------------------------------------------------
+// K8 — one-CTA GEMM with the low-rank correction on the TENSOR CORES (narrow shapes, where the
+// FFMA epilogue of K6 is bound by its shared-memory broadcasts of L_B: 2r FMAs and 2r/4 LDS.128
+// per output).  L_A and L_B are held as bf16 hi / lo pairs (x = hi + lo + O(2^-17 |x|)), rows
+// zero-padded to 64 columns = one 128-byte K-major SWIZZLE_128B atom, exactly the byte layout of
+// an int8 stage; per tile two extra ring stages carry [L_A hi | L_B hi] and [L_A lo | L_B lo] and
+// the MMA warp adds, after the int8 main loop, hi.hi + hi.lo + lo.hi (kind::f16, 12 x K16) into a
+// second fp32 TMEM accumulator.  Epilogue: D = alpha (acc / (lambda_A lambda_B) + corr) + beta D
+// -- two TMEM loads and three flops per output.  BN = 128: TMEM = 2 tiles x (int32 128 | fp32 128).
+namespace g8 {
+constexpr int BM = 128, BN = 128, BK = 128, UK = 32;
+constexpr int kStageBytes = BM * BK + BN * BK;  // 32 KB: int8 A | B, or bf16 [L_A | L_B] (hi or lo)
+constexpr int kEG = 2;                          // epilogue groups (one per accumulator pair)
+constexpr int kThreads = 64 + 128 * kEG;
+constexpr int kStages = 6;
+constexpr int kSmem = kStages * kStageBytes + kEG * BN * 4 + 256 + 1024;
+}  // namespace g8
+
+struct G8Params {
+  int64_t M, N;
+  int num_kb, num_m, num_n;
+  const float* inv_a;
+  const float* inv_b;
+  float alpha, beta;
+  float* D;
+  int64_t ldd;
+  int vec_ok;
+};
+
+__global__ void __launch_bounds__(g8::kThreads, 1)
+    k8_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+               const __grid_constant__ CUtensorMap mapLAh, const __grid_constant__ CUtensorMap mapLAl,
+               const __grid_constant__ CUtensorMap mapLBh, const __grid_constant__ CUtensorMap mapLBl, G8Params p) {
+  using namespace g8;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* sSB0 = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // kEG x BN: 1/lambda_B of the tile
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sSB0 + kEG * BN);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages;
+  uint64_t* tfull = bars + 2 * kStages;  // 2
+  uint64_t* tempty = tfull + 2;          // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_tiles = p.num_m * p.num_n;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mapA);
+    tma_prefetch_desc(&mapB);
+    tma_prefetch_desc(&mapLAh);
+    tma_prefetch_desc(&mapLAl);
+    tma_prefetch_desc(&mapLBh);
+    tma_prefetch_desc(&mapLBl);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (warp == 0) {
+    // -------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      auto next = [&]() {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], kStageBytes);
+      };
+      auto advance = [&]() {
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      };
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, p.num_m, p.num_n, mb, nb);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          next();
+          uint8_t* st = smem + stage * kStageBytes;
+          tma_load_2d(st, &mapA, &full[stage], kb * BK, mb * BM);
+          tma_load_2d(st + BM * BK, &mapB, &full[stage], kb * BK, nb * BN);
+          advance();
+        }
+        next();  // [L_A hi | L_B hi]
+        tma_load_2d(smem + stage * kStageBytes, &mapLAh, &full[stage], 0, mb * BM);
+        tma_load_2d(smem + stage * kStageBytes + BM * BK, &mapLBh, &full[stage], 0, nb * BN);
+        advance();
+        next();  // [L_A lo | L_B lo]
+        tma_load_2d(smem + stage * kStageBytes, &mapLAl, &full[stage], 0, mb * BM);
+        tma_load_2d(smem + stage * kStageBytes + BM * BK, &mapLBl, &full[stage], 0, nb * BN);
+        advance();
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // -------------------------------------------------------------- UMMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idi8 = make_idesc_i8(BM, BN);
+      constexpr uint32_t idbf = make_idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int lt = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+        const int acc = lt & 1;
+        mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_main = tmem_base + acc * 256, d_corr = d_main + 128;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * kStageBytes);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            umma_i8(d_main, make_sw128_kmajor_desc(a_addr + k * UK), make_sw128_kmajor_desc(a_addr + BM * BK + k * UK),
+                    idi8, (kb | k) != 0 ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        // correction: stage x = [L_A hi | L_B hi], stage y = [L_A lo | L_B lo]
+        const int sx = stage;
+        const uint32_t px = phase;
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        const int sy = stage;
+        const uint32_t py = phase;
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        mbar_wait(&full[sx], px);
+        mbar_wait(&full[sy], py);
+        tc_fence_after();
+        const uint32_t xa = smem_u32(smem + sx * kStageBytes), ya = smem_u32(smem + sy * kStageBytes);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // 4 x K16 = the 64 bf16 of one atom
+          const uint32_t o = k * 32;
+          umma_bf16(d_corr, make_sw128_kmajor_desc(xa + o), make_sw128_kmajor_desc(xa + BM * BK + o), idbf, k != 0);
+          umma_bf16(d_corr, make_sw128_kmajor_desc(xa + o), make_sw128_kmajor_desc(ya + BM * BK + o), idbf, 1u);
+          umma_bf16(d_corr, make_sw128_kmajor_desc(ya + o), make_sw128_kmajor_desc(xa + BM * BK + o), idbf, 1u);
+        }
+        umma_commit(&empty[sx]);
+        umma_commit(&empty[sy]);
+        umma_commit(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    // group e = accumulator pair e: tiles lt = e, e + 2, ...
+    const int egrp = (warp - 2) >> 2;
+    const int et = threadIdx.x - 64 - 128 * egrp;
+    const int quad = warp & 3;
+    float* sSB = sSB0 + egrp * BN;
+    int lt = egrp;
+    for (int t = blockIdx.x + egrp * gridDim.x; t < num_tiles; t += 2 * gridDim.x, lt += 2) {
+      int mb, nb;
+      tile_coords(t, p.num_m, p.num_n, mb, nb);
+      const int acc = lt & 1;
+      const int64_t row = (int64_t)mb * BM + quad * 32 + lane;
+      const int n0 = nb * BN;
+      epi_bar_id(1 + egrp);  // the previous tile's readers of sSB are done
+      for (int j = et; j < BN; j += 128) sSB[j] = n0 + j < p.N ? __ldg(p.inv_b + n0 + j) : 0.f;
+      const float sa = row < p.M ? p.alpha * __ldg(p.inv_a + row) : 0.f;
+      epi_bar_id(1 + egrp);
+      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * 256;
+#pragma unroll 1
+      for (int g = 0; g < BN / 8; ++g) {
+        uint32_t ri[8], rc[8];
+        tmem_ld_32x32b_x8(t_row + g * 8, ri);
+        tmem_ld_32x32b_x8(t_row + 128 + g * 8, rc);
+        tmem_ld_wait();
+        const int col0 = n0 + g * 8;
+        if (row >= p.M || col0 >= p.N) continue;
+        float v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          v[c] = fmaf(p.alpha, __uint_as_float(rc[c]),
+                      __fmul_rn(static_cast<float>(static_cast<int32_t>(ri[c])), __fmul_rn(sa, sSB[g * 8 + c])));
+        float* out = p.D + row * p.ldd + col0;
+        if (p.vec_ok && col0 + 8 <= p.N) {
+          if (p.beta != 0.f) {
+            const float4 o0 = *reinterpret_cast<const float4*>(out);
+            const float4 o1 = *reinterpret_cast<const float4*>(out + 4);
+            v[0] = fmaf(p.beta, o0.x, v[0]); v[1] = fmaf(p.beta, o0.y, v[1]);
+            v[2] = fmaf(p.beta, o0.z, v[2]); v[3] = fmaf(p.beta, o0.w, v[3]);
+            v[4] = fmaf(p.beta, o1.x, v[4]); v[5] = fmaf(p.beta, o1.y, v[5]);
+            v[6] = fmaf(p.beta, o1.z, v[6]); v[7] = fmaf(p.beta, o1.w, v[7]);
+          }
+          __stcs(reinterpret_cast<float4*>(out), make_float4(v[0], v[1], v[2], v[3]));
+          __stcs(reinterpret_cast<float4*>(out + 4), make_float4(v[4], v[5], v[6], v[7]));
+        } else {
+          for (int c = 0; c < 8; ++c)
+            if (col0 + c < p.N) out[c] = p.beta != 0.f ? fmaf(p.beta, out[c], v[c]) : v[c];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free<512>(tmem_base);
+  }
+}
+
+// L (rows x R2 fp32) -> bf16 hi / lo halves, rows of 64 (zero-padded): the K8 correction operands
+__global__ void k_split_bf16(const float* __restrict__ L, int64_t rows, int R2, __nv_bfloat16* __restrict__ hi,
+                             __nv_bfloat16* __restrict__ lo) {
+  ::lrqmm::pdl_enter();
+  const int64_t total = rows * 64;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e >> 6;
+    const int c = (int)(e & 63);
+    const float x = c < R2 ? L[r * R2 + c] : 0.f;
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    hi[e] = h;
+    lo[e] = __float2bfloat16_rn(x - __bfloat162float(h));
+  }
+}
+
+void launch_split_bf16(const float* L, int64_t rows, int R2, void* hi, void* lo, cudaStream_t st) {
+  if (rows <= 0) return;
+  int64_t g = (rows * 64 + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  launch_pdl(k_split_bf16, (int)g, 256, 0, st, L, rows, R2, reinterpret_cast<__nv_bfloat16*>(hi),
+             reinterpret_cast<__nv_bfloat16*>(lo));
+  ++launch_counter();
+}
+
+int gemm_prepare_maps_tc(const GemmTcOperands& o, void* maps) {
+  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(maps);
+  if (encode_codes_map(m + 0, reinterpret_cast<const int8_t*>(o.LAh), o.M, 128, g8::BM)) return 1;
+  if (encode_codes_map(m + 1, reinterpret_cast<const int8_t*>(o.LAl), o.M, 128, g8::BM)) return 1;
+  if (encode_codes_map(m + 2, reinterpret_cast<const int8_t*>(o.LBh), o.N, 128, g8::BN)) return 1;
+  if (encode_codes_map(m + 3, reinterpret_cast<const int8_t*>(o.LBl), o.N, 128, g8::BN)) return 1;
+  return 0;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -731,13 +977,13 @@ int encode_map_2d_sw(void* map, int dtype, const void* base, uint64_t inner, uin
   return r == CUDA_SUCCESS ? 0 : 2;
 }
 
-int& gemm_variant() {  // 0 auto, 1 force one-CTA K6, 2 force CTA-pair K7 (test hook)
+int& gemm_variant() {  // 0 auto, 1 force one-CTA K6, 2 force CTA-pair K7, 3 force K8 (test hook)
   static int v = 0;
   return v;
 }
 
 static bool use_2sm(int64_t M, int64_t N, const int* sched) {
-  if (!sched || gemm_variant() == 1) return false;
+  if (!sched || gemm_variant() == 1 || gemm_variant() == 3) return false;
   if (gemm_variant() == 2) return true;
   // CTA pairs need enough 256 x 256 tiles to fill 74 pairs for several waves: below ~512 of them
   // (c2, 4096^2: 256) the one-CTA kernel's 2x more, smaller tiles balance better (measured 87 vs
@@ -808,6 +1054,37 @@ static void launch_t7(G6Params p, const CUtensorMap* mA, const CUtensorMap* mB, 
   k7_gemm_i8_2sm<kR2><<<2 * pairs, g7::kThreads, kSmem, st>>>(*mA, *mB, p); ++launch_counter();
 }
 
+// the tensor-core correction kernel K8 replaces K6 for the fused LRQMM epilogue (R2 > 0) unless a
+// test forces another variant or LRQMM_NO_TC_CORR is set
+bool gemm_uses_tc(int64_t M, int64_t N, int R2, const int* sched) {
+  static const bool off = getenv("LRQMM_NO_TC_CORR") != nullptr;
+  if (R2 <= 0 || off || gemm_variant() == 1 || gemm_variant() == 2) return false;
+  return gemm_variant() == 3 || !use_2sm(M, N, sched);
+}
+
+static void launch_k8(const GemmArgs& g, const CUtensorMap* mA, const CUtensorMap* mB, const CUtensorMap* tc,
+                      int nsm, cudaStream_t st) {
+  static std::atomic<unsigned> attr{0};
+  ensure_smem(k8_gemm_tc, g8::kSmem, attr);
+  G8Params p{};
+  p.M = g.M;
+  p.N = g.N;
+  p.num_kb = (g.Kp + g8::BK - 1) / g8::BK;
+  p.num_m = (int)((g.M + g8::BM - 1) / g8::BM);
+  p.num_n = (int)((g.N + g8::BN - 1) / g8::BN);
+  p.inv_a = g.inv_a;
+  p.inv_b = g.inv_b;
+  p.alpha = g.alpha;
+  p.beta = g.beta;
+  p.D = g.D;
+  p.ldd = g.ldd;
+  p.vec_ok = ((reinterpret_cast<uintptr_t>(g.D) & 15) == 0) && (g.ldd % 4 == 0);
+  const int tiles = p.num_m * p.num_n;
+  const int grid = tiles < nsm ? tiles : nsm;
+  k8_gemm_tc<<<grid, g8::kThreads, g8::kSmem, st>>>(*mA, *mB, tc[0], tc[1], tc[2], tc[3], p);
+  ++launch_counter();
+}
+
 int launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStream_t st) {
   if (g.M == 0 || g.N == 0) return 0;
   G6Params p;
@@ -837,6 +1114,10 @@ int launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStrea
   const CUtensorMap* mA = reinterpret_cast<const CUtensorMap*>(mapA);
   const CUtensorMap* mB = reinterpret_cast<const CUtensorMap*>(mapB);
   const int r2 = g.epi == 0 ? 0 : g.R2;
+  if (g.tc_maps && gemm_uses_tc(g.M, g.N, r2, g.sched)) {
+    launch_k8(g, mA, mB + 2, reinterpret_cast<const CUtensorMap*>(g.tc_maps), nsm, st);  // B box 128 rows
+    return 0;
+  }
   if (use_2sm(g.M, g.N, g.sched)) {
     switch (r2) {
       case 0: launch_t7<0>(p, mA + 1, mB + 1, nsm, st); break;

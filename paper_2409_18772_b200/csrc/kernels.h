@@ -360,10 +360,24 @@ struct GemmArgs {
   int32_t* Cint;         // M x N (ldd)
   int64_t ldd;
   int* sched;            // device int: dynamic tile counter of the CTA-pair GEMM (zeroed per launch)
+  const void* tc_maps;   // 4 CUtensorMaps of L_A hi / lo, L_B hi / lo (gemm_prepare_maps_tc) or nullptr
 };
+// bf16 hi / lo operands of the tensor-core correction (K8): rows x 64 bf16 each (128-byte rows)
+struct GemmTcOperands {
+  const void* LAh;
+  const void* LAl;
+  const void* LBh;
+  const void* LBl;
+  int64_t M, N;
+};
+int gemm_prepare_maps_tc(const GemmTcOperands& o, void* maps);  // 4 maps; 0 on success
+// whether launch_gemm will run K8 for these sizes (R2 > 0): then L_A / L_B must be split first
+bool gemm_uses_tc(int64_t M, int64_t N, int R2, const int* sched);
+// L (rows x R2 fp32) -> hi, lo (rows x 64 bf16, zero-padded)
+void launch_split_bf16(const float* L, int64_t rows, int R2, void* hi, void* lo, cudaStream_t st);
 // mapA / mapB: arrays of four CUtensorMap (one-CTA, CTA-pair and narrow-N box shapes); 0 on success
 int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB);
-int& gemm_variant();  // 0 auto (CTA pairs when M, N >= 512 and >= 512 pair tiles), 1 one-CTA K6, 2 CTA-pair K7
+int& gemm_variant();  // 0 auto (CTA pairs when M, N >= 512 and >= 512 pair tiles, else K8 / K6), 1 K6, 2 K7, 3 K8
 // 2D TMA map, dims {inner, outer} elements of u8 (dtype 0), fp32 (1) or u16 (2); returns 0 on success
 int encode_map_2d_sw(void* map, int dtype, const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
                      uint32_t box_inner, uint32_t box_outer, int swizzle_bytes /* 0, 32, 64, 128 */);

@@ -64,6 +64,10 @@ struct lrqmm_handle_s {
   Side s[2];
   float* LA = nullptr;  // m x R2
   float* LB = nullptr;  // n x R2
+  // bf16 hi / lo copies of L_A, L_B (rows x 64) for the tensor-core correction GEMM (K8)
+  void *LAh = nullptr, *LAl = nullptr, *LBh = nullptr, *LBl = nullptr;
+  alignas(64) CUtensorMap mapTC[4];
+  bool tc_ready = false;
   float* partial = nullptr;
   int64_t partial_elems = 0;
   double* Gcross = nullptr;  // W x W
@@ -234,7 +238,8 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   }
   cudaFree(h->fcnt);
   cudaFree(h->trace);
-  cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->partial); cudaFree(h->Gcross); cudaFree(h->gpart_cross);
+  cudaFree(h->LA); cudaFree(h->LB); cudaFree(h->LAh); cudaFree(h->LAl); cudaFree(h->LBh); cudaFree(h->LBl);
+  cudaFree(h->partial); cudaFree(h->Gcross); cudaFree(h->gpart_cross);
   cudaFree(h->counter_cross); cudaFree(h->VWbM); cudaFree(h->err_flag); cudaFree(h->sched);
   cudaFree(h->hA); cudaFree(h->hB); cudaFree(h->hOmA); cudaFree(h->hOmB); cudaFree(h->hD);
   for (auto& sl : h->slot) {
@@ -316,6 +321,10 @@ static lrqmm_status_t create_impl(const lrqmm_config_t* cfg, int loopback_group,
     // split-K / split-row partials: <= 2 outputs x ~4 waves of splits, bounded at 64 MiB
     h->partial_elems = std::min<int64_t>((int64_t)16 << 20, 2 * 32 * maxrows * h->W);
     ok = ok && dalloc(&h->LA, cfg->m * h->R2) && dalloc(&h->LB, nfull * h->R2) &&
+         dalloc(reinterpret_cast<uint16_t**>(&h->LAh), std::max<int64_t>(cfg->m, 1) * 64) &&
+         dalloc(reinterpret_cast<uint16_t**>(&h->LAl), std::max<int64_t>(cfg->m, 1) * 64) &&
+         dalloc(reinterpret_cast<uint16_t**>(&h->LBh), std::max<int64_t>(nfull, 1) * 64) &&
+         dalloc(reinterpret_cast<uint16_t**>(&h->LBl), std::max<int64_t>(nfull, 1) * 64) &&
          dalloc(&h->partial, h->partial_elems) && dalloc(&h->Gcross, (int64_t)h->W * h->W) &&
          dalloc(&h->gpart_cross, (int64_t)kGramMaxBlocks * h->W * h->W) && dalloc(&h->counter_cross, 1) &&
          dalloc(&h->VWbM, (int64_t)h->W * h->W) && dalloc(&h->fcnt, 64);
@@ -352,6 +361,14 @@ static lrqmm_status_t create_impl(const lrqmm_config_t* cfg, int loopback_group,
   if (gemm_prepare_maps(g, h->mapA, h->mapB) != 0) {
     lrqmm_destroy(h);
     return LRQMM_ERR_CUDA;
+  }
+  if (h->R2 > 0) {
+    GemmTcOperands o{h->LAh, h->LAl, h->LBh, h->LBl, std::max<int64_t>(cfg->m, 1), std::max<int64_t>(nfull, 1)};
+    if (gemm_prepare_maps_tc(o, h->mapTC) != 0) {
+      lrqmm_destroy(h);
+      return LRQMM_ERR_CUDA;
+    }
+    h->tc_ready = true;
   }
   if (cfg->qt_terms > 0) {
     g.A = h->s[0].rcodes;
@@ -758,6 +775,12 @@ static lrqmm_status_t assemble(lrqmm_handle_t h, bool cross = true, bool wait_fo
     lrqmm_status_t e = allgather_b(h, h->LB_full, sizeof(float) * h->R2);
     if (e != LRQMM_OK) return e;
   }
+  // bf16 hi / lo operands of the tensor-core correction (K8; always formed, so that a graph captured
+  // under one kernel choice stays valid under another)
+  if (h->tc_ready) {
+    launch_split_bf16(h->LA, h->cfg.m, h->R2, h->LAh, h->LAl, h->st);
+    launch_split_bf16(h->LB_full, h->bsh ? h->b_blk * h->cfg.world_size : h->cfg.n, h->R2, h->LBh, h->LBl, h->st);
+  }
   return check_launch(h);
 }
 
@@ -1092,6 +1115,7 @@ static lrqmm_status_t run_gemm(lrqmm_handle_t h, int epi, float alpha, float bet
   g.Cint = Cint;
   g.ldd = ldd;
   g.sched = h->sched;
+  g.tc_maps = (epi == 1 && g.R2 > 0 && h->tc_ready) ? h->mapTC : nullptr;
   if (launch_gemm(g, ra ? h->mapRA : h->mapA, rb ? h->mapRB : h->mapB, h->st) != 0) return LRQMM_ERR_UNSUPPORTED;
   return check_launch(h);
 }
@@ -1349,7 +1373,7 @@ extern "C" lrqmm_status_t lrqmm_debug_inject_fault(int kind) {
 }
 
 extern "C" lrqmm_status_t lrqmm_debug_set_gemm_variant(int variant) {
-  if (variant < 0 || variant > 2) return LRQMM_ERR_INVALID_ARGUMENT;
+  if (variant < 0 || variant > 3) return LRQMM_ERR_INVALID_ARGUMENT;
   gemm_variant() = variant;
   return LRQMM_OK;
 }

@@ -34,10 +34,30 @@ LRQMM_DEV void stage_rows_in(const float* __restrict__ src, int64_t i0, int nr, 
   }
 }
 
+// The same tile staged asynchronously (cp.async, 16 bytes per copy, into the padded rows): no
+// register staging, so the next tile's loads are in flight while this one is multiplied; one commit
+// group per call.
+template <int W>
+LRQMM_DEV void stage_rows_async(const float* __restrict__ src, int64_t i0, int nr, float* sm) {
+  constexpr int L = ap_ld(W);
+  const float4* s4 = reinterpret_cast<const float4*>(src + i0 * W);
+#pragma unroll
+  for (int u = 0; u < W / 4; ++u) {
+    const int e = threadIdx.x + u * kApRows;
+    if (e < nr * (W / 4)) {
+      const uint32_t dst = smem_u32(sm + (e / (W / 4)) * L + 4 * (e % (W / 4)));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(s4 + e) : "memory");
+    }
+  }
+}
+LRQMM_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+LRQMM_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // OUT[i, col0 + o] = sum_c IN1[i,c] S1[c,o] (+ sum_c IN2[i,c] S2[c,o]),  o < nout (<= W).
 // Up to kMaxApply jobs per launch: job q owns blocks [first[q], first[q+1]) and walks its rows.
 template <int W>
-__global__ void __launch_bounds__(kApRows) k_apply_small(const ApplyJobs jobs) {
+__global__ void __launch_bounds__(kApRows) k_apply_small(const __grid_constant__ ApplyJobs jobs) {
   ::lrqmm::pdl_enter();
   constexpr int L = ap_ld(W);
   extern __shared__ __align__(16) float apsm[];
@@ -45,10 +65,9 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const ApplyJobs jobs) {
   while (q + 1 < jobs.n && (int)blockIdx.x >= jobs.first[q + 1]) ++q;
   const ApplyJob& J = jobs.j[q];
   const int b0 = jobs.first[q], nb = jobs.first[q + 1] - b0;
-  float* sin1 = apsm;                    // kApRows x L
-  float* sin2 = sin1 + kApRows * L;      // kApRows x L
-  float* s1 = sin2 + kApRows * L;        // W x W
+  float* s1 = apsm;                      // W x W
   float* s2 = s1 + W * W;                // W x W
+  float* sin_base = s2 + W * W;          // 2 buffers x (IN1, IN2) x kApRows x L (cp.async double buffer)
   const int nout = J.nout;
   for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
     const int c = e / W, o = e % W;
@@ -57,11 +76,24 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const ApplyJobs jobs) {
   }
   const int64_t n = J.n;
   const bool vec_out = nout % 4 == 0 && J.col0 % 4 == 0 && J.ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(J.OUT) & 15) == 0;
-  for (int64_t i0 = (int64_t)(blockIdx.x - b0) * kApRows; i0 < n; i0 += (int64_t)nb * kApRows) {
+  const int64_t step = (int64_t)nb * kApRows;
+  auto stage = [&](int64_t i0, int slot) {
+    if (i0 < n) {
+      const int nr = (int)(n - i0 < kApRows ? n - i0 : kApRows);
+      stage_rows_async<W>(J.IN1, i0, nr, sin_base + slot * 2 * kApRows * L);
+      if (J.IN2) stage_rows_async<W>(J.IN2, i0, nr, sin_base + (slot * 2 + 1) * kApRows * L);
+    }
+    cp_async_commit();
+  };
+  const int64_t first = (int64_t)(blockIdx.x - b0) * kApRows;
+  stage(first, 0);
+  stage(first + step, 1);
+  int it = 0;
+  for (int64_t i0 = first; i0 < n; i0 += step, ++it) {
     const int nr = (int)(n - i0 < kApRows ? n - i0 : kApRows);
-    __syncthreads();
-    stage_rows_in<W>(J.IN1, i0, nr, sin1);
-    if (J.IN2) stage_rows_in<W>(J.IN2, i0, nr, sin2);
+    float* sin1 = sin_base + (it & 1) * 2 * kApRows * L;
+    float* sin2 = sin1 + kApRows * L;
+    cp_async_wait<1>();  // this tile's group has landed (the next one may still be in flight)
     __syncthreads();
     float acc[W];
 #pragma unroll
@@ -88,6 +120,8 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const ApplyJobs jobs) {
         }
       }
     }
+    __syncthreads();  // every row of this buffer has been read: stage the tile after next into it
+    stage(i0 + 2 * step, it & 1);
     // outputs straight from registers: this thread's row, 16-byte stores when aligned
     if (threadIdx.x < nr) {
       float* orow = J.OUT + (i0 + threadIdx.x) * J.ldo + J.col0;
@@ -117,7 +151,7 @@ static int assign_blocks(const int64_t* n, int njobs, int* first) {
 
 template <int W>
 static void apply_small_t(ApplyJobs& jobs, cudaStream_t st) {
-  constexpr int smem = (2 * kApRows * ap_ld(W) + 2 * W * W) * (int)sizeof(float);
+  constexpr int smem = (4 * kApRows * ap_ld(W) + 2 * W * W) * (int)sizeof(float);
   static std::atomic<unsigned> attr{0};
   ensure_smem(k_apply_small<W>, smem, attr);
   int64_t n[kMaxApply];
@@ -148,15 +182,15 @@ void launch_apply_small(const float* IN1, const float* S1, const float* IN2, con
 // OUT = IN S with S in fp64 and fp64 accumulation (orthonormalisation: keeps Q orthonormal to
 // fp32 rounding instead of cond(IN) * eps32).  Same staging as above; one launch for both sides.
 template <int W>
-__global__ void __launch_bounds__(kApRows) k_apply64(const Apply64Jobs jobs) {
+__global__ void __launch_bounds__(kApRows) k_apply64(const __grid_constant__ Apply64Jobs jobs) {
   ::lrqmm::pdl_enter();
   constexpr int L = ap_ld(W);
   extern __shared__ __align__(16) double apsm64[];
   const int q = (jobs.n > 1 && (int)blockIdx.x >= jobs.first[1]) ? 1 : 0;
   const Apply64Job& J = jobs.j[q];
   const int b0 = jobs.first[q], nb = jobs.first[q + 1] - b0;
-  double* s = apsm64;                                      // W x W
-  float* sin = reinterpret_cast<float*>(apsm64 + W * W);   // kApRows x L
+  double* s = apsm64;                                           // W x W
+  float* sin_base = reinterpret_cast<float*>(apsm64 + W * W);   // 2 x kApRows x L (cp.async double buffer)
   for (int e = threadIdx.x; e < W * W; e += blockDim.x) s[e] = J.S[e];
   unsigned run[(W + 31) / 32];  // lane c: running column max of column c (+32)
 #pragma unroll
@@ -164,10 +198,19 @@ __global__ void __launch_bounds__(kApRows) k_apply64(const Apply64Jobs jobs) {
   __shared__ unsigned bmax[64];
   if (threadIdx.x < 64) bmax[threadIdx.x] = 0u;
   const int64_t n = J.n;
-  for (int64_t i0 = (int64_t)(blockIdx.x - b0) * kApRows; i0 < n; i0 += (int64_t)nb * kApRows) {
+  const int64_t step = (int64_t)nb * kApRows;
+  auto stage = [&](int64_t i0, int slot) {
+    if (i0 < n) stage_rows_async<W>(J.IN, i0, (int)(n - i0 < kApRows ? n - i0 : kApRows), sin_base + slot * kApRows * L);
+    cp_async_commit();
+  };
+  const int64_t first = (int64_t)(blockIdx.x - b0) * kApRows;
+  stage(first, 0);
+  stage(first + step, 1);
+  int it = 0;
+  for (int64_t i0 = first; i0 < n; i0 += step, ++it) {
     const int nr = (int)(n - i0 < kApRows ? n - i0 : kApRows);
-    __syncthreads();
-    stage_rows_in<W>(J.IN, i0, nr, sin);
+    const float* sin = sin_base + (it & 1) * kApRows * L;
+    cp_async_wait<1>();  // this tile's group has landed (the next one may still be in flight)
     __syncthreads();
     double acc[W];
 #pragma unroll
@@ -183,6 +226,8 @@ __global__ void __launch_bounds__(kApRows) k_apply64(const Apply64Jobs jobs) {
           for (int o = 0; o < W; ++o) acc[o] = fma(xs[j], s[(4 * c4 + j) * W + o], acc[o]);
       }
     }
+    __syncthreads();  // every row of this buffer has been read: stage the tile after next into it
+    stage(i0 + 2 * step, it & 1);
     if (threadIdx.x < nr) {  // outputs straight from registers (16-byte stores of this thread's row)
       float4* orow = reinterpret_cast<float4*>(J.OUT + (i0 + threadIdx.x) * W);
 #pragma unroll
@@ -212,7 +257,7 @@ __global__ void __launch_bounds__(kApRows) k_apply64(const Apply64Jobs jobs) {
 
 template <int W>
 static void apply64_t(Apply64Jobs& jobs, cudaStream_t st) {
-  constexpr int smem = W * W * (int)sizeof(double) + kApRows * ap_ld(W) * (int)sizeof(float);
+  constexpr int smem = W * W * (int)sizeof(double) + 2 * kApRows * ap_ld(W) * (int)sizeof(float);
   static std::atomic<unsigned> attr{0};
   ensure_smem(k_apply64<W>, smem, attr);
   int64_t n[2] = {jobs.j[0].n, jobs.n > 1 ? jobs.j[1].n : 0};

@@ -324,20 +324,12 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
   __shared__ uint64_t ld_bar[2];
   __shared__ int ticket;
   constexpr int npairs = W * W;
-  // Gram in 4 x 4 register tiles: tile (a, c), a <= c, of T x T tiles; G row groups per block
-  constexpr int T = W / 4;
-  constexpr int U = T * (T + 1) / 2;
-  constexpr int G = 256 / U;
-  int ta = 0, tc = 0;
-  const int tu = threadIdx.x % U, tg = threadIdx.x / U;
-  const bool gram_thread = threadIdx.x < U * G;
-  {
-    int u = tu;
-    for (int a = 0; a < T; ++a) {
-      if (u < T - a) { ta = a; tc = a + u; break; }
-      u -= T - a;
-    }
-  }
+  // Gram on the fp64 tensor cores (DMMA m8n8k4): for a 4-row slice r0..r0+3 of the chunk, lane l
+  // holds v[a] = Y[r0 + l%4][8a + l/4] -- at once the A fragment (rows 8a..8a+7 of Y^T) and the B
+  // fragment (columns 8b..8b+7 of Y) of every 8 x 8 block (a, b), a <= b, of G.  Each fp32 is
+  // converted once and feeds NB DMMAs from registers (the FFMA-tile form was shared-memory bound).
+  constexpr int NB = W / 8, NBLK = NB * (NB + 1) / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t rpb = (jb.n + gridDim.x - 1) / gridDim.x;
   const int64_t r_begin = (int64_t)blockIdx.x * rpb;
   const int64_t r_end = (jb.n < r_begin + rpb) ? jb.n : r_begin + rpb;
@@ -361,48 +353,56 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
     if (nchunk > 0) issue(0);
     if (nchunk > 1) issue(1);
   }
-  double acc[16];
+  double acc[NBLK][2];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  for (int q = 0; q < NBLK; ++q) acc[q][0] = acc[q][1] = 0.0;
   for (int c = 0; c < nchunk; ++c) {
     const int64_t r0 = r_begin + (int64_t)c * kFRows;
     const int nr = (int)(r_end - r0 < kFRows ? r_end - r0 : kFRows);
     mbar_wait(&ld_bar[c & 1], (c >> 1) & 1);
     const float* bY = buf + (c & 1) * kFRows * W;
-    if (gram_thread) {
-      for (int i = tg; i < nr; i += G) {
-        const float4 x4 = *reinterpret_cast<const float4*>(bY + i * W + 4 * ta);
-        const float4 y4 = *reinterpret_cast<const float4*>(bY + i * W + 4 * tc);
-        const double xa[4] = {x4.x, x4.y, x4.z, x4.w}, yc[4] = {y4.x, y4.y, y4.z, y4.w};
+    for (int sl = warp; 4 * sl < nr; sl += 8) {
+      const int rr = 4 * sl + (lane & 3);
+      double v[NB];
 #pragma unroll
-        for (int p = 0; p < 4; ++p)
+      for (int a = 0; a < NB; ++a) v[a] = rr < nr ? (double)bY[rr * W + 8 * a + (lane >> 2)] : 0.0;
+      int blk = 0;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[p * 4 + q] = fma(xa[p], yc[q], acc[p * 4 + q]);
-      }
+      for (int a = 0; a < NB; ++a)
+#pragma unroll
+        for (int b = a; b < NB; ++b, ++blk)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[blk][0]), "+d"(acc[blk][1])
+                       : "d"(v[a]), "d"(v[b]));
     }
-    __syncthreads();  // every thread is done with buffer (c & 1): refill it with chunk c + 2
+    __syncthreads();  // every warp is done with buffer (c & 1): refill it with chunk c + 2
     if (threadIdx.x == 0 && c + 2 < nchunk) issue(c + 2);
   }
-  // fixed-order reduction of the G row groups of each tile, then the block partial (both halves)
-  __syncthreads();
-  double (*red)[16] = reinterpret_cast<double (*)[16]>(dyn);  // (G * U) x 16
-  if (gram_thread)
+  // fixed-order sum of the 8 warps' blocks (warp 0 stores, warps 1..7 add in turn), then the block
+  // partial, both halves (block (a, a): the entry with row <= col goes to both positions)
+  double* S = dyn;  // NBLK x 64 (the chunk buffers are free)
+  for (int w = 0; w < 8; ++w) {
+    if (warp == w)
 #pragma unroll
-    for (int q = 0; q < 16; ++q) red[tg * U + tu][q] = acc[q];
-  __syncthreads();
+      for (int q = 0; q < NBLK; ++q)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) S[q * 64 + 2 * lane + i] = w == 0 ? acc[q][i] : S[q * 64 + 2 * lane + i] + acc[q][i];
+    __syncthreads();
+  }
   double* part = jb.gpart + (int64_t)blockIdx.x * npairs;
-  for (int e = threadIdx.x; e < U * 16; e += 256) {
-    const int u = e / 16, q = e % 16;
-    double sum = 0.0;
-    for (int g = 0; g < G; ++g) sum += red[g * U + u][q];
-    int a = 0, c = 0, uu = u;
-    for (int aa = 0; aa < T; ++aa) {
-      if (uu < T - aa) { a = aa; c = aa + uu; break; }
-      uu -= T - aa;
+  for (int e = threadIdx.x; e < NBLK * 64; e += 256) {
+    int q = e / 64, a = 0, b = 0;
+    for (int aa = 0, k = q; aa < NB; ++aa) {
+      if (k < NB - aa) { a = aa; b = aa + k; break; }
+      k -= NB - aa;
     }
-    const int i = 4 * a + q / 4, j = 4 * c + q % 4;
-    part[i * W + j] = sum;  // diagonal tiles: (p, q) and (q, p) hold bitwise-equal sums
-    part[j * W + i] = sum;
+    const int l = (e % 64) / 2, i = e % 2;
+    const int row = 8 * a + l / 4, col = 8 * b + 2 * (l % 4) + i;
+    const double val = S[e];
+    if (a != b || row <= col) {
+      part[row * W + col] = val;
+      part[col * W + row] = val;
+    }
   }
   // two-level fixed-order reduction of the block partials: the last block of each group of 16
   // sums its group (-> gpart[nb + g]), the last group finisher sums the groups (-> G).  Counters:

@@ -102,9 +102,10 @@ def test_nonfinite_is_reported():
 
 
 # ------------------------------------------------------------ K6 / K7 int GEMM
-@pytest.fixture(params=[1, 2], ids=["gemm1cta", "gemm2cta"])
+@pytest.fixture(params=[1, 2, 3], ids=["gemm1cta", "gemm2cta", "gemm_tc_corr"])
 def gemm_variant(request):
-    """Runs the test with the one-CTA GEMM (K6) and the CTA-pair GEMM (K7) forced."""
+    """Runs the test with the one-CTA GEMM (K6, FFMA correction), the CTA-pair GEMM (K7) and the
+    one-CTA GEMM with the tensor-core correction (K8) forced."""
     lib = L.load_library()
     assert lib.lrqmm_debug_set_gemm_variant(request.param) == 0
     yield request.param
