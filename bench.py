@@ -765,6 +765,7 @@ def main():
         "roofline": {"bound": "tensor",
                      "kernel": ("k7_gemm_i8_2sm (CTA-pair tcgen05.mma.cta_group::2 kind::i8 + fused LRQMM epilogue)"
                                 if Mloc >= 512 and N >= 512 and ((Mloc + 255) // 256) * ((N + 255) // 256) >= 512
+                                and (r == 0 or K > 2048)
                                 else ("k8_gemm_tc (tcgen05 kind::i8 + the rank-2r correction as bf16 hi/lo "
                                       "kind::f16 MMAs into a second TMEM accumulator)" if r > 0 else
                                       "k6_gemm_i8 (tcgen05 kind::i8 + dequantising epilogue)")),  # gemm_i8.cu rules

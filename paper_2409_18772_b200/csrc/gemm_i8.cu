@@ -978,7 +978,10 @@ int encode_map_2d_sw(void* map, int dtype, const void* base, uint64_t inner, uin
 }
 
 int& gemm_variant() {  // 0 auto, 1 force one-CTA K6, 2 force CTA-pair K7, 3 force K8 (test hook)
-  static int v = 0;
+  static int v = [] {
+    const char* e = getenv("LRQMM_GEMM_VARIANT");  // A/B timing of the kernel choice
+    return e ? atoi(e) : 0;
+  }();
   return v;
 }
 
@@ -1054,12 +1057,14 @@ static void launch_t7(G6Params p, const CUtensorMap* mA, const CUtensorMap* mB, 
   k7_gemm_i8_2sm<kR2><<<2 * pairs, g7::kThreads, kSmem, st>>>(*mA, *mB, p); ++launch_counter();
 }
 
-// the tensor-core correction kernel K8 replaces K6 for the fused LRQMM epilogue (R2 > 0) unless a
-// test forces another variant or LRQMM_NO_TC_CORR is set
-bool gemm_uses_tc(int64_t M, int64_t N, int R2, const int* sched) {
+// the tensor-core correction kernel K8 runs the fused LRQMM epilogue (R2 > 0) wherever the FFMA
+// correction would not hide behind a long main loop: every shape the one-CTA K6 would take, and
+// CTA-pair shapes with K <= 2048 (c4: layer2-3 1x1 convolutions 1.02 -> 0.69 ms with K8 instead
+// of K7).  Tests force a variant; LRQMM_NO_TC_CORR turns K8 off.
+bool gemm_uses_tc(int64_t M, int64_t N, int Kp, int R2, const int* sched) {
   static const bool off = getenv("LRQMM_NO_TC_CORR") != nullptr;
   if (R2 <= 0 || off || gemm_variant() == 1 || gemm_variant() == 2) return false;
-  return gemm_variant() == 3 || !use_2sm(M, N, sched);
+  return gemm_variant() == 3 || !use_2sm(M, N, sched) || Kp <= 2048;
 }
 
 static void launch_k8(const GemmArgs& g, const CUtensorMap* mA, const CUtensorMap* mB, const CUtensorMap* tc,
@@ -1114,7 +1119,7 @@ int launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStrea
   const CUtensorMap* mA = reinterpret_cast<const CUtensorMap*>(mapA);
   const CUtensorMap* mB = reinterpret_cast<const CUtensorMap*>(mapB);
   const int r2 = g.epi == 0 ? 0 : g.R2;
-  if (g.tc_maps && gemm_uses_tc(g.M, g.N, r2, g.sched)) {
+  if (g.tc_maps && gemm_uses_tc(g.M, g.N, g.Kp, r2, g.sched)) {
     launch_k8(g, mA, mB + 2, reinterpret_cast<const CUtensorMap*>(g.tc_maps), nsm, st);  // B box 128 rows
     return 0;
   }

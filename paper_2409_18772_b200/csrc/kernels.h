@@ -372,7 +372,7 @@ struct GemmTcOperands {
 };
 int gemm_prepare_maps_tc(const GemmTcOperands& o, void* maps);  // 4 maps; 0 on success
 // whether launch_gemm will run K8 for these sizes (R2 > 0): then L_A / L_B must be split first
-bool gemm_uses_tc(int64_t M, int64_t N, int R2, const int* sched);
+bool gemm_uses_tc(int64_t M, int64_t N, int Kp, int R2, const int* sched);
 // L (rows x R2 fp32) -> hi, lo (rows x 64 bf16, zero-padded)
 void launch_split_bf16(const float* L, int64_t rows, int R2, void* hi, void* lo, cudaStream_t st);
 // mapA / mapB: arrays of four CUtensorMap (one-CTA, CTA-pair and narrow-N box shapes); 0 on success

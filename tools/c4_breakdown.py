@@ -26,7 +26,7 @@ calls, cur = [], []
 for k in order:
     n = data[k]['name']
     cur.append(k)
-    if 'gemm_i8' in n:
+    if 'gemm_i8' in n or 'gemm_tc' in n:
         calls.append(cur)
         cur = []
 second = [c for i, c in enumerate(calls) if i % 2 == 1]
