@@ -54,9 +54,11 @@ LRQMM_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "me
 template <int N>
 LRQMM_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// OUT[i, col0 + o] = sum_c IN1[i,c] S1[c,o] (+ sum_c IN2[i,c] S2[c,o]),  o < nout (<= W).
+// OUT[i, col0 + o] = sum_c IN1[i,c] S1[c,o] (+ sum_c IN2[i,c] S2[c,o]),  o < nout (<= NO <= W).
 // Up to kMaxApply jobs per launch: job q owns blocks [first[q], first[q+1]) and walks its rows.
-template <int W>
+// NO = the outputs computed per row (nout rounded up to 8): no FMAs or shared-memory reads for the
+// W - NO columns that no job writes (the factor assembly writes r of W).
+template <int W, int NO>
 __global__ void __launch_bounds__(kApRows) k_apply_small(const __grid_constant__ ApplyJobs jobs) {
   ::lrqmm::pdl_enter();
   constexpr int L = ap_ld(W);
@@ -65,12 +67,12 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const __grid_constant__
   while (q + 1 < jobs.n && (int)blockIdx.x >= jobs.first[q + 1]) ++q;
   const ApplyJob& J = jobs.j[q];
   const int b0 = jobs.first[q], nb = jobs.first[q + 1] - b0;
-  float* s1 = apsm;                      // W x W
-  float* s2 = s1 + W * W;                // W x W
-  float* sin_base = s2 + W * W;          // 2 buffers x (IN1, IN2) x kApRows x L (cp.async double buffer)
+  float* s1 = apsm;                      // W x NO
+  float* s2 = s1 + W * NO;               // W x NO
+  float* sin_base = s2 + W * NO;         // 2 buffers x (IN1, IN2) x kApRows x L (cp.async double buffer)
   const int nout = J.nout;
-  for (int e = threadIdx.x; e < W * W; e += blockDim.x) {
-    const int c = e / W, o = e % W;
+  for (int e = threadIdx.x; e < W * NO; e += blockDim.x) {
+    const int c = e / NO, o = e % NO;
     s1[e] = o < nout ? J.S1[c * J.ldS + o] : 0.f;
     s2[e] = (J.IN2 && o < nout) ? J.S2[c * J.ldS + o] : 0.f;
   }
@@ -95,28 +97,28 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const __grid_constant__
     float* sin2 = sin1 + kApRows * L;
     cp_async_wait<1>();  // this tile's group has landed (the next one may still be in flight)
     __syncthreads();
-    float acc[W];
+    float acc[NO];
 #pragma unroll
-    for (int o = 0; o < W; ++o) acc[o] = 0.f;
+    for (int o = 0; o < NO; ++o) acc[o] = 0.f;
     if (threadIdx.x < nr) {
-#pragma unroll
+#pragma unroll(W <= 32 ? W / 4 : 2)  // bounded unrolling for the wide sketches (build time)
       for (int c4 = 0; c4 < W / 4; ++c4) {
         const float4 v = *reinterpret_cast<const float4*>(sin1 + threadIdx.x * L + 4 * c4);
         const float xs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
-          for (int o = 0; o < W; ++o) acc[o] = fmaf(xs[j], s1[(4 * c4 + j) * W + o], acc[o]);
+          for (int o = 0; o < NO; ++o) acc[o] = fmaf(xs[j], s1[(4 * c4 + j) * NO + o], acc[o]);
       }
       if (J.IN2) {
-#pragma unroll
+#pragma unroll(W <= 32 ? W / 4 : 2)
         for (int c4 = 0; c4 < W / 4; ++c4) {
           const float4 v = *reinterpret_cast<const float4*>(sin2 + threadIdx.x * L + 4 * c4);
           const float xs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j)
 #pragma unroll
-            for (int o = 0; o < W; ++o) acc[o] = fmaf(xs[j], s2[(4 * c4 + j) * W + o], acc[o]);
+            for (int o = 0; o < NO; ++o) acc[o] = fmaf(xs[j], s2[(4 * c4 + j) * NO + o], acc[o]);
         }
       }
     }
@@ -127,11 +129,11 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const __grid_constant__
       float* orow = J.OUT + (i0 + threadIdx.x) * J.ldo + J.col0;
       if (vec_out) {
 #pragma unroll
-        for (int o4 = 0; o4 < W / 4; ++o4)
+        for (int o4 = 0; o4 < NO / 4; ++o4)
           if (4 * o4 < nout) *reinterpret_cast<float4*>(orow + 4 * o4) = make_float4(acc[4 * o4], acc[4 * o4 + 1], acc[4 * o4 + 2], acc[4 * o4 + 3]);
       } else {
 #pragma unroll
-        for (int o = 0; o < W; ++o)
+        for (int o = 0; o < NO; ++o)
           if (o < nout) orow[o] = acc[o];
       }
     }
@@ -149,15 +151,25 @@ static int assign_blocks(const int64_t* n, int njobs, int* first) {
   return first[njobs];
 }
 
-template <int W>
+template <int W, int NO>
 static void apply_small_t(ApplyJobs& jobs, cudaStream_t st) {
-  constexpr int smem = (4 * kApRows * ap_ld(W) + 2 * W * W) * (int)sizeof(float);
+  constexpr int smem = (4 * kApRows * ap_ld(W) + 2 * W * NO) * (int)sizeof(float);
   static std::atomic<unsigned> attr{0};
-  ensure_smem(k_apply_small<W>, smem, attr);
+  ensure_smem(k_apply_small<W, NO>, smem, attr);
   int64_t n[kMaxApply];
   for (int q = 0; q < jobs.n; ++q) n[q] = jobs.j[q].n;
   const int grid = assign_blocks(n, jobs.n, jobs.first);
-  launch_pdl(k_apply_small<W>, grid, kApRows, smem, st, jobs);
+  launch_pdl(k_apply_small<W, NO>, grid, kApRows, smem, st, jobs);
+}
+// NO = W - 8 covers the factor assembly for the default oversampling (r + 5 <= W = roundup(r + p, 8)
+// puts roundup(r, 8) at W - 8 or W); everything else computes all W columns (instantiations and
+// build time stay bounded)
+template <int W>
+static void apply_small_w(ApplyJobs& jobs, int no, cudaStream_t st) {
+  if constexpr (W >= 16) {
+    if (no <= W - 8) return apply_small_t<W, W - 8>(jobs, st);
+  }
+  apply_small_t<W, W>(jobs, st);
 }
 
 void launch_apply_jobs(const ApplyJobs& in, int W, cudaStream_t st) {
@@ -165,7 +177,9 @@ void launch_apply_jobs(const ApplyJobs& in, int W, cudaStream_t st) {
   for (int q = 0; q < in.n; ++q)
     if (in.j[q].n > 0 && in.j[q].nout > 0) jobs.j[jobs.n++] = in.j[q];
   if (jobs.n == 0) return;
-#define AS_CASE(w) case w: apply_small_t<w>(jobs, st); break;
+  int no = 0;
+  for (int q = 0; q < jobs.n; ++q) no = jobs.j[q].nout > no ? jobs.j[q].nout : no;
+#define AS_CASE(w) case w: apply_small_w<w>(jobs, no, st); break;
   switch (W) { AS_CASE(8) AS_CASE(16) AS_CASE(24) AS_CASE(32) AS_CASE(40) AS_CASE(48) AS_CASE(56) AS_CASE(64) default: break; }
 #undef AS_CASE
   ++launch_counter();
@@ -216,7 +230,7 @@ __global__ void __launch_bounds__(kApRows) k_apply64(const __grid_constant__ App
 #pragma unroll
     for (int o = 0; o < W; ++o) acc[o] = 0.0;
     if (threadIdx.x < nr) {
-#pragma unroll
+#pragma unroll(W <= 32 ? W / 4 : 2)  // bounded unrolling for the wide sketches (build time)
       for (int c4 = 0; c4 < W / 4; ++c4) {
         const float4 v = *reinterpret_cast<const float4*>(sin + threadIdx.x * L + 4 * c4);
         const double xs[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
