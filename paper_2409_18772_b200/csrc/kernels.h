@@ -147,6 +147,7 @@ struct TcPassSide {
   const unsigned* cmax2;
   const uint8_t* pimg1;   // prebuilt B image of P1 / P2 (launch_apply_prep), or nullptr: built by the pass
   const uint8_t* pimg2;
+  int sm_reserve;         // SMs the pass leaves free (another graph branch's small kernels run there)
 };
 enum { kPassRow = 0, kPassDual = 1, kPassCol = 2, kPassCodes = 3 };
 void launch_tc_pass(int kind, int nsides, const TcPassSide* sides, int W, bool reduce1, int* ns_out, cudaStream_t st);

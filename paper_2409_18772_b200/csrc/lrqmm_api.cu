@@ -102,6 +102,8 @@ struct lrqmm_handle_s {
   cudaStream_t cap_st = nullptr;
   cudaStream_t side_st = nullptr;                      // forked branch (cross Gram || truncation)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;  // the two sides' range finders as graph branches
+  int pass_sm_reserve = 0;  // while they run: SMs each persistent pass leaves to the other branch
   cudaGraphExec_t rsvd_exec[3] = {};  // per rsvd_body kind
   int rsvd_calls[3] = {};
   int64_t rsvd_graph_kernels[3] = {};
@@ -257,6 +259,8 @@ lrqmm_status_t lrqmm_destroy(lrqmm_handle_t h) {
   if (h->side_st) cudaStreamDestroy(h->side_st);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->ev_fork2) cudaEventDestroy(h->ev_fork2);
+  if (h->ev_join2) cudaEventDestroy(h->ev_join2);
   delete h->comm;
   delete h;
   return LRQMM_OK;
@@ -585,7 +589,7 @@ static void pass_sides(lrqmm_handle_t h, int kind, int sides, const float* const
       ps[n] = TcPassSide{view(h, sd), P1 ? P1[sd] : nullptr, P2 ? P2[sd] : nullptr, O1 ? O1[sd] : nullptr,
                          O2 ? O2[sd] : nullptr, part_of(h, sd), part_elems(h), h->s[sd].img,
                          cm1 ? cm1[sd] : nullptr, cm2 ? cm2[sd] : nullptr, pi1 ? pi1[sd] : nullptr,
-                         pi2 ? pi2[sd] : nullptr};
+                         pi2 ? pi2[sd] : nullptr, h->pass_sm_reserve};
       idx[n++] = sd;
     }
   int ns[2] = {0, 0};
@@ -734,12 +738,10 @@ static lrqmm_status_t rsvd_chain(lrqmm_handle_t h, int sides, int kind) {
 // on a forked branch (side stream, event fork/join; captured into the graph as a parallel branch)
 // while the one-CTA-per-side eigensolver occupies two SMs.
 static lrqmm_status_t fork_cross_gram(lrqmm_handle_t h) {
-  if (!h->side_st) {
-    if (cudaStreamCreateWithFlags(&h->side_st, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess)
-      return LRQMM_ERR_CUDA;
-  }
+  if (!h->side_st && cudaStreamCreateWithFlags(&h->side_st, cudaStreamNonBlocking) != cudaSuccess) return LRQMM_ERR_CUDA;
+  if (!h->ev_fork && (cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+                      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess))
+    return LRQMM_ERR_CUDA;
   LQ_CUDA(cudaEventRecord(h->ev_fork, h->st));
   LQ_CUDA(cudaStreamWaitEvent(h->side_st, h->ev_fork, 0));
   GramJobs j{};
@@ -797,7 +799,37 @@ static lrqmm_status_t rsvd_body(lrqmm_handle_t h, int kind) {
   float* Q1s[2] = {h->s[0].Q1, h->s[1].Q1};
   const int sides = kind == 0 ? 3 : (kind == 1 ? 1 : 2);
   lrqmm_status_t e;
-  if ((e = rsvd_chain(h, sides, kind)) != LRQMM_OK) return e;
+  // Range finders: one rank, both sides -> two independent branches (side B on the side stream), so
+  // that one side's streaming passes run while the other side's serial small solves (Gram, CholQR,
+  // apply, image prep) would otherwise leave the GPU idle; they join before S3, which needs both Q1.
+  // With NCCL (world > 1) every collective must stay in one stream order: one branch.
+  const bool branches = kind == 0 && h->cfg.world_size == 1 && h->s[0].rows > 0 && h->s[1].rows > 0 &&
+                        !getenv("LRQMM_RSVD_ONE_STREAM");
+  if (branches) {
+    if (!h->side_st && cudaStreamCreateWithFlags(&h->side_st, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(h, LRQMM_ERR_CUDA);
+    if (!h->ev_fork2 && (cudaEventCreateWithFlags(&h->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
+                         cudaEventCreateWithFlags(&h->ev_join2, cudaEventDisableTiming) != cudaSuccess))
+      return fail(h, LRQMM_ERR_CUDA);
+    LQ_CUDA(cudaEventRecord(h->ev_fork2, h->st));
+    LQ_CUDA(cudaStreamWaitEvent(h->side_st, h->ev_fork2, 0));
+    static const int reserve = [] {
+      const char* v = getenv("LRQMM_BRANCH_SMS");
+      return v ? atoi(v) : 16;
+    }();
+    h->pass_sm_reserve = reserve;
+    if ((e = rsvd_chain(h, 1, kind)) != LRQMM_OK) return e;
+    cudaStream_t main_st = h->st;
+    h->st = h->side_st;
+    e = rsvd_chain(h, 2, kind);
+    h->st = main_st;
+    h->pass_sm_reserve = 0;
+    if (e != LRQMM_OK) return e;
+    LQ_CUDA(cudaEventRecord(h->ev_join2, h->side_st));
+    LQ_CUDA(cudaStreamWaitEvent(h->st, h->ev_join2, 0));
+  } else if ((e = rsvd_chain(h, sides, kind)) != LRQMM_OK) {
+    return e;
+  }
   int nsp[2] = {1, 1};
   if (h->cfg.power_iters == 0) {
     const int64_t kdim[2] = {h->cfg.k, h->cfg.k};

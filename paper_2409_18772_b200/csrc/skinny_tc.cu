@@ -925,9 +925,8 @@ static void run_tc(int nsides, const TcPassSide* sides, int W, bool reduce1, int
   constexpr bool kHasU = C::kHasU, kHasC = C::kHasC;
   static std::atomic<unsigned> attr{0};
   ensure_smem(k_tc_proj<kMode, NA, kVar, false>, C::kSmem, attr);
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int nsm = sm_count();
+  if (sides[0].sm_reserve > 0 && sides[0].sm_reserve < nsm / 2) nsm -= sides[0].sm_reserve;
   TcArgs2 args{};
   alignas(64) TcMaps2 maps;
   memset(&maps, 0, sizeof(maps));
