@@ -573,7 +573,7 @@ static bool launch_k1_tma_t(const QuantArgs& a, bool fixed, cudaStream_t st) {
   const int slot = (a.K * 4 + 1023) / 1024 * 1024;
   int ns = k1t::kSmemBudget / slot;
   if (ns > 8) ns = 8;
-  if (ns < 2) return false;
+  if (ns < 1) return false;
   const int smem = 1024 + ns * slot;
   const int nsm = sm_count();
   const int grid = (int)(a.rows < nsm ? a.rows : nsm);
@@ -607,6 +607,9 @@ static bool launch_k1_tma(const QuantArgs& a, bool fixed, cudaStream_t st) {
   if (Kp <= C4 * 4) return launch_k1_tma_t<4>(a, fixed, st);
   if (Kp <= C4 * 8) return launch_k1_tma_t<8>(a, fixed, st);
   if (Kp <= C4 * 12) return launch_k1_tma_t<12>(a, fixed, st);
+  // long rows (c5: K = 32768, 128 KB): one ring slot -- the consumers hold the row in registers
+  // and release the slot before they quantize, so the next row still streams in meanwhile
+  if (Kp <= C4 * 16) return launch_k1_tma_t<16>(a, fixed, st);
   return false;
 }
 

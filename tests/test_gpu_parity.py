@@ -52,7 +52,7 @@ def run_gpu(A, Bt, bits, r, p, OmA=None, OmB=None, q=1, rounding="floor", gran="
 @pytest.mark.parametrize("bits", [4, 8])
 @pytest.mark.parametrize("rounding", ["floor", "trunc", "nearest"])
 @pytest.mark.parametrize("gran", ["row", "tensor"])
-@pytest.mark.parametrize("shape", [(300, 1000), (130, 130), (5, 40000), (1000, 77)])
+@pytest.mark.parametrize("shape", [(300, 1000), (130, 130), (5, 40000), (7, 30000), (1000, 77)])
 def test_quantize_bit_exact(bits, rounding, gran, shape):
     rows, K = shape
     X = S.gen_matrix("normal", rows, K, 7 + bits)

@@ -62,6 +62,7 @@ int main(int argc, char** argv) {
   double* dG; float* dT; unsigned long long* dt;
   cudaMalloc(&dG, 8 * G.size()); cudaMalloc(&dT, 4 * G.size()); cudaMalloc(&dt, 8);
   cudaMemcpy(dG, G.data(), 8 * G.size(), cudaMemcpyHostToDevice);
+  run<512>(dG, dT, dt);
   run<256>(dG, dT, dt);
   run<128>(dG, dT, dt);
   run<64>(dG, dT, dt);
