@@ -11,6 +11,8 @@
 //   d = fma(lambda, x, -n) has the sign of the exact lambda x - n, so
 //   floor = n - (d < 0), ceil = n + (d > 0), trunc = floor / ceil by sign, nearest = n.
 //   (d underflows to 0 only for n = 0 with |lambda x| < 2^-149: then x decides floor.)
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -806,6 +808,282 @@ __global__ void __launch_bounds__(256) k1_quantize_im2col(const float* __restric
   }
 }
 
+// Tiled implicit im2col (dw == 1, kw >= sw: the window leaves no gaps).  A CTA owns TW
+// consecutive output pixels (b, ho, wo0 .. wo0 + TW - 1) at a time: their input window -- kh
+// input rows x WI = (TW - 1) sw + kw pixels x C channels, zero outside the image -- is staged in
+// shared memory by cp.async (zero-fill for the padding), double buffered so the next tile's window
+// is in flight while this one is quantized.  With dw == 1, column k = (i kw + j) C + c of output
+// pixel wl sits at window[i RS + wl sw C + (j C + c)], so a per-CTA table off[k] = i RS + (j C + c)
+// turns every element into two shared loads (one table load per quad of columns when C % 4 == 0)
+// -- no per-element index arithmetic, no L1 / L2 gathers.  Padded columns K <= k < Kp point into a
+// zeroed strip behind the window.  A row is handled by LPR lanes (32 / LPR rows per warp, so short
+// rows -- the 7x7 stem's 147 columns = 40 quads = 8 lanes x 5 -- leave no lanes idle and share
+// the per-row reduction / division); columns go in quads, so the codes and both Q15 planes are
+// written with 4-byte stores.  Arithmetic and results identical to k1_quantize_im2col (same amax,
+// lambda, code_fast / q15_fast / u_q15_slow).
+namespace im2t {
+constexpr int kThreads = 256;
+constexpr int kBudget = 100 * 1024;  // dynamic shared memory per CTA (two windows + zero strip + table)
+struct Tile {
+  int TW, ntw, WI, RS;  // tile width (output pixels), tiles per output row, window pixels, row stride (floats)
+  int zero;             // floats of the zero strip (0: no padded columns)
+};
+// one staged window, rounded up to 16 bytes
+__host__ __device__ inline int tile_floats(const ConvGeom& g, const Tile& t) { return (g.kh * t.RS + 3) & ~3; }
+// two buffers, each a window followed by its zero strip, then the offset table
+inline int smem_bytes(const ConvGeom& g, const Tile& t, int Kp, bool vec) {
+  return 2 * (tile_floats(g, t) + t.zero) * 4 + (vec ? Kp / 4 : Kp) * 4;
+}
+// shared loads on 32-bit addresses; volatile (ordered against bar.sync) but no memory clobber, so
+// the global stores of the quantize pass stay free to overlap them
+__device__ __forceinline__ float ld1(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float4 ld4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int4 ld4i(uint32_t a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int ld1i(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+// global -> shared copy of E floats, zero-filled when !valid (src-size 0: nothing is read)
+template <int E>
+__device__ __forceinline__ void cp_zfill(uint32_t dst, const float* src, bool valid) {
+  if (E == 4)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+}  // namespace im2t
+
+template <int kMode, bool kVec, int VPT, int LPR>
+__global__ void __launch_bounds__(im2t::kThreads) k1_quantize_im2col_tile(
+    const float* __restrict__ X, const ConvGeom g, const im2t::Tile tl, int K, int Kp, int qmax,
+    int8_t* __restrict__ codes, float* __restrict__ lam_out, float* __restrict__ inv_out, int* __restrict__ err_flag,
+    uint8_t* __restrict__ U, int64_t ldu, int64_t uplane, int64_t ntiles) {
+  extern __shared__ float4 im2t_smem[];
+  float* win = reinterpret_cast<float*>(im2t_smem);
+  const int tf = im2t::tile_floats(g, tl);
+  const int bstride = tf + tl.zero;  // floats per buffer
+  int* off = reinterpret_cast<int*>(win + 2 * bstride);
+  const uint32_t s_win = (uint32_t)__cvta_generic_to_shared(win);
+  const uint32_t s_off = (uint32_t)__cvta_generic_to_shared(off);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int RPW = 32 / LPR;  // rows per warp
+  const int sub = lane / LPR, sl = lane - sub * LPR;
+  const int nq = Kp >> 2;  // column quads (Kp % 4 == 0)
+  const int KWC = g.kw * g.C;
+  // byte offsets from a pixel's window origin: i RS + (j C + c) floats, or (padded columns) the
+  // buffer's zero strip right behind its window
+  const int zoff = tf;
+  if (kVec) {  // quad table: a quad lies in one tap (C % 4 == 0)
+    for (int q = tid; q < nq; q += im2t::kThreads) {
+      const int k = q * 4, i = k / KWC;
+      off[q] = 4 * (k < K ? i * tl.RS + (k - i * KWC) : zoff);
+    }
+  } else {
+    for (int k = tid; k < Kp; k += im2t::kThreads) {
+      const int i = k / KWC;
+      off[k] = 4 * (k < K ? i * tl.RS + (k - i * KWC) : zoff);
+    }
+  }
+  for (int z = tid; z < tl.zero; z += im2t::kThreads) win[tf + z] = win[bstride + tf + z] = 0.f;
+  ::lrqmm::pdl_enter();
+  const int64_t img = (int64_t)g.H * g.W * g.C;
+  constexpr int E = kVec ? 4 : 1;
+  // stage the window of tile t into buffer `buf` (cp.async, one group per call)
+  auto stage = [&](int64_t t, int buf) {
+    if (t < ntiles) {
+      const int64_t bh = t / tl.ntw;
+      const int wt = (int)(t - bh * tl.ntw);
+      const int b = (int)(bh / g.Ho), ho = (int)(bh - (int64_t)b * g.Ho);
+      const int wi0 = wt * tl.TW * g.sw - g.pw;
+      const int flo = max(0, -wi0) * g.C, fhi = min(tl.WI, g.W - wi0) * g.C;
+      const float* xb = X + b * img + (int64_t)wi0 * g.C;
+      const int hb = ho * g.sh - g.ph;
+      const uint32_t dbase = s_win + 4u * (uint32_t)(buf * bstride);
+      for (int i = 0; i < g.kh; ++i) {  // staged row i: input row hb + i dh, contiguous in X
+        const int hi = hb + i * g.dh;
+        const bool inh = (unsigned)hi < (unsigned)g.H;
+        const float* src = xb + (int64_t)hi * g.W * g.C;
+        const uint32_t dst = dbase + 4u * (uint32_t)(i * tl.RS);
+        for (int f = tid * E; f < tl.RS; f += im2t::kThreads * E) {
+          const bool in = inh && f >= flo && f < fhi;
+          im2t::cp_zfill<E>(dst + 4u * f, in ? src + f : X, in);
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  constexpr int SPAN = LPR * VPT;  // quads per batch
+  const bool one = nq <= SPAN;     // the whole row stays in registers between the two passes
+  int buf = 0;
+  stage(blockIdx.x, 0);
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, buf ^= 1) {
+    stage(t + gridDim.x, buf ^ 1);  // the buffer the previous tile used (freed by the barrier below)
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();  // every thread's copies of this tile have landed
+    const int64_t bh = t / tl.ntw;
+    const int wo0 = (int)(t - bh * tl.ntw) * tl.TW;
+    const int tw = min(tl.TW, g.Wo - wo0);
+    const uint32_t s_buf = s_win + 4u * (uint32_t)(buf * bstride);
+    for (int wl0 = warp * RPW; wl0 < tw; wl0 += (im2t::kThreads / 32) * RPW) {
+      const int wl = wl0 + sub;
+      const bool active = wl < tw;
+      const uint32_t s_row = s_buf + 4u * (uint32_t)((active ? wl : 0) * g.sw * g.C);
+      const int64_t row = bh * g.Wo + wo0 + wl;
+      float v[VPT][4];
+      auto load = [&](int q0) {
+#pragma unroll
+        for (int u = 0; u < VPT; ++u) {
+          const int q = q0 + u * LPR + sl;
+          if (q >= nq) {  // past the row: keeps the amax / stores inert
+            v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0.f;
+            continue;
+          }
+          if (kVec) {
+            const float4 x = im2t::ld4(s_row + im2t::ld1i(s_off + 4u * q));
+            v[u][0] = x.x; v[u][1] = x.y; v[u][2] = x.z; v[u][3] = x.w;
+          } else {
+            const int4 o = im2t::ld4i(s_off + 16u * q);
+            v[u][0] = im2t::ld1(s_row + o.x);
+            v[u][1] = im2t::ld1(s_row + o.y);
+            v[u][2] = im2t::ld1(s_row + o.z);
+            v[u][3] = im2t::ld1(s_row + o.w);
+          }
+        }
+      };
+      float amax = 0.f;  // NaN-propagating, as k1_quantize_im2col
+      for (int q0 = 0; q0 < nq; q0 += SPAN) {
+        load(q0);
+#pragma unroll
+        for (int u = 0; u < VPT; ++u)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) amax = fmax_nan(amax, fabsf(v[u][e]));
+      }
+      if (active && !(amax <= 3.402823466e38f)) atomicOr(err_flag, 1);
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      const float lam = (amax == 0.f) ? 1.f : __fdiv_rn(static_cast<float>(qmax), amax);
+      if (active && sl == 0) {
+        lam_out[row] = lam;
+        inv_out[row] = __frcp_rn(lam);
+      }
+      if (!active) continue;  // no further shuffles below
+      const float l32 = lam * 32768.f;
+      uint32_t* crow = reinterpret_cast<uint32_t*>(codes + row * Kp) + sl;
+      uint32_t* urow = U ? reinterpret_cast<uint32_t*>(U + row * ldu) + sl : nullptr;
+      uint32_t* lrow = U ? reinterpret_cast<uint32_t*>(U + uplane + row * ldu) + sl : nullptr;
+      // pass 2, unswitched on the row-uniform choices (rounding form, residual planes or not)
+      auto emit = [&](auto kFast, auto kU) {
+        for (int q0 = 0; q0 < nq; q0 += SPAN) {
+          if (!one) load(q0);
+#pragma unroll
+          for (int u = 0; u < VPT; ++u) {
+            if (q0 + u * LPR + sl >= nq) continue;
+            int c[4], s[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              c[e] = code_fast<kMode>(lam, v[u][e], qmax);
+              if (decltype(kU)::value) s[e] = decltype(kFast)::value ? q15_fast<kMode>(l32, v[u][e], c[e])
+                                                                     : u_q15_slow(lam, v[u][e], c[e]);
+            }
+            crow[q0 + u * LPR] = bytes4(c[0], c[1], c[2], c[3]);
+            if (decltype(kU)::value) {
+              __stcg(urow + q0 + u * LPR, hbytes4(s[0], s[1], s[2], s[3]));
+              __stcg(lrow + q0 + u * LPR, bytes4(s[0], s[1], s[2], s[3]));
+            }
+          }
+        }
+      };
+      using T_ = std::true_type;
+      using F_ = std::false_type;
+      if (!U) emit(T_{}, F_{});
+      else if (lam < 0x1p100f) emit(T_{}, T_{});
+      else emit(F_{}, T_{});  // 2^15 lambda overflows (rows of ~1e-28)
+    }
+    __syncthreads();  // this buffer is free for the window staged in the next iteration
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+// tile geometry for the tiled kernel, or TW = 0 when it does not apply
+static im2t::Tile im2col_tile_geom(const ConvGeom& g, int Kp, bool vec) {
+  im2t::Tile t{0, 0, 0, 0, 0};
+  if (getenv("LRQMM_IM2COL_GATHER")) return t;
+  if (g.dw != 1 || g.kw < g.sw || Kp % 4 || g.Wo <= 0) return t;
+  const int K = g.kh * g.kw * g.C;
+  // zero strip read by the padded columns of every pixel of the tile (a quad of 4 when vec)
+  auto zero_strip = [&](int tw) { return K < Kp ? (((tw - 1) * g.sw * g.C + 4) + 3) & ~3 : 0; };
+  // per-CTA target (several CTAs per SM keep cp.async and the quantize pass overlapped); a tile
+  // narrower than min(8, Wo) pixels re-reads too much halo per row: the gather kernel then
+  static const int target = env_int("LRQMM_IM2COL_SMEM_KB", 56) * 1024;
+  static const int min_tw = env_int("LRQMM_IM2COL_MIN_TW", 8);
+  int tw = g.Wo < 64 ? g.Wo : 64;
+  for (;; tw = (tw + 1) / 2) {
+    const int WI = (tw - 1) * g.sw + g.kw;
+    im2t::Tile c{tw, 0, WI, WI * g.C, zero_strip(tw)};
+    const int bytes = im2t::smem_bytes(g, c, Kp, vec);
+    if (bytes <= target && bytes <= im2t::kBudget) break;
+    if (tw == 1) return t;
+  }
+  if (tw < (g.Wo < min_tw ? g.Wo : min_tw)) return t;
+  // balance: the fewest tiles of at most tw pixels, equal widths
+  const int ntw = (g.Wo + tw - 1) / tw;
+  t.TW = (g.Wo + ntw - 1) / ntw;
+  t.ntw = (g.Wo + t.TW - 1) / t.TW;
+  t.WI = (t.TW - 1) * g.sw + g.kw;
+  t.RS = t.WI * g.C;
+  t.zero = zero_strip(t.TW);
+  return t;
+}
+
+template <bool kVec, int VPT, int LPR>
+static void im2col_tile_t(const QuantArgs& a, const ConvGeom& g, const im2t::Tile& tl, cudaStream_t st) {
+  const int smem = im2t::smem_bytes(g, tl, a.Kp, kVec);
+  static std::atomic<unsigned> done[3];  // the attribute is the budget, not this launch's size
+  const int64_t ntiles = (int64_t)g.batch * g.Ho * tl.ntw;
+  auto go = [&](auto kernel, std::atomic<unsigned>& d) {
+    ensure_smem(kernel, im2t::kBudget, d);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, im2t::kThreads, smem) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    int64_t grid = (int64_t)sm_count() * per_sm;  // persistent: one wave, tiles strided over it
+    if (grid > ntiles) grid = ntiles;
+    launch_pdl(kernel, (int)grid, im2t::kThreads, smem, st, a.X, g, tl, a.K, a.Kp, a.qmax, a.codes, a.lam, a.inv_lam,
+               a.err_flag, a.U, a.ldu, a.uplane, ntiles);
+  };
+  if (a.mode == kRoundFloor) go(k1_quantize_im2col_tile<kRoundFloor, kVec, VPT, LPR>, done[0]);
+  else if (a.mode == kRoundTrunc) go(k1_quantize_im2col_tile<kRoundTrunc, kVec, VPT, LPR>, done[1]);
+  else go(k1_quantize_im2col_tile<kRoundNearest, kVec, VPT, LPR>, done[2]);
+  ++launch_counter();
+}
+
+// lanes per row / quads per lane: the fewest idle quad slots, short rows shared by sub-warps
+template <bool kVec>
+static void im2col_tile_v(const QuantArgs& a, const ConvGeom& g, const im2t::Tile& tl, cudaStream_t st) {
+  const int nq = a.Kp / 4;
+  if (nq <= 8) im2col_tile_t<kVec, 1, 8>(a, g, tl, st);
+  else if (nq <= 16) im2col_tile_t<kVec, 2, 8>(a, g, tl, st);
+  else if (nq <= 40) im2col_tile_t<kVec, 5, 8>(a, g, tl, st);
+  else if (nq <= 80) im2col_tile_t<kVec, 5, 16>(a, g, tl, st);
+  else im2col_tile_t<kVec, 5, 32>(a, g, tl, st);
+}
+
 template <bool kVec>
 static void im2col_t(const QuantArgs& a, const ConvGeom& g, cudaStream_t st) {
   int dev = 0, nsm = 148;
@@ -826,6 +1104,12 @@ static void im2col_t(const QuantArgs& a, const ConvGeom& g, cudaStream_t st) {
 void launch_quantize_im2col(const QuantArgs& a, const ConvGeom& g, cudaStream_t st) {
   if (a.rows == 0) return;
   const bool vec = g.C % 4 == 0 && (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
+  const im2t::Tile tl = im2col_tile_geom(g, a.Kp, vec);
+  if (tl.TW > 0) {
+    if (vec) im2col_tile_v<true>(a, g, tl, st);
+    else im2col_tile_v<false>(a, g, tl, st);
+    return;
+  }
   if (vec) im2col_t<true>(a, g, st);
   else im2col_t<false>(a, g, st);
 }

@@ -409,6 +409,9 @@ def test_empty_problem_is_a_no_op():
     (1, 12, 10, 8, 3, 3, 1, 2, 2, 24),      # dilated
     (2, 11, 10, 3, 3, 3, 1, 2, 2, 8),       # dilated, C = 3 (scalar per-tap stepping)
     (2, 9, 13, 5, 5, 3, 1, 0, 1, 12),       # C = 5, rectangular input, no padding (scalar spans)
+    (1, 5, 130, 8, 3, 3, 1, 1, 1, 16),      # 130 outputs per image row: 3 staged tiles, ragged last one
+    (1, 6, 150, 3, 7, 7, 2, 3, 1, 8),       # stem geometry, 75 outputs per row (2 tiles)
+    (1, 6, 6, 512, 3, 3, 1, 1, 1, 8),       # K = 4608: the staged window limits the tile width
 ])
 @pytest.mark.parametrize("bits,rounding", [(4, "floor"), (8, "nearest"), (4, "trunc")])
 def test_quantize_im2col_matches_explicit(geom, bits, rounding):
