@@ -428,20 +428,25 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
   __syncthreads();
   if (ticket != ngrp - 1) return;
   __threadfence();
+  // G also into shared memory behind the solvers' scratch: the solver reads it from there, not back
+  // through L2 (W <= 32)
+  double* Gs = dyn + 3 * 32 * 33;
   for (int pr = threadIdx.x; pr < npairs; pr += 256) {
     double a = 0.0;
     for (int g = 0; g < ngrp; ++g) a += __ldcg(jb.gpart + (int64_t)(nb + g) * npairs + pr);
     jb.G[pr] = a;
+    if (W <= 32) Gs[pr] = a;
   }
   if (threadIdx.x == 0) jb.counter[0] = 0;  // re-arm for the next launch (stream ordered)
   if (jb.cmax && threadIdx.x < 64) jb.cmax[threadIdx.x] = 0u;  // the next apply64's column maxima
   __threadfence_block();
   __syncthreads();
   if constexpr (W <= 32) {
+    static_assert(3 * 32 * 33 * 8 + W * W * 8 <= kDynSmem && eig_smem_bytes(W) <= 3 * 32 * 33 * 8, "G staging");
     if (mode == 0 && threadIdx.x < 32) {
-      warp_chol_orth<W>(jb.G, jb.T64, dyn, dyn + 32 * 33, dyn + 2 * 32 * 33);
+      warp_chol_orth<W>(Gs, jb.T64, dyn, dyn + 32 * 33, dyn + 2 * 32 * 33);
     }
-    if (mode == 1) dev_eig_trunc<W>(jb.G, jb.T, jb.r, dyn);
+    if (mode == 1) dev_eig_trunc<W>(Gs, jb.T, jb.r, dyn);
   } else {
     if (mode == 0) dev_chol_orth<W>(jb.G, jb.T64, dyn);
     else if (mode == 1) dev_eig_trunc<W>(jb.G, jb.T, jb.r, dyn);

@@ -13,32 +13,50 @@ LRQMM_DEV void group_bar(int id, int count) { asm volatile("bar.sync %0, %1;" ::
 
 // ------------------------------------------------- one-warp solvers (n <= 32)
 // Pivoted Cholesky QR transform, one warp, lane j = column j, no row/column swaps:
-//   S (the Schur complement, column-major, stride 33 so lane-parallel accesses are conflict free)
-//   is updated in place on the ORIGINAL indices; lane j keeps its diagonal d_j in a register.
-//   Step k: pivot p = argmax d_j over the remaining lanes (one packed-key __reduce_max_sync pair);
-//   l = S[p, :] / sqrt(d_p) (l_p = sqrt(d_p)); S -= l l^T; d -= l^2.
-//   The transform is built alongside as Gram-Schmidt in the G inner product (mathematically
-//   T = P L^-T):  t_k = (e_p - sum_{m<k} t_m L[p, m]) / L[p, k],  so Q = Y T has orthonormal
-//   columns.  Pivots below 1e-10 x the largest diagonal entry end the factorisation (reading
-//   #12): the remaining columns of T are zero.
+//   lane j keeps column j of S (the Schur complement, on the ORIGINAL indices) in registers
+//   s[0..n) and its diagonal d_j.  Step k: pivot p = argmax d_j over the remaining lanes (one
+//   packed-key __reduce_max_sync pair); l_j = S[p, j] / sqrt(d_p) (l_p = sqrt(d_p)), where S[p, j]
+//   is lane j's own s[p] (a select over the unrolled registers, overlapping the rsqrt); l goes to
+//   Lsm row k; S -= l l^T is register-only (l_i broadcast from Lsm); d -= l^2.  Per step the
+//   dependent chain is argmax -> rsqrt -> l -> one broadcast round, no shared-memory matrix traffic.
+//   The transform (mathematically T = P L^-T) is formed after the factorisation as Gram-Schmidt in
+//   the G inner product, lane = row of T with the row in registers:
+//     t_k = (e_{p_k} - sum_{m<k} t_m L[p_k, m]) / L[p_k, k],
+//   so Q = Y T has orthonormal columns.  Pivots below 1e-10 x the largest diagonal entry end the
+//   factorisation (reading #12): the remaining columns of T are zero.
+//   Shared scratch: sm (>= 2 x 32 doubles: pivot indices, 1 / L[p_k, k]), Lsm (32 x 33 doubles),
+//   Tsm (32 x 33 doubles, output staging).
 // Output T64[j * n + k] = T[j, k].
 template <int n>
 __device__ void warp_chol_orth(const double* G, double* T64, double* sm, double* Lsm, double* Tsm) {
   const int lane = threadIdx.x & 31;
-#define SA(i, j) sm[(j) * 33 + (i)]
+  int* piv = reinterpret_cast<int*>(sm);
+  double* invs = sm + 32;
+  double s[n];
   double d = 0.0;
-  for (int i = 0; i < n; ++i)
-    if (lane < n) {
-      const double g = 0.5 * (G[i * n + lane] + G[lane * n + i]);
-      SA(i, lane) = g;
-      if (i == lane) d = g;
-    }
+  // column `lane` of the symmetrised G; every load of a chunk of 8 rows issues before its use (G may
+  // be in global memory: one round trip per chunk, not per row)
+#pragma unroll
+  for (int i0 = 0; i0 < n; i0 += 8) {
+    double ga[8], gb[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      if (i0 + t < n) {
+        ga[t] = lane < n ? G[(i0 + t) * n + lane] : 0.0;
+        gb[t] = lane < n ? G[lane * n + i0 + t] : 0.0;
+      }
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      if (i0 + t < n) {
+        s[i0 + t] = 0.5 * (ga[t] + gb[t]);
+        if (i0 + t == lane) d = s[i0 + t];
+      }
+  }
   double dmax = d;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   const double thr = 1e-10 * dmax;
   bool done = lane >= n;
-  __syncwarp();
   int k = 0;
   for (; k < n; ++k) {
     // argmax of d over the remaining lanes; ties (to 2^-46 relative) -> lowest lane
@@ -54,50 +72,47 @@ __device__ void warp_chol_orth(const double* G, double* T64, double* sm, double*
     if (!(dmax > 0.0) || dp < thr || dp <= 0.0) break;
     const double inv = rsqrt(dp);
     const double lkk = dp * inv;
-    const double spj = SA(p, lane);
-    double l = done ? 0.0 : (lane == p ? lkk : spj * inv);
+    double spj = s[0];  // S[p, lane] = s[p]
+#pragma unroll
+    for (int i = 1; i < n; ++i) spj = p == i ? s[i] : spj;
+    const double l = done ? 0.0 : (lane == p ? lkk : spj * inv);
     if (lane == p) done = true;
     Lsm[k * 33 + lane] = l;
+    if (lane == 0) {
+      piv[k] = p;
+      invs[k] = inv;
+    }
     if (!done) d = fma(-l, l, d);
     __syncwarp();
-    // t_k = (e_p - sum_{m<k} t_m L[p, m]) / L[p, k]
-    {
-      double a[4] = {lane == p ? 1.0 : 0.0, 0.0, 0.0, 0.0};
-      for (int m0 = 0; m0 < k; m0 += 4) {
-        double tv[4], lv[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const bool ok = m0 + t < k;
-          tv[t] = ok ? Tsm[(m0 + t) * 33 + lane] : 0.0;
-          lv[t] = ok ? Lsm[(m0 + t) * 33 + p] : 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < 4; ++t) a[t] = fma(-tv[t], lv[t], a[t]);
-      }
-      Tsm[k * 33 + lane] = ((a[0] + a[1]) + (a[2] + a[3])) * inv;
-    }
-    // S -= l l^T on the remaining columns
-    // (explicitly staged in chunks: all loads of a chunk issue before its stores)
+    // S -= l l^T on the remaining columns (registers; l_i broadcast)
     if (!done) {
 #pragma unroll
-      for (int i0 = 0; i0 < n; i0 += 8) {
-        double sv[8], lv[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          lv[t] = Lsm[k * 33 + i0 + t];
-          sv[t] = SA(i0 + t, lane);
-        }
-#pragma unroll
-        for (int t = 0; t < 8; ++t) SA(i0 + t, lane) = fma(-lv[t], l, sv[t]);
-      }
+      for (int i = 0; i < n; ++i) s[i] = fma(-Lsm[k * 33 + i], l, s[i]);
     }
-    __syncwarp();
   }
   const int rk = k;
   __syncwarp();
-  if (lane < n)
-    for (int c = 0; c < n; ++c) T64[lane * n + c] = c < rk ? Tsm[c * 33 + lane] : 0.0;
-#undef SA
+  // T row `lane` (registers, reusing s): t[k] = (e_p - sum_{m<k} t[m] L[p, m]) * inv_k, partial sums
+  // over m mod 4 in order, as the factorisation-time form
+  double* t = s;
+#pragma unroll
+  for (int kk = 0; kk < n; ++kk) {
+    if (kk < rk) {
+      const int p = piv[kk];
+      double a[4] = {lane == p ? 1.0 : 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int m = 0; m < kk; ++m) a[m & 3] = fma(-t[m], Lsm[m * 33 + p], a[m & 3]);
+      t[kk] = ((a[0] + a[1]) + (a[2] + a[3])) * invs[kk];
+    } else {
+      t[kk] = 0.0;
+    }
+  }
+  // coalesced output through Tsm (column c of T at Tsm[c * 33 + row])
+#pragma unroll
+  for (int c = 0; c < n; ++c) Tsm[c * 33 + lane] = t[c];
+  __syncwarp();
+  for (int e = lane; e < n * n; e += 32) T64[e] = Tsm[(e % n) * 33 + e / n];
+  __syncwarp();
 }
 
 // --------------------------------------------- parallel Jacobi (truncation)
@@ -114,6 +129,19 @@ __device__ void warp_chol_orth(const double* G, double* T64, double* sm, double*
 // in every warp) and hands c, s out by shuffle.
 // Stop: off(A)^2 <= 1e-16 diag(A)^2 (off-diagonal <= 1e-8 relative: eigenvector error ~1e-8 / relative
 // gap, at the fp32 precision of the output T; reading #29).
+#ifndef LRQMM_JAC_NEWTON
+#define LRQMM_JAC_NEWTON 2
+#endif
+__device__ __forceinline__ double jac_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+__device__ __forceinline__ double jac_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
 __device__ __forceinline__ int jac_P(int k) { return k == 0 ? 0 : k + 1; }
 __device__ __forceinline__ int jac_Q(int k, int na) { return k == 0 ? 1 : na - k; }
 __device__ __forceinline__ int jac_sigma(int d, int na) { return d == 0 ? 0 : (d == 1 ? na - 1 : d - 1); }
@@ -128,6 +156,15 @@ __host__ __device__ constexpr int eig_smem_bytes(int n) { return 3 * n * (n + 1)
 // Run by a group of NT threads (tid = 0 .. NT-1 within the group, whole warps) that synchronise with
 // named barrier `bar` (bar 0 over blockDim.x threads is the CTA barrier).  Shared scratch: dyn (the
 // eig_smem_bytes(n) matrices) and aux (eig_aux_bytes(NT): per-warp sums, scale, na, order).
+#ifdef LRQMM_EIG_STATS
+__device__ int eig_stats_steps;
+#endif
+#ifndef LRQMM_EIG_SKIP
+#define LRQMM_EIG_SKIP 0  // micro-benchmark only (tools/eig_bench.cu): 1 no V, 2 fixed rotation, 4 no A blocks
+#endif
+#ifndef LRQMM_EIG_SWEEPS
+#define LRQMM_EIG_SWEEPS 0  // micro-benchmark only: run exactly this many sweeps (0: convergence test)
+#endif
 template <int n, int NT>
 __device__ void group_eig_trunc(const double* G, float* T, int r, double* dyn, double* aux, int tid, int bar) {
   constexpr int ld = n + 1;
@@ -187,9 +224,7 @@ __device__ void group_eig_trunc(const double* G, float* T, int r, double* dyn, d
     return (o2 <= 1e-16 * d2) || (o2 == 0.0);
   };
   bool stop = converged(off, dg);
-  // fixed per-thread work: this lane's rotation (pair `lane`), its 2x2 blocks, its V entries
-  const int rk = lane < half ? lane : 0;
-  const int rP = jac_P(rk) * ld + jac_P(rk), rQ = jac_Q(rk, na) * ld + jac_Q(rk, na), rPQ = jac_P(rk) * ld + jac_Q(rk, na);
+  // fixed per-thread work: its 2x2 blocks, its V entries (lane k < half computes pair k's rotation)
   int bk1[kBlk], bk2[kBlk], brd[kBlk][4], bwr[kBlk][4];
   bool bok[kBlk], bdiag[kBlk];
 #pragma unroll
@@ -216,52 +251,79 @@ __device__ void group_eig_trunc(const double* G, float* T, int r, double* dyn, d
     vP[u] = jac_P(vk[u]);
     vQ[u] = jac_Q(vk[u], na);
   }
+  // rotation (c, s) of pair k at the current step (positions P_k, Q_k of Ac); bitwise identical
+  // wherever it is evaluated.  The angle comes from fp64 approximations (MUFU.RCP64H / RSQ64H, no
+  // fp32 round trips); any rotation is an exact similarity once c, s are orthonormal to fp64
+  // rounding (the Newton steps); only convergence depends on the angle's accuracy.
+  auto rotation = [&](const double* Ac, int k, double& c, double& s) {
+    const int P = jac_P(k), Q = jac_Q(k, na);
+    const double app = Ac[P * ld + P], aqq = Ac[Q * ld + Q], apq = Ac[P * ld + Q];
+    c = 1.0;
+    s = 0.0;
+    if (LRQMM_EIG_SKIP & 2) {
+      c = 0.8;
+      s = 0.6;
+    } else if (apq != 0.0) {
+      const double theta = (aqq - app) * jac_rcp(2.0 * apq);
+      const double at = fabs(theta);
+      double t;
+      if (at < 1e100) {
+        const double x = fma(theta, theta, 1.0);
+        t = copysign(jac_rcp(fma(x, jac_rsqrt(x), at)), theta);  // 1 / (|theta| + sqrt(1 + theta^2))
+      } else {
+        t = 0.5 * jac_rcp(theta);
+      }
+      const double x = fma(t, t, 1.0);
+      double y = jac_rsqrt(x);
+      y = y * fma(-0.5 * x, y * y, 1.5);
+#if LRQMM_JAC_NEWTON > 1
+      y = y * fma(-0.5 * x, y * y, 1.5);
+#endif
+      c = y;
+      s = t * y;
+    }
+  };
+  // V' = V J of a step, applied one step late (off the A chain): rotations (cv, sv) of lane k < half
+  // = pair k of step `vs`
+  double cv = 1.0, sv = 0.0;
+  auto v_update = [&](int vs) {
+#pragma unroll
+    for (int u = 0; u < kV && !(LRQMM_EIG_SKIP & 1); ++u) {
+      const double ck = __shfl_sync(0xffffffffu, cv, vk[u]), sk = __shfl_sync(0xffffffffu, sv, vk[u]);
+      if (vok[u]) {
+        const int vp = vrow[u] + jac_orig(vs, vP[u], m), vq = vrow[u] + jac_orig(vs, vQ[u], m);
+        const double x0 = V[vp], x1 = V[vq];
+        V[vp] = ck * x0 - sk * x1;
+        V[vq] = sk * x0 + ck * x1;
+      }
+    }
+  };
   int total = 0;  // steps done
-  for (int sweep = 0; sweep < 30 && !stop; ++sweep) {
+  int pstep = -1;  // step (within its sweep) of the V update still pending
+  for (int sweep = 0; LRQMM_EIG_SWEEPS ? sweep < LRQMM_EIG_SWEEPS : (sweep < 30 && !stop); ++sweep) {
     for (int step = 0; step < m; ++step, ++total) {
       const double* Ac = Abuf + (total & 1) * n * ld;
       double* An = Abuf + ((total + 1) & 1) * n * ld;
       const bool last = step + 1 == m;
-      // every load of the step first (none depends on this step's rotations; the compiler cannot
-      // hoist them past the previous item's stores itself): the 2x2 blocks, the V pairs, the pivots
-      double bv[kBlk][4], vv[kV][2];
-      int vp[kV], vq[kV];
+      // every load of the step first: the 2x2 blocks
+      double bv[kBlk][4];
 #pragma unroll
       for (int u = 0; u < kBlk; ++u)
         if (bok[u]) {
           bv[u][0] = Ac[brd[u][0]]; bv[u][1] = Ac[brd[u][1]]; bv[u][2] = Ac[brd[u][2]]; bv[u][3] = Ac[brd[u][3]];
         }
-#pragma unroll
-      for (int u = 0; u < kV; ++u)
-        if (vok[u]) {
-          vp[u] = vrow[u] + jac_orig(step, vP[u], m);
-          vq[u] = vrow[u] + jac_orig(step, vQ[u], m);
-          vv[u][0] = V[vp[u]];
-          vv[u][1] = V[vq[u]];
-        }
+      // the previous step's V update (its rotations are in cv, sv: independent of this step's chain)
+      if (pstep >= 0) v_update(pstep);
+      // this step's rotations: lane k < half -> pair k (every warp redundantly), handed out by shuffle
       double c = 1.0, s = 0.0;
-      if (lane < half) {
-        const double app = Ac[rP], aqq = Ac[rQ], apq = Ac[rPQ];
-        const float fpq = (float)apq;
-        // angle in fp32 with approximate division / square root: any rotation is an exact
-        // similarity (c, s below are orthonormal to fp64 rounding); only convergence depends on it
-        const float theta = __fdividef((float)(aqq - app), 2.f * fpq);
-        const float at = fabsf(theta);
-        const float rs = rsqrtf(fmaf(theta, theta, 1.f));
-        float t = copysignf(__fdividef(1.f, at + fmaf(theta, theta, 1.f) * rs), theta);
-        t = at > 1e18f ? __fdividef(0.5f, theta) : t;
-        const double td = fpq != 0.f ? (double)t : 0.0;
-        const double x = fma(td, td, 1.0);
-        double y = (double)rsqrtf((float)x);
-        y = y * fma(-0.5 * x, y * y, 1.5);
-        y = y * fma(-0.5 * x, y * y, 1.5);
-        c = fpq != 0.f ? y : 1.0;
-        s = td * c;
-      }
+      if (lane < half) rotation(Ac, lane, c, s);
+      cv = c;
+      sv = s;
+      pstep = step;
       off = 0.0;
       dg = 0.0;
 #pragma unroll
-      for (int u = 0; u < kBlk; ++u) {
+      for (int u = 0; u < kBlk && !(LRQMM_EIG_SKIP & 4); ++u) {
         const double c1 = __shfl_sync(0xffffffffu, c, bk1[u]), s1 = __shfl_sync(0xffffffffu, s, bk1[u]);
         const double c2 = __shfl_sync(0xffffffffu, c, bk2[u]), s2 = __shfl_sync(0xffffffffu, s, bk2[u]);
         if (bok[u]) {
@@ -279,19 +341,15 @@ __device__ void group_eig_trunc(const double* G, float* T, int r, double* dyn, d
           }
         }
       }
-#pragma unroll
-      for (int u = 0; u < kV; ++u) {
-        const double ck = __shfl_sync(0xffffffffu, c, vk[u]), sk = __shfl_sync(0xffffffffu, s, vk[u]);
-        if (vok[u]) {
-          V[vp[u]] = ck * vv[u][0] - sk * vv[u][1];
-          V[vq[u]] = sk * vv[u][0] + ck * vv[u][1];
-        }
-      }
       if (last) stop = converged(off, dg);  // its barrier ends the step
       else sync();
     }
   }
+  if (pstep >= 0) v_update(pstep);
   sync();
+#ifdef LRQMM_EIG_STATS
+  if (tid == 0) eig_stats_steps = total;  // micro-benchmark only (tools/eig_bench.cu)
+#endif
   // position d < na holds eigenvalue A[d][d] with eigenvector V[:, orig(total mod m, d)];
   // indices >= na: eigenvalue 0, eigenvector e_d
   const double* Af = Abuf + (total & 1) * n * ld;

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <vector>
 
+#define LRQMM_EIG_STATS
 #include "solvers.cuh"
 
 using namespace lrqmm;
@@ -32,9 +33,37 @@ __global__ void k_bench_warp(const double* G, float* T, int r, unsigned long lon
   if (threadIdx.x == 0) *t = t1 - t0;
 }
 
-template <int NT>
+template <int n>
+__global__ void k_bench_chol(const double* G, double* T64, unsigned long long* t) {
+  __shared__ double sm[3 * 32 * 33];
+  unsigned long long t0, t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  warp_chol_orth<n>(G, T64, sm, sm + 32 * 33, sm + 2 * 32 * 33);
+  __syncwarp();
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  if (threadIdx.x == 0) *t = t1 - t0;
+}
+
+template <int n>
+void run_chol(const double* dG, unsigned long long* dt) {
+  double* dT;
+  cudaMalloc(&dT, 8 * n * n);
+  unsigned long long best = ~0ull;
+  for (int i = 0; i < 20; ++i) {
+    k_bench_chol<n><<<1, 32>>>(dG, dT, dt);
+    unsigned long long t;
+    cudaMemcpy(&t, dt, 8, cudaMemcpyDeviceToHost);
+    if (t < best) best = t;
+  }
+  std::vector<double> T(n * n);
+  cudaMemcpy(T.data(), dT, 8 * n * n, cudaMemcpyDeviceToHost);
+  printf("chol n=%d  best %.1f us   T[0][0..2] = %.6e %.6e %.6e  (%s)\n", n, best / 1e3, T[0], T[1], T[2],
+         cudaGetErrorString(cudaGetLastError()));
+  cudaFree(dT);
+}
+
+template <int NT, int n = 24>
 void run(const double* dG, float* dT, unsigned long long* dt) {
-  constexpr int n = 24;
   cudaFuncSetAttribute(k_bench<n, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, eig_smem_bytes(n));
   unsigned long long best = ~0ull;
   for (int i = 0; i < 20; ++i) {
@@ -46,9 +75,15 @@ void run(const double* dG, float* dT, unsigned long long* dt) {
   std::vector<float> T(n * n);
   cudaMemcpy(T.data(), dT, sizeof(float) * n * n, cudaMemcpyDeviceToHost);
   if (NT == 256) {
-    FILE* o = fopen("gpurun_out/eig_T_256.bin", "wb");
+    char fn[64];
+    snprintf(fn, sizeof fn, "gpurun_out/eig_T_256_n%d.bin", n);
+    FILE* o = fopen(fn, "wb");
     if (o) { fwrite(T.data(), 4, T.size(), o); fclose(o); }
   }
+  int steps = 0;
+  cudaMemcpyFromSymbol(&steps, eig_stats_steps, sizeof(int));
+  printf("steps %d  ", steps);
+  printf("n=%d ", n);
   printf("NT=%3d  best %.1f us   T[0][0..3] = %.6f %.6f %.6f %.6f  (%s)\n", NT, best / 1e3, T[0], T[1], T[2], T[3],
          cudaGetErrorString(cudaGetLastError()));
 }
@@ -62,6 +97,7 @@ int main(int argc, char** argv) {
   double* dG; float* dT; unsigned long long* dt;
   cudaMalloc(&dG, 8 * G.size()); cudaMalloc(&dT, 4 * G.size()); cudaMalloc(&dt, 8);
   cudaMemcpy(dG, G.data(), 8 * G.size(), cudaMemcpyHostToDevice);
+  run_chol<24>(dG, dt);
   run<512>(dG, dT, dt);
   run<256>(dG, dT, dt);
   run<128>(dG, dT, dt);
@@ -81,6 +117,21 @@ int main(int argc, char** argv) {
            cudaGetErrorString(cudaGetLastError()));
     FILE* o = fopen("gpurun_out/eig_T_warp.bin", "wb");
     if (o) { fwrite(T.data(), 4, T.size(), o); fclose(o); }
+  }
+  {  // c4-like n = 32 (tools/eig_gen.py)
+    std::vector<double> G32(32 * 32);
+    FILE* f32 = fopen("tools/eig_G32.bin", "rb");
+    if (f32 && fread(G32.data(), 8, G32.size(), f32) == G32.size()) {
+      double* dG32;
+      float* dT32;
+      cudaMalloc(&dG32, 8 * G32.size());
+      cudaMalloc(&dT32, 4 * G32.size());
+      cudaMemcpy(dG32, G32.data(), 8 * G32.size(), cudaMemcpyHostToDevice);
+      run_chol<32>(dG32, dt);
+      run<256, 32>(dG32, dT32, dt);
+      run<512, 32>(dG32, dT32, dt);
+    }
+    if (f32) fclose(f32);
   }
   return 0;
 }
