@@ -565,24 +565,46 @@ __global__ void __launch_bounds__(g8::kThreads, 1)
   }
 }
 
-// L (rows x R2 fp32) -> bf16 hi / lo halves, rows of 64 (zero-padded): the K8 correction operands
+// L (rows x R2 fp32) -> bf16 hi / lo halves, rows of 64 (zero-padded): the K8 correction operands.
+// One thread per 8 columns of a row: two 16-byte loads (R2 % 4 == 0; else scalar), packed
+// conversions (cvt.rn.bf16x2.f32), one 16-byte store per half.
 __global__ void k_split_bf16(const float* __restrict__ L, int64_t rows, int R2, __nv_bfloat16* __restrict__ hi,
                              __nv_bfloat16* __restrict__ lo) {
   ::lrqmm::pdl_enter();
-  const int64_t total = rows * 64;
+  const int64_t total = rows * 8;  // 8-column groups
+  const bool vec = (R2 & 3) == 0 && (reinterpret_cast<uintptr_t>(L) & 15) == 0;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e >> 6;
-    const int c = (int)(e & 63);
-    const float x = c < R2 ? L[r * R2 + c] : 0.f;
-    const __nv_bfloat16 h = __float2bfloat16_rn(x);
-    hi[e] = h;
-    lo[e] = __float2bfloat16_rn(x - __bfloat162float(h));
+    const int64_t r = e >> 3;
+    const int c0 = (int)(e & 7) * 8;
+    float x[8];
+    const float* src = L + r * R2 + c0;
+    if (vec) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float4 v = c0 + 4 * h < R2 ? __ldg(reinterpret_cast<const float4*>(src) + h) : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[4 * h] = v.x; x[4 * h + 1] = v.y; x[4 * h + 2] = v.z; x[4 * h + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) x[t] = c0 + t < R2 ? src[t] : 0.f;
+    }
+    uint32_t hw[4], lw[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * t], x[2 * t + 1]);
+      const float2 hf = __bfloat1622float2(h2);
+      const __nv_bfloat162 l2 = __floats2bfloat162_rn(x[2 * t] - hf.x, x[2 * t + 1] - hf.y);
+      hw[t] = *reinterpret_cast<const uint32_t*>(&h2);
+      lw[t] = *reinterpret_cast<const uint32_t*>(&l2);
+    }
+    *reinterpret_cast<uint4*>(hi + e * 8) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    *reinterpret_cast<uint4*>(lo + e * 8) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   }
 }
 
 void launch_split_bf16(const float* L, int64_t rows, int R2, void* hi, void* lo, cudaStream_t st) {
   if (rows <= 0) return;
-  int64_t g = (rows * 64 + 255) / 256;
+  int64_t g = (rows * 8 + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
   launch_pdl(k_split_bf16, (int)g, 256, 0, st, L, rows, R2, reinterpret_cast<__nv_bfloat16*>(hi),
              reinterpret_cast<__nv_bfloat16*>(lo));

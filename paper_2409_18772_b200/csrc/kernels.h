@@ -261,6 +261,7 @@ struct Apply64Job {
   float* OUT;
   unsigned* cmax;       // if set: atomicMax of the float bits of |OUT[i, c] * cscale[i]| per column c
   const float* cscale;  // (zeroed beforehand; cscale nullptr = 1)
+  int kin;              // live columns: IN[:, c >= kin] and S[c >= kin, :], S[:, c >= kin] are zero (0: W)
 };
 struct Apply64Jobs {
   Apply64Job j[2];
@@ -279,6 +280,7 @@ struct ApplyJob {
   float* OUT;
   int64_t ldo;
   int col0;
+  int kin;  // live input columns: IN1 / IN2[:, c >= kin] are zero (0: W)
 };
 struct ApplyJobs {
   ApplyJob j[kMaxApply];

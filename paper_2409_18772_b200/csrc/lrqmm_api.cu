@@ -656,7 +656,7 @@ static lrqmm_status_t gram_step(lrqmm_handle_t h, float* const Y[2], const int64
     for (int sd = 0; sd < 2; ++sd)
       if (sides & (1 << sd))
         aj.j[aj.n++] = Apply64Job{Y[sd], h->s[sd].T64, n[sd], Q[sd], which == 0 ? h->s[sd].cmax0 : h->s[sd].cmax1,
-                                  which == 0 ? h->s[sd].inv_lam : nullptr};
+                                  which == 0 ? h->s[sd].inv_lam : nullptr, (int)h->kk};
     launch_apply64_jobs(aj, W, h->st);
   }
   return check_launch(h);
@@ -768,10 +768,10 @@ static lrqmm_status_t assemble(lrqmm_handle_t h, bool cross = true, bool wait_fo
   float* YB = h->cfg.power_iters == 0 ? h->s[1].Q0 : h->s[1].Y;
   ApplyJobs aj{};
   aj.n = 4;
-  aj.j[0] = ApplyJob{YA, h->s[0].VW, nullptr, nullptr, rows[0], W, r, h->LA, h->R2, 0};        // U_A S_A
-  aj.j[1] = ApplyJob{h->s[0].Gp, h->s[1].VW, nullptr, nullptr, rows[0], W, r, h->LA, h->R2, r}; // A~ V_B
-  aj.j[2] = ApplyJob{h->s[1].Gp, h->s[0].VW, YB, h->VWbM, rows[1], W, r, h->LB, h->R2, 0};      // B~^T V_A + U_B S_B M
-  aj.j[3] = ApplyJob{YB, h->s[1].VW, nullptr, nullptr, rows[1], W, r, h->LB, h->R2, r};         // U_B S_B
+  aj.j[0] = ApplyJob{YA, h->s[0].VW, nullptr, nullptr, rows[0], W, r, h->LA, h->R2, 0, (int)h->kk};        // U_A S_A
+  aj.j[1] = ApplyJob{h->s[0].Gp, h->s[1].VW, nullptr, nullptr, rows[0], W, r, h->LA, h->R2, r, (int)h->kk}; // A~ V_B
+  aj.j[2] = ApplyJob{h->s[1].Gp, h->s[0].VW, YB, h->VWbM, rows[1], W, r, h->LB, h->R2, 0, (int)h->kk};      // B~^T V_A + U_B S_B M
+  aj.j[3] = ApplyJob{YB, h->s[1].VW, nullptr, nullptr, rows[1], W, r, h->LB, h->R2, r, (int)h->kk};         // U_B S_B
   launch_apply_jobs(aj, W, h->st);
   if (h->bsh) {  // the epilogue of every rank's GEMM reads all rows of L_B
     lrqmm_status_t e = allgather_b(h, h->LB_full, sizeof(float) * h->R2);

@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const __grid_constant__
   float* s2 = s1 + W * NO;               // W x NO
   float* sin_base = s2 + W * NO;         // 2 buffers x (IN1, IN2) x kApRows x L (cp.async double buffer)
   const int nout = J.nout;
+  const int kin = J.kin > 0 && J.kin < W ? J.kin : W;
   for (int e = threadIdx.x; e < W * NO; e += blockDim.x) {
     const int c = e / NO, o = e % NO;
     s1[e] = o < nout ? J.S1[c * J.ldS + o] : 0.f;
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const __grid_constant__
     if (threadIdx.x < nr) {
 #pragma unroll(W <= 32 ? W / 4 : 2)  // bounded unrolling for the wide sketches (build time)
       for (int c4 = 0; c4 < W / 4; ++c4) {
+        if (4 * c4 >= kin) break;  // zero-padded sketch columns contribute nothing
         const float4 v = *reinterpret_cast<const float4*>(sin1 + threadIdx.x * L + 4 * c4);
         const float xs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const __grid_constant__
       if (J.IN2) {
 #pragma unroll(W <= 32 ? W / 4 : 2)
         for (int c4 = 0; c4 < W / 4; ++c4) {
+          if (4 * c4 >= kin) break;
           const float4 v = *reinterpret_cast<const float4*>(sin2 + threadIdx.x * L + 4 * c4);
           const float xs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -189,13 +192,15 @@ void launch_apply_small(const float* IN1, const float* S1, const float* IN2, con
                         int ldS, int nout, float* OUT, int64_t ldo, int col0, cudaStream_t st) {
   ApplyJobs j{};
   j.n = 1;
-  j.j[0] = ApplyJob{IN1, S1, IN2, S2, n, ldS, nout, OUT, ldo, col0};
+  j.j[0] = ApplyJob{IN1, S1, IN2, S2, n, ldS, nout, OUT, ldo, col0, 0};
   launch_apply_jobs(j, W, st);
 }
 
 // OUT = IN S with S in fp64 and fp64 accumulation (orthonormalisation: keeps Q orthonormal to
 // fp32 rounding instead of cond(IN) * eps32).  Same staging as above; one launch for both sides.
-template <int W>
+// NO: outputs computed per row (the rest of the W are zero: columns >= kin of S are zero); inputs
+// c >= kin are skipped (zero-padded sketch columns).
+template <int W, int NO>
 __global__ void __launch_bounds__(kApRows) k_apply64(const __grid_constant__ Apply64Jobs jobs) {
   ::lrqmm::pdl_enter();
   constexpr int L = ap_ld(W);
@@ -206,6 +211,7 @@ __global__ void __launch_bounds__(kApRows) k_apply64(const __grid_constant__ App
   double* s = apsm64;                                           // W x W
   float* sin_base = reinterpret_cast<float*>(apsm64 + W * W);   // 2 x kApRows x L (cp.async double buffer)
   for (int e = threadIdx.x; e < W * W; e += blockDim.x) s[e] = J.S[e];
+  const int kin = J.kin > 0 && J.kin < W ? J.kin : W;
   unsigned run[(W + 31) / 32];  // lane c: running column max of column c (+32)
 #pragma unroll
   for (int u = 0; u < (W + 31) / 32; ++u) run[u] = 0u;
@@ -226,18 +232,19 @@ __global__ void __launch_bounds__(kApRows) k_apply64(const __grid_constant__ App
     const float* sin = sin_base + (it & 1) * kApRows * L;
     cp_async_wait<1>();  // this tile's group has landed (the next one may still be in flight)
     __syncthreads();
-    double acc[W];
+    double acc[NO];
 #pragma unroll
-    for (int o = 0; o < W; ++o) acc[o] = 0.0;
+    for (int o = 0; o < NO; ++o) acc[o] = 0.0;
     if (threadIdx.x < nr) {
 #pragma unroll(W <= 32 ? W / 4 : 2)  // bounded unrolling for the wide sketches (build time)
       for (int c4 = 0; c4 < W / 4; ++c4) {
+        if (4 * c4 >= kin) break;  // zero-padded sketch columns contribute nothing
         const float4 v = *reinterpret_cast<const float4*>(sin + threadIdx.x * L + 4 * c4);
         const double xs[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
-          for (int o = 0; o < W; ++o) acc[o] = fma(xs[j], s[(4 * c4 + j) * W + o], acc[o]);
+          for (int o = 0; o < NO; ++o) acc[o] = fma(xs[j], s[(4 * c4 + j) * W + o], acc[o]);
       }
     }
     __syncthreads();  // every row of this buffer has been read: stage the tile after next into it
@@ -246,13 +253,16 @@ __global__ void __launch_bounds__(kApRows) k_apply64(const __grid_constant__ App
       float4* orow = reinterpret_cast<float4*>(J.OUT + (i0 + threadIdx.x) * W);
 #pragma unroll
       for (int o4 = 0; o4 < W / 4; ++o4)
-        orow[o4] = make_float4((float)acc[4 * o4], (float)acc[4 * o4 + 1], (float)acc[4 * o4 + 2], (float)acc[4 * o4 + 3]);
+        orow[o4] = 4 * o4 < NO ? make_float4((float)acc[4 * o4], (float)acc[4 * o4 + 1], (float)acc[4 * o4 + 2],
+                                             (float)acc[4 * o4 + 3])
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     if (J.cmax) {
-      // column maxima of |OUT * cscale| for the next pass's B image (same fp32 product as there)
+      // column maxima of |OUT * cscale| for the next pass's B image (same fp32 product as there);
+      // columns >= NO are zero
       const float cs = (J.cscale && threadIdx.x < nr) ? J.cscale[i0 + threadIdx.x] : 1.f;
 #pragma unroll
-      for (int o = 0; o < W; ++o) {
+      for (int o = 0; o < NO; ++o) {
         const unsigned b = threadIdx.x < nr ? __float_as_uint(fabsf((float)acc[o] * cs)) : 0u;
         const unsigned m = __reduce_max_sync(0xffffffffu, b);
         if ((threadIdx.x & 31) == (o & 31)) run[o >> 5] = max(run[o >> 5], m);
@@ -269,14 +279,25 @@ __global__ void __launch_bounds__(kApRows) k_apply64(const __grid_constant__ App
   }
 }
 
-template <int W>
+template <int W, int NO>
 static void apply64_t(Apply64Jobs& jobs, cudaStream_t st) {
   constexpr int smem = W * W * (int)sizeof(double) + 2 * kApRows * ap_ld(W) * (int)sizeof(float);
   static std::atomic<unsigned> attr{0};
-  ensure_smem(k_apply64<W>, smem, attr);
+  ensure_smem(k_apply64<W, NO>, smem, attr);
   int64_t n[2] = {jobs.j[0].n, jobs.n > 1 ? jobs.j[1].n : 0};
   const int grid = assign_blocks(n, jobs.n, jobs.first);
-  launch_pdl(k_apply64<W>, grid, kApRows, smem, st, jobs);
+  launch_pdl(k_apply64<W, NO>, grid, kApRows, smem, st, jobs);
+}
+// NO = W - 4 when every job's live columns fit (W = roundup(r + p, 8): the default oversampling
+// leaves 3..7 zero columns), else W
+template <int W>
+static void apply64_w(Apply64Jobs& jobs, cudaStream_t st) {
+  int kin = 0;
+  for (int q = 0; q < jobs.n; ++q) kin = max(kin, jobs.j[q].kin > 0 ? jobs.j[q].kin : W);
+  if constexpr (W >= 8) {
+    if (kin <= W - 4) return apply64_t<W, W - 4>(jobs, st);
+  }
+  apply64_t<W, W>(jobs, st);
 }
 
 void launch_apply64_jobs(const Apply64Jobs& in, int W, cudaStream_t st) {
@@ -284,7 +305,7 @@ void launch_apply64_jobs(const Apply64Jobs& in, int W, cudaStream_t st) {
   for (int q = 0; q < in.n; ++q)
     if (in.j[q].n > 0) jobs.j[jobs.n++] = in.j[q];
   if (jobs.n == 0) return;
-#define A64_CASE(w) case w: apply64_t<w>(jobs, st); break;
+#define A64_CASE(w) case w: apply64_w<w>(jobs, st); break;
   switch (W) { A64_CASE(8) A64_CASE(16) A64_CASE(24) A64_CASE(32) A64_CASE(40) A64_CASE(48) A64_CASE(56) A64_CASE(64) default: break; }
 #undef A64_CASE
   ++launch_counter();
