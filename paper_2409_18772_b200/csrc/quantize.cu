@@ -543,9 +543,16 @@ static int64_t launch_k1_rows_tma(const QuantArgs& a, bool fixed, cudaStream_t s
   const int64_t nchunks = rows_full / R;
   const int grid = (int)(nchunks < 2 * nsm ? nchunks : 2 * nsm);
   const bool v4 = a.K % 4 == 0;
-  int L = 32;  // lanes per row: the smallest power of two covering the row's float4s (vec4 path)
+  // lanes per row (vec4 path): ~4 float4 per lane, at least 8 lanes (one full 32-byte sector per
+  // row and store instruction); fewer lanes per row = more rows per warp sharing one amax
+  // reduction, division and lambda store (short rows are bound by that per-row work)
+  static const int f4pl = [] {
+    const char* e = getenv("LRQMM_K1_F4PL");
+    return e && atoi(e) > 0 ? atoi(e) : 4;
+  }();
+  int L = 32;
   if (v4)
-    while (L > 1 && L / 2 >= a.K / 4) L /= 2;
+    while (L > 8 && (L / 2) * f4pl >= a.K / 4) L /= 2;
 #define K1R_LAUNCH(V, F, M)                                                                                      \
   do {                                                                                                           \
     cudaFuncSetAttribute(k1_quantize_rows_tma<V, F, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);     \
