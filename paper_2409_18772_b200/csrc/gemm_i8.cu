@@ -370,7 +370,9 @@ constexpr int kStageBytes = BM * BK + BN * BK;  // 32 KB: int8 A | B, or bf16 [L
 constexpr int kEG = 2;                          // epilogue groups (one per accumulator pair)
 constexpr int kThreads = 64 + 128 * kEG;
 constexpr int kStages = 6;
-constexpr int kSmem = kStages * kStageBytes + kEG * BN * 4 + 256 + 1024;
+constexpr int kStile = 8 * 32 * 32 * 4;  // epilogue transpose tiles: 32 x 32 fp32 per epilogue warp
+constexpr int kSmem = kStages * kStageBytes + kStile + kEG * BN * 4 + 256 + 1024;
+static_assert(kSmem <= 232448, "K8 shared memory");
 }  // namespace g8
 
 struct G8Params {
@@ -391,7 +393,8 @@ __global__ void __launch_bounds__(g8::kThreads, 1)
   using namespace g8;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* sSB0 = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // kEG x BN: 1/lambda_B of the tile
+  float* stile0 = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // 8 x 32 x 32 (XOR-swizzled)
+  float* sSB0 = stile0 + kStile / 4;  // kEG x BN: 1/lambda_B of the tile
   uint64_t* bars = reinterpret_cast<uint64_t*>(sSB0 + kEG * BN);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
@@ -524,35 +527,58 @@ __global__ void __launch_bounds__(g8::kThreads, 1)
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * 256;
+      // 32-column chunks: lane = row while reading TMEM and forming D, then a warp-private 32 x 32
+      // transpose in shared memory (16-byte groups XOR-swizzled by row: float4 (r, g) at
+      // r * 32 + 4 (g ^ (r & 7)), conflict-free for the row-wise writes and the column-wise reads),
+      // so that each 16-byte store instruction writes 4 whole 128-byte row segments instead of 32
+      // rows' 16-byte pieces
+      float* stile = stile0 + (warp - 2) * 32 * 32;
+      const int64_t row0 = (int64_t)mb * BM + quad * 32;
+      const int rsub = lane >> 3, g4 = lane & 7;
 #pragma unroll 1
-      for (int g = 0; g < BN / 8; ++g) {
-        uint32_t ri[8], rc[8];
-        tmem_ld_32x32b_x8(t_row + g * 8, ri);
-        tmem_ld_32x32b_x8(t_row + 128 + g * 8, rc);
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        const int col0 = n0 + ch * 32;
+        if (col0 >= p.N) break;  // warp-uniform
+        uint32_t ri[32], rc[32];
+        tmem_ld_32x32b_x32(t_row + ch * 32, ri);
+        tmem_ld_32x32b_x32(t_row + 128 + ch * 32, rc);
         tmem_ld_wait();
-        const int col0 = n0 + g * 8;
-        if (row >= p.M || col0 >= p.N) continue;
-        float v[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          v[c] = fmaf(p.alpha, __uint_as_float(rc[c]),
-                      __fmul_rn(static_cast<float>(static_cast<int32_t>(ri[c])), __fmul_rn(sa, sSB[g * 8 + c])));
-        float* out = p.D + row * p.ldd + col0;
-        if (p.vec_ok && col0 + 8 <= p.N) {
-          if (p.beta != 0.f) {
-            const float4 o0 = *reinterpret_cast<const float4*>(out);
-            const float4 o1 = *reinterpret_cast<const float4*>(out + 4);
-            v[0] = fmaf(p.beta, o0.x, v[0]); v[1] = fmaf(p.beta, o0.y, v[1]);
-            v[2] = fmaf(p.beta, o0.z, v[2]); v[3] = fmaf(p.beta, o0.w, v[3]);
-            v[4] = fmaf(p.beta, o1.x, v[4]); v[5] = fmaf(p.beta, o1.y, v[5]);
-            v[6] = fmaf(p.beta, o1.z, v[6]); v[7] = fmaf(p.beta, o1.w, v[7]);
+        for (int g = 0; g < 8; ++g) {
+          float4 v;
+          float* pv = &v.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c = 4 * g + e;
+            pv[e] = fmaf(p.alpha, __uint_as_float(rc[c]),
+                         __fmul_rn(static_cast<float>(static_cast<int32_t>(ri[c])), __fmul_rn(sa, sSB[ch * 32 + c])));
           }
-          __stcs(reinterpret_cast<float4*>(out), make_float4(v[0], v[1], v[2], v[3]));
-          __stcs(reinterpret_cast<float4*>(out + 4), make_float4(v[4], v[5], v[6], v[7]));
-        } else {
-          for (int c = 0; c < 8; ++c)
-            if (col0 + c < p.N) out[c] = p.beta != 0.f ? fmaf(p.beta, out[c], v[c]) : v[c];
+          *reinterpret_cast<float4*>(stile + lane * 32 + 4 * (g ^ (lane & 7))) = v;
         }
+        __syncwarp();
+        const int c = col0 + 4 * g4;
+        const bool full4 = p.vec_ok && c + 4 <= p.N;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int r = 4 * it + rsub;
+          const int64_t rw = row0 + r;
+          float4 v = *reinterpret_cast<const float4*>(stile + r * 32 + 4 * (g4 ^ (r & 7)));
+          if (rw >= p.M || c >= p.N) continue;
+          float* out = p.D + rw * p.ldd + c;
+          if (full4) {
+            if (p.beta != 0.f) {
+              const float4 o = *reinterpret_cast<const float4*>(out);
+              v.x = fmaf(p.beta, o.x, v.x); v.y = fmaf(p.beta, o.y, v.y);
+              v.z = fmaf(p.beta, o.z, v.z); v.w = fmaf(p.beta, o.w, v.w);
+            }
+            __stcs(reinterpret_cast<float4*>(out), v);
+          } else {
+            const float* pv = &v.x;
+            for (int e = 0; e < 4; ++e)
+              if (c + e < p.N) out[e] = p.beta != 0.f ? fmaf(p.beta, out[e], pv[e]) : pv[e];
+          }
+        }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
