@@ -65,7 +65,10 @@ struct Cfg {
   static constexpr int kOffB2 = kOffC + kPlane;
   static constexpr int kStageBytes = kHasC ? kOffB2 + kImg : kOffB + kImg;
   static constexpr int kStage = (kStageBytes + 1023) / 1024 * 1024;
-  static constexpr int kScratch = kFuse ? kFuseScratch : 0;
+  // kFuse: the fused Gram scratch; else (no codes operand) the epilogue's output transpose tiles
+  // (4 warps x 32 x 32 fp32); the dual pass keeps its third ring stage instead
+  static constexpr int kScratch = kFuse ? kFuseScratch : (kHasC ? 0 : 16 * 1024);
+  static constexpr bool kTransposeOut = !kFuse && !kHasC;
   static constexpr int S0 = (216 * 1024 - kScratch) / kStage;
   static constexpr int S = S0 > 6 ? 6 : S0;
   static_assert(S >= 2, "ring depth");
@@ -624,25 +627,20 @@ __global__ void __launch_bounds__(kFuse ? tcp::kThreadsFused : tcp::kThreads, 1)
       float o[NG][32];
 #pragma unroll
       for (int g = 0; g < GU; ++g) {
-        // 256 (H1 + H2 2^-7 + H3 2^-14) + L1 + L2 2^-7, then 2^-15 / lambda / s_c
-        uint32_t v[32];
+        // 256 (H1 + H2 2^-7 + H3 2^-14) + L1 + L2 2^-7, then 2^-15 / lambda / s_c (same order of
+        // operations as ever; the loads go in pairs so that one wait covers two TMEM round trips)
+        uint32_t v[32], w[32];
         const uint32_t tH = trow + g * 32, tL = trow + 3 * WN + g * 32;
         tmem_ld_32x32b_x32(tH + 2 * WN, v);
+        tmem_ld_32x32b_x32(tH + WN, w);
         tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < 32; ++c) o[g][c] = (float)(int)v[c] * 0x1p-14f;
-        tmem_ld_32x32b_x32(tH + WN, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < 32; ++c) o[g][c] += (float)(int)v[c] * 0x1p-7f;
+        for (int c = 0; c < 32; ++c) o[g][c] = (float)(int)v[c] * 0x1p-14f + (float)(int)w[c] * 0x1p-7f;
         tmem_ld_32x32b_x32(tH, v);
+        tmem_ld_32x32b_x32(tL + WN, w);
         tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < 32; ++c) o[g][c] = (o[g][c] + (float)(int)v[c]) * 256.f;
-        tmem_ld_32x32b_x32(tL + WN, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < 32; ++c) o[g][c] += (float)(int)v[c] * 0x1p-7f;
+        for (int c = 0; c < 32; ++c) o[g][c] = (o[g][c] + (float)(int)v[c]) * 256.f + (float)(int)w[c] * 0x1p-7f;
         tmem_ld_32x32b_x32(tL, v);
         tmem_ld_wait();
 #pragma unroll
@@ -686,7 +684,31 @@ __global__ void __launch_bounds__(kFuse ? tcp::kThreadsFused : tcp::kThreads, 1)
 #pragma unroll
           for (int c = 0; c < 32; ++c) o[GU + g][c] = o[GU + g][c] * (inv_row * cs[g * 32 + c]);
       }
-      if (orow < a.nout) {
+      if constexpr (C::kTransposeOut) {
+        // warp-private 32 x 32 transpose (16-byte groups XOR-swizzled by row) per 32-column group, so
+        // that each 16-byte store instruction writes 4 whole row segments of this warp's 32 rows
+        float* stile = scratch + (warp - 2) * 32 * 32;
+        const int64_t orow0 = (int64_t)blk * BM + quad * 32;
+        float* obase = a.out1 + (int64_t)split * a.nout * a.W;
+        const int rsub = lane >> 3, g4 = lane & 7;
+#pragma unroll
+        for (int g = 0; g < GU; ++g) {
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<float4*>(stile + lane * 32 + 4 * (q ^ (lane & 7))) =
+                make_float4(o[g][4 * q], o[g][4 * q + 1], o[g][4 * q + 2], o[g][4 * q + 3]);
+          __syncwarp();
+          const int col = g * 32 + 4 * g4;
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int r = 4 * it + rsub;
+            const float4 v4 = *reinterpret_cast<const float4*>(stile + r * 32 + 4 * (g4 ^ (r & 7)));
+            if (orow0 + r < a.nout && col < a.W)
+              *reinterpret_cast<float4*>(obase + (orow0 + r) * a.W + col) = v4;
+          }
+        }
+      } else if (orow < a.nout) {
         if (kHasU) {
           float4* o1 = reinterpret_cast<float4*>(a.out1 + (int64_t)split * a.nout * a.W + orow * a.W);
 #pragma unroll
