@@ -593,17 +593,26 @@ __global__ void __launch_bounds__(g8::kThreads, 1)
 
 // L (rows x R2 fp32) -> bf16 hi / lo halves, rows of 64 (zero-padded): the K8 correction operands.
 // One thread per 8 columns of a row: two 16-byte loads (R2 % 4 == 0; else scalar), packed
-// conversions (cvt.rn.bf16x2.f32), one 16-byte store per half.
-__global__ void k_split_bf16(const float* __restrict__ L, int64_t rows, int R2, __nv_bfloat16* __restrict__ hi,
-                             __nv_bfloat16* __restrict__ lo) {
+// conversions (cvt.rn.bf16x2.f32), one 16-byte store per half.  Both factors (L_A, L_B) in one
+// launch: thread index e < rows0 * 8 -> job 0, the rest -> job 1.
+struct SplitJob {
+  const float* L;
+  int64_t rows;
+  __nv_bfloat16* hi;
+  __nv_bfloat16* lo;
+};
+__global__ void k_split_bf16(const SplitJob j0, const SplitJob j1, int R2) {
   ::lrqmm::pdl_enter();
-  const int64_t total = rows * 8;  // 8-column groups
-  const bool vec = (R2 & 3) == 0 && (reinterpret_cast<uintptr_t>(L) & 15) == 0;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t n0 = j0.rows * 8, total = n0 + j1.rows * 8;  // 8-column groups
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const bool second = t >= n0;
+    const SplitJob& J = second ? j1 : j0;
+    const int64_t e = second ? t - n0 : t;
+    const bool vec = (R2 & 3) == 0 && (reinterpret_cast<uintptr_t>(J.L) & 15) == 0;
     const int64_t r = e >> 3;
     const int c0 = (int)(e & 7) * 8;
     float x[8];
-    const float* src = L + r * R2 + c0;
+    const float* src = J.L + r * R2 + c0;
     if (vec) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -612,28 +621,31 @@ __global__ void k_split_bf16(const float* __restrict__ L, int64_t rows, int R2, 
       }
     } else {
 #pragma unroll
-      for (int t = 0; t < 8; ++t) x[t] = c0 + t < R2 ? src[t] : 0.f;
+      for (int q = 0; q < 8; ++q) x[q] = c0 + q < R2 ? src[q] : 0.f;
     }
     uint32_t hw[4], lw[4];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * t], x[2 * t + 1]);
+    for (int q = 0; q < 4; ++q) {
+      const __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * q], x[2 * q + 1]);
       const float2 hf = __bfloat1622float2(h2);
-      const __nv_bfloat162 l2 = __floats2bfloat162_rn(x[2 * t] - hf.x, x[2 * t + 1] - hf.y);
-      hw[t] = *reinterpret_cast<const uint32_t*>(&h2);
-      lw[t] = *reinterpret_cast<const uint32_t*>(&l2);
+      const __nv_bfloat162 l2 = __floats2bfloat162_rn(x[2 * q] - hf.x, x[2 * q + 1] - hf.y);
+      hw[q] = *reinterpret_cast<const uint32_t*>(&h2);
+      lw[q] = *reinterpret_cast<const uint32_t*>(&l2);
     }
-    *reinterpret_cast<uint4*>(hi + e * 8) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-    *reinterpret_cast<uint4*>(lo + e * 8) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    *reinterpret_cast<uint4*>(J.hi + e * 8) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    *reinterpret_cast<uint4*>(J.lo + e * 8) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   }
 }
 
-void launch_split_bf16(const float* L, int64_t rows, int R2, void* hi, void* lo, cudaStream_t st) {
-  if (rows <= 0) return;
-  int64_t g = (rows * 8 + 255) / 256;
+void launch_split_bf16(const float* LA, int64_t rowsA, const float* LB, int64_t rowsB, int R2, void* Ahi, void* Alo,
+                       void* Bhi, void* Blo, cudaStream_t st) {
+  const int64_t total = (rowsA > 0 ? rowsA : 0) * 8 + (rowsB > 0 ? rowsB : 0) * 8;
+  if (total <= 0) return;
+  int64_t g = (total + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
-  launch_pdl(k_split_bf16, (int)g, 256, 0, st, L, rows, R2, reinterpret_cast<__nv_bfloat16*>(hi),
-             reinterpret_cast<__nv_bfloat16*>(lo));
+  const SplitJob j0{LA, rowsA > 0 ? rowsA : 0, reinterpret_cast<__nv_bfloat16*>(Ahi), reinterpret_cast<__nv_bfloat16*>(Alo)};
+  const SplitJob j1{LB, rowsB > 0 ? rowsB : 0, reinterpret_cast<__nv_bfloat16*>(Bhi), reinterpret_cast<__nv_bfloat16*>(Blo)};
+  launch_pdl(k_split_bf16, (int)g, 256, 0, st, j0, j1, R2);
   ++launch_counter();
 }
 

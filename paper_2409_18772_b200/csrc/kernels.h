@@ -377,7 +377,9 @@ int gemm_prepare_maps_tc(const GemmTcOperands& o, void* maps);  // 4 maps; 0 on 
 // whether launch_gemm will run K8 for these sizes (R2 > 0): then L_A / L_B must be split first
 bool gemm_uses_tc(int64_t M, int64_t N, int Kp, int R2, const int* sched);
 // L (rows x R2 fp32) -> hi, lo (rows x 64 bf16, zero-padded)
-void launch_split_bf16(const float* L, int64_t rows, int R2, void* hi, void* lo, cudaStream_t st);
+// L_A (rowsA x R2) and L_B (rowsB x R2) -> bf16 hi / lo (rows of 64, zero-padded), one launch
+void launch_split_bf16(const float* LA, int64_t rowsA, const float* LB, int64_t rowsB, int R2, void* Ahi, void* Alo,
+                       void* Bhi, void* Blo, cudaStream_t st);
 // mapA / mapB: arrays of four CUtensorMap (one-CTA, CTA-pair and narrow-N box shapes); 0 on success
 int gemm_prepare_maps(const GemmArgs& g, void* mapA, void* mapB);
 int& gemm_variant();  // 0 auto (CTA pairs when M, N >= 512 and >= 512 pair tiles, else K8 / K6), 1 K6, 2 K7, 3 K8

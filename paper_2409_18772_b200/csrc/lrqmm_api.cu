@@ -781,8 +781,8 @@ static lrqmm_status_t assemble(lrqmm_handle_t h, bool cross = true, bool wait_fo
   // under one kernel choice stays valid under another).  (Writing them from the assembly kernel
   // itself measured slower: 4-byte per-row stores, c4 apply 3.6 -> 8.5 ms.)
   if (h->tc_ready) {
-    launch_split_bf16(h->LA, h->cfg.m, h->R2, h->LAh, h->LAl, h->st);
-    launch_split_bf16(h->LB_full, h->bsh ? h->b_blk * h->cfg.world_size : h->cfg.n, h->R2, h->LBh, h->LBl, h->st);
+    launch_split_bf16(h->LA, h->cfg.m, h->LB_full, h->bsh ? h->b_blk * h->cfg.world_size : h->cfg.n, h->R2, h->LAh,
+                      h->LAl, h->LBh, h->LBl, h->st);
   }
   return check_launch(h);
 }

@@ -416,26 +416,37 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
   __syncthreads();
   if (ticket != gsize - 1) return;
   __threadfence();
-  for (int pr = threadIdx.x; pr < npairs; pr += 256) {
-    double a = 0.0;
-    for (int b = 16 * grp; b < 16 * grp + gsize; ++b) a += __ldcg(jb.gpart + (int64_t)b * npairs + pr);
-    jb.gpart[(int64_t)(nb + grp) * npairs + pr] = a;
-  }
-  if (threadIdx.x == 0) jb.counter[1 + grp] = 0;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) ticket = atomicAdd(jb.counter, 1);
-  __syncthreads();
-  if (ticket != ngrp - 1) return;
-  __threadfence();
   // G also into shared memory behind the solvers' scratch: the solver reads it from there, not back
   // through L2 (W <= 32)
   double* Gs = dyn + 3 * 32 * 33;
-  for (int pr = threadIdx.x; pr < npairs; pr += 256) {
-    double a = 0.0;
-    for (int g = 0; g < ngrp; ++g) a += __ldcg(jb.gpart + (int64_t)(nb + g) * npairs + pr);
-    jb.G[pr] = a;
-    if (W <= 32) Gs[pr] = a;
+  if (ngrp == 1) {  // one group: its finisher is the last block (the same sums as the two-level path)
+    for (int pr = threadIdx.x; pr < npairs; pr += 256) {
+      double a = 0.0;
+      for (int b = 0; b < gsize; ++b) a += __ldcg(jb.gpart + (int64_t)b * npairs + pr);
+      const double g = 0.0 + a;  // the second level adds the single group sum to 0
+      jb.G[pr] = g;
+      if (W <= 32) Gs[pr] = g;
+    }
+    if (threadIdx.x == 0) jb.counter[1] = 0;
+  } else {
+    for (int pr = threadIdx.x; pr < npairs; pr += 256) {
+      double a = 0.0;
+      for (int b = 16 * grp; b < 16 * grp + gsize; ++b) a += __ldcg(jb.gpart + (int64_t)b * npairs + pr);
+      jb.gpart[(int64_t)(nb + grp) * npairs + pr] = a;
+    }
+    if (threadIdx.x == 0) jb.counter[1 + grp] = 0;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) ticket = atomicAdd(jb.counter, 1);
+    __syncthreads();
+    if (ticket != ngrp - 1) return;
+    __threadfence();
+    for (int pr = threadIdx.x; pr < npairs; pr += 256) {
+      double a = 0.0;
+      for (int g = 0; g < ngrp; ++g) a += __ldcg(jb.gpart + (int64_t)(nb + g) * npairs + pr);
+      jb.G[pr] = a;
+      if (W <= 32) Gs[pr] = a;
+    }
   }
   if (threadIdx.x == 0) jb.counter[0] = 0;  // re-arm for the next launch (stream ordered)
   if (jb.cmax && threadIdx.x < 64) jb.cmax[threadIdx.x] = 0u;  // the next apply64's column maxima
