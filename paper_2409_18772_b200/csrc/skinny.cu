@@ -198,6 +198,106 @@ void launch_apply_small(const float* IN1, const float* S1, const float* IN2, con
 
 // OUT = IN S with S in fp64 and fp64 accumulation (orthonormalisation: keeps Q orthonormal to
 // fp32 rounding instead of cond(IN) * eps32).  Same staging as above; one launch for both sides.
+// Same product on the fp64 tensor cores (W <= 32): Q = Y T with mma.sync.m8n8k4.f64 (DMMA). A warp
+// owns 32 rows of the staged 128-row tile as four 8-row slabs; T's fragments (B: lane l holds
+// T[4 kt + l % 4][8 nt + l / 4]) stay in registers for the whole launch, the A fragment of a slab
+// (lane l holds Y[r0 + l / 4][4 kt + l % 4], converted to fp64 once) comes from shared memory
+// (conflict-free for L = W + 4), and only the k-tiles / n-tiles that reach the live columns run.
+// fp64 products and accumulation as the FMA form (a different, fixed summation order).  Outputs:
+// lane l holds Q[r0 + l / 4][8 nt + 2 (l % 4) + {0, 1}]; column maxima as in k_apply64.
+template <int W>
+__global__ void __launch_bounds__(kApRows) k_apply64_tc(const __grid_constant__ Apply64Jobs jobs) {
+  ::lrqmm::pdl_enter();
+  constexpr int L = ap_ld(W);
+  constexpr int KT = W / 4, NT = W / 8;
+  extern __shared__ __align__(16) double apsm64[];
+  const int q = (jobs.n > 1 && (int)blockIdx.x >= jobs.first[1]) ? 1 : 0;
+  const Apply64Job& J = jobs.j[q];
+  const int b0 = jobs.first[q], nb = jobs.first[q + 1] - b0;
+  float* sin_base = reinterpret_cast<float*>(apsm64 + W * W);  // 2 x kApRows x L (cp.async double buffer)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kin = J.kin > 0 && J.kin < W ? J.kin : W;
+  const int kt_live = (kin + 3) / 4, nt_live = (kin + 7) / 8;
+  double bfr[KT][NT];
+#pragma unroll
+  for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) bfr[kt][nt] = J.S[(4 * kt + (lane & 3)) * W + 8 * nt + (lane >> 2)];
+  __shared__ unsigned bmax[64];
+  if (threadIdx.x < 64) bmax[threadIdx.x] = 0u;
+  float run[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) run[nt][0] = run[nt][1] = 0.f;
+  const int64_t n = J.n;
+  const int64_t step = (int64_t)nb * kApRows;
+  auto stage = [&](int64_t i0, int slot) {
+    if (i0 < n) stage_rows_async<W>(J.IN, i0, (int)(n - i0 < kApRows ? n - i0 : kApRows), sin_base + slot * kApRows * L);
+    cp_async_commit();
+  };
+  const int64_t first = (int64_t)(blockIdx.x - b0) * kApRows;
+  stage(first, 0);
+  stage(first + step, 1);
+  int it = 0;
+  for (int64_t i0 = first; i0 < n; i0 += step, ++it) {
+    const float* sin = sin_base + (it & 1) * kApRows * L;
+    cp_async_wait<1>();  // this tile's group has landed (the next one may still be in flight)
+    __syncthreads();
+    double acc[4][NT][2];
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[sl][nt][0] = acc[sl][nt][1] = 0.0;
+      const float* arow = sin + (warp * 32 + sl * 8 + (lane >> 2)) * L + (lane & 3);
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        if (kt >= kt_live) break;  // zero-padded sketch columns
+        const double a = (double)arow[4 * kt];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          if (nt >= nt_live) break;
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[sl][nt][0]), "+d"(acc[sl][nt][1])
+                       : "d"(a), "d"(bfr[kt][nt]));
+        }
+      }
+    }
+    __syncthreads();  // every row of this buffer has been read: stage the tile after next into it
+    stage(i0 + 2 * step, it & 1);
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl) {
+      const int64_t row = i0 + warp * 32 + sl * 8 + (lane >> 2);
+      const bool ok = row < n;
+      const float cs = (J.cscale && ok) ? J.cscale[row] : 1.f;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const float v0 = (float)acc[sl][nt][0], v1 = (float)acc[sl][nt][1];
+        if (ok) *reinterpret_cast<float2*>(J.OUT + row * W + 8 * nt + 2 * (lane & 3)) = make_float2(v0, v1);
+        if (J.cmax) {  // same fp32 product as the next pass's B image
+          float m0 = ok ? fabsf(v0 * cs) : 0.f, m1 = ok ? fabsf(v1 * cs) : 0.f;
+#pragma unroll
+          for (int o = 4; o < 32; o <<= 1) {
+            m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+            m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+          }
+          run[nt][0] = fmaxf(run[nt][0], m0);
+          run[nt][1] = fmaxf(run[nt][1], m1);
+        }
+      }
+    }
+  }
+  if (J.cmax) {
+    __syncthreads();
+    if (lane < 4)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (run[nt][h] > 0.f) atomicMax(&bmax[8 * nt + 2 * lane + h], __float_as_uint(run[nt][h]));
+    __syncthreads();
+    if (threadIdx.x < W && bmax[threadIdx.x]) atomicMax(J.cmax + threadIdx.x, bmax[threadIdx.x]);
+  }
+}
+
 // NO: outputs computed per row (the rest of the W are zero: columns >= kin of S are zero); inputs
 // c >= kin are skipped (zero-padded sketch columns).
 template <int W, int NO>
@@ -291,7 +391,20 @@ static void apply64_t(Apply64Jobs& jobs, cudaStream_t st) {
 // NO = W - 4 when every job's live columns fit (W = roundup(r + p, 8): the default oversampling
 // leaves 3..7 zero columns), else W
 template <int W>
+static void apply64_tc_t(Apply64Jobs& jobs, cudaStream_t st) {
+  constexpr int smem = W * W * (int)sizeof(double) + 2 * kApRows * ap_ld(W) * (int)sizeof(float);
+  static std::atomic<unsigned> attr{0};
+  ensure_smem(k_apply64_tc<W>, smem, attr);
+  int64_t n[2] = {jobs.j[0].n, jobs.n > 1 ? jobs.j[1].n : 0};
+  const int grid = assign_blocks(n, jobs.n, jobs.first);
+  launch_pdl(k_apply64_tc<W>, grid, kApRows, smem, st, jobs);
+}
+template <int W>
 static void apply64_w(Apply64Jobs& jobs, cudaStream_t st) {
+  static const bool fma_form = getenv("LRQMM_APPLY64_FMA") != nullptr;  // A/B of the two forms
+  if constexpr (W <= 32) {
+    if (!fma_form) return apply64_tc_t<W>(jobs, st);
+  }
   int kin = 0;
   for (int q = 0; q < jobs.n; ++q) kin = max(kin, jobs.j[q].kin > 0 ? jobs.j[q].kin : W);
   if constexpr (W >= 8) {
