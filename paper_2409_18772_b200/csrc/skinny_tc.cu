@@ -65,11 +65,13 @@ struct Cfg {
   static constexpr int kOffB2 = kOffC + kPlane;
   static constexpr int kStageBytes = kHasC ? kOffB2 + kImg : kOffB + kImg;
   static constexpr int kStage = (kStageBytes + 1023) / 1024 * 1024;
-  // kFuse: the fused Gram scratch; else (no codes operand) the epilogue's output transpose tiles
-  // (4 warps x 32 x 32 fp32); the dual pass keeps its third ring stage instead
-  static constexpr int kScratch = kFuse ? kFuseScratch : (kHasC ? 0 : 16 * 1024);
-  static constexpr bool kTransposeOut = !kFuse && !kHasC;
-  static constexpr int S0 = (216 * 1024 - kScratch) / kStage;
+  // kFuse: the fused Gram scratch; else the epilogue's output transpose tiles, 4 warps x 32 rows x
+  // kTCols fp32 (16 columns when a codes operand makes the stage large: the dual pass keeps its
+  // third ring stage)
+  static constexpr bool kTransposeOut = !kFuse;
+  static constexpr int kTCols = kHasC ? 16 : 32;
+  static constexpr int kScratch = kFuse ? kFuseScratch : 4 * 32 * kTCols * 4;
+  static constexpr int S0 = (227 * 1024 - 1280 - kScratch) / kStage;
   static constexpr int S = S0 > 6 ? 6 : S0;
   static_assert(S >= 2, "ring depth");
   static_assert(!kFuse || NA == 1, "fused Gram / solver for W <= 32 only");
@@ -649,16 +651,13 @@ __global__ void __launch_bounds__(kFuse ? tcp::kThreadsFused : tcp::kThreads, 1)
       if (kHasC) {
 #pragma unroll
         for (int g = 0; g < NA; ++g) {
-          uint32_t v[32];
+          uint32_t v[32], w[32];
           const uint32_t tC = trow + C::kOffAccC + g * 32;
           tmem_ld_32x32b_x32(tC + 2 * WN, v);
+          tmem_ld_32x32b_x32(tC + WN, w);
           tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < 32; ++c) o[GU + g][c] = (float)(int)v[c] * 0x1p-14f;
-          tmem_ld_32x32b_x32(tC + WN, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int c = 0; c < 32; ++c) o[GU + g][c] += (float)(int)v[c] * 0x1p-7f;
+          for (int c = 0; c < 32; ++c) o[GU + g][c] = (float)(int)v[c] * 0x1p-14f + (float)(int)w[c] * 0x1p-7f;
           tmem_ld_32x32b_x32(tC, v);
           tmem_ld_wait();
 #pragma unroll
@@ -685,28 +684,41 @@ __global__ void __launch_bounds__(kFuse ? tcp::kThreadsFused : tcp::kThreads, 1)
           for (int c = 0; c < 32; ++c) o[GU + g][c] = o[GU + g][c] * (inv_row * cs[g * 32 + c]);
       }
       if constexpr (C::kTransposeOut) {
-        // warp-private 32 x 32 transpose (16-byte groups XOR-swizzled by row) per 32-column group, so
-        // that each 16-byte store instruction writes 4 whole row segments of this warp's 32 rows
-        float* stile = scratch + (warp - 2) * 32 * 32;
+        // warp-private transpose through shared memory (32 rows x kTCols, 16-byte groups XOR-swizzled
+        // by row), so that each 16-byte store instruction writes whole row segments of 4 (32 columns)
+        // or 8 (16 columns) rows instead of 16-byte pieces of 32 rows
+        constexpr int TC = C::kTCols, NQ = TC / 4, RPI = 32 / NQ;  // float4 per row, rows per instruction
+        float* stile = scratch + (warp - 2) * 32 * TC;
         const int64_t orow0 = (int64_t)blk * BM + quad * 32;
-        float* obase = a.out1 + (int64_t)split * a.nout * a.W;
-        const int rsub = lane >> 3, g4 = lane & 7;
-#pragma unroll
-        for (int g = 0; g < GU; ++g) {
+        const int rsub = lane / NQ, gq = lane % NQ;
+        auto put = [&](const float* ov, float* obase, int col_base) {
           __syncwarp();
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            *reinterpret_cast<float4*>(stile + lane * 32 + 4 * (q ^ (lane & 7))) =
-                make_float4(o[g][4 * q], o[g][4 * q + 1], o[g][4 * q + 2], o[g][4 * q + 3]);
+          for (int qq = 0; qq < NQ; ++qq)
+            *reinterpret_cast<float4*>(stile + lane * TC + 4 * (qq ^ (lane & (NQ - 1)))) =
+                make_float4(ov[4 * qq], ov[4 * qq + 1], ov[4 * qq + 2], ov[4 * qq + 3]);
           __syncwarp();
-          const int col = g * 32 + 4 * g4;
+          const int col = col_base + 4 * gq;
 #pragma unroll
-          for (int it = 0; it < 8; ++it) {
-            const int r = 4 * it + rsub;
-            const float4 v4 = *reinterpret_cast<const float4*>(stile + r * 32 + 4 * (g4 ^ (r & 7)));
-            if (orow0 + r < a.nout && col < a.W)
-              *reinterpret_cast<float4*>(obase + (orow0 + r) * a.W + col) = v4;
+          for (int it = 0; it < 32 / RPI; ++it) {
+            const int r = RPI * it + rsub;
+            const float4 v4 = *reinterpret_cast<const float4*>(stile + r * TC + 4 * (gq ^ (r & (NQ - 1))));
+            if (orow0 + r < a.nout && col < a.W) *reinterpret_cast<float4*>(obase + (orow0 + r) * a.W + col) = v4;
           }
+        };
+        if (kHasU) {
+          float* obase = a.out1 + (int64_t)split * a.nout * a.W;
+#pragma unroll
+          for (int g = 0; g < GU; ++g)
+#pragma unroll
+            for (int h = 0; h < 32 / TC; ++h) put(&o[g][h * TC], obase, g * 32 + h * TC);
+        }
+        if (kHasC) {
+          float* obase = a.out2 + (int64_t)split * a.nout * a.W;
+#pragma unroll
+          for (int g = 0; g < NA; ++g)
+#pragma unroll
+            for (int h = 0; h < 32 / TC; ++h) put(&o[GU + g][h * TC], obase, g * 32 + h * TC);
         }
       } else if (orow < a.nout) {
         if (kHasU) {
