@@ -58,7 +58,9 @@ LRQMM_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)
 // Up to kMaxApply jobs per launch: job q owns blocks [first[q], first[q+1]) and walks its rows.
 // NO = the outputs computed per row (nout rounded up to 8): no FMAs or shared-memory reads for the
 // W - NO columns that no job writes (the factor assembly writes r of W).
-template <int W, int NO>
+// kIn2: some job of the launch has IN2 (staging for both inputs); else one input, half the staging
+// shared memory (more resident blocks for the tall single-input assembly jobs)
+template <int W, int NO, bool kIn2>
 __global__ void __launch_bounds__(kApRows) k_apply_small(const __grid_constant__ ApplyJobs jobs) {
   ::lrqmm::pdl_enter();
   constexpr int L = ap_ld(W);
@@ -69,7 +71,8 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const __grid_constant__
   const int b0 = jobs.first[q], nb = jobs.first[q + 1] - b0;
   float* s1 = apsm;                      // W x NO
   float* s2 = s1 + W * NO;               // W x NO
-  float* sin_base = s2 + W * NO;         // 2 buffers x (IN1, IN2) x kApRows x L (cp.async double buffer)
+  float* sin_base = s2 + W * NO;         // 2 buffers x (IN1[, IN2]) x kApRows x L (cp.async double buffer)
+  constexpr int kSlot = (kIn2 ? 2 : 1) * kApRows * L;
   const int nout = J.nout;
   const int kin = J.kin > 0 && J.kin < W ? J.kin : W;
   for (int e = threadIdx.x; e < W * NO; e += blockDim.x) {
@@ -83,8 +86,8 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const __grid_constant__
   auto stage = [&](int64_t i0, int slot) {
     if (i0 < n) {
       const int nr = (int)(n - i0 < kApRows ? n - i0 : kApRows);
-      stage_rows_async<W>(J.IN1, i0, nr, sin_base + slot * 2 * kApRows * L);
-      if (J.IN2) stage_rows_async<W>(J.IN2, i0, nr, sin_base + (slot * 2 + 1) * kApRows * L);
+      stage_rows_async<W>(J.IN1, i0, nr, sin_base + slot * kSlot);
+      if (kIn2 && J.IN2) stage_rows_async<W>(J.IN2, i0, nr, sin_base + slot * kSlot + kApRows * L);
     }
     cp_async_commit();
   };
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const __grid_constant__
   int it = 0;
   for (int64_t i0 = first; i0 < n; i0 += step, ++it) {
     const int nr = (int)(n - i0 < kApRows ? n - i0 : kApRows);
-    float* sin1 = sin_base + (it & 1) * 2 * kApRows * L;
+    float* sin1 = sin_base + (it & 1) * kSlot;
     float* sin2 = sin1 + kApRows * L;
     cp_async_wait<1>();  // this tile's group has landed (the next one may still be in flight)
     __syncthreads();
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(kApRows) k_apply_small(const __grid_constant__
 #pragma unroll
           for (int o = 0; o < NO; ++o) acc[o] = fmaf(xs[j], s1[(4 * c4 + j) * NO + o], acc[o]);
       }
-      if (J.IN2) {
+      if (kIn2 && J.IN2) {
 #pragma unroll(W <= 32 ? W / 4 : 2)
         for (int c4 = 0; c4 < W / 4; ++c4) {
           if (4 * c4 >= kin) break;
@@ -154,15 +157,35 @@ static int assign_blocks(const int64_t* n, int njobs, int* first) {
   return first[njobs];
 }
 
-template <int W, int NO>
+template <int W, int NO, bool kIn2>
 static void apply_small_t(ApplyJobs& jobs, cudaStream_t st) {
-  constexpr int smem = (4 * kApRows * ap_ld(W) + 2 * W * NO) * (int)sizeof(float);
+  constexpr int smem = ((kIn2 ? 4 : 2) * kApRows * ap_ld(W) + 2 * W * NO) * (int)sizeof(float);
   static std::atomic<unsigned> attr{0};
-  ensure_smem(k_apply_small<W, NO>, smem, attr);
+  ensure_smem(k_apply_small<W, NO, kIn2>, smem, attr);
   int64_t n[kMaxApply];
   for (int q = 0; q < jobs.n; ++q) n[q] = jobs.j[q].n;
   const int grid = assign_blocks(n, jobs.n, jobs.first);
-  launch_pdl(k_apply_small<W, NO>, grid, kApRows, smem, st, jobs);
+  launch_pdl(k_apply_small<W, NO, kIn2>, grid, kApRows, smem, st, jobs);
+}
+// tall single-input jobs (>= 64K rows) go in a launch of their own with half the staging memory;
+// otherwise one launch for all (a launch costs more than the occupancy buys on short panels)
+template <int W, int NO>
+static void apply_small_t(ApplyJobs& jobs, cudaStream_t st) {
+  ApplyJobs one{}, two{};
+  int64_t tall1 = 0;
+  for (int q = 0; q < jobs.n; ++q) {
+    if (jobs.j[q].IN2) {
+      two.j[two.n++] = jobs.j[q];
+    } else {
+      one.j[one.n++] = jobs.j[q];
+      tall1 = jobs.j[q].n > tall1 ? jobs.j[q].n : tall1;
+    }
+  }
+  if (two.n == 0) return apply_small_t<W, NO, false>(jobs, st);
+  if (one.n == 0 || tall1 < 65536) return apply_small_t<W, NO, true>(jobs, st);
+  apply_small_t<W, NO, false>(one, st);
+  apply_small_t<W, NO, true>(two, st);
+  ++launch_counter();
 }
 // NO = W - 8 covers the factor assembly for the default oversampling (r + 5 <= W = roundup(r + p, 8)
 // puts roundup(r, 8) at W - 8 or W); everything else computes all W columns (instantiations and
