@@ -254,19 +254,28 @@ __global__ void __launch_bounds__(256) k_prep_img(PrepJobs jb) {
         x[t] = __ldg(J.P + j * W + (cok ? c : 0));
         y[t] = __ldg(sp + (hs ? j : 0));
       }
-      uint32_t w1[4] = {0, 0, 0, 0}, w2[4] = {0, 0, 0, 0}, w3[4] = {0, 0, 0, 0};
+      // digits of v = p1 + p2 / 128 + p3 / 16384 (each rounded to nearest even in turn):
+      //   p1 = rint(v), p2 = rint((v - p1) 128), p3 = rint(((v - p1) 128 - p2) 128).  Every difference
+      //   and power-of-two scaling is exact (|v| < 64) and shifting by an even integer commutes with
+      //   rint, so with n_e = rint(2^e v): p1 = n_0, p2 = n_7 - 128 n_0, p3 = n_14 - 128 n_7.
+      //   Bytes packed four at a time (PRMT).
+      uint32_t w1[4], w2[4], w3[4];
 #pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const int64_t j = g * tcp::BK + ch * 16 + t;
-        const float v = j < n ? (hs ? x[t] * y[t] : x[t]) * sc : 0.f;
-        const float p1 = rintf(v);
-        const float r1 = (v - p1) * 128.f;  // exact: |v| < 64, power-of-two scaling
-        const float p2 = rintf(r1);
-        const float p3 = rintf((r1 - p2) * 128.f);
-        const int sh = 8 * (t & 3);
-        w1[t >> 2] |= ((uint32_t)(int)p1 & 0xffu) << sh;
-        w2[t >> 2] |= ((uint32_t)(int)p2 & 0xffu) << sh;
-        w3[t >> 2] |= ((uint32_t)(int)p3 & 0xffu) << sh;
+      for (int t4 = 0; t4 < 4; ++t4) {
+        int a1[4], a2[4], a3[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int t = 4 * t4 + u;
+          const int64_t j = g * tcp::BK + ch * 16 + t;
+          const float v = j < n ? (hs ? x[t] * y[t] : x[t]) * sc : 0.f;
+          const int n0 = __float2int_rn(v), n7 = __float2int_rn(v * 128.f), n14 = __float2int_rn(v * 16384.f);
+          a1[u] = n0;
+          a2[u] = n7 - 128 * n0;
+          a3[u] = n14 - 128 * n7;
+        }
+        w1[t4] = __byte_perm(__byte_perm(a1[0], a1[1], 0x0040), __byte_perm(a1[2], a1[3], 0x0040), 0x5410);
+        w2[t4] = __byte_perm(__byte_perm(a2[0], a2[1], 0x0040), __byte_perm(a2[2], a2[3], 0x0040), 0x5410);
+        w3[t4] = __byte_perm(__byte_perm(a3[0], a3[1], 0x0040), __byte_perm(a3[2], a3[3], 0x0040), 0x5410);
       }
       uint8_t* base = J.img + g * kImg;
       *reinterpret_cast<uint4*>(base + off_k128(c, ch * 16)) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
@@ -1365,19 +1374,28 @@ __global__ void __launch_bounds__(kApT) k_apply_prep(const ApplyPrep ap, int* er
         x[t] = __ldcg(J.P + j * W + (cok ? c : 0));
         y[t] = hs ? __ldg(J.scale + j) : 1.f;
       }
-      uint32_t w1[4] = {0, 0, 0, 0}, w2[4] = {0, 0, 0, 0}, w3[4] = {0, 0, 0, 0};
+      // digits of v = p1 + p2 / 128 + p3 / 16384 (each rounded to nearest even in turn):
+      //   p1 = rint(v), p2 = rint((v - p1) 128), p3 = rint(((v - p1) 128 - p2) 128).  Every difference
+      //   and power-of-two scaling is exact (|v| < 64) and shifting by an even integer commutes with
+      //   rint, so with n_e = rint(2^e v): p1 = n_0, p2 = n_7 - 128 n_0, p3 = n_14 - 128 n_7.
+      //   Bytes packed four at a time (PRMT).
+      uint32_t w1[4], w2[4], w3[4];
 #pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const int64_t j = g * tcp::BK + ch * 16 + t;
-        const float v = j < n ? (hs ? x[t] * y[t] : x[t]) * sc : 0.f;
-        const float p1 = rintf(v);
-        const float r1 = (v - p1) * 128.f;  // exact: |v| < 64, power-of-two scaling
-        const float p2 = rintf(r1);
-        const float p3 = rintf((r1 - p2) * 128.f);
-        const int sh = 8 * (t & 3);
-        w1[t >> 2] |= ((uint32_t)(int)p1 & 0xffu) << sh;
-        w2[t >> 2] |= ((uint32_t)(int)p2 & 0xffu) << sh;
-        w3[t >> 2] |= ((uint32_t)(int)p3 & 0xffu) << sh;
+      for (int t4 = 0; t4 < 4; ++t4) {
+        int a1[4], a2[4], a3[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int t = 4 * t4 + u;
+          const int64_t j = g * tcp::BK + ch * 16 + t;
+          const float v = j < n ? (hs ? x[t] * y[t] : x[t]) * sc : 0.f;
+          const int n0 = __float2int_rn(v), n7 = __float2int_rn(v * 128.f), n14 = __float2int_rn(v * 16384.f);
+          a1[u] = n0;
+          a2[u] = n7 - 128 * n0;
+          a3[u] = n14 - 128 * n7;
+        }
+        w1[t4] = __byte_perm(__byte_perm(a1[0], a1[1], 0x0040), __byte_perm(a1[2], a1[3], 0x0040), 0x5410);
+        w2[t4] = __byte_perm(__byte_perm(a2[0], a2[1], 0x0040), __byte_perm(a2[2], a2[3], 0x0040), 0x5410);
+        w3[t4] = __byte_perm(__byte_perm(a3[0], a3[1], 0x0040), __byte_perm(a3[2], a3[3], 0x0040), 0x5410);
       }
       uint8_t* base = J.img + g * kImg;
       *reinterpret_cast<uint4*>(base + off_k128(c, ch * 16)) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
