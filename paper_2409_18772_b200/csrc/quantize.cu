@@ -298,7 +298,11 @@ constexpr int kThreads = kCons + 32;       // + producer warp
 constexpr int kSmemBudget = 200 * 1024;
 }  // namespace k1t
 
-template <int VPT, bool kFixedLam, int kMode>
+// G consumer groups (kCons / G threads each) work on G different rows at a time: ring slot `it` goes
+// to group it % G, each group has its own named barrier (1 + group) for the row's amax.  G = 1 is one
+// row at a time over all 16 warps; mid-size rows (K ~ 4K: few rows per CTA) use G = 2 so that the
+// per-row chain (amax reduction, barrier, division) of one row overlaps another's.
+template <int VPT, bool kFixedLam, int kMode, int G>
 __global__ void __launch_bounds__(k1t::kThreads, 1)
     k1_quantize_tma(const float* __restrict__ X, int64_t ldx, int rows, int K, int Kp, int qmax, int mode,
                     int8_t* __restrict__ codes, float* __restrict__ lam_out, float* __restrict__ inv_out,
@@ -306,6 +310,7 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
                     int64_t ldu, int64_t uplane, int ns, int slot_bytes) {
   ::lrqmm::pdl_enter();
   using namespace k1t;
+  constexpr int TG = kCons / G, WG = TG / 32;  // threads / warps per group
   extern __shared__ __align__(128) uint8_t smem_k1[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_k1);
   uint64_t* empty = full + ns;
@@ -315,7 +320,7 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kCons / 32);
+      mbar_init(&empty[s], WG);
     }
     fence_mbar_init();
   }
@@ -335,8 +340,9 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
     return;
   }
   // --------------------------------------------------------------- consumers
-  int it = 0;
-  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, ++it) {
+  const int grp = tid / TG, gt = tid - grp * TG;  // group, thread within the group
+  int it = grp, kr = 0;
+  for (int64_t r = blockIdx.x + (int64_t)grp * gridDim.x; r < rows; r += (int64_t)G * gridDim.x, it += G, ++kr) {
     const int s = it % ns;
     mbar_wait(&full[s], (it / ns) & 1);
     const uint32_t base = smem_u32(ring + (size_t)s * slot_bytes);
@@ -344,7 +350,7 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
     float amax = 0.f, chk = 0.f;  // chk = sum x * 0: NaN iff some x is NaN or Inf
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
-      const int col = (tid + i * kCons) * 4;
+      const int col = (gt + i * TG) * 4;
       v[i] = col < K ? lds128(base + (uint32_t)col * 4u) : make_float4(0.f, 0.f, 0.f, 0.f);
       chk = __fmaf_rn(v[i].x, 0.f, chk);
       chk = __fmaf_rn(v[i].y, 0.f, chk);
@@ -362,14 +368,14 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
       lam = lam_in[0];
     } else {
       amax = warp_max(amax);
-      if (lane == 0) red[it & 1][warp] = amax;
-      asm volatile("bar.sync 1, %0;" ::"n"(kCons) : "memory");
-      float m = red[it & 1][0];
+      if (lane == 0) red[kr & 1][warp] = amax;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(TG) : "memory");
+      float m = red[kr & 1][grp * WG];
 #pragma unroll
-      for (int w = 1; w < kCons / 32; ++w) m = fmaxf(m, red[it & 1][w]);
+      for (int w = 1; w < WG; ++w) m = fmaxf(m, red[kr & 1][grp * WG + w]);
       // lambda = RN32(qmax / amax) (IEEE division), 1 for an all-zero row.
       lam = (m == 0.f) ? 1.f : __fdiv_rn(static_cast<float>(qmax), m);
-      if (tid == 0) {
+      if (gt == 0) {
         lam_out[r] = lam;
         inv_out[r] = __frcp_rn(lam);
       }
@@ -380,7 +386,7 @@ __global__ void __launch_bounds__(k1t::kThreads, 1)
     const float l32 = lam * 32768.f;
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
-      const int col = (tid + i * kCons) * 4;
+      const int col = (gt + i * TG) * 4;
       if (col < Kp) {
         // padded columns (K <= col < Kp) hold x = 0 -> code 0, u = 0
         const int c0 = code_fast<kMode>(lam, v[i].x, qmax), c1 = code_fast<kMode>(lam, v[i].y, qmax);
@@ -577,7 +583,7 @@ static int64_t launch_k1_rows_tma(const QuantArgs& a, bool fixed, cudaStream_t s
   return rows_full;
 }
 
-template <int VPT>
+template <int VPT, int G = 1>
 static bool launch_k1_tma_t(const QuantArgs& a, bool fixed, cudaStream_t st) {
   const int slot = (a.K * 4 + 1023) / 1024 * 1024;
   int ns = k1t::kSmemBudget / slot;
@@ -588,8 +594,8 @@ static bool launch_k1_tma_t(const QuantArgs& a, bool fixed, cudaStream_t st) {
   const int grid = (int)(a.rows < nsm ? a.rows : nsm);
 #define K1T_LAUNCH(F, M)                                                                                         \
   do {                                                                                                           \
-    cudaFuncSetAttribute(k1_quantize_tma<VPT, F, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);        \
-    launch_pdl(k1_quantize_tma<VPT, F, M>, grid, k1t::kThreads, smem, st, a.X, a.ldx, (int)a.rows, a.K, a.Kp, a.qmax,   \
+    cudaFuncSetAttribute(k1_quantize_tma<VPT, F, M, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);     \
+    launch_pdl(k1_quantize_tma<VPT, F, M, G>, grid, k1t::kThreads, smem, st, a.X, a.ldx, (int)a.rows, a.K, a.Kp, a.qmax, \
                                                                   a.mode, a.codes, a.lam, a.inv_lam, a.lam_fixed, \
                                                                   a.err_flag, a.U, a.ldu, a.uplane, ns, slot);   \
   } while (0)
@@ -612,7 +618,16 @@ static bool launch_k1_tma(const QuantArgs& a, bool fixed, cudaStream_t st) {
   if ((reinterpret_cast<uintptr_t>(a.X) & 15) != 0 || a.ldx % 4 != 0 || a.K % 4 != 0 || a.K < 4096) return false;
   const int Kp = a.Kp;
   constexpr int C4 = k1t::kCons * 4;
-  if (Kp <= C4 * 2) return launch_k1_tma_t<2>(a, fixed, st);
+  // mid-size rows (K <= 4096): four consumer groups, four rows in flight per CTA (c2: 29.5 -> 19 us per
+  // side); LRQMM_K1_GROUPS=1 / 2 for A/B
+  static const int groups = [] {
+    const char* e = getenv("LRQMM_K1_GROUPS");
+    return e && atoi(e) > 0 ? atoi(e) : 4;
+  }();
+  if (Kp <= C4 * 2) {
+    if (groups >= 4) return launch_k1_tma_t<8, 4>(a, fixed, st);
+    return groups >= 2 ? launch_k1_tma_t<4, 2>(a, fixed, st) : launch_k1_tma_t<2>(a, fixed, st);
+  }
   if (Kp <= C4 * 4) return launch_k1_tma_t<4>(a, fixed, st);
   if (Kp <= C4 * 8) return launch_k1_tma_t<8>(a, fixed, st);
   if (Kp <= C4 * 12) return launch_k1_tma_t<12>(a, fixed, st);
