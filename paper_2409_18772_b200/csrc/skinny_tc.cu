@@ -627,12 +627,14 @@ __global__ void __launch_bounds__(kFuse ? tcp::kThreadsFused : tcp::kThreads, 1)
       const TcArgs& a = args.a[side];
       const int acc = NACC == 2 ? (lu & 1) : 0;
       const uint32_t tph = NACC == 2 ? ((lu >> 1) & 1) : (lu & 1);
+      const int64_t orow = (int64_t)blk * BM + quad * 32 + lane;
+      // ROW: rows of R and X~ carry 1/lambda_i (COL folded it into P); loaded before the wait on the
+      // accumulator so its latency overlaps the unit's MMAs
+      float inv_row = 1.f;
+      if (kMode == 0) inv_row = orow < a.rows ? __ldg(a.inv_lam + orow) : 1.f;
       mbar_wait(&tfull[acc], tph);
       tc_fence_after();
-      const int64_t orow = (int64_t)blk * BM + quad * 32 + lane;
       const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + acc * C::kAccCols;
-      float inv_row = 1.f;  // ROW: rows of R and X~ carry 1/lambda_i (COL folded it into P)
-      if (kMode == 0) inv_row = orow < a.rows ? __ldg(a.inv_lam + orow) : 1.f;
       constexpr int GU = kHasU ? NA : 0;       // output groups of the residual product
       constexpr int NG = GU + (kHasC ? NA : 0);  // 32-column output groups per row
       float o[NG][32];
