@@ -52,7 +52,9 @@ def run_gpu(A, Bt, bits, r, p, OmA=None, OmB=None, q=1, rounding="floor", gran="
 @pytest.mark.parametrize("bits", [4, 8])
 @pytest.mark.parametrize("rounding", ["floor", "trunc", "nearest"])
 @pytest.mark.parametrize("gran", ["row", "tensor"])
-@pytest.mark.parametrize("shape", [(300, 1000), (130, 130), (5, 40000), (7, 30000), (1000, 77)])
+@pytest.mark.parametrize("shape", [(300, 1000), (130, 130), (5, 40000), (7, 30000), (1000, 77),
+                                   # short-row K1 at 8 / 16 lanes per row; four-group TMA K1 with fewer rows than SMs
+                                   (600, 64), (301, 128), (257, 256), (33, 4096), (700, 4096)])
 def test_quantize_bit_exact(bits, rounding, gran, shape):
     rows, K = shape
     X = S.gen_matrix("normal", rows, K, 7 + bits)
