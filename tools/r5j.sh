@@ -1,0 +1,5 @@
+# dual pass: the other side's Q1 image built once (shared by both sides)
+timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_parity.py tests/test_gpu_multirank.py -q -x > gpurun_out/r5j_tests.log 2>&1; echo rc=$? >> gpurun_out/r5j_tests.log
+cp paper_2409_18772_b200/liblrqmm.so /tmp/new.so
+bash tools/ab.sh $PWD/paper_2409_18772_b200/liblrqmm_prev.so $PWD/paper_2409_18772_b200/liblrqmm.so c2 3 > gpurun_out/r5j_ab.log 2>&1
+timeout 600 python bench.py --config c4 --steps 3 --warmup 2 --no-cpu-baseline --no-e2e > gpurun_out/r5j_bench_c4.json 2>&1
