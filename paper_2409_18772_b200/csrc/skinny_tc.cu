@@ -998,17 +998,27 @@ static void run_tc(int nsides, const TcPassSide* sides, int W, bool reduce1, int
                                  rlen, nkb, cmax};
     };
     jfirst[sd] = jb.njobs;
-    // an operand image is either prebuilt (pimg: launch_apply_prep) or built by this pass's prep
+    // an operand image is either prebuilt (pimg: launch_apply_prep), already built by this pass's prep
+    // for the other side (the dual pass multiplies each side by the other's Q1: the same operand, the
+    // same column maxima, the same image), or built now
     auto image = [&](const float* P, const float* scale, uint8_t* img, const unsigned* cmax, const uint8_t* pre,
                      const uint8_t*& out_img, const float*& out_cinv) {
       if (pre) {
         out_img = pre;
         out_cinv = img_cinv(const_cast<uint8_t*>(pre), rlen, W);
-      } else {
-        add_job(P, scale, img, cmax);
-        out_img = img;
-        out_cinv = jb.j[jb.njobs - 1].cinv;
+        return;
       }
+      for (int q = 0; q < jb.njobs; ++q) {
+        const PrepJob& o = jb.j[q];
+        if (cmax && o.P == P && o.scale == scale && o.cmax_in == cmax && o.n == rlen) {
+          out_img = o.img;
+          out_cinv = o.cinv;
+          return;
+        }
+      }
+      add_job(P, scale, img, cmax);
+      out_img = img;
+      out_cinv = jb.j[jb.njobs - 1].cinv;
     };
     if (kVar == 2) {
       image(sides[sd].P2, nullptr, sides[sd].img, sides[sd].cmax2, sides[sd].pimg2, a.img1, a.cinv1);

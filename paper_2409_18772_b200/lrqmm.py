@@ -279,12 +279,27 @@ class Lrqmm:
         _check(self.lib.lrqmm_gemm_int32(self.h, ptr, ld), "lrqmm_gemm_int32")
         return C
 
+    def _getter(self, call):
+        """Run a getter that writes freshly allocated tensors on the handle stream.  The tensors come
+        from the caller's current stream (the caching allocator may hand out memory that stream still
+        uses) and are read there afterwards, so when the handle has a stream of its own both orderings
+        are enforced: handle stream after the current one, current one after the copy."""
+        import torch
+
+        cur = torch.cuda.current_stream(self.device)
+        other = self.stream is not None and self.stream != cur
+        if other:
+            self.stream.wait_stream(cur)
+        call()
+        if other:
+            cur.wait_stream(self.stream)
+
     def codes(self, side: int):
         import torch
 
         rows = self.side_rows(side)
         out = torch.empty((rows, self.k), dtype=torch.int8, device=f"cuda:{self.device}")
-        _check(self.lib.lrqmm_get_codes(self.h, side, _ptr(out), self.k), "lrqmm_get_codes")
+        self._getter(lambda: _check(self.lib.lrqmm_get_codes(self.h, side, _ptr(out), self.k), "lrqmm_get_codes"))
         return out
 
     def scales(self, side: int):
@@ -292,7 +307,7 @@ class Lrqmm:
 
         rows = self.side_rows(side)
         out = torch.empty((rows,), dtype=torch.float32, device=f"cuda:{self.device}")
-        _check(self.lib.lrqmm_get_scales(self.h, side, _ptr(out)), "lrqmm_get_scales")
+        self._getter(lambda: _check(self.lib.lrqmm_get_scales(self.h, side, _ptr(out)), "lrqmm_get_scales"))
         return out
 
     def factors(self, side: int):
@@ -301,7 +316,7 @@ class Lrqmm:
         rows = self.side_rows(side)
         us = torch.empty((rows, self.rank), dtype=torch.float32, device=f"cuda:{self.device}")
         v = torch.empty((self.k, self.rank), dtype=torch.float32, device=f"cuda:{self.device}")
-        _check(self.lib.lrqmm_get_factors(self.h, side, _ptr(us), _ptr(v)), "lrqmm_get_factors")
+        self._getter(lambda: _check(self.lib.lrqmm_get_factors(self.h, side, _ptr(us), _ptr(v)), "lrqmm_get_factors"))
         return us, v
 
     def correction(self, side: int):
@@ -310,7 +325,7 @@ class Lrqmm:
         rows = self.side_rows(side)
         w = self.lib.lrqmm_correction_width(self.h)
         out = torch.empty((rows, w), dtype=torch.float32, device=f"cuda:{self.device}")
-        _check(self.lib.lrqmm_get_correction(self.h, side, _ptr(out)), "lrqmm_get_correction")
+        self._getter(lambda: _check(self.lib.lrqmm_get_correction(self.h, side, _ptr(out)), "lrqmm_get_correction"))
         return out
 
     def timings_us(self):
