@@ -307,9 +307,11 @@ __global__ void __launch_bounds__(32) k_warp_chol(EigJobs jobs) {
 
 // ------------------------------------------------- fused orth / truncation
 // One launch per RSVD orthonormalisation (or truncation) step, both sides (blockIdx.y):
-//   phase 1 (all blocks): Y = sum of the split-K partials (fixed order) -> written once;
-//                         the block's rows are kept in smem and their fp64 Gram partial formed;
-//   phase 2 (last block by ticket): fixed-order sum of the Gram partials -> G, then the
+//   phase 1 (all blocks): the block's rows of the dense Y (split-K partials were reduced by the
+//                         launch before) stream into shared memory by bulk copies, double-buffered,
+//                         and their fp64 Gram partial is formed on the fp64 tensor cores;
+//   phase 2 (last block by ticket): fixed-order sum of the Gram partials -> G (one level when all
+//                         blocks form one group of 16, else two), then G in shared memory and the
 //                         pivoted CholQR transform (mode 0) or the truncation eigenvectors
 //                         (mode 1), or nothing (mode 2: G must first be summed across ranks).
 // rows per shared-memory chunk (fp32, two buffers in the 66.5 KB dynamic allocation)
