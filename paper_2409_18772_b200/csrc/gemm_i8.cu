@@ -591,6 +591,217 @@ __global__ void __launch_bounds__(g8::kThreads, 1)
   }
 }
 
+// K8w -- K8 with 128 x 256 tiles (UMMA N = 256): per k-block a stage carries A (16 KB) and B (32 KB),
+// so the shared-memory operand traffic per MMA flop is 3/4 of K8's (at N = 128 the operand fetch,
+// not the tensor pipe, bounds a one-CTA tile).  TMEM holds ONE tile: main int32 in columns 0..255,
+// the bf16 correction in 256..511; the epilogue does not overlap the next tile's MMAs, the two
+// epilogue groups split the tile's columns (0..127 | 128..255) so it drains twice as fast, and the
+// producer keeps streaming the next tile's stages meanwhile.  Same arithmetic as K8.
+namespace g8w {
+constexpr int BM = 128, BN = 256, BK = 128, UK = 32;
+constexpr int kStageBytes = BM * BK + BN * BK;  // 48 KB: int8 A | B, or bf16 [L_A | L_B] (hi or lo)
+constexpr int kThreads = 64 + 256;
+constexpr int kStages = 4;
+constexpr int kStile = 8 * 32 * 32 * 4;
+constexpr int kSmem = kStages * kStageBytes + kStile + BN * 4 + 256 + 1024;
+static_assert(kSmem <= 232448, "K8w shared memory");
+}  // namespace g8w
+
+__global__ void __launch_bounds__(g8w::kThreads, 1)
+    k8w_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                const __grid_constant__ CUtensorMap mapLAh, const __grid_constant__ CUtensorMap mapLAl,
+                const __grid_constant__ CUtensorMap mapLBh, const __grid_constant__ CUtensorMap mapLBl, G8Params p) {
+  using namespace g8w;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* stile0 = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // 8 x 32 x 32 (XOR-swizzled)
+  float* sSB0 = stile0 + kStile / 4;                                      // BN: 1/lambda_B of the tile
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sSB0 + BN);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages;
+  uint64_t* tfull = bars + 2 * kStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_tiles = p.num_m * p.num_n;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mapA);
+    tma_prefetch_desc(&mapB);
+    tma_prefetch_desc(&mapLAh);
+    tma_prefetch_desc(&mapLAl);
+    tma_prefetch_desc(&mapLBh);
+    tma_prefetch_desc(&mapLBl);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 256);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (warp == 0) {
+    // -------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      auto next = [&]() {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], kStageBytes);
+      };
+      auto advance = [&]() {
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      };
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, p.num_m, p.num_n, mb, nb);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          next();
+          uint8_t* st = smem + stage * kStageBytes;
+          tma_load_2d(st, &mapA, &full[stage], kb * BK, mb * BM);
+          tma_load_2d(st + BM * BK, &mapB, &full[stage], kb * BK, nb * BN);
+          advance();
+        }
+        next();  // [L_A hi | L_B hi]
+        tma_load_2d(smem + stage * kStageBytes, &mapLAh, &full[stage], 0, mb * BM);
+        tma_load_2d(smem + stage * kStageBytes + BM * BK, &mapLBh, &full[stage], 0, nb * BN);
+        advance();
+        next();  // [L_A lo | L_B lo]
+        tma_load_2d(smem + stage * kStageBytes, &mapLAl, &full[stage], 0, mb * BM);
+        tma_load_2d(smem + stage * kStageBytes + BM * BK, &mapLBl, &full[stage], 0, nb * BN);
+        advance();
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // -------------------------------------------------------------- UMMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idi8 = make_idesc_i8(BM, BN);
+      constexpr uint32_t idbf = make_idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int lt = 0;
+      const uint32_t d_main = tmem_base, d_corr = tmem_base + 256;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+        mbar_wait(tempty, (lt & 1) ^ 1);  // the previous tile's epilogue drained the accumulators
+        tc_fence_after();
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * kStageBytes);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            umma_i8(d_main, make_sw128_kmajor_desc(a_addr + k * UK), make_sw128_kmajor_desc(a_addr + BM * BK + k * UK),
+                    idi8, (kb | k) != 0 ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        const int sx = stage;
+        const uint32_t px = phase;
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        const int sy = stage;
+        const uint32_t py = phase;
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        mbar_wait(&full[sx], px);
+        mbar_wait(&full[sy], py);
+        tc_fence_after();
+        const uint32_t xa = smem_u32(smem + sx * kStageBytes), ya = smem_u32(smem + sy * kStageBytes);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // 4 x K16 = the 64 bf16 of one atom
+          const uint32_t o = k * 32;
+          umma_bf16(d_corr, make_sw128_kmajor_desc(xa + o), make_sw128_kmajor_desc(xa + BM * BK + o), idbf, k != 0);
+          umma_bf16(d_corr, make_sw128_kmajor_desc(xa + o), make_sw128_kmajor_desc(ya + BM * BK + o), idbf, 1u);
+          umma_bf16(d_corr, make_sw128_kmajor_desc(ya + o), make_sw128_kmajor_desc(xa + BM * BK + o), idbf, 1u);
+        }
+        umma_commit(&empty[sx]);
+        umma_commit(&empty[sy]);
+        umma_commit(tfull);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    // group e = columns [128 e, 128 e + 128) of every tile; warp quad = 32 rows
+    const int egrp = (warp - 2) >> 2;
+    const int et = threadIdx.x - 64 - 128 * egrp;
+    const int quad = warp & 3;
+    float* sSB = sSB0 + egrp * 128;
+    float* stile = stile0 + (warp - 2) * 32 * 32;
+    const int rsub = lane >> 3, g4 = lane & 7;
+    int lt = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+      int mb, nb;
+      tile_coords(t, p.num_m, p.num_n, mb, nb);
+      const int64_t row = (int64_t)mb * BM + quad * 32 + lane;
+      const int n0 = nb * BN + egrp * 128;
+      epi_bar_id(1 + egrp);  // the previous tile's readers of sSB are done
+      for (int j = et; j < 128; j += 128) sSB[j] = n0 + j < p.N ? __ldg(p.inv_b + n0 + j) : 0.f;
+      const float sa = row < p.M ? p.alpha * __ldg(p.inv_a + row) : 0.f;
+      epi_bar_id(1 + egrp);
+      mbar_wait(tfull, lt & 1);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(quad * 32) << 16) + egrp * 128;
+      const int64_t row0 = (int64_t)mb * BM + quad * 32;
+#pragma unroll 1
+      for (int ch = 0; ch < 4; ++ch) {
+        const int col0 = n0 + ch * 32;
+        if (col0 >= p.N) break;  // warp-uniform
+        uint32_t ri[32], rc[32];
+        tmem_ld_32x32b_x32(t_row + ch * 32, ri);
+        tmem_ld_32x32b_x32(t_row + 256 + ch * 32, rc);
+        tmem_ld_wait();
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          float4 v;
+          float* pv = &v.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c = 4 * g + e;
+            pv[e] = fmaf(p.alpha, __uint_as_float(rc[c]),
+                         __fmul_rn(static_cast<float>(static_cast<int32_t>(ri[c])), __fmul_rn(sa, sSB[ch * 32 + c])));
+          }
+          *reinterpret_cast<float4*>(stile + lane * 32 + 4 * (g ^ (lane & 7))) = v;
+        }
+        __syncwarp();
+        const int c = col0 + 4 * g4;
+        const bool full4 = p.vec_ok && c + 4 <= p.N;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int r = 4 * it + rsub;
+          const int64_t rw = row0 + r;
+          float4 v = *reinterpret_cast<const float4*>(stile + r * 32 + 4 * (g4 ^ (r & 7)));
+          if (rw >= p.M || c >= p.N) continue;
+          float* out = p.D + rw * p.ldd + c;
+          if (full4) {
+            if (p.beta != 0.f) {
+              const float4 o = *reinterpret_cast<const float4*>(out);
+              v.x = fmaf(p.beta, o.x, v.x); v.y = fmaf(p.beta, o.y, v.y);
+              v.z = fmaf(p.beta, o.z, v.z); v.w = fmaf(p.beta, o.w, v.w);
+            }
+            __stcs(reinterpret_cast<float4*>(out), v);
+          } else {
+            const float* pv = &v.x;
+            for (int e = 0; e < 4; ++e)
+              if (c + e < p.N) out[e] = p.beta != 0.f ? fmaf(p.beta, out[e], pv[e]) : pv[e];
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      mbar_arrive(tempty);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free<512>(tmem_base);
+  }
+}
+
 // L (rows x R2 fp32) -> bf16 hi / lo halves, rows of 64 (zero-padded): the K8 correction operands.
 // One thread per 8 columns of a row: two 16-byte loads (R2 % 4 == 0; else scalar), packed
 // conversions (cvt.rn.bf16x2.f32), one 16-byte store per half.  Both factors (L_A, L_B) in one
@@ -655,6 +866,8 @@ int gemm_prepare_maps_tc(const GemmTcOperands& o, void* maps) {
   if (encode_codes_map(m + 1, reinterpret_cast<const int8_t*>(o.LAl), o.M, 128, g8::BM)) return 1;
   if (encode_codes_map(m + 2, reinterpret_cast<const int8_t*>(o.LBh), o.N, 128, g8::BN)) return 1;
   if (encode_codes_map(m + 3, reinterpret_cast<const int8_t*>(o.LBl), o.N, 128, g8::BN)) return 1;
+  if (encode_codes_map(m + 4, reinterpret_cast<const int8_t*>(o.LBh), o.N, 128, g8w::BN)) return 1;  // K8w
+  if (encode_codes_map(m + 5, reinterpret_cast<const int8_t*>(o.LBl), o.N, 128, g8w::BN)) return 1;
   return 0;
 }
 
@@ -1150,6 +1363,30 @@ static void launch_k8(const GemmArgs& g, const CUtensorMap* mA, const CUtensorMa
   ++launch_counter();
 }
 
+// K8w: mB256 = the B codes map with 256-row boxes, tc[4] / tc[5] = L_B hi / lo with 256-row boxes
+static void launch_k8w(const GemmArgs& g, const CUtensorMap* mA, const CUtensorMap* mB256, const CUtensorMap* tc,
+                       int nsm, cudaStream_t st) {
+  static std::atomic<unsigned> attr{0};
+  ensure_smem(k8w_gemm_tc, g8w::kSmem, attr);
+  G8Params p{};
+  p.M = g.M;
+  p.N = g.N;
+  p.num_kb = (g.Kp + g8w::BK - 1) / g8w::BK;
+  p.num_m = (int)((g.M + g8w::BM - 1) / g8w::BM);
+  p.num_n = (int)((g.N + g8w::BN - 1) / g8w::BN);
+  p.inv_a = g.inv_a;
+  p.inv_b = g.inv_b;
+  p.alpha = g.alpha;
+  p.beta = g.beta;
+  p.D = g.D;
+  p.ldd = g.ldd;
+  p.vec_ok = ((reinterpret_cast<uintptr_t>(g.D) & 15) == 0) && (g.ldd % 4 == 0);
+  const int tiles = p.num_m * p.num_n;
+  const int grid = tiles < nsm ? tiles : nsm;
+  k8w_gemm_tc<<<grid, g8w::kThreads, g8w::kSmem, st>>>(*mA, *mB256, tc[0], tc[1], tc[4], tc[5], p);
+  ++launch_counter();
+}
+
 int launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStream_t st) {
   if (g.M == 0 || g.N == 0) return 0;
   G6Params p;
@@ -1180,7 +1417,16 @@ int launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStrea
   const CUtensorMap* mB = reinterpret_cast<const CUtensorMap*>(mapB);
   const int r2 = g.epi == 0 ? 0 : g.R2;
   if (g.tc_maps && gemm_uses_tc(g.M, g.N, g.Kp, r2, g.sched)) {
-    launch_k8(g, mA, mB + 2, reinterpret_cast<const CUtensorMap*>(g.tc_maps), nsm, st);  // B box 128 rows
+    // K8w (128 x 256 tiles) for N >= 256 with a main loop long enough to carry its non-overlapped
+    // epilogue (c2, 4096^3: 82 -> 72 us); LRQMM_K8W=0 keeps K8, =2 uses K8w at any K
+    static const int wide = [] {
+      const char* e = getenv("LRQMM_K8W");
+      return e ? atoi(e) : 1;
+    }();
+    if (wide && g.N >= 256 && (wide == 2 || g.Kp >= 2048))
+      launch_k8w(g, mA, mB, reinterpret_cast<const CUtensorMap*>(g.tc_maps), nsm, st);  // B box 256 rows
+    else
+      launch_k8(g, mA, mB + 2, reinterpret_cast<const CUtensorMap*>(g.tc_maps), nsm, st);  // B box 128 rows
     return 0;
   }
   if (use_2sm(g.M, g.N, g.sched)) {

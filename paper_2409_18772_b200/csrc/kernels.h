@@ -363,7 +363,7 @@ struct GemmArgs {
   int32_t* Cint;         // M x N (ldd)
   int64_t ldd;
   int* sched;            // device int: dynamic tile counter of the CTA-pair GEMM (zeroed per launch)
-  const void* tc_maps;   // 4 CUtensorMaps of L_A hi / lo, L_B hi / lo (gemm_prepare_maps_tc) or nullptr
+  const void* tc_maps;   // 6 CUtensorMaps of L_A hi / lo, L_B hi / lo, L_B hi / lo 256-row boxes (gemm_prepare_maps_tc) or nullptr
 };
 // bf16 hi / lo operands of the tensor-core correction (K8): rows x 64 bf16 each (128-byte rows)
 struct GemmTcOperands {

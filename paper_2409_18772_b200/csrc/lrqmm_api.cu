@@ -66,7 +66,7 @@ struct lrqmm_handle_s {
   float* LB = nullptr;  // n x R2
   // bf16 hi / lo copies of L_A, L_B (rows x 64) for the tensor-core correction GEMM (K8)
   void *LAh = nullptr, *LAl = nullptr, *LBh = nullptr, *LBl = nullptr;
-  alignas(64) CUtensorMap mapTC[4];
+  alignas(64) CUtensorMap mapTC[6];  // L_A hi / lo, L_B hi / lo (128-row boxes), L_B hi / lo (256-row boxes, K8w)
   bool tc_ready = false;
   float* partial = nullptr;
   int64_t partial_elems = 0;
