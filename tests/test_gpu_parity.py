@@ -172,6 +172,18 @@ def test_lrqmm_rank_and_power_iters(q, r, p, gemm_variant):
     check_d(A, Bt, run_gpu(A, Bt, 4, r, p, OmA, OmB, q=q), ref)
 
 
+@pytest.mark.parametrize("shape,beta", [((300, 520, 2100), 0.0), ((256, 768, 2048), -0.5)])
+def test_wide_tile_gemm_matches_oracle(shape, beta, gemm_variant):
+    """N >= 256 and Kp >= 2048: with the tensor-core correction forced (variant 3) this is the
+    128 x 256-tile K8w (ragged M and N, beta != 0), next to K6 / K7 on the same inputs."""
+    M, N, K = shape
+    A, Bt, OmA, OmB = S.problem(M, N, K, 21, s=9, dist="normal")
+    D0 = np.random.default_rng(1).standard_normal((M, N)).astype(np.float32)
+    ref = O.lrqmm(A, Bt, 4, 16, OmA, OmB, alpha=1.25, beta=beta, D=D0)
+    out = run_gpu(A, Bt, 4, 16, 5, OmA, OmB, alpha=1.25, beta=beta, D0=D0)
+    assert O.relative_error(ref, out["D"]) <= TOL_D
+
+
 def test_direct_quant_modes_match_oracle():
     A, Bt, _, _ = S.problem(300, 260, 900, 1, s=3, dist="u01")
     for rounding, gran in [("trunc", "tensor"), ("nearest", "row"), ("floor", "row")]:
