@@ -152,7 +152,8 @@ def check_d(A, Bt, out, ref):
 @pytest.mark.parametrize("dist", ["normal", "u01", "exp4", "pois10"])
 @pytest.mark.parametrize("shape,r,p", [((256, 256, 256), 8, 5), ((384, 272, 520), 10, 5), ((200, 333, 1100), 4, 0),
                                        ((1000, 130, 700), 16, 5),
-                                       ((1300, 260, 576), 20, 5)])  # the c4 sketch: W = 32, 25 live columns
+                                       ((1300, 260, 576), 20, 5),   # the c4 sketch: W = 32, 25 live columns
+                                       ((700, 300, 500), 12, 5)])   # W = 24, 17 live: a one-column tail block
 def test_lrqmm_matches_oracle(bits, dist, shape, r, p):
     M, N, K = shape
     A, Bt, OmA, OmB = S.problem(M, N, K, r + p, s=1, dist=dist)
