@@ -1423,7 +1423,10 @@ int launch_gemm(const GemmArgs& g, const void* mapA, const void* mapB, cudaStrea
       const char* e = getenv("LRQMM_K8W");
       return e ? atoi(e) : 1;
     }();
-    if (wide && g.N >= 256 && (wide == 2 || g.Kp >= 2048))
+    // ... and with at least one full wave of 128 x 256 tiles (a row-sharded slice with few rows keeps
+    // K8's twice as many tiles busy on more SMs)
+    const int64_t wtiles = ((g.M + 127) / 128) * ((g.N + 255) / 256);
+    if (wide && g.N >= 256 && (wide == 2 || (g.Kp >= 2048 && wtiles >= nsm)))
       launch_k8w(g, mA, mB, reinterpret_cast<const CUtensorMap*>(g.tc_maps), nsm, st);  // B box 256 rows
     else
       launch_k8(g, mA, mB + 2, reinterpret_cast<const CUtensorMap*>(g.tc_maps), nsm, st);  // B box 128 rows
