@@ -1095,6 +1095,10 @@ static void im2col_tile_t(const QuantArgs& a, const ConvGeom& g, const im2t::Til
   ++launch_counter();
 }
 
+static bool im2col_l16() {  // A/B: LRQMM_IM2COL_L16=0 keeps 32 lanes x 5 quads for 81..144 quads
+  static const bool on = !(getenv("LRQMM_IM2COL_L16") && atoi(getenv("LRQMM_IM2COL_L16")) == 0);
+  return on;
+}
 // lanes per row / quads per lane: the fewest idle quad slots, short rows shared by sub-warps
 template <bool kVec>
 static void im2col_tile_v(const QuantArgs& a, const ConvGeom& g, const im2t::Tile& tl, cudaStream_t st) {
@@ -1103,6 +1107,9 @@ static void im2col_tile_v(const QuantArgs& a, const ConvGeom& g, const im2t::Til
   else if (nq <= 16) im2col_tile_t<kVec, 2, 8>(a, g, tl, st);
   else if (nq <= 40) im2col_tile_t<kVec, 5, 8>(a, g, tl, st);
   else if (nq <= 80) im2col_tile_t<kVec, 5, 16>(a, g, tl, st);
+  else if (nq <= 144 && im2col_l16()) im2col_tile_t<kVec, 9, 16>(a, g, tl, st);  // 3x3 / C = 64: 16 x 9 = 144 quads
+  else if (nq <= 160) im2col_tile_t<kVec, 5, 32>(a, g, tl, st);
+  else if (nq <= 288 && im2col_l16()) im2col_tile_t<kVec, 9, 32>(a, g, tl, st);  // 3x3 / C = 128: 32 x 9 = 288
   else im2col_tile_t<kVec, 5, 32>(a, g, tl, st);
 }
 
