@@ -1113,21 +1113,32 @@ static void im2col_tile_v(const QuantArgs& a, const ConvGeom& g, const im2t::Til
   else im2col_tile_t<kVec, 5, 32>(a, g, tl, st);
 }
 
-template <bool kVec>
-static void im2col_t(const QuantArgs& a, const ConvGeom& g, cudaStream_t st) {
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+template <bool kVec, int VPT>
+static void im2col_launch(const QuantArgs& a, const ConvGeom& g, cudaStream_t st) {
+  const int nsm = sm_count();
   int64_t blocks = (a.rows + 7) / 8;
   if (blocks > 16LL * nsm) blocks = 16LL * nsm;
   const int gb = (int)(blocks < 1 ? 1 : blocks);
 #define IM_ARGS a.X, g, a.K, a.Kp, a.qmax, a.codes, a.lam, a.inv_lam, a.err_flag, a.U, a.ldu, a.uplane, (int)a.rows
-  constexpr int VPT = kVec ? 8 : 8;
   if (a.mode == kRoundFloor) launch_pdl(k1_quantize_im2col<kRoundFloor, kVec, VPT>, gb, 256, 0, st, IM_ARGS);
   else if (a.mode == kRoundTrunc) launch_pdl(k1_quantize_im2col<kRoundTrunc, kVec, VPT>, gb, 256, 0, st, IM_ARGS);
   else launch_pdl(k1_quantize_im2col<kRoundNearest, kVec, VPT>, gb, 256, 0, st, IM_ARGS);
 #undef IM_ARGS
   ++launch_counter();
+}
+// groups per lane and batch: the row in one register batch when it fits in 9, else the batch size
+// (8 or 9) that leaves the fewest idle slots (K = 1152 / 2304 / 4608 = 9 / 18 / 36 float4 per lane)
+template <bool kVec>
+static void im2col_t(const QuantArgs& a, const ConvGeom& g, cudaStream_t st) {
+  const int per = 32 * (kVec ? 4 : 1);
+  const int need = (a.Kp + per - 1) / per;
+  if (need <= 2) return im2col_launch<kVec, 2>(a, g, st);
+  if (need <= 4) return im2col_launch<kVec, 4>(a, g, st);
+  if (need <= 8) return im2col_launch<kVec, 8>(a, g, st);
+  if (need <= 9) return im2col_launch<kVec, 9>(a, g, st);
+  const int slots8 = (need + 7) / 8 * 8, slots9 = (need + 8) / 9 * 9;
+  if (slots9 < slots8) return im2col_launch<kVec, 9>(a, g, st);
+  im2col_launch<kVec, 8>(a, g, st);
 }
 
 void launch_quantize_im2col(const QuantArgs& a, const ConvGeom& g, cudaStream_t st) {
