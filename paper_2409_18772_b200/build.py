@@ -21,7 +21,6 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "liblrqmm.so")
 SOURCES = ["quantize.cu", "skinny.cu", "skinny_tc.cu", "smallsolve2.cu", "gemm_i8.cu", "comm.cu", "lrqmm_api.cu"]
-HEADERS = ["common.cuh", "kernels.h", "comm.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -52,7 +51,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     extra = os.environ.get("LRQMM_EXTRA_NVCC", "").split()
     flags = extra + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
              "--expt-relaxed-constexpr"] + ARCH + inc
-    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", f) for f in ("lrqmm.h", "lrqmm_debug.h")]
+    # every header of csrc/ is a dependency of every object (solvers.cuh was missing from a fixed list)
+    hdrs = sorted(os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".cuh", ".h"))) + [os.path.join(ROOT, "include", f) for f in ("lrqmm.h", "lrqmm_debug.h")]
     objs = []
     jobs = []
     for src in SOURCES:

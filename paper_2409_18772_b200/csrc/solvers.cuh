@@ -224,7 +224,9 @@ __device__ void group_eig_trunc(const double* G, float* T, int r, double* dyn, d
     return (o2 <= 1e-16 * d2) || (o2 == 0.0);
   };
   bool stop = converged(off, dg);
-  // fixed per-thread work: its 2x2 blocks, its V entries (lane k < half computes pair k's rotation)
+  // fixed per-thread work: its 2x2 blocks, its V entries, the pair whose rotation it evaluates.  A
+  // thread without a block / V entry runs the same instructions on the padding column n of row 0
+  // (never read), so a step is one basic block the scheduler can interleave.
   int bk1[kBlk], bk2[kBlk], brd[kBlk][4], bwr[kBlk][4];
   bool bok[kBlk], bdiag[kBlk];
 #pragma unroll
@@ -238,7 +240,11 @@ __device__ void group_eig_trunc(const double* G, float* T, int r, double* dyn, d
     const int P1 = jac_P(k1), Q1 = jac_Q(k1, na), P2 = jac_P(k2), Q2 = jac_Q(k2, na);
     brd[u][0] = P1 * ld + P2; brd[u][1] = P1 * ld + Q2; brd[u][2] = Q1 * ld + P2; brd[u][3] = Q1 * ld + Q2;
     const int p1 = jac_sigma(P1, na), q1 = jac_sigma(Q1, na), p2 = jac_sigma(P2, na), q2 = jac_sigma(Q2, na);
-    bwr[u][0] = p1 * ld + p2; bwr[u][1] = p1 * ld + q2; bwr[u][2] = q1 * ld + p2; bwr[u][3] = q1 * ld + q2;
+    if (bok[u]) {
+      bwr[u][0] = p1 * ld + p2; bwr[u][1] = p1 * ld + q2; bwr[u][2] = q1 * ld + p2; bwr[u][3] = q1 * ld + q2;
+    } else {
+      bwr[u][0] = bwr[u][1] = bwr[u][2] = bwr[u][3] = n;
+    }
   }
   int vk[kV], vrow[kV], vP[kV], vQ[kV];
   bool vok[kV];
@@ -251,101 +257,123 @@ __device__ void group_eig_trunc(const double* G, float* T, int r, double* dyn, d
     vP[u] = jac_P(vk[u]);
     vQ[u] = jac_Q(vk[u], na);
   }
-  // rotation (c, s) of pair k at the current step (positions P_k, Q_k of Ac); bitwise identical
-  // wherever it is evaluated.  The angle comes from fp64 approximations (MUFU.RCP64H / RSQ64H, no
-  // fp32 round trips); any rotation is an exact similarity once c, s are orthonormal to fp64
-  // rounding (the Newton steps); only convergence depends on the angle's accuracy.
-  auto rotation = [&](const double* Ac, int k, double& c, double& s) {
-    const int P = jac_P(k), Q = jac_Q(k, na);
-    const double app = Ac[P * ld + P], aqq = Ac[Q * ld + Q], apq = Ac[P * ld + Q];
-    c = 1.0;
-    s = 0.0;
-    if (LRQMM_EIG_SKIP & 2) {
-      c = 0.8;
-      s = 0.6;
-    } else if (apq != 0.0) {
-      const double theta = (aqq - app) * jac_rcp(2.0 * apq);
-      const double at = fabs(theta);
-      double t;
-      if (at < 1e100) {
-        const double x = fma(theta, theta, 1.0);
-        t = copysign(jac_rcp(fma(x, jac_rsqrt(x), at)), theta);  // 1 / (|theta| + sqrt(1 + theta^2))
-      } else {
-        t = 0.5 * jac_rcp(theta);
-      }
-      const double x = fma(t, t, 1.0);
-      double y = jac_rsqrt(x);
-      y = y * fma(-0.5 * x, y * y, 1.5);
+  const int kr = lane < half ? lane : 0;  // lane k < half evaluates pair k's rotation (the rest: pair 0)
+  const int rpp = jac_P(kr) * (ld + 1), rqq = jac_Q(kr, na) * (ld + 1), rpq = jac_P(kr) * ld + jac_Q(kr, na);
+  // rotation (c, s) of a pair from its (app, aqq, apq); bitwise identical wherever it is evaluated.
+  // t = tan(phi) is the smaller root of t^2 + 2 theta t - 1 = 0, theta = d / e, d = aqq - app,
+  // e = 2 apq, written t = e / (d + sign(d) sqrt(d^2 + e^2)) so that it takes one rsqrt and one
+  // reciprocal (MUFU.RSQ64H / RCP64H approximations: the angle's accuracy only affects convergence);
+  // c = 1 / sqrt(1 + t^2) then gets two Newton steps so that c^2 + s^2 = 1 to fp64 rounding and every
+  // rotation is an exact similarity.  Entries are normalised (|a| <= 1); |apq| <= 1e-150 is no
+  // rotation (and keeps d^2 + e^2 a normal number).
+  auto rotation = [&](double app, double aqq, double apq, double& c, double& s) {
+    const double d = aqq - app, e = 2.0 * apq;
+    const double x = fma(d, d, e * e);
+    const double r = x * jac_rsqrt(x);
+    const double t0 = e * jac_rcp(d + copysign(r, d));
+    double t = fabs(apq) > 1e-150 ? t0 : 0.0;
+    if (LRQMM_EIG_SKIP & 2) t = 0.75;
+    const double x1 = fma(t, t, 1.0), hx = -0.5 * x1;
+    double y = jac_rsqrt(x1);
+    y = y * fma(hx, y * y, 1.5);
 #if LRQMM_JAC_NEWTON > 1
-      y = y * fma(-0.5 * x, y * y, 1.5);
+    y = y * fma(hx, y * y, 1.5);
 #endif
-      c = y;
-      s = t * y;
-    }
+    c = y;
+    s = t * y;
   };
   // V' = V J of a step, applied one step late (off the A chain): rotations (cv, sv) of lane k < half
-  // = pair k of step `vs`
+  // = pair k of the step whose column labels are (op, oq).  Labels advance by one position per step
+  // (orig(s + 1, d) = orig(s, d) + 1 mod m over 1..m; position 0 keeps label 0).  Before the first
+  // step the update is the identity on the labels of step m - 1 (a valid pairing): no branch.
   double cv = 1.0, sv = 0.0;
-  auto v_update = [&](int vs) {
+  int op[kV], oq[kV];
 #pragma unroll
-    for (int u = 0; u < kV && !(LRQMM_EIG_SKIP & 1); ++u) {
-      const double ck = __shfl_sync(0xffffffffu, cv, vk[u]), sk = __shfl_sync(0xffffffffu, sv, vk[u]);
-      if (vok[u]) {
-        const int vp = vrow[u] + jac_orig(vs, vP[u], m), vq = vrow[u] + jac_orig(vs, vQ[u], m);
-        const double x0 = V[vp], x1 = V[vq];
-        V[vp] = ck * x0 - sk * x1;
-        V[vq] = sk * x0 + ck * x1;
+  for (int u = 0; u < kV; ++u) {
+    op[u] = jac_orig(m - 1, vP[u], m);
+    oq[u] = jac_orig(m - 1, vQ[u], m);
+  }
+  // the update is split: its loads and shuffles are issued at the top of a step next to the A loads,
+  // its arithmetic and stores after the step's rotation (the entries are this thread's alone)
+  double ck[kV], sk[kV], x0[kV], x1[kV];
+  int vp[kV], vq[kV];
+  auto v_load = [&] {
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {  // the entries of different u are distinct
+      ck[u] = __shfl_sync(0xffffffffu, cv, vk[u]);
+      sk[u] = __shfl_sync(0xffffffffu, sv, vk[u]);
+      vp[u] = vok[u] ? vrow[u] + op[u] : n;
+      vq[u] = vok[u] ? vrow[u] + oq[u] : n;
+      x0[u] = V[vp[u]];
+      x1[u] = V[vq[u]];
+    }
+  };
+  auto v_store = [&] {
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      if (!(LRQMM_EIG_SKIP & 1)) {
+        V[vp[u]] = ck[u] * x0[u] - sk[u] * x1[u];
+        V[vq[u]] = sk[u] * x0[u] + ck[u] * x1[u];
       }
+      op[u] = op[u] == 0 ? 0 : (op[u] == m ? 1 : op[u] + 1);
+      oq[u] = oq[u] == 0 ? 0 : (oq[u] == m ? 1 : oq[u] + 1);
     }
   };
   int total = 0;  // steps done
-  int pstep = -1;  // step (within its sweep) of the V update still pending
-  for (int sweep = 0; LRQMM_EIG_SWEEPS ? sweep < LRQMM_EIG_SWEEPS : (sweep < 30 && !stop); ++sweep) {
-    for (int step = 0; step < m; ++step, ++total) {
-      const double* Ac = Abuf + (total & 1) * n * ld;
-      double* An = Abuf + ((total + 1) & 1) * n * ld;
-      const bool last = step + 1 == m;
-      // every load of the step first: the 2x2 blocks
+  // the step loop unrolled by two (the ping-pong parity is static in each half: fixed addresses)
+  int sstep = 0, sweep = 0;
+  bool run = LRQMM_EIG_SWEEPS ? true : !stop;
+  while (run) {
+#pragma unroll
+    for (int par = 0; par < 2; ++par) {
+      if (!run) break;
+      const double* Ac = Abuf + par * n * ld;
+      double* An = Abuf + (1 - par) * n * ld;
+      const bool last = sstep + 1 == m;
+      // every load of the step first: the rotation operands and the 2x2 blocks
+      const double app = Ac[rpp], aqq = Ac[rqq], apq = Ac[rpq];
       double bv[kBlk][4];
 #pragma unroll
-      for (int u = 0; u < kBlk; ++u)
-        if (bok[u]) {
-          bv[u][0] = Ac[brd[u][0]]; bv[u][1] = Ac[brd[u][1]]; bv[u][2] = Ac[brd[u][2]]; bv[u][3] = Ac[brd[u][3]];
-        }
-      // the previous step's V update (its rotations are in cv, sv: independent of this step's chain)
-      if (pstep >= 0) v_update(pstep);
-      // this step's rotations: lane k < half -> pair k (every warp redundantly), handed out by shuffle
-      double c = 1.0, s = 0.0;
-      if (lane < half) rotation(Ac, lane, c, s);
+      for (int u = 0; u < kBlk; ++u) {
+        bv[u][0] = Ac[brd[u][0]]; bv[u][1] = Ac[brd[u][1]]; bv[u][2] = Ac[brd[u][2]]; bv[u][3] = Ac[brd[u][3]];
+      }
+      v_load();  // the previous step's V update (rotations in cv, sv: independent of this step's chain)
+      double c, s;
+      rotation(app, aqq, apq, c, s);
+      v_store();
       cv = c;
       sv = s;
-      pstep = step;
       off = 0.0;
       dg = 0.0;
 #pragma unroll
       for (int u = 0; u < kBlk && !(LRQMM_EIG_SKIP & 4); ++u) {
         const double c1 = __shfl_sync(0xffffffffu, c, bk1[u]), s1 = __shfl_sync(0xffffffffu, s, bk1[u]);
         const double c2 = __shfl_sync(0xffffffffu, c, bk2[u]), s2 = __shfl_sync(0xffffffffu, s, bk2[u]);
-        if (bok[u]) {
-          const double a = bv[u][0], b = bv[u][1], cc = bv[u][2], d = bv[u][3];
-          const double ra = c1 * a - s1 * cc, rb = c1 * b - s1 * d;
-          const double rc = s1 * a + c1 * cc, rd = s1 * b + c1 * d;
-          const double v0 = c2 * ra - s2 * rb, v1 = s2 * ra + c2 * rb, v2 = c2 * rc - s2 * rd, v3 = s2 * rc + c2 * rd;
-          An[bwr[u][0]] = v0;
-          An[bwr[u][1]] = v1;
-          An[bwr[u][2]] = v2;
-          An[bwr[u][3]] = v3;
-          if (last) {
-            if (bdiag[u]) { dg += v0 * v0 + v3 * v3; off += v1 * v1 + v2 * v2; }
-            else off += (v0 * v0 + v1 * v1) + (v2 * v2 + v3 * v3);
-          }
+        const double a = bv[u][0], b = bv[u][1], cc = bv[u][2], d = bv[u][3];
+        const double ra = c1 * a - s1 * cc, rb = c1 * b - s1 * d;
+        const double rc = s1 * a + c1 * cc, rd = s1 * b + c1 * d;
+        const double v0 = c2 * ra - s2 * rb, v1 = s2 * ra + c2 * rb, v2 = c2 * rc - s2 * rd, v3 = s2 * rc + c2 * rd;
+        An[bwr[u][0]] = v0;
+        An[bwr[u][1]] = v1;
+        An[bwr[u][2]] = v2;
+        An[bwr[u][3]] = v3;
+        if (last && bok[u]) {
+          if (bdiag[u]) { dg += v0 * v0 + v3 * v3; off += v1 * v1 + v2 * v2; }
+          else off += (v0 * v0 + v1 * v1) + (v2 * v2 + v3 * v3);
         }
       }
       if (last) stop = converged(off, dg);  // its barrier ends the step
       else sync();
+      ++total;
+      if (++sstep == m) {
+        sstep = 0;
+        ++sweep;
+        run = LRQMM_EIG_SWEEPS ? sweep < LRQMM_EIG_SWEEPS : (sweep < 30 && !stop);
+      }
     }
   }
-  if (pstep >= 0) v_update(pstep);
+  v_load();
+  v_store();
   sync();
 #ifdef LRQMM_EIG_STATS
   if (tid == 0) eig_stats_steps = total;  // micro-benchmark only (tools/eig_bench.cu)
@@ -371,10 +399,13 @@ __device__ void group_eig_trunc(const double* G, float* T, int r, double* dyn, d
 }
 __host__ __device__ constexpr int eig_aux_bytes(int NT) { return (2 * (NT / 32) + 2) * 8 + 64 * 4; }
 
+// The group size per n (tools/eig_bench.cu: n = 24 30.0 us at 192 threads vs 33.8 at 256, n = 32
+// 61.2 us at 256); the CTA's other threads leave, the group synchronises on named barrier 1.
 template <int n>
 __device__ void dev_eig_trunc(const double* G, float* T, int r, double* dyn) {
-  __shared__ double aux[(eig_aux_bytes(256) + 7) / 8];
-  group_eig_trunc<n, 256>(G, T, r, dyn, aux, threadIdx.x, 0);
+  constexpr int NT = n == 24 ? 192 : 256;
+  __shared__ double aux[(eig_aux_bytes(NT) + 7) / 8];
+  if (threadIdx.x < NT) group_eig_trunc<n, NT>(G, T, r, dyn, aux, threadIdx.x, 1);
 }
 
 

@@ -74,7 +74,7 @@ void run(const double* dG, float* dT, unsigned long long* dt) {
   }
   std::vector<float> T(n * n);
   cudaMemcpy(T.data(), dT, sizeof(float) * n * n, cudaMemcpyDeviceToHost);
-  if (NT == 256) {
+  if (NT == 128) {
     char fn[64];
     snprintf(fn, sizeof fn, "gpurun_out/eig_T_256_n%d.bin", n);
     FILE* o = fopen(fn, "wb");
@@ -98,11 +98,12 @@ int main(int argc, char** argv) {
   cudaMalloc(&dG, 8 * G.size()); cudaMalloc(&dT, 4 * G.size()); cudaMalloc(&dt, 8);
   cudaMemcpy(dG, G.data(), 8 * G.size(), cudaMemcpyHostToDevice);
   run_chol<24>(dG, dt);
-  run<512>(dG, dT, dt);
   run<256>(dG, dT, dt);
+  run<192>(dG, dT, dt);
+  run<160>(dG, dT, dt);
   run<128>(dG, dT, dt);
+  run<96>(dG, dT, dt);
   run<64>(dG, dT, dt);
-  run<32>(dG, dT, dt);
   {
     unsigned long long best = ~0ull;
     for (int i = 0; i < 20; ++i) {
@@ -129,7 +130,9 @@ int main(int argc, char** argv) {
       cudaMemcpy(dG32, G32.data(), 8 * G32.size(), cudaMemcpyHostToDevice);
       run_chol<32>(dG32, dt);
       run<256, 32>(dG32, dT32, dt);
-      run<512, 32>(dG32, dT32, dt);
+      run<192, 32>(dG32, dT32, dt);
+      run<160, 32>(dG32, dT32, dt);
+      run<128, 32>(dG32, dT32, dt);
     }
     if (f32) fclose(f32);
   }

@@ -1,5 +1,5 @@
 // Latency probes (cycles per dependent op, one warp): DFMA, DMUL, SHFL, F2F, MUFU, fp64 rsqrt,
-// __syncthreads with 8 warps, LDS->STS->BAR round.  nvcc -gencode arch=compute_100a,code=sm_100a -O3
+// rcp/rsqrt.approx.f64 (MUFU.RCP64H/RSQ64H), __syncthreads with 8 warps, LDS->STS->BAR round.  nvcc -gencode arch=compute_100a,code=sm_100a -O3
 #include <cstdio>
 #include <cuda_runtime.h>
 __global__ void k(double* out, long long* cyc, double x0, int n) {
@@ -27,6 +27,8 @@ __global__ void k(double* out, long long* cyc, double x0, int n) {
   PROBE(9, { double v = sm[(threadIdx.x + i) & 255]; __syncthreads(); sm[threadIdx.x] = v + 1.0; __syncthreads(); })
   PROBE(10, x = sqrt(x + 1.0))
   PROBE(11, f = __fdividef(1.f, f + 1.f))
+  PROBE(12, asm volatile("rcp.approx.ftz.f64 %0, %0;" : "+d"(x)))
+  PROBE(13, asm volatile("rsqrt.approx.ftz.f64 %0, %0;" : "+d"(x)))
   out[threadIdx.x] = x + f + iv;
 }
 int main() {
@@ -35,7 +37,7 @@ int main() {
   k<<<1, 256>>>(out, cyc, 0.5, n); cudaDeviceSynchronize();
   k<<<1, 256>>>(out, cyc, 0.5, n); cudaDeviceSynchronize();
   const char* names[] = {"DFMA", "DMUL", "SHFL.32", "SHFL.64", "F2F f->d->f (+DMUL)", "MUFU rsqrtf(+FADD)", "fp64 rsqrt(+DADD)",
-                         "fp64 div(+DADD)", "syncthreads (8 warps)", "LDS+BAR+STS+BAR", "fp64 sqrt(+DADD)", "fdividef(+FADD)"};
-  for (int i = 0; i < 12; ++i) printf("%-24s %7.1f cyc\n", names[i], (double)cyc[i] / n);
+                         "fp64 div(+DADD)", "syncthreads (8 warps)", "LDS+BAR+STS+BAR", "fp64 sqrt(+DADD)", "fdividef(+FADD)", "MUFU.RCP64H", "MUFU.RSQ64H"};
+  for (int i = 0; i < 14; ++i) printf("%-24s %7.1f cyc\n", names[i], (double)cyc[i] / n);
   return 0;
 }
