@@ -18,18 +18,28 @@ LRQMM_DEV void group_bar(int id, int count) { asm volatile("bar.sync %0, %1;" ::
 //   packed-key __reduce_max_sync pair); l_j = S[p, j] / sqrt(d_p) (l_p = sqrt(d_p)), where S[p, j]
 //   is lane j's own s[p] (a select over the unrolled registers, overlapping the rsqrt); l goes to
 //   Lsm row k; S -= l l^T is register-only (l_i broadcast from Lsm); d -= l^2.  Per step the
-//   dependent chain is argmax -> rsqrt -> l -> one broadcast round, no shared-memory matrix traffic.
+//   dependent chain is argmax -> rsqrt (MUFU approximation + two Newton steps) -> l -> one broadcast
+//   round, no shared-memory matrix traffic.
 //   The transform (mathematically T = P L^-T) is formed after the factorisation as Gram-Schmidt in
 //   the G inner product, lane = row of T with the row in registers:
 //     t_k = (e_{p_k} - sum_{m<k} t_m L[p_k, m]) / L[p_k, k],
 //   so Q = Y T has orthonormal columns.  Pivots below 1e-10 x the largest diagonal entry end the
-//   factorisation (reading #12): the remaining columns of T are zero.
+//   factorisation (reading #12): the remaining columns of T are zero (rows >= rank of L, their
+//   pivots and 1 / L[p_k, k] are zeroed, so the transform loop is branch-free).
 //   Shared scratch: sm (>= 2 x 32 doubles: pivot indices, 1 / L[p_k, k]), Lsm (32 x 33 doubles),
 //   Tsm (32 x 33 doubles, output staging).
 // Output T64[j * n + k] = T[j, k].
+#ifdef LRQMM_CHOL_PROF
+__device__ long long chol_prof[8];  // micro-benchmark only (tools/eig_bench.cu): phase clocks
+#define CHOL_MARK(i) \
+  if (lane == 0) chol_prof[i] = clock64();
+#else
+#define CHOL_MARK(i)
+#endif
 template <int n>
 __device__ void warp_chol_orth(const double* G, double* T64, double* sm, double* Lsm, double* Tsm) {
   const int lane = threadIdx.x & 31;
+  CHOL_MARK(0)
   int* piv = reinterpret_cast<int*>(sm);
   double* invs = sm + 32;
   double s[n];
@@ -56,6 +66,7 @@ __device__ void warp_chol_orth(const double* G, double* T64, double* sm, double*
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   const double thr = 1e-10 * dmax;
+  CHOL_MARK(1)
   bool done = lane >= n;
   int k = 0;
   for (; k < n; ++k) {
@@ -70,11 +81,30 @@ __device__ void warp_chol_orth(const double* G, double* T64, double* sm, double*
     const int p = 63 - (int)(mlo & 63u);
     const double dp = __shfl_sync(0xffffffffu, d, p);
     if (!(dmax > 0.0) || dp < thr || dp <= 0.0) break;
-    const double inv = rsqrt(dp);
+    // 1 / sqrt(dp): MUFU approximation + two Newton steps (fp64 accurate)
+    double inv;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(dp));
+    const double hdp = -0.5 * dp;
+    inv = inv * fma(hdp, inv * inv, 1.5);
+    inv = inv * fma(hdp, inv * inv, 1.5);
     const double lkk = dp * inv;
-    double spj = s[0];  // S[p, lane] = s[p]
+    // S[p, lane] = s[p]: a select over the unrolled registers, as a tree on the bits of p for n = 32
+    // (tools/eig_bench.cu: n = 32 11.8 -> 10.9 us; the linear chain is faster at n = 24, 8.9 vs 10.8)
+    double spj;
+    if constexpr (n >= 32) {
+      double v[32];
 #pragma unroll
-    for (int i = 1; i < n; ++i) spj = p == i ? s[i] : spj;
+      for (int i = 0; i < 32; ++i) v[i] = i < n ? s[i] : 0.0;
+#pragma unroll
+      for (int w = 1; w < 32; w *= 2)
+#pragma unroll
+        for (int i = 0; i < 32; i += 2 * w) v[i] = (p & w) ? v[i + w] : v[i];
+      spj = v[0];
+    } else {
+      spj = s[0];
+#pragma unroll
+      for (int i = 1; i < n; ++i) spj = p == i ? s[i] : spj;
+    }
     const double l = done ? 0.0 : (lane == p ? lkk : spj * inv);
     if (lane == p) done = true;
     Lsm[k * 33 + lane] = l;
@@ -84,35 +114,41 @@ __device__ void warp_chol_orth(const double* G, double* T64, double* sm, double*
     }
     if (!done) d = fma(-l, l, d);
     __syncwarp();
-    // S -= l l^T on the remaining columns (registers; l_i broadcast)
-    if (!done) {
+    // S -= l l^T (registers; l_i broadcast; a finished lane's column is never read again)
 #pragma unroll
-      for (int i = 0; i < n; ++i) s[i] = fma(-Lsm[k * 33 + i], l, s[i]);
-    }
+    for (int i = 0; i < n; ++i) s[i] = fma(-Lsm[k * 33 + i], l, s[i]);
   }
   const int rk = k;
+  // rows rk.. of L and the pivots beyond the rank: zero, so that the transform below is branch-free
+  // (t[kk] = 0 for kk >= rk)
+  for (int kk = rk; kk < n; ++kk) {
+    Lsm[kk * 33 + lane] = 0.0;
+    if (lane == 0) {
+      piv[kk] = 0;
+      invs[kk] = 0.0;
+    }
+  }
   __syncwarp();
+  CHOL_MARK(2)
   // T row `lane` (registers, reusing s): t[k] = (e_p - sum_{m<k} t[m] L[p, m]) * inv_k, partial sums
   // over m mod 4 in order, as the factorisation-time form
   double* t = s;
 #pragma unroll
   for (int kk = 0; kk < n; ++kk) {
-    if (kk < rk) {
-      const int p = piv[kk];
-      double a[4] = {lane == p ? 1.0 : 0.0, 0.0, 0.0, 0.0};
+    const int p = piv[kk];
+    double a[4] = {lane == p ? 1.0 : 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int m = 0; m < kk; ++m) a[m & 3] = fma(-t[m], Lsm[m * 33 + p], a[m & 3]);
-      t[kk] = ((a[0] + a[1]) + (a[2] + a[3])) * invs[kk];
-    } else {
-      t[kk] = 0.0;
-    }
+    for (int m = 0; m < kk; ++m) a[m & 3] = fma(-t[m], Lsm[m * 33 + p], a[m & 3]);
+    t[kk] = ((a[0] + a[1]) + (a[2] + a[3])) * invs[kk];
   }
+  CHOL_MARK(3)
   // coalesced output through Tsm (column c of T at Tsm[c * 33 + row])
 #pragma unroll
   for (int c = 0; c < n; ++c) Tsm[c * 33 + lane] = t[c];
   __syncwarp();
   for (int e = lane; e < n * n; e += 32) T64[e] = Tsm[(e % n) * 33 + e / n];
   __syncwarp();
+  CHOL_MARK(4)
 }
 
 // --------------------------------------------- parallel Jacobi (truncation)

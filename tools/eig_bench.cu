@@ -57,6 +57,12 @@ void run_chol(const double* dG, unsigned long long* dt) {
   }
   std::vector<double> T(n * n);
   cudaMemcpy(T.data(), dT, 8 * n * n, cudaMemcpyDeviceToHost);
+#ifdef LRQMM_CHOL_PROF
+  long long pc[8];
+  cudaMemcpyFromSymbol(pc, chol_prof, sizeof pc);
+  printf("chol n=%d phases (cycles): load %lld  factor %lld  transform %lld  output %lld\n", n, pc[1] - pc[0], pc[2] - pc[1],
+         pc[3] - pc[2], pc[4] - pc[3]);
+#endif
   printf("chol n=%d  best %.1f us   T[0][0..2] = %.6e %.6e %.6e  (%s)\n", n, best / 1e3, T[0], T[1], T[2],
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(dT);
