@@ -288,6 +288,30 @@ struct ApplyJobs {
   int first[kMaxApply + 1];
 };
 void launch_apply_jobs(const ApplyJobs& jobs, int W, cudaStream_t st);
+// The factor assembly of one side in one row pass (Algorithm 2):
+//   OUT[i, 0:nout) = IN1 S1 (+ IN2 S3),  OUT[i, nout:2 nout) = IN2 S2   (fp32, ld ldo),
+// and, when hi is set, the bf16 hi / lo split of the row for K8 (hi = RN_bf16(x), lo = RN_bf16(x - hi),
+// 64 columns per row, zero beyond 2 nout: the layout k_split_bf16 writes).  nout % 4 == 0.
+struct AsmJob {
+  const float* IN1;
+  const float* S1;
+  const float* IN2;
+  const float* S2;
+  const float* S3;  // nullable
+  int64_t n;
+  int ldS, nout;
+  float* OUT;
+  int64_t ldo;
+  void* hi;  // bf16 [n][64] or null
+  void* lo;
+  int kin;
+};
+struct AsmJobs {
+  AsmJob j[2];
+  int n;
+  int first[3];
+};
+void launch_assemble(AsmJobs& jobs, int W, cudaStream_t st);
 // OUT[i, col0 + o] = sum_c IN1[i,c] S1[c,o] (+ sum_c IN2[i,c] S2[c,o]), o < nout; IN ld W, S ld ldS, OUT ld ldo
 void launch_apply_small(const float* IN1, const float* S1, const float* IN2, const float* S2, int64_t n, int W,
                         int ldS, int nout, float* OUT, int64_t ldo, int col0, cudaStream_t st);

@@ -766,6 +766,17 @@ static lrqmm_status_t assemble(lrqmm_handle_t h, bool cross = true, bool wait_fo
   // row-side factor: W = R Q1 (q >= 1), or the orthonormal Q0 (q = 0: R_k = Q0 B, B = Z^T)
   float* YA = h->cfg.power_iters == 0 ? h->s[0].Q0 : h->s[0].Y;
   float* YB = h->cfg.power_iters == 0 ? h->s[1].Q0 : h->s[1].Y;
+  // one row pass per side writing fp32 L and the bf16 hi / lo operands of K8 (single rank; r % 4 == 0)
+  if (h->tc_ready && W <= 32 && r % 4 == 0 && !h->bsh && h->cfg.world_size == 1 && rows[0] > 0 && rows[1] > 0) {
+    AsmJobs jb{};
+    jb.n = 2;
+    jb.j[0] = AsmJob{YA, h->s[0].VW, h->s[0].Gp, h->s[1].VW, nullptr, rows[0], W, r, h->LA, h->R2, h->LAh, h->LAl,
+                     (int)h->kk};                                                   // [U_A S_A | A~ V_B]
+    jb.j[1] = AsmJob{h->s[1].Gp, h->s[0].VW, YB, h->s[1].VW, h->VWbM, rows[1], W, r, h->LB, h->R2, h->LBh, h->LBl,
+                     (int)h->kk};                                                   // [B~^T V_A + U_B S_B M | U_B S_B]
+    launch_assemble(jb, W, h->st);
+    return check_launch(h);
+  }
   ApplyJobs aj{};
   aj.n = 4;
   aj.j[0] = ApplyJob{YA, h->s[0].VW, nullptr, nullptr, rows[0], W, r, h->LA, h->R2, 0, (int)h->kk};        // U_A S_A

@@ -2,6 +2,7 @@
 // factor assembly of Algorithm 2).
 #include "common.cuh"
 #include "kernels.h"
+#include <cuda_bf16.h>
 
 namespace lrqmm {
 
@@ -219,6 +220,239 @@ void launch_apply_small(const float* IN1, const float* S1, const float* IN2, con
   launch_apply_jobs(j, W, st);
 }
 
+// ------------------------------------------------------------ factor assembly
+// One side of the assembly in one pass over its rows (see AsmJob): both inputs staged per 128-row
+// tile (cp.async double buffer), the row's two halves in registers, the tile's output rows staged in
+// shared memory and written as fp32 and as the bf16 hi / lo operands of K8 with coalesced 16-byte
+// stores.  This replaces two single-product jobs (each writing half of every row) plus the
+// k_split_bf16 pass that re-read the fp32 factor.  Same products, same summation order as
+// k_apply_small; same bf16 split as k_split_bf16.
+LRQMM_DEV void tf32_split(float x, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(x - __uint_as_float(hi)));
+}
+LRQMM_DEV void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, {%0, %1, %2, %3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// C[16 x 8 NT] (+)= A[16 x W] S[W x 8 NT] for the two 16-row m-tiles of a warp, 3xTF32 (hi.hi + hi.lo
+// + lo.hi, fp32 accumulation: fp32-level accuracy, the products' lo.lo term below fp32 rounding).
+// A rows from the staged tile (ld L), S from shared memory (ld NO).  Fragments of
+// mma.m16n8k8.tf32: lane = 4 g + t; A (g, t), (g + 8, t), (g, t + 4), (g + 8, t + 4); B (t, g),
+// (t + 4, g); C (g, 2t), (g, 2t + 1), (g + 8, 2t), (g + 8, 2t + 1).
+template <int W, int NO>
+LRQMM_DEV void asm_mma(float (&c)[2][NO / 8][4], const float* sin, int rbase, const float* S, int lane) {
+  constexpr int L = ap_ld(W);
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int kt = 0; kt < W / 8; ++kt) {
+    uint32_t ah[2][4], al[2][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const float* r0 = sin + (rbase + 16 * mt + g) * L + 8 * kt + t;
+      tf32_split(r0[0], ah[mt][0], al[mt][0]);
+      tf32_split(r0[8 * L], ah[mt][1], al[mt][1]);
+      tf32_split(r0[4], ah[mt][2], al[mt][2]);
+      tf32_split(r0[8 * L + 4], ah[mt][3], al[mt][3]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < NO / 8; ++nt) {
+      uint32_t bh0, bl0, bh1, bl1;
+      tf32_split(S[(8 * kt + t) * NO + 8 * nt + g], bh0, bl0);
+      tf32_split(S[(8 * kt + t + 4) * NO + 8 * nt + g], bh1, bl1);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        mma_tf32(c[mt][nt], al[mt], bh0, bh1);
+        mma_tf32(c[mt][nt], ah[mt], bl0, bl1);
+        mma_tf32(c[mt][nt], ah[mt], bh0, bh1);
+      }
+    }
+  }
+}
+
+// kTc (W <= 32, NO % 8 == 0): the products on the tensor cores (3xTF32 mma.sync, warp w owns rows
+// 32 w .. 32 w + 31 of the tile); else fp32 FFMA, one row per thread
+template <int W, int NO, bool kTc>
+__global__ void __launch_bounds__(kApRows) k_assemble(const __grid_constant__ AsmJobs jobs) {
+  ::lrqmm::pdl_enter();
+  constexpr int L = ap_ld(W);
+  extern __shared__ __align__(16) float asm_sm[];
+  const int q = (jobs.n > 1 && (int)blockIdx.x >= jobs.first[1]) ? 1 : 0;
+  const AsmJob& J = jobs.j[q];
+  const int b0 = jobs.first[q], nb = jobs.first[q + 1] - b0;
+  float* s1 = asm_sm;
+  float* s2 = s1 + W * NO;
+  float* s3 = s2 + W * NO;
+  float* sin_base = s3 + W * NO;  // 2 buffers x (IN1, IN2) x kApRows x L
+  constexpr int kSlot = 2 * kApRows * L;
+  float* sout = sin_base + 2 * kSlot;  // kApRows x (2 nout + 4) output rows
+  const int nout = J.nout;
+  const int kin = J.kin > 0 && J.kin < W ? J.kin : W;
+  const bool has3 = J.S3 != nullptr;
+  for (int e = threadIdx.x; e < W * NO; e += blockDim.x) {
+    const int c = e / NO, o = e % NO;
+    s1[e] = o < nout ? J.S1[c * J.ldS + o] : 0.f;
+    s2[e] = o < nout ? J.S2[c * J.ldS + o] : 0.f;
+    s3[e] = (has3 && o < nout) ? J.S3[c * J.ldS + o] : 0.f;
+  }
+  const int64_t n = J.n;
+  const int64_t step = (int64_t)nb * kApRows;
+  auto stage = [&](int64_t i0, int slot) {
+    if (i0 < n) {
+      const int nr = (int)(n - i0 < kApRows ? n - i0 : kApRows);
+      stage_rows_async<W>(J.IN1, i0, nr, sin_base + slot * kSlot);
+      stage_rows_async<W>(J.IN2, i0, nr, sin_base + slot * kSlot + kApRows * L);
+    }
+    cp_async_commit();
+  };
+  const int64_t first = (int64_t)(blockIdx.x - b0) * kApRows;
+  stage(first, 0);
+  stage(first + step, 1);
+  int it = 0;
+  for (int64_t i0 = first; i0 < n; i0 += step, ++it) {
+    const int nr = (int)(n - i0 < kApRows ? n - i0 : kApRows);
+    const float* sin1 = sin_base + (it & 1) * kSlot;
+    const float* sin2 = sin1 + kApRows * L;
+    cp_async_wait<1>();
+    __syncthreads();
+    // the tile's rows go through shared memory (row stride 2 nout + 4 floats: an odd number of
+    // 16-byte units), then out with coalesced copies: the tile is one contiguous block of L (ld =
+    // 2 nout) and of each bf16 operand (ld 64)
+    const int ow = 2 * nout, ostr = ow + 4;
+    if constexpr (kTc) {
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      float c1[2][NO / 8][4] = {}, c2[2][NO / 8][4] = {};
+      asm_mma<W, NO>(c1, sin1, 32 * warp, s1, lane);
+      if (has3) asm_mma<W, NO>(c1, sin2, 32 * warp, s3, lane);
+      asm_mma<W, NO>(c2, sin2, 32 * warp, s2, lane);
+      __syncthreads();  // every row of this buffer has been read: stage the tile after next into it
+      stage(i0 + 2 * step, it & 1);
+      const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NO / 8; ++nt) {
+          const int col = 8 * nt + 2 * t;
+          if (col < nout) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              float* orow = sout + (32 * warp + 16 * mt + g + 8 * h) * ostr;
+              *reinterpret_cast<float2*>(orow + col) = make_float2(c1[mt][nt][2 * h], c1[mt][nt][2 * h + 1]);
+              *reinterpret_cast<float2*>(orow + nout + col) = make_float2(c2[mt][nt][2 * h], c2[mt][nt][2 * h + 1]);
+            }
+          }
+        }
+    } else {
+      float acc1[NO], acc2[NO];
+#pragma unroll
+      for (int o = 0; o < NO; ++o) acc1[o] = acc2[o] = 0.f;
+      if (threadIdx.x < nr) {
+#pragma unroll(W <= 32 ? W / 4 : 2)
+        for (int c4 = 0; c4 < W / 4; ++c4) {
+          if (4 * c4 >= kin) break;  // zero-padded sketch columns contribute nothing
+          const float4 v = *reinterpret_cast<const float4*>(sin1 + threadIdx.x * L + 4 * c4);
+          const float xs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int o = 0; o < NO; ++o) acc1[o] = fmaf(xs[j], s1[(4 * c4 + j) * NO + o], acc1[o]);
+        }
+#pragma unroll(W <= 32 ? W / 4 : 2)
+        for (int c4 = 0; c4 < W / 4; ++c4) {
+          if (4 * c4 >= kin) break;
+          const float4 v = *reinterpret_cast<const float4*>(sin2 + threadIdx.x * L + 4 * c4);
+          const float xs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (has3) {
+#pragma unroll
+              for (int o = 0; o < NO; ++o) acc1[o] = fmaf(xs[j], s3[(4 * c4 + j) * NO + o], acc1[o]);
+            }
+#pragma unroll
+            for (int o = 0; o < NO; ++o) acc2[o] = fmaf(xs[j], s2[(4 * c4 + j) * NO + o], acc2[o]);
+          }
+        }
+      }
+      __syncthreads();  // every row of this buffer has been read: stage the tile after next into it
+      stage(i0 + 2 * step, it & 1);
+      if (threadIdx.x < nr) {
+        float* orow = sout + threadIdx.x * ostr;
+#pragma unroll
+        for (int o4 = 0; o4 < NO / 4; ++o4)
+          if (4 * o4 < nout) {
+            *reinterpret_cast<float4*>(orow + 4 * o4) = make_float4(acc1[4 * o4], acc1[4 * o4 + 1], acc1[4 * o4 + 2], acc1[4 * o4 + 3]);
+            *reinterpret_cast<float4*>(orow + nout + 4 * o4) = make_float4(acc2[4 * o4], acc2[4 * o4 + 1], acc2[4 * o4 + 2], acc2[4 * o4 + 3]);
+          }
+      }
+    }
+    __syncthreads();
+    {
+      float4* dst = reinterpret_cast<float4*>(J.OUT + i0 * J.ldo);
+      const int nq = nr * ow / 4, qpr = ow / 4;
+      for (int e = threadIdx.x; e < nq; e += kApRows)
+        dst[e] = *reinterpret_cast<const float4*>(sout + (e / qpr) * ostr + 4 * (e % qpr));
+    }
+    if (J.hi) {
+      uint4* hd = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(J.hi) + i0 * 64);
+      uint4* ld = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(J.lo) + i0 * 64);
+      for (int e = threadIdx.x; e < nr * 8; e += kApRows) {  // 8-column groups, as k_split_bf16
+        const int row = e >> 3, c0 = (e & 7) * 8;
+        float x[8];
+        if (c0 < ow) {  // ow % 8 == 0 when nout % 4 == 0
+          const float4 v0 = *reinterpret_cast<const float4*>(sout + row * ostr + c0);
+          const float4 v1 = *reinterpret_cast<const float4*>(sout + row * ostr + c0 + 4);
+          x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w; x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) x[u] = 0.f;
+        }
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * u], x[2 * u + 1]);
+          const float2 hf = __bfloat1622float2(h2);
+          const __nv_bfloat162 l2 = __floats2bfloat162_rn(x[2 * u] - hf.x, x[2 * u + 1] - hf.y);
+          hw[u] = *reinterpret_cast<const uint32_t*>(&h2);
+          lw[u] = *reinterpret_cast<const uint32_t*>(&l2);
+        }
+        hd[e] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        ld[e] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      }
+    }
+  }
+}
+
+template <int W, int NO>
+static void assemble_t(AsmJobs& jobs, cudaStream_t st) {
+  constexpr bool kTc = W <= 32 && NO % 8 == 0 && W % 8 == 0;
+  constexpr int smem = (4 * kApRows * ap_ld(W) + 3 * W * NO + kApRows * (2 * NO + 4)) * (int)sizeof(float);
+  static std::atomic<unsigned> attr{0};
+  ensure_smem(k_assemble<W, NO, kTc>, smem, attr);
+  int64_t n[kMaxApply] = {};
+  for (int q = 0; q < jobs.n; ++q) n[q] = jobs.j[q].n;
+  int first[kMaxApply + 1];
+  const int grid = assign_blocks(n, jobs.n, first);
+  for (int q = 0; q <= jobs.n; ++q) jobs.first[q] = first[q];
+  launch_pdl(k_assemble<W, NO, kTc>, grid, kApRows, smem, st, jobs);
+}
+template <int W>
+static void assemble_w(AsmJobs& jobs, int no, cudaStream_t st) {
+  if constexpr (W >= 16) {
+    if (no <= W - 8) return assemble_t<W, W - 8>(jobs, st);
+  }
+  assemble_t<W, W>(jobs, st);
+}
+void launch_assemble(AsmJobs& jobs, int W, cudaStream_t st) {
+  int no = 0;
+  for (int q = 0; q < jobs.n; ++q) no = jobs.j[q].nout > no ? jobs.j[q].nout : no;
+  if (jobs.n == 0 || no == 0) return;
+#define AW_CASE(w) case w: assemble_w<w>(jobs, no, st); break;
+  switch (W) { AW_CASE(8) AW_CASE(16) AW_CASE(24) AW_CASE(32) default: break; }  // W <= 32 (the caller's contract)
+#undef AW_CASE
+  ++launch_counter();
+}
+
 // OUT = IN S with S in fp64 and fp64 accumulation (orthonormalisation: keeps Q orthonormal to
 // fp32 rounding instead of cond(IN) * eps32).  Same staging as above; one launch for both sides.
 // Same product on the fp64 tensor cores (W <= 32): Q = Y T with mma.sync.m8n8k4.f64 (DMMA). A warp
@@ -295,20 +529,23 @@ __global__ void __launch_bounds__(kApRows) k_apply64_tc(const __grid_constant__ 
       for (int nt = 0; nt < NT; ++nt) {
         const float v0 = (float)acc[sl][nt][0], v1 = (float)acc[sl][nt][1];
         if (ok) *reinterpret_cast<float2*>(J.OUT + row * W + 8 * nt + 2 * (lane & 3)) = make_float2(v0, v1);
-        if (J.cmax) {  // same fp32 product as the next pass's B image
-          float m0 = ok ? fabsf(v0 * cs) : 0.f, m1 = ok ? fabsf(v1 * cs) : 0.f;
-#pragma unroll
-          for (int o = 4; o < 32; o <<= 1) {
-            m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
-            m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
-          }
-          run[nt][0] = fmaxf(run[nt][0], m0);
-          run[nt][1] = fmaxf(run[nt][1], m1);
+        if (J.cmax) {  // same fp32 product as the next pass's B image; per-lane running maxima
+          run[nt][0] = fmaxf(run[nt][0], ok ? fabsf(v0 * cs) : 0.f);
+          run[nt][1] = fmaxf(run[nt][1], ok ? fabsf(v1 * cs) : 0.f);
         }
       }
     }
   }
   if (J.cmax) {
+    // lanes with the same lane & 3 hold the same columns: one shuffle reduction per block (max is
+    // exact in any order), not one per tile and row slice
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        run[nt][0] = fmaxf(run[nt][0], __shfl_xor_sync(0xffffffffu, run[nt][0], o));
+        run[nt][1] = fmaxf(run[nt][1], __shfl_xor_sync(0xffffffffu, run[nt][1], o));
+      }
     __syncthreads();
     if (lane < 4)
 #pragma unroll

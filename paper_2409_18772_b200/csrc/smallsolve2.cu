@@ -484,7 +484,10 @@ void launch_fused_small(const SmallJobs& jobs, int W, int mode, cudaStream_t st)
   int64_t nb = (nmax + 2 * fr - 1) / (2 * fr);
   for (int i = 0; i < jobs.n; ++i)
     if (jobs.j[i].nsplit != 1) return;  // contract: Y is reduced before the fused kernel
-  if (nb > 444) nb = 444;  // three resident blocks per SM (66.5 KB each)
+  // one wave: two blocks fit per SM (66.5 KB of shared memory and 98 registers x 256 threads each;
+  // ncu), and 444 blocks had run as 1.5 waves (802 816-row panel: half the SMs idle for a third)
+  const int64_t wave = 2LL * sm_count();
+  if (nb > wave) nb = wave;
   if (nb > kGramMaxBlocks) nb = kGramMaxBlocks;
   if (nb < 1) nb = 1;
   switch (W) {
