@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(g6::threads_for(kR2, BN), 1)
   constexpr uint32_t kTmemCols = g6::tmem_cols(NACC * BN);
   constexpr int STAGES = g6::stages_for(kR2, BN);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // offset from the __shared__ array: shared-space accesses, not generic
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * kABytes;
   constexpr int EG = g6::epi_groups(kR2, BN);
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(g8::kThreads, 1)
                const __grid_constant__ CUtensorMap mapLBh, const __grid_constant__ CUtensorMap mapLBl, G8Params p) {
   using namespace g8;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // offset from the __shared__ array: shared-space accesses, not generic
   float* stile0 = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // 8 x 32 x 32 (XOR-swizzled)
   float* sSB0 = stile0 + kStile / 4;  // kEG x BN: 1/lambda_B of the tile
   uint64_t* bars = reinterpret_cast<uint64_t*>(sSB0 + kEG * BN);
@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(g8w::kThreads, 1)
                 const __grid_constant__ CUtensorMap mapLBh, const __grid_constant__ CUtensorMap mapLBl, G8Params p) {
   using namespace g8w;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // offset from the __shared__ array: shared-space accesses, not generic
   float* stile0 = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // 8 x 32 x 32 (XOR-swizzled)
   float* sSB0 = stile0 + kStile / 4;                                      // BN: 1/lambda_B of the tile
   uint64_t* bars = reinterpret_cast<uint64_t*>(sSB0 + BN);
@@ -985,7 +985,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g7::kThreads, 1)
   using namespace g7;
   constexpr int STAGES = stages_for(kR2);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // offset from the __shared__ array: shared-space accesses, not generic
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * kABytes;
   float* sLB = reinterpret_cast<float*>(smem + STAGES * kStageBytes);  // BN x kR2

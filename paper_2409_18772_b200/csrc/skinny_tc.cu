@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(kFuse ? tcp::kThreadsFused : tcp::kThreads, 1)
   constexpr int NACC = C::kAccBufs;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ float cinv_s[2][2][64];  // [side][P1 / P2][column]
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // offset from the __shared__ array: shared-space accesses, not generic
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStage);
   uint64_t* full = bars;          // S: stage landed (TMA tx)
   uint64_t* freeb = bars + S;     // S: MMA done with the stage

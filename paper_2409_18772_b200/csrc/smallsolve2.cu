@@ -316,6 +316,21 @@ __global__ void __launch_bounds__(32) k_warp_chol(EigJobs jobs) {
 //                         (mode 1), or nothing (mode 2: G must first be summed across ranks).
 // rows per shared-memory chunk (fp32, two buffers in the 66.5 KB dynamic allocation)
 __host__ __device__ constexpr int frows(int w) { return w <= 32 ? 256 : 128; }
+// ((0 + p[0]) + p[s]) + p[2 s] + ... in index order (the fixed-order partial sums), loads issued 8 at
+// a time so that a chain of L2 round trips does not serialise the finisher
+LRQMM_DEV double sum_strided(const double* p, int64_t stride, int cnt) {
+  double a = 0.0;
+  for (int b0 = 0; b0 < cnt; b0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = b0 + u < cnt ? __ldcg(p + (int64_t)(b0 + u) * stride) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (b0 + u < cnt) a += v[u];
+  }
+  return a;
+}
+
 template <int W>
 __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
   ::lrqmm::pdl_enter();
@@ -423,8 +438,7 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
   double* Gs = dyn + 3 * 32 * 33;
   if (ngrp == 1) {  // one group: its finisher is the last block (the same sums as the two-level path)
     for (int pr = threadIdx.x; pr < npairs; pr += 256) {
-      double a = 0.0;
-      for (int b = 0; b < gsize; ++b) a += __ldcg(jb.gpart + (int64_t)b * npairs + pr);
+      const double a = sum_strided(jb.gpart + pr, npairs, gsize);
       const double g = 0.0 + a;  // the second level adds the single group sum to 0
       jb.G[pr] = g;
       if (W <= 32) Gs[pr] = g;
@@ -432,8 +446,7 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
     if (threadIdx.x == 0) jb.counter[1] = 0;
   } else {
     for (int pr = threadIdx.x; pr < npairs; pr += 256) {
-      double a = 0.0;
-      for (int b = 16 * grp; b < 16 * grp + gsize; ++b) a += __ldcg(jb.gpart + (int64_t)b * npairs + pr);
+      const double a = sum_strided(jb.gpart + (int64_t)(16 * grp) * npairs + pr, npairs, gsize);
       jb.gpart[(int64_t)(nb + grp) * npairs + pr] = a;
     }
     if (threadIdx.x == 0) jb.counter[1 + grp] = 0;
@@ -444,8 +457,7 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
     if (ticket != ngrp - 1) return;
     __threadfence();
     for (int pr = threadIdx.x; pr < npairs; pr += 256) {
-      double a = 0.0;
-      for (int g = 0; g < ngrp; ++g) a += __ldcg(jb.gpart + (int64_t)(nb + g) * npairs + pr);
+      const double a = sum_strided(jb.gpart + (int64_t)nb * npairs + pr, npairs, ngrp);
       jb.G[pr] = a;
       if (W <= 32) Gs[pr] = a;
     }
