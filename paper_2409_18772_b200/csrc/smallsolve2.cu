@@ -316,6 +316,22 @@ __global__ void __launch_bounds__(32) k_warp_chol(EigJobs jobs) {
 //                         (mode 1), or nothing (mode 2: G must first be summed across ranks).
 // rows per shared-memory chunk (fp32, two buffers in the 66.5 KB dynamic allocation)
 __host__ __device__ constexpr int frows(int w) { return w <= 32 ? 256 : 128; }
+#ifdef LRQMM_FS_TRACE
+// development only (tools/fs_trace.py): globaltimer stamps of the last k_fused_small launch per mode
+__device__ unsigned long long fs_trace[16];
+extern "C" int lrqmm_debug_fs_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, fs_trace, sizeof fs_trace) == cudaSuccess ? 0 : 1;
+}
+#define FS_T(i)                                                         \
+  if (threadIdx.x == 0 && blockIdx.y == 0) {                            \
+    unsigned long long t_;                                              \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));              \
+    fs_trace[8 * (mode & 1) + (i)] = t_;                                \
+  }
+#else
+#define FS_T(i)
+#endif
+
 // ((0 + p[0]) + p[s]) + p[2 s] + ... in index order (the fixed-order partial sums), loads issued 8 at
 // a time so that a chain of L2 round trips does not serialise the finisher
 LRQMM_DEV double sum_strided(const double* p, int64_t stride, int cnt) {
@@ -334,6 +350,7 @@ LRQMM_DEV double sum_strided(const double* p, int64_t stride, int cnt) {
 template <int W>
 __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
   ::lrqmm::pdl_enter();
+  if (blockIdx.x == 0) { FS_T(0) }
   constexpr int kFRows = frows(W);
   extern __shared__ __align__(128) double dyn[];
   const SmallJob jb = jobs.j[blockIdx.y];
@@ -395,6 +412,7 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
     __syncthreads();  // every warp is done with buffer (c & 1): refill it with chunk c + 2
     if (threadIdx.x == 0 && c + 2 < nchunk) issue(c + 2);
   }
+  if (blockIdx.x == 0) { FS_T(1) }
   // fixed-order sum of the 8 warps' blocks (warp 0 stores, warps 1..7 add in turn), then the block
   // partial, both halves (block (a, a): the entry with row <= col goes to both positions)
   double* S = dyn;  // NBLK x 64 (the chunk buffers are free)
@@ -427,12 +445,14 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
   const int nb = (int)gridDim.x;
   const int grp = blockIdx.x / 16, ngrp = (nb + 15) / 16;
   const int gsize = nb - 16 * grp < 16 ? nb - 16 * grp : 16;
+  if (blockIdx.x == 0) { FS_T(2) }
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) ticket = atomicAdd(jb.counter + 1 + grp, 1);
   __syncthreads();
   if (ticket != gsize - 1) return;
   __threadfence();
+  FS_T(3)
   // G also into shared memory behind the solvers' scratch: the solver reads it from there, not back
   // through L2 (W <= 32)
   double* Gs = dyn + 3 * 32 * 33;
@@ -466,6 +486,7 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
   if (jb.cmax && threadIdx.x < 64) jb.cmax[threadIdx.x] = 0u;  // the next apply64's column maxima
   __threadfence_block();
   __syncthreads();
+  FS_T(4)
   if constexpr (W <= 32) {
     static_assert(3 * 32 * 33 * 8 + W * W * 8 <= kDynSmem && eig_smem_bytes(W) <= 3 * 32 * 33 * 8, "G staging");
     if (mode == 0 && threadIdx.x < 32) {
@@ -476,6 +497,7 @@ __global__ void __launch_bounds__(256) k_fused_small(SmallJobs jobs, int mode) {
     if (mode == 0) dev_chol_orth<W>(jb.G, jb.T64, dyn);
     else if (mode == 1) dev_eig_trunc<W>(jb.G, jb.T, jb.r, dyn);
   }
+  FS_T(5)
 }
 
 template <int W>
