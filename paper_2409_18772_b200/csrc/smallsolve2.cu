@@ -320,7 +320,13 @@ __host__ __device__ constexpr int frows(int w) { return w <= 32 ? 256 : 128; }
 // development only (tools/fs_trace.py): globaltimer stamps of the last k_fused_small launch per mode
 __device__ unsigned long long fs_trace[16];
 extern "C" int lrqmm_debug_fs_trace(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, fs_trace, sizeof fs_trace) == cudaSuccess ? 0 : 1;
+  if (cudaMemcpyFromSymbol(out, fs_trace, sizeof fs_trace) != cudaSuccess) return 1;
+#ifdef LRQMM_EIG_STATS
+  int steps = 0;  // Jacobi steps of the last truncation (this translation unit's solver)
+  cudaMemcpyFromSymbol(&steps, eig_stats_steps, sizeof steps);
+  out[15] = (unsigned long long)steps;
+#endif
+  return 0;
 }
 #define FS_T(i)                                                         \
   if (threadIdx.x == 0 && blockIdx.y == 0) {                            \

@@ -168,6 +168,9 @@ __device__ void warp_chol_orth(const double* G, double* T64, double* sm, double*
 #ifndef LRQMM_JAC_NEWTON
 #define LRQMM_JAC_NEWTON 2
 #endif
+#ifndef LRQMM_JAC_TOL
+#define LRQMM_JAC_TOL 1e-16  // off(A)^2 <= tol * diag(A)^2 ends the sweeps (reading #29)
+#endif
 __device__ __forceinline__ double jac_rcp(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -257,7 +260,7 @@ __device__ void group_eig_trunc(const double* G, float* T, int r, double* dyn, d
     double o2 = 0.0, d2 = 0.0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) { o2 += red[w][0]; d2 += red[w][1]; }
-    return (o2 <= 1e-16 * d2) || (o2 == 0.0);
+    return (o2 <= LRQMM_JAC_TOL * d2) || (o2 == 0.0);
   };
   bool stop = converged(off, dg);
   // fixed per-thread work: its 2x2 blocks, its V entries, the pair whose rotation it evaluates.  A

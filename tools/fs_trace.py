@@ -41,3 +41,4 @@ for mode in (0, 1):
     t = [buf[8 * mode + i] for i in range(6)]
     print(f"mode {mode} ({'CholQR' if mode == 0 else 'truncation'}):",
           "  ".join(f"{names[i]} +{(t[i] - t[0]) / 1e3:.1f}us" for i in range(1, 6)))
+print("Jacobi steps of the last truncation (with -DLRQMM_EIG_STATS):", buf[15])
