@@ -236,25 +236,46 @@ LRQMM_DEV void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint
                : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
                : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// W = 32 staging without padding: row r's 16-byte chunk c at chunk c ^ (r & 7) of the 128-byte row, so
+// the MMA fragment reads (8 rows x 4 columns per k-tile) hit 32 distinct banks; 25 % less shared
+// memory than the W + 4 padded rows (k_assemble: three resident blocks per SM instead of two)
+template <int W>
+LRQMM_DEV int swz_at(int row, int col) {
+  return row * W + ((((col >> 2) ^ (row & 7)) << 2) | (col & 3));
+}
+template <int W>
+LRQMM_DEV void stage_rows_swz(const float* __restrict__ src, int64_t i0, int nr, float* sm) {
+  const float4* s4 = reinterpret_cast<const float4*>(src + i0 * W);
+#pragma unroll
+  for (int u = 0; u < W / 4; ++u) {
+    const int e = threadIdx.x + u * kApRows;
+    if (e < nr * (W / 4)) {
+      const uint32_t dst = smem_u32(sm + swz_at<W>(e / (W / 4), 4 * (e % (W / 4))));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(s4 + e) : "memory");
+    }
+  }
+}
+
 // C[16 x 8 NT] (+)= A[16 x W] S[W x 8 NT] for the two 16-row m-tiles of a warp, 3xTF32 (hi.hi + hi.lo
 // + lo.hi, fp32 accumulation: fp32-level accuracy, the products' lo.lo term below fp32 rounding).
 // A rows from the staged tile (ld L), S from shared memory (ld NO).  Fragments of
 // mma.m16n8k8.tf32: lane = 4 g + t; A (g, t), (g + 8, t), (g, t + 4), (g + 8, t + 4); B (t, g),
 // (t + 4, g); C (g, 2t), (g, 2t + 1), (g + 8, 2t), (g + 8, 2t + 1).
-template <int W, int NO>
+template <int W, int NO, bool kSwz>
 LRQMM_DEV void asm_mma(float (&c)[2][NO / 8][4], const float* sin, int rbase, const float* S, int lane) {
   constexpr int L = ap_ld(W);
   const int g = lane >> 2, t = lane & 3;
+  auto at = [&](int row, int col) { return kSwz ? sin[swz_at<W>(row, col)] : sin[row * L + col]; };
 #pragma unroll
   for (int kt = 0; kt < W / 8; ++kt) {
     uint32_t ah[2][4], al[2][4];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
-      const float* r0 = sin + (rbase + 16 * mt + g) * L + 8 * kt + t;
-      tf32_split(r0[0], ah[mt][0], al[mt][0]);
-      tf32_split(r0[8 * L], ah[mt][1], al[mt][1]);
-      tf32_split(r0[4], ah[mt][2], al[mt][2]);
-      tf32_split(r0[8 * L + 4], ah[mt][3], al[mt][3]);
+      const int r0 = rbase + 16 * mt + g, c0 = 8 * kt + t;
+      tf32_split(at(r0, c0), ah[mt][0], al[mt][0]);
+      tf32_split(at(r0 + 8, c0), ah[mt][1], al[mt][1]);
+      tf32_split(at(r0, c0 + 4), ah[mt][2], al[mt][2]);
+      tf32_split(at(r0 + 8, c0 + 4), ah[mt][3], al[mt][3]);
     }
 #pragma unroll
     for (int nt = 0; nt < NO / 8; ++nt) {
@@ -284,9 +305,13 @@ __global__ void __launch_bounds__(kApRows) k_assemble(const __grid_constant__ As
   float* s1 = asm_sm;
   float* s2 = s1 + W * NO;
   float* s3 = s2 + W * NO;
-  float* sin_base = s3 + W * NO;  // 2 buffers x (IN1, IN2) x kApRows x L
-  constexpr int kSlot = 2 * kApRows * L;
-  float* sout = sin_base + 2 * kSlot;  // kApRows x (2 nout + 4) output rows
+  // kSwz (tensor-core path at W = 32): unpadded swizzled rows, and the output rows staged in the
+  // tile's own input slot once its MMAs are done (no separate output buffer)
+  constexpr bool kSwz = kTc && W == 32 && NO <= 24;  // kApRows x (2 NO + 4) output rows fit one slot
+  constexpr int LS = kSwz ? W : L;
+  float* sin_base = s3 + W * NO;  // 2 buffers x (IN1, IN2) x kApRows x LS
+  constexpr int kSlot = 2 * kApRows * LS;
+  float* sout_own = sin_base + 2 * kSlot;  // kApRows x (2 nout + 4) output rows (not kSwz)
   const int nout = J.nout;
   const int kin = J.kin > 0 && J.kin < W ? J.kin : W;
   const bool has3 = J.S3 != nullptr;
@@ -301,8 +326,13 @@ __global__ void __launch_bounds__(kApRows) k_assemble(const __grid_constant__ As
   auto stage = [&](int64_t i0, int slot) {
     if (i0 < n) {
       const int nr = (int)(n - i0 < kApRows ? n - i0 : kApRows);
-      stage_rows_async<W>(J.IN1, i0, nr, sin_base + slot * kSlot);
-      stage_rows_async<W>(J.IN2, i0, nr, sin_base + slot * kSlot + kApRows * L);
+      if constexpr (kSwz) {
+        stage_rows_swz<W>(J.IN1, i0, nr, sin_base + slot * kSlot);
+        stage_rows_swz<W>(J.IN2, i0, nr, sin_base + slot * kSlot + kApRows * LS);
+      } else {
+        stage_rows_async<W>(J.IN1, i0, nr, sin_base + slot * kSlot);
+        stage_rows_async<W>(J.IN2, i0, nr, sin_base + slot * kSlot + kApRows * LS);
+      }
     }
     cp_async_commit();
   };
@@ -312,8 +342,9 @@ __global__ void __launch_bounds__(kApRows) k_assemble(const __grid_constant__ As
   int it = 0;
   for (int64_t i0 = first; i0 < n; i0 += step, ++it) {
     const int nr = (int)(n - i0 < kApRows ? n - i0 : kApRows);
-    const float* sin1 = sin_base + (it & 1) * kSlot;
-    const float* sin2 = sin1 + kApRows * L;
+    float* sin1 = sin_base + (it & 1) * kSlot;
+    const float* sin2 = sin1 + kApRows * LS;
+    float* sout = kSwz ? sin1 : sout_own;
     cp_async_wait<1>();
     __syncthreads();
     // the tile's rows go through shared memory (row stride 2 nout + 4 floats: an odd number of
@@ -323,11 +354,11 @@ __global__ void __launch_bounds__(kApRows) k_assemble(const __grid_constant__ As
     if constexpr (kTc) {
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
       float c1[2][NO / 8][4] = {}, c2[2][NO / 8][4] = {};
-      asm_mma<W, NO>(c1, sin1, 32 * warp, s1, lane);
-      if (has3) asm_mma<W, NO>(c1, sin2, 32 * warp, s3, lane);
-      asm_mma<W, NO>(c2, sin2, 32 * warp, s2, lane);
-      __syncthreads();  // every row of this buffer has been read: stage the tile after next into it
-      stage(i0 + 2 * step, it & 1);
+      asm_mma<W, NO, kSwz>(c1, sin1, 32 * warp, s1, lane);
+      if (has3) asm_mma<W, NO, kSwz>(c1, sin2, 32 * warp, s3, lane);
+      asm_mma<W, NO, kSwz>(c2, sin2, 32 * warp, s2, lane);
+      __syncthreads();  // every row of this buffer has been read
+      if (!kSwz) stage(i0 + 2 * step, it & 1);  // kSwz: the slot holds the output rows first
       const int g = lane >> 2, t = lane & 3;
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
@@ -420,13 +451,20 @@ __global__ void __launch_bounds__(kApRows) k_assemble(const __grid_constant__ As
         ld[e] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
       }
     }
+    if constexpr (kSwz) {  // the output rows are out of the slot: stage the tile after next into it
+      __syncthreads();
+      stage(i0 + 2 * step, it & 1);
+    }
   }
 }
 
 template <int W, int NO>
 static void assemble_t(AsmJobs& jobs, cudaStream_t st) {
   constexpr bool kTc = W <= 32 && NO % 8 == 0 && W % 8 == 0;
-  constexpr int smem = (4 * kApRows * ap_ld(W) + 3 * W * NO + kApRows * (2 * NO + 4)) * (int)sizeof(float);
+  constexpr bool kSwz = kTc && W == 32 && NO <= 24;  // as in the kernel: 74.8 KB, three blocks per SM
+  constexpr int smem = (kSwz ? 4 * kApRows * W + 3 * W * NO
+                             : 4 * kApRows * ap_ld(W) + 3 * W * NO + kApRows * (2 * NO + 4)) * (int)sizeof(float);
+  static_assert(!kSwz || kApRows * (2 * NO + 4) <= 2 * kApRows * W, "output rows fit one staging slot");
   static std::atomic<unsigned> attr{0};
   ensure_smem(k_assemble<W, NO, kTc>, smem, attr);
   int64_t n[kMaxApply] = {};

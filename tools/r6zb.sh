@@ -1,0 +1,4 @@
+# k_assemble at W = 32: swizzled unpadded staging, output rows in the consumed slot (3 blocks / SM)
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/r6zb_tests.log 2>&1; echo rc=$? >> gpurun_out/r6zb_tests.log
+timeout 600 python bench.py --config c4 --steps 3 --warmup 2 --no-cpu-baseline --no-e2e > gpurun_out/r6zb_bench_c4.json 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.pct_of_peak_sustained_active,launch__occupancy_limit_shared_mem --clock-control none -k regex:k_assemble --csv --log-file gpurun_out/r6zb_asm.csv python tools/one_layer.py layer1.0.conv3 2 > /dev/null 2>&1
