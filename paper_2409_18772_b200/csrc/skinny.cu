@@ -501,7 +501,7 @@ void launch_assemble(AsmJobs& jobs, int W, cudaStream_t st) {
 // fp64 products and accumulation as the FMA form (a different, fixed summation order).  Outputs:
 // lane l holds Q[r0 + l / 4][8 nt + 2 (l % 4) + {0, 1}]; column maxima as in k_apply64.
 template <int W>
-__global__ void __launch_bounds__(kApRows) k_apply64_tc(const __grid_constant__ Apply64Jobs jobs) {
+__global__ void __launch_bounds__(kApRows, 4) k_apply64_tc(const __grid_constant__ Apply64Jobs jobs) {
   ::lrqmm::pdl_enter();
   constexpr int L = ap_ld(W);
   constexpr int KT = W / 4, NT = W / 8;
@@ -537,11 +537,13 @@ __global__ void __launch_bounds__(kApRows) k_apply64_tc(const __grid_constant__ 
     const float* sin = sin_base + (it & 1) * kApRows * L;
     cp_async_wait<1>();  // this tile's group has landed (the next one may still be in flight)
     __syncthreads();
-    double acc[4][NT][2];
+    // one 8-row slab at a time, its outputs stored from registers at once (8 fp64 accumulators
+    // live instead of 32: four resident blocks per SM instead of three)
 #pragma unroll
     for (int sl = 0; sl < 4; ++sl) {
+      double acc[NT][2];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) acc[sl][nt][0] = acc[sl][nt][1] = 0.0;
+      for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
       const float* arow = sin + (warp * 32 + sl * 8 + (lane >> 2)) * L + (lane & 3);
 #pragma unroll
       for (int kt = 0; kt < KT; ++kt) {
@@ -551,21 +553,16 @@ __global__ void __launch_bounds__(kApRows) k_apply64_tc(const __grid_constant__ 
         for (int nt = 0; nt < NT; ++nt) {
           if (nt >= nt_live) break;
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                       : "+d"(acc[sl][nt][0]), "+d"(acc[sl][nt][1])
+                       : "+d"(acc[nt][0]), "+d"(acc[nt][1])
                        : "d"(a), "d"(bfr[kt][nt]));
         }
       }
-    }
-    __syncthreads();  // every row of this buffer has been read: stage the tile after next into it
-    stage(i0 + 2 * step, it & 1);
-#pragma unroll
-    for (int sl = 0; sl < 4; ++sl) {
       const int64_t row = i0 + warp * 32 + sl * 8 + (lane >> 2);
       const bool ok = row < n;
       const float cs = (J.cscale && ok) ? J.cscale[row] : 1.f;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const float v0 = (float)acc[sl][nt][0], v1 = (float)acc[sl][nt][1];
+        const float v0 = (float)acc[nt][0], v1 = (float)acc[nt][1];
         if (ok) *reinterpret_cast<float2*>(J.OUT + row * W + 8 * nt + 2 * (lane & 3)) = make_float2(v0, v1);
         if (J.cmax) {  // same fp32 product as the next pass's B image; per-lane running maxima
           run[nt][0] = fmaxf(run[nt][0], ok ? fabsf(v0 * cs) : 0.f);
@@ -573,6 +570,8 @@ __global__ void __launch_bounds__(kApRows) k_apply64_tc(const __grid_constant__ 
         }
       }
     }
+    __syncthreads();  // every row of this buffer has been read: stage the tile after next into it
+    stage(i0 + 2 * step, it & 1);
   }
   if (J.cmax) {
     // lanes with the same lane & 3 hold the same columns: one shuffle reduction per block (max is
