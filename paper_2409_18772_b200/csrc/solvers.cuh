@@ -204,10 +204,12 @@ __device__ int eig_stats_steps;
 #ifndef LRQMM_EIG_SWEEPS
 #define LRQMM_EIG_SWEEPS 0  // micro-benchmark only: run exactly this many sweeps (0: convergence test)
 #endif
-template <int n, int NT>
+// NA (<= n): the largest live size na the caller guarantees (sizes the per-thread block / V slots)
+template <int n, int NT, int NA = n>
 __device__ void group_eig_trunc(const double* G, float* T, int r, double* dyn, double* aux, int tid, int bar) {
+  static_assert(NA <= n && NA % 2 == 0, "live size");
   constexpr int ld = n + 1;
-  constexpr int kBlk = ((n / 2) * (n / 2) + NT - 1) / NT, kV = ((n / 2) * n + NT - 1) / NT;
+  constexpr int kBlk = ((NA / 2) * (NA / 2) + NT - 1) / NT, kV = ((NA / 2) * NA + NT - 1) / NT;
   constexpr int NW = NT / 32;
   double* Abuf = dyn;                 // 2 x n x ld (ping-pong, relabelled)
   double* V = dyn + 2 * n * ld;       // n x ld, original labels
@@ -234,7 +236,7 @@ __device__ void group_eig_trunc(const double* G, float* T, int r, double* dyn, d
       scale_s = dm > 0.0 ? 1.0 / dm : 1.0;
       // a zero diagonal entry of a Gram matrix means a zero row and column
       const int na = (last + 2) & ~1;
-      na_s = na < 2 ? 2 : (na > n ? n : na);
+      na_s = na < 2 ? 2 : (na > NA ? NA : na);
     }
   }
   sync();
@@ -440,10 +442,25 @@ __host__ __device__ constexpr int eig_aux_bytes(int NT) { return (2 * (NT / 32) 
 
 // The group size per n (tools/eig_bench.cu: n = 24 30.0 us at 192 threads vs 33.8 at 256, n = 32
 // 61.2 us at 256); the CTA's other threads leave, the group synchronises on named barrier 1.
+// n = 32 with at most 26 live columns (r + p <= 25, c4's r = 20, p = 5): the n = 24 shape of the
+// work (169 blocks, 192 threads); the live size is read off G's diagonal first (one warp).
 template <int n>
 __device__ void dev_eig_trunc(const double* G, float* T, int r, double* dyn) {
   constexpr int NT = n == 24 ? 192 : 256;
   __shared__ double aux[(eig_aux_bytes(NT) + 7) / 8];
+  if constexpr (n == 32) {
+    __shared__ int live_s;
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      const int last = __reduce_max_sync(0xffffffffu, G[lane * n + lane] != 0.0 ? lane : -1);
+      if (lane == 0) live_s = (last + 2) & ~1;
+    }
+    __syncthreads();
+    if (live_s <= 26) {
+      if (threadIdx.x < 192) group_eig_trunc<32, 192, 26>(G, T, r, dyn, aux, threadIdx.x, 1);
+      return;
+    }
+  }
   if (threadIdx.x < NT) group_eig_trunc<n, NT>(G, T, r, dyn, aux, threadIdx.x, 1);
 }
 

@@ -10,14 +10,14 @@
 
 using namespace lrqmm;
 
-template <int n, int NT>
+template <int n, int NT, int NA = n>
 __global__ void k_bench(const double* G, float* T, int r, unsigned long long* t) {
   extern __shared__ double dyn[];
   __shared__ double aux[(eig_aux_bytes(NT) + 7) / 8];
   unsigned long long t0, t1;
   __syncthreads();
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  if (threadIdx.x < NT) group_eig_trunc<n, NT>(G, T, r, dyn, aux, threadIdx.x, 1);
+  if (threadIdx.x < NT) group_eig_trunc<n, NT, NA>(G, T, r, dyn, aux, threadIdx.x, 1);
   __syncthreads();
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
   if (threadIdx.x == 0) *t = t1 - t0;
@@ -68,19 +68,19 @@ void run_chol(const double* dG, unsigned long long* dt) {
   cudaFree(dT);
 }
 
-template <int NT, int n = 24>
+template <int NT, int n = 24, int NA = n>
 void run(const double* dG, float* dT, unsigned long long* dt) {
-  cudaFuncSetAttribute(k_bench<n, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, eig_smem_bytes(n));
+  cudaFuncSetAttribute(k_bench<n, NT, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, eig_smem_bytes(n));
   unsigned long long best = ~0ull;
   for (int i = 0; i < 20; ++i) {
-    k_bench<n, NT><<<1, NT, eig_smem_bytes(n)>>>(dG, dT, 16, dt);
+    k_bench<n, NT, NA><<<1, NT, eig_smem_bytes(n)>>>(dG, dT, 16, dt);
     unsigned long long t;
     cudaMemcpy(&t, dt, 8, cudaMemcpyDeviceToHost);
     if (t < best) best = t;
   }
   std::vector<float> T(n * n);
   cudaMemcpy(T.data(), dT, sizeof(float) * n * n, cudaMemcpyDeviceToHost);
-  if (NT == 128) {
+  if (NT == 192) {
     char fn[64];
     snprintf(fn, sizeof fn, "gpurun_out/eig_T_256_n%d.bin", n);
     FILE* o = fopen(fn, "wb");
@@ -89,7 +89,7 @@ void run(const double* dG, float* dT, unsigned long long* dt) {
   int steps = 0;
   cudaMemcpyFromSymbol(&steps, eig_stats_steps, sizeof(int));
   printf("steps %d  ", steps);
-  printf("n=%d ", n);
+  printf("n=%d NA=%d ", n, NA);
   printf("NT=%3d  best %.1f us   T[0][0..3] = %.6f %.6f %.6f %.6f  (%s)\n", NT, best / 1e3, T[0], T[1], T[2], T[3],
          cudaGetErrorString(cudaGetLastError()));
 }
@@ -139,6 +139,7 @@ int main(int argc, char** argv) {
       run<192, 32>(dG32, dT32, dt);
       run<160, 32>(dG32, dT32, dt);
       run<128, 32>(dG32, dT32, dt);
+      run<192, 32, 26>(dG32, dT32, dt);
     }
     if (f32) fclose(f32);
   }
