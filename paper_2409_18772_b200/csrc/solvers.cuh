@@ -443,22 +443,30 @@ __host__ __device__ constexpr int eig_aux_bytes(int NT) { return (2 * (NT / 32) 
 // The group size per n (tools/eig_bench.cu: n = 24 30.0 us at 192 threads vs 33.8 at 256, n = 32
 // 61.2 us at 256); the CTA's other threads leave, the group synchronises on named barrier 1.
 // n = 32 with at most 26 live columns (r + p <= 25, c4's r = 20, p = 5): the n = 24 shape of the
-// work (169 blocks, 192 threads); the live size is read off G's diagonal first (one warp).
+// work (169 blocks, 192 threads); n = 24 with at most 22 (121 blocks, 128 threads).  The live size
+// is read off G's diagonal first (one warp).
 template <int n>
 __device__ void dev_eig_trunc(const double* G, float* T, int r, double* dyn) {
   constexpr int NT = n == 24 ? 192 : 256;
   __shared__ double aux[(eig_aux_bytes(NT) + 7) / 8];
-  if constexpr (n == 32) {
+  if constexpr (n == 24 || n == 32) {
     __shared__ int live_s;
     if (threadIdx.x < 32) {
       const int lane = threadIdx.x;
-      const int last = __reduce_max_sync(0xffffffffu, G[lane * n + lane] != 0.0 ? lane : -1);
+      const int last = __reduce_max_sync(0xffffffffu, lane < n && G[lane * n + lane] != 0.0 ? lane : -1);
       if (lane == 0) live_s = (last + 2) & ~1;
     }
     __syncthreads();
-    if (live_s <= 26) {
-      if (threadIdx.x < 192) group_eig_trunc<32, 192, 26>(G, T, r, dyn, aux, threadIdx.x, 1);
-      return;
+    if constexpr (n == 32) {
+      if (live_s <= 26) {
+        if (threadIdx.x < 192) group_eig_trunc<n, 192, 26>(G, T, r, dyn, aux, threadIdx.x, 1);
+        return;
+      }
+    } else {
+      if (live_s <= 22) {  // r + p <= 21 (c2 / c3: r = 16, p = 5): 26.8 vs 30.1 us
+        if (threadIdx.x < 128) group_eig_trunc<n, 128, 22>(G, T, r, dyn, aux, threadIdx.x, 1);
+        return;
+      }
     }
   }
   if (threadIdx.x < NT) group_eig_trunc<n, NT>(G, T, r, dyn, aux, threadIdx.x, 1);

@@ -110,6 +110,9 @@ int main(int argc, char** argv) {
   run<128>(dG, dT, dt);
   run<96>(dG, dT, dt);
   run<64>(dG, dT, dt);
+  run<192, 24, 22>(dG, dT, dt);
+  run<160, 24, 22>(dG, dT, dt);
+  run<128, 24, 22>(dG, dT, dt);
   {
     unsigned long long best = ~0ull;
     for (int i = 0; i < 20; ++i) {
