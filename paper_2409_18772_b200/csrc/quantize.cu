@@ -1055,15 +1055,24 @@ static im2t::Tile im2col_tile_geom(const ConvGeom& g, int Kp, bool vec) {
   // narrower than min(8, Wo) pixels re-reads too much halo per row: the gather kernel then
   static const int target = env_int("LRQMM_IM2COL_SMEM_KB", 56) * 1024;
   static const int min_tw = env_int("LRQMM_IM2COL_MIN_TW", 8);
-  int tw = g.Wo < 64 ? g.Wo : 64;
-  for (;; tw = (tw + 1) / 2) {
-    const int WI = (tw - 1) * g.sw + g.kw;
-    im2t::Tile c{tw, 0, WI, WI * g.C, zero_strip(tw)};
-    const int bytes = im2t::smem_bytes(g, c, Kp, vec);
-    if (bytes <= target && bytes <= im2t::kBudget) break;
-    if (tw == 1) return t;
-  }
-  if (tw < (g.Wo < min_tw ? g.Wo : min_tw)) return t;
+  // widest tile of at most 64 pixels within `budget` bytes, 0 if narrower than min(mtw, Wo)
+  auto widest = [&](int budget, int mtw) {
+    int tw = g.Wo < 64 ? g.Wo : 64;
+    for (;; tw = (tw + 1) / 2) {
+      const int WI = (tw - 1) * g.sw + g.kw;
+      im2t::Tile c{tw, 0, WI, WI * g.C, zero_strip(tw)};
+      const int bytes = im2t::smem_bytes(g, c, Kp, vec);
+      if (bytes <= budget && bytes <= im2t::kBudget) break;
+      if (tw == 1) return 0;
+    }
+    return tw < (g.Wo < mtw ? g.Wo : mtw) ? 0 : tw;
+  };
+  int tw = widest(target, min_tw);
+  // deep windows (C >= 256: 14- and 7-pixel rows) where no 8-pixel tile fits the per-CTA target:
+  // one or two CTAs per SM with tiles of >= 4 pixels still beat the gather kernel (layer3.x.conv2
+  // 150 -> 114 us, layer3.0.conv2 158 -> 133, layer4.x.conv2 77 -> 74)
+  if (tw == 0) tw = widest(env_int("LRQMM_IM2COL_DEEP_KB", 100) * 1024, 4);
+  if (tw == 0) return t;
   // balance: the fewest tiles of at most tw pixels, equal widths
   const int ntw = (g.Wo + tw - 1) / tw;
   t.TW = (g.Wo + ntw - 1) / ntw;
